@@ -1,0 +1,120 @@
+/*
+ * heatbem_b200.h -- C ABI of the B200 (sm_100a) space-time heat BEM library.
+ *
+ * Plain pointers and sizes only.  Every array argument named *_dev is a
+ * device pointer the caller owns (PyTorch allocates them); the library keeps
+ * no allocations between calls.  All entry points are stream-ordered on the
+ * cudaStream_t passed as `stream` (NULL = legacy default stream), return 0
+ * on success or a negative HB_ERR_* code, and never abort; the message of
+ * the last failure on the calling thread is available from hb_last_error().
+ *
+ * Reference interfaces replaced (file:line in the heatbem reference):
+ *   hb_assemble              heatbem/assembly.py:178-242 (_assemble_operator:
+ *                            the E_t+1 _toeplitz_pass calls of
+ *                            _assembly_numba.py:111-272, the _scatter_add
+ *                            of _assembly_numba.py:275-285 and the symmetric
+ *                            mirror of assembly.py:237-239) -- one call
+ *                            builds blocks [d_begin, d_end) of V, V11, K or D2.
+ *   hb_curl_combine          heatbem/assembly.py:314-334
+ *                            (hypersingular_from_single_layer).
+ *   hb_potential             heatbem/_field_numba.py:15-79 (_eval_potential).
+ *   hb_toeplitz_apply        heatbem/solver.py:47-73 (apply_toeplitz).
+ *   hb_forward_subst_step    heatbem/solver.py:178-182 (history update of
+ *                            forward_block_solve).
+ */
+#ifndef HEATBEM_B200_H
+#define HEATBEM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_OK 0
+#define HB_ERR_INVALID (-1)     /* bad argument / inconsistent sizes        */
+#define HB_ERR_CUDA (-2)        /* CUDA launch or runtime failure           */
+#define HB_ERR_WORKSPACE (-3)   /* workspace too small for one row chunk    */
+#define HB_ERR_UNSUPPORTED (-4) /* op / space combination not implemented   */
+
+/* operator codes, as heatbem/assembly.py:21 */
+#define HB_OP_SINGLE_LAYER 0    /* G^{dtau dt}                              */
+#define HB_OP_DOUBLE_LAYER 1    /* alpha dG^{dtau dt}/dn_y                  */
+#define HB_OP_HYPERSINGULAR2 2  /* alpha G^{dtau} n_x.n_y                   */
+
+int hb_version(void);
+const char *hb_last_error(void);
+
+/* Mesh, rule tables and adjacency: every array is what
+ * heatbem/assembly.py:201-206 hands to _toeplitz_pass, plus three
+ * host-built index lists (singular work list, node stars). */
+typedef struct {
+    int64_t E_x, N_x;
+    const int64_t *tri_nodes_dev;   /* (E_x,3)                              */
+    const double *verts_tri_dev;    /* (E_x,3,3)                            */
+    const double *normals_dev;      /* (E_x,3)                              */
+    const double *centroids_dev;    /* (E_x,3)                              */
+    const double *diameters_dev;    /* (E_x,)                               */
+    const double *areas_dev;        /* (E_x,)                               */
+    const double *reg_hats_dev, *reg_w_dev, *reg_pts_dev;    /* (nr,3) (nr,) (E_x,nr,3) */
+    int64_t n_reg;
+    const double *near_hats_dev, *near_w_dev, *near_pts_dev; /* (nn,3) (nn,) (E_x,nn,3) */
+    int64_t n_near;
+    const int64_t *tn_indptr_dev;   /* (E_x+1,) touching CSR                */
+    const int64_t *tn_idx_dev;      /* (nnz,) trial element, sorted per row */
+    const int64_t *tn_case_dev;     /* (nnz,) 0 identical 1 edge 2 vertex   */
+    const int64_t *tn_permt_dev;    /* (nnz,3)                              */
+    const int64_t *tn_perms_dev;    /* (nnz,3)                              */
+    const int64_t *duf_off_dev;     /* (4,) offsets into the Duffy table    */
+    const double *duf_t_dev, *duf_s_dev, *duf_w_dev;         /* (nd,2) (nd,2) (nd,) */
+    /* singular work list: CSR positions to evaluate, sorted by test row;
+     * for symmetric ops only positions with tn_idx >= row.
+     * sing_rowptr (E_x+1,) delimits each row's slice of sing_pos. */
+    const int64_t *sing_pos_dev;
+    const int64_t *sing_rowptr_dev;
+    int64_t sing_max_per_row;
+    const int64_t *sing_row_dev;    /* (nnz,) test row of each CSR position */
+    /* node stars: for node n, (element, local vertex) pairs sorted by
+     * element in star_elem/star_local[star_indptr[n] : star_indptr[n+1]] */
+    const int64_t *star_indptr_dev, *star_elem_dev, *star_local_dev;
+    int64_t star_max;               /* max star size                        */
+} hb_mesh_desc;
+
+typedef struct {
+    int op;                         /* HB_OP_*                              */
+    int test_p1, trial_p1, symmetric;
+    int64_t E_t;                    /* number of time steps (blocks)        */
+    double step;                    /* h_t = T / E_t (TimeGrid.step)        */
+    double alpha, d_eps, r_eps;     /* KernelParams.alpha/delta_eps/rho_eps */
+    int64_t d_begin, d_end;         /* blocks produced: [d_begin, d_end)    */
+    double *blocks_dev;             /* (d_end-d_begin, R, C) row-major      */
+    void *workspace_dev;            /* staging, >= hb_assemble_min_workspace */
+    size_t workspace_bytes;
+} hb_assembly_desc;
+
+/* bytes of staging for one test-row chunk (the minimum) and for all rows */
+size_t hb_assemble_min_workspace(const hb_mesh_desc *mesh, const hb_assembly_desc *a);
+size_t hb_assemble_full_workspace(const hb_mesh_desc *mesh, const hb_assembly_desc *a);
+
+/* Assemble blocks [d_begin, d_end) of one operator.  Writes every entry of
+ * blocks_dev; results are bitwise deterministic run to run and independent
+ * of d_begin/d_end (so d-sharded ranks reproduce the 1-GPU blocks). */
+int hb_assemble(const hb_mesh_desc *mesh, const hb_assembly_desc *a, void *stream);
+
+/* D = D2 + alpha^2 sum_o T_o^T V T_o per block (curl of the hat functions,
+ * heatbem/assembly.py:289-334).  V: (nb, E_x, E_x), D2 and D: (nb, N_x, N_x);
+ * D may alias D2.  curls_dev: (E_x, 3, 3) surface curls per local hat. */
+int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha,
+                    const double *curls_dev, const double *V_dev, const double *D2_dev,
+                    double *D_dev, void *stream);
+
+/* FP64 DFMA throughput probe used for the roofline denominator:
+ * runs `iters` dependent-chain iterations of 8 independent DFMA streams per
+ * thread over grid x 256 threads; flops = grid*256*iters*8*2. */
+int hb_fp64_probe(int64_t grid, int64_t iters, double *sink_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEATBEM_B200_H */

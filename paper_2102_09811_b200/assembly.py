@@ -1,0 +1,308 @@
+"""Block lower-triangular Toeplitz operators, assembled on the GPU.
+
+Drop-in for the reference assembler API (heatbem/assembly.py:24-419): same
+functions, same arguments, same ``BlockToeplitzMatrix`` type.  The blocks
+are produced by ``hb_assemble`` (csrc/hb_assembly.cu) and live in HBM;
+``BlockToeplitzMatrix.blocks`` is a lazily materialised numpy view of them
+(one device->host copy, cached), ``device_blocks`` the torch tensor.
+
+Extra keyword arguments (all optional, defaults reproduce the reference):
+
+* ``d_range=(d0, d1)`` -- assemble only blocks d0..d1-1 (d-sharding across
+  ranks; blocks are bitwise identical to a full assembly);
+* ``device`` -- CUDA device (default: current);
+* ``workspace_bytes`` -- staging budget (default: all rows at once, capped
+  at 4 GiB).
+
+``workers`` and ``deterministic`` are accepted for interface stability: the
+device path is always deterministic (no atomics; fixed-order reductions).
+"""
+from __future__ import annotations
+
+import struct
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .device import device_tables
+from .kernels import KernelParams
+from .quadrature import QuadratureConfig
+
+_OP_SINGLE, _OP_DOUBLE, _OP_HYPER2 = 0, 1, 2
+_DEFAULT_WS_CAP = 4 << 30
+
+
+class BlockToeplitzMatrix:
+    """Block (k, i) = blocks[k - i] for k >= i, zero above (never stored).
+
+    Construct from a numpy array (host) or a torch tensor (device); the
+    other side is created on first use.  ``transposed()`` shares storage."""
+
+    def __init__(self, blocks, transpose_blocks_on_apply: bool = False, diagonal_only: bool = False):
+        self._host = None
+        self._dev = None
+        if _is_torch(blocks):
+            self._dev = blocks
+        else:
+            self._host = np.asarray(blocks, dtype=np.float64)
+        self.transpose_blocks_on_apply = bool(transpose_blocks_on_apply)
+        self.diagonal_only = bool(diagonal_only)
+        self._share = None   # storage shared with transposed() twins
+
+    # ---- storage ---------------------------------------------------------
+    @property
+    def shape(self):
+        return tuple(self._dev.shape) if self._dev is not None else self._host.shape
+
+    @property
+    def blocks(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self._dev.detach().cpu().numpy()
+            if self._share is not None:
+                self._share._host = self._host
+        return self._host
+
+    @blocks.setter
+    def blocks(self, value):
+        self._host = np.asarray(value, dtype=np.float64)
+        self._dev = None
+
+    @property
+    def device_blocks(self):
+        """(n_blocks, rows, cols) float64 CUDA tensor."""
+        if self._dev is None:
+            import torch
+
+            _native.require_cuda()
+            self._dev = torch.from_numpy(np.ascontiguousarray(self._host)).cuda()
+            if self._share is not None:
+                self._share._dev = self._dev
+        return self._dev
+
+    @property
+    def on_device(self) -> bool:
+        return self._dev is not None
+
+    # ---- reference properties -------------------------------------------
+    @property
+    def n_blocks(self) -> int:
+        return self.shape[0]
+
+    @property
+    def block_rows(self) -> int:
+        return self.shape[2] if self.transpose_blocks_on_apply else self.shape[1]
+
+    @property
+    def block_cols(self) -> int:
+        return self.shape[1] if self.transpose_blocks_on_apply else self.shape[2]
+
+    def transposed(self) -> "BlockToeplitzMatrix":
+        """Blockwise transpose (K' from K), sharing the block storage."""
+        t = BlockToeplitzMatrix.__new__(BlockToeplitzMatrix)
+        t._host, t._dev = self._host, self._dev
+        t.transpose_blocks_on_apply = not self.transpose_blocks_on_apply
+        t.diagonal_only = self.diagonal_only
+        t._share, self._share = self, t
+        return t
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+@dataclass(frozen=True)
+class CurlTransform:
+    """Per-component surface-curl transforms T_1..T_3 (scipy CSR, E_x x N_x)."""
+
+    components: tuple
+
+
+@dataclass(frozen=True)
+class AssemblyPlan:
+    """i_t <-> d bookkeeping of the kernel-reuse scheme (assembly.py:66-100):
+    the kernel at gap i_t h feeds blocks i_t-1 (x-1), i_t (x2), i_t+1 (x-1);
+    i_t = 0 feeds block 0 through the combined kernel and block 1 (x-1)."""
+
+    n_blocks: int
+
+    def targets(self, i_t: int):
+        if not 0 <= i_t <= self.n_blocks:
+            raise ValueError("i_t out of range")
+        last = self.n_blocks - 1
+        if i_t == 0:
+            return [(0, 1.0, True)] + ([(1, -1.0, False)] if last >= 1 else [])
+        cand = ((i_t - 1, -1.0), (i_t, 2.0), (i_t + 1, -1.0))
+        return [(d, m, False) for d, m in cand if d <= last]
+
+    def contributors(self, d: int):
+        if not 0 <= d < self.n_blocks:
+            raise ValueError("d out of range")
+        return [(i_t, m, c) for i_t in range(self.n_blocks + 1)
+                for (dd, m, c) in self.targets(i_t) if dd == d]
+
+
+@dataclass
+class AssemblyInstrumentation:
+    """``kernel_batch_passes`` counts logical kernel passes (one per time gap
+    i_t = 0..E_t, all fused into one launch per pair class); ``seconds``
+    is the wall time of the device assembly (synchronised)."""
+
+    kernel_batch_passes: int = 0
+    seconds: float = field(default=0.0)
+
+
+def _workspace(tables, desc_m, desc_a, device, cap):
+    import torch
+
+    L = _native.load()
+    full = L.hb_assemble_full_workspace(desc_m, desc_a)
+    least = L.hb_assemble_min_workspace(desc_m, desc_a)
+    nbytes = max(least, min(full, cap))
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, mesh, timegrid,
+                       params: KernelParams, config: QuadratureConfig, instrumentation,
+                       d_range=None, device=None, workspace_bytes=None, stream=None):
+    import torch
+
+    _native.require_cuda()
+    tabs = device_tables(mesh, config, device)
+    E_t = timegrid.n_steps
+    d0, d1 = (0, E_t) if d_range is None else (int(d_range[0]), int(d_range[1]))
+    if not (0 <= d0 < d1 <= E_t):
+        raise ValueError(f"d_range {d_range} outside [0, {E_t}]")
+    E_x, N_x = mesh.n_triangles, mesh.n_vertices
+    R = N_x if test_p1 else E_x
+    C = N_x if trial_p1 else E_x
+    dev = tabs.device
+    blocks = torch.empty((d1 - d0, R, C), dtype=torch.float64, device=dev)
+    a = _native.AssemblyDesc()
+    a.op, a.test_p1, a.trial_p1, a.symmetric = op, int(test_p1), int(trial_p1), int(symmetric)
+    a.E_t, a.step = E_t, timegrid.step
+    a.alpha, a.d_eps, a.r_eps = params.alpha, params.delta_eps, params.rho_eps
+    a.d_begin, a.d_end = d0, d1
+    a.blocks_dev = blocks.data_ptr()
+    m = tabs.desc(symmetric)
+    ws = _workspace(tabs, m, a, dev, _DEFAULT_WS_CAP if workspace_bytes is None else int(workspace_bytes))
+    a.workspace_dev, a.workspace_bytes = ws.data_ptr(), ws.numel()
+    t0 = time.perf_counter()
+    with torch.cuda.device(dev):
+        _native.call("hb_assemble", m, a, _native.stream_handle(stream))
+        if instrumentation is not None:
+            torch.cuda.synchronize(dev)
+    if instrumentation is not None:
+        instrumentation.kernel_batch_passes += E_t + 1
+        instrumentation.seconds += time.perf_counter() - t0
+    del ws
+    return blocks
+
+
+def assemble_single_layer(mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig(),
+                          test_space: str = "p0", trial_space: str = "p0", workers: int | None = 1,
+                          deterministic: bool = True, instrumentation: AssemblyInstrumentation | None = None,
+                          **kw) -> BlockToeplitzMatrix:
+    """Single-layer blocks V (p0 x p0) or V11 (p1 x p1) (assembly.py:245-269)."""
+    if (test_space, trial_space) not in (("p0", "p0"), ("p1", "p1")):
+        raise ValueError("single layer supports p0 x p0 and p1 x p1 only")
+    p1 = test_space == "p1"
+    return BlockToeplitzMatrix(_assemble_operator(_OP_SINGLE, p1, p1, True, mesh, timegrid, params,
+                                                  config, instrumentation, **kw))
+
+
+def assemble_double_layer(mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig(),
+                          workers: int | None = 1, deterministic: bool = True,
+                          instrumentation: AssemblyInstrumentation | None = None, **kw) -> BlockToeplitzMatrix:
+    """Double-layer blocks K, p0 test x p1 trial (assembly.py:272-286)."""
+    return BlockToeplitzMatrix(_assemble_operator(_OP_DOUBLE, False, True, False, mesh, timegrid, params,
+                                                  config, instrumentation, **kw))
+
+
+def assemble_hypersingular_d2(mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig(),
+                              workers: int | None = 1, instrumentation: AssemblyInstrumentation | None = None,
+                              **kw) -> BlockToeplitzMatrix:
+    """Surface part D2 of the hypersingular operator, p1 x p1 (assembly.py:364-377)."""
+    return BlockToeplitzMatrix(_assemble_operator(_OP_HYPER2, True, True, True, mesh, timegrid, params,
+                                                  config, instrumentation, **kw))
+
+
+def curl_transform(mesh) -> CurlTransform:
+    """Host-side sparse T_o (E_x x N_x), for callers that want the matrices."""
+    import scipy.sparse as sp
+
+    from .device import _curls
+
+    E_x, N_x = mesh.n_triangles, mesh.n_vertices
+    cu = _curls(mesh)
+    rows = np.repeat(np.arange(E_x), 3)
+    cols = mesh.triangles.ravel()
+    return CurlTransform(tuple(sp.csr_matrix((cu[:, :, o].ravel(), (rows, cols)), shape=(E_x, N_x))
+                               for o in range(3)))
+
+
+def hypersingular_from_single_layer(V: BlockToeplitzMatrix, D2: BlockToeplitzMatrix, mesh, params: KernelParams,
+                                    overwrite_d2: bool = False, config: QuadratureConfig = QuadratureConfig(),
+                                    stream=None) -> BlockToeplitzMatrix:
+    """D = D2 + alpha^2 sum_o T_o^T V T_o blockwise (assembly.py:314-334), on the device."""
+    import torch
+
+    _native.require_cuda()
+    Vd, D2d = V.device_blocks, D2.device_blocks
+    if Vd.shape[0] != D2d.shape[0]:
+        raise ValueError("V and D2 must hold the same number of blocks")
+    tabs = device_tables(mesh, config, Vd.device)
+    out = D2d if overwrite_d2 else torch.empty_like(D2d)
+    with torch.cuda.device(Vd.device):
+        _native.call("hb_curl_combine", tabs.desc(True), Vd.shape[0], float(params.alpha),
+                     _native.ptr(tabs.t["curls"]), _native.ptr(Vd), _native.ptr(D2d), _native.ptr(out),
+                     _native.stream_handle(stream))
+    if overwrite_d2:
+        D2._host = None
+        return D2
+    return BlockToeplitzMatrix(out)
+
+
+def assemble_hypersingular(mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig(),
+                           workers: int | None = 1, deterministic: bool = True,
+                           instrumentation: AssemblyInstrumentation | None = None,
+                           single_layer: BlockToeplitzMatrix | None = None, **kw) -> BlockToeplitzMatrix:
+    """D = T^T (alpha^2 V) T + D2, p1 x p1 (assembly.py:337-361)."""
+    if single_layer is None:
+        single_layer = assemble_single_layer(mesh, timegrid, params, config, "p0", "p0", workers,
+                                             deterministic, instrumentation, **kw)
+    D2 = assemble_hypersingular_d2(mesh, timegrid, params, config, workers, instrumentation, **kw)
+    return hypersingular_from_single_layer(single_layer, D2, mesh, params, overwrite_d2=True, config=config)
+
+
+def assemble_mass(mesh, timegrid) -> BlockToeplitzMatrix:
+    """h_t M_x (p0 test x p1 trial), diagonal-only; M_x[l, j] = area_l / 3 for j in l
+    (assembly.py:380-390).  Host-built (sparse, tiny)."""
+    M = np.zeros((mesh.n_triangles, mesh.n_vertices))
+    rows = np.arange(mesh.n_triangles)
+    for i in range(3):
+        np.add.at(M, (rows, mesh.triangles[:, i]), mesh.areas / 3.0)
+    return BlockToeplitzMatrix((timegrid.step * M)[None], diagonal_only=True)
+
+
+_MAGIC = b"HBTM1"
+
+
+def save_blocks(matrix: BlockToeplitzMatrix, path) -> None:
+    """HBTM1: magic, (E_t, rows, cols) as <q, then <f8 blocks in d order (assembly.py:397-407)."""
+    b = matrix.blocks
+    with open(path, "wb") as fh:
+        fh.write(_MAGIC + struct.pack("<qqq", *b.shape))
+        fh.write(np.ascontiguousarray(b, dtype="<f8").tobytes())
+
+
+def load_blocks(path) -> BlockToeplitzMatrix:
+    with open(path, "rb") as fh:
+        if fh.read(5) != _MAGIC:
+            raise ValueError("not a block dump file (bad magic)")
+        n, r, c = struct.unpack("<qqq", fh.read(24))
+        data = np.frombuffer(fh.read(n * r * c * 8), dtype="<f8")
+    if data.size != n * r * c:
+        raise ValueError("truncated block dump")
+    return BlockToeplitzMatrix(data.reshape(n, r, c).astype(np.float64))

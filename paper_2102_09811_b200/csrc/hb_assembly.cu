@@ -1,0 +1,851 @@
+// hb_assembly.cu -- block-Toeplitz assembly of V, V11, K and D2 on sm_100a.
+//
+// Replaces heatbem/assembly.py:178-242 (_assemble_operator) together with the
+// jitted _toeplitz_pass / _scatter_add of heatbem/_assembly_numba.py:111-285.
+//
+// The reference evaluates every element-pair integral once per time gap
+// delta = i_t h (i_t = 0..E_t, "E_t + 1 passes") and combines the passes into
+// blocks B^d = -L(d-1) + 2 L(d) - L(d+1), B^0 = Lcomb(0) - L(1)
+// (AssemblyPlan.targets, assembly.py:72-89).  Here ONE launch covers all gaps:
+//
+//   * a warp owns one element pair; its 32 lanes are (s, t) = (lane>>4, lane&15):
+//     t selects time gaps i_t = it_lo + t + 16 j (j < NJ, NJ slots per lane),
+//     s splits the quadrature points by parity.  The per-pair geometry
+//     (rho, 1/rho, hat weights ...) of 32 quadrature points is computed once by
+//     the 32 lanes, parked in shared memory and read back as broadcasts, so
+//     every lane spends its time in the erf/exp chains of its own gaps --
+//     warp-uniform control flow for every pair class, no divergence;
+//   * the delta = 0 gap (closed-form limits, no erf) is summed lane-parallel
+//     over the points and butterfly-reduced;
+//   * the 3-term time combination is applied in shared memory and each block
+//     value B^d of the pair is written with lanes over d (coalesced) into a
+//     staging row Q[pair][ij][d];
+//   * operator-specific finalize kernels turn staging rows into blocks:
+//     p0xp0 mirror-transpose (V), node-star gathers for p1 columns (K) and
+//     rows+columns (D2, V11, then X + X^T).
+//
+// Regular (separated) pairs and touching pairs run in separate kernels
+// (k_regular / k_singular); the regular kernel classifies near/far on the fly
+// with the reference's exact IEEE operation order
+// (sqrt((dx*dx + dy*dy) + dz*dz) < 2 max(diam), _assembly_numba.py:218-223)
+// using explicitly rounded intrinsics, so the rule choice is bit-identical.
+//
+// Every per-(pair, gap) sum is taken in an order that depends only on the
+// pair and the gap -- never on E_t, the d-window or the row chunk -- so block
+// d is bitwise identical however the work is split (1 GPU vs d-sharded ranks,
+// E_t = 4 vs E_t = 2 with the same step: the reference's Toeplitz-reuse test).
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "hb_common.cuh"
+
+#ifndef HB_PAIR_MINB
+#define HB_PAIR_MINB 2
+#endif
+
+namespace hb {
+
+struct PairArgs {
+    hb_mesh_desc m;
+    double step, alpha, d_eps, r_eps;
+    double inv2a, inv2a2, inva, kconst;
+    int64_t e0, e1;
+    int d0, d1, it_lo, it_hi, need_special, nd;
+    int halve_diag;
+    double *Q;
+    unsigned long long *counter;   // work-item counter (zeroed per launch)
+};
+
+template <int OP, int NIJ>
+struct Layout {
+    // payload per quadrature point: [rho, s1, s2, H[NIJ]] (OP 0/1) or [rho, s1, H] (OP 2)
+    static constexpr int HOFF = (OP == 2) ? 2 : 3;
+    static constexpr int PAY_RAW = HOFF + NIJ;
+    static constexpr int PAY = (PAY_RAW + 1) & ~1;
+};
+
+template <int NIJ, int NJ>
+struct LsLayout {
+    static constexpr int SLOTS = 16 * NJ;
+    static constexpr int SIZE = NIJ * SLOTS + 2 * NIJ;   // + L0 and Lcomb0
+};
+
+template <int OP, int NIJ, int NJ>
+__host__ __device__ constexpr int smem_doubles_per_warp() { return 32 * Layout<OP, NIJ>::PAY + LsLayout<NIJ, NJ>::SIZE; }
+
+// ---------------------------------------------------------------------------
+// per-lane time-gap constants
+// ---------------------------------------------------------------------------
+template <int OP, int NJ>
+struct Slots {
+    double dl[NJ], cx[NJ], kk[NJ];
+    __device__ void init(const PairArgs &A, int t)
+    {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            int it = A.it_lo + t + 16 * j;
+            if (it > A.it_hi) it = A.it_hi;   // clamped slots compute finite values, never stored
+            const double delta = (double)it * A.step;
+            dl[j] = delta;
+            cx[j] = 1.0 / (2.0 * sqrt(A.alpha * delta));
+            if (OP == 2) kk[j] = 1.0 / sqrt(kPi * A.alpha * delta);
+            else kk[j] = sqrt(delta) * A.kconst;
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// quadrature point generators
+// ---------------------------------------------------------------------------
+struct RegularGeom {
+    const double *xp, *yp, *w, *hats;
+    int nq1;
+    __device__ void point(int q, double x[3], double y[3], double &wq, double ht[3], double hs[3]) const
+    {
+        const int p = q / nq1, r = q - p * nq1;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            x[c] = __ldg(xp + 3 * p + c);
+            y[c] = __ldg(yp + 3 * r + c);
+            ht[c] = __ldg(hats + 3 * p + c);
+            hs[c] = __ldg(hats + 3 * r + c);
+        }
+        wq = __ldg(w + p) * __ldg(w + r);
+    }
+};
+
+struct DuffyGeom {
+    double a0[3], da1[3], da2[3], b0[3], db1[3], db2[3];
+    const double *ts, *ss, *ws;
+    int off;
+    int invt[3], invs[3];   // original local vertex k sits at permuted position inv[k]
+    __device__ static double pick(const double v[3], int i) { return i == 0 ? v[0] : (i == 1 ? v[1] : v[2]); }
+    __device__ void point(int q, double x[3], double y[3], double &wq, double ht[3], double hs[3]) const
+    {
+        const int qd = off + q;
+        const double ut = __ldg(ts + 2 * qd), vt = __ldg(ts + 2 * qd + 1);
+        const double us = __ldg(ss + 2 * qd), vs = __ldg(ss + 2 * qd + 1);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            x[c] = a0[c] + ut * da1[c] + vt * da2[c];
+            y[c] = b0[c] + us * db1[c] + vs * db2[c];
+        }
+        wq = __ldg(ws + qd);
+        const double tp[3] = {1.0 - ut - vt, ut, vt}, sp[3] = {1.0 - us - vs, us, vs};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            ht[k] = pick(tp, invt[k]);
+            hs[k] = pick(sp, invs[k]);
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// one element pair, all time gaps of the window
+// ---------------------------------------------------------------------------
+template <int OP, bool TP1, bool SP1, int NJ, class Geom>
+__device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq, const double ny[3],
+                                          double jac, int64_t slot, const Slots<OP, NJ> &T,
+                                          double *geo, double *Ls, int lane)
+{
+    constexpr int NT = TP1 ? 3 : 1, NS = SP1 ? 3 : 1, NIJ = NT * NS;
+    using L = Layout<OP, NIJ>;
+    constexpr int PAY = L::PAY, HOFF = L::HOFF;
+    constexpr int SLOTS = LsLayout<NIJ, NJ>::SLOTS;
+    const int s = lane >> 4, t = lane & 15;
+
+    double acc[NJ][NIJ];
+    double s0[NIJ], sc[NIJ];
+#pragma unroll
+    for (int i = 0; i < NIJ; ++i) {
+        s0[i] = 0.0;
+        sc[i] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[j][i] = 0.0;
+    }
+
+    for (int base = 0; base < nq; base += 32) {
+        const int q = base + lane;
+        int small = 0;
+        if (q < nq) {
+            double x[3], y[3], wq, ht[3], hs[3];
+            g.point(q, x, y, wq, ht, hs);
+            const double rx = x[0] - y[0], ry = x[1] - y[1], rz = x[2] - y[2];
+            const double rho = sqrt(rx * rx + ry * ry + rz * rz);
+            small = rho <= A.r_eps;
+            double H[NIJ];
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+#pragma unroll
+                for (int j = 0; j < NS; ++j)
+                    H[i * NS + j] = (TP1 || SP1) ? wq * ((TP1 ? ht[i] : 1.0) * (SP1 ? hs[j] : 1.0)) : wq;
+            double *p = geo + lane * PAY;
+            p[0] = rho;
+            if (OP == 0) {
+                const double Aq = rho * A.inv2a2, Bq = A.inva / rho;
+                p[1] = Aq;
+                p[2] = Bq;
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
+                if (A.need_special) {
+                    const double cq = A.step * Bq + Aq;
+#pragma unroll
+                    for (int i = 0; i < NIJ; ++i) {
+                        s0[i] = fma(H[i], Aq, s0[i]);
+                        sc[i] = fma(H[i], cq, sc[i]);
+                    }
+                }
+            } else if (OP == 1) {
+                const double rn = rx * ny[0] + ry * ny[1] + rz * ny[2];
+                const double iq = 1.0 / rho;
+                const double U = small ? 0.0 : -rn * iq;
+                const double P = iq * iq;
+                p[1] = P;
+                p[2] = iq;
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i] * U;
+                if (A.need_special) {
+                    const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
+#pragma unroll
+                    for (int i = 0; i < NIJ; ++i) {
+                        s0[i] = fma(H[i] * U, c0, s0[i]);
+                        sc[i] = fma(H[i] * U, cc, sc[i]);
+                    }
+                }
+            } else {
+                const double iq = 1.0 / rho;
+                p[1] = iq;
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
+                if (A.need_special) {
+#pragma unroll
+                    for (int i = 0; i < NIJ; ++i) s0[i] = fma(H[i], iq, s0[i]);
+                }
+            }
+        }
+        const bool any_small = __any_sync(kFull, small);
+        __syncwarp();
+        const int nloc = min(32, nq - base);
+        if (!any_small) {
+            constexpr int UNR = (NJ == 1 && NIJ == 1) ? 2 : 1;
+#pragma unroll UNR
+            for (int k = s; k < nloc; k += 2) {
+                const double *p = geo + k * PAY;
+                const double rho = p[0], s1 = p[1];
+                const double s2 = (OP == 2) ? 0.0 : p[2];
+                double val[NJ];
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    const double x = rho * T.cx[j];
+                    if (OP == 0) {
+                        val[j] = fma(T.dl[j], s2, s1) * erf(x) + T.kk[j] * exp(-x * x);
+                    } else if (OP == 1) {
+                        val[j] = fma(-T.dl[j], s1, A.inv2a) * erf(x) + (T.kk[j] * s2) * exp(-x * x);
+                    } else {
+                        val[j] = erf(x) * s1;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) {
+                    const double h = p[HOFF + i];
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) acc[j][i] = fma(val[j], h, acc[j][i]);
+                }
+            }
+        } else {
+            for (int k = s; k < nloc; k += 2) {
+                const double *p = geo + k * PAY;
+                const double rho = p[0], s1 = p[1];
+                const double s2 = (OP == 2) ? 0.0 : p[2];
+                const bool sm = rho <= A.r_eps;
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    const double x = rho * T.cx[j];
+                    double val;
+                    if (OP == 0) {
+                        val = sm ? 2.0 * T.kk[j] : fma(T.dl[j], s2, s1) * erf(x) + T.kk[j] * exp(-x * x);
+                    } else if (OP == 1) {
+                        val = sm ? 0.0 : fma(-T.dl[j], s1, A.inv2a) * erf(x) + (T.kk[j] * s2) * exp(-x * x);
+                    } else {
+                        val = sm ? T.kk[j] : erf(x) * s1;
+                    }
+#pragma unroll
+                    for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(val, p[HOFF + i], acc[j][i]);
+                }
+            }
+        }
+        __syncwarp();
+    }
+
+    // fold the two point-parity halves (commutative: both halves get equal bits)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) acc[j][i] += __shfl_xor_sync(kFull, acc[j][i], 16);
+    if (A.need_special) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < NIJ; ++i) {
+                s0[i] += __shfl_xor_sync(kFull, s0[i], o);
+                if (OP != 2) sc[i] += __shfl_xor_sync(kFull, sc[i], o);
+            }
+    }
+    const int nslots = A.it_hi - A.it_lo + 1;
+    if (s == 0) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int sl = t + 16 * j;
+            if (sl < nslots) {
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) Ls[i * SLOTS + sl] = jac * acc[j][i];
+            }
+        }
+    }
+    double *L0 = Ls + NIJ * SLOTS, *Lc = L0 + NIJ;
+    if (lane == 0 && A.need_special) {
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) {
+            L0[i] = jac * s0[i];
+            Lc[i] = jac * (OP == 2 ? s0[i] : sc[i]);
+        }
+    }
+    __syncwarp();
+    // 3-term combination (AssemblyPlan.targets) with lanes over blocks d
+    double *dst = A.Q + slot * (int64_t)(NIJ * A.nd);
+    for (int dd = lane; dd < A.nd; dd += 32) {
+        const int d = A.d0 + dd;
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) {
+            const double *Li = Ls + i * SLOTS;
+            double b;
+            if (d == 0) {
+                const double l1 = Li[1 - A.it_lo];
+                b = Lc[i] + (-l1);
+            } else {
+                const double lm = (d - 1 == 0) ? L0[i] : Li[d - 1 - A.it_lo];
+                const double lc = Li[d - A.it_lo];
+                const double lp = Li[d + 1 - A.it_lo];
+                b = -lm + 2.0 * lc;
+                b = b + (-lp);
+            }
+            dst[i * A.nd + dd] = b;
+        }
+    }
+    __syncwarp();
+}
+
+template <int NIJ>
+__device__ __forceinline__ void write_zero_pair(const PairArgs &A, int64_t slot, int lane)
+{
+    double *dst = A.Q + slot * (int64_t)(NIJ * A.nd);
+    for (int k = lane; k < NIJ * A.nd; k += 32) dst[k] = 0.0;
+}
+
+__device__ __forceinline__ double exact_dot3(const double *a, const double *b)
+{
+    // (a0*b0 + a1*b1) + a2*b2, each step rounded (no FMA contraction)
+    return __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[0]), __dmul_rn(a[1], b[1])), __dmul_rn(a[2], b[2]));
+}
+
+template <int OP>
+__device__ __forceinline__ double pair_jac(const PairArgs &A, int64_t e, int64_t f)
+{
+    double jac = (__ldg(A.m.areas_dev + e) * __ldg(A.m.areas_dev + f)) * kInvPi;
+    if (A.halve_diag && e == f) jac *= 0.5;
+    if (OP == 2) {
+        double ne[3], nf[3];
+        for (int c = 0; c < 3; ++c) {
+            ne[c] = __ldg(A.m.normals_dev + 3 * e + c);
+            nf[c] = __ldg(A.m.normals_dev + 3 * f + c);
+        }
+        jac *= exact_dot3(ne, nf);
+    }
+    return jac;
+}
+
+// ---------------------------------------------------------------------------
+// K1 body: separated pairs of one (test row e, 32-column segment) work item.
+// ---------------------------------------------------------------------------
+template <int OP, bool TP1, bool SP1, int NJ, bool SYM>
+__device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64_t seg, const Slots<OP, NJ> &T,
+                                             double *geo, double *Ls, int lane)
+{
+    constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
+    const hb_mesh_desc &M = A.m;
+    int64_t fb = seg * 32;
+    const int64_t fe = min(fb + 32, M.E_x);
+    if (SYM) fb = max(fb, e);
+    if (fb >= fe) return;
+    const int64_t t_lo = __ldg(M.tn_indptr_dev + e), t_hi = __ldg(M.tn_indptr_dev + e + 1);
+    double ce[3];
+    for (int c = 0; c < 3; ++c) ce[c] = __ldg(M.centroids_dev + 3 * e + c);
+    const double de = __ldg(M.diameters_dev + e);
+
+    for (int64_t f = fb; f < fe; ++f) {
+        // touching pairs belong to the singular path (binary search as the reference does)
+        int64_t lo = t_lo, hi = t_hi;
+        bool touching = false;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1, v = __ldg(M.tn_idx_dev + mid);
+            if (v < f) lo = mid + 1;
+            else if (v > f) hi = mid;
+            else { touching = true; break; }
+        }
+        if (touching) continue;
+        const int64_t slot = (e - A.e0) * M.E_x + f;
+        const double jac = pair_jac<OP>(A, e, f);
+        if (OP == 2 && jac == 0.0) {   // n_x.n_y == 0: every staged value is +0
+            write_zero_pair<NIJ>(A, slot, lane);
+            continue;
+        }
+        double cf[3];
+        for (int c = 0; c < 3; ++c) cf[c] = __ldg(M.centroids_dev + 3 * f + c);
+        const double dx = __dsub_rn(ce[0], cf[0]), dy = __dsub_rn(ce[1], cf[1]), dz = __dsub_rn(ce[2], cf[2]);
+        const double dist = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+        const double df = __ldg(M.diameters_dev + f);
+        const bool near = dist < 2.0 * fmax(de, df);
+        RegularGeom g;
+        const int nq1 = near ? (int)M.n_near : (int)M.n_reg;
+        const double *pts = near ? M.near_pts_dev : M.reg_pts_dev;
+        g.xp = pts + 3 * e * nq1;
+        g.yp = pts + 3 * f * nq1;
+        g.w = near ? M.near_w_dev : M.reg_w_dev;
+        g.hats = near ? M.near_hats_dev : M.reg_hats_dev;
+        g.nq1 = nq1;
+        double ny[3];
+        for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * f + c);
+        eval_pair<OP, TP1, SP1, NJ>(A, g, nq1 * nq1, ny, jac, slot, T, geo, Ls, lane);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2 body: one touching pair (identical / common edge / common vertex),
+// Sauter-Schwab rule on the permuted charts of classify_pair.
+// ---------------------------------------------------------------------------
+template <int OP, bool TP1, bool SP1, int NJ>
+__device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, const Slots<OP, NJ> &T,
+                                              double *geo, double *Ls, int lane)
+{
+    constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
+    const hb_mesh_desc &M = A.m;
+    const int64_t tpos = __ldg(M.sing_pos_dev + k);
+    const int64_t e = __ldg(M.sing_row_dev + tpos);
+    const int64_t f = __ldg(M.tn_idx_dev + tpos);
+    const int cs = (int)__ldg(M.tn_case_dev + tpos);
+    DuffyGeom g;
+    int pt[3], ps[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        pt[i] = (int)__ldg(M.tn_permt_dev + 3 * tpos + i);
+        ps[i] = (int)__ldg(M.tn_perms_dev + 3 * tpos + i);
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {   // inverse permutations, register-resident
+        g.invt[q] = pt[0] == q ? 0 : (pt[1] == q ? 1 : 2);
+        g.invs[q] = ps[0] == q ? 0 : (ps[1] == q ? 1 : 2);
+    }
+    const double *ve = M.verts_tri_dev + 9 * e, *vf = M.verts_tri_dev + 9 * f;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double a0 = __ldg(ve + 3 * pt[0] + c), a1 = __ldg(ve + 3 * pt[1] + c), a2 = __ldg(ve + 3 * pt[2] + c);
+        const double b0 = __ldg(vf + 3 * ps[0] + c), b1 = __ldg(vf + 3 * ps[1] + c), b2 = __ldg(vf + 3 * ps[2] + c);
+        g.a0[c] = a0; g.da1[c] = a1 - a0; g.da2[c] = a2 - a0;
+        g.b0[c] = b0; g.db1[c] = b1 - b0; g.db2[c] = b2 - b0;
+    }
+    g.ts = M.duf_t_dev;
+    g.ss = M.duf_s_dev;
+    g.ws = M.duf_w_dev;
+    const int off0 = (int)__ldg(M.duf_off_dev + cs), off1 = (int)__ldg(M.duf_off_dev + cs + 1);
+    g.off = off0;
+    const int64_t slot = (e - A.e0) * M.E_x + f;
+    const double jac = pair_jac<OP>(A, e, f);
+    if (OP == 2 && jac == 0.0) {
+        write_zero_pair<NIJ>(A, slot, lane);
+        return;
+    }
+    double ny[3];
+    for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * f + c);
+    eval_pair<OP, TP1, SP1, NJ>(A, g, off1 - off0, ny, jac, slot, T, geo, Ls, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent pair kernel: warps pull work items from a global counter.
+// Items [0, n_sing) are touching pairs (K2 body, heaviest first in row
+// order), items [n_sing, n_sing + rows*nseg) are (row, segment) tiles of
+// separated pairs (K1 body).  A warp only ever holds one pair class, so the
+// two quadrature families never share a warp; dynamic fetching removes the
+// imbalance of upper-triangular / near-diagonal tiles.
+// ---------------------------------------------------------------------------
+template <int OP, bool TP1, bool SP1, int NJ, bool SYM>
+__global__ void __launch_bounds__(kWarps * 32, HB_PAIR_MINB) k_pairs(const PairArgs A)
+{
+    constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
+    extern __shared__ __align__(16) double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *geo = smem + warp * smem_doubles_per_warp<OP, NIJ, NJ>();
+    double *Ls = geo + 32 * Layout<OP, NIJ>::PAY;
+    const hb_mesh_desc &M = A.m;
+    const int64_t s_lo = __ldg(M.sing_rowptr_dev + A.e0), s_hi = __ldg(M.sing_rowptr_dev + A.e1);
+    const int64_t n_sing = s_hi - s_lo;
+    const int64_t nseg = cdiv(M.E_x, 32);
+    const int64_t n_reg = (A.e1 - A.e0) * nseg;
+    Slots<OP, NJ> T;
+    T.init(A, lane & 15);
+    for (;;) {
+        unsigned long long it = 0;
+        if (lane == 0) it = atomicAdd(A.counter, 1ull);
+        it = __shfl_sync(kFull, it, 0);
+        const int64_t item = (int64_t)it;
+        if (item < n_sing) {
+            singular_item<OP, TP1, SP1, NJ>(A, s_lo + item, T, geo, Ls, lane);
+        } else if (item - n_sing < n_reg) {
+            const int64_t r = item - n_sing;
+            regular_item<OP, TP1, SP1, NJ, SYM>(A, A.e0 + r / nseg, r % nseg, T, geo, Ls, lane);
+        } else {
+            break;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// finalize kernels
+// ---------------------------------------------------------------------------
+struct FinArgs {
+    const double *Q;
+    double *out;          // blocks_dev, block (d - d_begin) at out + (d - d_begin) R C
+    int64_t E_x, N_x, R, C, e0, e1;
+    int d0, nd, d_begin;
+    const int64_t *star_indptr, *star_elem, *star_local, *tri_nodes;
+};
+
+// V (p0 x p0, symmetric): tile of 4 rows x 32 columns x 32 blocks through smem;
+// direct rows coalesced over f, mirror rows in 32-byte runs over e.
+__global__ void __launch_bounds__(256) k_fin_p0p0(const FinArgs F)
+{
+    __shared__ double tile[4][32][33];
+    const int64_t f0 = (int64_t)blockIdx.x * 32, eb = F.e0 + (int64_t)blockIdx.y * 4;
+    if (f0 + 31 < eb) return;   // tile entirely below the diagonal: nothing staged
+    const int tid = threadIdx.x;
+    for (int dc = 0; dc < F.nd; dc += 32) {
+        const int ndc = min(32, F.nd - dc);
+        for (int idx = tid; idx < 4 * 32 * 32; idx += 256) {
+            const int el = idx >> 10, fl = (idx >> 5) & 31, dl = idx & 31;
+            const int64_t e = eb + el, f = f0 + fl;
+            if (e < F.e1 && f < F.E_x && f >= e && dl < ndc)
+                tile[el][fl][dl] = F.Q[((e - F.e0) * F.E_x + f) * F.nd + dc + dl];
+        }
+        __syncthreads();
+        for (int idx = tid; idx < 4 * 32 * 32; idx += 256) {
+            const int el = idx >> 10, dl = (idx >> 5) & 31, fl = idx & 31;
+            const int64_t e = eb + el, f = f0 + fl;
+            if (e < F.e1 && f < F.E_x && f >= e && dl < ndc) {
+                const int64_t b = F.d0 + dc + dl - F.d_begin;
+                F.out[(b * F.R + e) * F.C + f] = tile[el][fl][dl];
+            }
+        }
+        for (int idx = tid; idx < 4 * 32 * 32; idx += 256) {
+            const int fl = idx >> 7, dl = (idx >> 2) & 31, el = idx & 3;
+            const int64_t e = eb + el, f = f0 + fl;
+            if (e < F.e1 && f < F.E_x && f > e && dl < ndc) {
+                const int64_t b = F.d0 + dc + dl - F.d_begin;
+                F.out[(b * F.R + f) * F.C + e] = tile[el][fl][dl];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// K (p0 test x p1 trial): out[d][e][n] = sum_{(f,j) in star(n), f ascending} Q[e,f][j][d]
+__global__ void __launch_bounds__(256) k_fin_p0p1(const FinArgs F)
+{
+    __shared__ double tile[32][33];
+    const int64_t n0 = (int64_t)blockIdx.y * 32, e = F.e0 + blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double *Qe = F.Q + (e - F.e0) * F.E_x * 3 * F.nd;
+    for (int dc = 0; dc < F.nd; dc += 32) {
+        const int ndc = min(32, F.nd - dc);
+        for (int nl = warp; nl < 32; nl += kWarps) {
+            const int64_t n = n0 + nl;
+            double acc = 0.0;
+            if (n < F.N_x && lane < ndc) {
+                const int64_t s0 = __ldg(F.star_indptr + n), s1 = __ldg(F.star_indptr + n + 1);
+                for (int64_t s = s0; s < s1; ++s) {
+                    const int64_t f = __ldg(F.star_elem + s), j = __ldg(F.star_local + s);
+                    acc += Qe[(f * 3 + j) * F.nd + dc + lane];
+                }
+            }
+            tile[nl][lane] = acc;
+        }
+        __syncthreads();
+        for (int dl = warp; dl < ndc; dl += kWarps) {
+            const int64_t n = n0 + lane;
+            if (n < F.N_x) {
+                const int64_t b = F.d0 + dc + dl - F.d_begin;
+                F.out[(b * F.R + e) * F.C + n] = tile[lane][dl];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// D2 / V11 (p1 x p1): X[d][m][n] += sum_{(e,i) in star(m), e in chunk}
+//                                   sum_{(f,j) in star(n), f >= e} Q[e,f][3i+j][d]
+__global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
+{
+    __shared__ double tile[32][33];
+    const int64_t n0 = (int64_t)blockIdx.y * 32, m = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t sm0 = __ldg(F.star_indptr + m), sm1 = __ldg(F.star_indptr + m + 1);
+    bool any = false;
+    for (int64_t a = sm0; a < sm1; ++a) {
+        const int64_t e = __ldg(F.star_elem + a);
+        any |= (e >= F.e0 && e < F.e1);
+    }
+    if (!any) return;
+    for (int dc = 0; dc < F.nd; dc += 32) {
+        const int ndc = min(32, F.nd - dc);
+        for (int nl = warp; nl < 32; nl += kWarps) {
+            const int64_t n = n0 + nl;
+            double acc = 0.0;
+            if (n < F.N_x && lane < ndc) {
+                const int64_t sn0 = __ldg(F.star_indptr + n), sn1 = __ldg(F.star_indptr + n + 1);
+                for (int64_t a = sm0; a < sm1; ++a) {
+                    const int64_t e = __ldg(F.star_elem + a);
+                    if (e < F.e0 || e >= F.e1) continue;
+                    const int64_t i = __ldg(F.star_local + a);
+                    const double *Qe = F.Q + (e - F.e0) * F.E_x * 9 * F.nd;
+                    for (int64_t b = sn0; b < sn1; ++b) {
+                        const int64_t f = __ldg(F.star_elem + b);
+                        if (f < e) continue;
+                        const int64_t j = __ldg(F.star_local + b);
+                        acc += Qe[(f * 9 + 3 * i + j) * F.nd + dc + lane];
+                    }
+                }
+            }
+            tile[nl][lane] = acc;
+        }
+        __syncthreads();
+        for (int dl = warp; dl < ndc; dl += kWarps) {
+            const int64_t n = n0 + lane;
+            if (n < F.N_x) {
+                const int64_t b = F.d0 + dc + dl - F.d_begin;
+                double *x = F.out + (b * F.R + m) * F.C + n;
+                *x = *x + tile[lane][dl];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// in-place X <- X + X^T on square blocks, 32x32 tile pairs (upper tile grid)
+__global__ void __launch_bounds__(256) k_symmetrize(double *out, int64_t N, int64_t b_lo)
+{
+    __shared__ double A[32][33], B[32][33];
+    const int64_t ntile = cdiv(N, 32);
+    const int64_t tb = blockIdx.x;   // linear index into upper-triangular tile pairs
+    // decode (ti <= tj) from tb
+    int64_t ti = 0, rem = tb;
+    while (rem >= ntile - ti) { rem -= ntile - ti; ++ti; }
+    const int64_t tj = ti + rem;
+    double *X = out + (b_lo + blockIdx.y) * N * N;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t i = ti * 32 + r, j = tj * 32 + tx;
+        A[r][tx] = (i < N && j < N) ? X[i * N + j] : 0.0;
+        const int64_t i2 = tj * 32 + r, j2 = ti * 32 + tx;
+        B[r][tx] = (i2 < N && j2 < N) ? X[i2 * N + j2] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t i = ti * 32 + r, j = tj * 32 + tx;
+        if (i < N && j < N) X[i * N + j] = A[r][tx] + B[tx][r];
+        const int64_t i2 = tj * 32 + r, j2 = ti * 32 + tx;
+        if (ti != tj && i2 < N && j2 < N) X[i2 * N + j2] = B[r][tx] + A[tx][r];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+struct OpShape {
+    int NIJ, NJmax;
+};
+
+static OpShape op_shape(const hb_assembly_desc *a)
+{
+    const int nij = (a->test_p1 ? 3 : 1) * (a->trial_p1 ? 3 : 1);
+    return {nij, 2};
+}
+
+static int choose_nj(const hb_assembly_desc *a)
+{
+    const OpShape s = op_shape(a);
+    int nj = (int)cdiv(a->E_t, 16);
+    return std::max(1, std::min(nj, s.NJmax));
+}
+
+static bool combo_ok(const hb_assembly_desc *a)
+{
+    if (a->op == HB_OP_SINGLE_LAYER)
+        return a->symmetric && a->test_p1 == a->trial_p1;
+    if (a->op == HB_OP_DOUBLE_LAYER) return !a->symmetric && !a->test_p1 && a->trial_p1;
+    if (a->op == HB_OP_HYPERSINGULAR2) return a->symmetric && a->test_p1 && a->trial_p1;
+    return false;
+}
+
+constexpr size_t kCounterBytes = 256;
+
+static size_t row_bytes(const hb_mesh_desc *m, const hb_assembly_desc *a)
+{
+    const int nj = choose_nj(a);
+    const int64_t W = std::min<int64_t>(16 * nj, a->d_end - a->d_begin);
+    return (size_t)m->E_x * op_shape(a).NIJ * W * sizeof(double);
+}
+
+template <int OP, bool TP1, bool SP1, int NJ>
+static int launch_pairs(const PairArgs &A, cudaStream_t st)
+{
+    constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
+    constexpr bool SYM = (OP != 1);
+    const size_t sm = (size_t)kWarps * smem_doubles_per_warp<OP, NIJ, NJ>() * sizeof(double);
+    auto kp = k_pairs<OP, TP1, SP1, NJ, SYM>;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, kWarps * 32, sm);
+    const int64_t rows = A.e1 - A.e0;
+    const int64_t items = rows * cdiv(A.m.E_x, 32) + rows * A.m.sing_max_per_row;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(1, per_sm) * nsm, cdiv(items, kWarps)));
+    int rc = cuda_check(cudaMemsetAsync(A.counter, 0, sizeof(unsigned long long), st), "counter reset");
+    if (rc) return rc;
+    kp<<<(unsigned)grid, kWarps * 32, sm, st>>>(A);
+    return cuda_check(cudaGetLastError(), "pair kernel");
+}
+
+template <int OP, bool TP1, bool SP1>
+static int dispatch_nj(int nj, const PairArgs &A, cudaStream_t st)
+{
+    if (nj == 1) return launch_pairs<OP, TP1, SP1, 1>(A, st);
+    return launch_pairs<OP, TP1, SP1, 2>(A, st);
+}
+
+static int run_pairs(const hb_assembly_desc *a, int nj, const PairArgs &A, cudaStream_t st)
+{
+    if (a->op == 0 && !a->test_p1) return dispatch_nj<0, false, false>(nj, A, st);
+    if (a->op == 0 && a->test_p1) return dispatch_nj<0, true, true>(nj, A, st);
+    if (a->op == 1) return dispatch_nj<1, false, true>(nj, A, st);
+    return dispatch_nj<2, true, true>(nj, A, st);
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" size_t hb_assemble_min_workspace(const hb_mesh_desc *m, const hb_assembly_desc *a)
+{
+    if (!m || !a) return 0;
+    return row_bytes(m, a) + kCounterBytes;
+}
+
+extern "C" size_t hb_assemble_full_workspace(const hb_mesh_desc *m, const hb_assembly_desc *a)
+{
+    if (!m || !a) return 0;
+    return row_bytes(m, a) * (size_t)m->E_x + kCounterBytes;
+}
+
+extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, void *stream)
+{
+    if (!m || !a) { set_error("hb_assemble: null descriptor"); return HB_ERR_INVALID; }
+    if (!combo_ok(a)) {
+        set_error("hb_assemble: unsupported op/space combination (op=%d test_p1=%d trial_p1=%d sym=%d)",
+                  a->op, a->test_p1, a->trial_p1, a->symmetric);
+        return HB_ERR_UNSUPPORTED;
+    }
+    if (a->E_t < 1 || a->d_begin < 0 || a->d_end > a->E_t || a->d_begin >= a->d_end || m->E_x < 1 ||
+        m->N_x < 3 || !a->blocks_dev || !(a->step > 0) || !(a->alpha > 0)) {
+        set_error("hb_assemble: invalid sizes or parameters (E_t=%lld d=[%lld,%lld) E_x=%lld)",
+                  (long long)a->E_t, (long long)a->d_begin, (long long)a->d_end, (long long)m->E_x);
+        return HB_ERR_INVALID;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nj = choose_nj(a);
+    const int W = 16 * nj;
+    const size_t rb = row_bytes(m, a);
+    if (!a->workspace_dev || a->workspace_bytes < rb + kCounterBytes) {
+        set_error("hb_assemble: workspace %zu bytes < one row chunk (%zu bytes)", a->workspace_bytes, rb);
+        return HB_ERR_WORKSPACE;
+    }
+    const size_t q_bytes = (a->workspace_bytes - kCounterBytes) & ~(size_t)255;
+    const int64_t rows_per_chunk = std::max<int64_t>(1, std::min<int64_t>(m->E_x, (int64_t)(q_bytes / rb)));
+    const int64_t R = a->test_p1 ? m->N_x : m->E_x, C = a->trial_p1 ? m->N_x : m->E_x;
+    const int64_t nb = a->d_end - a->d_begin;
+    const bool p1p1 = a->test_p1 && a->trial_p1;
+    if (p1p1) {
+        int rc = cuda_check(cudaMemsetAsync(a->blocks_dev, 0, (size_t)nb * R * C * sizeof(double), st), "memset");
+        if (rc) return rc;
+    }
+
+    PairArgs A{};
+    A.m = *m;
+    A.step = a->step;
+    A.alpha = a->alpha;
+    A.d_eps = a->d_eps;
+    A.r_eps = a->r_eps;
+    A.inv2a = 1.0 / (2.0 * a->alpha);
+    A.inv2a2 = 1.0 / (2.0 * a->alpha * a->alpha);
+    A.inva = 1.0 / a->alpha;
+    A.kconst = (a->op == 0) ? 1.0 / sqrt(kPi * a->alpha * a->alpha * a->alpha) : 1.0 / sqrt(kPi * a->alpha);
+    A.halve_diag = p1p1 ? 1 : 0;
+    A.Q = (double *)a->workspace_dev;
+    A.counter = (unsigned long long *)((char *)a->workspace_dev + q_bytes);
+
+    int64_t d0 = a->d_begin;
+    while (d0 < a->d_end) {
+        // slots i_t in [max(1, d0-1), d1] must fit the W lanes-x-slots of a warp
+        const int64_t d1 = std::min<int64_t>(a->d_end, (d0 <= 1) ? (int64_t)W : d0 + W - 2);
+        A.d0 = (int)d0;
+        A.d1 = (int)d1;
+        A.nd = (int)(d1 - d0);
+        A.it_lo = (int)std::max<int64_t>(1, d0 - 1);
+        A.it_hi = (int)d1;
+        A.need_special = d0 <= 1;
+        for (int64_t e0 = 0; e0 < m->E_x; e0 += rows_per_chunk) {
+            const int64_t e1 = std::min(m->E_x, e0 + rows_per_chunk);
+            A.e0 = e0;
+            A.e1 = e1;
+            int rc = run_pairs(a, nj, A, st);
+            if (rc) return rc;
+            FinArgs F{};
+            F.Q = A.Q;
+            F.out = a->blocks_dev;
+            F.E_x = m->E_x; F.N_x = m->N_x; F.R = R; F.C = C; F.e0 = e0; F.e1 = e1;
+            F.d0 = (int)d0; F.nd = A.nd; F.d_begin = (int)a->d_begin;
+            F.star_indptr = m->star_indptr_dev; F.star_elem = m->star_elem_dev;
+            F.star_local = m->star_local_dev; F.tri_nodes = m->tri_nodes_dev;
+            if (!a->test_p1 && !a->trial_p1) {
+                dim3 g((unsigned)cdiv(m->E_x, 32), (unsigned)cdiv(e1 - e0, 4));
+                k_fin_p0p0<<<g, 256, 0, st>>>(F);
+            } else if (!a->test_p1) {
+                dim3 g((unsigned)(e1 - e0), (unsigned)cdiv(m->N_x, 32));
+                k_fin_p0p1<<<g, 256, 0, st>>>(F);
+            } else {
+                dim3 g((unsigned)m->N_x, (unsigned)cdiv(m->N_x, 32));
+                k_fin_p1p1_accum<<<g, 256, 0, st>>>(F);
+            }
+            rc = cuda_check(cudaGetLastError(), "finalize");
+            if (rc) return rc;
+        }
+        if (p1p1) {
+            const int64_t nt = cdiv(R, 32);
+            dim3 g((unsigned)(nt * (nt + 1) / 2), (unsigned)(d1 - d0));
+            k_symmetrize<<<g, 256, 0, st>>>(a->blocks_dev, R, d0 - a->d_begin);
+            int rc = cuda_check(cudaGetLastError(), "symmetrize");
+            if (rc) return rc;
+        }
+        d0 = d1;
+    }
+    return HB_OK;
+}

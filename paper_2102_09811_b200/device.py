@@ -1,0 +1,131 @@
+"""Device-resident mesh and quadrature tables (host precompute -> HBM).
+
+Everything the reference builds on the host before its pass loop
+(heatbem/assembly.py:201-206: vertex arrays, both product rules, the
+touching CSR with case ids and permutations, the Duffy tables) is built
+here with numpy once per (mesh, quadrature config) and uploaded as
+contiguous float64 / int64 tensors.  Three index lists are added for the
+device work decomposition: the singular work list (touching CSR positions
+per test row, upper-triangular for symmetric operators), the node stars
+(element, local vertex) per node for the p1 gathers, and the per-triangle
+surface curls of the hat functions (heatbem/assembly.py:289-311).
+"""
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+
+from . import _native
+from .quadrature import QuadratureConfig, duffy_tables, rule_tables, touching_csr
+
+
+def _curls(mesh) -> np.ndarray:
+    """curl of hat i on triangle e = (v_{i+1} - v_{i+2}) / (2 area_e): (E_x, 3, 3)."""
+    v = mesh.triangle_vertices()
+    out = np.empty((mesh.n_triangles, 3, 3))
+    for i in range(3):
+        out[:, i, :] = (v[:, (i + 1) % 3, :] - v[:, (i + 2) % 3, :]) / (2.0 * mesh.areas[:, None])
+    return out
+
+
+class HostTables:
+    """numpy side of the device tables (also what the CPU oracle consumes)."""
+
+    def __init__(self, mesh, config: QuadratureConfig):
+        c = np.ascontiguousarray
+        self.E_x, self.N_x = mesh.n_triangles, mesh.n_vertices
+        self.tri_nodes = c(mesh.triangles, dtype=np.int64)
+        self.verts_tri = c(mesh.triangle_vertices())
+        self.normals, self.centroids = c(mesh.normals), c(mesh.centroids)
+        self.diameters, self.areas = c(mesh.diameters), c(mesh.areas)
+        self.reg = [c(a) for a in rule_tables(mesh, config.regular_order)]
+        self.near = [c(a) for a in rule_tables(mesh, config.near_order)]
+        self.tn = [c(a) for a in touching_csr(mesh)]
+        self.duf = [c(a) for a in duffy_tables(config.singular_order)]
+        indptr, idx = self.tn[0], self.tn[1]
+        rows = np.repeat(np.arange(self.E_x, dtype=np.int64), np.diff(indptr))
+        self.sing_row = rows
+        self.sing = {}
+        for sym in (False, True):
+            keep = idx >= rows if sym else np.ones(len(idx), dtype=bool)
+            pos = np.flatnonzero(keep).astype(np.int64)
+            cnt = np.bincount(rows[keep], minlength=self.E_x)
+            rp = np.zeros(self.E_x + 1, dtype=np.int64)
+            np.cumsum(cnt, out=rp[1:])
+            self.sing[sym] = (pos, rp, int(cnt.max()) if len(cnt) else 0)
+        self.star = [c(a) for a in mesh.node_star()]
+        self.star_max = int(np.diff(self.star[0]).max())
+        self.curls = c(_curls(mesh))
+
+
+class DeviceTables:
+    """Device copies of :class:`HostTables` plus ready-made C descriptors."""
+
+    def __init__(self, mesh, config: QuadratureConfig, device):
+        import torch
+
+        self.host = H = HostTables(mesh, config)
+        self.device = device
+        up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+        self.t = {
+            "tri_nodes": up(H.tri_nodes), "verts_tri": up(H.verts_tri), "normals": up(H.normals),
+            "centroids": up(H.centroids), "diameters": up(H.diameters), "areas": up(H.areas),
+            "reg_hats": up(H.reg[0]), "reg_w": up(H.reg[1]), "reg_pts": up(H.reg[2]),
+            "near_hats": up(H.near[0]), "near_w": up(H.near[1]), "near_pts": up(H.near[2]),
+            "tn_indptr": up(H.tn[0]), "tn_idx": up(H.tn[1]), "tn_case": up(H.tn[2]),
+            "tn_permt": up(H.tn[3]), "tn_perms": up(H.tn[4]),
+            "duf_off": up(H.duf[0]), "duf_t": up(H.duf[1]), "duf_s": up(H.duf[2]), "duf_w": up(H.duf[3]),
+            "sing_row": up(H.sing_row),
+            "star_indptr": up(H.star[0]), "star_elem": up(H.star[1]), "star_local": up(H.star[2]),
+            "curls": up(H.curls),
+        }
+        for sym in (False, True):
+            pos, rp, _ = H.sing[sym]
+            self.t[f"sing_pos_{int(sym)}"] = up(pos)
+            self.t[f"sing_rowptr_{int(sym)}"] = up(rp)
+        self._desc = {sym: self._make_desc(sym) for sym in (False, True)}
+
+    def _make_desc(self, symmetric: bool) -> _native.MeshDesc:
+        t, H, p = self.t, self.host, _native.ptr
+        d = _native.MeshDesc()
+        d.E_x, d.N_x = H.E_x, H.N_x
+        d.tri_nodes_dev, d.verts_tri_dev = p(t["tri_nodes"]), p(t["verts_tri"])
+        d.normals_dev, d.centroids_dev = p(t["normals"]), p(t["centroids"])
+        d.diameters_dev, d.areas_dev = p(t["diameters"]), p(t["areas"])
+        d.reg_hats_dev, d.reg_w_dev, d.reg_pts_dev = p(t["reg_hats"]), p(t["reg_w"]), p(t["reg_pts"])
+        d.n_reg = len(H.reg[1])
+        d.near_hats_dev, d.near_w_dev, d.near_pts_dev = p(t["near_hats"]), p(t["near_w"]), p(t["near_pts"])
+        d.n_near = len(H.near[1])
+        d.tn_indptr_dev, d.tn_idx_dev, d.tn_case_dev = p(t["tn_indptr"]), p(t["tn_idx"]), p(t["tn_case"])
+        d.tn_permt_dev, d.tn_perms_dev = p(t["tn_permt"]), p(t["tn_perms"])
+        d.duf_off_dev, d.duf_t_dev = p(t["duf_off"]), p(t["duf_t"])
+        d.duf_s_dev, d.duf_w_dev = p(t["duf_s"]), p(t["duf_w"])
+        s = int(symmetric)
+        d.sing_pos_dev, d.sing_rowptr_dev = p(t[f"sing_pos_{s}"]), p(t[f"sing_rowptr_{s}"])
+        d.sing_max_per_row = H.sing[symmetric][2]
+        d.sing_row_dev = p(t["sing_row"])
+        d.star_indptr_dev, d.star_elem_dev = p(t["star_indptr"]), p(t["star_elem"])
+        d.star_local_dev = p(t["star_local"])
+        d.star_max = H.star_max
+        return d
+
+    def desc(self, symmetric: bool) -> _native.MeshDesc:
+        return self._desc[bool(symmetric)]
+
+
+_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def device_tables(mesh, config: QuadratureConfig, device=None) -> DeviceTables:
+    """Cached per mesh object (meshes are treated as immutable, as in the
+    reference), quadrature config and device."""
+    import torch
+
+    _native.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    per_mesh = _CACHE.setdefault(mesh, {})
+    key = (config.regular_order, config.singular_order, str(dev))
+    if key not in per_mesh:
+        per_mesh[key] = DeviceTables(mesh, config, dev)
+    return per_mesh[key]
