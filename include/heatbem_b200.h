@@ -17,7 +17,8 @@
  *                            builds blocks [d_begin, d_end) of V, V11, K or D2.
  *   hb_curl_combine          heatbem/assembly.py:314-334
  *                            (hypersingular_from_single_layer).
- *   hb_potential             heatbem/_field_numba.py:15-79 (_eval_potential).
+ *   hb_potential             heatbem/_field_numba.py:15-79 (_eval_potential)
+ *                            plus the per-point loop of field.py:147-167.
  *   hb_toeplitz_apply        heatbem/solver.py:47-73 (apply_toeplitz).
  *   hb_forward_subst_step    heatbem/solver.py:178-182 (history update of
  *                            forward_block_solve).
@@ -102,12 +103,50 @@ size_t hb_assemble_full_workspace(const hb_mesh_desc *mesh, const hb_assembly_de
  * of d_begin/d_end (so d-sharded ranks reproduce the 1-GPU blocks). */
 int hb_assemble(const hb_mesh_desc *mesh, const hb_assembly_desc *a, void *stream);
 
+/* Pair classes exactly as the assembly kernels see them, for test rows
+ * [e0, e1) and every trial element: out[(e-e0)*E_x + f] = 0 separated far,
+ * 1 separated near (bumped rule), 2 identical, 3 common edge, 4 common
+ * vertex -- the reference's _touching_csr + near test
+ * (assembly.py:119-144, _assembly_numba.py:139-151,217-223). */
+int hb_pair_classes(const hb_mesh_desc *mesh, int64_t e0, int64_t e1, int8_t *out_dev, void *stream);
+
 /* D = D2 + alpha^2 sum_o T_o^T V T_o per block (curl of the hat functions,
  * heatbem/assembly.py:289-334).  V: (nb, E_x, E_x), D2 and D: (nb, N_x, N_x);
  * D may alias D2.  curls_dev: (E_x, 3, 3) surface curls per local hat. */
 int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha,
                     const double *curls_dev, const double *V_dev, const double *D2_dev,
                     double *D_dev, void *stream);
+
+/* Interior potential, heatbem/_field_numba.py:15-79 (kind 0: single layer,
+ * kind 1: double layer).  Evaluation outputs are grouped by spatial point and
+ * time offset: group g = (gx[g], geps[g]) owns outputs gptr[g]..gptr[g+1]-1,
+ * output o has k[o] completed intervals (ascending within a group), the
+ * current-interval flag cur[o] (eps > 0 and k < E_t) and is written to
+ * out[out_idx[o]].  The kernel values of a group are evaluated once per
+ * (element, node, gap) and shared by all its output times.
+ * dens_dev: (E_t, E_x, nq) density at the spatial quadrature nodes;
+ * qpts_dev: (E_x, nq, 3); qw_dev (nq,); kmax = max k over all outputs. */
+int hb_potential(int kind, int64_t n_groups, int64_t E_t, int64_t E_x, int64_t nq,
+                 const double *gx_dev, const double *geps_dev, const int64_t *gptr_dev,
+                 const int64_t *k_dev, const uint8_t *cur_dev, const int64_t *out_idx_dev, int64_t kmax,
+                 const double *dens_dev, const double *qpts_dev, const double *qw_dev,
+                 const double *areas_dev, const double *normals_dev,
+                 double step, double alpha, double d_eps, double r_eps, double *out_dev, void *stream);
+
+/* y^k = sum_{d<=k} A^d x^{k-d} (heatbem/solver.py:47-73).  blocks
+ * (n_blocks, R, C) row-major; transpose applies A^d^T (input length R,
+ * output length C); diagonal_only uses A^0 for every k (mass matrix).
+ * x (n_steps, n_in), y (n_steps, n_out), n_steps <= n_blocks unless
+ * diagonal_only. */
+int hb_toeplitz_apply(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev,
+                      int transpose, int diagonal_only, int64_t n_steps,
+                      const double *x_dev, double *y_dev, void *stream);
+
+/* Forward-substitution history of heatbem/solver.py:178-182 for step k:
+ * acc -= sum_{d=1..k} A^d x^{k-d}, x holding the solved steps 0..k-1. */
+int hb_forward_subst_step(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev,
+                          int transpose, int64_t k, const double *x_dev, double *acc_dev,
+                          void *stream);
 
 /* FP64 DFMA throughput probe used for the roofline denominator:
  * runs `iters` dependent-chain iterations of 8 independent DFMA streams per

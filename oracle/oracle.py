@@ -21,7 +21,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libheatbem_oracle.so")
+_LIBQ_PATH = os.path.join(_HERE, "libheatbem_oracle_q.so")
 _lib = None
+_libq = None
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -36,9 +38,8 @@ _PROBLEM = [_INT, _INT, _INT, _INT, _I64, _I64, _D, _D, _D, _D,
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB_PATH) or (
-        os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "heatbem_oracle.c"))
-    ):
+    src = os.path.getmtime(os.path.join(_HERE, "heatbem_oracle.c"))
+    if force or any(not os.path.exists(p) or os.path.getmtime(p) < src for p in (_LIB_PATH, _LIBQ_PATH)):
         subprocess.check_call(["make", "-s", "-C", _HERE], stdout=subprocess.DEVNULL)
     return _LIB_PATH
 
@@ -59,6 +60,25 @@ def lib():
         L.hb_oracle_max_threads.restype = _INT
         _lib = L
     return _lib
+
+
+def libq():
+    """Quad-precision build (heatbem_oracle_q.c): exact value of the same quadrature."""
+    global _libq
+    if _libq is None:
+        if not os.path.exists(_LIBQ_PATH):
+            build()
+        L = ctypes.CDLL(_LIBQ_PATH)
+        L.hb_oracle_assemble_q.argtypes = _PROBLEM + [_I64, _D, _P, _INT]
+        L.hb_oracle_rows_q.argtypes = _PROBLEM + [_I64, _D, _P, _I64, _P, _INT]
+        L.hb_oracle_potential_q.argtypes = [_INT, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                            _I64, _I64, _I64, _I64, _D, _D, _D, _D, _P, _INT]
+        L.hb_oracle_curl_combine_q.argtypes = [_I64, _I64, _I64, _D, _P, _P, _P, _P, _P, _INT]
+        for f in (L.hb_oracle_assemble_q, L.hb_oracle_rows_q, L.hb_oracle_potential_q,
+                  L.hb_oracle_curl_combine_q):
+            f.restype = _INT
+        _libq = L
+    return _libq
 
 
 def max_threads() -> int:
@@ -119,25 +139,28 @@ class OracleProblem:
                 m.n_vertices if self.trial_p1 else m.n_triangles)
 
 
-def assemble(mesh, timegrid, params, config, op: str, n_threads: int = 0) -> np.ndarray:
-    """Full (E_t, R, C) blocks, as heatbem.assembly._assemble_operator."""
+def assemble(mesh, timegrid, params, config, op: str, n_threads: int = 0, exact: bool = False) -> np.ndarray:
+    """Full (E_t, R, C) blocks, as heatbem.assembly._assemble_operator
+    (exact=True: the same quadrature in 113-bit arithmetic, rounded once)."""
     P = OracleProblem(mesh, params, config, op, timegrid.step)
     R, C = P.shape_rc
     out = np.empty((timegrid.n_steps, R, C))
-    rc = lib().hb_oracle_assemble(*P.args(), timegrid.n_steps, timegrid.step, _ptr(out), n_threads)
+    fn = libq().hb_oracle_assemble_q if exact else lib().hb_oracle_assemble
+    rc = fn(*P.args(), timegrid.n_steps, timegrid.step, _ptr(out), n_threads)
     if rc != 0:
         raise MemoryError("oracle assemble failed")
     return out
 
 
-def assemble_rows(mesh, timegrid, params, config, op: str, rows, n_threads: int = 0) -> np.ndarray:
+def assemble_rows(mesh, timegrid, params, config, op: str, rows, n_threads: int = 0,
+                  exact: bool = False) -> np.ndarray:
     """Rows of all blocks of a p0-test operator (V or K): (E_t, len(rows), C)."""
     P = OracleProblem(mesh, params, config, op, timegrid.step)
     rows = np.ascontiguousarray(rows, dtype=np.int64)
     _, C = P.shape_rc
     out = np.empty((timegrid.n_steps, len(rows), C))
-    rc = lib().hb_oracle_rows(*P.args(), timegrid.n_steps, timegrid.step, _ptr(rows), len(rows),
-                              _ptr(out), n_threads)
+    fn = libq().hb_oracle_rows_q if exact else lib().hb_oracle_rows
+    rc = fn(*P.args(), timegrid.n_steps, timegrid.step, _ptr(rows), len(rows), _ptr(out), n_threads)
     if rc != 0:
         raise RuntimeError(f"oracle rows failed ({rc})")
     return out
@@ -179,8 +202,24 @@ def curl_combine(V, D2, mesh, alpha):
     return out
 
 
+def curl_combine_exact(V, D2, mesh, alpha, n_threads: int = 0) -> np.ndarray:
+    """Quad-precision D = D2 + alpha^2 sum (curl . curl) V (inputs double)."""
+    from paper_2102_09811_b200.device import _curls
+
+    c = np.ascontiguousarray
+    V, D2 = c(V, dtype=np.float64), c(D2, dtype=np.float64)
+    curls = c(_curls(mesh))
+    tri = c(mesh.triangles, dtype=np.int64)
+    out = np.empty_like(D2)
+    rc = libq().hb_oracle_curl_combine_q(V.shape[0], mesh.n_triangles, mesh.n_vertices, float(alpha),
+                                         _ptr(tri), _ptr(curls), _ptr(V), _ptr(D2), _ptr(out), n_threads)
+    if rc != 0:
+        raise MemoryError("oracle curl combine failed")
+    return out
+
+
 def potential(kind, points, k_arr, eps_arr, cur_arr, dens, qpts, qw, areas, normals,
-              h_t, alpha, d_eps, r_eps, n_threads: int = 0) -> np.ndarray:
+              h_t, alpha, d_eps, r_eps, n_threads: int = 0, exact: bool = False) -> np.ndarray:
     c = np.ascontiguousarray
     points, dens, qpts, qw = c(points, dtype=np.float64), c(dens), c(qpts), c(qw)
     k_arr = c(k_arr, dtype=np.int64)
@@ -188,7 +227,8 @@ def potential(kind, points, k_arr, eps_arr, cur_arr, dens, qpts, qw, areas, norm
     cur = c(cur_arr, dtype=np.uint8)
     areas, normals = c(areas), c(normals)
     out = np.empty(len(points))
-    lib().hb_oracle_potential(int(kind), _ptr(points), _ptr(k_arr), _ptr(eps_arr), _ptr(cur),
+    fn = libq().hb_oracle_potential_q if exact else lib().hb_oracle_potential
+    fn(int(kind), _ptr(points), _ptr(k_arr), _ptr(eps_arr), _ptr(cur),
                               _ptr(dens), _ptr(qpts), _ptr(qw), _ptr(areas), _ptr(normals),
                               len(points), dens.shape[0], dens.shape[1], dens.shape[2],
                               h_t, alpha, d_eps, r_eps, _ptr(out), n_threads)

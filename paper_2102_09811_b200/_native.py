@@ -60,7 +60,7 @@ class AssemblyDesc(ctypes.Structure):
 EXPORTED = (
     "hb_version", "hb_last_error", "hb_assemble", "hb_assemble_min_workspace",
     "hb_assemble_full_workspace", "hb_curl_combine", "hb_potential",
-    "hb_toeplitz_apply", "hb_forward_subst_step", "hb_fp64_probe",
+    "hb_toeplitz_apply", "hb_forward_subst_step", "hb_fp64_probe", "hb_pair_classes",
 )
 
 _lib = None
@@ -85,16 +85,15 @@ def load():
         getattr(L, fn).restype = ctypes.c_size_t
     L.hb_curl_combine.argtypes = [ctypes.POINTER(MeshDesc), _I64, _D, _P, _P, _P, _P, _P]
     L.hb_curl_combine.restype = _INT
-    if hasattr(L, "hb_potential"):
-        L.hb_potential.argtypes = [_INT, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                                   _D, _D, _D, _D, _P, _P]
-        L.hb_potential.restype = _INT
-    if hasattr(L, "hb_toeplitz_apply"):
-        L.hb_toeplitz_apply.argtypes = [_I64, _I64, _I64, _P, _INT, _INT, _I64, _P, _P, _P]
-        L.hb_toeplitz_apply.restype = _INT
-    if hasattr(L, "hb_forward_subst_step"):
-        L.hb_forward_subst_step.argtypes = [_I64, _I64, _I64, _P, _INT, _I64, _P, _P, _P]
-        L.hb_forward_subst_step.restype = _INT
+    L.hb_potential.argtypes = [_INT, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _I64,
+                               _P, _P, _P, _P, _P, _D, _D, _D, _D, _P, _P]
+    L.hb_potential.restype = _INT
+    L.hb_toeplitz_apply.argtypes = [_I64, _I64, _I64, _P, _INT, _INT, _I64, _P, _P, _P]
+    L.hb_toeplitz_apply.restype = _INT
+    L.hb_forward_subst_step.argtypes = [_I64, _I64, _I64, _P, _INT, _I64, _P, _P, _P]
+    L.hb_forward_subst_step.restype = _INT
+    L.hb_pair_classes.argtypes = [ctypes.POINTER(MeshDesc), _I64, _I64, _P, _P]
+    L.hb_pair_classes.restype = _INT
     L.hb_fp64_probe.argtypes = [_I64, _I64, _P, _P]
     L.hb_fp64_probe.restype = _INT
     _lib = L

@@ -68,6 +68,7 @@ class BlockToeplitzMatrix:
     def blocks(self, value):
         self._host = np.asarray(value, dtype=np.float64)
         self._dev = None
+        self._lu_cache = None
 
     @property
     def device_blocks(self):
@@ -306,3 +307,17 @@ def load_blocks(path) -> BlockToeplitzMatrix:
     if data.size != n * r * c:
         raise ValueError("truncated block dump")
     return BlockToeplitzMatrix(data.reshape(n, r, c).astype(np.float64))
+
+
+def pair_classes(mesh, config: QuadratureConfig = QuadratureConfig(), rows=None, device=None) -> np.ndarray:
+    """(len(rows), E_x) int8 pair classes as the device kernels see them:
+    0 far, 1 near (bumped rule), 2 identical, 3 common edge, 4 common vertex."""
+    import torch
+
+    _native.require_cuda()
+    tabs = device_tables(mesh, config, device)
+    e0, e1 = (0, mesh.n_triangles) if rows is None else (int(rows[0]), int(rows[1]))
+    out = torch.empty((e1 - e0, mesh.n_triangles), dtype=torch.int8, device=tabs.device)
+    with torch.cuda.device(tabs.device):
+        _native.call("hb_pair_classes", tabs.desc(True), e0, e1, _native.ptr(out), _native.stream_handle())
+    return out.cpu().numpy()

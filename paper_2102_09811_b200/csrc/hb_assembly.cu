@@ -366,6 +366,50 @@ __device__ __forceinline__ double pair_jac(const PairArgs &A, int64_t e, int64_t
 }
 
 // ---------------------------------------------------------------------------
+// pair classification, shared by the pair kernel and hb_pair_classes
+// ---------------------------------------------------------------------------
+// position of f in e's touching list (binary search, as _assembly_numba.py:139-151), -1 if absent
+__device__ __forceinline__ int64_t touching_pos(const hb_mesh_desc &M, int64_t t_lo, int64_t t_hi, int64_t f)
+{
+    int64_t lo = t_lo, hi = t_hi;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1, v = __ldg(M.tn_idx_dev + mid);
+        if (v < f) lo = mid + 1;
+        else if (v > f) hi = mid;
+        else return mid;
+    }
+    return -1;
+}
+
+// near/far: sqrt((dx*dx + dy*dy) + dz*dz) < 2 max(diam_e, diam_f), every
+// operation separately rounded as in _assembly_numba.py:218-223 (no FMA)
+__device__ __forceinline__ bool near_test(const hb_mesh_desc &M, const double ce[3], double de, int64_t f)
+{
+    const double dx = __dsub_rn(ce[0], __ldg(M.centroids_dev + 3 * f));
+    const double dy = __dsub_rn(ce[1], __ldg(M.centroids_dev + 3 * f + 1));
+    const double dz = __dsub_rn(ce[2], __ldg(M.centroids_dev + 3 * f + 2));
+    const double dist = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    return dist < 2.0 * fmax(de, __ldg(M.diameters_dev + f));
+}
+
+// class codes: 0 far, 1 near, 2 identical, 3 common edge, 4 common vertex
+__global__ void k_pair_classes(const hb_mesh_desc M, int64_t e0, int64_t e1, int8_t *out)
+{
+    const int64_t n = (e1 - e0) * M.E_x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = e0 + i / M.E_x, f = i % M.E_x;
+        const int64_t tp = touching_pos(M, __ldg(M.tn_indptr_dev + e), __ldg(M.tn_indptr_dev + e + 1), f);
+        if (tp >= 0) {
+            out[i] = (int8_t)(2 + __ldg(M.tn_case_dev + tp));
+        } else {
+            double ce[3];
+            for (int c = 0; c < 3; ++c) ce[c] = __ldg(M.centroids_dev + 3 * e + c);
+            out[i] = near_test(M, ce, __ldg(M.diameters_dev + e), f) ? 1 : 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K1 body: separated pairs of one (test row e, 32-column segment) work item.
 // ---------------------------------------------------------------------------
 template <int OP, bool TP1, bool SP1, int NJ, bool SYM>
@@ -384,28 +428,15 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
     const double de = __ldg(M.diameters_dev + e);
 
     for (int64_t f = fb; f < fe; ++f) {
-        // touching pairs belong to the singular path (binary search as the reference does)
-        int64_t lo = t_lo, hi = t_hi;
-        bool touching = false;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1, v = __ldg(M.tn_idx_dev + mid);
-            if (v < f) lo = mid + 1;
-            else if (v > f) hi = mid;
-            else { touching = true; break; }
-        }
-        if (touching) continue;
+        // touching pairs belong to the singular path
+        if (touching_pos(M, t_lo, t_hi, f) >= 0) continue;
         const int64_t slot = (e - A.e0) * M.E_x + f;
         const double jac = pair_jac<OP>(A, e, f);
         if (OP == 2 && jac == 0.0) {   // n_x.n_y == 0: every staged value is +0
             write_zero_pair<NIJ>(A, slot, lane);
             continue;
         }
-        double cf[3];
-        for (int c = 0; c < 3; ++c) cf[c] = __ldg(M.centroids_dev + 3 * f + c);
-        const double dx = __dsub_rn(ce[0], cf[0]), dy = __dsub_rn(ce[1], cf[1]), dz = __dsub_rn(ce[2], cf[2]);
-        const double dist = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-        const double df = __ldg(M.diameters_dev + f);
-        const bool near = dist < 2.0 * fmax(de, df);
+        const bool near = near_test(M, ce, de, f);
         RegularGeom g;
         const int nq1 = near ? (int)M.n_near : (int)M.n_reg;
         const double *pts = near ? M.near_pts_dev : M.reg_pts_dev;
@@ -848,4 +879,16 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
         d0 = d1;
     }
     return HB_OK;
+}
+
+extern "C" int hb_pair_classes(const hb_mesh_desc *m, int64_t e0, int64_t e1, int8_t *out_dev, void *stream)
+{
+    if (!m || e0 < 0 || e1 > m->E_x || e0 >= e1 || !out_dev) {
+        set_error("hb_pair_classes: bad arguments");
+        return HB_ERR_INVALID;
+    }
+    const int64_t n = (e1 - e0) * m->E_x;
+    k_pair_classes<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 32), 256, 0, (cudaStream_t)stream>>>(*m, e0, e1,
+                                                                                                        out_dev);
+    return cuda_check(cudaGetLastError(), "hb_pair_classes");
 }

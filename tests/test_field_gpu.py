@@ -1,0 +1,67 @@
+"""Potentials (representation formula) vs the reference (golden) and the
+oracle.  Tolerance 1e-12 relative (north star: 1e-11; the potentials carry
+no time second difference, heatbem/tests/test_field.py uses 1e-12)."""
+import numpy as np
+import pytest
+
+import paper_2102_09811_b200 as hb
+from _hb_util import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def test_cube1_potentials_vs_reference():
+    g = golden("field")
+    m = hb.generate_cube_surface(1)
+    tg = hb.TimeGrid(1.0, 4)
+    p = hb.KernelParams(0.5, tg.step, length_scale=m.diameter)
+    pts = [hb.EvalPoint(x, t) for x, t in zip(g["cube1_x"], g["cube1_t"])]
+    sl, w1 = hb.eval_single_layer_potential(g["cube1_w"], pts, m, tg, p)
+    dl, w2 = hb.eval_double_layer_potential(g["cube1_u"], pts, m, tg, p)
+    rep, w3 = hb.represent(g["cube1_w"], g["cube1_u"], pts, m, tg, p)
+    for got, key in ((sl, "cube1_sl"), (dl, "cube1_dl"), (rep, "cube1_rep")):
+        ref = g[key]
+        assert np.allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max()), key
+    assert not (w1.any() or w2.any() or w3.any())
+
+
+def test_c4_subset_vs_reference():
+    """BASELINE config 4 shape: unit cube L4, N = 64, seeded densities, the
+    golden points at all 64 time-step ends (represent_grid path)."""
+    g = golden("field")
+    m = hb.unit_cube_mesh(4)
+    tg = hb.TimeGrid(1.0, 64)
+    p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
+    rng = np.random.default_rng(0)
+    q = rng.uniform(-1, 1, (64, m.n_triangles))
+    gg = rng.uniform(-1, 1, (64, m.n_vertices))
+    X = rng.uniform(0.05, 0.95, (100000, 3))
+    u = hb.represent_grid(q, gg, X[g["c4_sel"]], m, tg, p).reshape(-1)
+    ref = g["c4_u"]
+    assert np.max(np.abs(u - ref)) <= 1e-11 * np.abs(ref).max()
+    pts = [hb.EvalPoint(X[i], k / 64) for i in g["c4_sel"][:2] for k in range(1, 65)]
+    u2, _ = hb.represent(q, gg, pts, m, tg, p)
+    assert np.array_equal(u2, u[:128])
+
+
+def test_random_points_vs_oracle(oracle):
+    from paper_2102_09811_b200.field import _decompose, _interp_density_np
+    from paper_2102_09811_b200.quadrature import rule_tables
+
+    m = hb.unit_cube_mesh(2)
+    tg = hb.TimeGrid(1.0, 16)
+    p = hb.KernelParams(0.7, tg.step, length_scale=m.diameter)
+    rng = np.random.default_rng(7)
+    w = rng.standard_normal((16, m.n_triangles))
+    uu = rng.standard_normal((16, m.n_vertices))
+    X = rng.uniform(0.1, 0.9, (40, 3))
+    T = np.concatenate([rng.uniform(0, 1.2, 30), np.arange(1, 11) / 16])
+    pts = [hb.EvalPoint(x, t) for x, t in zip(X, T)]
+    hats, qw, qpts = rule_tables(m, 6)
+    k, eps = _decompose(T, tg.step)
+    cur = (eps > 0) & (k < 16)
+    for kind, coef in ((0, w), (1, uu)):
+        got, _ = (hb.eval_single_layer_potential if kind == 0 else hb.eval_double_layer_potential)(coef, pts, m, tg, p)
+        ref = oracle.potential(kind, X, k, eps, cur, _interp_density_np(coef, m, hats), qpts, qw, m.areas,
+                               m.normals, tg.step, p.alpha, p.delta_eps, p.rho_eps)
+        assert np.allclose(got, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max()), kind

@@ -1,0 +1,91 @@
+"""Block-Toeplitz apply / forward substitution / FGMRES on the device vs
+dense expansions and the reference's config-2 Dirichlet solve."""
+import numpy as np
+import pytest
+
+import paper_2102_09811_b200 as hb
+from _hb_util import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def dense(blocks, E_t, transpose=False, diag=False):
+    nb, R, C = blocks.shape
+    A = blocks.transpose(0, 2, 1) if transpose else blocks
+    r, c = A.shape[1:]
+    out = np.zeros((E_t * r, E_t * c))
+    for k in range(E_t):
+        for i in range(k + 1):
+            d = k - i
+            if diag and d:
+                continue
+            out[k * r:(k + 1) * r, i * c:(i + 1) * c] = A[0 if diag else d]
+    return out
+
+
+@pytest.mark.parametrize("R,C,E_t", [(7, 7, 5), (20, 11, 9), (64, 40, 33)])
+def test_apply_toeplitz_vs_dense(R, C, E_t):
+    rng = np.random.default_rng(R)
+    B = rng.standard_normal((E_t, R, C))
+    M = hb.BlockToeplitzMatrix(B)
+    x = rng.standard_normal((E_t, C))
+    y = hb.apply_toeplitz(M, x)
+    ref = (dense(B, E_t) @ x.ravel()).reshape(E_t, R)
+    assert np.allclose(y, ref, rtol=1e-13, atol=1e-12)
+    xt = rng.standard_normal((E_t, R))
+    yt = hb.apply_toeplitz(M, xt, transpose_blocks=True)
+    assert np.allclose(yt, (dense(B, E_t, True) @ xt.ravel()).reshape(E_t, C), rtol=1e-13, atol=1e-12)
+    assert np.array_equal(hb.apply_toeplitz(M.transposed(), xt), yt)
+    assert np.array_equal(hb.apply_toeplitz(M.transposed(), x, transpose_blocks=True), y)
+    Mass = hb.BlockToeplitzMatrix(B[:1], diagonal_only=True)
+    assert np.allclose(hb.apply_toeplitz(Mass, x), (dense(B[:1], E_t, diag=True) @ x.ravel()).reshape(E_t, R))
+
+
+def test_forward_block_solve_exact():
+    rng = np.random.default_rng(1)
+    E_t, n = 12, 30
+    B = 0.1 * rng.standard_normal((E_t, n, n))
+    B[0] += 4 * np.eye(n)
+    M = hb.BlockToeplitzMatrix(B)
+    rhs = rng.standard_normal((E_t, n))
+    x = hb.forward_block_solve(M, rhs)
+    assert np.allclose(hb.apply_toeplitz(M, x), rhs, rtol=1e-12, atol=1e-12)
+    xt = hb.forward_block_solve(M, rhs, transpose_blocks=True)
+    assert np.allclose(hb.apply_toeplitz(M, xt, transpose_blocks=True), rhs, rtol=1e-12, atol=1e-12)
+
+
+def test_fgmres_identity_and_nonconvergence():
+    rng = np.random.default_rng(2)
+    b = rng.standard_normal((4, 5))
+    x, rep = hb.fgmres(lambda v: v, b, rel_tol=1e-12)
+    assert rep.converged and np.allclose(x, b)
+    A = rng.standard_normal((20, 20))
+    x, rep = hb.fgmres(lambda v: A @ v, rng.standard_normal(20), rel_tol=1e-14, max_iter=3, restart=2)
+    assert not rep.converged and rep.iterations == 3
+
+
+def test_c2_dirichlet_solve_vs_reference():
+    """BASELINE config 2 solve: rhs = 1/2 M g + K g with g the X10 projection
+    of G(x - y0, t + 0.1); FGMRES(V) with forward substitution, tol 1e-10."""
+    g = golden("solve_c2")
+    m = hb.unit_cube_mesh(3)
+    tg = hb.TimeGrid(1.0, 32)
+    p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
+    V = hb.assemble_single_layer(m, tg, p)
+    K = hb.assemble_double_layer(m, tg, p)
+    Mm = hb.assemble_mass(m, tg)
+    y0 = np.array([1.5, 1.5, 1.5])
+    data = hb.project_to_space(lambda x, t, n=None: hb.fundamental(np.asarray(x) - y0, t + 0.1, 1.0), m, tg, "X10")
+    assert np.allclose(data, g["g"], rtol=1e-13, atol=1e-16)
+    rhs = 0.5 * hb.apply_toeplitz(Mm, data) + hb.apply_toeplitz(K, data)
+    assert np.max(np.abs(rhs - g["rhs"])) <= 1e-10 * np.abs(g["rhs"]).max()
+    x, rep = hb.fgmres(hb.toeplitz_operator(V), rhs, rel_tol=1e-10,
+                       right_precond=lambda v: hb.forward_block_solve(V, v))
+    assert rep.converged and rep.residual <= 1e-10
+    assert np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"]) <= 1e-9
+    xf = hb.forward_block_solve(V, rhs)
+    assert np.linalg.norm(xf - g["x_fwd"]) / np.linalg.norm(g["x_fwd"]) <= 1e-9
+    Vx = hb.apply_toeplitz(V, g["probe_x"])
+    assert np.max(np.abs(Vx - g["probe_Vx"])) <= 1e-10 * np.abs(g["probe_Vx"]).max()
+    KTx = hb.apply_toeplitz(K, g["probe_x"][:, :m.n_triangles], True)
+    assert np.max(np.abs(KTx - g["probe_KTx"])) <= 1e-10 * np.abs(g["probe_KTx"]).max()
