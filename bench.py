@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark: BEM matrix entries assembled per second (fp64 V / K / D).
+
+Workload = BASELINE config 2 (the config the headline metric is quoted on
+that fits one GPU): unit-cube surface refined 3x (768 triangles, 386 nodes),
+N = 32 time steps, alpha = 1.  One step assembles V (p0 x p0), K (p0 x p1;
+K' is the blockwise-transposed view, not re-counted) and D = D2 + curl(V)
+(p1 x p1) -- E_t (E_x^2 + E_x N_x + N_x^2) = 33.1 M entries.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+N > 1 runs one process per GPU (torchrun); ranks own contiguous ranges of
+time-difference blocks d (no data-path collective: block d depends only on
+the kernel at gaps d-1, d, d+1), value = all ranks' entries / max-over-ranks
+device time.  ``--impl reference`` times the reference's CPU algorithm (the
+oracle port, oracle/heatbem_oracle.c, all host threads) on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BEM matrix entries assembled/sec (fp64 V/K/D) and % of FP64 roofline"
+UNIT = "entries/s"
+LEVEL, E_T, ALPHA = 3, 32, 1.0
+WORKLOAD = ("BASELINE config 2: unit-cube [0,1]^3 surface refined 3x (768 triangles, 386 nodes), "
+            "N=32 steps, T=1, alpha=1, quadrature (4,4): V p0p0 + K p0p1 (K' = transposed view) + "
+            "D = D2 + alpha^2 curl(V) p1p1")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def setup():
+    import paper_2102_09811_b200 as hb
+
+    mesh = hb.unit_cube_mesh(LEVEL)
+    tg = hb.TimeGrid(1.0, E_T)
+    params = hb.KernelParams(ALPHA, tg.step, length_scale=mesh.diameter)
+    return hb, mesh, tg, params
+
+
+def entries_total(mesh, nb):
+    E, N = mesh.n_triangles, mesh.n_vertices
+    return nb * (E * E + E * N + N * N)
+
+
+def d_range(rank, world, E_t):
+    base, rem = divmod(E_t, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm: the oracle port of the reference algorithm
+# ---------------------------------------------------------------------------
+def cpu_reference_step(mesh, tg, params, threads):
+    """One bounded sample of the reference algorithm on the config-2 mesh:
+    one full _toeplitz_pass (i_t = 1) of each of V, K, D2 plus the curl
+    combine of one block, extrapolated to the E_t + 1 passes and E_t blocks
+    of a full assembly (every i_t >= 1 pass does identical work)."""
+    import paper_2102_09811_b200 as hb
+    from oracle import oracle as O
+
+    q = hb.QuadratureConfig()
+    t_pass = {}
+    for op in ("V", "K", "D2"):
+        t0 = time.perf_counter()
+        O.single_pass(mesh, params, q, op, tg.step, 1, n_threads=threads)
+        t_pass[op] = time.perf_counter() - t0
+    E, N = mesh.n_triangles, mesh.n_vertices
+    rng = np.random.default_rng(0)
+    V1, D21 = rng.standard_normal((1, E, E)), rng.standard_normal((1, N, N))
+    t0 = time.perf_counter()
+    O.curl_combine(V1, D21, mesh, params.alpha)
+    t_curl = time.perf_counter() - t0
+    t_full = (tg.n_steps + 1) * sum(t_pass.values()) + tg.n_steps * t_curl
+    return t_full, t_pass, t_curl
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    O.build()
+    hb, mesh, tg, params = setup()
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_step(mesh, tg, params, threads)
+    ts = []
+    for _ in range(args.steps):
+        ts.append(cpu_reference_step(mesh, tg, params, threads)[0])
+    t = statistics.median(ts)
+    n_entries = entries_total(mesh, tg.n_steps)
+    val = n_entries / t
+    sample = (f"per step: one full i_t=1 pass each of V, K, D2 on the config-2 mesh + curl combine of one block "
+              f"(oracle/heatbem_oracle.c, {threads} OpenMP threads), extrapolated to (E_t+1)=33 passes and "
+              f"32 blocks = {n_entries} entries")
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (config-2 mesh generated in-run)",
+           "config": {"workload": WORKLOAD, "E_x": mesh.n_triangles, "N_x": mesh.n_vertices, "E_t": tg.n_steps},
+           "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# native arm
+# ---------------------------------------------------------------------------
+def fp64_peak(torch, _native):
+    """In-run DFMA probe (MEASURED_PEAKS.json carries no FP64 entry)."""
+    sink = torch.zeros(148 * 8, dtype=torch.float64, device="cuda")
+    grid, iters = 148 * 8, 40000
+    for _ in range(2):
+        _native.call("hb_fp64_probe", grid, 2000, _native.ptr(sink), _native.stream_handle())
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    _native.call("hb_fp64_probe", grid, iters, _native.ptr(sink), _native.stream_handle())
+    e.record()
+    torch.cuda.synchronize()
+    return grid * 256 * iters * 8 * 2 / (s.elapsed_time(e) * 1e-3) / 1e12
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+def run_native(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    hb, mesh, tg, params = setup()
+    from paper_2102_09811_b200 import _native, device as hbdev, workload
+    from paper_2102_09811_b200.assembly import _assemble_operator
+
+    _native.require_cuda()
+    d0, d1 = d_range(rank, world, tg.n_steps)
+    nb = d1 - d0
+    q = hb.QuadratureConfig()
+    E, N = mesh.n_triangles, mesh.n_vertices
+    dev = torch.device("cuda", local_rank)
+    outV = torch.empty((nb, E, E), dtype=torch.float64, device=dev)
+    outK = torch.empty((nb, E, N), dtype=torch.float64, device=dev)
+    outD = torch.empty((nb, N, N), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    tabs = hbdev.device_tables(mesh, q, dev)
+
+    def step(stats=None):
+        st = stats if stats is not None else [None, None, None]
+        _assemble_operator(0, False, False, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outV,
+                           stats=st[0])
+        _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(d0, d1), out=outK,
+                           stats=st[1])
+        _assemble_operator(2, True, True, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outD,
+                           stats=st[2])
+        _native.call("hb_curl_combine", tabs.desc(True), nb, params.alpha, _native.ptr(tabs.t["curls"]),
+                     _native.ptr(outV), _native.ptr(outD), _native.ptr(outD), _native.stream_handle())
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    peak = fp64_peak(torch, _native) if rank == 0 else None
+
+    # ---- timed region: K steps, events per step, L2 flushed between steps ----
+    stats = [_native.AssemblyStats() for _ in range(3)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = []
+    gpu = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[0]) if world == 1 else local_rank
+    with ClockSampler(gpu) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            step()
+            e.record()
+            e.synchronize()
+            step_ms.append(s.elapsed_time(e))
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    # kernel timing pass (stats sync inside each call; kept out of the headline)
+    for _ in range(max(1, args.steps // 2)):
+        step(stats)
+    torch.cuda.synchronize()
+
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    n_entries = entries_total(mesh, tg.n_steps)   # all ranks together
+    value = n_entries / (ms_per_step * 1e-3)
+
+    # ---- e2e: public API, host buffers, copies inside the timed region ----
+    Hpin = hbdev.pin_host_tables(hbdev.host_tables(mesh, q))
+    pinV = torch.empty(outV.shape, dtype=torch.float64).pin_memory()
+    pinK = torch.empty(outK.shape, dtype=torch.float64).pin_memory()
+    pinD = torch.empty(outD.shape, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        hbdev.drop_device_tables(mesh)              # re-upload inputs from pinned host memory
+        V = hb.assemble_single_layer(mesh, tg, params, q, d_range=(d0, d1))
+        K = hb.assemble_double_layer(mesh, tg, params, q, d_range=(d0, d1))
+        D = hb.assemble_hypersingular(mesh, tg, params, q, single_layer=V, d_range=(d0, d1))
+        pinV.copy_(V.device_blocks, non_blocking=True)
+        pinK.copy_(K.device_blocks, non_blocking=True)
+        pinD.copy_(D.device_blocks, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for _ in range(args.steps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        e2e_step()
+        e.record()
+        e.synchronize()
+        e2e_ms.append(s.elapsed_time(e))
+    te = torch.tensor([sum(e2e_ms) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = n_entries / (float(te.item()) * 1e-3)
+    h2d = Hpin.pinned_bytes
+    d2h = (pinV.numel() + pinK.numel() + pinD.numel()) * 8
+
+    # ---- roofline of the dominant kernel: the K pair kernel (k_pairs<1,...>) ----
+    it_lo, it_hi = max(1, d0 - 1), d1
+    n_windows = 0
+    dd = d0
+    while dd < d1:   # windows of <= 32 gap slots (csrc/hb_assembly.cu)
+        nd1 = min(d1, 32 if dd <= 1 else dd + 30)
+        n_windows += 1
+        dd = nd1
+    wK = workload.operator_work(mesh, "K", 1, q)
+    gapsK = (it_hi - it_lo + 1) + 2 * (n_windows - 1)
+    flops_per_call = wK["flops"] * gapsK           # one call = n_windows launches
+    sK = stats[1]
+    pair_ms_per_call = sK.pair_ms / max(1, args.steps // 2)
+    launches_per_call = sK.pair_launches / max(1, args.steps // 2)
+    achieved = flops_per_call / (pair_ms_per_call * 1e-3) / 1e12
+    shares = {nm: st.pair_ms / max(1e-9, st.pair_ms + st.finalize_ms) for nm, st in zip(("V", "K", "D2"), stats)}
+    launches_step = sum(st.launches for st in stats) / max(1, args.steps // 2) + 1
+    traffic = load_traffic().get("k_pairs_K_dram_bytes_per_launch")
+
+    if rank != 0:
+        return
+    clocks = clk.summary()
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+
+        O.build()
+        threads = os.cpu_count() or 1
+        cpu_reference_step(mesh, tg, params, threads)         # page-in / thread start
+        ts = [cpu_reference_step(mesh, tg, params, threads)[0] for _ in range(3)]
+        cpu = {"value": n_entries / statistics.median(ts), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": "3 x (one full i_t=1 pass each of V, K, D2 on the config-2 mesh + curl combine of one "
+                         "block), oracle/heatbem_oracle.c with all host threads, extrapolated to the 33 passes / "
+                         "32 blocks of a full assembly"}
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: BASELINE config-2 mesh and time grid generated in-run (no dataset)",
+        "config": {"workload": WORKLOAD, "E_x": E, "N_x": N, "E_t": tg.n_steps, "entries_per_step": n_entries,
+                   "parallelism": f"d-sharded x{world} (contiguous time-difference blocks per rank)",
+                   "l2": "flushed between timed steps (256 MiB device write, outside the events)",
+                   "fp64_peak_tflops": peak, "pair_kernel_share": shares},
+        "roofline": {"bound": "fp64", "kernel": "k_pairs<op=K> (double-layer pair kernel)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                     "peak_source": "measured in-run (hb_fp64_probe DFMA loop; MEASURED_PEAKS.json has no FP64 entry)",
+                     "flops_per_launch": flops_per_call / max(1.0, launches_per_call),
+                     "flops_definition": "SURVEY 8(d): N_eval (pairs x points x gaps) x 124 flop",
+                     "avg_launch_ms": pair_ms_per_call / max(1.0, launches_per_call),
+                     "traffic": traffic},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "path": "public API assemble_single_layer / assemble_double_layer / assemble_hypersingular, "
+                        "mesh tables re-uploaded from pinned host memory and all blocks copied to pinned host "
+                        "memory every step"},
+        "clocks": clocks,
+        "gpu_launches": int(round(launches_step * args.steps * world)),
+        "impl": "native",
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("native", "reference"), default="native")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl")
+    try:
+        run_native(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

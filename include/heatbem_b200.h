@@ -82,6 +82,17 @@ typedef struct {
     int64_t star_max;               /* max star size                        */
 } hb_mesh_desc;
 
+/* Optional per-call statistics (host memory).  When hb_assembly_desc.stats
+ * is non-NULL, hb_assemble brackets every pair-kernel and finalize launch
+ * with CUDA events on `stream`, synchronises the stream before returning
+ * and ADDS the elapsed times and launch counts here. */
+typedef struct {
+    double pair_ms;                 /* k_pairs launches (regular + singular) */
+    double finalize_ms;             /* staging -> blocks (+ symmetrize)      */
+    int64_t pair_launches;
+    int64_t launches;               /* all kernels launched by the call      */
+} hb_assembly_stats;
+
 typedef struct {
     int op;                         /* HB_OP_*                              */
     int test_p1, trial_p1, symmetric;
@@ -92,6 +103,7 @@ typedef struct {
     double *blocks_dev;             /* (d_end-d_begin, R, C) row-major      */
     void *workspace_dev;            /* staging, >= hb_assemble_min_workspace */
     size_t workspace_bytes;
+    hb_assembly_stats *stats;       /* optional (NULL: no timing, no sync)  */
 } hb_assembly_desc;
 
 /* bytes of staging for one test-row chunk (the minimum) and for all rows */

@@ -47,12 +47,17 @@ class MeshDesc(ctypes.Structure):
     ]
 
 
+class AssemblyStats(ctypes.Structure):
+    _fields_ = [("pair_ms", _D), ("finalize_ms", _D), ("pair_launches", _I64), ("launches", _I64)]
+
+
 class AssemblyDesc(ctypes.Structure):
     _fields_ = [
         ("op", _INT), ("test_p1", _INT), ("trial_p1", _INT), ("symmetric", _INT),
         ("E_t", _I64), ("step", _D), ("alpha", _D), ("d_eps", _D), ("r_eps", _D),
         ("d_begin", _I64), ("d_end", _I64),
         ("blocks_dev", _P), ("workspace_dev", _P), ("workspace_bytes", ctypes.c_size_t),
+        ("stats", ctypes.POINTER(AssemblyStats)),
     ]
 
 

@@ -166,7 +166,7 @@ def _workspace(tables, desc_m, desc_a, device, cap):
 
 def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, mesh, timegrid,
                        params: KernelParams, config: QuadratureConfig, instrumentation,
-                       d_range=None, device=None, workspace_bytes=None, stream=None):
+                       d_range=None, device=None, workspace_bytes=None, stream=None, stats=None, out=None):
     import torch
 
     _native.require_cuda()
@@ -179,7 +179,12 @@ def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, 
     R = N_x if test_p1 else E_x
     C = N_x if trial_p1 else E_x
     dev = tabs.device
-    blocks = torch.empty((d1 - d0, R, C), dtype=torch.float64, device=dev)
+    if out is not None:
+        if tuple(out.shape) != (d1 - d0, R, C) or out.dtype != torch.float64 or not out.is_contiguous():
+            raise ValueError("out must be a contiguous float64 tensor of shape (n_blocks, R, C)")
+        blocks = out
+    else:
+        blocks = torch.empty((d1 - d0, R, C), dtype=torch.float64, device=dev)
     a = _native.AssemblyDesc()
     a.op, a.test_p1, a.trial_p1, a.symmetric = op, int(test_p1), int(trial_p1), int(symmetric)
     a.E_t, a.step = E_t, timegrid.step
@@ -189,6 +194,10 @@ def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, 
     m = tabs.desc(symmetric)
     ws = _workspace(tabs, m, a, dev, _DEFAULT_WS_CAP if workspace_bytes is None else int(workspace_bytes))
     a.workspace_dev, a.workspace_bytes = ws.data_ptr(), ws.numel()
+    if stats is not None:
+        import ctypes
+
+        a.stats = ctypes.pointer(stats)
     t0 = time.perf_counter()
     with torch.cuda.device(dev):
         _native.call("hb_assemble", m, a, _native.stream_handle(stream))

@@ -142,6 +142,28 @@ struct DuffyGeom {
 };
 
 // ---------------------------------------------------------------------------
+// kernel value at one (point pair, gap) in the general branch (scaled by 4 pi):
+//   op 0: (rho/(2a^2) + delta/(a rho)) erf(x) + sqrt(delta/(pi a^3)) exp(-x^2)
+//   op 1: -(rn/rho) [(1/(2a) - delta/rho^2) erf(x) + sqrt(delta/(pi a)) exp(-x^2)/rho]
+//         (the -(rn/rho) factor lives in the hat weights)
+//   op 2: erf(x) / rho
+// Every product/sum is pinned (fma / __dmul_rn): after unrolling the gap
+// slots the compiler must not contract the same expression differently per
+// slot, or a gap's value would depend on the slot it lands in.
+// ---------------------------------------------------------------------------
+template <int OP, int NJ>
+__device__ __forceinline__ double eval_general(const PairArgs &A, const Slots<OP, NJ> &T, int j, double rho,
+                                               double s1, double s2)
+{
+    const double x = __dmul_rn(rho, T.cx[j]);
+    const double e1 = erf(x);
+    if (OP == 2) return __dmul_rn(e1, s1);
+    const double e2 = exp(-__dmul_rn(x, x));
+    if (OP == 0) return fma(fma(T.dl[j], s2, s1), e1, __dmul_rn(T.kk[j], e2));
+    return fma(fma(-T.dl[j], s1, A.inv2a), e1, __dmul_rn(__dmul_rn(T.kk[j], s2), e2));
+}
+
+// ---------------------------------------------------------------------------
 // one element pair, all time gaps of the window
 // ---------------------------------------------------------------------------
 template <int OP, bool TP1, bool SP1, int NJ, class Geom>
@@ -200,7 +222,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                 const double rn = rx * ny[0] + ry * ny[1] + rz * ny[2];
                 const double iq = 1.0 / rho;
                 const double U = small ? 0.0 : -rn * iq;
-                const double P = iq * iq;
+                const double P = 1.0 / __dmul_rn(rho, rho);
                 p[1] = P;
                 p[2] = iq;
 #pragma unroll
@@ -236,16 +258,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                 const double s2 = (OP == 2) ? 0.0 : p[2];
                 double val[NJ];
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    const double x = rho * T.cx[j];
-                    if (OP == 0) {
-                        val[j] = fma(T.dl[j], s2, s1) * erf(x) + T.kk[j] * exp(-x * x);
-                    } else if (OP == 1) {
-                        val[j] = fma(-T.dl[j], s1, A.inv2a) * erf(x) + (T.kk[j] * s2) * exp(-x * x);
-                    } else {
-                        val[j] = erf(x) * s1;
-                    }
-                }
+                for (int j = 0; j < NJ; ++j) val[j] = eval_general<OP>(A, T, j, rho, s1, s2);
 #pragma unroll
                 for (int i = 0; i < NIJ; ++i) {
                     const double h = p[HOFF + i];
@@ -261,15 +274,10 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                 const bool sm = rho <= A.r_eps;
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
-                    const double x = rho * T.cx[j];
                     double val;
-                    if (OP == 0) {
-                        val = sm ? 2.0 * T.kk[j] : fma(T.dl[j], s2, s1) * erf(x) + T.kk[j] * exp(-x * x);
-                    } else if (OP == 1) {
-                        val = sm ? 0.0 : fma(-T.dl[j], s1, A.inv2a) * erf(x) + (T.kk[j] * s2) * exp(-x * x);
-                    } else {
-                        val = sm ? T.kk[j] : erf(x) * s1;
-                    }
+                    if (OP == 0) val = sm ? 2.0 * T.kk[j] : eval_general<OP>(A, T, j, rho, s1, s2);
+                    else if (OP == 1) val = sm ? 0.0 : eval_general<OP>(A, T, j, rho, s1, s2);
+                    else val = sm ? T.kk[j] : eval_general<OP>(A, T, j, rho, s1, s2);
 #pragma unroll
                     for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(val, p[HOFF + i], acc[j][i]);
                 }
@@ -637,33 +645,43 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
     if (!any) return;
     for (int dc = 0; dc < F.nd; dc += 32) {
         const int ndc = min(32, F.nd - dc);
+        // stage X[d][m][n0..n0+31] (coalesced over n), add this chunk's
+        // elements one at a time in ascending e, write back: the sequence of
+        // additions is X = ((0 + s_e1) + s_e2) + ... whatever the row chunking
+        for (int dl = warp; dl < ndc; dl += kWarps) {
+            const int64_t n = n0 + lane;
+            const int64_t b = F.d0 + dc + dl - F.d_begin;
+            tile[lane][dl] = n < F.N_x ? F.out[(b * F.R + m) * F.C + n] : 0.0;
+        }
+        __syncthreads();
         for (int nl = warp; nl < 32; nl += kWarps) {
             const int64_t n = n0 + nl;
-            double acc = 0.0;
             if (n < F.N_x && lane < ndc) {
+                double x = tile[nl][lane];
                 const int64_t sn0 = __ldg(F.star_indptr + n), sn1 = __ldg(F.star_indptr + n + 1);
                 for (int64_t a = sm0; a < sm1; ++a) {
                     const int64_t e = __ldg(F.star_elem + a);
                     if (e < F.e0 || e >= F.e1) continue;
                     const int64_t i = __ldg(F.star_local + a);
                     const double *Qe = F.Q + (e - F.e0) * F.E_x * 9 * F.nd;
+                    double se = 0.0;
                     for (int64_t b = sn0; b < sn1; ++b) {
                         const int64_t f = __ldg(F.star_elem + b);
                         if (f < e) continue;
                         const int64_t j = __ldg(F.star_local + b);
-                        acc += Qe[(f * 9 + 3 * i + j) * F.nd + dc + lane];
+                        se += Qe[(f * 9 + 3 * i + j) * F.nd + dc + lane];
                     }
+                    x += se;
                 }
+                tile[nl][lane] = x;
             }
-            tile[nl][lane] = acc;
         }
         __syncthreads();
         for (int dl = warp; dl < ndc; dl += kWarps) {
             const int64_t n = n0 + lane;
             if (n < F.N_x) {
                 const int64_t b = F.d0 + dc + dl - F.d_begin;
-                double *x = F.out + (b * F.R + m) * F.C + n;
-                *x = *x + tile[lane][dl];
+                F.out[(b * F.R + m) * F.C + n] = tile[lane][dl];
             }
         }
         __syncthreads();
@@ -787,6 +805,44 @@ extern "C" size_t hb_assemble_full_workspace(const hb_mesh_desc *m, const hb_ass
     return row_bytes(m, a) * (size_t)m->E_x + kCounterBytes;
 }
 
+namespace hb {
+// brackets launches with events when stats are requested
+struct LaunchTimer {
+    hb_assembly_stats *st;
+    cudaStream_t s;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pair_ev, fin_ev;
+    int64_t launches = 0, pair_launches = 0;
+    cudaEvent_t begin(cudaStream_t s_)
+    {
+        if (!st) return nullptr;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s_);
+        return e;
+    }
+    void end(cudaEvent_t b, bool is_pair, cudaStream_t s_)
+    {
+        if (!st) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s_);
+        (is_pair ? pair_ev : fin_ev).emplace_back(b, e);
+    }
+    int finish()
+    {
+        if (!st) return HB_OK;
+        int rc = cuda_check(cudaStreamSynchronize(s), "stats sync");
+        for (auto &pr : pair_ev) { float ms = 0; cudaEventElapsedTime(&ms, pr.first, pr.second); st->pair_ms += ms; }
+        for (auto &pr : fin_ev) { float ms = 0; cudaEventElapsedTime(&ms, pr.first, pr.second); st->finalize_ms += ms; }
+        for (auto *v : {&pair_ev, &fin_ev})
+            for (auto &pr : *v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+        st->launches += launches;
+        st->pair_launches += pair_launches;
+        return rc;
+    }
+};
+}  // namespace hb
+
 extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, void *stream)
 {
     if (!m || !a) { set_error("hb_assemble: null descriptor"); return HB_ERR_INVALID; }
@@ -833,6 +889,8 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
     A.Q = (double *)a->workspace_dev;
     A.counter = (unsigned long long *)((char *)a->workspace_dev + q_bytes);
 
+    LaunchTimer LT{a->stats, st};
+    if (p1p1) LT.launches += 0;   // memset is not a kernel
     int64_t d0 = a->d_begin;
     while (d0 < a->d_end) {
         // slots i_t in [max(1, d0-1), d1] must fit the W lanes-x-slots of a warp
@@ -847,8 +905,13 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
             const int64_t e1 = std::min(m->E_x, e0 + rows_per_chunk);
             A.e0 = e0;
             A.e1 = e1;
+            cudaEvent_t ev = LT.begin(st);
             int rc = run_pairs(a, nj, A, st);
             if (rc) return rc;
+            LT.end(ev, true, st);
+            LT.launches += 1;
+            LT.pair_launches += 1;
+            ev = LT.begin(st);
             FinArgs F{};
             F.Q = A.Q;
             F.out = a->blocks_dev;
@@ -868,17 +931,22 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
             }
             rc = cuda_check(cudaGetLastError(), "finalize");
             if (rc) return rc;
+            LT.end(ev, false, st);
+            LT.launches += 1;
         }
         if (p1p1) {
             const int64_t nt = cdiv(R, 32);
             dim3 g((unsigned)(nt * (nt + 1) / 2), (unsigned)(d1 - d0));
+            cudaEvent_t ev = LT.begin(st);
             k_symmetrize<<<g, 256, 0, st>>>(a->blocks_dev, R, d0 - a->d_begin);
             int rc = cuda_check(cudaGetLastError(), "symmetrize");
             if (rc) return rc;
+            LT.end(ev, false, st);
+            LT.launches += 1;
         }
         d0 = d1;
     }
-    return HB_OK;
+    return LT.finish();
 }
 
 extern "C" int hb_pair_classes(const hb_mesh_desc *m, int64_t e0, int64_t e1, int8_t *out_dev, void *stream)

@@ -114,15 +114,15 @@ __global__ void __launch_bounds__(kPotWarps * 32) k_potential(const PotArgs P)
                             double c = (hi >= 0 && hi < P.E_t) ? Ds[hi] : 0.0;
                             if (lo >= 0 && lo < P.E_t && (lo < k || cu[r])) c -= Ds[lo];
                             if (c == 0.0) continue;
-                            s += c * Gs[m];
+                            s = fma(c, Gs[m], s);
                         }
-                        if (cu[r] && k >= 0 && k < P.E_t) s += Ds[k] * G0[0];
-                        el[r] += w * s;
+                        if (cu[r] && k >= 0 && k < P.E_t) s = fma(Ds[k], G0[0], s);
+                        el[r] = fma(w, s, el[r]);
                     }
                     __syncwarp();
                 }
                 const double a2 = 2.0 * __ldg(P.areas + e);
-                for (int r = 0; r < kOutPerLane; ++r) acc[r] += a2 * el[r];
+                for (int r = 0; r < kOutPerLane; ++r) acc[r] = fma(a2, el[r], acc[r]);
             }
             for (int r = 0; r < kOutPerLane; ++r)
                 if (ok[r]) P.out[P.out_idx[oi[r]]] = acc[r];

@@ -60,14 +60,21 @@ class HostTables:
 
 
 class DeviceTables:
-    """Device copies of :class:`HostTables` plus ready-made C descriptors."""
+    """Device copies of :class:`HostTables` plus ready-made C descriptors.
+    With ``pinned`` host staging the uploads are async copies from page-locked
+    memory (the end-to-end benchmark path)."""
 
-    def __init__(self, mesh, config: QuadratureConfig, device):
+    def __init__(self, mesh, config: QuadratureConfig, device, host: HostTables | None = None):
         import torch
 
-        self.host = H = HostTables(mesh, config)
+        self.host = H = host if host is not None else host_tables(mesh, config)
         self.device = device
-        up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+        pin = getattr(H, "pinned", None)
+
+        def up(a):
+            if pin is not None:
+                return pin[id(a)].to(device, non_blocking=True)
+            return torch.from_numpy(np.ascontiguousarray(a)).to(device)
         self.t = {
             "tri_nodes": up(H.tri_nodes), "verts_tri": up(H.verts_tri), "normals": up(H.normals),
             "centroids": up(H.centroids), "diameters": up(H.diameters), "areas": up(H.areas),
@@ -115,6 +122,33 @@ class DeviceTables:
 
 
 _CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_HOST: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def host_tables(mesh, config: QuadratureConfig) -> HostTables:
+    per_mesh = _HOST.setdefault(mesh, {})
+    key = (config.regular_order, config.singular_order)
+    if key not in per_mesh:
+        per_mesh[key] = HostTables(mesh, config)
+    return per_mesh[key]
+
+
+def pin_host_tables(H: HostTables):
+    """Page-locked copies of every host array (uploads become async DMA)."""
+    import torch
+
+    arrays = [H.tri_nodes, H.verts_tri, H.normals, H.centroids, H.diameters, H.areas, *H.reg, *H.near,
+              *H.tn, *H.duf, H.sing_row, *H.star, H.curls]
+    for sym in (False, True):
+        arrays += list(H.sing[sym][:2])
+    H.pinned = {id(a): torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays}
+    H.pinned_bytes = sum(t.numel() * t.element_size() for t in H.pinned.values())
+    return H
+
+
+def drop_device_tables(mesh):
+    """Forget the uploaded tables of a mesh (next call re-uploads them)."""
+    _CACHE.pop(mesh, None)
 
 
 def device_tables(mesh, config: QuadratureConfig, device=None) -> DeviceTables:
@@ -127,5 +161,5 @@ def device_tables(mesh, config: QuadratureConfig, device=None) -> DeviceTables:
     per_mesh = _CACHE.setdefault(mesh, {})
     key = (config.regular_order, config.singular_order, str(dev))
     if key not in per_mesh:
-        per_mesh[key] = DeviceTables(mesh, config, dev)
+        per_mesh[key] = DeviceTables(mesh, config, dev, host_tables(mesh, config))
     return per_mesh[key]

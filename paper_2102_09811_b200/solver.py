@@ -134,13 +134,16 @@ def fgmres(op, rhs, rel_tol: float = 1e-8, max_iter: int = 500, restart: int = 5
     shape = b.shape
     b = b.reshape(-1)
 
+    # user callables see the array type the caller passed (numpy in -> numpy)
+    view = (lambda v: v.reshape(shape)) if was_torch else (lambda v: v.reshape(shape).cpu().numpy())
+
     def A(v):
-        return torch.as_tensor(op(v.reshape(shape)), dtype=torch.float64, device=b.device).reshape(-1).clone()
+        return torch.as_tensor(op(view(v)), dtype=torch.float64, device=b.device).reshape(-1).clone()
 
     def M(v):
         if right_precond is None:
             return v
-        return torch.as_tensor(right_precond(v.reshape(shape)), dtype=torch.float64, device=b.device).reshape(-1)
+        return torch.as_tensor(right_precond(view(v)), dtype=torch.float64, device=b.device).reshape(-1)
 
     def out(x):
         x = x.reshape(shape)
