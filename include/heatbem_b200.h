@@ -154,6 +154,12 @@ int hb_toeplitz_apply(int64_t n_blocks, int64_t R, int64_t C, const double *bloc
                       int transpose, int diagonal_only, int64_t n_steps,
                       const double *x_dev, double *y_dev, void *stream);
 
+/* Partial product of a d-sharded operator: y^k = sum over the LOCAL blocks
+ * d in [d_off, d_off + n_blocks), d <= k, of A^d x^{k-d}; summing y over the
+ * ranks (one all-reduce) gives apply_toeplitz of the full operator. */
+int hb_toeplitz_apply_range(int64_t d_off, int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev,
+                            int transpose, int64_t n_steps, const double *x_dev, double *y_dev, void *stream);
+
 /* Forward-substitution history of heatbem/solver.py:178-182 for step k:
  * acc -= sum_{d=1..k} A^d x^{k-d}, x holding the solved steps 0..k-1. */
 int hb_forward_subst_step(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev,

@@ -66,6 +66,7 @@ EXPORTED = (
     "hb_version", "hb_last_error", "hb_assemble", "hb_assemble_min_workspace",
     "hb_assemble_full_workspace", "hb_curl_combine", "hb_potential",
     "hb_toeplitz_apply", "hb_forward_subst_step", "hb_fp64_probe", "hb_pair_classes",
+    "hb_toeplitz_apply_range",
 )
 
 _lib = None
@@ -95,6 +96,8 @@ def load():
     L.hb_potential.restype = _INT
     L.hb_toeplitz_apply.argtypes = [_I64, _I64, _I64, _P, _INT, _INT, _I64, _P, _P, _P]
     L.hb_toeplitz_apply.restype = _INT
+    L.hb_toeplitz_apply_range.argtypes = [_I64, _I64, _I64, _I64, _P, _INT, _I64, _P, _P, _P]
+    L.hb_toeplitz_apply_range.restype = _INT
     L.hb_forward_subst_step.argtypes = [_I64, _I64, _I64, _P, _INT, _I64, _P, _P, _P]
     L.hb_forward_subst_step.restype = _INT
     L.hb_pair_classes.argtypes = [ctypes.POINTER(MeshDesc), _I64, _I64, _P, _P]

@@ -16,8 +16,9 @@ constexpr int kTR = 16, kTK = 16, kTC = 32;
 // diagonal_only: only d == 0 with x[k] for every k.
 __global__ void __launch_bounds__(256) k_toeplitz(const double *__restrict__ blocks, int64_t R, int64_t C,
                                                   int transpose, int diagonal_only, int64_t n_steps,
-                                                  int64_t k_lo, int d_min, const double *__restrict__ x,
-                                                  double *__restrict__ y, int accumulate_neg)
+                                                  int64_t k_lo, int64_t d_min, int64_t d_off, int64_t n_blocks,
+                                                  const double *__restrict__ x, double *__restrict__ y,
+                                                  int accumulate_neg)
 {
     __shared__ double As[kTR][kTC + 1];
     __shared__ double Xs[kTK][kTC + 1];
@@ -27,9 +28,9 @@ __global__ void __launch_bounds__(256) k_toeplitz(const double *__restrict__ blo
     const int64_t r = r0 + tr, k = k0 + tk;
     double acc = 0.0;
     const int64_t kmax_tile = min(k0 + kTK - 1, n_steps - 1);
-    const int64_t dmax = diagonal_only ? 0 : kmax_tile;
-    for (int64_t d = d_min; d <= dmax; ++d) {
-        const double *Ad = blocks + d * R * C;
+    const int64_t dmax = diagonal_only ? 0 : min(kmax_tile, d_off + n_blocks - 1);
+    for (int64_t d = max(d_min, d_off); d <= dmax; ++d) {
+        const double *Ad = blocks + (d - d_off) * R * C;
         for (int64_t c0 = 0; c0 < n_in; c0 += kTC) {
             // stage A^d(r0.., c0..) and x[k - d][c0..] for the tile's k
             for (int i = threadIdx.x; i < kTR * kTC; i += 256) {
@@ -81,9 +82,24 @@ extern "C" int hb_toeplitz_apply(int64_t n_blocks, int64_t R, int64_t C, const d
     }
     const int64_t n_out = transpose ? C : R;
     dim3 g((unsigned)cdiv(n_out, kTR), (unsigned)cdiv(n_steps, kTK));
-    k_toeplitz<<<g, 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, transpose, diagonal_only, n_steps, 0, 0,
-                                                    x_dev, y_dev, 0);
+    k_toeplitz<<<g, 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, transpose, diagonal_only, n_steps, 0, 0, 0,
+                                                    n_blocks, x_dev, y_dev, 0);
     return cuda_check(cudaGetLastError(), "hb_toeplitz_apply");
+}
+
+extern "C" int hb_toeplitz_apply_range(int64_t d_off, int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev,
+                                       int transpose, int64_t n_steps, const double *x_dev, double *y_dev,
+                                       void *stream)
+{
+    if (d_off < 0 || n_blocks < 1 || R < 1 || C < 1 || n_steps < 1 || !blocks_dev || !x_dev || !y_dev) {
+        set_error("hb_toeplitz_apply_range: bad arguments");
+        return HB_ERR_INVALID;
+    }
+    const int64_t n_out = transpose ? C : R;
+    dim3 g((unsigned)cdiv(n_out, kTR), (unsigned)cdiv(n_steps, kTK));
+    k_toeplitz<<<g, 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, transpose, 0, n_steps, 0, 0, d_off, n_blocks,
+                                                    x_dev, y_dev, 0);
+    return cuda_check(cudaGetLastError(), "hb_toeplitz_apply_range");
 }
 
 extern "C" int hb_forward_subst_step(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int transpose,
@@ -97,7 +113,7 @@ extern "C" int hb_forward_subst_step(int64_t n_blocks, int64_t R, int64_t C, con
     const int64_t n_out = transpose ? C : R;
     // one output time (k); y row offset so that y + k * n_out == acc
     dim3 g((unsigned)cdiv(n_out, kTR), 1);
-    k_toeplitz<<<g, 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, transpose, 0, k + 1, k, 1, x_dev,
+    k_toeplitz<<<g, 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, transpose, 0, k + 1, k, 1, 0, n_blocks, x_dev,
                                                     acc_dev - k * n_out, 1);
     return cuda_check(cudaGetLastError(), "hb_forward_subst_step");
 }

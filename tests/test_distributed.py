@@ -1,0 +1,95 @@
+"""N > 1 host logic on CPU: world_size-2 gloo process groups.
+
+The d-sharded products are checked against dense expansions; the per-rank
+CUDA partial product is replaced by a numpy stand-in (a test double -- the
+package itself has no CPU path)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2102_09811_b200 import distributed as D
+
+
+def test_block_ranges_cover_exactly_once():
+    for n in (1, 5, 16, 32, 64, 256):
+        for w in (1, 2, 3, 4, 8):
+            if w > n:
+                continue
+            rs = [D.block_range(r, w, n) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+
+
+def test_gap_slots_halo_accounting():
+    assert D.gap_slots(0, 32) == 32
+    assert D.gap_slots(0, 16) + D.gap_slots(16, 32) == 34        # one extra halo pair
+    assert D.gap_slots(0, 256) == 256 + 2 * 8            # 9 windows: [0,32) then 30 blocks each
+    assert D.gap_slots(3, 5) == 4                          # gaps 2..5
+
+
+def _numpy_partial(self, x, d_min=0):
+    A = self.local.numpy()
+    if self.transpose:
+        A = A.transpose(0, 2, 1)
+    E_t = x.shape[0]
+    y = np.zeros((E_t, A.shape[1]))
+    for k in range(E_t):
+        for d in range(max(self.d0, d_min), min(self.d1, k + 1)):
+            y[k] += A[d - self.d0] @ x[k - d].numpy()
+    return torch.from_numpy(y)
+
+
+def _worker(rank, world, port, B, x, rhs, out):
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        D.ShardedToeplitz.local_partial = _numpy_partial
+        n = B.shape[0]
+        d0, d1 = D.block_range(rank, world, n)
+        for tr in (False, True):
+            S = D.ShardedToeplitz(torch.from_numpy(B[d0:d1].copy()), d0, d1, n, transpose_blocks=tr)
+            xx = torch.from_numpy(x if not tr else x[:, : B.shape[1]].copy())
+            y = S.apply(xx)
+            xs = S.forward_solve(torch.from_numpy(rhs if not tr else rhs[:, : B.shape[2]].copy()))
+            full = D.gather_blocks(S)
+            if rank == 0:
+                out[f"y{int(tr)}"] = y.numpy()
+                out[f"x{int(tr)}"] = xs.numpy()
+                out[f"full{int(tr)}"] = full.numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_apply_and_forward_solve_gloo(world):
+    rng = np.random.default_rng(0)
+    E_t, n = 9, 6
+    B = 0.2 * rng.standard_normal((E_t, n, n))
+    B[0] += 3 * np.eye(n)
+    x = rng.standard_normal((E_t, n))
+    rhs = rng.standard_normal((E_t, n))
+    out = mp.Manager().dict()
+    mp.spawn(_worker, args=(world, _free_port(), B, x, rhs, out), nprocs=world, join=True)
+    for tr in (False, True):
+        A = B.transpose(0, 2, 1) if tr else B
+        dense = np.zeros((E_t * n, E_t * n))
+        for k in range(E_t):
+            for i in range(k + 1):
+                dense[k * n:(k + 1) * n, i * n:(i + 1) * n] = A[k - i]
+        assert np.allclose(out[f"y{int(tr)}"].ravel(), dense @ x.ravel(), rtol=1e-13, atol=1e-13)
+        assert np.allclose(dense @ out[f"x{int(tr)}"].ravel(), rhs.ravel(), rtol=1e-12, atol=1e-12)
+        assert np.array_equal(out[f"full{int(tr)}"], B)
