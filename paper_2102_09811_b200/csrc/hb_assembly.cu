@@ -39,9 +39,13 @@
 #include <vector>
 
 #include "hb_common.cuh"
+#include "hb_special.cuh"
 
 #ifndef HB_PAIR_MINB
 #define HB_PAIR_MINB 2
+#endif
+#ifndef HB_FUSED
+#define HB_FUSED 1   // fused special-function evaluation (hb_special.cuh); 0 = CUDA erf/exp path
 #endif
 
 namespace hb {
@@ -79,7 +83,7 @@ __host__ __device__ constexpr int smem_doubles_per_warp() { return 32 * Layout<O
 // ---------------------------------------------------------------------------
 template <int OP, int NJ>
 struct Slots {
-    double dl[NJ], cx[NJ], kk[NJ];
+    double dl[NJ], cx[NJ], ic[NJ], kk[NJ];
     __device__ void init(const PairArgs &A, int t)
     {
 #pragma unroll
@@ -88,7 +92,8 @@ struct Slots {
             if (it > A.it_hi) it = A.it_hi;   // clamped slots compute finite values, never stored
             const double delta = (double)it * A.step;
             dl[j] = delta;
-            cx[j] = 1.0 / (2.0 * sqrt(A.alpha * delta));
+            ic[j] = 2.0 * sqrt(A.alpha * delta);     // 1 / cx: x = rho cx, 1/x = (1/rho) ic
+            cx[j] = 1.0 / ic[j];
             if (OP == 2) kk[j] = 1.0 / sqrt(kPi * A.alpha * delta);
             else kk[j] = sqrt(delta) * A.kconst;
         }
@@ -169,7 +174,7 @@ __device__ __forceinline__ double eval_general(const PairArgs &A, const Slots<OP
 template <int OP, bool TP1, bool SP1, int NJ, class Geom>
 __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq, const double ny[3],
                                           double jac, int64_t slot, const Slots<OP, NJ> &T,
-                                          double *geo, double *Ls, int lane)
+                                          double *geo, double *Ls, int lane, const double *tab)
 {
     constexpr int NT = TP1 ? 3 : 1, NS = SP1 ? 3 : 1, NIJ = NT * NS;
     using L = Layout<OP, NIJ>;
@@ -205,9 +210,10 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
             double *p = geo + lane * PAY;
             p[0] = rho;
             if (OP == 0) {
-                const double Aq = rho * A.inv2a2, Bq = A.inva / rho;
+                const double iq = 1.0 / rho;
+                const double Aq = rho * A.inv2a2, Bq = A.inva * iq;
                 p[1] = Aq;
-                p[2] = Bq;
+                p[2] = HB_FUSED ? iq : Bq;
 #pragma unroll
                 for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
                 if (A.need_special) {
@@ -223,10 +229,10 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                 const double iq = 1.0 / rho;
                 const double U = small ? 0.0 : -rn * iq;
                 const double P = 1.0 / __dmul_rn(rho, rho);
-                p[1] = P;
+                p[1] = HB_FUSED ? iq : P;
                 p[2] = iq;
 #pragma unroll
-                for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i] * U;
+                for (int i = 0; i < NIJ; ++i) p[HOFF + i] = HB_FUSED ? (H[i] * U) * A.inv2a : H[i] * U;
                 if (A.need_special) {
                     const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
 #pragma unroll
@@ -250,15 +256,30 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
         __syncwarp();
         const int nloc = min(32, nq - base);
         if (!any_small) {
+#ifdef HB_UNR
+            constexpr int UNR = HB_UNR;
+#else
             constexpr int UNR = (NJ == 1 && NIJ == 1) ? 2 : 1;
+#endif
 #pragma unroll UNR
             for (int k = s; k < nloc; k += 2) {
                 const double *p = geo + k * PAY;
                 const double rho = p[0], s1 = p[1];
                 const double s2 = (OP == 2) ? 0.0 : p[2];
                 double val[NJ];
+#if HB_FUSED
+                const unsigned mask = __activemask();
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    const double x = __dmul_rn(rho, T.cx[j]);
+                    const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
+                    const double f = special::eval<OP>(x, ix, tab, mask);
+                    val[j] = OP == 0 ? __dmul_rn(s1, f) : (OP == 1 ? f : __dmul_rn(s1, f));
+                }
+#else
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) val[j] = eval_general<OP>(A, T, j, rho, s1, s2);
+#endif
 #pragma unroll
                 for (int i = 0; i < NIJ; ++i) {
                     const double h = p[HOFF + i];
@@ -272,12 +293,25 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                 const double rho = p[0], s1 = p[1];
                 const double s2 = (OP == 2) ? 0.0 : p[2];
                 const bool sm = rho <= A.r_eps;
+#if HB_FUSED
+                const unsigned mask = __activemask();
+#endif
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
                     double val;
+#if HB_FUSED
+                    const double x = __dmul_rn(rho, T.cx[j]);
+                    const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
+                    const double f = special::eval<OP>(x, ix, tab, mask);
+                    const double g = OP == 0 ? __dmul_rn(s1, f) : (OP == 1 ? f : __dmul_rn(s1, f));
+                    if (OP == 0) val = sm ? 2.0 * T.kk[j] : g;
+                    else if (OP == 1) val = sm ? 0.0 : g;
+                    else val = sm ? T.kk[j] : g;
+#else
                     if (OP == 0) val = sm ? 2.0 * T.kk[j] : eval_general<OP>(A, T, j, rho, s1, s2);
                     else if (OP == 1) val = sm ? 0.0 : eval_general<OP>(A, T, j, rho, s1, s2);
                     else val = sm ? T.kk[j] : eval_general<OP>(A, T, j, rho, s1, s2);
+#endif
 #pragma unroll
                     for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(val, p[HOFF + i], acc[j][i]);
                 }
@@ -422,7 +456,7 @@ __global__ void k_pair_classes(const hb_mesh_desc M, int64_t e0, int64_t e1, int
 // ---------------------------------------------------------------------------
 template <int OP, bool TP1, bool SP1, int NJ, bool SYM>
 __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64_t seg, const Slots<OP, NJ> &T,
-                                             double *geo, double *Ls, int lane)
+                                             double *geo, double *Ls, int lane, const double *tab)
 {
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     const hb_mesh_desc &M = A.m;
@@ -455,7 +489,7 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
         g.nq1 = nq1;
         double ny[3];
         for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * f + c);
-        eval_pair<OP, TP1, SP1, NJ>(A, g, nq1 * nq1, ny, jac, slot, T, geo, Ls, lane);
+        eval_pair<OP, TP1, SP1, NJ>(A, g, nq1 * nq1, ny, jac, slot, T, geo, Ls, lane, tab);
     }
 }
 
@@ -465,7 +499,7 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
 // ---------------------------------------------------------------------------
 template <int OP, bool TP1, bool SP1, int NJ>
 __device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, const Slots<OP, NJ> &T,
-                                              double *geo, double *Ls, int lane)
+                                              double *geo, double *Ls, int lane, const double *tab)
 {
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     const hb_mesh_desc &M = A.m;
@@ -506,7 +540,7 @@ __device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, cons
     }
     double ny[3];
     for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * f + c);
-    eval_pair<OP, TP1, SP1, NJ>(A, g, off1 - off0, ny, jac, slot, T, geo, Ls, lane);
+    eval_pair<OP, TP1, SP1, NJ>(A, g, off1 - off0, ny, jac, slot, T, geo, Ls, lane, tab);
 }
 
 // ---------------------------------------------------------------------------
@@ -523,7 +557,10 @@ __global__ void __launch_bounds__(kWarps * 32, HB_PAIR_MINB) k_pairs(const PairA
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double *geo = smem + warp * smem_doubles_per_warp<OP, NIJ, NJ>();
+    double *tab = smem;
+    special::load_table(tab);
+    __syncthreads();
+    double *geo = smem + special::kTabDoubles + warp * smem_doubles_per_warp<OP, NIJ, NJ>();
     double *Ls = geo + 32 * Layout<OP, NIJ>::PAY;
     const hb_mesh_desc &M = A.m;
     const int64_t s_lo = __ldg(M.sing_rowptr_dev + A.e0), s_hi = __ldg(M.sing_rowptr_dev + A.e1);
@@ -538,10 +575,10 @@ __global__ void __launch_bounds__(kWarps * 32, HB_PAIR_MINB) k_pairs(const PairA
         it = __shfl_sync(kFull, it, 0);
         const int64_t item = (int64_t)it;
         if (item < n_sing) {
-            singular_item<OP, TP1, SP1, NJ>(A, s_lo + item, T, geo, Ls, lane);
+            singular_item<OP, TP1, SP1, NJ>(A, s_lo + item, T, geo, Ls, lane, tab);
         } else if (item - n_sing < n_reg) {
             const int64_t r = item - n_sing;
-            regular_item<OP, TP1, SP1, NJ, SYM>(A, A.e0 + r / nseg, r % nseg, T, geo, Ls, lane);
+            regular_item<OP, TP1, SP1, NJ, SYM>(A, A.e0 + r / nseg, r % nseg, T, geo, Ls, lane, tab);
         } else {
             break;
         }
@@ -758,7 +795,7 @@ static int launch_pairs(const PairArgs &A, cudaStream_t st)
 {
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     constexpr bool SYM = (OP != 1);
-    const size_t sm = (size_t)kWarps * smem_doubles_per_warp<OP, NIJ, NJ>() * sizeof(double);
+    const size_t sm = ((size_t)kWarps * smem_doubles_per_warp<OP, NIJ, NJ>() + special::kTabDoubles) * sizeof(double);
     auto kp = k_pairs<OP, TP1, SP1, NJ, SYM>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int dev = 0, nsm = 0, per_sm = 0;
