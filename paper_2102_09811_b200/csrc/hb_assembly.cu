@@ -256,30 +256,58 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
         __syncwarp();
         const int nloc = min(32, nq - base);
         if (!any_small) {
-#ifdef HB_UNR
-            constexpr int UNR = HB_UNR;
+#if HB_FUSED
+            // two quadrature points of the same parity per iteration, evaluated
+            // together per gap slot: their x are close, so the small/large-x
+            // branch skipping survives, and the two Horner chains interleave
+            const unsigned mask = __activemask();
+            if constexpr (NIJ == 9) {
+                // p1 x p1: nine hat weights per point -- one point per iteration
+                for (int k = s; k < nloc; k += 2) {
+                    const double *p = geo + k * PAY;
+                    const double rho = p[0], s1 = p[1];
+                    const double s2 = (OP == 2) ? 0.0 : p[2];
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) {
+                        const double x = __dmul_rn(rho, T.cx[j]);
+                        const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
+                        const double f = special::eval<OP>(x, ix, tab, mask);
+                        const double v = OP == 1 ? f : __dmul_rn(s1, f);
+#pragma unroll
+                        for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, p[HOFF + i], acc[j][i]);
+                    }
+                }
+            } else
+            for (int k = s; k < nloc; k += 4) {
+                const bool two = k + 2 < nloc;
+                const double *p0 = geo + k * PAY, *p1 = geo + (two ? k + 2 : k) * PAY;
+                const double rho0 = p0[0], rho1 = p1[0];
+                const double a0 = p0[1], a1 = p1[1];
+                const double b0 = (OP == 2) ? 0.0 : p0[2], b1 = (OP == 2) ? 0.0 : p1[2];
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    const double xs[2] = {__dmul_rn(rho0, T.cx[j]), __dmul_rn(rho1, T.cx[j])};
+                    const double ixs[2] = {__dmul_rn(OP == 0 ? b0 : a0, T.ic[j]), __dmul_rn(OP == 0 ? b1 : a1, T.ic[j])};
+                    double fs[2];
+                    special::eval_n<OP, 2>(xs, ixs, fs, tab, mask);
+                    const double v0 = OP == 1 ? fs[0] : __dmul_rn(a0, fs[0]);
+                    const double v1 = OP == 1 ? fs[1] : __dmul_rn(a1, fs[1]);
+#pragma unroll
+                    for (int i = 0; i < NIJ; ++i) {
+                        acc[j][i] = fma(v0, p0[HOFF + i], acc[j][i]);
+                        if (two) acc[j][i] = fma(v1, p1[HOFF + i], acc[j][i]);
+                    }
+                }
+            }
 #else
-            constexpr int UNR = (NJ == 1 && NIJ == 1) ? 2 : 1;
-#endif
-#pragma unroll UNR
+#pragma unroll 1
             for (int k = s; k < nloc; k += 2) {
                 const double *p = geo + k * PAY;
                 const double rho = p[0], s1 = p[1];
                 const double s2 = (OP == 2) ? 0.0 : p[2];
                 double val[NJ];
-#if HB_FUSED
-                const unsigned mask = __activemask();
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    const double x = __dmul_rn(rho, T.cx[j]);
-                    const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                    const double f = special::eval<OP>(x, ix, tab, mask);
-                    val[j] = OP == 0 ? __dmul_rn(s1, f) : (OP == 1 ? f : __dmul_rn(s1, f));
-                }
-#else
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) val[j] = eval_general<OP>(A, T, j, rho, s1, s2);
-#endif
 #pragma unroll
                 for (int i = 0; i < NIJ; ++i) {
                     const double h = p[HOFF + i];
@@ -287,6 +315,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                     for (int j = 0; j < NJ; ++j) acc[j][i] = fma(val[j], h, acc[j][i]);
                 }
             }
+#endif
         } else {
             for (int k = s; k < nloc; k += 2) {
                 const double *p = geo + k * PAY;

@@ -82,5 +82,60 @@ __device__ __forceinline__ double eval(double x, double ix, const double *__rest
     return r;
 }
 
+// All NJ gap slots of one quadrature point at once: one small-x and one
+// large-x region for the whole group, so the NJ independent Horner chains
+// interleave (ILP NJ) instead of being serialised by per-slot branches.
+template <int KIND, int NJ>
+__device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)[NJ], double (&r)[NJ],
+                                       const double *__restrict__ tab, unsigned mask)
+{
+    double t[NJ];
+    bool small[NJ], any_s = false, any_l = false;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        t[j] = __dmul_rn(x[j], x[j]);
+        small[j] = x[j] < kX0;
+        any_s |= small[j];
+        any_l |= !small[j];
+        r[j] = 0.0;
+    }
+    if (__any_sync(mask, any_s)) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            if (KIND == 0) r[j] = fma(x[j], horner(kPh, t[j]), __dmul_rn(kTwoInvSqrtPi, ix[j]));
+            else if (KIND == 1) r[j] = __dmul_rn(x[j], horner(kPf, t[j]));
+            else r[j] = __dmul_rn(x[j], horner(kPe, t[j]));
+        }
+    }
+    if (__any_sync(mask, any_l)) {
+        const double *mid = tab + (kQDeg + 1) * kQPieces;
+        double E[NJ], u[NJ], q[NJ];
+        int pc[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            E[j] = exp(-t[j]);
+            pc[j] = (x[j] >= kQBreak1) + (x[j] >= kQBreak2) + (x[j] >= kQBreak3);
+            u[j] = __dmul_rn(fmin(x[j], kQBreak4) - mid[pc[j]], mid[kQPieces + pc[j]]);
+            q[j] = tab[kQDeg * kQPieces + pc[j]];
+        }
+#pragma unroll
+        for (int k = kQDeg - 1; k >= 0; --k)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], u[j], tab[k * kQPieces + pc[j]]);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            double lv;
+            if (KIND == 2) {
+                lv = fma(-E[j], q[j], 1.0);
+            } else {
+                const double hx = __dmul_rn(0.5 * ix[j], ix[j]);
+                const double a = KIND == 0 ? 1.0 + hx : 1.0 - hx;
+                lv = fma(E[j], fma(-q[j], a, __dmul_rn(kInvSqrtPi, ix[j])), a);
+            }
+            if (!small[j]) r[j] = lv;
+        }
+    }
+}
+
 }  // namespace special
 }  // namespace hb
