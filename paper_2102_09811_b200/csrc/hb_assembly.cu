@@ -260,42 +260,62 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
             // two quadrature points of the same parity per iteration, evaluated
             // together per gap slot: their x are close, so the small/large-x
             // branch skipping survives, and the two Horner chains interleave
-            const unsigned mask = __activemask();
+            // uniform trip count for both point-parity halves (tail points of
+            // an odd chunk get zero weight), so the branch votes below span the
+            // full warp and compile to uniform branches
+            const int nloc4 = (nloc + 3) & ~3;
             if constexpr (NIJ == 9) {
                 // p1 x p1: nine hat weights per point -- one point per iteration
-                for (int k = s; k < nloc; k += 2) {
-                    const double *p = geo + k * PAY;
+                for (int k = s; k < nloc4; k += 2) {
+                    const bool ok = k < nloc;
+                    const double *p = geo + (ok ? k : 0) * PAY;
                     const double rho = p[0], s1 = p[1];
                     const double s2 = (OP == 2) ? 0.0 : p[2];
 #pragma unroll
                     for (int j = 0; j < NJ; ++j) {
                         const double x = __dmul_rn(rho, T.cx[j]);
                         const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                        const double f = special::eval<OP>(x, ix, tab, mask);
-                        const double v = OP == 1 ? f : __dmul_rn(s1, f);
+                        const double f = special::eval<OP>(x, ix, tab, kFull);
+                        const double v = ok ? (OP == 1 ? f : __dmul_rn(s1, f)) : 0.0;
 #pragma unroll
                         for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, p[HOFF + i], acc[j][i]);
                     }
                 }
-            } else
-            for (int k = s; k < nloc; k += 4) {
-                const bool two = k + 2 < nloc;
-                const double *p0 = geo + k * PAY, *p1 = geo + (two ? k + 2 : k) * PAY;
-                const double rho0 = p0[0], rho1 = p1[0];
-                const double a0 = p0[1], a1 = p1[1];
-                const double b0 = (OP == 2) ? 0.0 : p0[2], b1 = (OP == 2) ? 0.0 : p1[2];
+            } else {
+#ifndef HB_QGROUP
+#define HB_QGROUP 2
+#endif
+                // G points of the same parity per branch region (x close -> the
+                // small/large-x skipping survives; G independent Horner chains)
+                constexpr int G = HB_QGROUP;
+                const int nlocg = (nloc + 2 * G - 1) / (2 * G) * (2 * G);
+                for (int k = s; k < nlocg; k += 2 * G) {
+                    bool ok[G];
+                    const double *pp[G];
+                    double rho[G], a[G], b[G];
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    const double xs[2] = {__dmul_rn(rho0, T.cx[j]), __dmul_rn(rho1, T.cx[j])};
-                    const double ixs[2] = {__dmul_rn(OP == 0 ? b0 : a0, T.ic[j]), __dmul_rn(OP == 0 ? b1 : a1, T.ic[j])};
-                    double fs[2];
-                    special::eval_n<OP, 2>(xs, ixs, fs, tab, mask);
-                    const double v0 = OP == 1 ? fs[0] : __dmul_rn(a0, fs[0]);
-                    const double v1 = OP == 1 ? fs[1] : __dmul_rn(a1, fs[1]);
+                    for (int g = 0; g < G; ++g) {
+                        ok[g] = k + 2 * g < nloc;
+                        pp[g] = geo + (ok[g] ? k + 2 * g : 0) * PAY;
+                        rho[g] = pp[g][0];
+                        a[g] = pp[g][1];
+                        b[g] = (OP == 2) ? 0.0 : pp[g][2];
+                    }
 #pragma unroll
-                    for (int i = 0; i < NIJ; ++i) {
-                        acc[j][i] = fma(v0, p0[HOFF + i], acc[j][i]);
-                        if (two) acc[j][i] = fma(v1, p1[HOFF + i], acc[j][i]);
+                    for (int j = 0; j < NJ; ++j) {
+                        double xs[G], ixs[G], fs[G];
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            xs[g] = __dmul_rn(rho[g], T.cx[j]);
+                            ixs[g] = __dmul_rn(OP == 0 ? b[g] : a[g], T.ic[j]);
+                        }
+                        special::eval_n<OP, G>(xs, ixs, fs, tab, kFull);
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            const double v = ok[g] ? (OP == 1 ? fs[g] : __dmul_rn(a[g], fs[g])) : 0.0;
+#pragma unroll
+                            for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, pp[g][HOFF + i], acc[j][i]);
+                        }
                     }
                 }
             }
