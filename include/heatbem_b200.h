@@ -124,10 +124,12 @@ int hb_pair_classes(const hb_mesh_desc *mesh, int64_t e0, int64_t e1, int8_t *ou
 
 /* D = D2 + alpha^2 sum_o T_o^T V T_o per block (curl of the hat functions,
  * heatbem/assembly.py:289-334).  V: (nb, E_x, E_x), D2 and D: (nb, N_x, N_x);
- * D may alias D2.  curls_dev: (E_x, 3, 3) surface curls per local hat. */
+ * D may alias D2.  curls_dev: (E_x, 3, 3) surface curls per local hat.
+ * workspace: >= hb_curl_workspace(mesh, 1) bytes (more = more blocks per pass). */
+size_t hb_curl_workspace(const hb_mesh_desc *mesh, int64_t blocks_per_pass);
 int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha,
                     const double *curls_dev, const double *V_dev, const double *D2_dev,
-                    double *D_dev, void *stream);
+                    double *D_dev, void *workspace_dev, size_t workspace_bytes, void *stream);
 
 /* Interior potential, heatbem/_field_numba.py:15-79 (kind 0: single layer,
  * kind 1: double layer).  Evaluation outputs are grouped by spatial point and

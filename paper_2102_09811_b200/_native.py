@@ -66,7 +66,7 @@ EXPORTED = (
     "hb_version", "hb_last_error", "hb_assemble", "hb_assemble_min_workspace",
     "hb_assemble_full_workspace", "hb_curl_combine", "hb_potential",
     "hb_toeplitz_apply", "hb_forward_subst_step", "hb_fp64_probe", "hb_pair_classes",
-    "hb_toeplitz_apply_range",
+    "hb_toeplitz_apply_range", "hb_curl_workspace",
 )
 
 _lib = None
@@ -89,7 +89,9 @@ def load():
     for fn in ("hb_assemble_min_workspace", "hb_assemble_full_workspace"):
         getattr(L, fn).argtypes = [ctypes.POINTER(MeshDesc), ctypes.POINTER(AssemblyDesc)]
         getattr(L, fn).restype = ctypes.c_size_t
-    L.hb_curl_combine.argtypes = [ctypes.POINTER(MeshDesc), _I64, _D, _P, _P, _P, _P, _P]
+    L.hb_curl_combine.argtypes = [ctypes.POINTER(MeshDesc), _I64, _D, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]
+    L.hb_curl_workspace.argtypes = [ctypes.POINTER(MeshDesc), _I64]
+    L.hb_curl_workspace.restype = ctypes.c_size_t
     L.hb_curl_combine.restype = _INT
     L.hb_potential.argtypes = [_INT, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _I64,
                                _P, _P, _P, _P, _P, _D, _D, _D, _D, _P, _P]

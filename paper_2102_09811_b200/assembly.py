@@ -99,6 +99,27 @@ class BlockToeplitzMatrix:
     def block_cols(self) -> int:
         return self.shape[1] if self.transpose_blocks_on_apply else self.shape[2]
 
+    def to_host_async(self, out=None, stream=None):
+        """Start a device->host copy of the blocks into page-locked memory on
+        ``stream`` (a side stream by default) once the work queued so far on
+        the current stream is done; returns (host tensor, event).  Lets the
+        copy of one operator overlap the assembly of the next."""
+        import torch
+
+        dev = self.device_blocks
+        if out is None:
+            out = torch.empty(dev.shape, dtype=dev.dtype, pin_memory=True)
+        s = stream if stream is not None else _copy_stream(dev.device)
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(dev.device))
+        s.wait_event(ready)
+        with torch.cuda.stream(s):
+            out.copy_(dev, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(s)
+        dev.record_stream(s)
+        return out, done
+
     def transposed(self) -> "BlockToeplitzMatrix":
         """Blockwise transpose (K' from K), sharing the block storage."""
         t = BlockToeplitzMatrix.__new__(BlockToeplitzMatrix)
@@ -107,6 +128,18 @@ class BlockToeplitzMatrix:
         t.diagonal_only = self.diagonal_only
         t._share, self._share = self, t
         return t
+
+
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(device):
+    import torch
+
+    key = str(device)
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=device)
+    return _COPY_STREAMS[key]
 
 
 def _is_torch(x) -> bool:
@@ -264,14 +297,25 @@ def hypersingular_from_single_layer(V: BlockToeplitzMatrix, D2: BlockToeplitzMat
         raise ValueError("V and D2 must hold the same number of blocks")
     tabs = device_tables(mesh, config, Vd.device)
     out = D2d if overwrite_d2 else torch.empty_like(D2d)
-    with torch.cuda.device(Vd.device):
-        _native.call("hb_curl_combine", tabs.desc(True), Vd.shape[0], float(params.alpha),
-                     _native.ptr(tabs.t["curls"]), _native.ptr(Vd), _native.ptr(D2d), _native.ptr(out),
-                     _native.stream_handle(stream))
+    curl_combine_into(tabs, Vd, D2d, out, float(params.alpha), stream)
     if overwrite_d2:
         D2._host = None
         return D2
     return BlockToeplitzMatrix(out)
+
+
+def curl_combine_into(tabs, Vd, D2d, out, alpha: float, stream=None, workspace_cap: int = 1 << 30):
+    """hb_curl_combine with a workspace of up to ``workspace_cap`` bytes."""
+    import torch
+
+    L = _native.load()
+    m = tabs.desc(True)
+    per = L.hb_curl_workspace(m, 1)
+    nb = Vd.shape[0]
+    ws = torch.empty(max(per, min(per * nb, workspace_cap)), dtype=torch.uint8, device=Vd.device)
+    with torch.cuda.device(Vd.device):
+        _native.call("hb_curl_combine", m, nb, alpha, _native.ptr(tabs.t["curls"]), _native.ptr(Vd),
+                     _native.ptr(D2d), _native.ptr(out), _native.ptr(ws), ws.numel(), _native.stream_handle(stream))
 
 
 def assemble_hypersingular(mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig(),

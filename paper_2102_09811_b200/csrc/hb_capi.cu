@@ -1,5 +1,6 @@
 // hb_capi.cu -- C-ABI glue: error state, version, FP64 throughput probe,
 // and the curl combination D = D2 + alpha^2 sum_o T_o^T V T_o.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 
@@ -41,35 +42,76 @@ __global__ void __launch_bounds__(256) k_fp64_probe(int64_t iters, double *sink)
     if (s == 12345.678) sink[blockIdx.x] = s;   // never true; keeps the chains live
 }
 
-// D[d][m][n] = D2[d][m][n] + a2 * sum_{(e,i) in star(m)} sum_{(f,j) in star(n)}
-//              (curl_{e,i} . curl_{f,j}) V[d][e][f], computed for n >= m and mirrored
-__global__ void __launch_bounds__(256) k_curl_combine(hb_mesh_desc M, double a2, const double *curls,
-                                                      const double *V, const double *D2, double *D)
+// D = D2 + a2 * sum_{(e,i) in star(m)} sum_{(f,j) in star(n)} (curl_ei . curl_fj) V[e][f]
+// in two stages per block d:
+//   W[e][o][n] = sum_{(f,j) in star(n)} curl_fj[o] V[e][f]    (row e of V staged in smem)
+//   D[m][n]    = D2[m][n] + a2 sum_{(e,i) in star(m)} sum_o curl_ei[o] W[e][o][n]
+// the second stage runs on 32x32 tile pairs (ti <= tj), computes n >= m and
+// writes the mirror through shared memory (exact symmetry, coalesced).
+__global__ void __launch_bounds__(256) k_curl_w(hb_mesh_desc M, const double *curls, const double *V, double *W,
+                                                int64_t d0)
 {
-    const int64_t m = blockIdx.x, d = blockIdx.y;
+    extern __shared__ double vrow[];
+    const int64_t e = blockIdx.x, d = d0 + blockIdx.y;
+    const int64_t E = M.E_x, N = M.N_x;
+    const double *Ve = V + (d * E + e) * E;
+    for (int64_t f = threadIdx.x; f < E; f += blockDim.x) vrow[f] = Ve[f];
+    __syncthreads();
+    double *We = W + ((int64_t)blockIdx.y * E + e) * 3 * N;
+    for (int64_t n = threadIdx.x; n < N; n += blockDim.x) {
+        const int64_t s0 = __ldg(M.star_indptr_dev + n), s1 = __ldg(M.star_indptr_dev + n + 1);
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+        for (int64_t s = s0; s < s1; ++s) {
+            const int64_t f = __ldg(M.star_elem_dev + s), j = __ldg(M.star_local_dev + s);
+            const double v = vrow[f];
+            w0 = fma(__ldg(curls + 9 * f + 3 * j), v, w0);
+            w1 = fma(__ldg(curls + 9 * f + 3 * j + 1), v, w1);
+            w2 = fma(__ldg(curls + 9 * f + 3 * j + 2), v, w2);
+        }
+        We[n] = w0;
+        We[N + n] = w1;
+        We[2 * N + n] = w2;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_curl_d(hb_mesh_desc M, double a2, const double *curls, const double *W,
+                                                const double *D2, double *D, int64_t d0)
+{
+    __shared__ double tile[32][33];
     const int64_t N = M.N_x, E = M.E_x;
-    const double *Vd = V + d * E * E;
+    const int64_t nt = cdiv(N, 32);
+    int64_t ti = 0, rem = blockIdx.x;
+    while (rem >= nt - ti) { rem -= nt - ti; ++ti; }
+    const int64_t tj = ti + rem;
+    const int64_t d = d0 + blockIdx.y;
+    const double *Wd = W + (int64_t)blockIdx.y * E * 3 * N;
     const double *D2d = D2 + d * N * N;
     double *Dd = D + d * N * N;
-    const int64_t sm0 = __ldg(M.star_indptr_dev + m), sm1 = __ldg(M.star_indptr_dev + m + 1);
-    for (int64_t n = m + threadIdx.x; n < N; n += blockDim.x) {
-        const int64_t sn0 = __ldg(M.star_indptr_dev + n), sn1 = __ldg(M.star_indptr_dev + n + 1);
-        double acc = 0.0;
-        for (int64_t a = sm0; a < sm1; ++a) {
-            const int64_t e = __ldg(M.star_elem_dev + a), i = __ldg(M.star_local_dev + a);
-            const double c0 = __ldg(curls + 9 * e + 3 * i), c1 = __ldg(curls + 9 * e + 3 * i + 1),
-                         c2 = __ldg(curls + 9 * e + 3 * i + 2);
-            const double *Ve = Vd + e * E;
-            for (int64_t b = sn0; b < sn1; ++b) {
-                const int64_t f = __ldg(M.star_elem_dev + b), j = __ldg(M.star_local_dev + b);
-                const double dot = c0 * __ldg(curls + 9 * f + 3 * j) + c1 * __ldg(curls + 9 * f + 3 * j + 1) +
-                                   c2 * __ldg(curls + 9 * f + 3 * j + 2);
-                acc = fma(dot, __ldg(Ve + f), acc);
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t n = tj * 32 + tx;
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t m = ti * 32 + r;
+        double val = 0.0;
+        if (m < N && n < N && n >= m) {
+            const int64_t s0 = __ldg(M.star_indptr_dev + m), s1 = __ldg(M.star_indptr_dev + m + 1);
+            double acc = 0.0;
+            for (int64_t s = s0; s < s1; ++s) {
+                const int64_t e = __ldg(M.star_elem_dev + s), i = __ldg(M.star_local_dev + s);
+                const double *We = Wd + e * 3 * N;
+                acc = fma(__ldg(curls + 9 * e + 3 * i), We[n], acc);
+                acc = fma(__ldg(curls + 9 * e + 3 * i + 1), We[N + n], acc);
+                acc = fma(__ldg(curls + 9 * e + 3 * i + 2), We[2 * N + n], acc);
             }
+            val = D2d[m * N + n] + a2 * acc;
+            Dd[m * N + n] = val;
         }
-        const double val = D2d[m * N + n] + a2 * acc;
-        Dd[m * N + n] = val;
-        Dd[n * N + m] = val;
+        tile[r][tx] = val;
+    }
+    __syncthreads();
+    // mirror: D[n][m] = D[m][n] for n > m (rows of the tj tile, columns of ti)
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t nn = tj * 32 + r, mm = ti * 32 + tx;
+        if (nn < N && mm < N && nn > mm) Dd[nn * N + mm] = tile[tx][r];
     }
 }
 
@@ -88,14 +130,39 @@ extern "C" int hb_fp64_probe(int64_t grid, int64_t iters, double *sink_dev, void
     return cuda_check(cudaGetLastError(), "hb_fp64_probe");
 }
 
+extern "C" size_t hb_curl_workspace(const hb_mesh_desc *mesh, int64_t blocks_per_pass)
+{
+    if (!mesh || blocks_per_pass < 1) return 0;
+    return (size_t)blocks_per_pass * mesh->E_x * 3 * mesh->N_x * sizeof(double);
+}
+
 extern "C" int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha, const double *curls_dev,
-                               const double *V_dev, const double *D2_dev, double *D_dev, void *stream)
+                               const double *V_dev, const double *D2_dev, double *D_dev, void *workspace_dev,
+                               size_t workspace_bytes, void *stream)
 {
     if (!mesh || n_blocks < 1 || !curls_dev || !V_dev || !D2_dev || !D_dev) {
         set_error("hb_curl_combine: bad arguments");
         return HB_ERR_INVALID;
     }
-    dim3 g((unsigned)mesh->N_x, (unsigned)n_blocks);
-    k_curl_combine<<<g, 256, 0, (cudaStream_t)stream>>>(*mesh, alpha * alpha, curls_dev, V_dev, D2_dev, D_dev);
-    return cuda_check(cudaGetLastError(), "hb_curl_combine");
+    const size_t per = hb_curl_workspace(mesh, 1);
+    if (!workspace_dev || workspace_bytes < per) {
+        set_error("hb_curl_combine: workspace %zu bytes < one block (%zu)", workspace_bytes, per);
+        return HB_ERR_WORKSPACE;
+    }
+    const int64_t bpp = std::min<int64_t>(n_blocks, (int64_t)(workspace_bytes / per));
+    const size_t smem = (size_t)mesh->E_x * sizeof(double);
+    if (smem > 227 * 1024) { set_error("hb_curl_combine: E_x too large for the row stage"); return HB_ERR_UNSUPPORTED; }
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_curl_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nt = cdiv(mesh->N_x, 32);
+    for (int64_t d0 = 0; d0 < n_blocks; d0 += bpp) {
+        const int64_t nb = std::min(bpp, n_blocks - d0);
+        k_curl_w<<<dim3((unsigned)mesh->E_x, (unsigned)nb), 256, smem, st>>>(*mesh, curls_dev, V_dev,
+                                                                          (double *)workspace_dev, d0);
+        k_curl_d<<<dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)nb), 256, 0, st>>>(
+            *mesh, alpha * alpha, curls_dev, (const double *)workspace_dev, D2_dev, D_dev, d0);
+        int rc = cuda_check(cudaGetLastError(), "hb_curl_combine");
+        if (rc) return rc;
+    }
+    return HB_OK;
 }
