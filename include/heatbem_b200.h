@@ -138,12 +138,13 @@ int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha,
  * current-interval flag cur[o] (eps > 0 and k < E_t) and is written to
  * out[out_idx[o]].  The kernel values of a group are evaluated once per
  * (element, node, gap) and shared by all its output times.
- * dens_dev: (E_t, E_x, nq) density at the spatial quadrature nodes;
+ * dens_t_dev: (E_x, nq, E_t) density at the spatial quadrature nodes, time
+ * fastest (the reference's (E_t, E_x, nq) array transposed);
  * qpts_dev: (E_x, nq, 3); qw_dev (nq,); kmax = max k over all outputs. */
 int hb_potential(int kind, int64_t n_groups, int64_t E_t, int64_t E_x, int64_t nq,
                  const double *gx_dev, const double *geps_dev, const int64_t *gptr_dev,
                  const int64_t *k_dev, const uint8_t *cur_dev, const int64_t *out_idx_dev, int64_t kmax,
-                 const double *dens_dev, const double *qpts_dev, const double *qw_dev,
+                 const double *dens_t_dev, const double *qpts_dev, const double *qw_dev,
                  const double *areas_dev, const double *normals_dev,
                  double step, double alpha, double d_eps, double r_eps, double *out_dev, void *stream);
 

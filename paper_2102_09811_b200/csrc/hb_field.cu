@@ -6,37 +6,29 @@
 //     s = sum_{m=0..k} c_m G(rho, m h + eps)      (+ dens[k] G(rho, 0) if cur)
 //     c_m = dens[k-1-m] - dens[k-m] * [k-m < k or cur]
 // and recomputes every G for every output time.  The G values depend on
-// (x, eps, m) only, so points that share (x, eps) -- e.g. one spatial point
-// at all time-step ends -- share them: one warp owns such a group, its lanes
-// first evaluate G(m), m = 0..kmax, once per (e, q) into shared memory, then
-// each lane contracts them with its own output time's density differences.
-// The reference's evaluation order of the sums (m innermost, then q, then e)
-// is kept, and c_m is formed exactly as the reference forms it.
+// (x, eps, m) only, so outputs that share (x, eps) -- one spatial point at
+// all time-step ends -- share them: one CTA owns such a group; its warps split
+// the elements, the lanes of a warp first evaluate G(m), m = 0..kmax, once
+// per (e, q) into shared memory, then each lane contracts them with the
+// density differences of its two output times (one merged loop, so lanes
+// with short and long histories stay in step).  Per-warp partial sums are
+// added in fixed warp order: results are deterministic.
+//
+// Kernels (x = rho / (2 sqrt(a gap)), gap = m h + eps):
+//   single layer: G^{dtau}         = erf(x) / (4 pi a rho)
+//   double layer: a dG^{dtau}/dn_y = rn / (4 pi rho^3) * E(x),
+//                 E(x) = erf(x) - 2x e^{-x^2}/sqrt(pi)
+// erf and E come from the fused evaluator (hb_special.cuh); E is evaluated
+// without the small-x cancellation of the reference's
+// erf(x)/rho - e^{-x^2}/sqrt(pi a gap) form.  The reference's branches are
+// kept: gap <= d_eps (first for the single layer), rho <= r_eps.
+// The sums keep the reference's order (m, then q, then e within a warp).
 #include <algorithm>
 
 #include "hb_common.cuh"
+#include "hb_special.cuh"
 
 namespace hb {
-
-// heatbem/_assembly_numba.py:25-32 (delta branch first, then rho branch)
-__device__ __forceinline__ double dev_g_dtau(double rho, double delta, double a, double deps, double reps)
-{
-    if (delta <= deps) return 1.0 / (4.0 * kPi * a * rho);
-    if (rho <= reps) return 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (a * a * a) * delta));
-    const double x = rho / (2.0 * sqrt(a * delta));
-    return erf(x) / (4.0 * kPi * a * rho);
-}
-
-// heatbem/_assembly_numba.py:48-59 (rho branch first)
-__device__ __forceinline__ double dev_dn_g_dtau(double rn, double rho, double delta, double a, double deps,
-                                                double reps)
-{
-    if (rho <= reps) return 0.0;
-    if (delta <= deps) return rn / (4.0 * kPi * (rho * rho * rho));
-    const double x = rho / (2.0 * sqrt(a * delta));
-    const double inner = erf(x) / rho - exp(-x * x) / sqrt(kPi * a * delta);
-    return (rn / (rho * rho)) * inner / (4.0 * kPi);
-}
 
 struct PotArgs {
     int kind;
@@ -44,88 +36,131 @@ struct PotArgs {
     const double *gx;          // (n_groups, 3)
     const double *geps;        // (n_groups,)
     const int64_t *gptr;       // (n_groups+1,) outputs of each group
-    const int64_t *k;          // (n_out,) completed intervals per output
+    const int64_t *k;          // (n_out,) completed intervals per output (ascending in a group)
     const uint8_t *cur;        // (n_out,)
     const int64_t *out_idx;    // (n_out,) position in the caller's point list
-    const double *dens, *qpts, *qw, *areas, *normals;
+    const double *dens_t;      // (E_x, nq, E_t) density, time fastest
+    const double *qpts, *qw, *areas, *normals;
     double step, alpha, d_eps, r_eps;
     double *out;
-    int kcap;                  // smem capacity of the G / density arrays
+    int kcap;                  // per-warp smem capacity of the G / A / B / C arrays
 };
 
-constexpr int kPotWarps = 4;
-constexpr int kOutPerLane = 2;
+constexpr int kPotWarps = 8;
+constexpr int kOut = 64;       // outputs per pass (2 per lane)
 
+template <int KIND>
 __global__ void __launch_bounds__(kPotWarps * 32) k_potential(const PotArgs P)
 {
     extern __shared__ __align__(16) double psm[];
+    double *tab = psm;
+    special::load_table(tab);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double *Gs = psm + warp * 3 * P.kcap;      // G(m), m = 0..kmax
-    double *Ds = Gs + P.kcap;                  // dens[j], j = 0..kmax (j < E_t)
-    double *G0 = Ds + P.kcap;                  // G(rho, 0) for the current-interval term
-    for (int64_t g = (int64_t)blockIdx.x * kPotWarps + warp; g < P.n_groups; g += (int64_t)gridDim.x * kPotWarps) {
-        const double px = P.gx[3 * g], py = P.gx[3 * g + 1], pz = P.gx[3 * g + 2];
-        const double eps = P.geps[g];
-        const int64_t o0 = P.gptr[g], o1 = P.gptr[g + 1];
-        for (int64_t ob = o0; ob < o1; ob += 32 * kOutPerLane) {
-            // this lane's outputs: ob + lane and ob + 63 - lane (pairs a short
-            // history with a long one when the caller sorted k ascending)
-            int64_t oi[kOutPerLane];
-            int kk[kOutPerLane];
-            bool cu[kOutPerLane], ok[kOutPerLane];
-            int kmax = 0;
-            for (int r = 0; r < kOutPerLane; ++r) {
-                oi[r] = ob + (r == 0 ? lane : 32 * kOutPerLane - 1 - lane);
-                ok[r] = oi[r] < o1;
-                kk[r] = ok[r] ? (int)P.k[oi[r]] : 0;
-                cu[r] = ok[r] ? P.cur[oi[r]] != 0 : false;
-                kmax = max(kmax, kk[r]);
-            }
+    double *red = psm + special::kTabDoubles;                  // [kPotWarps][kOut]
+    double *G = red + kPotWarps * kOut + warp * 4 * P.kcap;    // G(m)
+    double *A = G + P.kcap;                                    // dens[j], 0 outside [0, E_t)
+    double *B = A + P.kcap;                                    // A[j-1] - A[j]
+    double *C = B + P.kcap;                                    // 1 / (2 sqrt(a gap_m))
+    __syncthreads();
+    const double inv4pi = 0.25 * kInvPi;
+    for (int64_t grp = blockIdx.x; grp < P.n_groups; grp += gridDim.x) {
+        const double px = P.gx[3 * grp], py = P.gx[3 * grp + 1], pz = P.gx[3 * grp + 2];
+        const double eps = P.geps[grp];
+        const int64_t o0 = P.gptr[grp], o1 = P.gptr[grp + 1];
+        for (int64_t ob = o0; ob < o1; ob += kOut) {
+            const int64_t oi1 = ob + lane, oi2 = ob + kOut - 1 - lane;
+            const bool ok1 = oi1 < o1, ok2 = oi2 < o1;
+            const int k1 = ok1 ? (int)P.k[oi1] : 0, k2 = ok2 ? (int)P.k[oi2] : 0;
+            const bool cu1 = ok1 && P.cur[oi1] != 0, cu2 = ok2 && P.cur[oi2] != 0;
+            int kmax = max(k1, k2);
             for (int o = 16; o >= 1; o >>= 1) kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
-            double acc[kOutPerLane];
-            for (int r = 0; r < kOutPerLane; ++r) acc[r] = 0.0;
-            for (int64_t e = 0; e < P.E_x; ++e) {
+            const int rounds = kmax / 32 + 1;
+            for (int m = lane; m <= kmax; m += 32) C[m] = 1.0 / (2.0 * sqrt(P.alpha * ((double)m * P.step + eps)));
+            __syncwarp();
+            double acc1 = 0.0, acc2 = 0.0;
+            for (int64_t e = warp; e < P.E_x; e += kPotWarps) {
                 const double nyx = __ldg(P.normals + 3 * e), nyy = __ldg(P.normals + 3 * e + 1),
                              nyz = __ldg(P.normals + 3 * e + 2);
-                double el[kOutPerLane];
-                for (int r = 0; r < kOutPerLane; ++r) el[r] = 0.0;
+                double el1 = 0.0, el2 = 0.0;
                 for (int64_t q = 0; q < P.nq; ++q) {
                     const double *y = P.qpts + 3 * (e * P.nq + q);
                     const double rx = px - __ldg(y), ry = py - __ldg(y + 1), rz = pz - __ldg(y + 2);
                     const double rho = sqrt(rx * rx + ry * ry + rz * rz);
                     const double rn = rx * nyx + ry * nyy + rz * nyz;
-                    for (int m = lane; m <= kmax; m += 32) {
-                        const double gap = (double)m * P.step + eps;
-                        Gs[m] = P.kind == 0 ? dev_g_dtau(rho, gap, P.alpha, P.d_eps, P.r_eps)
-                                            : dev_dn_g_dtau(rn, rho, gap, P.alpha, P.d_eps, P.r_eps);
-                        Ds[m] = m < P.E_t ? __ldg(P.dens + ((int64_t)m * P.E_x + e) * P.nq + q) : 0.0;
-                    }
-                    if (lane == 0)
-                        G0[0] = P.kind == 0 ? dev_g_dtau(rho, 0.0, P.alpha, P.d_eps, P.r_eps)
-                                            : dev_dn_g_dtau(rn, rho, 0.0, P.alpha, P.d_eps, P.r_eps);
-                    __syncwarp();
-                    const double w = __ldg(P.qw + q);
-                    for (int r = 0; r < kOutPerLane; ++r) {
-                        if (!ok[r]) continue;
-                        const int k = kk[r];
-                        double s = 0.0;
-                        for (int m = 0; m <= k; ++m) {
-                            const int hi = k - 1 - m, lo = k - m;
-                            double c = (hi >= 0 && hi < P.E_t) ? Ds[hi] : 0.0;
-                            if (lo >= 0 && lo < P.E_t && (lo < k || cu[r])) c -= Ds[lo];
-                            if (c == 0.0) continue;
-                            s = fma(c, Gs[m], s);
+                    const bool rsmall = rho <= P.r_eps;
+                    const double lim0 = KIND == 0 ? 1.0 / (4.0 * kPi * P.alpha * rho) : (rsmall ? 0.0 : inv4pi * rn / (rho * rho * rho));
+                    const double *dq = P.dens_t + (e * P.nq + q) * P.E_t;
+                    for (int r = 0; r < rounds; ++r) {
+                        const int m = lane + 32 * r;
+                        const int mc = m <= kmax ? m : kmax;
+                        const double gap = (double)mc * P.step + eps;
+                        const double x = __dmul_rn(rho, C[mc]);
+                        const double f = special::eval<KIND == 0 ? 2 : 3>(x, 0.0, tab, kFull);
+                        double g;
+                        if (gap <= P.d_eps) g = lim0;
+                        else if (rsmall) g = KIND == 0 ? 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (P.alpha * P.alpha * P.alpha) * gap)) : 0.0;
+                        else g = __dmul_rn(lim0, f);
+                        const double a = m < P.E_t ? __ldg(dq + m) : 0.0;
+                        const double am = (m >= 1 && m - 1 < P.E_t) ? __ldg(dq + m - 1) : 0.0;
+                        if (m <= kmax) {
+                            G[m] = g;
+                            A[m] = a;
+                            B[m] = am - a;
                         }
-                        if (cu[r] && k >= 0 && k < P.E_t) s = fma(Ds[k], G0[0], s);
-                        el[r] = fma(w, s, el[r]);
                     }
+                    __syncwarp();
+                    // m = 0: c = dens[k-1] - dens[k] [cur];  m >= 1: c = B[k - m]
+                    const double c1 = (k1 >= 1 ? A[k1 - 1] : 0.0) - (cu1 ? A[k1] : 0.0);
+                    const double c2 = (k2 >= 1 ? A[k2 - 1] : 0.0) - (cu2 ? A[k2] : 0.0);
+                    // two independent accumulation chains per output (even / odd m)
+                    const int n1 = ok1 ? k1 : 0, n2 = ok2 ? k2 : 0;
+                    double s1 = fma(c1, G[0], 0.0), s2 = fma(c2, G[0], 0.0), s1b = 0.0, s2b = 0.0;
+                    {
+                        const double *b = B + k1;
+                        int m = 1;
+                        for (; m + 1 <= n1; m += 2) {
+                            s1b = fma(b[-m], G[m], s1b);
+                            s1 = fma(b[-m - 1], G[m + 1], s1);
+                        }
+                        if (m <= n1) s1b = fma(b[-m], G[m], s1b);
+                    }
+                    {
+                        const double *b = B + k2;
+                        int m = 1;
+                        for (; m + 1 <= n2; m += 2) {
+                            s2b = fma(b[-m], G[m], s2b);
+                            s2 = fma(b[-m - 1], G[m + 1], s2);
+                        }
+                        if (m <= n2) s2b = fma(b[-m], G[m], s2b);
+                    }
+                    s1 += s1b;
+                    s2 += s2b;
+                    if (cu1 && k1 < P.E_t) s1 = fma(A[k1], lim0, s1);
+                    if (cu2 && k2 < P.E_t) s2 = fma(A[k2], lim0, s2);
+                    const double w = __ldg(P.qw + q);
+                    el1 = fma(w, s1, el1);
+                    el2 = fma(w, s2, el2);
                     __syncwarp();
                 }
                 const double a2 = 2.0 * __ldg(P.areas + e);
-                for (int r = 0; r < kOutPerLane; ++r) acc[r] = fma(a2, el[r], acc[r]);
+                acc1 = fma(a2, el1, acc1);
+                acc2 = fma(a2, el2, acc2);
             }
-            for (int r = 0; r < kOutPerLane; ++r)
-                if (ok[r]) P.out[P.out_idx[oi[r]]] = acc[r];
+            red[warp * kOut + lane] = acc1;
+            red[warp * kOut + kOut - 1 - lane] = acc2;
+            __syncthreads();
+            if (warp == 0) {
+                for (int h = 0; h < 2; ++h) {
+                    const int o = h == 0 ? lane : kOut - 1 - lane;
+                    const int64_t oi = ob + o;
+                    if (oi < o1) {
+                        double v = 0.0;
+                        for (int w = 0; w < kPotWarps; ++w) v += red[w * kOut + o];
+                        P.out[P.out_idx[oi]] = v;
+                    }
+                }
+            }
+            __syncthreads();
         }
     }
 }
@@ -136,12 +171,12 @@ using namespace hb;
 
 // Outputs sharing (x, eps) form one group (gptr); k ascending within a group.
 extern "C" int hb_potential(int kind, int64_t n_groups, int64_t E_t, int64_t E_x, int64_t nq,
-                                    const double *gx_dev, const double *geps_dev, const int64_t *gptr_dev,
-                                    const int64_t *k_dev, const uint8_t *cur_dev, const int64_t *out_idx_dev,
-                                    int64_t kmax, const double *dens_dev, const double *qpts_dev,
-                                    const double *qw_dev, const double *areas_dev, const double *normals_dev,
-                                    double step, double alpha, double d_eps, double r_eps, double *out_dev,
-                                    void *stream)
+                            const double *gx_dev, const double *geps_dev, const int64_t *gptr_dev,
+                            const int64_t *k_dev, const uint8_t *cur_dev, const int64_t *out_idx_dev,
+                            int64_t kmax, const double *dens_t_dev, const double *qpts_dev,
+                            const double *qw_dev, const double *areas_dev, const double *normals_dev,
+                            double step, double alpha, double d_eps, double r_eps, double *out_dev,
+                            void *stream)
 {
     if (kind < 0 || kind > 1 || n_groups < 0 || E_t < 1 || E_x < 1 || nq < 1 || kmax < 0 || !out_dev) {
         set_error("hb_potential: bad arguments");
@@ -151,17 +186,18 @@ extern "C" int hb_potential(int kind, int64_t n_groups, int64_t E_t, int64_t E_x
     PotArgs P{};
     P.kind = kind; P.n_groups = n_groups; P.E_t = E_t; P.E_x = E_x; P.nq = nq;
     P.gx = gx_dev; P.geps = geps_dev; P.gptr = gptr_dev; P.k = k_dev; P.cur = cur_dev; P.out_idx = out_idx_dev;
-    P.dens = dens_dev; P.qpts = qpts_dev; P.qw = qw_dev; P.areas = areas_dev; P.normals = normals_dev;
+    P.dens_t = dens_t_dev; P.qpts = qpts_dev; P.qw = qw_dev; P.areas = areas_dev; P.normals = normals_dev;
     P.step = step; P.alpha = alpha; P.d_eps = d_eps; P.r_eps = r_eps; P.out = out_dev;
-    P.kcap = (int)std::max<int64_t>(kmax + 1, E_t + 1);
-    const size_t sm = (size_t)kPotWarps * 3 * P.kcap * sizeof(double);
-    if (sm > 200 * 1024) { set_error("hb_potential: time history too long (%lld)", (long long)kmax); return HB_ERR_INVALID; }
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_potential, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    int dev = 0, nsm = 0;
+    P.kcap = (int)((kmax / 32 + 1) * 32);
+    const size_t sm = (special::kTabDoubles + (size_t)kPotWarps * kOut + (size_t)kPotWarps * 4 * P.kcap) * sizeof(double);
+    if (sm > 220 * 1024) { set_error("hb_potential: time history too long (%lld)", (long long)kmax); return HB_ERR_INVALID; }
+    auto kern = kind == 0 ? k_potential<0> : k_potential<1>;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t grid = std::min<int64_t>(cdiv(n_groups, kPotWarps), (int64_t)nsm * 16);
-    k_potential<<<(unsigned)grid, kPotWarps * 32, sm, (cudaStream_t)stream>>>(P);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPotWarps * 32, sm);
+    const int64_t grid = std::min<int64_t>(n_groups, (int64_t)std::max(1, per_sm) * nsm * 4);
+    kern<<<(unsigned)grid, kPotWarps * 32, sm, (cudaStream_t)stream>>>(P);
     return cuda_check(cudaGetLastError(), "hb_potential");
 }
-

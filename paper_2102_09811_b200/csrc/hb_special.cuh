@@ -46,7 +46,8 @@ __device__ __forceinline__ double horner(const double (&c)[N], double t)   // c:
     return p;
 }
 
-// KIND 0: H (single layer), 1: F (double layer), 2: erf (hypersingular D2).
+// KIND 0: H (single layer), 1: F (double layer), 2: erf (hypersingular D2),
+// 3: E(x) = erf(x) - 2x e^{-x^2}/sqrt(pi) (double-layer potential, = x^3 Pg(t)).
 // ix = 1/x (formed by the caller from precomputed 1/rho and 1/c); `mask` =
 // the lanes executing this call.
 template <int KIND>
@@ -58,7 +59,8 @@ __device__ __forceinline__ double eval(double x, double ix, const double *__rest
     if (__any_sync(mask, small)) {
         if (KIND == 0) r = fma(x, horner(kPh, t), __dmul_rn(kTwoInvSqrtPi, ix));
         else if (KIND == 1) r = __dmul_rn(x, horner(kPf, t));
-        else r = __dmul_rn(x, horner(kPe, t));
+        else if (KIND == 2) r = __dmul_rn(x, horner(kPe, t));
+        else r = __dmul_rn(__dmul_rn(x, t), horner(kPg, t));
     }
     if (__any_sync(mask, !small)) {
         const double E = exp(-t);
@@ -72,6 +74,8 @@ __device__ __forceinline__ double eval(double x, double ix, const double *__rest
         double lv;
         if (KIND == 2) {
             lv = fma(-E, q, 1.0);
+        } else if (KIND == 3) {
+            lv = fma(-E, fma(kTwoInvSqrtPi, x, q), 1.0);
         } else {
             const double hx = __dmul_rn(0.5 * ix, ix);
             const double a = KIND == 0 ? 1.0 + hx : 1.0 - hx;

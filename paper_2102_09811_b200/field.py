@@ -204,7 +204,7 @@ def _eval_grouped(kind, coeffs, xs, k, eps, cur, mesh, timegrid, params, config,
     _native.require_cuda()
     T = _tables(mesh, config, torch.device("cuda", torch.cuda.current_device()))
     dev = T.qw.device
-    dens = _density(coeffs, mesh, T)
+    dens = _density(coeffs, mesh, T).permute(1, 2, 0).contiguous()   # (E_x, nq, E_t): time fastest
     n = xs.shape[0]
     out = torch.empty(n, dtype=torch.float64, device=dev)
     if n == 0:
