@@ -44,6 +44,12 @@
 #ifndef HB_PAIR_MINB
 #define HB_PAIR_MINB 2
 #endif
+#ifndef HB_SEP
+#define HB_SEP 0     // separable p1 x p1 accumulation (slower at 128 registers; kept for study)
+#endif
+#ifndef HB_P1P1_MINB
+#define HB_P1P1_MINB HB_PAIR_MINB
+#endif
 #ifndef HB_FUSED
 #define HB_FUSED 1   // fused special-function evaluation (hb_special.cuh); 0 = CUDA erf/exp path
 #endif
@@ -104,6 +110,7 @@ struct Slots {
 // quadrature point generators
 // ---------------------------------------------------------------------------
 struct RegularGeom {
+    static constexpr bool kSeparable = true;   // point q = (p, r): weights and hats factor
     const double *xp, *yp, *w, *hats;
     int nq1;
     __device__ void point(int q, double x[3], double y[3], double &wq, double ht[3], double hs[3]) const
@@ -121,6 +128,7 @@ struct RegularGeom {
 };
 
 struct DuffyGeom {
+    static constexpr bool kSeparable = false;
     double a0[3], da1[3], da2[3], b0[3], db1[3], db2[3];
     const double *ts, *ss, *ws;
     int off;
@@ -182,7 +190,27 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
     constexpr int SLOTS = LsLayout<NIJ, NJ>::SLOTS;
     const int s = lane >> 4, t = lane & 15;
 
+    // p1 x p1 product rules factor: sum_q v w_p w_r ht_i(p) hs_j(r) =
+    // sum_p (w_p ht_i(p)) [sum_r v (w_r hs_j(r))] -- 3 FMA per evaluation
+    // instead of 9, the row sums flushed when the test point p changes
+    constexpr bool SEP = (NIJ == 9) && Geom::kSeparable && HB_FUSED && HB_SEP;
     double acc[NJ][NIJ];
+    double inner[NJ][3], arow[3] = {0.0, 0.0, 0.0};
+    int prow = -1;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+        for (int c = 0; c < 3; ++c) inner[j][c] = 0.0;
+    auto flush = [&]() {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[j][3 * i + c] = fma(arow[i], inner[j][c], acc[j][3 * i + c]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) inner[j][c] = 0.0;
+        }
+    };
     double s0[NIJ], sc[NIJ];
 #pragma unroll
     for (int i = 0; i < NIJ; ++i) {
@@ -209,13 +237,24 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                     H[i * NS + j] = (TP1 || SP1) ? wq * ((TP1 ? ht[i] : 1.0) * (SP1 ? hs[j] : 1.0)) : wq;
             double *p = geo + lane * PAY;
             p[0] = rho;
+            if constexpr (SEP) {   // [HOFF..+2] = w_r hs(r), [HOFF+3..+5] = w_p ht(p)
+                const int pr = q / g.nq1, rr = q - pr * g.nq1;
+                const double wp = __ldg(g.w + pr), wr = __ldg(g.w + rr);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    p[HOFF + c] = wr * hs[c];
+                    p[HOFF + 3 + c] = wp * ht[c];
+                }
+            }
             if (OP == 0) {
                 const double iq = 1.0 / rho;
                 const double Aq = rho * A.inv2a2, Bq = A.inva * iq;
                 p[1] = Aq;
                 p[2] = HB_FUSED ? iq : Bq;
+                if constexpr (!SEP) {
 #pragma unroll
-                for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
+                    for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
+                }
                 if (A.need_special) {
                     const double cq = A.step * Bq + Aq;
 #pragma unroll
@@ -244,8 +283,10 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
             } else {
                 const double iq = 1.0 / rho;
                 p[1] = iq;
+                if constexpr (!SEP) {
 #pragma unroll
-                for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
+                    for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
+                }
                 if (A.need_special) {
 #pragma unroll
                     for (int i = 0; i < NIJ; ++i) s0[i] = fma(H[i], iq, s0[i]);
@@ -264,7 +305,30 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
             // an odd chunk get zero weight), so the branch votes below span the
             // full warp and compile to uniform branches
             const int nloc4 = (nloc + 3) & ~3;
-            if constexpr (NIJ == 9) {
+            if constexpr (SEP) {
+                for (int k = s; k < nloc4; k += 2) {
+                    const bool ok = k < nloc;
+                    const double *p = geo + (ok ? k : 0) * PAY;
+                    const int pr = (base + k) / g.nq1;
+                    if (ok && pr != prow) {
+                        if (prow >= 0) flush();
+                        prow = pr;
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) arow[i] = p[HOFF + 3 + i];
+                    }
+                    const double rho = p[0], s1 = p[1];
+                    const double s2 = (OP == 2) ? 0.0 : p[2];
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) {
+                        const double x = __dmul_rn(rho, T.cx[j]);
+                        const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
+                        const double f = special::eval<OP>(x, ix, tab, kFull);
+                        const double v = ok ? (OP == 1 ? f : __dmul_rn(s1, f)) : 0.0;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) inner[j][c] = fma(v, p[HOFF + c], inner[j][c]);
+                    }
+                }
+            } else if constexpr (NIJ == 9) {
                 // p1 x p1: nine hat weights per point -- one point per iteration
                 for (int k = s; k < nloc4; k += 2) {
                     const bool ok = k < nloc;
@@ -337,6 +401,10 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
             }
 #endif
         } else {
+            if constexpr (SEP) {
+                if (prow >= 0) flush();
+                prow = -1;
+            }
             for (int k = s; k < nloc; k += 2) {
                 const double *p = geo + k * PAY;
                 const double rho = p[0], s1 = p[1];
@@ -361,12 +429,23 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                     else if (OP == 1) val = sm ? 0.0 : eval_general<OP>(A, T, j, rho, s1, s2);
                     else val = sm ? T.kk[j] : eval_general<OP>(A, T, j, rho, s1, s2);
 #endif
+                    if constexpr (SEP) {
 #pragma unroll
-                    for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(val, p[HOFF + i], acc[j][i]);
+                        for (int i = 0; i < 3; ++i)
+#pragma unroll
+                            for (int c = 0; c < 3; ++c)
+                                acc[j][3 * i + c] = fma(val, p[HOFF + 3 + i] * p[HOFF + c], acc[j][3 * i + c]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(val, p[HOFF + i], acc[j][i]);
+                    }
                 }
             }
         }
         __syncwarp();
+    }
+    if constexpr (SEP) {
+        if (prow >= 0) flush();
     }
 
     // fold the two point-parity halves (commutative: both halves get equal bits)
@@ -425,13 +504,6 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
         }
     }
     __syncwarp();
-}
-
-template <int NIJ>
-__device__ __forceinline__ void write_zero_pair(const PairArgs &A, int64_t slot, int lane)
-{
-    double *dst = A.Q + slot * (int64_t)(NIJ * A.nd);
-    for (int k = lane; k < NIJ * A.nd; k += 32) dst[k] = 0.0;
 }
 
 __device__ __forceinline__ double exact_dot3(const double *a, const double *b)
@@ -507,7 +579,6 @@ template <int OP, bool TP1, bool SP1, int NJ, bool SYM>
 __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64_t seg, const Slots<OP, NJ> &T,
                                              double *geo, double *Ls, int lane, const double *tab)
 {
-    constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     const hb_mesh_desc &M = A.m;
     int64_t fb = seg * 32;
     const int64_t fe = min(fb + 32, M.E_x);
@@ -523,10 +594,7 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
         if (touching_pos(M, t_lo, t_hi, f) >= 0) continue;
         const int64_t slot = (e - A.e0) * M.E_x + f;
         const double jac = pair_jac<OP>(A, e, f);
-        if (OP == 2 && jac == 0.0) {   // n_x.n_y == 0: every staged value is +0
-            write_zero_pair<NIJ>(A, slot, lane);
-            continue;
-        }
+        if (OP == 2 && jac == 0.0) continue;   // n_x.n_y == 0: no contribution (finalize skips it)
         const bool near = near_test(M, ce, de, f);
         RegularGeom g;
         const int nq1 = near ? (int)M.n_near : (int)M.n_reg;
@@ -550,7 +618,6 @@ template <int OP, bool TP1, bool SP1, int NJ>
 __device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, const Slots<OP, NJ> &T,
                                               double *geo, double *Ls, int lane, const double *tab)
 {
-    constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     const hb_mesh_desc &M = A.m;
     const int64_t tpos = __ldg(M.sing_pos_dev + k);
     const int64_t e = __ldg(M.sing_row_dev + tpos);
@@ -583,10 +650,7 @@ __device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, cons
     g.off = off0;
     const int64_t slot = (e - A.e0) * M.E_x + f;
     const double jac = pair_jac<OP>(A, e, f);
-    if (OP == 2 && jac == 0.0) {
-        write_zero_pair<NIJ>(A, slot, lane);
-        return;
-    }
+    if (OP == 2 && jac == 0.0) return;   // n_x.n_y == 0: no contribution (finalize skips it)
     double ny[3];
     for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * f + c);
     eval_pair<OP, TP1, SP1, NJ>(A, g, off1 - off0, ny, jac, slot, T, geo, Ls, lane, tab);
@@ -601,7 +665,7 @@ __device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, cons
 // imbalance of upper-triangular / near-diagonal tiles.
 // ---------------------------------------------------------------------------
 template <int OP, bool TP1, bool SP1, int NJ, bool SYM>
-__global__ void __launch_bounds__(kWarps * 32, HB_PAIR_MINB) k_pairs(const PairArgs A)
+__global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_PAIR_MINB) k_pairs(const PairArgs A)
 {
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     extern __shared__ __align__(16) double smem[];
@@ -643,6 +707,8 @@ struct FinArgs {
     int64_t E_x, N_x, R, C, e0, e1;
     int d0, nd, d_begin;
     const int64_t *star_indptr, *star_elem, *star_local, *tri_nodes;
+    const double *normals;
+    int skip_zero_dot;    // D2: pairs with n_e . n_f == 0 were not staged
 };
 
 // V (p0 x p0, symmetric): tile of 4 rows x 32 columns x 32 blocks through smem;
@@ -750,10 +816,17 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
                     if (e < F.e0 || e >= F.e1) continue;
                     const int64_t i = __ldg(F.star_local + a);
                     const double *Qe = F.Q + (e - F.e0) * F.E_x * 9 * F.nd;
+                    double ne[3];
+                    for (int c = 0; c < 3; ++c) ne[c] = __ldg(F.normals + 3 * e + c);
                     double se = 0.0;
                     for (int64_t b = sn0; b < sn1; ++b) {
                         const int64_t f = __ldg(F.star_elem + b);
                         if (f < e) continue;
+                        if (F.skip_zero_dot) {
+                            double nf[3];
+                            for (int c = 0; c < 3; ++c) nf[c] = __ldg(F.normals + 3 * f + c);
+                            if (exact_dot3(ne, nf) == 0.0) continue;
+                        }
                         const int64_t j = __ldg(F.star_local + b);
                         se += Qe[(f * 9 + 3 * i + j) * F.nd + dc + lane];
                     }
@@ -1005,6 +1078,7 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
             F.d0 = (int)d0; F.nd = A.nd; F.d_begin = (int)a->d_begin;
             F.star_indptr = m->star_indptr_dev; F.star_elem = m->star_elem_dev;
             F.star_local = m->star_local_dev; F.tri_nodes = m->tri_nodes_dev;
+            F.normals = m->normals_dev; F.skip_zero_dot = a->op == HB_OP_HYPERSINGULAR2;
             if (!a->test_p1 && !a->trial_p1) {
                 dim3 g((unsigned)cdiv(m->E_x, 32), (unsigned)cdiv(e1 - e0, 4));
                 k_fin_p0p0<<<g, 256, 0, st>>>(F);

@@ -18,6 +18,11 @@ for name, (op, tp, sp, sym) in ops.items():
         s.record(); B = _assemble_operator(op, tp, sp, sym, mesh, tg, p, q, None); e.record(); torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
     res[name] = min(ts)
+    from paper_2102_09811_b200._native import AssemblyStats
+    st = AssemblyStats()
+    _assemble_operator(op, tp, sp, sym, mesh, tg, p, q, None, stats=st)
+    res[name + "_pair"] = round(st.pair_ms, 3)
+    res[name + "_fin"] = round(st.finalize_ms, 3)
 sink = torch.zeros(148*8, dtype=torch.float64, device="cuda")
 grid, iters = 148*8, 20000
 for _ in range(2): _native.call("hb_fp64_probe", grid, iters, _native.ptr(sink), _native.stream_handle())
