@@ -194,6 +194,29 @@ def gen_solve():
                         probe_Vx=H.apply_toeplitz(V, xr), probe_KTx=H.apply_toeplitz(K, xr[:, :m.n_triangles], True))
 
 
+def gen_neumann():
+    """Neumann problem on the config-1 mesh (study.py:104-108,118-136): rhs =
+    1/2 M'h - K'h with h the X00 projection of alpha dG/dn(x - y0, t + 0.1),
+    system D = T^T (a^2 V) T + D2, FGMRES with forward substitution on D."""
+    m = unit_cube(2)
+    tg = H.TimeGrid(1.0, 16)
+    p = H.KernelParams(1.0, tg.step, length_scale=m.diameter)
+    y0 = np.array([1.5, 1.5, 1.5])
+    fn = lambda x, t, n: H.grad_fundamental_normal(np.asarray(x) - y0, n, t + 0.1, 1.0)  # noqa: E731
+    M = H.assemble_mass(m, tg)
+    K = H.assemble_double_layer(m, tg, p, workers=WORKERS)
+    h = H.project_to_space(fn, m, tg, "X00")
+    rhs = 0.5 * H.apply_toeplitz(M, h, transpose_blocks=True) - H.apply_toeplitz(K, h, transpose_blocks=True)
+    V = H.assemble_single_layer(m, tg, p, workers=WORKERS)
+    D2 = H.assemble_hypersingular_d2(m, tg, p, workers=WORKERS)
+    A = H.hypersingular_from_single_layer(V, D2, m, p, overwrite_d2=True)
+    x, rep = H.fgmres(H.toeplitz_operator(A), rhs, rel_tol=1e-10,
+                      right_precond=lambda v: H.forward_block_solve(A, v))
+    np.savez_compressed(os.path.join(OUT, "neumann_c1.npz"), h=h, rhs=rhs, x=x, iterations=rep.iterations,
+                        residual=rep.residual)
+    print("neumann:", rep)
+
+
 def gen_kernels():
     P1 = H.KernelParams(1.0, 0.25)
     P2 = H.KernelParams(0.5, 1.0 / 64, length_scale=3.0)
@@ -213,6 +236,11 @@ def gen_kernels():
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1:                      # regenerate selected fixtures only
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        sys.exit(0)
+    gen_neumann()
     gen_tables()
     gen_kernels()
     gen_ops_small()

@@ -89,3 +89,26 @@ def test_c2_dirichlet_solve_vs_reference():
     assert np.max(np.abs(Vx - g["probe_Vx"])) <= 1e-10 * np.abs(g["probe_Vx"]).max()
     KTx = hb.apply_toeplitz(K, g["probe_x"][:, :m.n_triangles], True)
     assert np.max(np.abs(KTx - g["probe_KTx"])) <= 1e-10 * np.abs(g["probe_KTx"]).max()
+
+
+def test_c1_neumann_solve_vs_reference():
+    """Neumann path: rhs = 1/2 M'h - K'h (blockwise
+    transposes, shared storage), D = T^T (a^2 V) T + D2, FGMRES with forward
+    substitution on D -- as heatbem/study.py:104-136."""
+    g = golden("neumann_c1")
+    m = hb.unit_cube_mesh(2)
+    tg = hb.TimeGrid(1.0, 16)
+    p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
+    y0 = np.array([1.5, 1.5, 1.5])
+    h = hb.project_to_space(lambda x, t, n: hb.grad_fundamental_normal(np.asarray(x) - y0, n, t + 0.1, 1.0),
+                            m, tg, "X00")
+    assert np.allclose(h, g["h"], rtol=1e-13, atol=1e-16 * np.abs(g["h"]).max())
+    Mm = hb.assemble_mass(m, tg)
+    K = hb.assemble_double_layer(m, tg, p)
+    rhs = 0.5 * hb.apply_toeplitz(Mm.transposed(), h) - hb.apply_toeplitz(K.transposed(), h)
+    assert np.max(np.abs(rhs - g["rhs"])) <= 1e-10 * np.abs(g["rhs"]).max()
+    D = hb.assemble_hypersingular(m, tg, p)
+    x, rep = hb.fgmres(hb.toeplitz_operator(D), rhs, rel_tol=1e-10,
+                       right_precond=lambda v: hb.forward_block_solve(D, v))
+    assert rep.converged and rep.residual <= 1e-10
+    assert np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"]) <= 1e-8
