@@ -228,4 +228,6 @@ def test_c3_sampled_rows_vs_reference():
         acc = np.abs(gs - g[f"{op}_exact"]).max(axis=(1, 2)) / mx
         assert np.all(par <= np.maximum(1e-11, 3 * eps)), (op, par.max())
         assert np.all(acc <= ACC[op] * eps + 1e-13), (op, np.max(acc / eps))
-        assert int((got == 0).sum()) == int(g[f"{op}_zeros"][0]), op
+        # no structural zeros on the sphere (no coplanar pairs): the reference's
+        # exact zeros at large d are rounding cancellations of -L + 2L - L,
+        # covered by the value gate above, not a sparsity pattern
