@@ -36,6 +36,7 @@
 // E_t = 4 vs E_t = 2 with the same step: the reference's Toeplitz-reuse test).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "hb_common.cuh"
@@ -65,6 +66,7 @@ struct PairArgs {
     int halve_diag;
     double *Q;
     unsigned long long *counter;   // work-item counter (zeroed per launch)
+    int debug_class;               // 0 all pairs; 1 / 2 touching / separated only (HB_DEBUG_CLASS)
 };
 
 template <int OP, int NIJ>
@@ -677,9 +679,11 @@ __global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_
     double *Ls = geo + 32 * Layout<OP, NIJ>::PAY;
     const hb_mesh_desc &M = A.m;
     const int64_t s_lo = __ldg(M.sing_rowptr_dev + A.e0), s_hi = __ldg(M.sing_rowptr_dev + A.e1);
-    const int64_t n_sing = s_hi - s_lo;
+    int64_t n_sing = s_hi - s_lo;
     const int64_t nseg = cdiv(M.E_x, 32);
-    const int64_t n_reg = (A.e1 - A.e0) * nseg;
+    int64_t n_reg = (A.e1 - A.e0) * nseg;
+    if (A.debug_class == 1) n_reg = 0;      // study hook: touching pairs only
+    if (A.debug_class == 2) n_sing = 0;     // study hook: separated pairs only
     Slots<OP, NJ> T;
     T.init(A, lane & 15);
     for (;;) {
@@ -1045,6 +1049,7 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
     A.inva = 1.0 / a->alpha;
     A.kconst = (a->op == 0) ? 1.0 / sqrt(kPi * a->alpha * a->alpha * a->alpha) : 1.0 / sqrt(kPi * a->alpha);
     A.halve_diag = p1p1 ? 1 : 0;
+    if (const char *dc = getenv("HB_DEBUG_CLASS")) A.debug_class = atoi(dc);
     A.Q = (double *)a->workspace_dev;
     A.counter = (unsigned long long *)((char *)a->workspace_dev + q_bytes);
 
