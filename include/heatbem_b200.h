@@ -80,6 +80,14 @@ typedef struct {
      * element in star_elem/star_local[star_indptr[n] : star_indptr[n+1]] */
     const int64_t *star_indptr_dev, *star_elem_dev, *star_local_dev;
     int64_t star_max;               /* max star size                        */
+    /* curl-combine plan over 32-node tiles t = 0..ceil(N_x/32)-1: the sorted
+     * distinct elements of the tile's node stars are
+     * curl_tile_elem[curl_tile_eptr[t] .. curl_tile_eptr[t+1]); star entry s
+     * (node n) sits at curl_star_pos[s] in the list of n's tile. */
+    const int64_t *curl_tile_eptr_dev, *curl_tile_elem_dev;
+    const int32_t *curl_star_pos_dev;
+    int64_t curl_tile_emax;         /* max elements per tile                */
+    int64_t curl_tile_smax;         /* max star entries per tile            */
 } hb_mesh_desc;
 
 /* Optional per-call statistics (host memory).  When hb_assembly_desc.stats
@@ -125,7 +133,8 @@ int hb_pair_classes(const hb_mesh_desc *mesh, int64_t e0, int64_t e1, int8_t *ou
 /* D = D2 + alpha^2 sum_o T_o^T V T_o per block (curl of the hat functions,
  * heatbem/assembly.py:289-334).  V: (nb, E_x, E_x), D2 and D: (nb, N_x, N_x);
  * D may alias D2.  curls_dev: (E_x, 3, 3) surface curls per local hat.
- * workspace: >= hb_curl_workspace(mesh, 1) bytes (more = more blocks per pass). */
+ * Needs the mesh's curl tile plan; hb_curl_workspace returns 0 (the
+ * workspace arguments are kept for ABI stability and may be NULL). */
 size_t hb_curl_workspace(const hb_mesh_desc *mesh, int64_t blocks_per_pass);
 int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha,
                     const double *curls_dev, const double *V_dev, const double *D2_dev,

@@ -44,6 +44,8 @@ class MeshDesc(ctypes.Structure):
         ("sing_row_dev", _P),
         ("star_indptr_dev", _P), ("star_elem_dev", _P), ("star_local_dev", _P),
         ("star_max", _I64),
+        ("curl_tile_eptr_dev", _P), ("curl_tile_elem_dev", _P), ("curl_star_pos_dev", _P),
+        ("curl_tile_emax", _I64), ("curl_tile_smax", _I64),
     ]
 
 

@@ -713,6 +713,9 @@ struct FinArgs {
     const int64_t *star_indptr, *star_elem, *star_local, *tri_nodes;
     const double *normals;
     int skip_zero_dot;    // D2: pairs with n_e . n_f == 0 were not staged
+    int star_max;
+    const int64_t *tile_eptr, *tile_elem;   // curl tile plan (32-node tiles)
+    const int32_t *star_pos;
 };
 
 // V (p0 x p0, symmetric): tile of 4 rows x 32 columns x 32 blocks through smem;
@@ -787,18 +790,74 @@ __global__ void __launch_bounds__(256) k_fin_p0p1(const FinArgs F)
 
 // D2 / V11 (p1 x p1): X[d][m][n] += sum_{(e,i) in star(m), e in chunk}
 //                                   sum_{(f,j) in star(n), f >= e} Q[e,f][3i+j][d]
+// CTA = (owner of node m, 32-node column tile), warp per column node n, lane
+// per block d.  Which (e,f) were staged (f >= e, and n_e . n_f != 0 for D2)
+// is decided once per CTA as a bitmask over the column tile's element list
+// (the mesh's curl tile plan); the star product loop is then a bit test and
+// a predicated load -- unstaged pairs add +0.0, which leaves the sum as is.
+constexpr int kFinMaxW = 8;   // bitmask words per star entry (tile lists <= 256 elements)
+
 __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
 {
     __shared__ double tile[32][33];
-    const int64_t n0 = (int64_t)blockIdx.y * 32, m = blockIdx.x;
+    extern __shared__ __align__(16) double fsm[];
+    // CTA x = (element of the chunk, local node): node m is handled by the
+    // CTA of the first chunk element in its (element-sorted) star only
+    const int64_t n0 = (int64_t)blockIdx.y * 32, eo = F.e0 + blockIdx.x / 3;
+    const int64_t m = __ldg(F.tri_nodes + 3 * eo + blockIdx.x % 3);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t sm0 = __ldg(F.star_indptr + m), sm1 = __ldg(F.star_indptr + m + 1);
-    bool any = false;
-    for (int64_t a = sm0; a < sm1; ++a) {
+    int64_t first = -1;
+    for (int64_t a = sm0; a < sm1 && first < 0; ++a) {
         const int64_t e = __ldg(F.star_elem + a);
-        any |= (e >= F.e0 && e < F.e1);
+        if (e >= F.e0) first = e;
     }
-    if (!any) return;
+    if (first != eo) return;
+    const int smax = F.star_max;
+    int64_t *sQ = (int64_t *)fsm;                          // [star_max] Q offset of (e - e0, 3i)
+    int64_t *sE = sQ + smax;                               // [star_max] e
+    int64_t *wFJ = sE + smax;                              // [kWarps][star_max] (9f + j) nd of node n's star
+    unsigned *okm = (unsigned *)(wFJ + kWarps * smax);     // [star_max][kFinMaxW]
+    int *wP = (int *)(okm + smax * kFinMaxW);              // [kWarps][star_max] tile position of f
+    __shared__ int na_s;
+    if (threadIdx.x == 0) {
+        int na = 0;
+        for (int64_t a = sm0; a < sm1; ++a) {
+            const int64_t e = __ldg(F.star_elem + a);
+            if (e < F.e0 || e >= F.e1) continue;
+            sE[na] = e;
+            sQ[na] = (e - F.e0) * F.E_x * 9 * (int64_t)F.nd + 3 * __ldg(F.star_local + a) * F.nd;
+            ++na;
+        }
+        na_s = na;
+    }
+    __syncthreads();
+    const int na = na_s;
+    const int64_t tB0 = F.tile_eptr[blockIdx.y], tB = F.tile_eptr[blockIdx.y + 1] - tB0;
+    {   // staged-pair bitmask: warp w owns word w (tile positions 32w..32w+31)
+        const int p = 32 * warp + lane;
+        int64_t f = -1;
+        double nf[3] = {0.0, 0.0, 0.0};
+        if (p < tB) {
+            f = F.tile_elem[tB0 + p];
+            for (int c = 0; c < 3; ++c) nf[c] = __ldg(F.normals + 3 * f + c);
+        }
+        for (int a = 0; a < na; ++a) {
+            const int64_t e = sE[a];
+            bool ok = p < tB && f >= e;
+            if (F.skip_zero_dot) {
+                const double ne[3] = {__ldg(F.normals + 3 * e), __ldg(F.normals + 3 * e + 1),
+                                      __ldg(F.normals + 3 * e + 2)};
+                ok = ok && exact_dot3(ne, nf) != 0.0;
+            }
+            const unsigned word = __ballot_sync(kFull, ok);
+            if (lane == 0) okm[a * kFinMaxW + warp] = word;
+        }
+    }
+    __syncthreads();
+    const bool dok = lane < F.nd;
+    int64_t *myFJ = wFJ + warp * smax;
+    int *myP = wP + warp * smax;
     for (int dc = 0; dc < F.nd; dc += 32) {
         const int ndc = min(32, F.nd - dc);
         // stage X[d][m][n0..n0+31] (coalesced over n), add this chunk's
@@ -810,34 +869,32 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
             tile[lane][dl] = n < F.N_x ? F.out[(b * F.R + m) * F.C + n] : 0.0;
         }
         __syncthreads();
+        const bool lok = dok && lane < ndc;
         for (int nl = warp; nl < 32; nl += kWarps) {
             const int64_t n = n0 + nl;
-            if (n < F.N_x && lane < ndc) {
-                double x = tile[nl][lane];
-                const int64_t sn0 = __ldg(F.star_indptr + n), sn1 = __ldg(F.star_indptr + n + 1);
-                for (int64_t a = sm0; a < sm1; ++a) {
-                    const int64_t e = __ldg(F.star_elem + a);
-                    if (e < F.e0 || e >= F.e1) continue;
-                    const int64_t i = __ldg(F.star_local + a);
-                    const double *Qe = F.Q + (e - F.e0) * F.E_x * 9 * F.nd;
-                    double ne[3];
-                    for (int c = 0; c < 3; ++c) ne[c] = __ldg(F.normals + 3 * e + c);
-                    double se = 0.0;
-                    for (int64_t b = sn0; b < sn1; ++b) {
-                        const int64_t f = __ldg(F.star_elem + b);
-                        if (f < e) continue;
-                        if (F.skip_zero_dot) {
-                            double nf[3];
-                            for (int c = 0; c < 3; ++c) nf[c] = __ldg(F.normals + 3 * f + c);
-                            if (exact_dot3(ne, nf) == 0.0) continue;
-                        }
-                        const int64_t j = __ldg(F.star_local + b);
-                        se += Qe[(f * 9 + 3 * i + j) * F.nd + dc + lane];
-                    }
-                    x += se;
-                }
-                tile[nl][lane] = x;
+            if (n >= F.N_x) break;
+            const int sn0 = (int)__ldg(F.star_indptr + n), nb = (int)__ldg(F.star_indptr + n + 1) - sn0;
+            for (int b = lane; b < nb; b += 32) {
+                myFJ[b] = (9 * __ldg(F.star_elem + sn0 + b) + __ldg(F.star_local + sn0 + b)) * F.nd;
+                myP[b] = F.star_pos[sn0 + b];
             }
+            __syncwarp();
+            double x = tile[nl][lane];
+            for (int a = 0; a < na; ++a) {
+                const double *Qe = F.Q + sQ[a] + dc + lane;
+                const unsigned *om = okm + a * kFinMaxW;
+                double se = 0.0;
+#pragma unroll 4
+                for (int b = 0; b < nb; ++b) {
+                    const int p = myP[b];
+                    const bool ok = lok && ((om[p >> 5] >> (p & 31)) & 1u);
+                    const double q = ok ? Qe[myFJ[b]] : 0.0;
+                    se += q;
+                }
+                x += se;
+            }
+            tile[nl][lane] = x;
+            __syncwarp();
         }
         __syncthreads();
         for (int dl = warp; dl < ndc; dl += kWarps) {
@@ -1020,6 +1077,12 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
                   (long long)a->E_t, (long long)a->d_begin, (long long)a->d_end, (long long)m->E_x);
         return HB_ERR_INVALID;
     }
+    if (a->test_p1 && a->trial_p1 &&
+        (!m->curl_tile_eptr_dev || !m->curl_tile_elem_dev || !m->curl_star_pos_dev ||
+         m->curl_tile_emax > 32 * kFinMaxW)) {
+        set_error("hb_assemble: p1 x p1 needs the mesh tile plan with <= %d elements per 32-node tile", 32 * kFinMaxW);
+        return HB_ERR_UNSUPPORTED;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     const int nj = choose_nj(a);
     const int W = 16 * nj;
@@ -1065,12 +1128,14 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
         A.it_lo = (int)std::max<int64_t>(1, d0 - 1);
         A.it_hi = (int)d1;
         A.need_special = d0 <= 1;
+        // a short (tail) window needs only the lanes-x-slots its gaps occupy
+        const int nj_w = std::min(nj, (int)cdiv(A.it_hi - A.it_lo + 1, 16));
         for (int64_t e0 = 0; e0 < m->E_x; e0 += rows_per_chunk) {
             const int64_t e1 = std::min(m->E_x, e0 + rows_per_chunk);
             A.e0 = e0;
             A.e1 = e1;
             cudaEvent_t ev = LT.begin(st);
-            int rc = run_pairs(a, nj, A, st);
+            int rc = run_pairs(a, nj_w, A, st);
             if (rc) return rc;
             LT.end(ev, true, st);
             LT.launches += 1;
@@ -1084,6 +1149,8 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
             F.star_indptr = m->star_indptr_dev; F.star_elem = m->star_elem_dev;
             F.star_local = m->star_local_dev; F.tri_nodes = m->tri_nodes_dev;
             F.normals = m->normals_dev; F.skip_zero_dot = a->op == HB_OP_HYPERSINGULAR2;
+            F.star_max = (int)m->star_max;
+            F.tile_eptr = m->curl_tile_eptr_dev; F.tile_elem = m->curl_tile_elem_dev; F.star_pos = m->curl_star_pos_dev;
             if (!a->test_p1 && !a->trial_p1) {
                 dim3 g((unsigned)cdiv(m->E_x, 32), (unsigned)cdiv(e1 - e0, 4));
                 k_fin_p0p0<<<g, 256, 0, st>>>(F);
@@ -1091,8 +1158,10 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
                 dim3 g((unsigned)(e1 - e0), (unsigned)cdiv(m->N_x, 32));
                 k_fin_p0p1<<<g, 256, 0, st>>>(F);
             } else {
-                dim3 g((unsigned)m->N_x, (unsigned)cdiv(m->N_x, 32));
-                k_fin_p1p1_accum<<<g, 256, 0, st>>>(F);
+                dim3 g((unsigned)(3 * (e1 - e0)), (unsigned)cdiv(m->N_x, 32));
+                const size_t fsm = (size_t)m->star_max * ((2 + kWarps) * sizeof(int64_t) + kFinMaxW * sizeof(unsigned) +
+                                                          kWarps * sizeof(int));
+                k_fin_p1p1_accum<<<g, 256, fsm, st>>>(F);
             }
             rc = cuda_check(cudaGetLastError(), "finalize");
             if (rc) return rc;

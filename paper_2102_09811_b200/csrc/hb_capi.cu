@@ -48,70 +48,163 @@ __global__ void __launch_bounds__(256) k_fp64_probe(int64_t iters, double *sink)
 //   D[m][n]    = D2[m][n] + a2 sum_{(e,i) in star(m)} sum_o curl_ei[o] W[e][o][n]
 // the second stage runs on 32x32 tile pairs (ti <= tj), computes n >= m and
 // writes the mirror through shared memory (exact symmetry, coalesced).
-__global__ void __launch_bounds__(256) k_curl_w(hb_mesh_desc M, const double *curls, const double *V, double *W,
-                                                int64_t d0)
-{
-    extern __shared__ double vrow[];
-    const int64_t e = blockIdx.x, d = d0 + blockIdx.y;
-    const int64_t E = M.E_x, N = M.N_x;
-    const double *Ve = V + (d * E + e) * E;
-    for (int64_t f = threadIdx.x; f < E; f += blockDim.x) vrow[f] = Ve[f];
-    __syncthreads();
-    double *We = W + ((int64_t)blockIdx.y * E + e) * 3 * N;
-    for (int64_t n = threadIdx.x; n < N; n += blockDim.x) {
-        const int64_t s0 = __ldg(M.star_indptr_dev + n), s1 = __ldg(M.star_indptr_dev + n + 1);
-        double w0 = 0.0, w1 = 0.0, w2 = 0.0;
-        for (int64_t s = s0; s < s1; ++s) {
-            const int64_t f = __ldg(M.star_elem_dev + s), j = __ldg(M.star_local_dev + s);
-            const double v = vrow[f];
-            w0 = fma(__ldg(curls + 9 * f + 3 * j), v, w0);
-            w1 = fma(__ldg(curls + 9 * f + 3 * j + 1), v, w1);
-            w2 = fma(__ldg(curls + 9 * f + 3 * j + 2), v, w2);
-        }
-        We[n] = w0;
-        We[N + n] = w1;
-        We[2 * N + n] = w2;
-    }
-}
+// D = D2 + a^2 sum_k T_k^T V T_k, one CTA per (node tile ti <= node tile tj)
+// and a range of blocks d.  The elements of the stars of a 32-node tile form
+// a sorted list (mesh plan: tile_eptr/tile_elem, star_pos = position of each
+// star entry in its node's tile list); the CTA stages V[rows of ti][cols of tj]
+// in shared memory 32 rows at a time and forms, entirely on chip,
+//   W_k[e][n] = sum_{(f,j) in star(n)} c_k(f,j) V[e][f]            (T stage)
+//   D[m][n]  += sum_{(e,i) in star(m), e in chunk} sum_k c_k(e,i) W_k[e][n]
+// in the star orders (node stars are element-sorted, chunks ascending), so
+// the sums are those of the two-pass W formulation without its E_x x 3N_x
+// intermediate in HBM.  Upper tiles only; the lower triangle is mirrored.
+constexpr int kCT = 32;    // nodes per tile
+constexpr int kRC = 32;    // staged V rows per chunk (one per lane)
+constexpr int kMaxJ = 8;   // column elements per tile <= 32 kMaxJ
 
-__global__ void __launch_bounds__(256) k_curl_d(hb_mesh_desc M, double a2, const double *curls, const double *W,
-                                                const double *D2, double *D, int64_t d0)
+struct CurlArgs {
+    hb_mesh_desc M;
+    double a2;
+    const double *curls, *V, *D2;
+    double *D;
+    int64_t n_blocks;
+    int dpc, ldv, smax, emax;
+};
+
+// star entry of a tile: curl vector of (element, local hat) and the element's
+// position in the tile's element list (two 16-byte broadcast loads)
+struct __align__(16) CurlEnt {
+    double c0, c1, c2;
+    int pos, pad;
+};
+
+__global__ void __launch_bounds__(256) k_curl_tile(const CurlArgs C)
 {
-    __shared__ double tile[32][33];
-    const int64_t N = M.N_x, E = M.E_x;
-    const int64_t nt = cdiv(N, 32);
+    extern __shared__ __align__(16) double csm[];
+    const int64_t N = C.M.N_x, E = C.M.E_x;
+    const int64_t nt = cdiv(N, kCT);
     int64_t ti = 0, rem = blockIdx.x;
     while (rem >= nt - ti) { rem -= nt - ti; ++ti; }
     const int64_t tj = ti + rem;
-    const int64_t d = d0 + blockIdx.y;
-    const double *Wd = W + (int64_t)blockIdx.y * E * 3 * N;
-    const double *D2d = D2 + d * N * N;
-    double *Dd = D + d * N * N;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int64_t n = tj * 32 + tx;
-    for (int r = ty; r < 32; r += 8) {
-        const int64_t m = ti * 32 + r;
-        double val = 0.0;
-        if (m < N && n < N && n >= m) {
-            const int64_t s0 = __ldg(M.star_indptr_dev + m), s1 = __ldg(M.star_indptr_dev + m + 1);
-            double acc = 0.0;
-            for (int64_t s = s0; s < s1; ++s) {
-                const int64_t e = __ldg(M.star_elem_dev + s), i = __ldg(M.star_local_dev + s);
-                const double *We = Wd + e * 3 * N;
-                acc = fma(__ldg(curls + 9 * e + 3 * i), We[n], acc);
-                acc = fma(__ldg(curls + 9 * e + 3 * i + 1), We[N + n], acc);
-                acc = fma(__ldg(curls + 9 * e + 3 * i + 2), We[2 * N + n], acc);
-            }
-            val = D2d[m * N + n] + a2 * acc;
-            Dd[m * N + n] = val;
-        }
-        tile[r][tx] = val;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    double *Vs = csm;                                   // [kRC][ldv]
+    double *Ts = Vs + kRC * C.ldv;                      // [3][kCT][33]: Ts[k][n][r]
+    double *Dt = Ts + 3 * kCT * 33;                     // [32][33]
+    CurlEnt *cE = (CurlEnt *)(Dt + 32 * 33);            // [smax] star entries of tile tj
+    CurlEnt *rE = cE + C.smax;                          // [smax] star entries of tile ti
+    int64_t *rowE = (int64_t *)(rE + C.smax);           // [emax] elements of ti
+    int *cPtr = (int *)(rowE + C.emax);                 // [33]
+    int *rPtr = cPtr + 33;                              // [33]
+
+    const int64_t nn0 = tj * kCT, mm0 = ti * kCT;
+    const int nnc = (int)(N - nn0 < kCT ? N - nn0 : (int64_t)kCT), nmr = (int)(N - mm0 < kCT ? N - mm0 : (int64_t)kCT);
+    const int64_t B0 = C.M.curl_tile_eptr_dev[tj], B = C.M.curl_tile_eptr_dev[tj + 1] - B0;
+    const int64_t A0 = C.M.curl_tile_eptr_dev[ti], A = C.M.curl_tile_eptr_dev[ti + 1] - A0;
+    const int64_t cs0 = C.M.star_indptr_dev[nn0], rs0 = C.M.star_indptr_dev[mm0];
+    int64_t coff[kMaxJ];                                // this lane's column elements
+#pragma unroll
+    for (int j = 0; j < kMaxJ; ++j) {
+        const int c = lane + 32 * j;
+        coff[j] = c < B ? C.M.curl_tile_elem_dev[B0 + c] : 0;
+    }
+    for (int i = tid; i < A; i += blockDim.x) rowE[i] = C.M.curl_tile_elem_dev[A0 + i];
+    for (int i = tid; i <= kCT; i += blockDim.x) {
+        cPtr[i] = (int)(C.M.star_indptr_dev[nn0 + min(i, nnc)] - cs0);
+        rPtr[i] = (int)(C.M.star_indptr_dev[mm0 + min(i, nmr)] - rs0);
     }
     __syncthreads();
-    // mirror: D[n][m] = D[m][n] for n > m (rows of the tj tile, columns of ti)
-    for (int r = ty; r < 32; r += 8) {
-        const int64_t nn = tj * 32 + r, mm = ti * 32 + tx;
-        if (nn < N && mm < N && nn > mm) Dd[nn * N + mm] = tile[tx][r];
+    for (int i = tid; i < cPtr[kCT]; i += blockDim.x) {
+        const int64_t s = cs0 + i, f = C.M.star_elem_dev[s], j = C.M.star_local_dev[s];
+        cE[i] = CurlEnt{C.curls[9 * f + 3 * j], C.curls[9 * f + 3 * j + 1], C.curls[9 * f + 3 * j + 2],
+                        C.M.curl_star_pos_dev[s], 0};
+    }
+    for (int i = tid; i < rPtr[kCT]; i += blockDim.x) {
+        const int64_t s = rs0 + i, e = C.M.star_elem_dev[s], l = C.M.star_local_dev[s];
+        rE[i] = CurlEnt{C.curls[9 * e + 3 * l], C.curls[9 * e + 3 * l + 1], C.curls[9 * e + 3 * l + 2],
+                        C.M.curl_star_pos_dev[s], 0};
+    }
+    __syncthreads();
+
+    const int64_t d_lo = (int64_t)blockIdx.y * C.dpc, d_hi = (C.n_blocks < d_lo + C.dpc ? C.n_blocks : d_lo + C.dpc);
+    const double *vrow = Vs + lane * C.ldv;
+    for (int64_t d = d_lo; d < d_hi; ++d) {
+        const double *Vd = C.V + d * E * E;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        int sp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sp[q] = rPtr[min(warp + 8 * q, kCT)];
+        for (int r0 = 0; r0 < (int)A; r0 += kRC) {
+            const int rc = (int)A - r0 < kRC ? (int)A - r0 : kRC;
+            // gather the chunk with async copies: all of its loads in flight at once
+            for (int r = warp; r < rc; r += 8) {
+                const double *Vr = Vd + rowE[r0 + r] * E;
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(Vs + r * C.ldv + lane);
+#pragma unroll
+                for (int j = 0; j < kMaxJ; ++j)
+                    if (lane + 32 * j < B)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa + 256 * j),
+                                     "l"(Vr + coff[j]) : "memory");
+            }
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            __syncthreads();
+            // T stage: warp per node (uniform star loop, broadcast entries), lane per staged row
+            // (rows >= rc compute unused values)
+            for (int nl = warp; nl < nnc; nl += 8) {
+                double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+                for (int s = cPtr[nl]; s < cPtr[nl + 1]; ++s) {
+                    const CurlEnt ce = cE[s];
+                    const double v = vrow[ce.pos];
+                    w0 = fma(ce.c0, v, w0);
+                    w1 = fma(ce.c1, v, w1);
+                    w2 = fma(ce.c2, v, w2);
+                }
+                Ts[(0 * kCT + nl) * 33 + lane] = w0;
+                Ts[(1 * kCT + nl) * 33 + lane] = w1;
+                Ts[(2 * kCT + nl) * 33 + lane] = w2;
+            }
+            __syncthreads();
+            // D stage: warp per output row m, lane per column n; the row's star
+            // entries in this chunk are the next ones (element-sorted stars)
+            const int rend = r0 + rc;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int ml = warp + 8 * q;
+                if (ml < nmr) {
+                    const int se = rPtr[ml + 1];
+                    int s = sp[q];
+                    for (; s < se; ++s) {
+                        const CurlEnt re = rE[s];
+                        if (re.pos >= rend) break;
+                        const int pr = re.pos - r0;
+                        acc[q] = fma(re.c0, Ts[(0 * kCT + lane) * 33 + pr], acc[q]);
+                        acc[q] = fma(re.c1, Ts[(1 * kCT + lane) * 33 + pr], acc[q]);
+                        acc[q] = fma(re.c2, Ts[(2 * kCT + lane) * 33 + pr], acc[q]);
+                    }
+                    sp[q] = s;
+                }
+            }
+            __syncthreads();
+        }
+        const double *D2d = C.D2 + d * N * N;
+        double *Dd = C.D + d * N * N;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int ml = warp + 8 * q;
+            const int64_t m = mm0 + ml, n = nn0 + lane;
+            double val = 0.0;
+            if (ml < nmr && lane < nnc && n >= m) {
+                val = fma(C.a2, acc[q], D2d[m * N + n]);
+                Dd[m * N + n] = val;
+            }
+            Dt[ml * 33 + lane] = val;
+        }
+        __syncthreads();
+        for (int r = warp; r < kCT; r += 8) {   // D[n][m] = D[m][n] for n > m
+            const int64_t n = nn0 + r, m = mm0 + lane;
+            if (r < nnc && lane < nmr && n > m) Dd[n * N + m] = Dt[lane * 33 + r];
+        }
+        __syncthreads();
     }
 }
 
@@ -132,37 +225,50 @@ extern "C" int hb_fp64_probe(int64_t grid, int64_t iters, double *sink_dev, void
 
 extern "C" size_t hb_curl_workspace(const hb_mesh_desc *mesh, int64_t blocks_per_pass)
 {
-    if (!mesh || blocks_per_pass < 1) return 0;
-    return (size_t)blocks_per_pass * mesh->E_x * 3 * mesh->N_x * sizeof(double);
+    (void)mesh; (void)blocks_per_pass;
+    return 0;   // the tile kernel keeps its intermediates on chip
 }
 
 extern "C" int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha, const double *curls_dev,
                                const double *V_dev, const double *D2_dev, double *D_dev, void *workspace_dev,
                                size_t workspace_bytes, void *stream)
 {
+    (void)workspace_dev; (void)workspace_bytes;
     if (!mesh || n_blocks < 1 || !curls_dev || !V_dev || !D2_dev || !D_dev) {
         set_error("hb_curl_combine: bad arguments");
         return HB_ERR_INVALID;
     }
-    const size_t per = hb_curl_workspace(mesh, 1);
-    if (!workspace_dev || workspace_bytes < per) {
-        set_error("hb_curl_combine: workspace %zu bytes < one block (%zu)", workspace_bytes, per);
-        return HB_ERR_WORKSPACE;
+    if (!mesh->curl_tile_eptr_dev || !mesh->curl_tile_elem_dev || !mesh->curl_star_pos_dev ||
+        mesh->curl_tile_emax < 1 || mesh->curl_tile_smax < 1) {
+        set_error("hb_curl_combine: mesh descriptor has no curl tile plan");
+        return HB_ERR_INVALID;
     }
-    const int64_t bpp = std::min<int64_t>(n_blocks, (int64_t)(workspace_bytes / per));
-    const size_t smem = (size_t)mesh->E_x * sizeof(double);
-    if (smem > 227 * 1024) { set_error("hb_curl_combine: E_x too large for the row stage"); return HB_ERR_UNSUPPORTED; }
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_curl_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaStream_t st = (cudaStream_t)stream;
-    const int64_t nt = cdiv(mesh->N_x, 32);
-    for (int64_t d0 = 0; d0 < n_blocks; d0 += bpp) {
-        const int64_t nb = std::min(bpp, n_blocks - d0);
-        k_curl_w<<<dim3((unsigned)mesh->E_x, (unsigned)nb), 256, smem, st>>>(*mesh, curls_dev, V_dev,
-                                                                          (double *)workspace_dev, d0);
-        k_curl_d<<<dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)nb), 256, 0, st>>>(
-            *mesh, alpha * alpha, curls_dev, (const double *)workspace_dev, D2_dev, D_dev, d0);
-        int rc = cuda_check(cudaGetLastError(), "hb_curl_combine");
-        if (rc) return rc;
+    CurlArgs C{};
+    C.M = *mesh; C.a2 = alpha * alpha; C.curls = curls_dev; C.V = V_dev; C.D2 = D2_dev; C.D = D_dev;
+    C.n_blocks = n_blocks;
+    C.emax = (int)mesh->curl_tile_emax;
+    C.smax = (int)mesh->curl_tile_smax;
+    C.ldv = C.emax | 1;
+    if (C.emax > 32 * kMaxJ) {
+        set_error("hb_curl_combine: %d elements around a 32-node tile (max %d)", C.emax, 32 * kMaxJ);
+        return HB_ERR_UNSUPPORTED;
     }
-    return HB_OK;
+    const size_t smem = sizeof(double) * ((size_t)kRC * C.ldv + 3 * kCT * 33 + 32 * 33) +
+                        sizeof(CurlEnt) * 2 * (size_t)C.smax + sizeof(int64_t) * (size_t)C.emax + sizeof(int) * 66;
+    if (smem > 227 * 1024) {
+        set_error("hb_curl_combine: node tiles too large for shared memory (%d elements)", C.emax);
+        return HB_ERR_UNSUPPORTED;
+    }
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_curl_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_curl_tile, 256, smem);
+    const int64_t nt = cdiv(mesh->N_x, kCT), npairs = nt * (nt + 1) / 2;
+    // blocks per CTA: enough CTAs for ~4 waves, the rest loops on chip (plan reuse)
+    const int64_t want = (int64_t)std::max(1, per_sm) * nsm * 4;
+    C.dpc = (int)std::max<int64_t>(1, std::min<int64_t>(n_blocks, npairs * n_blocks / std::max<int64_t>(1, want)));
+    const int64_t gy = cdiv(n_blocks, C.dpc);
+    k_curl_tile<<<dim3((unsigned)npairs, (unsigned)gy), 256, smem, (cudaStream_t)stream>>>(C);
+    return cuda_check(cudaGetLastError(), "hb_curl_combine");
 }

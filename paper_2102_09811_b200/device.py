@@ -57,6 +57,29 @@ class HostTables:
         self.star = [c(a) for a in mesh.node_star()]
         self.star_max = int(np.diff(self.star[0]).max())
         self.curls = c(_curls(mesh))
+        self.curl_plan = curl_tile_plan(self.star[0], self.star[1], self.N_x)
+
+
+CURL_TILE = 32   # nodes per tile of the curl-combine kernel (hb_capi.cu kCT)
+
+
+def curl_tile_plan(star_indptr, star_elem, n_nodes: int, tile: int = CURL_TILE):
+    """Per 32-node tile the sorted distinct elements of its node stars
+    (eptr, elem) and, per star entry, its position in its tile's list
+    (int32), plus the max list length and max star entries per tile."""
+    nt = -(-n_nodes // tile)
+    eptr = np.zeros(nt + 1, dtype=np.int64)
+    pos = np.empty(len(star_elem), dtype=np.int32)
+    lists, smax = [], 0
+    for t in range(nt):
+        s0, s1 = int(star_indptr[tile * t]), int(star_indptr[min(n_nodes, tile * t + tile)])
+        u = np.unique(star_elem[s0:s1])
+        lists.append(u)
+        eptr[t + 1] = eptr[t] + len(u)
+        pos[s0:s1] = np.searchsorted(u, star_elem[s0:s1])
+        smax = max(smax, s1 - s0)
+    elem = np.concatenate(lists).astype(np.int64) if lists else np.zeros(0, np.int64)
+    return eptr, elem, pos, int(np.diff(eptr).max()) if nt else 0, int(smax)
 
 
 class DeviceTables:
@@ -86,6 +109,8 @@ class DeviceTables:
             "sing_row": up(H.sing_row),
             "star_indptr": up(H.star[0]), "star_elem": up(H.star[1]), "star_local": up(H.star[2]),
             "curls": up(H.curls),
+            "curl_tile_eptr": up(H.curl_plan[0]), "curl_tile_elem": up(H.curl_plan[1]),
+            "curl_star_pos": up(H.curl_plan[2]),
         }
         for sym in (False, True):
             pos, rp, _ = H.sing[sym]
@@ -115,6 +140,9 @@ class DeviceTables:
         d.star_indptr_dev, d.star_elem_dev = p(t["star_indptr"]), p(t["star_elem"])
         d.star_local_dev = p(t["star_local"])
         d.star_max = H.star_max
+        d.curl_tile_eptr_dev, d.curl_tile_elem_dev = p(t["curl_tile_eptr"]), p(t["curl_tile_elem"])
+        d.curl_star_pos_dev = p(t["curl_star_pos"])
+        d.curl_tile_emax, d.curl_tile_smax = H.curl_plan[3], H.curl_plan[4]
         return d
 
     def desc(self, symmetric: bool) -> _native.MeshDesc:
@@ -138,7 +166,7 @@ def pin_host_tables(H: HostTables):
     import torch
 
     arrays = [H.tri_nodes, H.verts_tri, H.normals, H.centroids, H.diameters, H.areas, *H.reg, *H.near,
-              *H.tn, *H.duf, H.sing_row, *H.star, H.curls]
+              *H.tn, *H.duf, H.sing_row, *H.star, H.curls, *H.curl_plan[:3]]
     for sym in (False, True):
         arrays += list(H.sing[sym][:2])
     H.pinned = {id(a): torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays}

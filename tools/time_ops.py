@@ -30,3 +30,14 @@ s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True
 s.record(); _native.call("hb_fp64_probe", grid, iters, _native.ptr(sink), _native.stream_handle()); e.record(); torch.cuda.synchronize()
 tf = grid*256*iters*8*2/(s.elapsed_time(e)*1e-3)/1e12
 print(json.dumps({"lib": os.environ.get("HB_LIB_PATH", "default"), "ms": res, "fp64_tflops": round(tf, 2)}))
+# curl combine (D = D2 + a^2 curl(V)) at this config
+from paper_2102_09811_b200 import device as hbdev
+from paper_2102_09811_b200.assembly import curl_combine_into
+tabs = hbdev.device_tables(mesh, q)
+Vb = _assemble_operator(0, False, False, True, mesh, tg, p, q, None)
+D2b = _assemble_operator(2, True, True, True, mesh, tg, p, q, None)
+out = torch.empty_like(D2b)
+for _ in range(2): curl_combine_into(tabs, Vb, D2b, out, p.alpha)
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize(); s.record(); curl_combine_into(tabs, Vb, D2b, out, p.alpha); e.record(); torch.cuda.synchronize()
+print(json.dumps({"curl_ms": s.elapsed_time(e)}))
