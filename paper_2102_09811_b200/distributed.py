@@ -30,6 +30,41 @@ def block_range(rank: int, world: int, n_blocks: int):
     return d0, d0 + base + (1 if rank < rem else 0)
 
 
+def window_slots(n_blocks: int) -> int:
+    """Gap slots per assembly window (hb_assembly.cu choose_nj): 16 per
+    lanes-x-slots group, two groups when the history is longer than 16."""
+    return 16 * max(1, min(2, -(-n_blocks // 16)))
+
+
+def window_edges(n_blocks: int):
+    """Block boundaries of hb_assemble's windows over [0, n_blocks): the
+    first window holds W blocks, every later one W - 2 (its two halo gaps)."""
+    W = window_slots(n_blocks)
+    edges, d = [0], 0
+    while d < n_blocks:
+        d = min(n_blocks, W if d <= 1 else d + W - 2)
+        edges.append(d)
+    return edges
+
+
+def aligned_chunks(n_blocks: int, max_blocks: int):
+    """Contiguous d-chunks of at most ``max_blocks`` blocks that start and
+    end on window edges (so chunked assembly evaluates no extra gap slots);
+    a window longer than ``max_blocks`` is split."""
+    edges = window_edges(n_blocks)
+    out, lo = [], 0
+    for a, b in zip(edges[:-1], edges[1:]):
+        if b - lo > max_blocks and a > lo:
+            out.append((lo, a))
+            lo = a
+        while b - lo > max_blocks:
+            out.append((lo, lo + max_blocks))
+            lo += max_blocks
+    if lo < n_blocks:
+        out.append((lo, n_blocks))
+    return out
+
+
 def gap_slots(d0: int, d1: int, window: int = 32):
     """Time gaps i_t >= 1 a rank evaluates for blocks [d0, d1) (incl. halo
     slots at window edges): the redundant work of d-sharding."""
