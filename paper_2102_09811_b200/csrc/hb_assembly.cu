@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_
     extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *tab = smem;
-    special::load_table(tab);
+    special::load_table<OP>(tab);
     __syncthreads();
     double *geo = smem + special::kTabDoubles + warp * smem_doubles_per_warp<OP, NIJ, NJ>();
     double *Ls = geo + 32 * Layout<OP, NIJ>::PAY;
@@ -1194,3 +1194,16 @@ extern "C" int hb_pair_classes(const hb_mesh_desc *m, int64_t e0, int64_t e1, in
                                                                                                         out_dev);
     return cuda_check(cudaGetLastError(), "hb_pair_classes");
 }
+
+#ifdef HB_COUNT_BRANCHES
+// diagnostics build only: warp-level branch mix of the pair kernels' eval_n calls
+extern "C" int hb_debug_branch_counts(unsigned long long *out4, int reset)
+{
+    cudaMemcpyFromSymbol(out4, hb::special::g_branch_count, 4 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(hb::special::g_branch_count, z, sizeof(z));
+    }
+    return cuda_check(cudaGetLastError(), "hb_debug_branch_counts");
+}
+#endif

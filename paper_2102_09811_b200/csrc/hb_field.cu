@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kPotWarps * 32) k_potential(const PotArgs P)
 {
     extern __shared__ __align__(16) double psm[];
     double *tab = psm;
-    special::load_table(tab);
+    special::load_table<KIND == 0 ? 2 : 3>(tab);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *red = psm + special::kTabDoubles;                  // [kPotWarps][kOut]
     double *G = red + kPotWarps * kOut + warp * 4 * P.kcap;    // G(m)

@@ -11,12 +11,19 @@
 // The reference's form of K, (1/(2a) - delta/rho^2) erf + sqrt(delta/(pi a))
 // e^{-x^2}/rho, cancels like 1/x^2 for small x; F(x) = x Pf(x^2) does not.
 //
-//   x <  X0: H = 2/(sqrt(pi) x) + x Ph(t), F = x Pf(t), erf = x Pe(t), t = x^2
-//   x >= X0: erf = 1 - E Q(x), E = e^{-x^2}, Q = erfcx (4 polynomial pieces in
-//            shared memory), H/F = a + E (1/(sqrt(pi) x) - Q a), a = 1 +- 1/(2x^2)
-// Coefficients: csrc/hb_special_coeffs.h (tools/gen_special.py, mpmath).
-// Lanes whose x lies on the other side of X0 follow the same instruction
-// stream (predicated); a branch is skipped when no active lane needs it.
+//   x <  X0 (= 1):  H = 2/(sqrt(pi) x) + x Ph(t), F = x Pf(t), erf = x Pe(t),
+//                   E = x^3 Pg(t), t = x^2 (coefficients uniform across the warp)
+//   X0 <= x < XL:   the function value itself as a degree-12 polynomial in
+//                   u = (x - mid_p) / half on 21 uniform pieces of width 1/4
+//                   (coefficients of the lane's piece from shared memory) --
+//                   all four functions are analytic there, no exp is needed
+//   x >= XL (6.25): the asymptote, erf = E = 1, H/F = 1 +- 1/(2x^2), which
+//                   the exact value rounds to (e^{-x^2}(...) < 2^-53 relative)
+// Coefficients: csrc/hb_special_coeffs.h (tools/gen_special.py, mpmath, with
+// the max relative error of each piece in double Horner).  A lane's region
+// depends on its own x only, so values do not depend on which lanes share a
+// warp (slot / window / rank invariance); a region is skipped when no lane of
+// the warp needs it.
 #pragma once
 
 #include "hb_common.cuh"
@@ -25,16 +32,20 @@
 namespace hb {
 namespace special {
 
-// shared-memory table: erfcx coefficients, then piece mids and 1/half-widths
-constexpr int kTabDoubles = (kQDeg + 1) * kQPieces + 2 * kQPieces;
+#ifdef HB_COUNT_BRANCHES
+__device__ unsigned long long g_branch_count[4];   // [small?1:0 + large?2:0]
+#endif
 
+// shared-memory table: the middle-region coefficients of one function
+// (coefficient k of piece p at tab[k * kMidPieces + p]: lanes in different
+// pieces read neighbouring words)
+constexpr int kTabDoubles = (kMidDeg + 1) * kMidPieces;
+
+template <int KIND>
 __device__ __forceinline__ void load_table(double *tab)
 {
-    for (int i = threadIdx.x; i < (kQDeg + 1) * kQPieces; i += blockDim.x) tab[i] = kQCoef[i];
-    for (int i = threadIdx.x; i < kQPieces; i += blockDim.x) {
-        tab[(kQDeg + 1) * kQPieces + i] = kQMid[i];
-        tab[(kQDeg + 1) * kQPieces + kQPieces + i] = kQInvHalf[i];
-    }
+    const double *src = KIND == 0 ? kMid0 : KIND == 1 ? kMid1 : KIND == 2 ? kMid2 : kMid3;
+    for (int i = threadIdx.x; i < kTabDoubles; i += blockDim.x) tab[i] = src[i];
 }
 
 template <int N>
@@ -46,99 +57,120 @@ __device__ __forceinline__ double horner(const double (&c)[N], double t)   // c:
     return p;
 }
 
+// small-x series (x < X0)
+template <int KIND>
+__device__ __forceinline__ double series(double x, double t, double ix)
+{
+    if (KIND == 0) return fma(x, horner(kPh, t), __dmul_rn(kTwoInvSqrtPi, ix));
+    if (KIND == 1) return __dmul_rn(x, horner(kPf, t));
+    if (KIND == 2) return __dmul_rn(x, horner(kPe, t));
+    return __dmul_rn(__dmul_rn(x, t), horner(kPg, t));
+}
+
+// asymptote (x >= XL)
+template <int KIND>
+__device__ __forceinline__ double asymptote(double ix)
+{
+    if (KIND >= 2) return 1.0;
+    const double hx = __dmul_rn(0.5 * ix, ix);
+    return KIND == 0 ? 1.0 + hx : 1.0 - hx;
+}
+
+// middle-region piece and local variable (exact: x - mid is exact within a piece)
+__device__ __forceinline__ int mid_piece(double x, double &u)
+{
+    const double pf = fmin(fmax(__dmul_rn(x - kX0, kMidInvW), 0.0), (double)(kMidPieces - 1));
+    const int pc = (int)pf;
+    const double mid = kX0 + ((double)pc + 0.5) * (1.0 / kMidInvW);
+    u = __dmul_rn(x - mid, kMidInvHalf);
+    return pc;
+}
+
 // KIND 0: H (single layer), 1: F (double layer), 2: erf (hypersingular D2),
-// 3: E(x) = erf(x) - 2x e^{-x^2}/sqrt(pi) (double-layer potential, = x^3 Pg(t)).
-// ix = 1/x (formed by the caller from precomputed 1/rho and 1/c); `mask` =
-// the lanes executing this call.
+// 3: E(x) = erf(x) - 2x e^{-x^2}/sqrt(pi) (double-layer potential).
+// ix = 1/x (formed by the caller from precomputed 1/rho and 1/c; used by
+// KIND 0/1 only); `mask` = the lanes executing this call.
 template <int KIND>
 __device__ __forceinline__ double eval(double x, double ix, const double *__restrict__ tab, unsigned mask)
 {
     const double t = __dmul_rn(x, x);
-    const bool small = x < kX0;
+    const bool small = x < kX0, huge = x >= kXL, midr = !small && !huge;
     double r = 0.0;
-    if (__any_sync(mask, small)) {
-        if (KIND == 0) r = fma(x, horner(kPh, t), __dmul_rn(kTwoInvSqrtPi, ix));
-        else if (KIND == 1) r = __dmul_rn(x, horner(kPf, t));
-        else if (KIND == 2) r = __dmul_rn(x, horner(kPe, t));
-        else r = __dmul_rn(__dmul_rn(x, t), horner(kPg, t));
-    }
-    if (__any_sync(mask, !small)) {
-        const double E = exp(-t);
-        const int pc = (x >= kQBreak1) + (x >= kQBreak2) + (x >= kQBreak3);
-        const double xc = fmin(x, kQBreak4);
-        const double *mid = tab + (kQDeg + 1) * kQPieces;
-        const double u = __dmul_rn(xc - mid[pc], mid[kQPieces + pc]);
-        double q = tab[kQDeg * kQPieces + pc];
+    if (__any_sync(mask, small)) r = series<KIND>(x, t, ix);
+    if (__any_sync(mask, midr)) {
+        double u;
+        const double *c = tab + mid_piece(x, u);
+        double q = c[kMidDeg * kMidPieces];
 #pragma unroll
-        for (int k = kQDeg - 1; k >= 0; --k) q = fma(q, u, tab[k * kQPieces + pc]);
-        double lv;
-        if (KIND == 2) {
-            lv = fma(-E, q, 1.0);
-        } else if (KIND == 3) {
-            lv = fma(-E, fma(kTwoInvSqrtPi, x, q), 1.0);
-        } else {
-            const double hx = __dmul_rn(0.5 * ix, ix);
-            const double a = KIND == 0 ? 1.0 + hx : 1.0 - hx;
-            lv = fma(E, fma(-q, a, __dmul_rn(kInvSqrtPi, ix)), a);
-        }
-        if (!small) r = lv;
+        for (int k = kMidDeg - 1; k >= 0; --k) q = fma(q, u, c[k * kMidPieces]);
+        asm volatile("" : "+d"(q));
+        r = midr ? q : r;
     }
+    if (huge) r = asymptote<KIND>(ix);
     return r;
 }
 
-// All NJ gap slots of one quadrature point at once: one small-x and one
-// large-x region for the whole group, so the NJ independent Horner chains
-// interleave (ILP NJ) instead of being serialised by per-slot branches.
+// NJ evaluations of one lane at once: one region pass for the whole group,
+// so the NJ independent Horner chains interleave (ILP NJ).
 template <int KIND, int NJ>
 __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)[NJ], double (&r)[NJ],
                                        const double *__restrict__ tab, unsigned mask)
 {
     double t[NJ];
-    bool small[NJ], any_s = false, any_l = false;
+    bool small[NJ], midr[NJ], huge[NJ], any_s = false, any_m = false;
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
         t[j] = __dmul_rn(x[j], x[j]);
+#if defined(HB_FORCE_SMALL)   // timing experiments only: wrong values
+        small[j] = true;
+        midr[j] = false;
+#elif defined(HB_FORCE_MID)
+        small[j] = false;
+        midr[j] = true;
+#else
         small[j] = x[j] < kX0;
+        midr[j] = !small[j] && x[j] < kXL;
+#endif
+        huge[j] = !small[j] && !midr[j];
         any_s |= small[j];
-        any_l |= !small[j];
+        any_m |= midr[j];
         r[j] = 0.0;
     }
+#ifdef HB_COUNT_BRANCHES   // diagnostics: warp-level region mix of eval_n calls
+    {
+        const bool vs = __any_sync(mask, any_s), vm = __any_sync(mask, any_m);
+        if ((threadIdx.x & 31) == (__ffs(mask) - 1))
+            atomicAdd(&g_branch_count[(vs ? 1 : 0) + (vm ? 2 : 0)], 1ull);
+    }
+#endif
+    // each region computes every lane's chains unconditionally (the NJ chains
+    // interleave; a per-lane condition would let the compiler sink a chain
+    // into a divergent branch) and lanes keep their own region's value
     if (__any_sync(mask, any_s)) {
 #pragma unroll
+        for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], ix[j]);
+    }
+    if (__any_sync(mask, any_m)) {
+        double u[NJ], q[NJ];
+        const double *c[NJ];
+#pragma unroll
         for (int j = 0; j < NJ; ++j) {
-            if (KIND == 0) r[j] = fma(x[j], horner(kPh, t[j]), __dmul_rn(kTwoInvSqrtPi, ix[j]));
-            else if (KIND == 1) r[j] = __dmul_rn(x[j], horner(kPf, t[j]));
-            else r[j] = __dmul_rn(x[j], horner(kPe, t[j]));
+            c[j] = tab + mid_piece(x[j], u[j]);
+            q[j] = c[j][kMidDeg * kMidPieces];
+        }
+#pragma unroll
+        for (int k = kMidDeg - 1; k >= 0; --k)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], u[j], c[j][k * kMidPieces]);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            asm volatile("" : "+d"(q[j]));
+            r[j] = midr[j] ? q[j] : r[j];
         }
     }
-    if (__any_sync(mask, any_l)) {
-        const double *mid = tab + (kQDeg + 1) * kQPieces;
-        double E[NJ], u[NJ], q[NJ];
-        int pc[NJ];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            E[j] = exp(-t[j]);
-            pc[j] = (x[j] >= kQBreak1) + (x[j] >= kQBreak2) + (x[j] >= kQBreak3);
-            u[j] = __dmul_rn(fmin(x[j], kQBreak4) - mid[pc[j]], mid[kQPieces + pc[j]]);
-            q[j] = tab[kQDeg * kQPieces + pc[j]];
-        }
-#pragma unroll
-        for (int k = kQDeg - 1; k >= 0; --k)
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], u[j], tab[k * kQPieces + pc[j]]);
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            double lv;
-            if (KIND == 2) {
-                lv = fma(-E[j], q[j], 1.0);
-            } else {
-                const double hx = __dmul_rn(0.5 * ix[j], ix[j]);
-                const double a = KIND == 0 ? 1.0 + hx : 1.0 - hx;
-                lv = fma(E[j], fma(-q[j], a, __dmul_rn(kInvSqrtPi, ix[j])), a);
-            }
-            if (!small[j]) r[j] = lv;
-        }
-    }
+    for (int j = 0; j < NJ; ++j)
+        if (huge[j]) r[j] = asymptote<KIND>(ix[j]);
 }
 
 }  // namespace special
