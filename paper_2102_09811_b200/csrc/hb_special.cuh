@@ -76,14 +76,15 @@ __device__ __forceinline__ double asymptote(double ix)
     return KIND == 0 ? 1.0 + hx : 1.0 - hx;
 }
 
-// middle-region piece and local variable (exact: x - mid is exact within a piece)
+// middle-region piece and local variable: y = (x - X0) / w, piece = floor(y),
+// u = 2 (y - piece) - 1 -- every step exact within a piece (w = 1/4), so u
+// equals (x - mid) / half exactly
 __device__ __forceinline__ int mid_piece(double x, double &u)
 {
-    const double pf = fmin(fmax(__dmul_rn(x - kX0, kMidInvW), 0.0), (double)(kMidPieces - 1));
-    const int pc = (int)pf;
-    const double mid = kX0 + ((double)pc + 0.5) * (1.0 / kMidInvW);
-    u = __dmul_rn(x - mid, kMidInvHalf);
-    return pc;
+    const double y = __dmul_rn(x - kX0, kMidInvW);
+    const double pf = fmin(fmax(floor(y), 0.0), (double)(kMidPieces - 1));
+    u = fma(2.0, y - pf, -1.0);
+    return __double2int_rz(pf);
 }
 
 // KIND 0: H (single layer), 1: F (double layer), 2: erf (hypersingular D2),
@@ -106,7 +107,9 @@ __device__ __forceinline__ double eval(double x, double ix, const double *__rest
         asm volatile("" : "+d"(q));
         r = midr ? q : r;
     }
-    if (huge) r = asymptote<KIND>(ix);
+    if (__any_sync(mask, huge)) {
+        if (huge) r = asymptote<KIND>(ix);
+    }
     return r;
 }
 
@@ -168,9 +171,14 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
             r[j] = midr[j] ? q[j] : r[j];
         }
     }
+    bool any_h = false;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
-        if (huge[j]) r[j] = asymptote<KIND>(ix[j]);
+    for (int j = 0; j < NJ; ++j) any_h |= huge[j];
+    if (__any_sync(mask, any_h)) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            if (huge[j]) r[j] = asymptote<KIND>(ix[j]);
+    }
 }
 
 }  // namespace special
