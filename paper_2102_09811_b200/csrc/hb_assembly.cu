@@ -48,6 +48,9 @@
 #ifndef HB_SEP
 #define HB_SEP 0     // separable p1 x p1 accumulation (slower at 128 registers; kept for study)
 #endif
+#ifndef HB_P1P1_GROUPED   // p1 x p1 through the G-point grouped loop (else one point per iteration)
+#define HB_P1P1_GROUPED 0
+#endif
 #ifndef HB_P1P1_MINB
 #define HB_P1P1_MINB HB_PAIR_MINB
 #endif
@@ -330,7 +333,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                         for (int c = 0; c < 3; ++c) inner[j][c] = fma(v, p[HOFF + c], inner[j][c]);
                     }
                 }
-            } else if constexpr (NIJ == 9) {
+            } else if constexpr (NIJ == 9 && !HB_P1P1_GROUPED) {
                 // p1 x p1: nine hat weights per point -- one point per iteration
                 for (int k = s; k < nloc4; k += 2) {
                     const bool ok = k < nloc;
