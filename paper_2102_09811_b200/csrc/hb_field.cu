@@ -24,6 +24,7 @@
 // kept: gap <= d_eps (first for the single layer), rho <= r_eps.
 // The sums keep the reference's order (m, then q, then e within a warp).
 #include <algorithm>
+#include <cstdlib>
 
 #include "hb_common.cuh"
 #include "hb_special.cuh"
@@ -165,6 +166,218 @@ __global__ void __launch_bounds__(kPotWarps * 32) k_potential(const PotArgs P)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tiled form for histories kmax <= 64 (config 4: every output time of 1e5
+// points).  With W = 2 area_e w_q, A_eq[k] = W dens[k] (0 for k >= E_t) and
+// B_eq[j] = W (dens[j-1] - dens[j]), the reference's sum is
+//     u(k) = sum_{m=0..k} S[k-m][m] + (cur ? U[k] : U0[k]),
+//     S[j][m] = sum_eq B_eq[j] G_eq[m],  U[k] = sum_eq A_eq[k] lim0_eq,
+//     U0[k] = sum_eq A_eq[k] G_eq[0]
+// (the m = 0 coefficient dens[k-1] - cur dens[k] is B[k] + (1 - cur) dens[k],
+// and the current-interval term adds cur dens[k] lim0).  S is a small GEMM
+// over the 36 864 (element, node) pairs: one CTA owns kTP points, stages the
+// density rows of kTC pairs once for all of them, evaluates their G values
+// into shared memory, and accumulates 4 x 4 register tiles of S (only the 153
+// tiles with j + m <= 64; (point, tile) items spread <= 2 per thread).  The
+// anti-diagonal sums are reduced in a fixed order: deterministic.
+constexpr int kTP = 3;                  // points per CTA
+#ifndef HB_POT_TC
+#define HB_POT_TC 16
+#endif
+#ifndef HB_POT_UNROLL
+#define HB_POT_UNROLL 4
+#endif
+constexpr int kTC = HB_POT_TC;          // (element, node) pairs per chunk
+constexpr int kTUnroll = HB_POT_UNROLL;
+constexpr int kTK = 68;                 // j, m in [0, 68): 17 tiles of 4
+constexpr int kTW = 85;                 // padded row: element m at m + m / 4 (chunks of 4 at a
+                                        // 40-byte stride -> tiles of a warp hit distinct banks)
+__device__ __forceinline__ int tpad(int m) { return m + (m >> 2); }
+constexpr int kNTile = 153;             // tiles (jt, mt), jt + mt <= 16
+constexpr int kTItems = kTP * kNTile;   // 459
+constexpr int kTThreads = 256;
+constexpr int kTMaxK = 64;
+
+// tiles enumerated jt-major (lanes of a warp mostly share the j-tile: the B
+// loads broadcast): id = off(jt) + mt, off(jt) = 17 jt - jt (jt - 1) / 2
+__device__ __forceinline__ int tile_off(int jt) { return 17 * jt - jt * (jt - 1) / 2; }
+__device__ __forceinline__ void tile_of(int t, int &jt, int &mt)
+{
+    jt = 0;
+    while (tile_off(jt + 1) <= t) ++jt;
+    mt = t - tile_off(jt);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kTThreads, 2) k_potential_tiles(const PotArgs P)
+{
+    extern __shared__ __align__(16) double tsm[];
+    double *tab = tsm;
+    double *As = tab + special::kTabDoubles;          // [kTC][kTW]
+    double *Bs = As + kTC * kTW;                      // [kTC][kTW]
+    double *Gs = Bs + kTC * kTW;                      // [kTP][kTC][kTW]; later T [kTItems][7]
+    double *Ls = Gs + kTP * kTC * kTW;                // [kTP][kTC]
+    double *Cm = Ls + kTP * kTC;                      // [kTP][kTK]: 1 / (2 sqrt(a (m h + eps)))
+    double *Gq = Cm + kTP * kTK;                      // [kTP][kTC][2]: rho
+    double *Rs = Gq + kTP * kTC * 2;                  // [3][kTP][65]: R, U, U0
+    special::load_table<KIND == 0 ? 2 : 3>(tab);
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t g0 = (int64_t)blockIdx.x * kTP;
+    const int64_t EQ = P.E_x * P.nq;
+    double px[kTP], py[kTP], pz[kTP];
+    int kmax = 0;
+#pragma unroll
+    for (int p = 0; p < kTP; ++p) {
+        const int64_t g = min(g0 + p, P.n_groups - 1);
+        px[p] = P.gx[3 * g]; py[p] = P.gx[3 * g + 1]; pz[p] = P.gx[3 * g + 2];
+        if (g0 + p < P.n_groups) kmax = max(kmax, (int)P.k[P.gptr[g + 1] - 1]);
+    }
+    for (int i = tid; i < kTP * kTK; i += kTThreads) {
+        const int p = i / kTK, m = i % kTK;
+        const int64_t g = min(g0 + p, P.n_groups - 1);
+        Cm[i] = 1.0 / (2.0 * sqrt(P.alpha * ((double)m * P.step + P.geps[g])));
+    }
+    // this thread's (point, tile) items
+    int it_p[2], it_j[2], it_m[2];
+    bool it_ok[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int item = tid + r * kTThreads;
+        it_ok[r] = item < kTItems;
+        const int ii = it_ok[r] ? item : 0;
+        int jt, mt;
+        tile_of(ii % kNTile, jt, mt);
+        it_p[r] = ii / kNTile;
+        it_j[r] = 4 * jt;
+        it_m[r] = 4 * mt;
+    }
+    double acc[2][16];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc[r][c] = 0.0;
+    const bool xt = tid < kTP * 65;       // X-term cell (p, k)
+    const int xp = xt ? tid / 65 : 0, xk = xt ? tid % 65 : 0;
+    double U = 0.0, U0 = 0.0;
+    const double inv4pi = 0.25 * kInvPi;
+    constexpr int kEvalIters = (kTP * kTC * kTK + kTThreads - 1) / kTThreads;
+    for (int64_t eq0 = 0; eq0 < EQ; eq0 += kTC) {
+        __syncthreads();   // previous chunk fully consumed
+        for (int i = tid; i < kTC * kTK; i += kTThreads) {
+            const int el = i / kTK, kk = i % kTK;
+            const int64_t eq = eq0 + el;
+            double a = 0.0, am = 0.0, W = 0.0;
+            if (eq < EQ) {
+                const double *dq = P.dens_t + eq * P.E_t;
+                W = 2.0 * __ldg(P.areas + eq / P.nq) * __ldg(P.qw + eq % P.nq);
+                if (kk < P.E_t) a = __ldg(dq + kk);
+                if (kk >= 1 && kk - 1 < P.E_t) am = __ldg(dq + kk - 1);
+            }
+            As[el * kTW + tpad(kk)] = W * a;
+            Bs[el * kTW + tpad(kk)] = W * (am - a);
+        }
+        if (tid < kTP * kTC) {   // per (point, pair): rho and the gap-independent factor lim0
+            const int p = tid / kTC, el = tid % kTC;
+            const int64_t eq = eq0 + el;
+            const int64_t e = eq < EQ ? eq / P.nq : 0, eqc = eq < EQ ? eq : 0;
+            const double rx = (p == 0 ? px[0] : p == 1 ? px[1] : px[2]) - P.qpts[3 * eqc];
+            const double ry = (p == 0 ? py[0] : p == 1 ? py[1] : py[2]) - P.qpts[3 * eqc + 1];
+            const double rz = (p == 0 ? pz[0] : p == 1 ? pz[1] : pz[2]) - P.qpts[3 * eqc + 2];
+            const double rho = sqrt(rx * rx + ry * ry + rz * rz);
+            const double rn = rx * P.normals[3 * e] + ry * P.normals[3 * e + 1] + rz * P.normals[3 * e + 2];
+            const bool rsmall = rho <= P.r_eps;
+            const double lim0 = KIND == 0 ? 1.0 / (4.0 * kPi * P.alpha * rho)
+                                          : (rsmall ? 0.0 : inv4pi * rn / (rho * rho * rho));
+            Gq[tid * 2] = rho;
+            Ls[tid] = eq < EQ ? lim0 : 0.0;
+        }
+        __syncthreads();
+        // kernel values G(rho, m h + eps) for kTP points x kTC pairs x m < kTK
+        // (uniform trip count: every lane takes part in the warp votes)
+#pragma unroll 1
+        for (int r = 0; r < kEvalIters; ++r) {
+            const int i = tid + r * kTThreads;
+            const bool ok = i < kTP * kTC * kTK;
+            const int ic = ok ? i : 0;
+            const int p = ic / (kTC * kTK), el = (ic / kTK) % kTC, m = ic % kTK;
+            const double rho = Gq[(p * kTC + el) * 2];
+            const bool rsmall = rho <= P.r_eps;
+            const double lim0 = Ls[p * kTC + el];
+            const int64_t g = min(g0 + p, P.n_groups - 1);
+            const double gap = (double)m * P.step + P.geps[g];
+            const double x = __dmul_rn(rho, Cm[p * kTK + m]);
+            const double f = special::eval<KIND == 0 ? 2 : 3>(x, 0.0, tab, kFull);
+            double gv;
+            if (gap <= P.d_eps) gv = lim0;
+            else if (rsmall) gv = KIND == 0 ? 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (P.alpha * P.alpha * P.alpha) * gap)) : 0.0;
+            else gv = __dmul_rn(lim0, f);
+            if (ok) Gs[(p * kTC + el) * kTW + tpad(m)] = (m <= kmax && eq0 + el < EQ) ? gv : 0.0;
+        }
+        __syncthreads();
+#pragma unroll kTUnroll
+        for (int el = 0; el < kTC; ++el) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                if (!it_ok[r]) continue;
+                const double *b = Bs + el * kTW + tpad(it_j[r]);
+                const double *gg = Gs + (it_p[r] * kTC + el) * kTW + tpad(it_m[r]);
+                const double b0 = b[0], b1 = b[1], b2 = b[2], b3 = b[3];
+                const double gv[4] = {gg[0], gg[1], gg[2], gg[3]};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    acc[r][0 * 4 + c] = fma(b0, gv[c], acc[r][0 * 4 + c]);
+                    acc[r][1 * 4 + c] = fma(b1, gv[c], acc[r][1 * 4 + c]);
+                    acc[r][2 * 4 + c] = fma(b2, gv[c], acc[r][2 * 4 + c]);
+                    acc[r][3 * 4 + c] = fma(b3, gv[c], acc[r][3 * 4 + c]);
+                }
+            }
+            if (xt) {
+                const double a = As[el * kTW + tpad(xk)];
+                U = fma(a, Ls[xp * kTC + el], U);
+                U0 = fma(a, Gs[(xp * kTC + el) * kTW], U0);
+            }
+        }
+    }
+    __syncthreads();
+    // anti-diagonal partial sums of each item: T[item][d], d = a + b (a ascending)
+    double *T = Gs;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        if (!it_ok[r]) continue;
+        const int item = tid + r * kTThreads;
+#pragma unroll
+        for (int d = 0; d < 7; ++d) {
+            double sdg = 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int bcol = d - a;
+                if (bcol >= 0 && bcol < 4) sdg += acc[r][a * 4 + bcol];
+            }
+            T[item * 7 + d] = sdg;
+        }
+    }
+    __syncthreads();
+    if (xt) {   // R[p][k]: tiles of anti-diagonal band s = jt + mt with 4s <= k <= 4s + 6
+        double R = 0.0;
+        for (int sd = max(0, (xk - 6 + 3) / 4); sd <= min(16, xk / 4); ++sd)
+            for (int jt = 0; jt <= sd; ++jt) R += T[(xp * kNTile + tile_off(jt) + (sd - jt)) * 7 + (xk - 4 * sd)];
+        Rs[xp * 65 + xk] = R;
+        Rs[kTP * 65 + xp * 65 + xk] = U;
+        Rs[2 * kTP * 65 + xp * 65 + xk] = U0;
+    }
+    __syncthreads();
+    for (int p = 0; p < kTP; ++p) {
+        const int64_t g = g0 + p;
+        if (g >= P.n_groups) break;
+        for (int64_t o = P.gptr[g] + tid; o < P.gptr[g + 1]; o += kTThreads) {
+            const int k = (int)P.k[o];
+            const bool cu = P.cur[o] != 0;
+            P.out[P.out_idx[o]] = Rs[p * 65 + k] + Rs[(cu ? 1 : 2) * kTP * 65 + p * 65 + k];
+        }
+    }
+    (void)lane;
+}
+
 }  // namespace hb
 
 using namespace hb;
@@ -188,6 +401,14 @@ extern "C" int hb_potential(int kind, int64_t n_groups, int64_t E_t, int64_t E_x
     P.gx = gx_dev; P.geps = geps_dev; P.gptr = gptr_dev; P.k = k_dev; P.cur = cur_dev; P.out_idx = out_idx_dev;
     P.dens_t = dens_t_dev; P.qpts = qpts_dev; P.qw = qw_dev; P.areas = areas_dev; P.normals = normals_dev;
     P.step = step; P.alpha = alpha; P.d_eps = d_eps; P.r_eps = r_eps; P.out = out_dev;
+    if (kmax <= kTMaxK && !getenv("HB_POT_GENERAL")) {   // tiled form (config 4 and shorter histories)
+        const size_t sm = sizeof(double) * (special::kTabDoubles + 2 * kTC * kTW + kTP * kTC * kTW + kTP * kTC +
+                                            kTP * kTK + kTP * kTC * 2 + 3 * kTP * 65);
+        auto kern = kind == 0 ? k_potential_tiles<0> : k_potential_tiles<1>;
+        if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kern<<<(unsigned)cdiv(n_groups, kTP), kTThreads, sm, (cudaStream_t)stream>>>(P);
+        return cuda_check(cudaGetLastError(), "hb_potential");
+    }
     P.kcap = (int)((kmax / 32 + 1) * 32);
     const size_t sm = (special::kTabDoubles + (size_t)kPotWarps * kOut + (size_t)kPotWarps * 4 * P.kcap) * sizeof(double);
     if (sm > 220 * 1024) { set_error("hb_potential: time history too long (%lld)", (long long)kmax); return HB_ERR_INVALID; }
