@@ -10,9 +10,13 @@ K' is the blockwise-transposed view, not re-counted) and D = D2 + curl(V)
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
 
 N > 1 runs one process per GPU (torchrun); ranks own contiguous ranges of
-time-difference blocks d (no data-path collective: block d depends only on
-the kernel at gaps d-1, d, d+1), value = all ranks' entries / max-over-ranks
-device time.  ``--impl reference`` times the reference's CPU algorithm (the
+time-difference blocks d.  With --parallel rows (default) the V and K pair
+work is split by balanced test-row ranges over all blocks and the finalize
+kernels store every block into its owner's shard through NVLink peer
+pointers (CUDA IPC; no halo gaps, no data-path collective), D2 and the curl
+combine stay d-local after a one-element all-reduce fence; --parallel d
+splits everything by d (block d depends only on the kernel at gaps d-1, d,
+d+1).  value = all ranks' entries / max-over-ranks device time.  ``--impl reference`` times the reference's CPU algorithm (the
 oracle port, oracle/heatbem_oracle.c, all host threads) on rank 0.
 """
 from __future__ import annotations
@@ -224,15 +228,36 @@ def run_native(args, rank, world, local_rank):
     outD = torch.empty((nb, N, N), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     tabs = hbdev.device_tables(mesh, q, dev)
+    rows_mode = world > 1 and args.parallel == "rows"
+    if rows_mode:
+        # V and K: pair work split by balanced test-row ranges over ALL blocks,
+        # stores into the d-owner's shard over NVLink (peer pointers); D2 and the
+        # curl combine stay d-local (they accumulate over rows / read local V)
+        from paper_2102_09811_b200 import distributed as Dm
+
+        peersV = Dm.PeerShardTable(outV, d0, d1, tg.n_steps)
+        peersK = Dm.PeerShardTable(outK, d0, d1, tg.n_steps)
+        rowsV = Dm.row_partition(Dm.row_weights(E, True), world)[rank]
+        rowsK = Dm.row_partition(Dm.row_weights(E, False), world)[rank]
+        fence = torch.zeros(1, dtype=torch.float64, device=dev)
+        dist.barrier()
 
     def step(stats=None):
         st = stats if stats is not None else [None, None, None]
-        _assemble_operator(0, False, False, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outV,
-                           stats=st[0])
-        _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(d0, d1), out=outK,
-                           stats=st[1])
+        if rows_mode:
+            _assemble_operator(0, False, False, True, mesh, tg, params, q, None, d_range=(0, tg.n_steps),
+                               row_range=rowsV, block_ptrs=peersV.table, stats=st[0])
+            _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(0, tg.n_steps),
+                               row_range=rowsK, block_ptrs=peersK.table, stats=st[1])
+        else:
+            _assemble_operator(0, False, False, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outV,
+                               stats=st[0])
+            _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(d0, d1), out=outK,
+                               stats=st[1])
         _assemble_operator(2, True, True, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outD,
                            stats=st[2])
+        if rows_mode:
+            dist.all_reduce(fence)   # device-side fence: every rank's V stores into this shard are done
         curl_combine_into(tabs, outV, outD, outD, params.alpha)
 
     for _ in range(max(3, args.warmup)):
@@ -273,6 +298,11 @@ def run_native(args, rank, world, local_rank):
     n_entries = entries_total(mesh, tg.n_steps)   # all ranks together
     value = n_entries / (ms_per_step * 1e-3)
 
+    if rows_mode:
+        dist.barrier()
+        peersV.close()
+        peersK.close()
+
     # ---- e2e: public API, host buffers, copies inside the timed region ----
     Hpin = hbdev.pin_host_tables(hbdev.host_tables(mesh, q))
     pinV = torch.empty(outV.shape, dtype=torch.float64).pin_memory()
@@ -309,16 +339,18 @@ def run_native(args, rank, world, local_rank):
     d2h = (pinV.numel() + pinK.numel() + pinD.numel()) * 8
 
     # ---- roofline of the dominant kernel: the K pair kernel (k_pairs<1,...>) ----
-    it_lo, it_hi = max(1, d0 - 1), d1
+    kd0, kd1 = (0, tg.n_steps) if rows_mode else (d0, d1)
+    it_lo, it_hi = max(1, kd0 - 1), kd1
     n_windows = 0
-    dd = d0
-    while dd < d1:   # windows of <= 32 gap slots (csrc/hb_assembly.cu)
-        nd1 = min(d1, 32 if dd <= 1 else dd + 30)
+    dd = kd0
+    while dd < kd1:   # windows of <= 32 gap slots (csrc/hb_assembly.cu)
+        nd1 = min(kd1, 32 if dd <= 1 else dd + 30)
         n_windows += 1
         dd = nd1
     wK = workload.operator_work(mesh, "K", 1, q)
     gapsK = (it_hi - it_lo + 1) + 2 * (n_windows - 1)
-    flops_per_call = wK["flops"] * gapsK           # one call = n_windows launches
+    row_frac = (rowsK[1] - rowsK[0]) / E if rows_mode else 1.0
+    flops_per_call = wK["flops"] * gapsK * row_frac   # one call = n_windows launches
     sK = stats[1]
     pair_ms_per_call = sK.pair_ms / max(1, args.steps // 2)
     launches_per_call = sK.pair_launches / max(1, args.steps // 2)
@@ -348,7 +380,9 @@ def run_native(args, rank, world, local_rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: BASELINE config-2 mesh and time grid generated in-run (no dataset)",
         "config": {"workload": WORKLOAD, "E_x": E, "N_x": N, "E_t": tg.n_steps, "entries_per_step": n_entries,
-                   "parallelism": f"d-sharded x{world} (contiguous time-difference blocks per rank)",
+                   "parallelism": (f"x{world}: V/K pair work split by balanced test-row ranges, blocks stored "
+                                   "into the d-owner's shard over NVLink peer memory; D2 + curl d-sharded")
+                   if rows_mode else f"d-sharded x{world} (contiguous time-difference blocks per rank)",
                    "l2": "flushed between timed steps (256 MiB device write, outside the events)",
                    "fp64_peak_tflops": peak, "pair_kernel_share": shares},
         "roofline": {"bound": "fp64", "kernel": "k_pairs<op=K> (double-layer pair kernel)",
@@ -378,6 +412,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("native", "reference"), default="native")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallel", choices=("rows", "d"), default="rows",
+                    help="N > 1: split V/K pair work by test rows (peer stores) or everything by d")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -112,6 +112,17 @@ typedef struct {
     void *workspace_dev;            /* staging, >= hb_assemble_min_workspace */
     size_t workspace_bytes;
     hb_assembly_stats *stats;       /* optional (NULL: no timing, no sync)  */
+    /* Row-parallel assembly.  Test rows [row_begin, row_end)
+     * only (row_end <= row_begin: all rows); with block_ptrs_dev != NULL
+     * (device array of d_end - d_begin pointers) block d is written at
+     * block_ptrs_dev[d - d_begin] -- e.g. the d-owner's memory on another
+     * GPU (CUDA IPC, hb_ipc_*) -- instead of blocks_dev.  Every entry of a
+     * block is written by exactly one row range (V: direct and mirrored
+     * entries of its rows), so ranks splitting the rows fill the d-sharded
+     * blocks bitwise as one GPU would.  p1 x p1 operators accumulate over
+     * rows: full range and contiguous blocks only. */
+    int64_t row_begin, row_end;
+    double *const *block_ptrs_dev;
 } hb_assembly_desc;
 
 /* bytes of staging for one test-row chunk (the minimum) and for all rows */
@@ -122,6 +133,15 @@ size_t hb_assemble_full_workspace(const hb_mesh_desc *mesh, const hb_assembly_de
  * blocks_dev; results are bitwise deterministic run to run and independent
  * of d_begin/d_end (so d-sharded ranks reproduce the 1-GPU blocks). */
 int hb_assemble(const hb_mesh_desc *mesh, const hb_assembly_desc *a, void *stream);
+
+/* CUDA IPC for row-parallel assembly: export a device pointer (anywhere
+ * inside an allocation) as a 64-byte handle of its allocation plus the byte
+ * offset; import opens the handle in this process (peer access enabled
+ * lazily) and returns the pointer; close releases an imported allocation
+ * (pass the pointer import returned). */
+int hb_ipc_export(const void *ptr_dev, void *handle64, int64_t *offset);
+int hb_ipc_import(const void *handle64, int64_t offset, void **ptr_dev);
+int hb_ipc_close(void *ptr_dev, int64_t offset);
 
 /* Pair classes exactly as the assembly kernels see them, for test rows
  * [e0, e1) and every trial element: out[(e-e0)*E_x + f] = 0 separated far,

@@ -60,6 +60,7 @@ class AssemblyDesc(ctypes.Structure):
         ("d_begin", _I64), ("d_end", _I64),
         ("blocks_dev", _P), ("workspace_dev", _P), ("workspace_bytes", ctypes.c_size_t),
         ("stats", ctypes.POINTER(AssemblyStats)),
+        ("row_begin", _I64), ("row_end", _I64), ("block_ptrs_dev", _P),
     ]
 
 
@@ -68,7 +69,7 @@ EXPORTED = (
     "hb_version", "hb_last_error", "hb_assemble", "hb_assemble_min_workspace",
     "hb_assemble_full_workspace", "hb_curl_combine", "hb_potential",
     "hb_toeplitz_apply", "hb_forward_subst_step", "hb_fp64_probe", "hb_pair_classes",
-    "hb_toeplitz_apply_range", "hb_curl_workspace",
+    "hb_toeplitz_apply_range", "hb_curl_workspace", "hb_ipc_export", "hb_ipc_import", "hb_ipc_close",
 )
 
 _lib = None
@@ -107,6 +108,9 @@ def load():
     L.hb_pair_classes.argtypes = [ctypes.POINTER(MeshDesc), _I64, _I64, _P, _P]
     L.hb_pair_classes.restype = _INT
     L.hb_fp64_probe.argtypes = [_I64, _I64, _P, _P]
+    L.hb_ipc_export.argtypes = [_P, _P, ctypes.POINTER(_I64)]
+    L.hb_ipc_import.argtypes = [_P, _I64, ctypes.POINTER(_P)]
+    L.hb_ipc_close.argtypes = [_P, _I64]
     L.hb_fp64_probe.restype = _INT
     _lib = L
     return L

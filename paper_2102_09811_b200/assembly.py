@@ -199,7 +199,12 @@ def _workspace(tables, desc_m, desc_a, device, cap):
 
 def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, mesh, timegrid,
                        params: KernelParams, config: QuadratureConfig, instrumentation,
-                       d_range=None, device=None, workspace_bytes=None, stream=None, stats=None, out=None):
+                       d_range=None, device=None, workspace_bytes=None, stream=None, stats=None, out=None,
+                       row_range=None, block_ptrs=None):
+    """Blocks [d0, d1) of one operator.  ``row_range`` restricts the test rows
+    and ``block_ptrs`` (int64 device tensor of d1 - d0 addresses) redirects
+    block d to block_ptrs[d - d0] (row-parallel assembly, distributed.py);
+    with ``block_ptrs`` nothing is allocated and None is returned."""
     import torch
 
     _native.require_cuda()
@@ -212,7 +217,13 @@ def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, 
     R = N_x if test_p1 else E_x
     C = N_x if trial_p1 else E_x
     dev = tabs.device
-    if out is not None:
+    if block_ptrs is not None:
+        if out is not None:
+            raise ValueError("out and block_ptrs are exclusive")
+        if tuple(block_ptrs.shape) != (d1 - d0,) or block_ptrs.dtype != torch.int64 or block_ptrs.device != dev:
+            raise ValueError("block_ptrs must be an int64 device tensor with one address per block")
+        blocks = None
+    elif out is not None:
         if tuple(out.shape) != (d1 - d0, R, C) or out.dtype != torch.float64 or not out.is_contiguous():
             raise ValueError("out must be a contiguous float64 tensor of shape (n_blocks, R, C)")
         blocks = out
@@ -223,7 +234,14 @@ def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, 
     a.E_t, a.step = E_t, timegrid.step
     a.alpha, a.d_eps, a.r_eps = params.alpha, params.delta_eps, params.rho_eps
     a.d_begin, a.d_end = d0, d1
-    a.blocks_dev = blocks.data_ptr()
+    a.blocks_dev = blocks.data_ptr() if blocks is not None else None
+    if block_ptrs is not None:
+        a.block_ptrs_dev = block_ptrs.data_ptr()
+    if row_range is not None:
+        r0, r1 = int(row_range[0]), int(row_range[1])
+        if not (0 <= r0 < r1 <= E_x):
+            raise ValueError(f"row_range {row_range} outside [0, {E_x}]")
+        a.row_begin, a.row_end = r0, r1
     m = tabs.desc(symmetric)
     ws = _workspace(tabs, m, a, dev, _DEFAULT_WS_CAP if workspace_bytes is None else int(workspace_bytes))
     a.workspace_dev, a.workspace_bytes = ws.data_ptr(), ws.numel()

@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_
 struct FinArgs {
     const double *Q;
     double *out;          // blocks_dev, block (d - d_begin) at out + (d - d_begin) R C
+    double *const *bptr;  // optional per-block destinations (row-parallel: the d-owner's memory)
     int64_t E_x, N_x, R, C, e0, e1;
     int d0, nd, d_begin;
     const int64_t *star_indptr, *star_elem, *star_local, *tri_nodes;
@@ -720,6 +721,13 @@ struct FinArgs {
     const int64_t *tile_eptr, *tile_elem;   // curl tile plan (32-node tiles)
     const int32_t *star_pos;
 };
+
+// destination of block d - d_begin = b: the caller's per-block pointer (another
+// GPU's memory over NVLink in a row-parallel run) or the contiguous blocks
+__device__ __forceinline__ double *fin_block(const FinArgs &F, int64_t b)
+{
+    return F.bptr ? F.bptr[b] : F.out + b * F.R * F.C;
+}
 
 // V (p0 x p0, symmetric): tile of 4 rows x 32 columns x 32 blocks through smem;
 // direct rows coalesced over f, mirror rows in 32-byte runs over e.
@@ -743,7 +751,7 @@ __global__ void __launch_bounds__(256) k_fin_p0p0(const FinArgs F)
             const int64_t e = eb + el, f = f0 + fl;
             if (e < F.e1 && f < F.E_x && f >= e && dl < ndc) {
                 const int64_t b = F.d0 + dc + dl - F.d_begin;
-                F.out[(b * F.R + e) * F.C + f] = tile[el][fl][dl];
+                fin_block(F, b)[e * F.C + f] = tile[el][fl][dl];
             }
         }
         for (int idx = tid; idx < 4 * 32 * 32; idx += 256) {
@@ -751,7 +759,7 @@ __global__ void __launch_bounds__(256) k_fin_p0p0(const FinArgs F)
             const int64_t e = eb + el, f = f0 + fl;
             if (e < F.e1 && f < F.E_x && f > e && dl < ndc) {
                 const int64_t b = F.d0 + dc + dl - F.d_begin;
-                F.out[(b * F.R + f) * F.C + e] = tile[el][fl][dl];
+                fin_block(F, b)[f * F.C + e] = tile[el][fl][dl];
             }
         }
         __syncthreads();
@@ -784,7 +792,7 @@ __global__ void __launch_bounds__(256) k_fin_p0p1(const FinArgs F)
             const int64_t n = n0 + lane;
             if (n < F.N_x) {
                 const int64_t b = F.d0 + dc + dl - F.d_begin;
-                F.out[(b * F.R + e) * F.C + n] = tile[lane][dl];
+                fin_block(F, b)[e * F.C + n] = tile[lane][dl];
             }
         }
         __syncthreads();
@@ -1075,9 +1083,20 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
         return HB_ERR_UNSUPPORTED;
     }
     if (a->E_t < 1 || a->d_begin < 0 || a->d_end > a->E_t || a->d_begin >= a->d_end || m->E_x < 1 ||
-        m->N_x < 3 || !a->blocks_dev || !(a->step > 0) || !(a->alpha > 0)) {
+        m->N_x < 3 || !(a->step > 0) || !(a->alpha > 0)) {
         set_error("hb_assemble: invalid sizes or parameters (E_t=%lld d=[%lld,%lld) E_x=%lld)",
                   (long long)a->E_t, (long long)a->d_begin, (long long)a->d_end, (long long)m->E_x);
+        return HB_ERR_INVALID;
+    }
+    const int64_t r0 = a->row_end > a->row_begin ? a->row_begin : 0;
+    const int64_t r1 = a->row_end > a->row_begin ? a->row_end : m->E_x;
+    if (r0 < 0 || r1 > m->E_x || (a->test_p1 && a->trial_p1 && (r0 != 0 || r1 != m->E_x || a->block_ptrs_dev))) {
+        set_error("hb_assemble: bad test-row range [%lld, %lld) (p1 x p1 operators accumulate over rows: "
+                  "full range and contiguous blocks only)", (long long)r0, (long long)r1);
+        return HB_ERR_INVALID;
+    }
+    if (!a->blocks_dev && !a->block_ptrs_dev) {
+        set_error("hb_assemble: no output (blocks_dev and block_ptrs_dev are NULL)");
         return HB_ERR_INVALID;
     }
     if (a->test_p1 && a->trial_p1 &&
@@ -1133,8 +1152,8 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
         A.need_special = d0 <= 1;
         // a short (tail) window needs only the lanes-x-slots its gaps occupy
         const int nj_w = std::min(nj, (int)cdiv(A.it_hi - A.it_lo + 1, 16));
-        for (int64_t e0 = 0; e0 < m->E_x; e0 += rows_per_chunk) {
-            const int64_t e1 = std::min(m->E_x, e0 + rows_per_chunk);
+        for (int64_t e0 = r0; e0 < r1; e0 += rows_per_chunk) {
+            const int64_t e1 = std::min(r1, e0 + rows_per_chunk);
             A.e0 = e0;
             A.e1 = e1;
             cudaEvent_t ev = LT.begin(st);
@@ -1147,6 +1166,7 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
             FinArgs F{};
             F.Q = A.Q;
             F.out = a->blocks_dev;
+            F.bptr = a->block_ptrs_dev;
             F.E_x = m->E_x; F.N_x = m->N_x; F.R = R; F.C = C; F.e0 = e0; F.e1 = e1;
             F.d0 = (int)d0; F.nd = A.nd; F.d_begin = (int)a->d_begin;
             F.star_indptr = m->star_indptr_dev; F.star_elem = m->star_elem_dev;

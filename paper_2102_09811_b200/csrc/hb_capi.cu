@@ -272,3 +272,62 @@ extern "C" int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, doubl
     k_curl_tile<<<dim3((unsigned)npairs, (unsigned)gy), 256, smem, (cudaStream_t)stream>>>(C);
     return cuda_check(cudaGetLastError(), "hb_curl_combine");
 }
+
+// ---------------------------------------------------------------------------
+// CUDA IPC for row-parallel assembly (peer d-shard buffers)
+// ---------------------------------------------------------------------------
+#include <cuda.h>
+#include <cstring>
+
+namespace {
+typedef CUresult (*PFN_ptrAttr)(void *, CUpointer_attribute, CUdeviceptr);
+PFN_ptrAttr ptr_attr_fn()
+{
+    static PFN_ptrAttr fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuPointerGetAttribute", &p, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = (PFN_ptrAttr)p;
+    }
+    return fn;
+}
+}  // namespace
+
+extern "C" int hb_ipc_export(const void *ptr_dev, void *handle64, int64_t *offset)
+{
+    if (!ptr_dev || !handle64 || !offset) { set_error("hb_ipc_export: bad arguments"); return HB_ERR_INVALID; }
+    PFN_ptrAttr fn = ptr_attr_fn();
+    if (!fn) { set_error("hb_ipc_export: cuPointerGetAttribute unavailable"); return HB_ERR_CUDA; }
+    CUdeviceptr base = 0;
+    if (fn(&base, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, (CUdeviceptr)ptr_dev) != CUDA_SUCCESS) {
+        set_error("hb_ipc_export: not a device allocation");
+        return HB_ERR_INVALID;
+    }
+    cudaIpcMemHandle_t h;
+    int rc = cuda_check(cudaIpcGetMemHandle(&h, (void *)base), "cudaIpcGetMemHandle");
+    if (rc) return rc;
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle64, &h, sizeof(h));
+    *offset = (int64_t)((CUdeviceptr)ptr_dev - base);
+    return HB_OK;
+}
+
+extern "C" int hb_ipc_import(const void *handle64, int64_t offset, void **ptr_dev)
+{
+    if (!handle64 || !ptr_dev || offset < 0) { set_error("hb_ipc_import: bad arguments"); return HB_ERR_INVALID; }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    void *base = nullptr;
+    int rc = cuda_check(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    if (rc) return rc;
+    *ptr_dev = (char *)base + offset;
+    return HB_OK;
+}
+
+extern "C" int hb_ipc_close(void *ptr_dev, int64_t offset)
+{
+    if (!ptr_dev) { set_error("hb_ipc_close: bad arguments"); return HB_ERR_INVALID; }
+    return cuda_check(cudaIpcCloseMemHandle((char *)ptr_dev - offset), "cudaIpcCloseMemHandle");
+}

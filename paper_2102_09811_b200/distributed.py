@@ -1,5 +1,6 @@
 """Multi-GPU layout: one process per GPU, operators sharded by time-difference
-block d.
+block d; pair work split by d (halo gaps) or by test rows
+(``assemble_row_parallel``: peer stores into the d-owners' shards).
 
 Block d of every operator depends only on the kernel at the three gaps
 d-1, d, d+1, so rank r assembles the contiguous range [d0_r, d1_r) with no
@@ -63,6 +64,131 @@ def aligned_chunks(n_blocks: int, max_blocks: int):
     if lo < n_blocks:
         out.append((lo, n_blocks))
     return out
+
+
+def row_weights(n_rows: int, symmetric: bool):
+    """Pair-kernel work per test row: symmetric operators evaluate the upper
+    triangle (row e: n_rows - e trial elements), the others every pair."""
+    e = np.arange(n_rows, dtype=np.float64)
+    return (n_rows - e) if symmetric else np.full(n_rows, float(n_rows))
+
+
+def row_partition(weights, world: int):
+    """Contiguous test-row ranges of near-equal total weight, one per rank."""
+    w = np.asarray(weights, dtype=np.float64)
+    c = np.concatenate([[0.0], np.cumsum(w)])
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(max(cuts[-1], int(np.searchsorted(c, c[-1] * r / world, side="left"))))
+    cuts.append(len(w))
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def block_pointer_table(shards, n_blocks: int, block_bytes: int):
+    """Address of every block d in [0, n_blocks) given, per rank, (base
+    address, d0, d1) of its contiguous d-shard: base_r + (d - d0_r) bytes."""
+    table = np.zeros(n_blocks, dtype=np.int64)
+    seen = np.zeros(n_blocks, dtype=bool)
+    for base, d0, d1 in shards:
+        for d in range(d0, d1):
+            if seen[d]:
+                raise ValueError(f"block {d} owned twice")
+            seen[d] = True
+            table[d] = int(base) + (d - d0) * block_bytes
+    if not seen.all():
+        raise ValueError("blocks without an owner")
+    return table
+
+
+def exchange_shard_meta(meta, group=None):
+    """All ranks' (ipc handle, offset, d0, d1) -- one all_gather_object."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        return [meta]
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, meta, group=group)
+    return out
+
+
+class PeerShardTable:
+    """Per-block addresses of a d-sharded operator across ranks: every rank
+    exports its shard (CUDA IPC, hb_ipc_export), the metadata is all-gathered
+    and peer shards are mapped (hb_ipc_import, peer access over NVLink).
+    ``table`` (int64 device tensor, one address per block d) is what the
+    row-parallel finalize kernels store through.  ``close()`` unmaps."""
+
+    def __init__(self, local, d0: int, d1: int, n_blocks: int, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        self._L = _native.load()
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        block_bytes = int(local[0].numel()) * 8 if local.shape[0] else 0
+        h = (ctypes.c_char * 64)()
+        off = ctypes.c_int64()
+        _native.call("hb_ipc_export", local.data_ptr(), h, ctypes.byref(off))
+        metas = exchange_shard_meta((bytes(h), off.value, d0, d1), group)
+        bases, self._opened = [], []
+        for r, (hr, o, a, b) in enumerate(metas):
+            if r == rank:
+                bases.append((local.data_ptr(), a, b))
+                continue
+            p = ctypes.c_void_p()
+            _native.call("hb_ipc_import", hr, o, ctypes.byref(p))
+            self._opened.append((p.value, o))
+            bases.append((p.value, a, b))
+        self.table = torch.as_tensor(block_pointer_table(bases, n_blocks, block_bytes), device=local.device)
+
+    def close(self):
+        for pv, o in self._opened:
+            self._L.hb_ipc_close(pv, o)
+        self._opened = []
+
+
+def assemble_row_parallel(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, mesh, timegrid, params,
+                          config, group=None, workspace_bytes=None):
+    """Row-parallel assembly with d-sharded storage: rank r
+    evaluates the pairs of a balanced test-row range for ALL blocks and the
+    finalize kernels store each block straight into the memory of the rank
+    that owns it (CUDA IPC peer pointers over NVLink; block_range split).
+    No halo gaps and no collective on the data path; every entry is written
+    by exactly one rank, so the shards are bitwise equal to the 1-GPU blocks.
+    p0 x p0 and p0 x p1 only (p1 x p1 accumulates over rows: use d-sharding)."""
+    import torch
+    import torch.distributed as dist
+
+    from .assembly import _assemble_operator
+
+    if test_p1 and trial_p1:
+        raise ValueError("row-parallel assembly needs p0 test functions (p1 x p1 accumulates over rows)")
+    E_t = timegrid.n_steps
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    E_x, N_x = mesh.n_triangles, mesh.n_vertices
+    R, C = (N_x if test_p1 else E_x), (N_x if trial_p1 else E_x)
+    d0, d1 = block_range(rank, world, E_t)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    local = torch.empty((d1 - d0, R, C), dtype=torch.float64, device=dev)
+    if world == 1:
+        _assemble_operator(op, test_p1, trial_p1, symmetric, mesh, timegrid, params, config, None,
+                           d_range=(0, E_t), out=local, workspace_bytes=workspace_bytes)
+        return ShardedToeplitz(local, d0, d1, E_t, group)
+    peers = PeerShardTable(local, d0, d1, E_t, group)
+    rows = row_partition(row_weights(E_x, symmetric), world)[rank]
+    dist.barrier(group)                      # every shard allocated and mapped
+    try:
+        if rows[1] > rows[0]:
+            _assemble_operator(op, test_p1, trial_p1, symmetric, mesh, timegrid, params, config, None,
+                               d_range=(0, E_t), row_range=rows, block_ptrs=peers.table,
+                               workspace_bytes=workspace_bytes)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group)                  # every rank's stores into every shard are done
+    finally:
+        peers.close()
+    return ShardedToeplitz(local, d0, d1, E_t, group)
 
 
 def gap_slots(d0: int, d1: int, window: int = 32):

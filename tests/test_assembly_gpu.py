@@ -193,6 +193,37 @@ def test_instrumentation_and_api_variants():
         hb.assemble_single_layer(m, tg, p, Q4, "p0", "p1")
 
 
+@pytest.mark.parametrize("world,E_t", [(2, 16), (3, 40)])
+def test_row_parallel_into_d_shards_bitwise(world, E_t):
+    """Row-parallel assembly (distributed.assemble_row_parallel's kernel path)
+    on one GPU: ``world`` balanced test-row ranges store through one block
+    pointer table into ``world`` separate NaN-filled d-shard buffers (stand-ins
+    for the peer GPUs' memory).  The shards are bitwise the 1-GPU blocks: V's
+    mirrored entries cross row ranges, K's rows do not; E_t = 40 spans two
+    windows.  p1 x p1 with a row range is refused."""
+    import torch
+
+    from paper_2102_09811_b200 import distributed as D
+    from paper_2102_09811_b200.assembly import _assemble_operator
+
+    m = hb.unit_cube_mesh(2)
+    tg = hb.TimeGrid(1.0, E_t)
+    p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
+    E, N = m.n_triangles, m.n_vertices
+    for code, (R, C) in (((0, False, False, True), (E, E)), ((1, False, True, False), (E, N))):
+        full = _assemble_operator(*code, m, tg, p, Q4, None)
+        ranges = [D.block_range(r, world, E_t) for r in range(world)]
+        shards = [torch.full((b - a, R, C), float("nan"), dtype=torch.float64, device="cuda") for a, b in ranges]
+        table = torch.as_tensor(D.block_pointer_table([(s.data_ptr(), a, b) for s, (a, b) in zip(shards, ranges)],
+                                                      E_t, R * C * 8), device="cuda")
+        for rows in D.row_partition(D.row_weights(E, code[3]), world):
+            _assemble_operator(*code, m, tg, p, Q4, None, d_range=(0, E_t), row_range=rows, block_ptrs=table)
+        got = torch.cat(shards)
+        assert torch.equal(got, full), code
+    with pytest.raises(Exception):
+        _assemble_operator(2, True, True, True, m, tg, p, Q4, None, row_range=(0, 10))
+
+
 @pytest.mark.slow
 def test_c5_sampled_rows_vs_reference():
     """BASELINE config 5 (unit cube L5, 12288 triangles, alpha = 1, N = 256)

@@ -93,3 +93,55 @@ def test_sharded_apply_and_forward_solve_gloo(world):
         assert np.allclose(out[f"y{int(tr)}"].ravel(), dense @ x.ravel(), rtol=1e-13, atol=1e-13)
         assert np.allclose(dense @ out[f"x{int(tr)}"].ravel(), rhs.ravel(), rtol=1e-12, atol=1e-12)
         assert np.array_equal(out[f"full{int(tr)}"], B)
+
+
+# ---------------------------------------------------------------------------
+# row-parallel assembly: host planning (the kernel path is tested on the GPU
+# in tests/test_assembly_gpu.py::test_row_parallel_into_d_shards_bitwise)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("symmetric", [True, False])
+def test_row_partition_covers_and_balances(symmetric):
+    for n in (1, 7, 192, 768, 12288):
+        w = D.row_weights(n, symmetric)
+        for world in (1, 2, 3, 4, 8):
+            parts = D.row_partition(w, world)
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+            loads = [w[a:b].sum() for a, b in parts]
+            assert max(loads) <= w.sum() / world + w.max() + 1e-9
+
+
+def test_block_pointer_table_owners():
+    t = D.block_pointer_table([(1000, 0, 2), (9000, 2, 5)], 5, 16)
+    assert list(t) == [1000, 1016, 9000, 9016, 9032]
+    with pytest.raises(ValueError):
+        D.block_pointer_table([(0, 0, 3), (64, 2, 4)], 4, 8)     # block 2 twice
+    with pytest.raises(ValueError):
+        D.block_pointer_table([(0, 0, 2)], 4, 8)                  # blocks 2, 3 unowned
+
+
+def _plan_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        E_t, R, C = 32, 768, 386
+        d0, d1 = D.block_range(rank, world, E_t)
+        fake_handle = bytes([rank]) * 64                  # stands in for hb_ipc_export's handle
+        metas = D.exchange_shard_meta((fake_handle, 128 * rank, d0, d1))
+        bases = [(10 ** 9 * (r + 1) + o, a, b) for r, (h, o, a, b) in enumerate(metas)]
+        table = D.block_pointer_table(bases, E_t, R * C * 8)
+        rows = D.row_partition(D.row_weights(768, False), world)[rank]
+        out[rank] = ([h for h, *_ in metas], list(table), rows)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_parallel_plan_exchange_gloo():
+    world = 2
+    out = mp.Manager().dict()
+    mp.spawn(_plan_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert out[0][0] == out[1][0] == [bytes([0]) * 64, bytes([1]) * 64]
+    assert out[0][1] == out[1][1]                          # every rank addresses every block alike
+    t = out[0][1]
+    assert t[0] == 10 ** 9 and t[16] == 2 * 10 ** 9 + 128   # rank 1 owns blocks 16..31
+    assert out[0][2] == (0, 384) and out[1][2] == (384, 768)

@@ -1,0 +1,68 @@
+"""Row-parallel assembly across PROCESSES on one GPU: two gloo ranks, both on
+cuda:0, exchange their d-shards by CUDA IPC (hb_ipc_export / hb_ipc_import),
+each evaluates its test-row range for all blocks and stores through the
+shared block-pointer table into both shards.  The ranks only meet at host
+barriers (no kernel waits on another rank's kernel).  The gathered shards must
+be bitwise the 1-GPU blocks -- this is distributed.assemble_row_parallel, the
+N-GPU path, with the peer memory living on the same device."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2102_09811_b200 as hb
+    from paper_2102_09811_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        m = hb.unit_cube_mesh(2)
+        tg = hb.TimeGrid(1.0, 16)
+        p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
+        q = hb.QuadratureConfig()
+        res = {}
+        for name, code in (("V", (0, False, False, True)), ("K", (1, False, True, False))):
+            S = D.assemble_row_parallel(*code, m, tg, p, q)
+            res[name] = (S.d0, S.d1, S.local.cpu().numpy())
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_parallel_two_processes_ipc():
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_2102_09811_b200 as hb
+    from paper_2102_09811_b200.assembly import _assemble_operator
+
+    world = 2
+    out = mp.get_context("spawn").Manager().dict()
+    mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, join=True, start_method="spawn")
+    m = hb.unit_cube_mesh(2)
+    tg = hb.TimeGrid(1.0, 16)
+    p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
+    q = hb.QuadratureConfig()
+    for name, code in (("V", (0, False, False, True)), ("K", (1, False, True, False))):
+        full = _assemble_operator(*code, m, tg, p, q, None).cpu().numpy()
+        got = np.concatenate([out[r][name][2] for r in range(world)])
+        assert [out[r][name][:2] for r in range(world)] == [(0, 8), (8, 16)]
+        assert np.array_equal(got, full), name
+    torch.cuda.synchronize()
