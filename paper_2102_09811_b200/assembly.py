@@ -50,6 +50,7 @@ class BlockToeplitzMatrix:
         self.transpose_blocks_on_apply = bool(transpose_blocks_on_apply)
         self.diagonal_only = bool(diagonal_only)
         self._share = None   # storage shared with transposed() twins
+        self.host_copy = None  # (page-locked host tensor, event) when streamed to the host
 
     # ---- storage ---------------------------------------------------------
     @property
@@ -305,8 +306,13 @@ def curl_transform(mesh) -> CurlTransform:
 
 def hypersingular_from_single_layer(V: BlockToeplitzMatrix, D2: BlockToeplitzMatrix, mesh, params: KernelParams,
                                     overwrite_d2: bool = False, config: QuadratureConfig = QuadratureConfig(),
-                                    stream=None) -> BlockToeplitzMatrix:
-    """D = D2 + alpha^2 sum_o T_o^T V T_o blockwise (assembly.py:314-334), on the device."""
+                                    stream=None, host_out=None, copy_chunks: int = 4) -> BlockToeplitzMatrix:
+    """D = D2 + alpha^2 sum_o T_o^T V T_o blockwise (assembly.py:314-334), on the device.
+
+    ``host_out`` (page-locked, D's shape): the combine runs in ``copy_chunks``
+    block chunks and each chunk's device->host copy starts on a side stream as
+    soon as it is formed, so only the last chunk's copy trails the assembly;
+    the result's ``host_copy`` is (host_out, event of the last copy)."""
     import torch
 
     _native.require_cuda()
@@ -315,11 +321,34 @@ def hypersingular_from_single_layer(V: BlockToeplitzMatrix, D2: BlockToeplitzMat
         raise ValueError("V and D2 must hold the same number of blocks")
     tabs = device_tables(mesh, config, Vd.device)
     out = D2d if overwrite_d2 else torch.empty_like(D2d)
-    curl_combine_into(tabs, Vd, D2d, out, float(params.alpha), stream)
+    host_copy = None
+    if host_out is None:
+        curl_combine_into(tabs, Vd, D2d, out, float(params.alpha), stream)
+    else:
+        if tuple(host_out.shape) != tuple(out.shape) or host_out.dtype != out.dtype:
+            raise ValueError("host_out must match D's shape and dtype")
+        n = Vd.shape[0]
+        bounds = np.linspace(0, n, max(1, min(int(copy_chunks), n)) + 1).astype(int)
+        cur = stream if stream is not None else torch.cuda.current_stream(Vd.device)
+        cs = _copy_stream(Vd.device)
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            curl_combine_into(tabs, Vd[a:b], D2d[a:b], out[a:b], float(params.alpha), cur)
+            ready = torch.cuda.Event()
+            ready.record(cur)
+            cs.wait_event(ready)
+            with torch.cuda.stream(cs):
+                host_out[a:b].copy_(out[a:b], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(cs)
+        out.record_stream(cs)
+        host_copy = (host_out, done)
     if overwrite_d2:
         D2._host = None
+        D2.host_copy = host_copy
         return D2
-    return BlockToeplitzMatrix(out)
+    res = BlockToeplitzMatrix(out)
+    res.host_copy = host_copy
+    return res
 
 
 def curl_combine_into(tabs, Vd, D2d, out, alpha: float, stream=None, workspace_cap: int = 1 << 30):
@@ -339,13 +368,16 @@ def curl_combine_into(tabs, Vd, D2d, out, alpha: float, stream=None, workspace_c
 def assemble_hypersingular(mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig(),
                            workers: int | None = 1, deterministic: bool = True,
                            instrumentation: AssemblyInstrumentation | None = None,
-                           single_layer: BlockToeplitzMatrix | None = None, **kw) -> BlockToeplitzMatrix:
-    """D = T^T (alpha^2 V) T + D2, p1 x p1 (assembly.py:337-361)."""
+                           single_layer: BlockToeplitzMatrix | None = None, host_out=None,
+                           **kw) -> BlockToeplitzMatrix:
+    """D = T^T (alpha^2 V) T + D2, p1 x p1 (assembly.py:337-361).  ``host_out``:
+    stream D to page-locked host memory chunk by chunk (hypersingular_from_single_layer)."""
     if single_layer is None:
         single_layer = assemble_single_layer(mesh, timegrid, params, config, "p0", "p0", workers,
                                              deterministic, instrumentation, **kw)
     D2 = assemble_hypersingular_d2(mesh, timegrid, params, config, workers, instrumentation, **kw)
-    return hypersingular_from_single_layer(single_layer, D2, mesh, params, overwrite_d2=True, config=config)
+    return hypersingular_from_single_layer(single_layer, D2, mesh, params, overwrite_d2=True, config=config,
+                                           host_out=host_out)
 
 
 def assemble_mass(mesh, timegrid) -> BlockToeplitzMatrix:

@@ -312,3 +312,22 @@ def test_c3_sampled_rows_vs_reference():
         # no structural zeros on the sphere (no coplanar pairs): the reference's
         # exact zeros at large d are rounding cancellations of -L + 2L - L,
         # covered by the value gate above, not a sparsity pattern
+
+
+def test_hypersingular_streamed_to_host_matches():
+    """assemble_hypersingular(host_out=...) (curl combine in block chunks, each
+    chunk copied to page-locked memory as soon as it is formed) equals the
+    device result bitwise."""
+    import torch
+
+    m = hb.unit_cube_mesh(2)
+    tg = hb.TimeGrid(1.0, 16)
+    p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
+    V = hb.assemble_single_layer(m, tg, p, Q4)
+    ref = hb.assemble_hypersingular(m, tg, p, Q4, single_layer=V).device_blocks.cpu()
+    pin = torch.empty(ref.shape, dtype=torch.float64).pin_memory()
+    D = hb.assemble_hypersingular(m, tg, p, Q4, single_layer=V, host_out=pin)
+    host, ev = D.host_copy
+    ev.synchronize()
+    assert host.data_ptr() == pin.data_ptr()
+    assert torch.equal(host, ref) and torch.equal(D.device_blocks.cpu(), ref)
