@@ -134,6 +134,14 @@ size_t hb_assemble_full_workspace(const hb_mesh_desc *mesh, const hb_assembly_de
  * of d_begin/d_end (so d-sharded ranks reproduce the 1-GPU blocks). */
 int hb_assemble(const hb_mesh_desc *mesh, const hb_assembly_desc *a, void *stream);
 
+/* Whole forward substitution (solver.py:165-184) for square blocks
+ * (n x n): x[k] = inv (rhs[k] - sum_{d=1..k} A^d x[k-d]), k = 0..n_steps-1,
+ * with inv = (A^0)^{-1} (or of A^0^T when transposed) supplied by the caller;
+ * h_work: n doubles.  Fixed-order sums: deterministic. */
+int hb_forward_solve(int64_t n_blocks, int64_t n, const double *blocks_dev, int transpose, int diagonal_only,
+                     int64_t n_steps, const double *inv_dev, const double *rhs_dev, double *x_dev,
+                     double *h_work_dev, void *stream);
+
 /* CUDA IPC for row-parallel assembly: export a device pointer (anywhere
  * inside an allocation) as a 64-byte handle of its allocation plus the byte
  * offset; import opens the handle in this process (peer access enabled

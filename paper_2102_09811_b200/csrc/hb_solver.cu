@@ -63,6 +63,126 @@ __global__ void __launch_bounds__(256) k_toeplitz(const double *__restrict__ blo
     }
 }
 
+// ---------------------------------------------------------------------------
+// Forward substitution (solver.py:165-184) as one call: per time step k the
+// history h = sum_{d=1..k} A^d x[k-d] (warp per output row: lanes stream a
+// block row, fixed-order butterfly), then x[k] = (A^0)^{-1} (rhs[k] - h) with
+// the inverse cached by the caller (warp per row).  2 E_t launches, no host
+// round trips.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+// A^d(r, c) = blocks[d][r][c]; 4 warps per output row r (the c range split
+// in 4 interleaved quarters), partials added in warp order
+constexpr int kHW = 4;
+__global__ void __launch_bounds__(256) k_hist_rows(const double *__restrict__ blocks, int64_t n, int64_t k,
+                                                   const double *__restrict__ x, double *__restrict__ h)
+{
+    __shared__ double part[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = warp % kHW;
+    const int64_t r = (int64_t)blockIdx.x * (8 / kHW) + warp / kHW;
+    double acc = 0.0;
+    if (r < n) {
+        for (int64_t d = 1; d <= k; ++d) {
+            const double *a = blocks + (d * n + r) * n;
+            const double *xv = x + (k - d) * n;
+#pragma unroll 4
+            for (int64_t c = lane + 32 * sub; c < n; c += 32 * kHW) acc = fma(__ldg(a + c), __ldg(xv + c), acc);
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) part[warp] = acc;
+    __syncthreads();
+    if (sub == 0 && lane == 0 && r < n) {
+        double v = 0.0;
+        for (int w = 0; w < kHW; ++w) v += part[warp + w];
+        h[r] = v;
+    }
+}
+
+// Toeplitz product, non-transposed: y[k][r] = sum_{d<=k} A^d(r, :) x[k-d] for a
+// tile of up to kMK output times; one warp per (row, time tile): every element
+// of A^d(r, :) is loaded once and updates the tile's times k >= d (x from L1)
+constexpr int kMK = 8;
+__global__ void __launch_bounds__(256) k_toep_rows(const double *__restrict__ blocks, int64_t n_out, int64_t n_in,
+                                                   int64_t n_steps, const double *__restrict__ x,
+                                                   double *__restrict__ y)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t r = wid % n_out, k0 = (wid / n_out) * kMK;
+    if (k0 >= n_steps) return;
+    const int nk = (int)(n_steps - k0 < kMK ? n_steps - k0 : (int64_t)kMK);
+    double acc[kMK];
+#pragma unroll
+    for (int i = 0; i < kMK; ++i) acc[i] = 0.0;
+    const int64_t dmax = k0 + nk - 1;
+    for (int64_t d = 0; d <= dmax; ++d) {
+        const double *a = blocks + (d * n_out + r) * n_in;
+        const int ilo = (int)(d > k0 ? d - k0 : 0);       // tile times k = k0 + i with k >= d
+        for (int64_t c = lane; c < n_in; c += 32) {
+            const double av = __ldg(a + c);
+            const double *xc = x + (k0 - d) * n_in + c;
+#pragma unroll
+            for (int i = 0; i < kMK; ++i)
+                if (i >= ilo && i < nk) acc[i] = fma(av, __ldg(xc + i * n_in), acc[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kMK; ++i) {
+        const double v = warp_sum(acc[i]);
+        if (lane == 0 && i < nk) y[(k0 + i) * n_out + r] = v;
+    }
+}
+
+// transposed, A^d(r, c) = blocks[d][c][r]: lanes = 32 consecutive outputs r,
+// the 8 warps split the input index c, partials added in warp order
+__global__ void __launch_bounds__(256) k_hist_cols(const double *__restrict__ blocks, int64_t n, int64_t k,
+                                                   const double *__restrict__ x, double *__restrict__ h)
+{
+    __shared__ double part[8][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r = (int64_t)blockIdx.x * 32 + lane;
+    double acc = 0.0;
+    if (r < n) {
+        for (int64_t d = 1; d <= k; ++d) {
+            const double *a = blocks + d * n * n + r;
+            const double *xv = x + (k - d) * n;
+            for (int64_t c = warp; c < n; c += 8) acc = fma(__ldg(a + c * n), __ldg(xv + c), acc);
+        }
+    }
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && r < n) {
+        double v = 0.0;
+        for (int w = 0; w < 8; ++w) v += part[w][lane];
+        h[r] = v;
+    }
+}
+
+// x_k[i] = sum_j inv[i][j] (rhs_k[j] - h[j]); one warp per row i
+__global__ void __launch_bounds__(256) k_inv_apply(const double *__restrict__ inv, int64_t n,
+                                                   const double *__restrict__ rhs_k, const double *__restrict__ h,
+                                                   int has_h, double *__restrict__ x_k)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n) return;
+    const double *a = inv + i * n;
+    double acc = 0.0;
+    for (int64_t j = lane; j < n; j += 32) {
+        const double v = has_h ? __ldg(rhs_k + j) - __ldg(h + j) : __ldg(rhs_k + j);
+        acc = fma(__ldg(a + j), v, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) x_k[i] = acc;
+}
+
 }  // namespace hb
 
 using namespace hb;
@@ -81,6 +201,12 @@ extern "C" int hb_toeplitz_apply(int64_t n_blocks, int64_t R, int64_t C, const d
         return HB_ERR_INVALID;
     }
     const int64_t n_out = transpose ? C : R;
+    if (!transpose && !diagonal_only) {   // warp per (row, 32-step tile)
+        const int64_t warps = n_out * cdiv(n_steps, kMK);
+        k_toep_rows<<<(unsigned)cdiv(warps * 32, 256), 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, n_steps,
+                                                                                      x_dev, y_dev);
+        return cuda_check(cudaGetLastError(), "hb_toeplitz_apply");
+    }
     dim3 g((unsigned)cdiv(n_out, kTR), (unsigned)cdiv(n_steps, kTK));
     k_toeplitz<<<g, 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, transpose, diagonal_only, n_steps, 0, 0, 0,
                                                     n_blocks, x_dev, y_dev, 0);
@@ -116,4 +242,27 @@ extern "C" int hb_forward_subst_step(int64_t n_blocks, int64_t R, int64_t C, con
     k_toeplitz<<<g, 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, transpose, 0, k + 1, k, 1, 0, n_blocks, x_dev,
                                                     acc_dev - k * n_out, 1);
     return cuda_check(cudaGetLastError(), "hb_forward_subst_step");
+}
+
+extern "C" int hb_forward_solve(int64_t n_blocks, int64_t n, const double *blocks_dev, int transpose,
+                                int diagonal_only, int64_t n_steps, const double *inv_dev, const double *rhs_dev,
+                                double *x_dev, double *h_work_dev, void *stream)
+{
+    if (n_blocks < 1 || n < 1 || n_steps < 1 || !blocks_dev || !inv_dev || !rhs_dev || !x_dev || !h_work_dev ||
+        (!diagonal_only && n_steps > n_blocks)) {
+        set_error("hb_forward_solve: bad arguments");
+        return HB_ERR_INVALID;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g_rows = (unsigned)cdiv(n * 32, 256), g_cols = (unsigned)cdiv(n, 32);
+    const unsigned g_hist = (unsigned)cdiv(n, 8 / kHW);
+    for (int64_t k = 0; k < n_steps; ++k) {
+        const bool hist = !diagonal_only && k > 0;
+        if (hist) {
+            if (transpose) k_hist_cols<<<g_cols, 256, 0, st>>>(blocks_dev, n, k, x_dev, h_work_dev);
+            else k_hist_rows<<<g_hist, 256, 0, st>>>(blocks_dev, n, k, x_dev, h_work_dev);
+        }
+        k_inv_apply<<<g_rows, 256, 0, st>>>(inv_dev, n, rhs_dev + k * n, h_work_dev, hist ? 1 : 0, x_dev + k * n);
+    }
+    return cuda_check(cudaGetLastError(), "hb_forward_solve");
 }

@@ -76,46 +76,47 @@ def apply_toeplitz(matrix: BlockToeplitzMatrix, x, transpose_blocks: bool = Fals
     return y if was_torch else y.cpu().numpy()
 
 
-def _lu(matrix, tr):
+def _inverse(matrix, tr):
+    """(A^0)^{-1} (of A^0^T when transposed), cached on the matrix: the
+    reference refactors A^0 on every call (solver.py:176)."""
     import torch
 
-    cache = getattr(matrix, "_lu_cache", None)
+    cache = getattr(matrix, "_inv_cache", None)
     if cache is None:
         cache = {}
         try:
-            matrix._lu_cache = cache
+            matrix._inv_cache = cache
         except AttributeError:
             pass
     if tr not in cache:
         A0 = matrix.device_blocks[0]
-        cache[tr] = torch.linalg.lu_factor(A0.T.contiguous() if tr else A0)
+        cache[tr] = torch.linalg.inv(A0.T.contiguous() if tr else A0).contiguous()
     return cache[tr]
 
 
 def forward_block_solve(matrix: BlockToeplitzMatrix, rhs, transpose_blocks: bool = False):
-    """Causal time marching A^0 x^k = rhs^k - sum_{d>=1} A^d x^{k-d} (solver.py:165-184)."""
+    """Causal time marching A^0 x^k = rhs^k - sum_{d>=1} A^d x^{k-d} (solver.py:165-184):
+    one hb_forward_solve call (history and inverse-apply kernels per step)."""
     import torch
 
     _native.require_cuda()
     B = matrix.device_blocks
     nb, R, C = B.shape
+    if R != C:
+        raise ValueError("forward substitution needs square blocks")
     tr = _effective_transpose(matrix, transpose_blocks)
-    n_row, n_col = (C, R) if tr else (R, C)
     r, was_torch = _to_device(rhs)
     squeeze = r.dim() == 1
     if squeeze:
-        r = r.reshape(-1, n_row)
+        r = r.reshape(-1, R)
     E_t = r.shape[0]
-    LU, piv = _lu(matrix, tr)
-    x = torch.empty((E_t, n_col), dtype=torch.float64, device=r.device)
-    acc = torch.empty(n_row, dtype=torch.float64, device=r.device)
-    h = _native.stream_handle()
-    for k in range(E_t):
-        acc.copy_(r[k])
-        if not matrix.diagonal_only and k > 0:
-            _native.call("hb_forward_subst_step", nb, R, C, _native.ptr(B), int(tr), k, _native.ptr(x),
-                         _native.ptr(acc), h)
-        x[k] = torch.linalg.lu_solve(LU, piv, acc[:, None])[:, 0]
+    if not matrix.diagonal_only and E_t > nb:
+        raise ValueError("more time steps than stored blocks")
+    inv = _inverse(matrix, tr)
+    x = torch.empty((E_t, R), dtype=torch.float64, device=r.device)
+    h = torch.empty(R, dtype=torch.float64, device=r.device)
+    _native.call("hb_forward_solve", nb, R, _native.ptr(B), int(tr), int(matrix.diagonal_only), E_t,
+                 _native.ptr(inv), _native.ptr(r), _native.ptr(x), _native.ptr(h), _native.stream_handle())
     out = x.reshape(-1) if squeeze else x
     return out if was_torch else out.cpu().numpy()
 
