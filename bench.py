@@ -208,6 +208,67 @@ def load_traffic():
         return {}
 
 
+def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd):
+    """The other SURVEY 8 rows on this GPU (device time, CUDA events): the
+    interior potentials on a config-4 sample (tiled kernel) and the config-2
+    Dirichlet solve on the blocks just assembled.  Reference times are the
+    SURVEY's measurements of the reference on this container (8 cores)."""
+    import numpy as np
+
+    from paper_2102_09811_b200.field import _eval_grouped
+
+    def ev_ms(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps
+
+    out = {}
+    m4 = hb.unit_cube_mesh(4)
+    tg4 = hb.TimeGrid(1.0, 64)
+    p4 = hb.KernelParams(1.0, tg4.step, length_scale=m4.diameter)
+    rng = np.random.default_rng(0)
+    qd = rng.uniform(-1, 1, (64, m4.n_triangles))
+    gd = rng.uniform(-1, 1, (64, m4.n_vertices))
+    X = rng.uniform(0.05, 0.95, (100000, 3))
+    npts = 2000
+    XX = np.repeat(X[:npts], 64, axis=0)
+    K = np.tile(np.arange(1, 65), npts)
+    z = np.zeros(npts * 64)
+    cur = np.zeros(npts * 64, dtype=bool)
+    ms = [ev_ms(lambda kind=kind, c=c: _eval_grouped(kind, c, XX, K, z, cur, m4, tg4, p4, q), reps=2)
+          for kind, c in ((0, qd), (1, gd))]
+    vals = npts * 64
+    out["potentials_c4"] = {"values_per_s": vals / (sum(ms) * 1e-3), "unit": "values/s (single + double layer)",
+                            "single_ms": ms[0], "double_ms": ms[1], "sample": f"{npts} of the 1e5 config-4 "
+                            "points x 64 times (seeded as SURVEY 8(d))",
+                            "full_config4_s": sum(ms) * 1e-3 * 100000 / npts,
+                            "reference_values_per_s": 83.0}
+    V = hb.BlockToeplitzMatrix(Vd)
+    Kb = hb.BlockToeplitzMatrix(Kd)
+    Mm = hb.assemble_mass(mesh, tg)
+    y0 = np.array([1.5, 1.5, 1.5])
+    data = hb.project_to_space(lambda x, t, n=None: hb.fundamental(np.asarray(x) - y0, t + 0.1, 1.0), mesh, tg, "X10")
+    rhs = torch.as_tensor(0.5 * hb.apply_toeplitz(Mm, data) + hb.apply_toeplitz(Kb, data), device=Vd.device)
+    info = {}
+
+    def solve():
+        x, rep = hb.fgmres(hb.toeplitz_operator(V), rhs, rel_tol=1e-10,
+                           right_precond=lambda v: hb.forward_block_solve(V, v))
+        info["it"], info["res"] = rep.iterations, rep.residual
+
+    out["solve_c2"] = {"matvec_ms": ev_ms(lambda: hb.apply_toeplitz(V, rhs), reps=10),
+                       "forward_subst_ms": ev_ms(lambda: hb.forward_block_solve(V, rhs), reps=10),
+                       "fgmres_ms": ev_ms(solve), "iterations": info["it"], "residual": info["res"],
+                       "reference_ms": {"matvec": 61.0, "forward_subst": 349.0}}
+    return out
+
+
 def run_native(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -359,6 +420,7 @@ def run_native(args, rank, world, local_rank):
     launches_step = sum(st.launches for st in stats) / max(1, args.steps // 2) + 2   # + curl (2 kernels)
     traffic = load_traffic().get("k_pairs_K_dram_bytes_per_launch")
 
+    paths = measure_paths(torch, hb, mesh, tg, params, q, outV, outK) if (world == 1 and not args.no_paths) else None
     if rank != 0:
         return
     clocks = clk.summary()
@@ -404,6 +466,7 @@ def run_native(args, rank, world, local_rank):
                         "the next operator's assembly; D is streamed back in 4 block chunks as the curl combine "
                         "forms them; the step ends when the last copy is done)"},
         "clocks": clocks,
+        "paths": paths,
         "gpu_launches": int(round(launches_step * args.steps * world)),
         "impl": "native",
     }
@@ -417,6 +480,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("native", "reference"), default="native")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-paths", action="store_true", help="skip the potentials / solve measurements")
     ap.add_argument("--parallel", choices=("rows", "d"), default="rows",
                     help="N > 1: split V/K pair work by test rows (peer stores) or everything by d")
     args = ap.parse_args()
