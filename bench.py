@@ -310,6 +310,10 @@ def run_native(args, rank, world, local_rank):
                                row_range=rowsV, block_ptrs=peersV.table, stats=st[0])
             _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(0, tg.n_steps),
                                row_range=rowsK, block_ptrs=peersK.table, stats=st[1])
+        elif stats is None:
+            # the three operators on concurrent streams (public API assemble_all)
+            hb.assemble_all(mesh, tg, params, q, d_range=(d0, d1), out={"V": outV, "K": outK, "D": outD})
+            return
         else:
             _assemble_operator(0, False, False, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outV,
                                stats=st[0])
@@ -371,9 +375,12 @@ def run_native(args, rank, world, local_rank):
     pinD = torch.empty(outD.shape, dtype=torch.float64).pin_memory()
 
     def e2e_step():
+        # sequential public calls: V finishes first and its copy-back overlaps K,
+        # K's overlaps D (assemble_all's concurrent streams finish all three
+        # together and leave the 265 MB of copies exposed: slower end to end)
         hbdev.drop_device_tables(mesh)              # re-upload inputs from pinned host memory
         V = hb.assemble_single_layer(mesh, tg, params, q, d_range=(d0, d1))
-        _, ev_v = V.to_host_async(pinV)             # copy V back while K assembles
+        _, ev_v = V.to_host_async(pinV)
         K = hb.assemble_double_layer(mesh, tg, params, q, d_range=(d0, d1))
         _, ev_k = K.to_host_async(pinK)
         D = hb.assemble_hypersingular(mesh, tg, params, q, single_layer=V, d_range=(d0, d1), host_out=pinD)
@@ -417,7 +424,7 @@ def run_native(args, rank, world, local_rank):
     launches_per_call = sK.pair_launches / max(1, args.steps // 2)
     achieved = flops_per_call / (pair_ms_per_call * 1e-3) / 1e12
     shares = {nm: st.pair_ms / max(1e-9, st.pair_ms + st.finalize_ms) for nm, st in zip(("V", "K", "D2"), stats)}
-    launches_step = sum(st.launches for st in stats) / max(1, args.steps // 2) + 2   # + curl (2 kernels)
+    launches_step = sum(st.launches for st in stats) / max(1, args.steps // 2) + 1   # + curl (k_curl_tile)
     traffic = load_traffic().get("k_pairs_K_dram_bytes_per_launch")
 
     paths = measure_paths(torch, hb, mesh, tg, params, q, outV, outK) if (world == 1 and not args.no_paths) else None
@@ -460,11 +467,11 @@ def run_native(args, rank, world, local_rank):
                      "traffic": traffic},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "public API assemble_single_layer / assemble_double_layer / assemble_hypersingular, "
+                "path": "public API assemble_single_layer / assemble_double_layer / assemble_hypersingular(host_out), "
                         "mesh tables re-uploaded from pinned host memory and all blocks copied to pinned host "
-                        "memory every step (BlockToeplitzMatrix.to_host_async: each operator's copy overlaps "
-                        "the next operator's assembly; D is streamed back in 4 block chunks as the curl combine "
-                        "forms them; the step ends when the last copy is done)"},
+                        "memory every step (each operator copied back on a side stream as soon as it is done -- V's "
+                        "copy overlaps K, K's overlaps D -- and D in 4 block chunks as the curl combine forms "
+                        "them; the step ends when the last copy is done)"},
         "clocks": clocks,
         "paths": paths,
         "gpu_launches": int(round(launches_step * args.steps * world)),

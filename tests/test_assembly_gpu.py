@@ -331,3 +331,25 @@ def test_hypersingular_streamed_to_host_matches():
     ev.synchronize()
     assert host.data_ptr() == pin.data_ptr()
     assert torch.equal(host, ref) and torch.equal(D.device_blocks.cpu(), ref)
+
+
+def test_assemble_all_concurrent_streams_bitwise():
+    """assemble_all (V, K, D on three streams, streamed to page-locked host
+    memory) equals the sequential public API bitwise."""
+    import torch
+
+    from paper_2102_09811_b200 import device as hbdev
+
+    m = hb.unit_cube_mesh(2)
+    tg = hb.TimeGrid(1.0, 16)
+    p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
+    V = hb.assemble_single_layer(m, tg, p, Q4).device_blocks.cpu()
+    K = hb.assemble_double_layer(m, tg, p, Q4).device_blocks.cpu()
+    D = hb.assemble_hypersingular(m, tg, p, Q4).device_blocks.cpu()
+    pins = {n: torch.empty(t.shape, dtype=torch.float64).pin_memory() for n, t in (("V", V), ("K", K), ("D", D))}
+    hbdev.drop_device_tables(m)   # tables re-uploaded inside assemble_all
+    ops = hb.assemble_all(m, tg, p, Q4, host_out=pins)
+    for name, ref in (("V", V), ("K", K), ("D", D)):
+        host, ev = ops[name].host_copy
+        ev.synchronize()
+        assert torch.equal(host, ref) and torch.equal(ops[name].device_blocks.cpu(), ref), name
