@@ -353,3 +353,24 @@ def test_assemble_all_concurrent_streams_bitwise():
         host, ev = ops[name].host_copy
         ev.synchronize()
         assert torch.equal(host, ref) and torch.equal(ops[name].device_blocks.cpu(), ref), name
+
+
+@pytest.mark.parametrize("E_t,orders", [(1, (4, 4)), (2, (4, 4)), (17, (4, 4)), (5, (2, 3)), (5, (6, 5))])
+def test_edge_sizes_and_orders_vs_oracle(oracle, E_t, orders):
+    """Edge cases against the CPU oracle on the reference's cube-1 mesh: a
+    single block (only the i_t = 0 / 1 passes), two blocks, 17 blocks (the
+    second 16-slot lane group holds one gap), and other quadrature orders
+    (regular/near rules and Duffy grids of other point counts)."""
+    m = hb.generate_cube_surface(1)
+    tg = hb.TimeGrid(1.0, E_t)
+    p = hb.KernelParams(0.8, tg.step, length_scale=m.diameter)
+    q = hb.QuadratureConfig(*orders)
+    ops = {"V": lambda: hb.assemble_single_layer(m, tg, p, q), "K": lambda: hb.assemble_double_layer(m, tg, p, q),
+           "D2": lambda: hb.assemble_hypersingular_d2(m, tg, p, q),
+           "V11": lambda: hb.assemble_single_layer(m, tg, p, q, "p1", "p1")}
+    for op, fn in ops.items():
+        got = fn().blocks
+        ref = oracle.assemble(m, tg, p, q, op)
+        assert got.shape == ref.shape == (E_t,) + ref.shape[1:]
+        assert rel_block_err(got, ref).max() <= 1e-11, (op, rel_block_err(got, ref).max())
+        assert np.array_equal(got == 0.0, ref == 0.0), op
