@@ -380,6 +380,66 @@ def assemble_hypersingular(mesh, timegrid, params: KernelParams, config: Quadrat
                                            host_out=host_out)
 
 
+_OP_CODES = {"V": (_OP_SINGLE, False, False, True), "K": (_OP_DOUBLE, False, True, False),
+             "D2": (_OP_HYPER2, True, True, True), "V11": (_OP_SINGLE, True, True, True)}
+
+
+def apply_assembled(op: str, mesh, timegrid, params: KernelParams, x, config: QuadratureConfig = QuadratureConfig(),
+                    transpose_blocks: bool = False, chunk_blocks: int = 64, writer: BlockFileWriter | None = None):
+    """y^k = sum_{d<=k} A^d x^{k-d} for an operator that is never stored whole
+    (apply-and-discard): window-aligned d-chunks of A are
+    assembled into one reused device buffer, applied with the per-range
+    Toeplitz product (hb_toeplitz_apply_range) and discarded -- e.g. the
+    config-5 right-hand side K g with K = 155 GB on one GPU.  ``op``: "V",
+    "K", "D2", "V11" or "D" (D2 + alpha^2 curl(V) per chunk).  ``writer``
+    (BlockFileWriter) additionally streams every chunk to an HBTM1 file.
+    x: (E_t, n_in) numpy or torch; returns the same type."""
+    import torch
+
+    from .distributed import aligned_chunks
+
+    _native.require_cuda()
+    E_t = timegrid.n_steps
+    E, N = mesh.n_triangles, mesh.n_vertices
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if op == "D":
+        R = C = N
+    elif op in _OP_CODES:
+        code = _OP_CODES[op]
+        R, C = (N if code[1] else E), (N if code[2] else E)
+    else:
+        raise ValueError(f"unknown operator {op!r}")
+    n_in, n_out = (R, C) if transpose_blocks else (C, R)
+    was_torch = _is_torch(x)
+    xd = (x.to(dtype=torch.float64, device=dev) if was_torch else
+          torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=dev)).reshape(-1, n_in).contiguous()
+    if xd.shape[0] > E_t:
+        raise ValueError("more time steps than blocks")
+    steps = xd.shape[0]
+    chunks = aligned_chunks(E_t, max(1, int(chunk_blocks)))
+    width = max(b - a for a, b in chunks)
+    buf = torch.empty((width, R, C), dtype=torch.float64, device=dev)
+    vbuf = torch.empty((width, E, E), dtype=torch.float64, device=dev) if op == "D" else None
+    tabs = device_tables(mesh, config, dev) if op == "D" else None
+    y = torch.zeros((steps, n_out), dtype=torch.float64, device=dev)
+    part = torch.empty_like(y)
+    for d0, d1 in chunks:
+        n = d1 - d0
+        if op == "D":
+            _assemble_operator(*_OP_CODES["V"], mesh, timegrid, params, config, None, d_range=(d0, d1), out=vbuf[:n])
+            _assemble_operator(*_OP_CODES["D2"], mesh, timegrid, params, config, None, d_range=(d0, d1), out=buf[:n])
+            curl_combine_into(tabs, vbuf[:n], buf[:n], buf[:n], float(params.alpha))
+        else:
+            _assemble_operator(*code, mesh, timegrid, params, config, None, d_range=(d0, d1), out=buf[:n])
+        if writer is not None:
+            writer.write(buf[:n])
+        if d0 < steps:
+            _native.call("hb_toeplitz_apply_range", d0, n, R, C, _native.ptr(buf), int(transpose_blocks), steps,
+                         _native.ptr(xd), _native.ptr(part), _native.stream_handle())
+            y += part
+    return y if was_torch else y.cpu().numpy()
+
+
 _OP_STREAMS: dict = {}
 
 
@@ -463,15 +523,67 @@ def save_blocks(matrix: BlockToeplitzMatrix, path) -> None:
         fh.write(np.ascontiguousarray(b, dtype="<f8").tobytes())
 
 
-def load_blocks(path) -> BlockToeplitzMatrix:
+def load_blocks(path, mmap: bool = False) -> BlockToeplitzMatrix:
+    """Read an HBTM1 file; ``mmap=True`` maps it instead (a lazy host view of
+    operators larger than host memory -- configs 3/5 -- read block by block)."""
     with open(path, "rb") as fh:
         if fh.read(5) != _MAGIC:
             raise ValueError("not a block dump file (bad magic)")
         n, r, c = struct.unpack("<qqq", fh.read(24))
+        if mmap:
+            import os
+
+            if os.fstat(fh.fileno()).st_size < 29 + n * r * c * 8:
+                raise ValueError("truncated block dump")
+            return BlockToeplitzMatrix(np.memmap(path, dtype="<f8", mode="r", offset=29, shape=(n, r, c)))
         data = np.frombuffer(fh.read(n * r * c * 8), dtype="<f8")
     if data.size != n * r * c:
         raise ValueError("truncated block dump")
     return BlockToeplitzMatrix(data.reshape(n, r, c).astype(np.float64))
+
+
+class BlockFileWriter:
+    """Streaming HBTM1 writer: the header, then blocks appended in d order,
+    one chunk at a time (device chunks go through a page-locked staging
+    buffer) -- operators of 100-300 GB never exist whole in any memory.
+    Same format as save_blocks / heatbem's dump (assembly.py:397-419)."""
+
+    def __init__(self, path, n_blocks: int, rows: int, cols: int):
+        self.shape = (int(n_blocks), int(rows), int(cols))
+        self.written = 0
+        self._fh = open(path, "wb")
+        self._fh.write(_MAGIC + struct.pack("<qqq", *self.shape))
+        self._stage = None
+
+    def write(self, blocks) -> None:
+        """Append (k, rows, cols) blocks (numpy, or a torch tensor on any device)."""
+        if tuple(blocks.shape[1:]) != self.shape[1:]:
+            raise ValueError("block shape mismatch")
+        if self.written + blocks.shape[0] > self.shape[0]:
+            raise ValueError("more blocks than declared")
+        if _is_torch(blocks):
+            import torch
+
+            if blocks.is_cuda:
+                if self._stage is None or self._stage.numel() < blocks.numel():
+                    self._stage = torch.empty(blocks.numel(), dtype=torch.float64).pin_memory()
+                host = self._stage[: blocks.numel()].view(blocks.shape)
+                host.copy_(blocks)
+                blocks = host
+            blocks = blocks.numpy()
+        self._fh.write(np.ascontiguousarray(blocks, dtype="<f8").tobytes())
+        self.written += blocks.shape[0]
+
+    def close(self) -> None:
+        self._fh.close()
+        if self.written != self.shape[0]:
+            raise ValueError(f"{self.written} of {self.shape[0]} blocks written")
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self._fh.close() if exc[0] is not None else self.close()
 
 
 def pair_classes(mesh, config: QuadratureConfig = QuadratureConfig(), rows=None, device=None) -> np.ndarray:

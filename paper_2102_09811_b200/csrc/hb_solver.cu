@@ -109,9 +109,13 @@ __global__ void __launch_bounds__(256) k_hist_rows(const double *__restrict__ bl
 // tile of up to kMK output times; one warp per (row, time tile): every element
 // of A^d(r, :) is loaded once and updates the tile's times k >= d (x from L1)
 constexpr int kMK = 8;
+// the warp-per-row form re-reads a block row once per time tile: short
+// histories only (config 2: 0.46 vs 1.47 ms); long ones (config 5, 256 steps)
+// keep the shared-memory tiles of k_toeplitz, which reuse each staged tile
+constexpr int64_t kRowsMaxSteps = 64;
 __global__ void __launch_bounds__(256) k_toep_rows(const double *__restrict__ blocks, int64_t n_out, int64_t n_in,
                                                    int64_t n_steps, const double *__restrict__ x,
-                                                   double *__restrict__ y)
+                                                   double *__restrict__ y, int64_t d_off, int64_t n_blocks)
 {
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -121,9 +125,10 @@ __global__ void __launch_bounds__(256) k_toep_rows(const double *__restrict__ bl
     double acc[kMK];
 #pragma unroll
     for (int i = 0; i < kMK; ++i) acc[i] = 0.0;
-    const int64_t dmax = k0 + nk - 1;
-    for (int64_t d = 0; d <= dmax; ++d) {
-        const double *a = blocks + (d * n_out + r) * n_in;
+    // blocks hold A^d for d in [d_off, d_off + n_blocks) (the full operator: d_off = 0)
+    const int64_t dmax = min(k0 + nk - 1, d_off + n_blocks - 1);
+    for (int64_t d = d_off; d <= dmax; ++d) {
+        const double *a = blocks + ((d - d_off) * n_out + r) * n_in;
         const int ilo = (int)(d > k0 ? d - k0 : 0);       // tile times k = k0 + i with k >= d
         for (int64_t c = lane; c < n_in; c += 32) {
             const double av = __ldg(a + c);
@@ -201,10 +206,10 @@ extern "C" int hb_toeplitz_apply(int64_t n_blocks, int64_t R, int64_t C, const d
         return HB_ERR_INVALID;
     }
     const int64_t n_out = transpose ? C : R;
-    if (!transpose && !diagonal_only) {   // warp per (row, 32-step tile)
+    if (!transpose && !diagonal_only && n_steps <= kRowsMaxSteps) {   // warp per (row, kMK-step tile)
         const int64_t warps = n_out * cdiv(n_steps, kMK);
         k_toep_rows<<<(unsigned)cdiv(warps * 32, 256), 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, n_steps,
-                                                                                      x_dev, y_dev);
+                                                                                      x_dev, y_dev, 0, n_blocks);
         return cuda_check(cudaGetLastError(), "hb_toeplitz_apply");
     }
     dim3 g((unsigned)cdiv(n_out, kTR), (unsigned)cdiv(n_steps, kTK));
@@ -222,6 +227,12 @@ extern "C" int hb_toeplitz_apply_range(int64_t d_off, int64_t n_blocks, int64_t 
         return HB_ERR_INVALID;
     }
     const int64_t n_out = transpose ? C : R;
+    if (!transpose && n_steps <= kRowsMaxSteps) {
+        const int64_t warps = n_out * cdiv(n_steps, kMK);
+        k_toep_rows<<<(unsigned)cdiv(warps * 32, 256), 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, n_steps,
+                                                                                      x_dev, y_dev, d_off, n_blocks);
+        return cuda_check(cudaGetLastError(), "hb_toeplitz_apply_range");
+    }
     dim3 g((unsigned)cdiv(n_out, kTR), (unsigned)cdiv(n_steps, kTK));
     k_toeplitz<<<g, 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, transpose, 0, n_steps, 0, 0, d_off, n_blocks,
                                                     x_dev, y_dev, 0);
