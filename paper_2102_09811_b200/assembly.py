@@ -12,7 +12,7 @@ Extra keyword arguments (all optional, defaults reproduce the reference):
   ranks; blocks are bitwise identical to a full assembly);
 * ``device`` -- CUDA device (default: current);
 * ``workspace_bytes`` -- staging budget (default: all rows at once, capped
-  at 4 GiB).
+  at 16 GiB and a quarter of the free device memory).
 
 ``workers`` and ``deterministic`` are accepted for interface stability: the
 device path is always deterministic (no atomics; fixed-order reductions).
@@ -31,7 +31,7 @@ from .kernels import KernelParams
 from .quadrature import QuadratureConfig
 
 _OP_SINGLE, _OP_DOUBLE, _OP_HYPER2 = 0, 1, 2
-_DEFAULT_WS_CAP = 4 << 30
+_DEFAULT_WS_CAP = 16 << 30
 
 
 class BlockToeplitzMatrix:
@@ -191,6 +191,8 @@ class AssemblyInstrumentation:
 def _workspace(tables, desc_m, desc_a, device, cap):
     import torch
 
+    if cap is None:   # default: up to 16 GiB, at most a quarter of the free device memory
+        cap = min(_DEFAULT_WS_CAP, torch.cuda.mem_get_info(device)[0] // 4)
     L = _native.load()
     full = L.hb_assemble_full_workspace(desc_m, desc_a)
     least = L.hb_assemble_min_workspace(desc_m, desc_a)
@@ -244,7 +246,7 @@ def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, 
             raise ValueError(f"row_range {row_range} outside [0, {E_x}]")
         a.row_begin, a.row_end = r0, r1
     m = tabs.desc(symmetric)
-    ws = _workspace(tabs, m, a, dev, _DEFAULT_WS_CAP if workspace_bytes is None else int(workspace_bytes))
+    ws = _workspace(tabs, m, a, dev, None if workspace_bytes is None else int(workspace_bytes))
     a.workspace_dev, a.workspace_bytes = ws.data_ptr(), ws.numel()
     if stats is not None:
         import ctypes
