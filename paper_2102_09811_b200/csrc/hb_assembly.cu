@@ -1134,7 +1134,9 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
     A.inva = 1.0 / a->alpha;
     A.kconst = (a->op == 0) ? 1.0 / sqrt(kPi * a->alpha * a->alpha * a->alpha) : 1.0 / sqrt(kPi * a->alpha);
     A.halve_diag = p1p1 ? 1 : 0;
+#ifdef HB_DIAGNOSTICS   // timing study only: restrict the pair classes (results incomplete)
     if (const char *dc = getenv("HB_DEBUG_CLASS")) A.debug_class = atoi(dc);
+#endif
     A.Q = (double *)a->workspace_dev;
     A.counter = (unsigned long long *)((char *)a->workspace_dev + q_bytes);
 
