@@ -188,16 +188,42 @@ class AssemblyInstrumentation:
     seconds: float = field(default=0.0)
 
 
-def _workspace(tables, desc_m, desc_a, device, cap):
+_WS_CACHE: dict = {}
+
+
+def _workspace(tables, desc_m, desc_a, device, cap, stream=None):
+    """Staging buffer for one hb_assemble call.  One buffer per (device,
+    stream) is kept and grown on demand: calls on a stream run in order, so
+    reusing it is safe, and consecutive calls of different operators do not
+    churn the caching allocator (fresh multi-100-MB buffers per call left the
+    GPU idle between launches)."""
     import torch
 
-    if cap is None:   # default: up to 16 GiB, at most a quarter of the free device memory
-        cap = min(_DEFAULT_WS_CAP, torch.cuda.mem_get_info(device)[0] // 4)
     L = _native.load()
     full = L.hb_assemble_full_workspace(desc_m, desc_a)
     least = L.hb_assemble_min_workspace(desc_m, desc_a)
-    nbytes = max(least, min(full, cap))
-    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+    st = stream if stream is not None else torch.cuda.current_stream(device)
+    key = (str(device), st.cuda_stream)
+    buf = _WS_CACHE.get(key)
+    if cap is None:   # default: up to 16 GiB, at most a quarter of the free device memory
+        want = min(full, _DEFAULT_WS_CAP)
+        if buf is not None and buf.numel() >= max(least, want):
+            return buf[: max(least, want)]
+        cap = min(_DEFAULT_WS_CAP, (torch.cuda.mem_get_info(device)[0] + (buf.numel() if buf is not None else 0)) // 4)
+        nbytes = max(least, min(full, cap))
+        if buf is not None and buf.numel() >= nbytes:
+            return buf[:nbytes]
+        _WS_CACHE.pop(key, None)
+        del buf
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = buf
+        return buf
+    return torch.empty(max(least, min(full, int(cap))), dtype=torch.uint8, device=device)
+
+
+def release_workspaces():
+    """Drop the cached staging buffers (e.g. before a large allocation)."""
+    _WS_CACHE.clear()
 
 
 def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, mesh, timegrid,
@@ -246,7 +272,7 @@ def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, 
             raise ValueError(f"row_range {row_range} outside [0, {E_x}]")
         a.row_begin, a.row_end = r0, r1
     m = tabs.desc(symmetric)
-    ws = _workspace(tabs, m, a, dev, None if workspace_bytes is None else int(workspace_bytes))
+    ws = _workspace(tabs, m, a, dev, None if workspace_bytes is None else int(workspace_bytes), stream)
     a.workspace_dev, a.workspace_bytes = ws.data_ptr(), ws.numel()
     if stats is not None:
         import ctypes
