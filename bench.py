@@ -13,8 +13,9 @@ N > 1 runs one process per GPU (torchrun); ranks own contiguous ranges of
 time-difference blocks d.  With --parallel rows (default) the V and K pair
 work is split by balanced test-row ranges over all blocks and the finalize
 kernels store every block into its owner's shard through NVLink peer
-pointers (CUDA IPC; no halo gaps, no data-path collective), D2 and the curl
-combine stay d-local after a one-element all-reduce fence; --parallel d
+pointers (CUDA IPC; no halo gaps, no data-path collective), D2's row partial
+sums meet in one reduce-scatter (also the fence before the d-local curl
+combine); --parallel d
 splits everything by d (block d depends only on the kernel at gaps d-1, d,
 d+1).  value = all ranks' entries / max-over-ranks device time.  ``--impl reference`` times the reference's CPU algorithm (the
 oracle port, oracle/heatbem_oracle.c, all host threads) on rank 0.
@@ -292,15 +293,16 @@ def run_native(args, rank, world, local_rank):
     rows_mode = world > 1 and args.parallel == "rows"
     if rows_mode:
         # V and K: pair work split by balanced test-row ranges over ALL blocks,
-        # stores into the d-owner's shard over NVLink (peer pointers); D2 and the
-        # curl combine stay d-local (they accumulate over rows / read local V)
+        # stores into the d-owner's shard over NVLink (peer pointers); D2: row
+        # partial sums + reduce-scatter; the curl combine is d-local
         from paper_2102_09811_b200 import distributed as Dm
 
         peersV = Dm.PeerShardTable(outV, d0, d1, tg.n_steps)
         peersK = Dm.PeerShardTable(outK, d0, d1, tg.n_steps)
-        rowsV = Dm.row_partition(Dm.row_weights(E, True), world)[rank]
-        rowsK = Dm.row_partition(Dm.row_weights(E, False), world)[rank]
-        fence = torch.zeros(1, dtype=torch.float64, device=dev)
+        rowsV = Dm.row_partition(Dm.row_weights_mesh(mesh, q, True), world)[rank]
+        rowsK = Dm.row_partition(Dm.row_weights_mesh(mesh, q, False), world)[rank]
+        rowsD = Dm.row_partition(Dm.row_weights_mesh(mesh, q, True, skip_perpendicular=True), world)[rank]
+        partD = torch.empty((tg.n_steps, N, N), dtype=torch.float64, device=dev)   # this rank's D2 rows
         dist.barrier()
 
     def step(stats=None):
@@ -319,10 +321,16 @@ def run_native(args, rank, world, local_rank):
                                stats=st[0])
             _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(d0, d1), out=outK,
                                stats=st[1])
-        _assemble_operator(2, True, True, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outD,
-                           stats=st[2])
         if rows_mode:
-            dist.all_reduce(fence)   # device-side fence: every rank's V stores into this shard are done
+            # D2: this rank's element rows for all blocks, summed into the d-owners'
+            # shards by one reduce-scatter -- which is also the fence after which
+            # every rank's V stores into this shard are complete
+            _assemble_operator(2, True, True, True, mesh, tg, params, q, None, d_range=(0, tg.n_steps),
+                               row_range=rowsD, out=partD, stats=st[2])
+            Dm.reduce_scatter_blocks(partD, outD, d0, d1)
+        else:
+            _assemble_operator(2, True, True, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outD,
+                               stats=st[2])
         curl_combine_into(tabs, outV, outD, outD, params.alpha)
 
     for _ in range(max(3, args.warmup)):
@@ -449,8 +457,9 @@ def run_native(args, rank, world, local_rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: BASELINE config-2 mesh and time grid generated in-run (no dataset)",
         "config": {"workload": WORKLOAD, "E_x": E, "N_x": N, "E_t": tg.n_steps, "entries_per_step": n_entries,
-                   "parallelism": (f"x{world}: V/K pair work split by balanced test-row ranges, blocks stored "
-                                   "into the d-owner's shard over NVLink peer memory; D2 + curl d-sharded")
+                   "parallelism": (f"x{world}: V/K/D2 pair work split by balanced test-row ranges over all "
+                                   "blocks; V/K blocks stored into the d-owner's shard over NVLink peer memory, "
+                                   "D2 row partials summed by one NCCL reduce-scatter; curl d-local")
                    if rows_mode else f"d-sharded x{world} (contiguous time-difference blocks per rank)",
                    "l2": "flushed between timed steps (256 MiB device write, outside the events)",
                    "fp64_peak_tflops": peak, "pair_kernel_share": shares},

@@ -120,7 +120,9 @@ typedef struct {
      * block is written by exactly one row range (V: direct and mirrored
      * entries of its rows), so ranks splitting the rows fill the d-sharded
      * blocks bitwise as one GPU would.  p1 x p1 operators accumulate over
-     * rows: full range and contiguous blocks only. */
+     * element rows: a row range gives the (symmetrised) contribution of those
+     * rows -- partial sums to be added across ranks (distributed.py: NCCL
+     * reduce-scatter); contiguous blocks only. */
     int64_t row_begin, row_end;
     double *const *block_ptrs_dev;
 } hb_assembly_desc;

@@ -70,6 +70,7 @@ struct PairArgs {
     double *Q;
     unsigned long long *counter;   // work-item counter (zeroed per launch)
     int debug_class;               // 0 all pairs; 1 / 2 touching / separated only (HB_DEBUG_CLASS)
+    int seg_len;                   // trial elements per separated-pair work item (32, or fewer for few rows)
 };
 
 template <int OP, int NIJ>
@@ -585,8 +586,8 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
                                              double *geo, double *Ls, int lane, const double *tab)
 {
     const hb_mesh_desc &M = A.m;
-    int64_t fb = seg * 32;
-    const int64_t fe = min(fb + 32, M.E_x);
+    int64_t fb = seg * A.seg_len;
+    const int64_t fe = min(fb + A.seg_len, M.E_x);
     if (SYM) fb = max(fb, e);
     if (fb >= fe) return;
     const int64_t t_lo = __ldg(M.tn_indptr_dev + e), t_hi = __ldg(M.tn_indptr_dev + e + 1);
@@ -683,7 +684,7 @@ __global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_
     const hb_mesh_desc &M = A.m;
     const int64_t s_lo = __ldg(M.sing_rowptr_dev + A.e0), s_hi = __ldg(M.sing_rowptr_dev + A.e1);
     int64_t n_sing = s_hi - s_lo;
-    const int64_t nseg = cdiv(M.E_x, 32);
+    const int64_t nseg = cdiv(M.E_x, (int64_t)A.seg_len);
     int64_t n_reg = (A.e1 - A.e0) * nseg;
     if (A.debug_class == 1) n_reg = 0;      // study hook: touching pairs only
     if (A.debug_class == 2) n_sing = 0;     // study hook: separated pairs only
@@ -997,11 +998,17 @@ static int launch_pairs(const PairArgs &A, cudaStream_t st)
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, kWarps * 32, sm);
     const int64_t rows = A.e1 - A.e0;
-    const int64_t items = rows * cdiv(A.m.E_x, 32) + rows * A.m.sing_max_per_row;
+    // separated-pair items of 32 trial elements, or shorter when few test rows
+    // (a row-parallel rank) would leave fewer than 4 items per resident warp
+    PairArgs B = A;
+    const int64_t warps = (int64_t)std::max(1, per_sm) * nsm * kWarps;
+    B.seg_len = 32;
+    while (B.seg_len > 4 && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < 4 * warps) B.seg_len /= 2;
+    const int64_t items = rows * cdiv(A.m.E_x, (int64_t)B.seg_len) + rows * A.m.sing_max_per_row;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(1, per_sm) * nsm, cdiv(items, kWarps)));
     int rc = cuda_check(cudaMemsetAsync(A.counter, 0, sizeof(unsigned long long), st), "counter reset");
     if (rc) return rc;
-    kp<<<(unsigned)grid, kWarps * 32, sm, st>>>(A);
+    kp<<<(unsigned)grid, kWarps * 32, sm, st>>>(B);
     return cuda_check(cudaGetLastError(), "pair kernel");
 }
 
@@ -1090,9 +1097,10 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
     }
     const int64_t r0 = a->row_end > a->row_begin ? a->row_begin : 0;
     const int64_t r1 = a->row_end > a->row_begin ? a->row_end : m->E_x;
-    if (r0 < 0 || r1 > m->E_x || (a->test_p1 && a->trial_p1 && (r0 != 0 || r1 != m->E_x || a->block_ptrs_dev))) {
+    if (r0 < 0 || r1 > m->E_x || r0 >= r1 || (a->test_p1 && a->trial_p1 && a->block_ptrs_dev)) {
         set_error("hb_assemble: bad test-row range [%lld, %lld) (p1 x p1 operators accumulate over rows: "
-                  "full range and contiguous blocks only)", (long long)r0, (long long)r1);
+                  "contiguous blocks only; a row range gives those rows' partial sum)", (long long)r0,
+                  (long long)r1);
         return HB_ERR_INVALID;
     }
     if (!a->blocks_dev && !a->block_ptrs_dev) {

@@ -73,6 +73,39 @@ def row_weights(n_rows: int, symmetric: bool):
     return (n_rows - e) if symmetric else np.full(n_rows, float(n_rows))
 
 
+def row_weights_mesh(mesh, config, symmetric: bool, skip_perpendicular: bool = False):
+    """Pair-kernel work per test row in quadrature points: n_reg^2 per
+    separated pair plus the Duffy point count of each touching pair (identical
+    / edge / vertex) -- the touching pairs dominate rows near the end of an
+    upper triangle, which the plain pair count misses.  ``skip_perpendicular``
+    (D2): pairs with n_e . n_f == 0 cost nothing."""
+    from .device import host_tables
+
+    H = host_tables(mesh, config)
+    E = mesh.n_triangles
+    indptr, idx, case = H.tn[0], H.tn[1], H.tn[2]
+    off = H.duf[0]
+    q_case = np.diff(off).astype(np.float64)
+    rows = np.repeat(np.arange(E), np.diff(indptr))
+    keep = idx >= rows if symmetric else np.ones(len(idx), dtype=bool)
+    nrm = np.asarray(mesh.normals, dtype=np.float64)
+    if skip_perpendicular:
+        keep &= np.einsum("ij,ij->i", nrm[rows], nrm[idx]) != 0.0
+    sing_pts = np.bincount(rows[keep], weights=q_case[case[keep]], minlength=E)
+    n_sing = np.bincount(rows[keep], minlength=E)
+    if skip_perpendicular:   # non-perpendicular trial elements per row (f >= e when symmetric)
+        n_pairs = np.empty(E)
+        for a in range(0, E, 2048):
+            nz = (nrm[a:a + 2048] @ nrm.T) != 0.0
+            if symmetric:
+                nz &= np.arange(E)[None, :] >= np.arange(a, min(E, a + 2048))[:, None]
+            n_pairs[a:a + 2048] = nz.sum(axis=1)
+    else:
+        n_pairs = (E - np.arange(E)) if symmetric else np.full(E, E)
+    n_reg = float(len(H.reg[1])) ** 2
+    return n_reg * (n_pairs - n_sing) + sing_pts
+
+
 def row_partition(weights, world: int):
     """Contiguous test-row ranges of near-equal total weight, one per rank."""
     w = np.asarray(weights, dtype=np.float64)
@@ -177,7 +210,7 @@ def assemble_row_parallel(op: int, test_p1: bool, trial_p1: bool, symmetric: boo
                            d_range=(0, E_t), out=local, workspace_bytes=workspace_bytes)
         return ShardedToeplitz(local, d0, d1, E_t, group)
     peers = PeerShardTable(local, d0, d1, E_t, group)
-    rows = row_partition(row_weights(E_x, symmetric), world)[rank]
+    rows = row_partition(row_weights_mesh(mesh, config, symmetric), world)[rank]
     dist.barrier(group)                      # every shard allocated and mapped
     try:
         if rows[1] > rows[0]:
@@ -188,6 +221,58 @@ def assemble_row_parallel(op: int, test_p1: bool, trial_p1: bool, symmetric: boo
         dist.barrier(group)                  # every rank's stores into every shard are done
     finally:
         peers.close()
+    return ShardedToeplitz(local, d0, d1, E_t, group)
+
+
+def reduce_scatter_blocks(partial, local, d0: int, d1: int, group=None):
+    """Sum every rank's full-size partial (E_t, R, C) and leave block range
+    [d0, d1) of the sum in ``local`` -- one NCCL reduce-scatter (block ranges
+    of unequal length are padded to the longest)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    E_t = partial.shape[0]
+    sizes = [b - a for a, b in (block_range(r, world, E_t) for r in range(world))]
+    w = max(sizes)
+    if all(n == w for n in sizes):
+        dist.reduce_scatter_tensor(local, partial, group=group)
+        return local
+    padded = torch.zeros((world * w,) + tuple(partial.shape[1:]), dtype=partial.dtype, device=partial.device)
+    for r in range(world):
+        a, b = block_range(r, world, E_t)
+        padded[r * w: r * w + (b - a)] = partial[a:b]
+    out = torch.empty((w,) + tuple(partial.shape[1:]), dtype=partial.dtype, device=partial.device)
+    dist.reduce_scatter_tensor(out, padded, group=group)
+    local.copy_(out[: d1 - d0])
+    return local
+
+
+def assemble_p1p1_row_parallel(op: int, mesh, timegrid, params, config, group=None, workspace_bytes=None):
+    """p1 x p1 operators (D2, V11) with the pair work split by element rows:
+    each rank assembles its rows' symmetrised contribution to ALL blocks into a
+    full-size partial (hb_assemble with a row range), one reduce-scatter sums
+    the partials into the d-owners' shards.  Results equal the 1-GPU blocks to
+    rounding (the cross-rank sum is NCCL's order).  Needs E_t N_x^2 doubles
+    per rank (config 2: 38 MB; large configs keep d-sharding)."""
+    import torch
+    import torch.distributed as dist
+
+    from .assembly import _assemble_operator
+
+    E_t, E_x, N_x = timegrid.n_steps, mesh.n_triangles, mesh.n_vertices
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    d0, d1 = block_range(rank, world, E_t)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    local = torch.empty((d1 - d0, N_x, N_x), dtype=torch.float64, device=dev)
+    rows = row_partition(row_weights_mesh(mesh, config, True, skip_perpendicular=(op == 2)), world)[rank]
+    partial = _assemble_operator(op, True, True, True, mesh, timegrid, params, config, None, d_range=(0, E_t),
+                                 row_range=rows, workspace_bytes=workspace_bytes)
+    if world == 1:
+        local.copy_(partial)
+    else:
+        reduce_scatter_blocks(partial, local, d0, d1, group)
     return ShardedToeplitz(local, d0, d1, E_t, group)
 
 

@@ -200,7 +200,7 @@ def test_row_parallel_into_d_shards_bitwise(world, E_t):
     pointer table into ``world`` separate NaN-filled d-shard buffers (stand-ins
     for the peer GPUs' memory).  The shards are bitwise the 1-GPU blocks: V's
     mirrored entries cross row ranges, K's rows do not; E_t = 40 spans two
-    windows.  p1 x p1 with a row range is refused."""
+    windows.  p1 x p1 row ranges give partial sums that add up to the blocks."""
     import torch
 
     from paper_2102_09811_b200 import distributed as D
@@ -220,8 +220,17 @@ def test_row_parallel_into_d_shards_bitwise(world, E_t):
             _assemble_operator(*code, m, tg, p, Q4, None, d_range=(0, E_t), row_range=rows, block_ptrs=table)
         got = torch.cat(shards)
         assert torch.equal(got, full), code
-    with pytest.raises(Exception):
-        _assemble_operator(2, True, True, True, m, tg, p, Q4, None, row_range=(0, 10))
+    # p1 x p1: row ranges give partial sums (added across ranks by a reduce-scatter)
+    for op in (2, 0):
+        full = _assemble_operator(op, True, True, True, m, tg, p, Q4, None)
+        parts = [_assemble_operator(op, True, True, True, m, tg, p, Q4, None, row_range=rows)
+                 for rows in D.row_partition(D.row_weights(E, True), world)]
+        tot = sum(parts)
+        assert torch.allclose(tot, full, rtol=1e-13, atol=1e-13 * full.abs().max()), op
+        assert all(torch.equal(t, t.transpose(1, 2)) for t in parts)
+    tab_d = torch.as_tensor(D.block_pointer_table([(full.data_ptr(), 0, E_t)], E_t, N * N * 8), device="cuda")
+    with pytest.raises(Exception):   # p1 x p1 cannot store through peer pointers
+        _assemble_operator(2, True, True, True, m, tg, p, Q4, None, row_range=(0, 10), block_ptrs=tab_d)
 
 
 @pytest.mark.slow
