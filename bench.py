@@ -211,12 +211,10 @@ def load_traffic():
 
 def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd):
     """The other SURVEY 8 rows on this GPU (device time, CUDA events): the
-    interior potentials on a config-4 sample (tiled kernel) and the config-2
+    interior potentials of the whole config 4 (register-blocked kernel) and the config-2
     Dirichlet solve on the blocks just assembled.  Reference times are the
     SURVEY's measurements of the reference on this container (8 cores)."""
     import numpy as np
-
-    from paper_2102_09811_b200.field import _eval_grouped
 
     def ev_ms(fn, reps=3):
         fn()
@@ -237,18 +235,20 @@ def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd):
     qd = rng.uniform(-1, 1, (64, m4.n_triangles))
     gd = rng.uniform(-1, 1, (64, m4.n_vertices))
     X = rng.uniform(0.05, 0.95, (100000, 3))
-    npts = 2000
-    XX = np.repeat(X[:npts], 64, axis=0)
-    K = np.tile(np.arange(1, 65), npts)
-    z = np.zeros(npts * 64)
-    cur = np.zeros(npts * 64, dtype=bool)
-    ms = [ev_ms(lambda kind=kind, c=c: _eval_grouped(kind, c, XX, K, z, cur, m4, tg4, p4, q), reps=2)
-          for kind, c in ((0, qd), (1, gd))]
-    vals = npts * 64
-    out["potentials_c4"] = {"values_per_s": vals / (sum(ms) * 1e-3), "unit": "values/s (single + double layer)",
-                            "single_ms": ms[0], "double_ms": ms[1], "sample": f"{npts} of the 1e5 config-4 "
-                            "points x 64 times (seeded as SURVEY 8(d))",
-                            "full_config4_s": sum(ms) * 1e-3 * 100000 / npts,
+    # the whole of config 4 through the public call (1e5 points x 64 times,
+    # single + double layer); warm-up on a 256-point slice
+    hb.represent_grid(qd, gd, X[:256], m4, tg4, p4, return_device=True)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    hb.represent_grid(qd, gd, X, m4, tg4, p4, return_device=True)
+    e.record()
+    torch.cuda.synchronize()
+    t_ms = s.elapsed_time(e)
+    vals = X.shape[0] * 64
+    out["potentials_c4"] = {"values_per_s": vals / (t_ms * 1e-3), "unit": "values/s (u = V~q - Wg)",
+                            "full_config4_s": t_ms * 1e-3,
+                            "sample": "all 1e5 config-4 points x 64 times (seeded as SURVEY 8(d)), represent_grid",
                             "reference_values_per_s": 83.0}
     V = hb.BlockToeplitzMatrix(Vd)
     Kb = hb.BlockToeplitzMatrix(Kd)

@@ -24,10 +24,15 @@
 // kept: gap <= d_eps (first for the single layer), rho <= r_eps.
 // The sums keep the reference's order (m, then q, then e within a warp).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "hb_common.cuh"
 #include "hb_special.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace hb {
 
@@ -45,6 +50,7 @@ struct PotArgs {
     double step, alpha, d_eps, r_eps;
     double *out;
     int kcap;                  // per-warp smem capacity of the G / A / B / C arrays
+    int skip_eps0;             // k_potential_tiles: leave eps = 0 groups to k_potential_reg
 };
 
 constexpr int kPotWarps = 8;
@@ -225,6 +231,11 @@ __global__ void __launch_bounds__(kTThreads, 2) k_potential_tiles(const PotArgs 
     const int64_t g0 = (int64_t)blockIdx.x * kTP;
     const int64_t EQ = P.E_x * P.nq;
     double px[kTP], py[kTP], pz[kTP];
+    if (P.skip_eps0) {   // every group of this CTA at a time-step end: k_potential_reg owns them
+        bool any = false;
+        for (int p = 0; p < kTP; ++p) any |= g0 + p < P.n_groups && P.geps[g0 + p] != 0.0;
+        if (!any) return;
+    }
     int kmax = 0;
 #pragma unroll
     for (int p = 0; p < kTP; ++p) {
@@ -378,6 +389,228 @@ __global__ void __launch_bounds__(kTThreads, 2) k_potential_tiles(const PotArgs 
     (void)lane;
 }
 
+// ---------------------------------------------------------------------------
+// Register-blocked form for points at time-step ends (eps = 0, histories
+// kmax <= KM; config 4 and represent_grid).  With W = 2 area_e w_q,
+// B[j] = W (dens[j-1] - dens[j]) and A1[k] = W dens[k-1] (dens = 0 outside
+// [0, E_t)), the reference's sum with cur = false is
+//     u(k) = sum_eq  A1[k] G(0) + sum_{m=1..k} B[k-m] G(m)
+// (its m = 0 coefficient dens[k-1] multiplies G(0) = lim0: gap 0 <= d_eps),
+// and u(0) = 0.  The outputs k = 1..KM are cut into four blocks of R = KM/4;
+// thread (point p, half h) owns blocks h and 3 - h, so both halves do the same
+// number of FMAs.  For a block [k0, k0 + R) the thread walks m = 0..k0+R-1,
+// loading G(m) of its point (shared memory, own column) and keeping the
+// window B[k0 + i - m], i < R, in registers: one new broadcast load per m
+// feeds R FMAs (the tile form above needs two shared loads per FMA).  Terms
+// with k - m < 0 are skipped at compile time (template recursion over m).
+// The G values of the CTA's 64 points are evaluated cooperatively with the
+// lanes of a warp over m (neighbouring gaps: mostly one special-function
+// region per warp).  Per eq: A (geometry, B / A1 rows) | sync | B (kernel
+// values) | sync | C (contraction).  A cluster of S CTAs splits the eq range
+// of the same points; the partial sums are added across the cluster through
+// distributed shared memory in rank order (deterministic).  Groups with
+// eps != 0 are left to k_potential_tiles (P.skip_eps0).
+constexpr int kRP = 64;                  // points per CTA
+constexpr int kRT = 2 * kRP;             // threads: (half, point)
+constexpr int kRS = kRP + 1;             // G row stride (doubles): conflict-free rows and columns
+
+template <int KM>
+struct RegBlock {
+    static constexpr int R = KM / 4;
+    // stage M of block K0: acc[i] += w[i] G(M) for the live i, then shift the
+    // window by one (w[i] <- w[i-1], w[0] <- B[K0 - M - 1])
+    template <int K0, int M>
+    static __device__ __forceinline__ void step(double (&acc)[R], double (&w)[R], const double *Gc,
+                                                const double *b)
+    {
+        if constexpr (M < K0 + R) {
+            const double g = Gc[M * kRS];
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                if (K0 + i - M >= 0) acc[i] = fma(w[i], g, acc[i]);
+#pragma unroll
+            for (int i = R - 1; i >= 1; --i) w[i] = w[i - 1];
+            if constexpr (K0 - M - 1 >= 0) w[0] = b[K0 - M - 1];
+            step<K0, M + 1>(acc, w, Gc, b);
+        }
+    }
+    template <int K0>
+    static __device__ __forceinline__ void run(double (&acc)[R], const double *Gc, const double *b,
+                                               const double *a1)
+    {
+        const double g0 = Gc[0];
+        double w[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            acc[i] = fma(a1[K0 + i], g0, acc[i]);
+            w[i] = b[K0 + i - 1];   // window for m = 1
+        }
+        step<K0, 1>(acc, w, Gc, b);
+    }
+};
+
+template <int KIND, int KM>
+#ifndef HB_POT_MINB
+#define HB_POT_MINB 4
+#endif
+__global__ void __launch_bounds__(kRT, HB_POT_MINB) k_potential_reg(const PotArgs P, int n_split)
+{
+    constexpr int R = KM / 4;
+    extern __shared__ __align__(16) double rsm[];
+    double *tab = rsm;
+    double *Gs = tab + special::kTabDoubles;   // [KM + 1][kRS]: G(m) of point p at m * kRS + p
+    double *Bs = Gs + (KM + 1) * kRS;          // [2][2][KM + 2]: B, A1 (double-buffered by eq parity)
+    double *Rs = Bs + 4 * (KM + 2);            // [kRP] rho
+    special::load_table<KIND == 0 ? 2 : 3>(tab);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int half = tid / kRP, pt = tid % kRP;   // warp-uniform half
+    const int split = blockIdx.x % n_split;
+    const int64_t pblock = blockIdx.x / n_split;
+    const int64_t g = pblock * kRP + pt;
+    const int64_t gc = g < P.n_groups ? g : P.n_groups - 1;
+    const double px = P.gx[3 * gc], py = P.gx[3 * gc + 1], pz = P.gx[3 * gc + 2];
+    const int64_t EQ = P.E_x * P.nq;
+    const int64_t eq_lo = EQ * split / n_split, eq_hi = EQ * (split + 1) / n_split;
+    // lane constants of the kernel-value phase: gaps m = lane + 1 + 32 s
+    constexpr int kS = KM >= 64 ? 2 : 1;
+    double cm[kS], gsmall[kS];
+    bool gzero[kS];
+#pragma unroll
+    for (int s = 0; s < kS; ++s) {
+        const double gap = (double)(lane + 1 + 32 * s) * P.step;
+        cm[s] = 1.0 / (2.0 * sqrt(P.alpha * gap));
+        gsmall[s] = KIND == 0 ? 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (P.alpha * P.alpha * P.alpha) * gap)) : 0.0;
+        gzero[s] = gap <= P.d_eps;
+    }
+    const double inv4pi = 0.25 * kInvPi;
+    double accA[R], accB[R];   // blocks half and 3 - half
+#pragma unroll
+    for (int i = 0; i < R; ++i) { accA[i] = 0.0; accB[i] = 0.0; }
+    int64_t e = eq_lo / P.nq, q = eq_lo % P.nq;
+    for (int64_t eq = eq_lo; eq < eq_hi; ++eq) {
+        const int buf = (int)(eq & 1);
+        // ---- A: point vs node eq (half 0 threads); the eq's B / A1 rows ----
+        if (half == 0) {
+            const double *y = P.qpts + 3 * eq;
+            const double rx = px - __ldg(y), ry = py - __ldg(y + 1), rz = pz - __ldg(y + 2);
+            const double rho = sqrt(rx * rx + ry * ry + rz * rz);
+            double lim0;
+            if (KIND == 0) {
+                lim0 = 1.0 / (4.0 * kPi * P.alpha * rho);
+            } else {
+                const double rn = rx * __ldg(P.normals + 3 * e) + ry * __ldg(P.normals + 3 * e + 1) +
+                                  rz * __ldg(P.normals + 3 * e + 2);
+                lim0 = rho <= P.r_eps ? 0.0 : inv4pi * rn / (rho * rho * rho);
+            }
+            Rs[pt] = rho;
+            Gs[pt] = lim0;   // G(0)
+        } else {
+            const double W = 2.0 * __ldg(P.areas + e) * __ldg(P.qw + q);
+            const double *dq = P.dens_t + eq * P.E_t;
+            for (int j = pt; j <= KM; j += kRP) {
+                const double d = j < P.E_t ? __ldg(dq + j) : 0.0;
+                const double dm = (j >= 1 && j - 1 < P.E_t) ? __ldg(dq + j - 1) : 0.0;
+                Bs[(2 * buf) * (KM + 2) + j] = W * (dm - d);
+                Bs[(2 * buf + 1) * (KM + 2) + j] = W * dm;
+            }
+        }
+        if (++q == P.nq) { q = 0; ++e; }
+        __syncthreads();
+        // ---- B: kernel values G(rho_p, m h), m = 1..KM, lanes over m ----
+#pragma unroll 1
+        for (int p = warp; p < kRP; p += kRT / 32) {
+            const double rho = Rs[p], lim0 = Gs[p];
+            const bool rsmall = rho <= P.r_eps;
+            double x[kS], ix[kS], r[kS];
+#pragma unroll
+            for (int s = 0; s < kS; ++s) { x[s] = __dmul_rn(rho, cm[s]); ix[s] = 0.0; }
+            special::eval_n<KIND == 0 ? 2 : 3, kS>(x, ix, r, tab, kFull);
+#pragma unroll
+            for (int s = 0; s < kS; ++s) {
+                const int m = lane + 1 + 32 * s;
+                const double gv = gzero[s] ? lim0 : rsmall ? gsmall[s] : __dmul_rn(lim0, r[s]);
+                if (m <= KM) Gs[m * kRS + p] = gv;
+            }
+        }
+        __syncthreads();
+        // ---- C: contraction, blocks (half, 3 - half) of this thread's point ----
+        {
+            const double *b = Bs + (2 * buf) * (KM + 2), *a1 = Bs + (2 * buf + 1) * (KM + 2);
+            const double *Gc = Gs + pt;
+            if (half == 0) {
+                RegBlock<KM>::template run<1>(accA, Gc, b, a1);
+                RegBlock<KM>::template run<1 + 3 * R>(accB, Gc, b, a1);
+            } else {
+                RegBlock<KM>::template run<1 + R>(accA, Gc, b, a1);
+                RegBlock<KM>::template run<1 + 2 * R>(accB, Gc, b, a1);
+            }
+        }
+    }
+    // ---- partial sums of the cluster's eq slices, added in rank order ----
+    __syncthreads();
+    double *Os = Gs;   // [kRP][KM + 2]: u(k) of point p at p * (KM + 2) + k
+    {
+        const int ka = 1 + (half == 0 ? 0 : R), kb = 1 + (half == 0 ? 3 * R : 2 * R);
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            Os[pt * (KM + 2) + ka + i] = accA[i];
+            Os[pt * (KM + 2) + kb + i] = accB[i];
+        }
+        if (half == 0) Os[pt * (KM + 2)] = 0.0;   // u(0) = 0 at eps = 0
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    for (int p = split + n_split * (tid / 32); p < kRP; p += n_split * (kRT / 32)) {   // warp per point
+        const int64_t gg = pblock * kRP + p;
+        if (gg >= P.n_groups || P.geps[gg] != 0.0) continue;
+        for (int64_t o = P.gptr[gg] + lane; o < P.gptr[gg + 1]; o += 32) {
+            const int k = (int)P.k[o];
+            double v = 0.0;
+            for (int s = 0; s < n_split; ++s) v += cl.map_shared_rank(Os, s)[p * (KM + 2) + k];
+            P.out[P.out_idx[o]] = v;
+        }
+    }
+    cl.sync();
+}
+
+template <int KIND, int KM>
+int launch_potential_reg(const PotArgs &P, cudaStream_t stream)
+{
+    auto kern = k_potential_reg<KIND, KM>;
+    const size_t sm = sizeof(double) * (special::kTabDoubles +
+                                        std::max<size_t>((KM + 1) * kRS + 4 * (KM + 2) + kRP, kRP * (KM + 2)));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRT, sm);
+    const int64_t slots = (int64_t)std::max(1, per_sm) * nsm;
+    const int64_t nb = cdiv(P.n_groups, kRP);
+    // eq split (cluster size) with the fullest last wave; ties -> fewer splits
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 8; ++s) {
+        if ((int64_t)s * 64 > P.E_x * P.nq) break;
+        const double waves = (double)(nb * s) / (double)slots;
+        const double eff = waves / std::ceil(waves);
+        if (eff > best_eff + 1e-3) { best_eff = eff; best = s; }
+    }
+    if (const char *f = getenv("HB_POT_SPLIT")) best = std::max(1, std::min(8, atoi(f)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(nb * best));
+    cfg.blockDim = dim3(kRT);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = best;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, P, best), "hb_potential (register-blocked)");
+}
+
 }  // namespace hb
 
 using namespace hb;
@@ -401,6 +634,18 @@ extern "C" int hb_potential(int kind, int64_t n_groups, int64_t E_t, int64_t E_x
     P.gx = gx_dev; P.geps = geps_dev; P.gptr = gptr_dev; P.k = k_dev; P.cur = cur_dev; P.out_idx = out_idx_dev;
     P.dens_t = dens_t_dev; P.qpts = qpts_dev; P.qw = qw_dev; P.areas = areas_dev; P.normals = normals_dev;
     P.step = step; P.alpha = alpha; P.d_eps = d_eps; P.r_eps = r_eps; P.out = out_dev;
+    if (kmax <= kTMaxK && !getenv("HB_POT_GENERAL") && !getenv("HB_POT_TILES")) {
+        // eps = 0 groups: register-blocked form; the rest: tiled form (below)
+        int rc;
+        if (kmax <= 16) rc = kind == 0 ? launch_potential_reg<0, 16>(P, (cudaStream_t)stream)
+                                       : launch_potential_reg<1, 16>(P, (cudaStream_t)stream);
+        else if (kmax <= 32) rc = kind == 0 ? launch_potential_reg<0, 32>(P, (cudaStream_t)stream)
+                                            : launch_potential_reg<1, 32>(P, (cudaStream_t)stream);
+        else rc = kind == 0 ? launch_potential_reg<0, 64>(P, (cudaStream_t)stream)
+                            : launch_potential_reg<1, 64>(P, (cudaStream_t)stream);
+        if (rc != HB_OK) return rc;
+        P.skip_eps0 = 1;
+    }
     if (kmax <= kTMaxK && !getenv("HB_POT_GENERAL")) {   // tiled form (config 4 and shorter histories)
         const size_t sm = sizeof(double) * (special::kTabDoubles + 2 * kTC * kTW + kTP * kTC * kTW + kTP * kTC +
                                             kTP * kTK + kTP * kTC * 2 + 3 * kTP * 65);

@@ -199,16 +199,9 @@ def _boundary_warnings(xs, mesh, T, chunk=8192):
 
 def _eval_grouped(kind, coeffs, xs, k, eps, cur, mesh, timegrid, params, config, stream=None):
     """Core: points xs (n,3) with per-point (k, eps, cur) -> values (n,) on device."""
-    import torch
-
-    _native.require_cuda()
-    T = _tables(mesh, config, torch.device("cuda", torch.cuda.current_device()))
-    dev = T.qw.device
-    dens = _density(coeffs, mesh, T).permute(1, 2, 0).contiguous()   # (E_x, nq, E_t): time fastest
     n = xs.shape[0]
-    out = torch.empty(n, dtype=torch.float64, device=dev)
     if n == 0:
-        return out
+        return _launch_groups(kind, coeffs, None, mesh, timegrid, params, config, stream)
     # group by (x, eps): lexicographic sort on (x0, x1, x2, eps, k)
     key = np.column_stack([xs, eps])
     order = np.lexsort((k, key[:, 3], key[:, 2], key[:, 1], key[:, 0]))
@@ -216,18 +209,39 @@ def _eval_grouped(kind, coeffs, xs, k, eps, cur, mesh, timegrid, params, config,
     new = np.ones(n, dtype=bool)
     new[1:] = np.any(ks[1:] != ks[:-1], axis=1)
     starts = np.flatnonzero(new)
-    gptr = np.append(starts, n).astype(np.int64)
+    groups = dict(gx=ks[starts, :3], geps=ks[starts, 3], gptr=np.append(starts, n), k=k[order],
+                  cur=cur[order], out_idx=order, kmax=int(k.max()))
+    return _launch_groups(kind, coeffs, groups, mesh, timegrid, params, config, stream)
+
+
+def _grid_groups(xs, ks):
+    """Groups of represent_grid: point i owns outputs i*nt .. i*nt + nt - 1
+    (times ks, ascending), eps = 0 -- no sort needed."""
+    M, nt = xs.shape[0], len(ks)
+    return dict(gx=xs, geps=np.zeros(M), gptr=np.arange(0, M * nt + 1, nt), k=np.tile(ks, M),
+                cur=np.zeros(M * nt, dtype=bool), out_idx=np.arange(M * nt), kmax=int(ks.max()) if nt else 0)
+
+
+def _launch_groups(kind, coeffs, groups, mesh, timegrid, params, config, stream=None):
+    import torch
+
+    _native.require_cuda()
+    T = _tables(mesh, config, torch.device("cuda", torch.cuda.current_device()))
+    dev = T.qw.device
+    if groups is None or len(groups["k"]) == 0:
+        return torch.empty(0, dtype=torch.float64, device=dev)
+    dens = _density(coeffs, mesh, T).permute(1, 2, 0).contiguous()   # (E_x, nq, E_t): time fastest
+    out = torch.empty(len(groups["k"]), dtype=torch.float64, device=dev)
     up = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)  # noqa: E731
-    gx = up(ks[starts, :3], torch.float64)
-    geps = up(ks[starts, 3], torch.float64)
-    kk = up(k[order], torch.int64)
-    cc = up(cur[order].astype(np.uint8), torch.uint8)
-    oi = up(order.astype(np.int64), torch.int64)
-    gp = up(gptr, torch.int64)
-    kmax = int(k.max()) if n else 0
-    _native.call("hb_potential", int(kind), len(starts), timegrid.n_steps, mesh.n_triangles, T.nq,
+    gx = up(groups["gx"], torch.float64)
+    geps = up(groups["geps"], torch.float64)
+    kk = up(groups["k"], torch.int64)
+    cc = up(np.asarray(groups["cur"]).astype(np.uint8), torch.uint8)
+    oi = up(groups["out_idx"], torch.int64)
+    gp = up(groups["gptr"], torch.int64)
+    _native.call("hb_potential", int(kind), len(groups["gx"]), timegrid.n_steps, mesh.n_triangles, T.nq,
                  _native.ptr(gx), _native.ptr(geps), _native.ptr(gp), _native.ptr(kk), _native.ptr(cc),
-                 _native.ptr(oi), kmax, _native.ptr(dens), _native.ptr(T.qpts), _native.ptr(T.qw),
+                 _native.ptr(oi), groups["kmax"], _native.ptr(dens), _native.ptr(T.qpts), _native.ptr(T.qw),
                  _native.ptr(T.areas), _native.ptr(T.normals), timegrid.step, params.alpha,
                  params.delta_eps, params.rho_eps, _native.ptr(out), _native.stream_handle(stream))
     return out
@@ -276,12 +290,13 @@ def represent_grid(w, u, xs, mesh, timegrid, params: KernelParams, config: Quadr
     xs = np.ascontiguousarray(xs, dtype=np.float64).reshape(-1, 3)
     ks = np.arange(1, timegrid.n_steps + 1) if time_steps is None else np.asarray(time_steps, dtype=np.int64)
     M, nt = xs.shape[0], len(ks)
-    X = np.repeat(xs, nt, axis=0)
-    K = np.tile(ks, M)
-    eps = np.zeros(M * nt)
-    cur = np.zeros(M * nt, dtype=bool)
-    sv = _eval_grouped(0, np.asarray(w), X, K, eps, cur, mesh, timegrid, params, config)
-    dv = _eval_grouped(1, np.asarray(u), X, K, eps, cur, mesh, timegrid, params, config)
+    if nt and (np.any(ks < 0) or np.any(ks > timegrid.n_steps)):
+        raise ValueError("time_steps must lie in [0, n_steps]")
+    if nt > 1 and np.any(np.diff(ks) < 0):
+        raise ValueError("time_steps must be ascending")
+    groups = _grid_groups(xs, ks)
+    sv = _launch_groups(0, np.asarray(w), groups, mesh, timegrid, params, config)
+    dv = _launch_groups(1, np.asarray(u), groups, mesh, timegrid, params, config)
     res = (sv - dv).reshape(M, nt)
     return res if return_device else res.cpu().numpy()
 
