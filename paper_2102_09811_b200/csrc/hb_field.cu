@@ -453,6 +453,9 @@ template <int KIND, int KM>
 #ifndef HB_POT_MINB
 #define HB_POT_MINB 4
 #endif
+#ifndef HB_POT_ONEPASS
+#define HB_POT_ONEPASS 0
+#endif
 __global__ void __launch_bounds__(kRT, HB_POT_MINB) k_potential_reg(const PotArgs P, int n_split)
 {
     constexpr int R = KM / 4;
@@ -524,7 +527,18 @@ __global__ void __launch_bounds__(kRT, HB_POT_MINB) k_potential_reg(const PotArg
             double x[kS], ix[kS], r[kS];
 #pragma unroll
             for (int s = 0; s < kS; ++s) { x[s] = __dmul_rn(rho, cm[s]); ix[s] = 0.0; }
+#if HB_POT_ONEPASS
             special::eval_n<KIND == 0 ? 2 : 3, kS>(x, ix, r, tab, kFull);
+#else
+            // one pass per 32 gaps: the far gaps (m > 32) are mostly all in
+            // the series region, so that pass runs one chain, not two
+#pragma unroll
+            for (int s = 0; s < kS; ++s) {
+                double xs[1] = {x[s]}, is[1] = {0.0}, rs[1];
+                special::eval_n<KIND == 0 ? 2 : 3, 1>(xs, is, rs, tab, kFull);
+                r[s] = rs[0];
+            }
+#endif
 #pragma unroll
             for (int s = 0; s < kS; ++s) {
                 const int m = lane + 1 + 32 * s;

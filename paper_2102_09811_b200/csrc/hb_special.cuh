@@ -82,9 +82,18 @@ __device__ __forceinline__ double asymptote(double ix)
 __device__ __forceinline__ int mid_piece(double x, double &u)
 {
     const double y = __dmul_rn(x - kX0, kMidInvW);
+#ifdef HB_PIECE_FLOOR
     const double pf = fmin(fmax(floor(y), 0.0), (double)(kMidPieces - 1));
     u = fma(2.0, y - pf, -1.0);
     return __double2int_rz(pf);
+#else
+    // integer floor and clamp (one conversion each way instead of the FP64
+    // floor / min / max sequence); identical for middle-region lanes
+    // (0 <= y < kMidPieces), other lanes' values are discarded
+    const int p = min(max(__double2int_rd(y), 0), kMidPieces - 1);
+    u = fma(2.0, y - (double)p, -1.0);
+    return p;
+#endif
 }
 
 // KIND 0: H (single layer), 1: F (double layer), 2: erf (hypersingular D2),

@@ -65,3 +65,37 @@ def test_random_points_vs_oracle(oracle):
         ref = oracle.potential(kind, X, k, eps, cur, _interp_density_np(coef, m, hats), qpts, qw, m.areas,
                                m.normals, tg.step, p.alpha, p.delta_eps, p.rho_eps)
         assert np.allclose(got, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max()), kind
+
+
+@pytest.mark.parametrize("E_t,steps", [(12, None), (24, None), (64, None), (64, [3, 17, 40, 64]), (40, [0, 1, 2, 40])])
+def test_register_kernel_vs_oracle(oracle, E_t, steps, monkeypatch):
+    """k_potential_reg (time-step-end points, histories of <= 16 / 32 / 64
+    steps, E_t below the block size, k = 0) vs the oracle, with the eq range
+    split across clusters of 1 and 7 CTAs (HB_POT_SPLIT)."""
+    from paper_2102_09811_b200.field import _interp_density_np
+    from paper_2102_09811_b200.quadrature import rule_tables
+
+    m = hb.unit_cube_mesh(1)
+    tg = hb.TimeGrid(1.0, E_t)
+    p = hb.KernelParams(0.8, tg.step, length_scale=m.diameter)
+    rng = np.random.default_rng(E_t)
+    w = rng.standard_normal((E_t, m.n_triangles))
+    uu = rng.standard_normal((E_t, m.n_vertices))
+    X = rng.uniform(0.05, 0.95, (70, 3))
+    ks = np.arange(1, E_t + 1) if steps is None else np.asarray(steps)
+    hats, qw, qpts = rule_tables(m, 6)
+    XX = np.repeat(X, len(ks), axis=0)
+    K = np.tile(ks, len(X))
+    z = np.zeros(len(K))
+    refs = [oracle.potential(kind, XX, K, z, z > 0, _interp_density_np(c, m, hats), qpts, qw, m.areas, m.normals,
+                             tg.step, p.alpha, p.delta_eps, p.rho_eps) for kind, c in ((0, w), (1, uu))]
+    ref = (refs[0] - refs[1]).reshape(len(X), len(ks))
+    outs = []
+    for split in ("1", "7"):
+        monkeypatch.setenv("HB_POT_SPLIT", split)
+        got = hb.represent_grid(w, uu, X, m, tg, p, time_steps=steps)
+        assert np.allclose(got, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max()), split
+        outs.append(got)
+    assert np.allclose(outs[0], outs[1], rtol=1e-13, atol=1e-14 * np.abs(ref).max())
+    if steps is not None and 0 in steps:
+        assert np.all(got[:, list(steps).index(0)] == 0.0)
