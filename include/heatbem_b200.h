@@ -208,6 +208,18 @@ int hb_forward_subst_step(int64_t n_blocks, int64_t R, int64_t C, const double *
                           int transpose, int64_t k, const double *x_dev, double *acc_dev,
                           void *stream);
 
+/* Row-sharded forward substitution (solver.py:178-182 on one rank's rows):
+ * h[r] = sum_{d=1..min(k, n_blocks-1)} A^d(r, :) x[k-d] for the R local rows
+ * of blocks (n_blocks, R, C); x (>= k, C) holds the solved steps (all
+ * columns, replicated); h (R,).  k = 0 writes zeros.  Fixed-order sums. */
+int hb_forward_history(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int64_t k,
+                       const double *x_dev, double *h_dev, void *stream);
+
+/* x = inv (rhs - h) (h may be NULL: x = inv rhs); inv (n, n) row-major: the
+ * (A^0)^{-1} step of forward_block_solve (solver.py:183). */
+int hb_inv_apply(int64_t n, const double *inv_dev, const double *rhs_dev, const double *h_dev,
+                 double *x_dev, void *stream);
+
 /* FP64 DFMA throughput probe used for the roofline denominator:
  * runs `iters` dependent-chain iterations of 8 independent DFMA streams per
  * thread over grid x 256 threads; flops = grid*256*iters*8*2. */

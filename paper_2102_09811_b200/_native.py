@@ -70,7 +70,7 @@ EXPORTED = (
     "hb_assemble_full_workspace", "hb_curl_combine", "hb_potential",
     "hb_toeplitz_apply", "hb_forward_subst_step", "hb_fp64_probe", "hb_pair_classes",
     "hb_toeplitz_apply_range", "hb_curl_workspace", "hb_ipc_export", "hb_ipc_import", "hb_ipc_close",
-    "hb_forward_solve",
+    "hb_forward_solve", "hb_forward_history", "hb_inv_apply",
 )
 
 _lib = None
@@ -115,6 +115,10 @@ def load():
     L.hb_forward_solve.argtypes = [_I64, _I64, _P, _INT, _INT, _I64, _P, _P, _P, _P, _P]
     L.hb_forward_solve.restype = _INT
     L.hb_fp64_probe.restype = _INT
+    L.hb_forward_history.argtypes = [_I64, _I64, _I64, _P, _I64, _P, _P, _P]
+    L.hb_forward_history.restype = _INT
+    L.hb_inv_apply.argtypes = [_I64, _P, _P, _P, _P, _P]
+    L.hb_inv_apply.restype = _INT
     _lib = L
     return L
 

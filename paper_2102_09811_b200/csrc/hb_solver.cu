@@ -80,25 +80,29 @@ __device__ __forceinline__ double warp_sum(double v)
 // A^d(r, c) = blocks[d][r][c]; 4 warps per output row r (the c range split
 // in 4 interleaved quarters), partials added in warp order
 constexpr int kHW = 4;
-__global__ void __launch_bounds__(256) k_hist_rows(const double *__restrict__ blocks, int64_t n, int64_t k,
-                                                   const double *__restrict__ x, double *__restrict__ h)
+// (R output rows -- all of a square operator, or one rank's row shard -- by
+// C columns; blocks d = 1..min(k, n_blocks - 1))
+__global__ void __launch_bounds__(256) k_hist_rows(const double *__restrict__ blocks, int64_t R, int64_t C,
+                                                   int64_t n_blocks, int64_t k, const double *__restrict__ x,
+                                                   double *__restrict__ h)
 {
     __shared__ double part[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = warp % kHW;
     const int64_t r = (int64_t)blockIdx.x * (8 / kHW) + warp / kHW;
     double acc = 0.0;
-    if (r < n) {
-        for (int64_t d = 1; d <= k; ++d) {
-            const double *a = blocks + (d * n + r) * n;
-            const double *xv = x + (k - d) * n;
+    if (r < R) {
+        const int64_t dmax = min(k, n_blocks - 1);
+        for (int64_t d = 1; d <= dmax; ++d) {
+            const double *a = blocks + (d * R + r) * C;
+            const double *xv = x + (k - d) * C;
 #pragma unroll 4
-            for (int64_t c = lane + 32 * sub; c < n; c += 32 * kHW) acc = fma(__ldg(a + c), __ldg(xv + c), acc);
+            for (int64_t c = lane + 32 * sub; c < C; c += 32 * kHW) acc = fma(__ldg(a + c), __ldg(xv + c), acc);
         }
     }
     acc = warp_sum(acc);
     if (lane == 0) part[warp] = acc;
     __syncthreads();
-    if (sub == 0 && lane == 0 && r < n) {
+    if (sub == 0 && lane == 0 && r < R) {
         double v = 0.0;
         for (int w = 0; w < kHW; ++w) v += part[warp + w];
         h[r] = v;
@@ -271,9 +275,33 @@ extern "C" int hb_forward_solve(int64_t n_blocks, int64_t n, const double *block
         const bool hist = !diagonal_only && k > 0;
         if (hist) {
             if (transpose) k_hist_cols<<<g_cols, 256, 0, st>>>(blocks_dev, n, k, x_dev, h_work_dev);
-            else k_hist_rows<<<g_hist, 256, 0, st>>>(blocks_dev, n, k, x_dev, h_work_dev);
+            else k_hist_rows<<<g_hist, 256, 0, st>>>(blocks_dev, n, n, n_blocks, k, x_dev, h_work_dev);
         }
         k_inv_apply<<<g_rows, 256, 0, st>>>(inv_dev, n, rhs_dev + k * n, h_work_dev, hist ? 1 : 0, x_dev + k * n);
     }
     return cuda_check(cudaGetLastError(), "hb_forward_solve");
+}
+
+extern "C" int hb_forward_history(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int64_t k,
+                                  const double *x_dev, double *h_dev, void *stream)
+{
+    if (n_blocks < 1 || R < 1 || C < 1 || k < 0 || !blocks_dev || !x_dev || !h_dev) {
+        set_error("hb_forward_history: bad arguments");
+        return HB_ERR_INVALID;
+    }
+    k_hist_rows<<<(unsigned)cdiv(R, 8 / kHW), 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, n_blocks, k, x_dev,
+                                                                            h_dev);
+    return cuda_check(cudaGetLastError(), "hb_forward_history");
+}
+
+extern "C" int hb_inv_apply(int64_t n, const double *inv_dev, const double *rhs_dev, const double *h_dev,
+                            double *x_dev, void *stream)
+{
+    if (n < 1 || !inv_dev || !rhs_dev || !x_dev) {
+        set_error("hb_inv_apply: bad arguments");
+        return HB_ERR_INVALID;
+    }
+    k_inv_apply<<<(unsigned)cdiv(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(inv_dev, n, rhs_dev, h_dev,
+                                                                             h_dev ? 1 : 0, x_dev);
+    return cuda_check(cudaGetLastError(), "hb_inv_apply");
 }

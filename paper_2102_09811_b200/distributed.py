@@ -366,6 +366,165 @@ class ShardedToeplitz:
         return y[k].clone()
 
 
+class RowShardedToeplitz:
+    """Rows [r0, r1) of every block A^d of a block lower-triangular Toeplitz
+    operator on this rank (SURVEY 8(e), row-sharded solve operator):
+    ``local`` (n_blocks, r1 - r0, C).  Vectors are replicated (E_t, n) time-
+    major arrays, as in the 1-GPU solver, so ``fgmres`` runs unchanged on
+    every rank.
+
+    * ``apply``: the local rows of y = A x from the replicated x, then ONE
+      all-gather of the row pieces -- the density all-gather of the solve.
+    * ``forward_solve``: per step the local rows of the history
+      h^k = sum_{d>=1} A^d x^{k-d} (hb_forward_history), one all-gather of h^k
+      (R values) and x^k = (A^0)^{-1} (rhs^k - h^k) on every rank (the
+      inverse is replicated: A^0's rows are gathered once).
+
+    The per-rank kernels are the methods ``local_apply`` / ``local_history``
+    / ``inv_apply`` (tests on CPU replace them by numpy stand-ins)."""
+
+    def __init__(self, local, r0: int, r1: int, n_rows: int, group=None):
+        if local.shape[1] != r1 - r0:
+            raise ValueError("local must hold rows [r0, r1) of every block")
+        self.local, self.r0, self.r1, self.n_rows, self.group = local, r0, r1, n_rows, group
+        self._inv = None
+
+    @property
+    def n_blocks(self):
+        return self.local.shape[0]
+
+    @property
+    def C(self):
+        return self.local.shape[2]
+
+    def _world(self):
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            return 1, 0
+        return dist.get_world_size(self.group), dist.get_rank(self.group)
+
+    def gather_rows(self, piece):
+        """(..., r1 - r0) on every rank -> (..., n_rows): one all-gather
+        (row ranges of unequal length are padded to the longest)."""
+        import torch
+        import torch.distributed as dist
+
+        world, _ = self._world()
+        if world == 1:
+            return piece
+        ranges = [block_range(r, world, self.n_rows) for r in range(world)]
+        w = max(b - a for a, b in ranges)
+        lead = tuple(piece.shape[:-1])
+        send = torch.zeros((w,) + lead, dtype=piece.dtype, device=piece.device)
+        send[: piece.shape[-1]] = piece.movedim(-1, 0)
+        buf = torch.empty((world * w,) + lead, dtype=piece.dtype, device=piece.device)
+        dist.all_gather_into_tensor(buf, send, group=self.group)
+        rows = torch.cat([buf[r * w: r * w + (b - a)] for r, (a, b) in enumerate(ranges)])
+        return rows.movedim(0, -1).contiguous()
+
+    # ---- per-rank kernels ----
+    def local_apply(self, x):
+        import torch
+
+        E_t = x.shape[0]
+        y = torch.empty((E_t, self.r1 - self.r0), dtype=torch.float64, device=x.device)
+        _native.call("hb_toeplitz_apply", self.n_blocks, self.r1 - self.r0, self.C, _native.ptr(self.local), 0, 0,
+                     E_t, _native.ptr(x), _native.ptr(y), _native.stream_handle())
+        return y
+
+    def local_history(self, x, k: int):
+        import torch
+
+        h = torch.empty(self.r1 - self.r0, dtype=torch.float64, device=x.device)
+        _native.call("hb_forward_history", self.n_blocks, self.r1 - self.r0, self.C, _native.ptr(self.local), k,
+                     _native.ptr(x), _native.ptr(h), _native.stream_handle())
+        return h
+
+    def inv_apply(self, inv, rhs_k, h):
+        import torch
+
+        x = torch.empty(inv.shape[0], dtype=torch.float64, device=inv.device)
+        _native.call("hb_inv_apply", inv.shape[0], _native.ptr(inv), _native.ptr(rhs_k), _native.ptr(h),
+                     _native.ptr(x), _native.stream_handle())
+        return x
+
+    def inverse(self):
+        """(A^0)^{-1}, replicated (A^0's rows gathered once, then inverted
+        on every rank -- the reference factorises A^0, solver.py:176)."""
+        import torch
+
+        if self._inv is None:
+            if self.n_rows != self.C:
+                raise ValueError("forward substitution needs square blocks")
+            A0 = self.gather_rows(self.local[0].T.contiguous()).T.contiguous()
+            self._inv = torch.linalg.inv(A0).contiguous()
+        return self._inv
+
+    # ---- operator ----
+    def apply(self, x):
+        """y = A x for replicated x (E_t, C) (or flat) -> replicated y (E_t, n_rows)."""
+        flat = x.dim() == 1
+        x = x.reshape(-1, self.C)
+        if x.shape[0] > self.n_blocks:
+            raise ValueError("more time steps than stored blocks")
+        y = self.gather_rows(self.local_apply(x.contiguous()))
+        return y.reshape(-1) if flat else y
+
+    def forward_solve(self, rhs):
+        """Causal time marching, one all-gather of h^k per step k >= 1."""
+        if rhs.dim() == 1:
+            return self.forward_solve(rhs.reshape(-1, self.n_rows)).reshape(-1)
+        import torch
+
+        inv = self.inverse()
+        E_t = rhs.shape[0]
+        if E_t > self.n_blocks:
+            raise ValueError("more time steps than stored blocks")
+        rhs = rhs.contiguous()
+        x = torch.zeros((E_t, self.C), dtype=torch.float64, device=rhs.device)
+        for k in range(E_t):
+            h = self.gather_rows(self.local_history(x, k)) if k > 0 else None
+            x[k] = self.inv_apply(inv, rhs[k], h)
+        return x
+
+    def solve(self, rhs, rel_tol: float = 1e-10, max_iter: int = 500, restart: int = 50):
+        """A x = rhs by FGMRES right-preconditioned with the forward
+        substitution (the Dirichlet solve of study.py:133-136), replicated
+        on every rank; returns (x, SolveReport)."""
+        from .solver import LinearOperator, fgmres
+
+        return fgmres(LinearOperator(self.apply), rhs, rel_tol=rel_tol, max_iter=max_iter, restart=restart,
+                      right_precond=self.forward_solve)
+
+
+def row_shards_from_d_shards(shard: ShardedToeplitz, group=None):
+    """Re-distribute a d-sharded operator (blocks [d0, d1), all rows) into
+    row shards (all blocks, rows block_range(rank, world, R)): one
+    all-to-all (each rank sends every other rank that rank's rows of its
+    blocks).  Non-transposed operators only."""
+    import torch
+    import torch.distributed as dist
+
+    if shard.transpose:
+        raise ValueError("row sharding of a transposed view: shard the stored operator instead")
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    nb_all, R, C = shard.n_blocks, shard.local.shape[1], shard.local.shape[2]
+    if world == 1:
+        return RowShardedToeplitz(shard.local, 0, R, R, group)
+    rows = [block_range(r, world, R) for r in range(world)]
+    dr = [block_range(r, world, nb_all) for r in range(world)]
+    r0, r1 = rows[rank]
+    send = torch.cat([shard.local[:, a:b, :].reshape(-1) for a, b in rows])
+    in_splits = [(shard.d1 - shard.d0) * (b - a) * C for a, b in rows]
+    out_splits = [(e - s) * (r1 - r0) * C for s, e in dr]
+    recv = torch.empty(sum(out_splits), dtype=shard.local.dtype, device=shard.local.device)
+    dist.all_to_all_single(recv, send, out_splits, in_splits, group=group)
+    local = recv.reshape(nb_all, r1 - r0, C)   # senders in rank order = blocks in d order
+    return RowShardedToeplitz(local, r0, r1, R, group)
+
+
 def gather_blocks(shard: ShardedToeplitz):
     """All blocks on every rank (small operators / tests)."""
     import torch

@@ -145,3 +145,75 @@ def test_row_parallel_plan_exchange_gloo():
     t = out[0][1]
     assert t[0] == 10 ** 9 and t[16] == 2 * 10 ** 9 + 128   # rank 1 owns blocks 16..31
     assert out[0][2] == (0, 384) and out[1][2] == (384, 768)
+
+
+# ---------------------------------------------------------------------------
+# row-sharded solve operator: one all-gather per product / per time step
+# ---------------------------------------------------------------------------
+def _np_local_apply(self, x):
+    A = self.local.numpy()
+    E_t = x.shape[0]
+    y = np.zeros((E_t, A.shape[1]))
+    for k in range(E_t):
+        for d in range(min(k + 1, A.shape[0])):
+            y[k] += A[d] @ x[k - d].numpy()
+    return torch.from_numpy(y)
+
+
+def _np_local_history(self, x, k):
+    A = self.local.numpy()
+    h = np.zeros(A.shape[1])
+    for d in range(1, min(k, A.shape[0] - 1) + 1):
+        h += A[d] @ x[k - d].numpy()
+    return torch.from_numpy(h)
+
+
+def _np_inv_apply(self, inv, rhs_k, h):
+    v = rhs_k.numpy() - (h.numpy() if h is not None else 0.0)
+    return torch.from_numpy(inv.numpy() @ v)
+
+
+def _row_worker(rank, world, port, B, x, rhs, out):
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        D.RowShardedToeplitz.local_apply = _np_local_apply
+        D.RowShardedToeplitz.local_history = _np_local_history
+        D.RowShardedToeplitz.inv_apply = _np_inv_apply
+        n_blocks, R, _ = B.shape
+        d0, d1 = D.block_range(rank, world, n_blocks)
+        S = D.ShardedToeplitz(torch.from_numpy(B[d0:d1].copy()), d0, d1, n_blocks)
+        Rs = D.row_shards_from_d_shards(S)
+        r0, r1 = D.block_range(rank, world, R)
+        assert (Rs.r0, Rs.r1) == (r0, r1)
+        assert np.array_equal(Rs.local.numpy(), B[:, r0:r1, :])
+        y = Rs.apply(torch.from_numpy(x))
+        xs = Rs.forward_solve(torch.from_numpy(rhs))
+        out[f"y{rank}"] = y.numpy()
+        out[f"x{rank}"] = xs.numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 7), (3, 8)])
+def test_row_sharded_apply_and_forward_solve_gloo(world, n):
+    """Row shards from d shards (all-to-all), apply (all-gather of the row
+    pieces) and forward substitution (one all-gather of h^k per step):
+    identical on every rank and equal to the dense expansion; row ranges of
+    unequal length (n = 7 over 2 ranks, 8 over 3)."""
+    rng = np.random.default_rng(n)
+    E_t = 7
+    B = 0.2 * rng.standard_normal((E_t, n, n))
+    B[0] += 3 * np.eye(n)
+    x = rng.standard_normal((E_t, n))
+    rhs = rng.standard_normal((E_t, n))
+    out = mp.Manager().dict()
+    mp.spawn(_row_worker, args=(world, _free_port(), B, x, rhs, out), nprocs=world, join=True)
+    dense = np.zeros((E_t * n, E_t * n))
+    for k in range(E_t):
+        for i in range(k + 1):
+            dense[k * n:(k + 1) * n, i * n:(i + 1) * n] = B[k - i]
+    for r in range(world):
+        assert np.array_equal(out[f"y{r}"], out["y0"]) and np.array_equal(out[f"x{r}"], out["x0"])
+    assert np.allclose(out["y0"].ravel(), dense @ x.ravel(), rtol=1e-13, atol=1e-13)
+    assert np.allclose(dense @ out["x0"].ravel(), rhs.ravel(), rtol=1e-12, atol=1e-12)
