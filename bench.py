@@ -297,8 +297,19 @@ def run_native(args, rank, world, local_rank):
         # partial sums + reduce-scatter; the curl combine is d-local
         from paper_2102_09811_b200 import distributed as Dm
 
-        peersV = Dm.PeerShardTable(outV, d0, d1, tg.n_steps)
-        peersK = Dm.PeerShardTable(outK, d0, d1, tg.n_steps)
+        # peer mappings are set up collectively: if any rank cannot map its
+        # peers (CUDA IPC / peer access), every rank falls back to d-sharding
+        ok = 1
+        try:
+            peersV = Dm.PeerShardTable(outV, d0, d1, tg.n_steps)
+            peersK = Dm.PeerShardTable(outK, d0, d1, tg.n_steps)
+        except Exception as exc:   # noqa: BLE001 -- reported, then the d-sharded layout runs
+            log(f"rank {rank}: peer shard mapping failed ({exc}); falling back to d-sharding")
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        rows_mode = bool(flag.item())
+    if rows_mode:
         rowsV = Dm.row_partition(Dm.row_weights_mesh(mesh, q, True), world)[rank]
         rowsK = Dm.row_partition(Dm.row_weights_mesh(mesh, q, False), world)[rank]
         rowsD = Dm.row_partition(Dm.row_weights_mesh(mesh, q, True, skip_perpendicular=True), world)[rank]
@@ -512,7 +523,11 @@ def main():
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl")
+        # HB_BENCH_EMULATE=1: every rank on cuda:0 over gloo -- a control-flow
+        # check of the N > 1 path on a one-GPU box, never a measurement
+        dist.init_process_group("gloo" if os.environ.get("HB_BENCH_EMULATE") else "nccl")
+        if os.environ.get("HB_BENCH_EMULATE"):
+            local_rank = 0
     try:
         run_native(args, rank, world, local_rank)
     finally:
