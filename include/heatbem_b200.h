@@ -187,6 +187,19 @@ int hb_potential(int kind, int64_t n_groups, int64_t E_t, int64_t E_x, int64_t n
                  const double *areas_dev, const double *normals_dev,
                  double step, double alpha, double d_eps, double r_eps, double *out_dev, void *stream);
 
+/* Representation formula on a space-time grid (heatbem/field.py:184-190 for
+ * the EvalPoints (x_i, k_j h), eps = 0): out[i][j] = V~q - W g at point x_i
+ * (n_points, 3) and time k_j h (k ascending, kmax <= 64).  Both potentials in
+ * one pass: the kernel values share x, the branch regions and the middle-
+ * region piece.  dens_single (p0 q) and dens_double (p1 g interpolated) at the
+ * quadrature nodes, (E_x, nq, E_t) time fastest, as for hb_potential. */
+int hb_represent_grid(int64_t n_points, int64_t n_times, int64_t E_t, int64_t E_x, int64_t nq,
+                      const double *x_dev, const int64_t *k_dev, int64_t kmax,
+                      const double *dens_single_dev, const double *dens_double_dev,
+                      const double *qpts_dev, const double *qw_dev, const double *areas_dev,
+                      const double *normals_dev, double step, double alpha, double d_eps, double r_eps,
+                      double *out_dev, void *stream);
+
 /* y^k = sum_{d<=k} A^d x^{k-d} (heatbem/solver.py:47-73).  blocks
  * (n_blocks, R, C) row-major; transpose applies A^d^T (input length R,
  * output length C); diagonal_only uses A^0 for every k (mass matrix).

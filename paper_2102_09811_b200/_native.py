@@ -70,7 +70,7 @@ EXPORTED = (
     "hb_assemble_full_workspace", "hb_curl_combine", "hb_potential",
     "hb_toeplitz_apply", "hb_forward_subst_step", "hb_fp64_probe", "hb_pair_classes",
     "hb_toeplitz_apply_range", "hb_curl_workspace", "hb_ipc_export", "hb_ipc_import", "hb_ipc_close",
-    "hb_forward_solve", "hb_forward_history", "hb_inv_apply",
+    "hb_forward_solve", "hb_forward_history", "hb_inv_apply", "hb_represent_grid",
 )
 
 _lib = None
@@ -119,6 +119,9 @@ def load():
     L.hb_forward_history.restype = _INT
     L.hb_inv_apply.argtypes = [_I64, _P, _P, _P, _P, _P]
     L.hb_inv_apply.restype = _INT
+    L.hb_represent_grid.argtypes = [_I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P, _P,
+                                    _D, _D, _D, _D, _P, _P]
+    L.hb_represent_grid.restype = _INT
     _lib = L
     return L
 

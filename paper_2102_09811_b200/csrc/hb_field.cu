@@ -414,7 +414,7 @@ constexpr int kRP = 64;                  // points per CTA
 constexpr int kRT = 2 * kRP;             // threads: (half, point)
 constexpr int kRS = kRP + 1;             // G row stride (doubles): conflict-free rows and columns
 
-template <int KM>
+template <int KM, int STRIDE = kRS>
 struct RegBlock {
     static constexpr int R = KM / 4;
     // stage M of block K0: acc[i] += w[i] G(M) for the live i, then shift the
@@ -424,7 +424,7 @@ struct RegBlock {
                                                 const double *b)
     {
         if constexpr (M < K0 + R) {
-            const double g = Gc[M * kRS];
+            const double g = Gc[M * STRIDE];
 #pragma unroll
             for (int i = 0; i < R; ++i)
                 if (K0 + i - M >= 0) acc[i] = fma(w[i], g, acc[i]);
@@ -625,6 +625,232 @@ int launch_potential_reg(const PotArgs &P, cudaStream_t stream)
     return cuda_check(cudaLaunchKernelEx(&cfg, kern, P, best), "hb_potential (register-blocked)");
 }
 
+// ---------------------------------------------------------------------------
+// Fused representation formula on a grid (represent_grid: M points x output
+// times k <= 64, eps = 0): u = V~q - W g in ONE pass.  The single- and
+// double-layer kernel values share x = rho / (2 sqrt(a m h)), the region
+// votes and the middle-region piece, so one evaluation yields erf(x) and
+// E(x) as two independent Horner chains.  The contraction is k_potential_reg's
+// (RegBlock): thread types 0/1 of a point own the single-layer blocks
+// (h, 3 - h), types 2/3 the double-layer ones (B / A1 rows stored negated),
+// and the two partial results are added per output at the end.  Otherwise as
+// k_potential_reg (cooperative kernel values, eq split over a cluster).
+constexpr int kFP = 32;                  // points per CTA
+constexpr int kFT = 4 * kFP;             // threads: (quarter, point)
+constexpr int kFS = kFP + 1;             // G row stride (doubles)
+
+// erf(x) and E(x) of one lane at once (hb_special.cuh regions; one vote set)
+__device__ __forceinline__ void eval_erf_E(double x, const double *__restrict__ tabS, const double *__restrict__ tabD,
+                                           double &rs, double &rd)
+{
+    const double t = __dmul_rn(x, x);
+    const bool small = x < special::kX0, midr = !small && x < special::kXL, huge = !small && !midr;
+    rs = 0.0;
+    rd = 0.0;
+    if (__any_sync(kFull, small)) {
+        rs = special::series<2>(x, t, 0.0);
+        rd = special::series<3>(x, t, 0.0);
+    }
+    if (__any_sync(kFull, midr)) {
+        double u;
+        const int pc = special::mid_piece(x, u);
+        const double *cs = tabS + pc, *cd = tabD + pc;
+        double qs = cs[special::kMidDeg * special::kMidPieces], qd = cd[special::kMidDeg * special::kMidPieces];
+#pragma unroll
+        for (int k = special::kMidDeg - 1; k >= 0; --k) {
+            qs = fma(qs, u, cs[k * special::kMidPieces]);
+            qd = fma(qd, u, cd[k * special::kMidPieces]);
+        }
+        asm volatile("" : "+d"(qs), "+d"(qd));
+        rs = midr ? qs : rs;
+        rd = midr ? qd : rd;
+    }
+    if (__any_sync(kFull, huge)) {
+        if (huge) { rs = 1.0; rd = 1.0; }
+    }
+}
+
+struct RepArgs {
+    int64_t n_points, n_times, E_t, E_x, nq;
+    const double *x;        // (n_points, 3)
+    const int64_t *k;       // (n_times,) ascending, <= KM
+    const double *dens_s, *dens_d;   // (E_x, nq, E_t) time fastest
+    const double *qpts, *qw, *areas, *normals;
+    double step, alpha, d_eps, r_eps;
+    double *out;            // (n_points, n_times)
+};
+
+#ifndef HB_REP_MINB
+#define HB_REP_MINB 3
+#endif
+template <int KM>
+__global__ void __launch_bounds__(kFT, HB_REP_MINB) k_represent_reg(const RepArgs P, int n_split)
+{
+    constexpr int R = KM / 4;
+    constexpr int BT = 4 * (KM + 2);
+    extern __shared__ __align__(16) double fsm[];
+    double *tabS = fsm, *tabD = tabS + special::kTabDoubles;
+    double *Gs = tabD + special::kTabDoubles;   // [KM + 1][kFS]
+    double *Gd = Gs + (KM + 1) * kFS;           // [KM + 1][kFS]
+    double *Bt = Gd + (KM + 1) * kFS;           // [2][BT]
+    double *Rs = Bt + 2 * BT;                   // [kFP]
+    special::load_table<2>(tabS);
+    special::load_table<3>(tabD);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int quarter = tid / kFP, pt = tid % kFP;   // warp-uniform quarter
+    const int split = blockIdx.x % n_split;
+    const int64_t pblock = blockIdx.x / n_split;
+    const int64_t g = pblock * kFP + pt;
+    const int64_t gc = g < P.n_points ? g : P.n_points - 1;
+    const double px = P.x[3 * gc], py = P.x[3 * gc + 1], pz = P.x[3 * gc + 2];
+    const int64_t EQ = P.E_x * P.nq;
+    const int64_t eq_lo = EQ * split / n_split, eq_hi = EQ * (split + 1) / n_split;
+    constexpr int kS = KM >= 64 ? 2 : 1;
+    double cm[kS], gsmall[kS];
+    bool gzero[kS];
+#pragma unroll
+    for (int s = 0; s < kS; ++s) {
+        const double gap = (double)(lane + 1 + 32 * s) * P.step;
+        cm[s] = 1.0 / (2.0 * sqrt(P.alpha * gap));
+        gsmall[s] = 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (P.alpha * P.alpha * P.alpha) * gap));
+        gzero[s] = gap <= P.d_eps;
+    }
+    const double inv4pi = 0.25 * kInvPi;
+    double accA[R], accB[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) { accA[i] = 0.0; accB[i] = 0.0; }
+    int64_t e = eq_lo / P.nq, q = eq_lo % P.nq;
+    for (int64_t eq = eq_lo; eq < eq_hi; ++eq) {
+        double *bt = Bt + (int)(eq & 1) * BT;
+        // ---- A: point geometry (quarter 0); the eq's B / A1 rows (quarters 1-3) ----
+        if (quarter == 0) {
+            const double *y = P.qpts + 3 * eq;
+            const double rx = px - __ldg(y), ry = py - __ldg(y + 1), rz = pz - __ldg(y + 2);
+            const double rho = sqrt(rx * rx + ry * ry + rz * rz);
+            const double rn = rx * __ldg(P.normals + 3 * e) + ry * __ldg(P.normals + 3 * e + 1) +
+                              rz * __ldg(P.normals + 3 * e + 2);
+            Rs[pt] = rho;
+            Gs[pt] = 1.0 / (4.0 * kPi * P.alpha * rho);
+            Gd[pt] = rho <= P.r_eps ? 0.0 : inv4pi * rn / (rho * rho * rho);
+        } else {
+            const double W = 2.0 * __ldg(P.areas + e) * __ldg(P.qw + q);
+            const double *ds = P.dens_s + eq * P.E_t, *dd = P.dens_d + eq * P.E_t;
+            for (int j = tid - kFP; j <= KM; j += kFT - kFP) {
+                const double s0 = j < P.E_t ? __ldg(ds + j) : 0.0;
+                const double s1 = (j >= 1 && j - 1 < P.E_t) ? __ldg(ds + j - 1) : 0.0;
+                const double d0 = j < P.E_t ? __ldg(dd + j) : 0.0;
+                const double d1 = (j >= 1 && j - 1 < P.E_t) ? __ldg(dd + j - 1) : 0.0;
+                bt[j] = W * (s1 - s0);
+                bt[(KM + 2) + j] = W * s1;
+                bt[2 * (KM + 2) + j] = -(W * (d1 - d0));
+                bt[3 * (KM + 2) + j] = -(W * d1);
+            }
+        }
+        if (++q == P.nq) { q = 0; ++e; }
+        __syncthreads();
+        // ---- B: kernel values of both potentials, lanes over m ----
+#pragma unroll 1
+        for (int p = warp; p < kFP; p += kFT / 32) {
+            const double rho = Rs[p], l0s = Gs[p], l0d = Gd[p];
+            const bool rsmall = rho <= P.r_eps;
+#pragma unroll
+            for (int s = 0; s < kS; ++s) {
+                double fs, fd;
+                eval_erf_E(__dmul_rn(rho, cm[s]), tabS, tabD, fs, fd);
+                const int m = lane + 1 + 32 * s;
+                const double vs = gzero[s] ? l0s : rsmall ? gsmall[s] : __dmul_rn(l0s, fs);
+                const double vd = gzero[s] ? l0d : rsmall ? 0.0 : __dmul_rn(l0d, fd);
+                if (m <= KM) {
+                    Gs[m * kFS + p] = vs;
+                    Gd[m * kFS + p] = vd;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- C: contraction; quarters 0/1: single layer, blocks (h, 3 - h);
+        //      quarters 2/3: double layer (B / A1 rows negated) ----
+        {
+            const int pot = quarter >> 1, h = quarter & 1;
+            const double *Gc = (pot ? Gd : Gs) + pt;
+            const double *b = bt + 2 * pot * (KM + 2), *a1 = b + (KM + 2);
+            if (h == 0) {
+                RegBlock<KM, kFS>::template run<1>(accA, Gc, b, a1);
+                RegBlock<KM, kFS>::template run<1 + 3 * R>(accB, Gc, b, a1);
+            } else {
+                RegBlock<KM, kFS>::template run<1 + R>(accA, Gc, b, a1);
+                RegBlock<KM, kFS>::template run<1 + 2 * R>(accB, Gc, b, a1);
+            }
+        }
+    }
+    __syncthreads();
+    double *Os = Gs;   // [2][kFP][KM + 2]: single, negated double (spans Gs and Gd)
+    {
+        const int pot = quarter >> 1, h = quarter & 1;
+        const int ka = 1 + (h == 0 ? 0 : R), kb = 1 + (h == 0 ? 3 * R : 2 * R);
+        double *o = Os + (pot * kFP + pt) * (KM + 2);
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            o[ka + i] = accA[i];
+            o[kb + i] = accB[i];
+        }
+        if (h == 0) o[0] = 0.0;   // u(0) = 0 at eps = 0
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    for (int p = split + n_split * warp; p < kFP; p += n_split * (kFT / 32)) {   // warp per point
+        const int64_t gg = pblock * kFP + p;
+        if (gg >= P.n_points) continue;
+        for (int64_t o = lane; o < P.n_times; o += 32) {
+            const int k = (int)P.k[o];
+            double v = 0.0;
+            for (int s = 0; s < n_split; ++s) {
+                const double *os = cl.map_shared_rank(Os, s);
+                v += os[p * (KM + 2) + k] + os[(kFP + p) * (KM + 2) + k];
+            }
+            P.out[gg * P.n_times + o] = v;
+        }
+    }
+    cl.sync();
+}
+
+template <int KM>
+int launch_represent_reg(const RepArgs &P, cudaStream_t stream)
+{
+    auto kern = k_represent_reg<KM>;
+    const size_t sm = sizeof(double) * (2 * special::kTabDoubles +
+                                        std::max<size_t>(2 * (KM + 1) * kFS + 8 * (KM + 2) + kFP,
+                                                         2 * kFP * (KM + 2)));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFT, sm);
+    const int64_t slots = (int64_t)std::max(1, per_sm) * nsm;
+    const int64_t nb = cdiv(P.n_points, kFP);
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 8; ++s) {
+        if ((int64_t)s * 64 > P.E_x * P.nq) break;
+        const double waves = (double)(nb * s) / (double)slots;
+        const double eff = waves / std::ceil(waves);
+        if (eff > best_eff + 1e-3) { best_eff = eff; best = s; }
+    }
+    if (const char *f = getenv("HB_POT_SPLIT")) best = std::max(1, std::min(8, atoi(f)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(nb * best));
+    cfg.blockDim = dim3(kFT);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = best;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, P, best), "hb_represent_grid");
+}
+
 }  // namespace hb
 
 using namespace hb;
@@ -680,4 +906,30 @@ extern "C" int hb_potential(int kind, int64_t n_groups, int64_t E_t, int64_t E_x
     const int64_t grid = std::min<int64_t>(n_groups, (int64_t)std::max(1, per_sm) * nsm * 4);
     kern<<<(unsigned)grid, kPotWarps * 32, sm, (cudaStream_t)stream>>>(P);
     return cuda_check(cudaGetLastError(), "hb_potential");
+}
+
+// u = V~q - W g at every point x_i and every output time k_j (k ascending,
+// eps = 0): represent_grid (heatbem/field.py:184-190 on a space-time grid).
+extern "C" int hb_represent_grid(int64_t n_points, int64_t n_times, int64_t E_t, int64_t E_x, int64_t nq,
+                                 const double *x_dev, const int64_t *k_dev, int64_t kmax,
+                                 const double *dens_single_dev, const double *dens_double_dev,
+                                 const double *qpts_dev, const double *qw_dev, const double *areas_dev,
+                                 const double *normals_dev, double step, double alpha, double d_eps, double r_eps,
+                                 double *out_dev, void *stream)
+{
+    if (n_points < 0 || n_times < 0 || E_t < 1 || E_x < 1 || nq < 1 || kmax < 0 || kmax > 64 ||
+        (n_points > 0 && n_times > 0 && (!x_dev || !k_dev || !dens_single_dev || !dens_double_dev || !out_dev))) {
+        set_error("hb_represent_grid: bad arguments (kmax %lld: at most 64 output steps)", (long long)kmax);
+        return HB_ERR_INVALID;
+    }
+    if (n_points == 0 || n_times == 0) return HB_OK;
+    RepArgs P{};
+    P.n_points = n_points; P.n_times = n_times; P.E_t = E_t; P.E_x = E_x; P.nq = nq;
+    P.x = x_dev; P.k = k_dev; P.dens_s = dens_single_dev; P.dens_d = dens_double_dev;
+    P.qpts = qpts_dev; P.qw = qw_dev; P.areas = areas_dev; P.normals = normals_dev;
+    P.step = step; P.alpha = alpha; P.d_eps = d_eps; P.r_eps = r_eps; P.out = out_dev;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (kmax <= 16) return launch_represent_reg<16>(P, st);
+    if (kmax <= 32) return launch_represent_reg<32>(P, st);
+    return launch_represent_reg<64>(P, st);
 }

@@ -14,6 +14,7 @@ build the right-hand side of the Dirichlet solve and measure errors.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -279,6 +280,27 @@ def represent(w, u, points, mesh, timegrid, params: KernelParams, config: Quadra
     return sv - dv, w1 | w2
 
 
+def _represent_grid_fused(w, u, xs, ks, mesh, timegrid, params, config, stream=None):
+    """u = V~w - W u at (x_i, k_j h) in one hb_represent_grid launch: the two
+    potentials share the kernel-value evaluation (csrc/hb_field.cu)."""
+    import torch
+
+    _native.require_cuda()
+    T = _tables(mesh, config, torch.device("cuda", torch.cuda.current_device()))
+    dev = T.qw.device
+    ds = _density(w, mesh, T).permute(1, 2, 0).contiguous()
+    dd = _density(u, mesh, T).permute(1, 2, 0).contiguous()
+    X = torch.as_tensor(np.ascontiguousarray(xs), dtype=torch.float64, device=dev)
+    K = torch.as_tensor(np.ascontiguousarray(ks, dtype=np.int64), device=dev)
+    out = torch.empty((xs.shape[0], len(ks)), dtype=torch.float64, device=dev)
+    _native.call("hb_represent_grid", xs.shape[0], len(ks), timegrid.n_steps, mesh.n_triangles, T.nq,
+                 _native.ptr(X), _native.ptr(K), int(ks.max()), _native.ptr(ds), _native.ptr(dd),
+                 _native.ptr(T.qpts), _native.ptr(T.qw), _native.ptr(T.areas), _native.ptr(T.normals),
+                 timegrid.step, params.alpha, params.delta_eps, params.rho_eps, _native.ptr(out),
+                 _native.stream_handle(stream))
+    return out
+
+
 def represent_grid(w, u, xs, mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig(),
                    time_steps=None, return_device: bool = False):
     """u(x_i, k h) for every point x_i (M, 3) and every k in time_steps
@@ -294,6 +316,9 @@ def represent_grid(w, u, xs, mesh, timegrid, params: KernelParams, config: Quadr
         raise ValueError("time_steps must lie in [0, n_steps]")
     if nt > 1 and np.any(np.diff(ks) < 0):
         raise ValueError("time_steps must be ascending")
+    if nt and int(ks.max()) <= 64 and not os.environ.get("HB_REP_SEPARATE"):
+        res = _represent_grid_fused(np.asarray(w), np.asarray(u), xs, ks, mesh, timegrid, params, config)
+        return res if return_device else res.cpu().numpy()
     groups = _grid_groups(xs, ks)
     sv = _launch_groups(0, np.asarray(w), groups, mesh, timegrid, params, config)
     dv = _launch_groups(1, np.asarray(u), groups, mesh, timegrid, params, config)

@@ -41,7 +41,9 @@ def test_c4_subset_vs_reference():
     assert np.max(np.abs(u - ref)) <= 1e-11 * np.abs(ref).max()
     pts = [hb.EvalPoint(X[i], k / 64) for i in g["c4_sel"][:2] for k in range(1, 65)]
     u2, _ = hb.represent(q, gg, pts, m, tg, p)
-    assert np.array_equal(u2, u[:128])
+    # represent: two k_potential_reg launches; represent_grid: the fused
+    # hb_represent_grid (same sums, the two potentials added per term)
+    assert np.allclose(u2, u[:128], rtol=1e-13, atol=1e-14 * np.abs(ref).max())
 
 
 def test_random_points_vs_oracle(oracle):
@@ -67,11 +69,16 @@ def test_random_points_vs_oracle(oracle):
         assert np.allclose(got, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max()), kind
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("E_t,steps", [(12, None), (24, None), (64, None), (64, [3, 17, 40, 64]), (40, [0, 1, 2, 40])])
-def test_register_kernel_vs_oracle(oracle, E_t, steps, monkeypatch):
-    """k_potential_reg (time-step-end points, histories of <= 16 / 32 / 64
-    steps, E_t below the block size, k = 0) vs the oracle, with the eq range
-    split across clusters of 1 and 7 CTAs (HB_POT_SPLIT)."""
+def test_register_kernel_vs_oracle(oracle, E_t, steps, fused, monkeypatch):
+    """k_represent_reg (fused: both potentials in one pass) and
+    k_potential_reg (one launch per potential, HB_REP_SEPARATE) for
+    time-step-end points, histories of <= 16 / 32 / 64 steps, E_t below the
+    block size, k = 0, vs the oracle, with the eq range split across clusters
+    of 1 and 7 CTAs (HB_POT_SPLIT)."""
+    if not fused:
+        monkeypatch.setenv("HB_REP_SEPARATE", "1")
     from paper_2102_09811_b200.field import _interp_density_np
     from paper_2102_09811_b200.quadrature import rule_tables
 
