@@ -209,7 +209,7 @@ def load_traffic():
         return {}
 
 
-def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd):
+def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd, cpu=True):
     """The other SURVEY 8 rows on this GPU (device time, CUDA events): the
     interior potentials of the whole config 4 (register-blocked kernel) and the config-2
     Dirichlet solve on the blocks just assembled.  Reference times are the
@@ -249,7 +249,7 @@ def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd):
     out["potentials_c4"] = {"values_per_s": vals / (t_ms * 1e-3), "unit": "values/s (u = V~q - Wg)",
                             "full_config4_s": t_ms * 1e-3,
                             "sample": "all 1e5 config-4 points x 64 times (seeded as SURVEY 8(d)), represent_grid",
-                            "reference_values_per_s": 83.0}
+                            "cpu_baseline": cpu_potentials(m4, tg4, p4, qd, gd, X) if cpu else None}
     V = hb.BlockToeplitzMatrix(Vd)
     Kb = hb.BlockToeplitzMatrix(Kd)
     Mm = hb.assemble_mass(mesh, tg)
@@ -265,9 +265,48 @@ def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd):
 
     out["solve_c2"] = {"matvec_ms": ev_ms(lambda: hb.apply_toeplitz(V, rhs), reps=10),
                        "forward_subst_ms": ev_ms(lambda: hb.forward_block_solve(V, rhs), reps=10),
-                       "fgmres_ms": ev_ms(solve), "iterations": info["it"], "residual": info["res"],
-                       "reference_ms": {"matvec": 61.0, "forward_subst": 349.0}}
+                       "fgmres_ms": ev_ms(solve), "iterations": info["it"], "residual": info["res"]}
+    if cpu:
+        out["solve_c2"]["cpu_baseline"] = cpu_solve(Vd.cpu().numpy(), rhs.cpu().numpy())
     return out
+
+
+def cpu_potentials(m4, tg4, p4, qd, gd, X, n_points=4):
+    """The reference algorithm (oracle port of _field_numba._eval_potential,
+    all host threads) on a bounded sample: n_points config-4 points x 64 times,
+    both potentials."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2102_09811_b200.field import _interp_density_np
+    from paper_2102_09811_b200.quadrature import rule_tables
+
+    O.build()
+    hats, qw, qpts = rule_tables(m4, 6)
+    XX = np.repeat(X[:n_points], 64, axis=0)
+    K = np.tile(np.arange(1, 65), n_points)
+    z = np.zeros(len(K))
+    t0 = time.perf_counter()
+    for kind, c in ((0, qd), (1, gd)):
+        O.potential(kind, XX, K, z, z > 0, _interp_density_np(c, m4, hats), qpts, qw, m4.areas, m4.normals,
+                    tg4.step, p4.alpha, p4.delta_eps, p4.rho_eps)
+    dt = time.perf_counter() - t0
+    return {"values_per_s": len(K) / dt, "cores": os.cpu_count() or 1, "kind": "port",
+            "sample": f"{n_points} config-4 points x 64 times, both potentials (oracle/heatbem_oracle.c)"}
+
+
+def cpu_solve(Vh, rhs_h):
+    """The reference's numpy solver loops (oracle.apply_toeplitz /
+    forward_block_solve, restating solver.py:47-73 / 165-184) on the host."""
+    from oracle import oracle as O
+
+    t0 = time.perf_counter()
+    O.apply_toeplitz(Vh, rhs_h)
+    t1 = time.perf_counter()
+    O.forward_block_solve(Vh, rhs_h)
+    t2 = time.perf_counter()
+    return {"matvec_ms": (t1 - t0) * 1e3, "forward_subst_ms": (t2 - t1) * 1e3, "kind": "port",
+            "cores": os.cpu_count() or 1, "sample": "config-2 V (32 x 768 x 768) and the solve's rhs, numpy"}
 
 
 def run_native(args, rank, world, local_rank):
@@ -446,7 +485,8 @@ def run_native(args, rank, world, local_rank):
     launches_step = sum(st.launches for st in stats) / max(1, args.steps // 2) + 1   # + curl (k_curl_tile)
     traffic = load_traffic().get("k_pairs_K_dram_bytes_per_launch")
 
-    paths = measure_paths(torch, hb, mesh, tg, params, q, outV, outK) if (world == 1 and not args.no_paths) else None
+    paths = (measure_paths(torch, hb, mesh, tg, params, q, outV, outK, cpu=not args.no_cpu_baseline)
+             if (world == 1 and not args.no_paths) else None)
     if rank != 0:
         return
     clocks = clk.summary()

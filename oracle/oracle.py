@@ -233,3 +233,35 @@ def potential(kind, points, k_arr, eps_arr, cur_arr, dens, qpts, qw, areas, norm
                               len(points), dens.shape[0], dens.shape[1], dens.shape[2],
                               h_t, alpha, d_eps, r_eps, _ptr(out), n_threads)
     return out
+
+
+# ---------------------------------------------------------------------------
+# solver restatements (numpy; the reference's solver is numpy too)
+# ---------------------------------------------------------------------------
+def apply_toeplitz(blocks: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """y^k = sum_{d <= k} A^d x^{k-d} -- heatbem/solver.py:47-73 (the
+    non-transposed, non-diagonal case), same loop order."""
+    E_t = x.shape[0]
+    y = np.empty((E_t, blocks.shape[1]))
+    for k in range(E_t):
+        acc = blocks[0] @ x[k]
+        for d in range(1, k + 1):
+            acc += blocks[d] @ x[k - d]
+        y[k] = acc
+    return y
+
+
+def forward_block_solve(blocks: np.ndarray, rhs: np.ndarray) -> np.ndarray:
+    """A^0 x^k = rhs^k - sum_{d>=1} A^d x^{k-d} with one LU of A^0 --
+    heatbem/solver.py:165-184, same loop order."""
+    import scipy.linalg
+
+    E_t = rhs.shape[0]
+    lu = scipy.linalg.lu_factor(np.ascontiguousarray(blocks[0]))
+    x = np.empty((E_t, blocks.shape[2]))
+    for k in range(E_t):
+        acc = rhs[k].copy()
+        for d in range(1, k + 1):
+            acc -= blocks[d] @ x[k - d]
+        x[k] = scipy.linalg.lu_solve(lu, acc)
+    return x

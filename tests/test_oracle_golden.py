@@ -106,3 +106,22 @@ def test_exact_oracle_close_to_reference(oracle):
     assert err.max() < 1e-12
     ex = golden("exact")
     assert ex["c1_V_eps_ref"].shape == (16,)
+
+
+def test_oracle_solver_restatement_vs_dense():
+    """oracle.apply_toeplitz / forward_block_solve (the bench's CPU baseline
+    of the solve path, restating solver.py:47-73 / 165-184) vs the dense
+    block lower-triangular expansion."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(3)
+    E_t, n = 6, 5
+    B = 0.2 * rng.standard_normal((E_t, n, n))
+    B[0] += 3 * np.eye(n)
+    x = rng.standard_normal((E_t, n))
+    dense = np.zeros((E_t * n, E_t * n))
+    for k in range(E_t):
+        for i in range(k + 1):
+            dense[k * n:(k + 1) * n, i * n:(i + 1) * n] = B[k - i]
+    assert np.allclose(O.apply_toeplitz(B, x).ravel(), dense @ x.ravel(), rtol=1e-14, atol=1e-14)
+    assert np.allclose(dense @ O.forward_block_solve(B, x).ravel(), x.ravel(), rtol=1e-12, atol=1e-12)
