@@ -512,6 +512,211 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
     __syncwarp();
 }
 
+// ---------------------------------------------------------------------------
+// K (p0 test x p1 trial) for both orientations of one separated pair.
+// The product rule of a separated pair (a, b) uses the same point pairs for
+// K(a, b) and K(b, a): rho -- hence x and F(x) at every gap -- is shared, and
+// only the per-point weights differ:
+//   K(a, b): -(r . n_b)/rho * w hs_j(y_r)      (test a, trial hats on b)
+//   K(b, a): +(r . n_a)/rho * w ht_j(x_p)      (test b, trial hats on a)
+// with r = x_p - y_r (the reverse orientation's r is -r, exactly).  Each
+// point's weight has the bits of the direct computation; one F evaluation
+// feeds both sums, halving the special-function work of K.  Every separated
+// pair is evaluated as its canonical (min, max) orientation whichever output
+// is needed, so the blocks do not depend on the row chunking / rank split.
+// ---------------------------------------------------------------------------
+constexpr int kDualPay = 10;   // rho, 1/rho, 1/rho, Hf[3], Hr[3], pad
+template <int NJ>
+__host__ __device__ constexpr int dual_smem_doubles_per_warp() { return 32 * kDualPay + 2 * LsLayout<3, NJ>::SIZE; }
+
+// 3-term time combination of one staged row of L values (Ls: [NIJ][SLOTS],
+// then L0[NIJ], Lcomb0[NIJ]) into Q slot `slot`, lanes over blocks d
+template <int NIJ, int NJ>
+__device__ __forceinline__ void combine_store(const PairArgs &A, const double *Ls, int64_t slot, int lane)
+{
+    constexpr int SLOTS = LsLayout<NIJ, NJ>::SLOTS;
+    const double *L0 = Ls + NIJ * SLOTS, *Lc = L0 + NIJ;
+    double *dst = A.Q + slot * (int64_t)(NIJ * A.nd);
+    for (int dd = lane; dd < A.nd; dd += 32) {
+        const int d = A.d0 + dd;
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) {
+            const double *Li = Ls + i * SLOTS;
+            double b;
+            if (d == 0) {
+                const double l1 = Li[1 - A.it_lo];
+                b = Lc[i] + (-l1);
+            } else {
+                const double lm = (d - 1 == 0) ? L0[i] : Li[d - 1 - A.it_lo];
+                const double lc = Li[d - A.it_lo];
+                const double lp = Li[d + 1 - A.it_lo];
+                b = -lm + 2.0 * lc;
+                b = b + (-lp);
+            }
+            dst[i * A.nd + dd] = b;
+        }
+    }
+}
+
+template <int NJ>
+__device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularGeom &g, int nq, const double nb[3],
+                                               const double na[3], double jac, int64_t slot_f, int64_t slot_r,
+                                               const Slots<1, NJ> &T, double *geo, double *Ls, int lane,
+                                               const double *tab)
+{
+    constexpr int PAY = kDualPay, SLOTS = LsLayout<3, NJ>::SLOTS, LSZ = LsLayout<3, NJ>::SIZE;
+    const int s = lane >> 4, t = lane & 15;
+    double af[NJ][3], ar[NJ][3], s0f[3], scf[3], s0r[3], scr[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        s0f[i] = scf[i] = s0r[i] = scr[i] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) af[j][i] = ar[j][i] = 0.0;
+    }
+    for (int base = 0; base < nq; base += 32) {
+        const int q = base + lane;
+        int small = 0;
+        if (q < nq) {
+            double x[3], y[3], wq, ht[3], hs[3];
+            g.point(q, x, y, wq, ht, hs);
+            const double rx = x[0] - y[0], ry = x[1] - y[1], rz = x[2] - y[2];
+            const double rho = sqrt(rx * rx + ry * ry + rz * rz);
+            small = rho <= A.r_eps;
+            const double rnb = rx * nb[0] + ry * nb[1] + rz * nb[2];
+            const double rna = (-rx) * na[0] + (-ry) * na[1] + (-rz) * na[2];   // reverse: r' = -r
+            const double iq = 1.0 / rho;
+            const double Uf = small ? 0.0 : -rnb * iq, Ur = small ? 0.0 : -rna * iq;
+            const double P = 1.0 / __dmul_rn(rho, rho);
+            double *p = geo + lane * PAY;
+            p[0] = rho;
+            p[1] = iq;
+            p[2] = iq;
+            double Hf[3], Hr[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                Hf[i] = wq * (1.0 * hs[i]);
+                Hr[i] = wq * (1.0 * ht[i]);
+                p[3 + i] = (Hf[i] * Uf) * A.inv2a;
+                p[6 + i] = (Hr[i] * Ur) * A.inv2a;
+            }
+            if (A.need_special) {
+                const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    s0f[i] = fma(Hf[i] * Uf, c0, s0f[i]);
+                    scf[i] = fma(Hf[i] * Uf, cc, scf[i]);
+                    s0r[i] = fma(Hr[i] * Ur, c0, s0r[i]);
+                    scr[i] = fma(Hr[i] * Ur, cc, scr[i]);
+                }
+            }
+        }
+        const bool any_small = __any_sync(kFull, small);
+        __syncwarp();
+        const int nloc = min(32, nq - base);
+        if (!any_small) {
+            constexpr int G = HB_QGROUP;
+            const int nlocg = (nloc + 2 * G - 1) / (2 * G) * (2 * G);
+            for (int k = s; k < nlocg; k += 2 * G) {
+                bool ok[G];
+                const double *pp[G];
+                double rho[G], a[G];
+#pragma unroll
+                for (int gg = 0; gg < G; ++gg) {
+                    ok[gg] = k + 2 * gg < nloc;
+                    pp[gg] = geo + (ok[gg] ? k + 2 * gg : 0) * PAY;
+                    rho[gg] = pp[gg][0];
+                    a[gg] = pp[gg][1];
+                }
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    double xs[G], ixs[G], fs[G];
+#pragma unroll
+                    for (int gg = 0; gg < G; ++gg) {
+                        xs[gg] = __dmul_rn(rho[gg], T.cx[j]);
+                        ixs[gg] = __dmul_rn(a[gg], T.ic[j]);
+                    }
+                    special::eval_n<1, G>(xs, ixs, fs, tab, kFull);
+#pragma unroll
+                    for (int gg = 0; gg < G; ++gg) {
+                        const double v = ok[gg] ? fs[gg] : 0.0;
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) {
+                            af[j][i] = fma(v, pp[gg][3 + i], af[j][i]);
+                            ar[j][i] = fma(v, pp[gg][6 + i], ar[j][i]);
+                        }
+                    }
+                }
+            }
+        } else {
+            for (int k = s; k < nloc; k += 2) {
+                const double *p = geo + k * PAY;
+                const double rho = p[0], s1 = p[1];
+                const bool sm = rho <= A.r_eps;
+                const unsigned mask = __activemask();
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    const double x = __dmul_rn(rho, T.cx[j]);
+                    const double ix = __dmul_rn(s1, T.ic[j]);
+                    const double f = special::eval<1>(x, ix, tab, mask);
+                    const double val = sm ? 0.0 : f;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        af[j][i] = fma(val, p[3 + i], af[j][i]);
+                        ar[j][i] = fma(val, p[6 + i], ar[j][i]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            af[j][i] += __shfl_xor_sync(kFull, af[j][i], 16);
+            ar[j][i] += __shfl_xor_sync(kFull, ar[j][i], 16);
+        }
+    if (A.need_special) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                s0f[i] += __shfl_xor_sync(kFull, s0f[i], o);
+                scf[i] += __shfl_xor_sync(kFull, scf[i], o);
+                s0r[i] += __shfl_xor_sync(kFull, s0r[i], o);
+                scr[i] += __shfl_xor_sync(kFull, scr[i], o);
+            }
+    }
+    const int nslots = A.it_hi - A.it_lo + 1;
+    double *Lf = Ls, *Lr = Ls + LSZ;
+    if (s == 0) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int sl = t + 16 * j;
+            if (sl < nslots) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    Lf[i * SLOTS + sl] = jac * af[j][i];
+                    Lr[i * SLOTS + sl] = jac * ar[j][i];
+                }
+            }
+        }
+    }
+    if (lane == 0 && A.need_special) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            Lf[3 * SLOTS + i] = jac * s0f[i];
+            Lf[3 * SLOTS + 3 + i] = jac * scf[i];
+            Lr[3 * SLOTS + i] = jac * s0r[i];
+            Lr[3 * SLOTS + 3 + i] = jac * scr[i];
+        }
+    }
+    __syncwarp();
+    if (slot_f >= 0) combine_store<3, NJ>(A, Lf, slot_f, lane);
+    if (slot_r >= 0) combine_store<3, NJ>(A, Lr, slot_r, lane);
+    __syncwarp();
+}
+
 __device__ __forceinline__ double exact_dot3(const double *a, const double *b)
 {
     // (a0*b0 + a1*b1) + a2*b2, each step rounded (no FMA contraction)
@@ -616,6 +821,47 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
     }
 }
 
+// K1 body for K with both orientations: separated pairs (e, f) of one
+// (test row e, segment) item, evaluated as the canonical pair (min, max).
+// Pairs with both rows in the chunk are produced once (by the smaller row);
+// a pair whose other row lies outside the chunk is still evaluated in its
+// canonical orientation and only this row's output is stored.
+template <int NJ>
+__device__ __forceinline__ void regular_item_dual(const PairArgs &A, int64_t e, int64_t seg, const Slots<1, NJ> &T,
+                                                  double *geo, double *Ls, int lane, const double *tab)
+{
+    const hb_mesh_desc &M = A.m;
+    const int64_t fb = seg * A.seg_len;
+    const int64_t fe = min(fb + A.seg_len, M.E_x);
+    if (fb >= fe) return;
+    const int64_t t_lo = __ldg(M.tn_indptr_dev + e), t_hi = __ldg(M.tn_indptr_dev + e + 1);
+    for (int64_t f = fb; f < fe; ++f) {
+        const bool f_in = f >= A.e0 && f < A.e1;
+        if (f < e && f_in) continue;                           // the canonical pair (f, e) belongs to row f
+        if (touching_pos(M, t_lo, t_hi, f) >= 0) continue;     // touching pairs: singular path (f == e too)
+        const int64_t a = f > e ? e : f, b = f > e ? f : e;
+        const int64_t slot_f = (a >= A.e0 && a < A.e1) ? (a - A.e0) * M.E_x + b : -1;   // test a, trial b
+        const int64_t slot_r = (b >= A.e0 && b < A.e1) ? (b - A.e0) * M.E_x + a : -1;   // test b, trial a
+        double ca[3];
+        for (int c = 0; c < 3; ++c) ca[c] = __ldg(M.centroids_dev + 3 * a + c);
+        const bool near = near_test(M, ca, __ldg(M.diameters_dev + a), b);
+        RegularGeom g;
+        const int nq1 = near ? (int)M.n_near : (int)M.n_reg;
+        const double *pts = near ? M.near_pts_dev : M.reg_pts_dev;
+        g.xp = pts + 3 * a * nq1;
+        g.yp = pts + 3 * b * nq1;
+        g.w = near ? M.near_w_dev : M.reg_w_dev;
+        g.hats = near ? M.near_hats_dev : M.reg_hats_dev;
+        g.nq1 = nq1;
+        double nb[3], na[3];
+        for (int c = 0; c < 3; ++c) {
+            nb[c] = __ldg(M.normals_dev + 3 * b + c);
+            na[c] = __ldg(M.normals_dev + 3 * a + c);
+        }
+        eval_pair_dual<NJ>(A, g, nq1 * nq1, nb, na, pair_jac<1>(A, a, b), slot_f, slot_r, T, geo, Ls, lane, tab);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K2 body: one touching pair (identical / common edge / common vertex),
 // Sauter-Schwab rule on the permuted charts of classify_pair.
@@ -670,7 +916,7 @@ __device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, cons
 // two quadrature families never share a warp; dynamic fetching removes the
 // imbalance of upper-triangular / near-diagonal tiles.
 // ---------------------------------------------------------------------------
-template <int OP, bool TP1, bool SP1, int NJ, bool SYM>
+template <int OP, bool TP1, bool SP1, int NJ, bool SYM, bool DUAL = false>
 __global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_PAIR_MINB) k_pairs(const PairArgs A)
 {
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
@@ -679,8 +925,10 @@ __global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_
     double *tab = smem;
     special::load_table<OP>(tab);
     __syncthreads();
-    double *geo = smem + special::kTabDoubles + warp * smem_doubles_per_warp<OP, NIJ, NJ>();
+    constexpr int kPerWarp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
+    double *geo = smem + special::kTabDoubles + warp * kPerWarp;
     double *Ls = geo + 32 * Layout<OP, NIJ>::PAY;
+    double *Ls_dual = geo + 32 * kDualPay;
     const hb_mesh_desc &M = A.m;
     const int64_t s_lo = __ldg(M.sing_rowptr_dev + A.e0), s_hi = __ldg(M.sing_rowptr_dev + A.e1);
     int64_t n_sing = s_hi - s_lo;
@@ -699,7 +947,8 @@ __global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_
             singular_item<OP, TP1, SP1, NJ>(A, s_lo + item, T, geo, Ls, lane, tab);
         } else if (item - n_sing < n_reg) {
             const int64_t r = item - n_sing;
-            regular_item<OP, TP1, SP1, NJ, SYM>(A, A.e0 + r / nseg, r % nseg, T, geo, Ls, lane, tab);
+            if constexpr (DUAL) regular_item_dual<NJ>(A, A.e0 + r / nseg, r % nseg, T, geo, Ls_dual, lane, tab);
+            else regular_item<OP, TP1, SP1, NJ, SYM>(A, A.e0 + r / nseg, r % nseg, T, geo, Ls, lane, tab);
         } else {
             break;
         }
@@ -985,13 +1234,14 @@ static size_t row_bytes(const hb_mesh_desc *m, const hb_assembly_desc *a)
     return (size_t)m->E_x * op_shape(a).NIJ * W * sizeof(double);
 }
 
-template <int OP, bool TP1, bool SP1, int NJ>
+template <int OP, bool TP1, bool SP1, int NJ, bool DUAL = false>
 static int launch_pairs(const PairArgs &A, cudaStream_t st)
 {
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     constexpr bool SYM = (OP != 1);
-    const size_t sm = ((size_t)kWarps * smem_doubles_per_warp<OP, NIJ, NJ>() + special::kTabDoubles) * sizeof(double);
-    auto kp = k_pairs<OP, TP1, SP1, NJ, SYM>;
+    constexpr int per_warp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
+    const size_t sm = ((size_t)kWarps * per_warp + special::kTabDoubles) * sizeof(double);
+    auto kp = k_pairs<OP, TP1, SP1, NJ, SYM, DUAL>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
@@ -1015,6 +1265,13 @@ static int launch_pairs(const PairArgs &A, cudaStream_t st)
 template <int OP, bool TP1, bool SP1>
 static int dispatch_nj(int nj, const PairArgs &A, cudaStream_t st)
 {
+    if constexpr (OP == 1) {   // K: both orientations of a separated pair per evaluation (HB_K_DUAL=0: off)
+        static const bool dual = !getenv("HB_K_DUAL") || atoi(getenv("HB_K_DUAL")) != 0;
+        if (dual) {
+            if (nj == 1) return launch_pairs<OP, TP1, SP1, 1, true>(A, st);
+            return launch_pairs<OP, TP1, SP1, 2, true>(A, st);
+        }
+    }
     if (nj == 1) return launch_pairs<OP, TP1, SP1, 1>(A, st);
     return launch_pairs<OP, TP1, SP1, 2>(A, st);
 }
