@@ -22,6 +22,9 @@
  *   hb_toeplitz_apply        heatbem/solver.py:47-73 (apply_toeplitz).
  *   hb_forward_subst_step    heatbem/solver.py:178-182 (history update of
  *                            forward_block_solve).
+ *   hb_project_data          heatbem/field.py:84-119 (project_to_space) for
+ *                            heat-kernel data; hb_p1_mass_solve its X10 mass
+ *                            solve; hb_error_sigma field.py:193-215.
  */
 #ifndef HEATBEM_B200_H
 #define HEATBEM_B200_H
@@ -232,6 +235,55 @@ int hb_forward_history(int64_t n_blocks, int64_t R, int64_t C, const double *blo
  * (A^0)^{-1} step of forward_block_solve (solver.py:183). */
 int hb_inv_apply(int64_t n, const double *inv_dev, const double *rhs_dev, const double *h_dev,
                  double *x_dev, void *stream);
+
+/* ---- boundary data (heatbem/field.py:84-119 project_to_space, :193-215
+ * relative_error_sigma) for the heat-kernel data family of the study driver
+ * (ManufacturedSolution, field.py:20-44):
+ *   HB_DATUM_VALUE         G_alpha(x - src, t + time_shift)        kernels.py:59-66
+ *   HB_DATUM_NORMAL_DERIV  alpha dG_alpha/dn_x (x - src, t + shift) kernels.py:69-86
+ * (zero for t + shift <= 0).  Tensor rule: the order-6 triangle rule
+ * (qpts (E_x,nq,3), qw (nq,), hats (nq,3)) x n_tq <= 8 Gauss points per step
+ * (tq, tw on [0,1]); t = i h + tq h as TimeGrid.node(i) + q h. */
+#define HB_DATUM_VALUE 0
+#define HB_DATUM_NORMAL_DERIV 1
+typedef struct {
+    int kind;
+    double src[3];
+    double alpha;
+    double time_shift;
+} hb_heat_datum;
+
+typedef struct {
+    int64_t E_x, N_x, nq;
+    const double *qpts_dev, *qw_dev, *hats_dev;
+    const double *areas_dev, *normals_dev;
+    const int64_t *tri_nodes_dev;
+    const int64_t *star_indptr_dev, *star_elem_dev, *star_local_dev;   /* node stars, as hb_mesh_desc */
+    int64_t n_tq;
+    double tq[8], tw[8];
+} hb_data_desc;
+
+/* L2(Sigma_h) projection of the datum: space 0 (X00) -> out (E_t, E_x),
+ * space 1 (X10) -> out (E_t, N_x), the p1 mass system solved per time step by
+ * Jacobi-PCG to ||r|| <= tol ||b|| (max_iter steps at most; the reference
+ * factorises the dense mass matrix, field.py:106-118).  X10 needs
+ * hb_project_workspace bytes; max_iters_out (optional, host) receives the
+ * largest CG iteration count and makes the call synchronous. */
+size_t hb_project_workspace(const hb_data_desc *data, int space, int64_t E_t);
+int hb_project_data(const hb_data_desc *data, const hb_heat_datum *g, int space, int64_t E_t, double step,
+                    double *out_dev, void *work_dev, size_t work_bytes, double tol, int64_t max_iter,
+                    int64_t *max_iters_out, void *stream);
+/* x_i = M^{-1} b_i for the p1 mass matrix (field.py:73-81), i < E_t; b, x
+ * (E_t, N_x); workspace 3 E_t N_x doubles. */
+int hb_p1_mass_solve(const hb_data_desc *data, int64_t E_t, const double *b_dev, double *x_dev, void *work_dev,
+                     size_t work_bytes, double tol, int64_t max_iter, void *stream);
+/* out2 = [sum w h 2A qw (g - u_h)^2, sum w h 2A qw g^2] over all steps,
+ * elements and nodes (relative error = sqrt(out2[0] / out2[1])); coeff
+ * (E_t, N_x) if p1 else (E_t, E_x); workspace 2 E_t E_x doubles.
+ * Fixed-order sums (deterministic). */
+int hb_error_sigma(const hb_data_desc *data, const hb_heat_datum *g, int64_t E_t, double step,
+                   const double *coeff_dev, int p1, double *out2_dev, void *work_dev, size_t work_bytes,
+                   void *stream);
 
 /* FP64 DFMA throughput probe used for the roofline denominator:
  * runs `iters` dependent-chain iterations of 8 independent DFMA streams per

@@ -64,6 +64,19 @@ class AssemblyDesc(ctypes.Structure):
     ]
 
 
+class HeatDatum(ctypes.Structure):
+    _fields_ = [("kind", _INT), ("src", _D * 3), ("alpha", _D), ("time_shift", _D)]
+
+
+class DataDesc(ctypes.Structure):
+    _fields_ = [
+        ("E_x", _I64), ("N_x", _I64), ("nq", _I64),
+        ("qpts_dev", _P), ("qw_dev", _P), ("hats_dev", _P), ("areas_dev", _P), ("normals_dev", _P),
+        ("tri_nodes_dev", _P), ("star_indptr_dev", _P), ("star_elem_dev", _P), ("star_local_dev", _P),
+        ("n_tq", _I64), ("tq", _D * 8), ("tw", _D * 8),
+    ]
+
+
 # every symbol include/heatbem_b200.h declares (checked by tests/test_capi.py)
 EXPORTED = (
     "hb_version", "hb_last_error", "hb_assemble", "hb_assemble_min_workspace",
@@ -71,6 +84,7 @@ EXPORTED = (
     "hb_toeplitz_apply", "hb_forward_subst_step", "hb_fp64_probe", "hb_pair_classes",
     "hb_toeplitz_apply_range", "hb_curl_workspace", "hb_ipc_export", "hb_ipc_import", "hb_ipc_close",
     "hb_forward_solve", "hb_forward_history", "hb_inv_apply", "hb_represent_grid",
+    "hb_project_workspace", "hb_project_data", "hb_p1_mass_solve", "hb_error_sigma",
 )
 
 _lib = None
@@ -122,6 +136,16 @@ def load():
     L.hb_represent_grid.argtypes = [_I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P, _P,
                                     _D, _D, _D, _D, _P, _P]
     L.hb_represent_grid.restype = _INT
+    L.hb_project_workspace.argtypes = [ctypes.POINTER(DataDesc), _INT, _I64]
+    L.hb_project_workspace.restype = ctypes.c_size_t
+    L.hb_project_data.argtypes = [ctypes.POINTER(DataDesc), ctypes.POINTER(HeatDatum), _INT, _I64, _D, _P, _P,
+                                  ctypes.c_size_t, _D, _I64, ctypes.POINTER(_I64), _P]
+    L.hb_project_data.restype = _INT
+    L.hb_p1_mass_solve.argtypes = [ctypes.POINTER(DataDesc), _I64, _P, _P, _P, ctypes.c_size_t, _D, _I64, _P]
+    L.hb_p1_mass_solve.restype = _INT
+    L.hb_error_sigma.argtypes = [ctypes.POINTER(DataDesc), ctypes.POINTER(HeatDatum), _I64, _D, _P, _INT, _P, _P,
+                                 ctypes.c_size_t, _P]
+    L.hb_error_sigma.restype = _INT
     _lib = L
     return L
 

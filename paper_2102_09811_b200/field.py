@@ -8,9 +8,12 @@ form for "M points x all time-step ends" (BASELINE config 4).  Evaluation
 points are grouped by (x, eps) so that one warp evaluates the kernel history
 of a spatial point once for all its output times (csrc/hb_field.cu).
 
-``project_to_space`` / ``relative_error_sigma`` / ``ManufacturedSolution``
-are the reference's host utilities (field.py:20-221), kept in numpy: they
-build the right-hand side of the Dirichlet solve and measure errors.
+``project_to_space`` / ``relative_error_sigma`` (field.py:84-119, 193-215)
+run on the device (csrc/hb_data.cu) whenever the datum is one the GPU can
+evaluate -- a :class:`HeatKernelDatum` or a trace method of
+:class:`ManufacturedSolution` (the study driver's data); an arbitrary Python
+callable can only be evaluated on the host, so for those the reference's
+numpy algorithm runs as before.
 """
 from __future__ import annotations
 
@@ -50,6 +53,45 @@ class ManufacturedSolution:
 
 
 @dataclass(frozen=True)
+class HeatKernelDatum:
+    """Boundary datum the GPU evaluates: ``kind="value"`` is
+    G_alpha(x - source_point, t + time_shift) (kernels.py:59-66),
+    ``kind="normal_derivative"`` is alpha dG_alpha/dn_x at the same
+    arguments (kernels.py:69-86).  Callable like the reference's data
+    functions ``fn(points, t, normals)`` (numpy, host)."""
+
+    source_point: tuple
+    alpha: float
+    time_shift: float = 0.0
+    kind: str = "value"
+
+    def __post_init__(self):
+        if self.kind not in ("value", "normal_derivative"):
+            raise ValueError("kind must be 'value' or 'normal_derivative'")
+        object.__setattr__(self, "source_point", tuple(float(v) for v in np.ravel(self.source_point)))
+
+    def __call__(self, points, t, normals=None):
+        r = np.asarray(points) - np.asarray(self.source_point)
+        if self.kind == "value":
+            return fundamental(r, t + self.time_shift, self.alpha)
+        return grad_fundamental_normal(r, normals, t + self.time_shift, self.alpha)
+
+
+def device_datum(fn):
+    """The :class:`HeatKernelDatum` equivalent of fn, or None when fn is an
+    arbitrary callable (host-only)."""
+    if isinstance(fn, HeatKernelDatum):
+        return fn
+    owner = getattr(fn, "__self__", None)
+    if isinstance(owner, ManufacturedSolution):
+        name = getattr(fn, "__name__", "")
+        kind = {"value": "value", "dirichlet_trace": "value", "neumann_trace": "normal_derivative"}.get(name)
+        if kind is not None and getattr(type(owner), name) is getattr(ManufacturedSolution, name):
+            return HeatKernelDatum(tuple(owner.source_point), float(owner.alpha), 0.0, kind)
+    return None
+
+
+@dataclass(frozen=True)
 class EvalPoint:
     """Interior point x at time t = k h_t + eps (heatbem/field.py:45-58)."""
 
@@ -78,11 +120,137 @@ def _p1_mass(mesh) -> sp.csr_matrix:
     return sp.csr_matrix((vals, (rows, cols)), shape=(mesh.n_vertices,) * 2)
 
 
-def project_to_space(fn, mesh, timegrid, space: str) -> np.ndarray:
-    """L2(Sigma) projection onto X00 (p0 x p0) or X10 (p1 x p0): (E_t, n_dof)
-    (heatbem/field.py:84-119; triangle order 6, 4 Gauss points per step)."""
+# ---------------------------------------------------------------------------
+# boundary data on the device (csrc/hb_data.cu)
+# ---------------------------------------------------------------------------
+
+class _DataTables:
+    """Order-6 triangle rule, 4-point time rule and node stars on the device."""
+
+    def __init__(self, mesh, device):
+        import torch
+
+        hats, qw, qpts = rule_tables(mesh, _NORM_TRI_ORDER)
+        tq, tw = gauss01(_NORM_TIME_POINTS)
+        up = lambda a, dt=torch.float64: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=device)  # noqa
+        indptr, elem, local = mesh.node_star()
+        self.t = {"qpts": up(qpts), "qw": up(qw), "hats": up(hats), "areas": up(mesh.areas),
+                  "normals": up(mesh.normals), "tri": up(mesh.triangles, torch.int64),
+                  "indptr": up(indptr, torch.int64), "elem": up(elem, torch.int64),
+                  "local": up(local, torch.int64)}
+        d = _native.DataDesc()
+        d.E_x, d.N_x, d.nq = mesh.n_triangles, mesh.n_vertices, len(qw)
+        P = _native.ptr
+        d.qpts_dev, d.qw_dev, d.hats_dev = P(self.t["qpts"]), P(self.t["qw"]), P(self.t["hats"])
+        d.areas_dev, d.normals_dev, d.tri_nodes_dev = P(self.t["areas"]), P(self.t["normals"]), P(self.t["tri"])
+        d.star_indptr_dev, d.star_elem_dev = P(self.t["indptr"]), P(self.t["elem"])
+        d.star_local_dev = P(self.t["local"])
+        d.n_tq = len(tq)
+        for i in range(len(tq)):
+            d.tq[i], d.tw[i] = float(tq[i]), float(tw[i])
+        self.desc = d
+        self.device = device
+
+
+_DATA_CACHE: dict = {}
+
+
+def _data_tables(mesh, device=None):
+    import torch
+    import weakref
+
+    _native.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    key = (id(mesh), str(dev))
+    hit = _DATA_CACHE.get(key)
+    if hit is None or hit[0]() is not mesh:
+        hit = (weakref.ref(mesh), _DataTables(mesh, dev))
+        _DATA_CACHE[key] = hit
+    return hit[1]
+
+
+def _datum_struct(g: HeatKernelDatum) -> "_native.HeatDatum":
+    h = _native.HeatDatum()
+    h.kind = 0 if g.kind == "value" else 1
+    for i in range(3):
+        h.src[i] = g.source_point[i]
+    h.alpha, h.time_shift = float(g.alpha), float(g.time_shift)
+    return h
+
+
+#: X10 mass solve: Jacobi-PCG per time step to ||r|| <= tol ||b||
+MASS_CG_TOL = 1e-15
+MASS_CG_MAX_ITER = 1000
+
+
+def project_data_device(datum: HeatKernelDatum, mesh, timegrid, space: str, stream=None):
+    """project_to_space of a device datum on the GPU; returns the (E_t, n_dof)
+    float64 tensor and the largest CG iteration count (X10; 0 for X00)."""
+    import ctypes
+
+    import torch
+
     if space not in ("X00", "X10"):
         raise ValueError("space must be 'X00' or 'X10'")
+    T = _data_tables(mesh)
+    sp_id = 0 if space == "X00" else 1
+    E_t = timegrid.n_steps
+    n = mesh.n_triangles if sp_id == 0 else mesh.n_vertices
+    out = torch.empty((E_t, n), dtype=torch.float64, device=T.device)
+    L = _native.load()
+    ws = int(L.hb_project_workspace(ctypes.byref(T.desc), sp_id, E_t))
+    work = torch.empty(max(ws, 8), dtype=torch.uint8, device=T.device)
+    iters = ctypes.c_int64(0)
+    _native.call("hb_project_data", ctypes.byref(T.desc), ctypes.byref(_datum_struct(datum)), sp_id, E_t,
+                 float(timegrid.step), _native.ptr(out), _native.ptr(work), ctypes.c_size_t(ws),
+                 MASS_CG_TOL, MASS_CG_MAX_ITER, ctypes.byref(iters) if sp_id == 1 else None,
+                 _native.stream_handle(stream))
+    return out, int(iters.value)
+
+
+def error_sigma_device(coeffs, datum: HeatKernelDatum, mesh, timegrid, stream=None):
+    """(num, den) of relative_error_sigma on the GPU (fixed-order sums)."""
+    import ctypes
+
+    import torch
+
+    T = _data_tables(mesh)
+    c = torch.as_tensor(coeffs, dtype=torch.float64, device=T.device).contiguous()
+    if c.ndim != 2 or c.shape[0] != timegrid.n_steps or c.shape[1] not in (mesh.n_triangles, mesh.n_vertices):
+        raise ValueError("coefficients must be (E_t, E_x) or (E_t, N_x)")
+    p1 = int(c.shape[1] == mesh.n_vertices and c.shape[1] != mesh.n_triangles)
+    out2 = torch.empty(2, dtype=torch.float64, device=T.device)
+    nb = 16 * timegrid.n_steps * mesh.n_triangles
+    work = torch.empty(nb, dtype=torch.uint8, device=T.device)
+    _native.call("hb_error_sigma", ctypes.byref(T.desc), ctypes.byref(_datum_struct(datum)), timegrid.n_steps,
+                 float(timegrid.step), _native.ptr(c), p1, _native.ptr(out2), _native.ptr(work),
+                 ctypes.c_size_t(nb), _native.stream_handle(stream))
+    num, den = out2.cpu().tolist()
+    return num, den
+
+
+def project_to_space(fn, mesh, timegrid, space: str, return_device: bool = False):
+    """L2(Sigma) projection onto X00 (p0 x p0) or X10 (p1 x p0): (E_t, n_dof)
+    (heatbem/field.py:84-119; triangle order 6, 4 Gauss points per step).
+    Device datum (HeatKernelDatum / ManufacturedSolution trace): computed on
+    the GPU (X10 mass system by PCG instead of the reference's dense
+    Cholesky; agrees to ~1e-15); any other callable: the reference's host
+    algorithm (``return_device`` then uploads the result)."""
+    if space not in ("X00", "X10"):
+        raise ValueError("space must be 'X00' or 'X10'")
+    g = device_datum(fn)
+    if g is not None:
+        out, _ = project_data_device(g, mesh, timegrid, space)
+        return out if return_device else out.cpu().numpy()
+    res = _project_host(fn, mesh, timegrid, space)
+    if return_device:
+        import torch
+
+        return torch.as_tensor(res, device=torch.device("cuda", torch.cuda.current_device()))
+    return res
+
+
+def _project_host(fn, mesh, timegrid, space: str) -> np.ndarray:
     hats, qw, qpts = rule_tables(mesh, _NORM_TRI_ORDER)
     tq, tw = gauss01(_NORM_TIME_POINTS)
     h, E_t, E_x = timegrid.step, timegrid.n_steps, mesh.n_triangles
@@ -109,7 +277,16 @@ def project_to_space(fn, mesh, timegrid, space: str) -> np.ndarray:
 
 
 def relative_error_sigma(coeffs, fn, mesh, timegrid) -> float:
-    """Relative L2(Sigma_h) error of a coefficient function against fn."""
+    """Relative L2(Sigma_h) error of a coefficient function against fn
+    (heatbem/field.py:193-215); on the GPU for a device datum."""
+    g = device_datum(fn)
+    if g is not None:
+        num, den = error_sigma_device(coeffs, g, mesh, timegrid)
+        if den == 0.0:
+            raise ValueError("exact function has zero L2(Sigma) norm")
+        return float(np.sqrt(num / den))
+    if not isinstance(coeffs, np.ndarray) and hasattr(coeffs, "cpu"):
+        coeffs = coeffs.cpu().numpy()
     hats, qw, qpts = rule_tables(mesh, _NORM_TRI_ORDER)
     tq, tw = gauss01(_NORM_TIME_POINTS)
     coeffs = np.asarray(coeffs)
@@ -255,7 +432,8 @@ def _eval_potential(kind, coeffs, points, mesh, timegrid, params, config=Quadrat
     t = np.array([float(p.t) for p in points])
     k, eps = _decompose(t, timegrid.step)
     cur = (eps > 0.0) & (k < timegrid.n_steps)
-    vals = _eval_grouped(kind, np.asarray(coeffs), xs, k, eps, cur, mesh, timegrid, params, config)
+    coeffs = coeffs if isinstance(coeffs, torch.Tensor) else np.asarray(coeffs)
+    vals = _eval_grouped(kind, coeffs, xs, k, eps, cur, mesh, timegrid, params, config)
     T = _tables(mesh, config, vals.device)
     warn = _boundary_warnings(torch.as_tensor(xs, device=vals.device), mesh, T)
     return vals.cpu().numpy(), warn.cpu().numpy()
