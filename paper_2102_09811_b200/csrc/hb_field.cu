@@ -655,9 +655,14 @@ __device__ __forceinline__ void eval_erf_E(double x, const double *__restrict__ 
         double u;
         const int pc = special::mid_piece(x, u);
         const double *cs = tabS + pc, *cd = tabD + pc;
-        double qs = cs[special::kMidDeg * special::kMidPieces], qd = cd[special::kMidDeg * special::kMidPieces];
+        // erf (degree DS) and E (degree DD >= DS): E's leading steps alone, then both chains
+        constexpr int DS = special::mid_deg<2>(), DD = special::mid_deg<3>();
+        static_assert(DD >= DS, "E's middle-region degree must not be below erf's");
+        double qs = cs[DS * special::kMidPieces], qd = cd[DD * special::kMidPieces];
 #pragma unroll
-        for (int k = special::kMidDeg - 1; k >= 0; --k) {
+        for (int k = DD - 1; k >= DS; --k) qd = fma(qd, u, cd[k * special::kMidPieces]);
+#pragma unroll
+        for (int k = DS - 1; k >= 0; --k) {
             qs = fma(qs, u, cs[k * special::kMidPieces]);
             qd = fma(qd, u, cd[k * special::kMidPieces]);
         }

@@ -12,9 +12,12 @@
 // e^{-x^2}/rho, cancels like 1/x^2 for small x; F(x) = x Pf(x^2) does not.
 //
 //   x <  X0 (= 1):  H = 2/(sqrt(pi) x) + x Ph(t), F = x Pf(t), erf = x Pe(t),
-//                   E = x^3 Pg(t), t = x^2 (coefficients uniform across the warp)
-//   X0 <= x < XL:   the function value itself as a degree-12 polynomial in
+//                   E = x^3 Pg(t), t = x^2 (coefficients uniform across the warp;
+//                   degrees 10 / 10 / 11 / 11)
+//   X0 <= x < XL:   the function value itself as a polynomial in
 //                   u = (x - mid_p) / half on 21 uniform pieces of width 1/4
+//                   (degree 12 for H, 10 for F and erf, 11 for E: per kind the
+//                   lowest degree that keeps the double Horner within 2.3e-16)
 //                   (coefficients of the lane's piece from shared memory) --
 //                   all four functions are analytic there, no exp is needed
 //   x >= XL (6.25): the asymptote, erf = E = 1, H/F = 1 +- 1/(2x^2), which
@@ -38,14 +41,17 @@ __device__ unsigned long long g_branch_count[4];   // [small?1:0 + large?2:0]
 
 // shared-memory table: the middle-region coefficients of one function
 // (coefficient k of piece p at tab[k * kMidPieces + p]: lanes in different
-// pieces read neighbouring words)
-constexpr int kTabDoubles = (kMidDeg + 1) * kMidPieces;
+// pieces read neighbouring words); kTabDoubles = room for any kind
+constexpr int kTabDoubles = (kMidDegMax + 1) * kMidPieces;
+
+template <int KIND>
+__host__ __device__ constexpr int mid_deg() { return kMidDegK[KIND]; }
 
 template <int KIND>
 __device__ __forceinline__ void load_table(double *tab)
 {
     const double *src = KIND == 0 ? kMid0 : KIND == 1 ? kMid1 : KIND == 2 ? kMid2 : kMid3;
-    for (int i = threadIdx.x; i < kTabDoubles; i += blockDim.x) tab[i] = src[i];
+    for (int i = threadIdx.x; i < (mid_deg<KIND>() + 1) * kMidPieces; i += blockDim.x) tab[i] = src[i];
 }
 
 template <int N>
@@ -110,9 +116,10 @@ __device__ __forceinline__ double eval(double x, double ix, const double *__rest
     if (__any_sync(mask, midr)) {
         double u;
         const double *c = tab + mid_piece(x, u);
-        double q = c[kMidDeg * kMidPieces];
+        constexpr int DEG = mid_deg<KIND>();
+        double q = c[DEG * kMidPieces];
 #pragma unroll
-        for (int k = kMidDeg - 1; k >= 0; --k) q = fma(q, u, c[k * kMidPieces]);
+        for (int k = DEG - 1; k >= 0; --k) q = fma(q, u, c[k * kMidPieces]);
         asm volatile("" : "+d"(q));
         r = midr ? q : r;
     }
@@ -163,15 +170,16 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
         for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], ix[j]);
     }
     if (__any_sync(mask, any_m)) {
+        constexpr int DEG = mid_deg<KIND>();
         double u[NJ], q[NJ];
         const double *c[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             c[j] = tab + mid_piece(x[j], u[j]);
-            q[j] = c[j][kMidDeg * kMidPieces];
+            q[j] = c[j][DEG * kMidPieces];
         }
 #pragma unroll
-        for (int k = kMidDeg - 1; k >= 0; --k)
+        for (int k = DEG - 1; k >= 0; --k)
 #pragma unroll
             for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], u[j], c[j][k * kMidPieces]);
 #pragma unroll
