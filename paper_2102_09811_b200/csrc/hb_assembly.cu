@@ -48,8 +48,8 @@
 #ifndef HB_SEP
 #define HB_SEP 0     // separable p1 x p1 accumulation (slower at 128 registers; kept for study)
 #endif
-#ifndef HB_P1P1_GROUPED   // p1 x p1 through the G-point grouped loop (else one point per iteration)
-#define HB_P1P1_GROUPED 0
+#ifndef HB_P1P1_GROUPED   // p1 x p1 through the G-point grouped loop (1, default: D2 pair kernel -4 %
+#define HB_P1P1_GROUPED 1  // with the per-kind degrees); 0 = one point per iteration
 #endif
 #ifndef HB_P1P1_MINB
 #define HB_P1P1_MINB HB_PAIR_MINB
