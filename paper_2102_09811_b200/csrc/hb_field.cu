@@ -658,13 +658,13 @@ __device__ __forceinline__ void eval_erf_E(double x, const double *__restrict__ 
         // erf (degree DS) and E (degree DD >= DS): E's leading steps alone, then both chains
         constexpr int DS = special::mid_deg<2>(), DD = special::mid_deg<3>();
         static_assert(DD >= DS, "E's middle-region degree must not be below erf's");
-        double qs = cs[DS * special::kMidPieces], qd = cd[DD * special::kMidPieces];
+        double qs = cs[DS * special::kTabStride], qd = cd[DD * special::kTabStride];
 #pragma unroll
-        for (int k = DD - 1; k >= DS; --k) qd = fma(qd, u, cd[k * special::kMidPieces]);
+        for (int k = DD - 1; k >= DS; --k) qd = fma(qd, u, cd[k * special::kTabStride]);
 #pragma unroll
         for (int k = DS - 1; k >= 0; --k) {
-            qs = fma(qs, u, cs[k * special::kMidPieces]);
-            qd = fma(qd, u, cd[k * special::kMidPieces]);
+            qs = fma(qs, u, cs[k * special::kTabStride]);
+            qd = fma(qd, u, cd[k * special::kTabStride]);
         }
         asm volatile("" : "+d"(qs), "+d"(qd));
         rs = midr ? qs : rs;

@@ -39,19 +39,48 @@ namespace special {
 __device__ unsigned long long g_branch_count[4];   // [small?1:0 + large?2:0]
 #endif
 
-// shared-memory table: the middle-region coefficients of one function
-// (coefficient k of piece p at tab[k * kMidPieces + p]: lanes in different
-// pieces read neighbouring words); kTabDoubles = room for any kind
-constexpr int kTabDoubles = (kMidDegMax + 1) * kMidPieces;
+// shared-memory table of one function: coefficient k of middle-region piece
+// p at tab[k * kTabStride + p] (lanes in different pieces read neighbouring
+// words), and in column kMidPieces the small-x series coefficient k -- so a
+// warp whose lanes straddle x = X0 runs ONE Horner chain, each lane with its
+// own variable (t or u) and column.  Rows above a polynomial's degree are
+// zero: leading fma(0, v, 0) / fma(0, v, c) steps are exact, so a lane's value
+// is bitwise the same as from its own region's chain alone (and so still
+// depends on its own x only).
+constexpr int kTabStride = kMidPieces + 1;
 
 template <int KIND>
 __host__ __device__ constexpr int mid_deg() { return kMidDegK[KIND]; }
 
 template <int KIND>
+__host__ __device__ constexpr int series_deg()
+{
+    return (KIND == 0 ? (int)(sizeof(kPh) / sizeof(double)) : KIND == 1 ? (int)(sizeof(kPf) / sizeof(double))
+            : KIND == 2 ? (int)(sizeof(kPe) / sizeof(double)) : (int)(sizeof(kPg) / sizeof(double))) - 1;
+}
+
+template <int KIND>
+__host__ __device__ constexpr int merged_deg() { return mid_deg<KIND>() > series_deg<KIND>() ? mid_deg<KIND>() : series_deg<KIND>(); }
+
+constexpr int kMergedDegMax = (merged_deg<0>() > merged_deg<1>() ? merged_deg<0>() : merged_deg<1>()) >
+                                      (merged_deg<2>() > merged_deg<3>() ? merged_deg<2>() : merged_deg<3>())
+                                  ? (merged_deg<0>() > merged_deg<1>() ? merged_deg<0>() : merged_deg<1>())
+                                  : (merged_deg<2>() > merged_deg<3>() ? merged_deg<2>() : merged_deg<3>());
+constexpr int kTabDoubles = (kMergedDegMax + 1) * kTabStride;   // room for any kind
+
+template <int KIND>
 __device__ __forceinline__ void load_table(double *tab)
 {
-    const double *src = KIND == 0 ? kMid0 : KIND == 1 ? kMid1 : KIND == 2 ? kMid2 : kMid3;
-    for (int i = threadIdx.x; i < (mid_deg<KIND>() + 1) * kMidPieces; i += blockDim.x) tab[i] = src[i];
+    const double *mid = KIND == 0 ? kMid0 : KIND == 1 ? kMid1 : KIND == 2 ? kMid2 : kMid3;
+    const double *ser = KIND == 0 ? kPh : KIND == 1 ? kPf : KIND == 2 ? kPe : kPg;
+    constexpr int DM = mid_deg<KIND>(), DS = series_deg<KIND>(), D = merged_deg<KIND>();
+    for (int i = threadIdx.x; i < (D + 1) * kTabStride; i += blockDim.x) {
+        const int k = i / kTabStride, p = i - k * kTabStride;
+        double v;
+        if (p < kMidPieces) v = k <= DM ? mid[k * kMidPieces + p] : 0.0;
+        else v = k <= DS ? ser[k] : 0.0;
+        tab[i] = v;
+    }
 }
 
 template <int N>
@@ -102,31 +131,13 @@ __device__ __forceinline__ int mid_piece(double x, double &u)
 #endif
 }
 
-// KIND 0: H (single layer), 1: F (double layer), 2: erf (hypersingular D2),
-// 3: E(x) = erf(x) - 2x e^{-x^2}/sqrt(pi) (double-layer potential).
-// ix = 1/x (formed by the caller from precomputed 1/rho and 1/c; used by
-// KIND 0/1 only); `mask` = the lanes executing this call.
+// small-x finish of a series polynomial value q = P(t) (as series<KIND>)
 template <int KIND>
-__device__ __forceinline__ double eval(double x, double ix, const double *__restrict__ tab, unsigned mask)
+__device__ __forceinline__ double series_finish(double x, double t, double ix, double q)
 {
-    const double t = __dmul_rn(x, x);
-    const bool small = x < kX0, huge = x >= kXL, midr = !small && !huge;
-    double r = 0.0;
-    if (__any_sync(mask, small)) r = series<KIND>(x, t, ix);
-    if (__any_sync(mask, midr)) {
-        double u;
-        const double *c = tab + mid_piece(x, u);
-        constexpr int DEG = mid_deg<KIND>();
-        double q = c[DEG * kMidPieces];
-#pragma unroll
-        for (int k = DEG - 1; k >= 0; --k) q = fma(q, u, c[k * kMidPieces]);
-        asm volatile("" : "+d"(q));
-        r = midr ? q : r;
-    }
-    if (__any_sync(mask, huge)) {
-        if (huge) r = asymptote<KIND>(ix);
-    }
-    return r;
+    if (KIND == 0) return fma(x, q, __dmul_rn(kTwoInvSqrtPi, ix));
+    if (KIND == 1 || KIND == 2) return __dmul_rn(x, q);
+    return __dmul_rn(__dmul_rn(x, t), q);
 }
 
 // NJ evaluations of one lane at once: one region pass for the whole group,
@@ -162,31 +173,49 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
             atomicAdd(&g_branch_count[(vs ? 1 : 0) + (vm ? 2 : 0)], 1ull);
     }
 #endif
-    // each region computes every lane's chains unconditionally (the NJ chains
-    // interleave; a per-lane condition would let the compiler sink a chain
-    // into a divergent branch) and lanes keep their own region's value
-    if (__any_sync(mask, any_s)) {
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], ix[j]);
-    }
-    if (__any_sync(mask, any_m)) {
-        constexpr int DEG = mid_deg<KIND>();
-        double u[NJ], q[NJ];
+    // one polynomial pass per warp: the constant-bank series when every lane
+    // is small, else ONE table chain in which small lanes use the series
+    // column with t and middle lanes their piece with u (merged degree when
+    // both occur).  Every chain is computed for all lanes unconditionally (the
+    // NJ chains interleave) and lanes keep their own region's value.
+    const bool vote_m = __any_sync(mask, any_m);
+    if (vote_m) {
+        const bool vote_s = __any_sync(mask, any_s);
+        double v[NJ], q[NJ];
         const double *c[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-            c[j] = tab + mid_piece(x[j], u[j]);
-            q[j] = c[j][DEG * kMidPieces];
+            double u;
+            const int pc = mid_piece(x[j], u);
+            c[j] = tab + (small[j] ? kMidPieces : pc);
+            v[j] = small[j] ? t[j] : u;
         }
+        if (vote_s) {
+            constexpr int DEG = merged_deg<KIND>();
 #pragma unroll
-        for (int k = DEG - 1; k >= 0; --k)
+            for (int j = 0; j < NJ; ++j) q[j] = c[j][DEG * kTabStride];
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], u[j], c[j][k * kMidPieces]);
+            for (int k = DEG - 1; k >= 0; --k)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], c[j][k * kTabStride]);
+        } else {
+            constexpr int DEG = mid_deg<KIND>();
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) q[j] = c[j][DEG * kTabStride];
+#pragma unroll
+            for (int k = DEG - 1; k >= 0; --k)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], c[j][k * kTabStride]);
+        }
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             asm volatile("" : "+d"(q[j]));
-            r[j] = midr[j] ? q[j] : r[j];
+            const double fs = series_finish<KIND>(x[j], t[j], ix[j], q[j]);
+            r[j] = small[j] ? fs : (midr[j] ? q[j] : r[j]);
         }
+    } else if (__any_sync(mask, any_s)) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], ix[j]);
     }
     bool any_h = false;
 #pragma unroll
@@ -196,6 +225,19 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
         for (int j = 0; j < NJ; ++j)
             if (huge[j]) r[j] = asymptote<KIND>(ix[j]);
     }
+}
+
+// KIND 0: H (single layer), 1: F (double layer), 2: erf (hypersingular D2),
+// 3: E(x) = erf(x) - 2x e^{-x^2}/sqrt(pi) (double-layer potential).
+// ix = 1/x (formed by the caller from precomputed 1/rho and 1/c; used by
+// KIND 0/1 only); `mask` = the lanes executing this call.
+template <int KIND>
+__device__ __forceinline__ double eval(double x, double ix, const double *__restrict__ tab, unsigned mask)
+{
+    double r[1];
+    const double xs[1] = {x}, is[1] = {ix};
+    eval_n<KIND, 1>(xs, is, r, tab, mask);
+    return r[0];
 }
 
 }  // namespace special
