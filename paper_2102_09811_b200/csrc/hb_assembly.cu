@@ -75,9 +75,13 @@ struct PairArgs {
 
 template <int OP, int NIJ>
 struct Layout {
-    // payload per quadrature point: [rho, s1, s2, H[NIJ]] (OP 0/1) or [rho, s1, H] (OP 2)
+    // payload per quadrature point: [rho, s1, s2, H[NIJ]] (OP 0/1) or [rho, s1, H] (OP 2);
+    // V (OP 0, NIJ 1) adds s1 H at FOFF (the grouped loop's weight: one FMA per
+    // evaluation instead of a multiply and an FMA)
     static constexpr int HOFF = (OP == 2) ? 2 : 3;
-    static constexpr int PAY_RAW = HOFF + NIJ;
+    static constexpr bool FOLD = (OP == 0 && NIJ == 1);
+    static constexpr int FOFF = HOFF + NIJ;
+    static constexpr int PAY_RAW = HOFF + NIJ + (FOLD ? 1 : 0);
     static constexpr int PAY = (PAY_RAW + 1) & ~1;
 };
 
@@ -229,7 +233,13 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
     for (int base = 0; base < nq; base += 32) {
         const int q = base + lane;
         int small = 0;
-        if (q < nq) {
+        if (q >= nq) {
+            // padding slot of the grouped loop: all zero (x = 0 and 1/x = 0 give
+            // finite series values, the zero weights add exact zeros)
+            double *p = geo + lane * PAY;
+#pragma unroll
+            for (int i = 0; i < PAY; ++i) p[i] = 0.0;
+        } else {
             double x[3], y[3], wq, ht[3], hs[3];
             g.point(q, x, y, wq, ht, hs);
             const double rx = x[0] - y[0], ry = x[1] - y[1], rz = x[2] - y[2];
@@ -261,6 +271,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
 #pragma unroll
                     for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
                 }
+                if constexpr (L::FOLD) p[L::FOFF] = __dmul_rn(Aq, H[0]);
                 if (A.need_special) {
                     const double cq = A.step * Bq + Aq;
 #pragma unroll
@@ -358,14 +369,18 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                 // G points of the same parity per branch region (x close -> the
                 // small/large-x skipping survives; G independent Horner chains)
                 constexpr int G = HB_QGROUP;
+                static_assert(32 % (2 * G) == 0, "padded group loop must stay inside the warp's 32 payload slots");
                 const int nlocg = (nloc + 2 * G - 1) / (2 * G) * (2 * G);
+                // (slots nloc..nlocg-1 hold the all-zero padding payload)
+                // (p1 x p1 keeps the explicit select: measured faster there)
+                constexpr bool SEL = NIJ == 9;
                 for (int k = s; k < nlocg; k += 2 * G) {
-                    bool ok[G];
                     const double *pp[G];
                     double rho[G], a[G], b[G];
+                    bool ok[G];
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
-                        ok[g] = k + 2 * g < nloc;
+                        ok[g] = !SEL || k + 2 * g < nloc;
                         pp[g] = geo + (ok[g] ? k + 2 * g : 0) * PAY;
                         rho[g] = pp[g][0];
                         a[g] = pp[g][1];
@@ -382,9 +397,13 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                         special::eval_n<OP, G>(xs, ixs, fs, tab, kFull);
 #pragma unroll
                         for (int g = 0; g < G; ++g) {
-                            const double v = ok[g] ? (OP == 1 ? fs[g] : __dmul_rn(a[g], fs[g])) : 0.0;
+                            if constexpr (L::FOLD) {
+                                acc[j][0] = fma(fs[g], pp[g][L::FOFF], acc[j][0]);
+                            } else {
+                                const double v = ok[g] ? (OP == 1 ? fs[g] : __dmul_rn(a[g], fs[g])) : 0.0;
 #pragma unroll
-                            for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, pp[g][HOFF + i], acc[j][i]);
+                                for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, pp[g][HOFF + i], acc[j][i]);
+                            }
                         }
                     }
                 }
@@ -576,7 +595,11 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
     for (int base = 0; base < nq; base += 32) {
         const int q = base + lane;
         int small = 0;
-        if (q < nq) {
+        if (q >= nq) {   // all-zero padding slot (see eval_pair)
+            double *p = geo + lane * PAY;
+#pragma unroll
+            for (int i = 0; i < PAY; ++i) p[i] = 0.0;
+        } else {
             double x[3], y[3], wq, ht[3], hs[3];
             g.point(q, x, y, wq, ht, hs);
             const double rx = x[0] - y[0], ry = x[1] - y[1], rz = x[2] - y[2];
@@ -615,15 +638,14 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
         const int nloc = min(32, nq - base);
         if (!any_small) {
             constexpr int G = HB_QGROUP;
+            static_assert(32 % (2 * G) == 0, "padded group loop must stay inside the warp's 32 payload slots");
             const int nlocg = (nloc + 2 * G - 1) / (2 * G) * (2 * G);
-            for (int k = s; k < nlocg; k += 2 * G) {
-                bool ok[G];
+            for (int k = s; k < nlocg; k += 2 * G) {   // padding slots are all zero
                 const double *pp[G];
                 double rho[G], a[G];
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
-                    ok[gg] = k + 2 * gg < nloc;
-                    pp[gg] = geo + (ok[gg] ? k + 2 * gg : 0) * PAY;
+                    pp[gg] = geo + (k + 2 * gg) * PAY;
                     rho[gg] = pp[gg][0];
                     a[gg] = pp[gg][1];
                 }
@@ -638,11 +660,10 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
                     special::eval_n<1, G>(xs, ixs, fs, tab, kFull);
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
-                        const double v = ok[gg] ? fs[gg] : 0.0;
 #pragma unroll
                         for (int i = 0; i < 3; ++i) {
-                            af[j][i] = fma(v, pp[gg][3 + i], af[j][i]);
-                            ar[j][i] = fma(v, pp[gg][6 + i], ar[j][i]);
+                            af[j][i] = fma(fs[gg], pp[gg][3 + i], af[j][i]);
+                            ar[j][i] = fma(fs[gg], pp[gg][6 + i], ar[j][i]);
                         }
                     }
                 }
