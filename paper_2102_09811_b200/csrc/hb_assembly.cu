@@ -75,13 +75,11 @@ struct PairArgs {
 
 template <int OP, int NIJ>
 struct Layout {
-    // payload per quadrature point: [rho, s1, s2, H[NIJ]] (OP 0/1) or [rho, s1, H] (OP 2);
-    // V (OP 0, NIJ 1) adds s1 H at FOFF (the grouped loop's weight: one FMA per
-    // evaluation instead of a multiply and an FMA)
+    // payload per quadrature point: [rho, s1, s2, W[NIJ]] (OP 0/1) or [rho, s1, W] (OP 2);
+    // W = the weight of the factor-free kernel value (hb_special.cuh kinds 4-6):
+    // w ht hs for V and D2, w ht hs (-r.n_y)/(2a) for K
     static constexpr int HOFF = (OP == 2) ? 2 : 3;
-    static constexpr bool FOLD = (OP == 0 && NIJ == 1);
-    static constexpr int FOFF = HOFF + NIJ;
-    static constexpr int PAY_RAW = HOFF + NIJ + (FOLD ? 1 : 0);
+    static constexpr int PAY_RAW = HOFF + NIJ;
     static constexpr int PAY = (PAY_RAW + 1) & ~1;
 };
 
@@ -99,7 +97,7 @@ __host__ __device__ constexpr int smem_doubles_per_warp() { return 32 * Layout<O
 // ---------------------------------------------------------------------------
 template <int OP, int NJ>
 struct Slots {
-    double dl[NJ], cx[NJ], ic[NJ], kk[NJ];
+    double dl[NJ], cx[NJ], ic[NJ], kk[NJ], sc[NJ];   // sc: per-gap factor of the factor-free kinds
     __device__ void init(const PairArgs &A, int t)
     {
 #pragma unroll
@@ -112,6 +110,8 @@ struct Slots {
             cx[j] = 1.0 / ic[j];
             if (OP == 2) kk[j] = 1.0 / sqrt(kPi * A.alpha * delta);
             else kk[j] = sqrt(delta) * A.kconst;
+            // V = (x H) ic / (2a^2), K = (F/x) (-rn/(2a)) cx, D2 = (erf/x) cx
+            sc[j] = OP == 0 ? ic[j] * A.inv2a2 : cx[j];
         }
     }
 };
@@ -271,7 +271,6 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
 #pragma unroll
                     for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
                 }
-                if constexpr (L::FOLD) p[L::FOFF] = __dmul_rn(Aq, H[0]);
                 if (A.need_special) {
                     const double cq = A.step * Bq + Aq;
 #pragma unroll
@@ -283,12 +282,12 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
             } else if (OP == 1) {
                 const double rn = rx * ny[0] + ry * ny[1] + rz * ny[2];
                 const double iq = 1.0 / rho;
-                const double U = small ? 0.0 : -rn * iq;
+                const double U = small ? 0.0 : -rn * iq, Ur = small ? 0.0 : -rn;
                 const double P = 1.0 / __dmul_rn(rho, rho);
                 p[1] = HB_FUSED ? iq : P;
                 p[2] = iq;
 #pragma unroll
-                for (int i = 0; i < NIJ; ++i) p[HOFF + i] = HB_FUSED ? (H[i] * U) * A.inv2a : H[i] * U;
+                for (int i = 0; i < NIJ; ++i) p[HOFF + i] = HB_FUSED ? (H[i] * Ur) * A.inv2a : H[i] * U;
                 if (A.need_special) {
                     const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
 #pragma unroll
@@ -339,8 +338,8 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                     for (int j = 0; j < NJ; ++j) {
                         const double x = __dmul_rn(rho, T.cx[j]);
                         const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                        const double f = special::eval<OP>(x, ix, tab, kFull);
-                        const double v = ok ? (OP == 1 ? f : __dmul_rn(s1, f)) : 0.0;
+                        const double f = special::eval<OP + 4>(x, ix, tab, kFull);
+                        const double v = ok ? f : 0.0;
 #pragma unroll
                         for (int c = 0; c < 3; ++c) inner[j][c] = fma(v, p[HOFF + c], inner[j][c]);
                     }
@@ -356,8 +355,8 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                     for (int j = 0; j < NJ; ++j) {
                         const double x = __dmul_rn(rho, T.cx[j]);
                         const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                        const double f = special::eval<OP>(x, ix, tab, kFull);
-                        const double v = ok ? (OP == 1 ? f : __dmul_rn(s1, f)) : 0.0;
+                        const double f = special::eval<OP + 4>(x, ix, tab, kFull);
+                        const double v = ok ? f : 0.0;
 #pragma unroll
                         for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, p[HOFF + i], acc[j][i]);
                     }
@@ -394,16 +393,12 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                             xs[g] = __dmul_rn(rho[g], T.cx[j]);
                             ixs[g] = __dmul_rn(OP == 0 ? b[g] : a[g], T.ic[j]);
                         }
-                        special::eval_n<OP, G>(xs, ixs, fs, tab, kFull);
+                        special::eval_n<OP + 4, G>(xs, ixs, fs, tab, kFull);
 #pragma unroll
                         for (int g = 0; g < G; ++g) {
-                            if constexpr (L::FOLD) {
-                                acc[j][0] = fma(fs[g], pp[g][L::FOFF], acc[j][0]);
-                            } else {
-                                const double v = ok[g] ? (OP == 1 ? fs[g] : __dmul_rn(a[g], fs[g])) : 0.0;
+                            const double v = ok[g] ? fs[g] : 0.0;
 #pragma unroll
-                                for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, pp[g][HOFF + i], acc[j][i]);
-                            }
+                            for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, pp[g][HOFF + i], acc[j][i]);
                         }
                     }
                 }
@@ -444,11 +439,11 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
 #if HB_FUSED
                     const double x = __dmul_rn(rho, T.cx[j]);
                     const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                    const double f = special::eval<OP>(x, ix, tab, mask);
-                    const double g = OP == 0 ? __dmul_rn(s1, f) : (OP == 1 ? f : __dmul_rn(s1, f));
-                    if (OP == 0) val = sm ? 2.0 * T.kk[j] : g;
-                    else if (OP == 1) val = sm ? 0.0 : g;
-                    else val = sm ? T.kk[j] : g;
+                    const double f = special::eval<OP + 4>(x, ix, tab, mask);
+                    // rho <= r_eps limits, divided by the per-gap factor applied at the end
+                    if (OP == 0) val = sm ? 2.0 * T.kk[j] / T.sc[j] : f;
+                    else if (OP == 1) val = sm ? 0.0 : f;
+                    else val = sm ? T.kk[j] / T.sc[j] : f;
 #else
                     if (OP == 0) val = sm ? 2.0 * T.kk[j] : eval_general<OP>(A, T, j, rho, s1, s2);
                     else if (OP == 1) val = sm ? 0.0 : eval_general<OP>(A, T, j, rho, s1, s2);
@@ -494,7 +489,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
             const int sl = t + 16 * j;
             if (sl < nslots) {
 #pragma unroll
-                for (int i = 0; i < NIJ; ++i) Ls[i * SLOTS + sl] = jac * acc[j][i];
+                for (int i = 0; i < NIJ; ++i) Ls[i * SLOTS + sl] = jac * (HB_FUSED ? acc[j][i] * T.sc[j] : acc[j][i]);
             }
         }
     }
@@ -609,6 +604,7 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             const double rna = (-rx) * na[0] + (-ry) * na[1] + (-rz) * na[2];   // reverse: r' = -r
             const double iq = 1.0 / rho;
             const double Uf = small ? 0.0 : -rnb * iq, Ur = small ? 0.0 : -rna * iq;
+            const double Vf = small ? 0.0 : -rnb, Vr = small ? 0.0 : -rna;   // rho U (factor-free F/x)
             const double P = 1.0 / __dmul_rn(rho, rho);
             double *p = geo + lane * PAY;
             p[0] = rho;
@@ -619,8 +615,8 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             for (int i = 0; i < 3; ++i) {
                 Hf[i] = wq * (1.0 * hs[i]);
                 Hr[i] = wq * (1.0 * ht[i]);
-                p[3 + i] = (Hf[i] * Uf) * A.inv2a;
-                p[6 + i] = (Hr[i] * Ur) * A.inv2a;
+                p[3 + i] = (Hf[i] * Vf) * A.inv2a;
+                p[6 + i] = (Hr[i] * Vr) * A.inv2a;
             }
             if (A.need_special) {
                 const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
@@ -657,7 +653,7 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
                         xs[gg] = __dmul_rn(rho[gg], T.cx[j]);
                         ixs[gg] = __dmul_rn(a[gg], T.ic[j]);
                     }
-                    special::eval_n<1, G>(xs, ixs, fs, tab, kFull);
+                    special::eval_n<5, G>(xs, ixs, fs, tab, kFull);
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
@@ -678,7 +674,7 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
                 for (int j = 0; j < NJ; ++j) {
                     const double x = __dmul_rn(rho, T.cx[j]);
                     const double ix = __dmul_rn(s1, T.ic[j]);
-                    const double f = special::eval<1>(x, ix, tab, mask);
+                    const double f = special::eval<5>(x, ix, tab, mask);
                     const double val = sm ? 0.0 : f;
 #pragma unroll
                     for (int i = 0; i < 3; ++i) {
@@ -717,8 +713,8 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             if (sl < nslots) {
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    Lf[i * SLOTS + sl] = jac * af[j][i];
-                    Lr[i * SLOTS + sl] = jac * ar[j][i];
+                    Lf[i * SLOTS + sl] = jac * (af[j][i] * T.sc[j]);
+                    Lr[i * SLOTS + sl] = jac * (ar[j][i] * T.sc[j]);
                 }
             }
         }
@@ -944,7 +940,7 @@ __global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_
     extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *tab = smem;
-    special::load_table<OP>(tab);
+    special::load_table<OP + 4>(tab);   // factor-free kinds (hb_special.cuh)
     __syncthreads();
     constexpr int kPerWarp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
     double *geo = smem + special::kTabDoubles + warp * kPerWarp;

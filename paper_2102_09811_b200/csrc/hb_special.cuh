@@ -52,27 +52,31 @@ constexpr int kTabStride = kMidPieces + 1;
 template <int KIND>
 __host__ __device__ constexpr int mid_deg() { return kMidDegK[KIND]; }
 
+// series polynomial of each kind: H and x H use Ph, F and F/x use Pf, erf and
+// erf/x use Pe, E uses Pg
 template <int KIND>
 __host__ __device__ constexpr int series_deg()
 {
-    return (KIND == 0 ? (int)(sizeof(kPh) / sizeof(double)) : KIND == 1 ? (int)(sizeof(kPf) / sizeof(double))
-            : KIND == 2 ? (int)(sizeof(kPe) / sizeof(double)) : (int)(sizeof(kPg) / sizeof(double))) - 1;
+    return (KIND == 0 || KIND == 4 ? (int)(sizeof(kPh) / sizeof(double))
+            : KIND == 1 || KIND == 5 ? (int)(sizeof(kPf) / sizeof(double))
+            : KIND == 2 || KIND == 6 ? (int)(sizeof(kPe) / sizeof(double)) : (int)(sizeof(kPg) / sizeof(double))) - 1;
 }
 
 template <int KIND>
 __host__ __device__ constexpr int merged_deg() { return mid_deg<KIND>() > series_deg<KIND>() ? mid_deg<KIND>() : series_deg<KIND>(); }
 
-constexpr int kMergedDegMax = (merged_deg<0>() > merged_deg<1>() ? merged_deg<0>() : merged_deg<1>()) >
-                                      (merged_deg<2>() > merged_deg<3>() ? merged_deg<2>() : merged_deg<3>())
-                                  ? (merged_deg<0>() > merged_deg<1>() ? merged_deg<0>() : merged_deg<1>())
-                                  : (merged_deg<2>() > merged_deg<3>() ? merged_deg<2>() : merged_deg<3>());
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+constexpr int kMergedDegMax = cmax(cmax(cmax(merged_deg<0>(), merged_deg<1>()), cmax(merged_deg<2>(), merged_deg<3>())),
+                                   cmax(cmax(merged_deg<4>(), merged_deg<5>()), merged_deg<6>()));
 constexpr int kTabDoubles = (kMergedDegMax + 1) * kTabStride;   // room for any kind
 
 template <int KIND>
 __device__ __forceinline__ void load_table(double *tab)
 {
-    const double *mid = KIND == 0 ? kMid0 : KIND == 1 ? kMid1 : KIND == 2 ? kMid2 : kMid3;
-    const double *ser = KIND == 0 ? kPh : KIND == 1 ? kPf : KIND == 2 ? kPe : kPg;
+    const double *mid = KIND == 0 ? kMid0 : KIND == 1 ? kMid1 : KIND == 2 ? kMid2 : KIND == 3 ? kMid3
+                      : KIND == 4 ? kMid4 : KIND == 5 ? kMid5 : kMid6;
+    const double *ser = (KIND == 0 || KIND == 4) ? kPh : (KIND == 1 || KIND == 5) ? kPf
+                      : (KIND == 2 || KIND == 6) ? kPe : kPg;
     constexpr int DM = mid_deg<KIND>(), DS = series_deg<KIND>(), D = merged_deg<KIND>();
     for (int i = threadIdx.x; i < (D + 1) * kTabStride; i += blockDim.x) {
         const int k = i / kTabStride, p = i - k * kTabStride;
@@ -99,15 +103,21 @@ __device__ __forceinline__ double series(double x, double t, double ix)
     if (KIND == 0) return fma(x, horner(kPh, t), __dmul_rn(kTwoInvSqrtPi, ix));
     if (KIND == 1) return __dmul_rn(x, horner(kPf, t));
     if (KIND == 2) return __dmul_rn(x, horner(kPe, t));
-    return __dmul_rn(__dmul_rn(x, t), horner(kPg, t));
+    if (KIND == 3) return __dmul_rn(__dmul_rn(x, t), horner(kPg, t));
+    if (KIND == 4) return fma(t, horner(kPh, t), kTwoInvSqrtPi);   // x H = 2/sqrt(pi) + t Ph(t)
+    if (KIND == 5) return horner(kPf, t);                          // F / x
+    return horner(kPe, t);                                         // erf / x
 }
 
 // asymptote (x >= XL)
 template <int KIND>
-__device__ __forceinline__ double asymptote(double ix)
+__device__ __forceinline__ double asymptote(double x, double ix)
 {
-    if (KIND >= 2) return 1.0;
+    if (KIND == 2 || KIND == 3) return 1.0;
+    if (KIND == 6) return ix;                            // erf / x
+    if (KIND == 4) return fma(0.5, ix, x);               // x H = x + 1/(2x)
     const double hx = __dmul_rn(0.5 * ix, ix);
+    if (KIND == 5) return __dmul_rn(ix, 1.0 - hx);       // F / x = (1 - 1/(2x^2)) / x
     return KIND == 0 ? 1.0 + hx : 1.0 - hx;
 }
 
@@ -137,7 +147,9 @@ __device__ __forceinline__ double series_finish(double x, double t, double ix, d
 {
     if (KIND == 0) return fma(x, q, __dmul_rn(kTwoInvSqrtPi, ix));
     if (KIND == 1 || KIND == 2) return __dmul_rn(x, q);
-    return __dmul_rn(__dmul_rn(x, t), q);
+    if (KIND == 3) return __dmul_rn(__dmul_rn(x, t), q);
+    if (KIND == 4) return fma(t, q, kTwoInvSqrtPi);
+    return q;
 }
 
 // NJ evaluations of one lane at once: one region pass for the whole group,
@@ -223,14 +235,16 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
     if (__any_sync(mask, any_h)) {
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
-            if (huge[j]) r[j] = asymptote<KIND>(ix[j]);
+            if (huge[j]) r[j] = asymptote<KIND>(x[j], ix[j]);
     }
 }
 
 // KIND 0: H (single layer), 1: F (double layer), 2: erf (hypersingular D2),
-// 3: E(x) = erf(x) - 2x e^{-x^2}/sqrt(pi) (double-layer potential).
-// ix = 1/x (formed by the caller from precomputed 1/rho and 1/c; used by
-// KIND 0/1 only); `mask` = the lanes executing this call.
+// 3: E(x) = erf(x) - 2x e^{-x^2}/sqrt(pi) (double-layer potential); the
+// assembly kernels use the factor-free forms 4: x H, 5: F/x, 6: erf/x (the
+// per-point factor rho^{+-1} of V / K / D2 becomes a per-gap constant).
+// ix = 1/x (formed by the caller from precomputed 1/rho and 1/c; used by the
+// KIND 0 series and the asymptotes only); `mask` = the lanes executing this call.
 template <int KIND>
 __device__ __forceinline__ double eval(double x, double ix, const double *__restrict__ tab, unsigned mask)
 {
