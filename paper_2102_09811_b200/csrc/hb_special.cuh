@@ -222,8 +222,11 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             asm volatile("" : "+d"(q[j]));
+            // huge lanes take q too and are overwritten by the asymptote below
+            // (vote_h covers them); for the factor-free kinds 5/6 the series
+            // finish is q itself, so there is no select at all
             const double fs = series_finish<KIND>(x[j], t[j], ix[j], q[j]);
-            r[j] = small[j] ? fs : (midr[j] ? q[j] : r[j]);
+            r[j] = small[j] ? fs : q[j];
         }
     } else if (__any_sync(mask, any_s)) {
 #pragma unroll
