@@ -14,7 +14,8 @@
 //   x <  X0 (= 1):  H = 2/(sqrt(pi) x) + x Ph(t), F = x Pf(t), erf = x Pe(t),
 //                   E = x^3 Pg(t), t = x^2 (coefficients uniform across the warp;
 //                   degrees 10 / 10 / 11 / 11)
-//   X0 <= x < XL:   the function value itself as a polynomial in
+//   X0 <= x < XL:   the function value itself (for the factor-free form x H:
+//                   M = (x H - 2/sqrt(pi)) / x^2) as a polynomial in
 //                   u = (x - mid_p) / half on 21 uniform pieces of width 1/4
 //                   (degree 12 for H, 10 for F and erf, 11 for E: per kind the
 //                   lowest degree that keeps the double Horner within 2.3e-16)
@@ -222,11 +223,12 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             asm volatile("" : "+d"(q[j]));
-            // huge lanes take q too and are overwritten by the asymptote below
-            // (vote_h covers them); for the factor-free kinds 5/6 the series
-            // finish is q itself, so there is no select at all
+            // huge lanes take this value too and are overwritten by the
+            // asymptote below; the factor-free kinds 4-6 finish series and
+            // table values alike (x H = 2/sqrt(pi) + t M with M from either,
+            // F/x and erf/x are q itself), so they need no select
             const double fs = series_finish<KIND>(x[j], t[j], ix[j], q[j]);
-            r[j] = small[j] ? fs : q[j];
+            r[j] = (KIND >= 4 || small[j]) ? fs : q[j];
         }
     } else if (__any_sync(mask, any_s)) {
 #pragma unroll
