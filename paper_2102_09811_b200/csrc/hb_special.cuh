@@ -160,39 +160,55 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
                                        const double *__restrict__ tab, unsigned mask)
 {
     double t[NJ];
-    bool small[NJ], midr[NJ], huge[NJ], any_s = false, any_m = false;
+    bool small[NJ], any_ns = false;
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
         t[j] = __dmul_rn(x[j], x[j]);
 #if defined(HB_FORCE_SMALL)   // timing experiments only: wrong values
         small[j] = true;
-        midr[j] = false;
 #elif defined(HB_FORCE_MID)
         small[j] = false;
-        midr[j] = true;
 #else
         small[j] = x[j] < kX0;
+#endif
+        any_ns |= !small[j];
+    }
+    // common case first: every lane of the warp in the series region -- one
+    // compare and one vote, then the constant-bank series
+    if (!__any_sync(mask, any_ns)) {
+#ifdef HB_COUNT_BRANCHES
+        if ((threadIdx.x & 31) == (__ffs(mask) - 1)) atomicAdd(&g_branch_count[1], 1ull);
+#endif
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], ix[j]);
+        return;
+    }
+    bool midr[NJ], huge[NJ], any_s = false, any_m = false, any_h = false;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#if defined(HB_FORCE_MID)
+        midr[j] = true;
+#else
         midr[j] = !small[j] && x[j] < kXL;
 #endif
         huge[j] = !small[j] && !midr[j];
         any_s |= small[j];
         any_m |= midr[j];
-        r[j] = 0.0;
+        any_h |= huge[j];
     }
-#ifdef HB_COUNT_BRANCHES   // diagnostics: warp-level region mix of eval_n calls
+#ifdef HB_COUNT_BRANCHES   // diagnostics: warp-level region mix of the other eval_n calls
     {
         const bool vs = __any_sync(mask, any_s), vm = __any_sync(mask, any_m);
         if ((threadIdx.x & 31) == (__ffs(mask) - 1))
             atomicAdd(&g_branch_count[(vs ? 1 : 0) + (vm ? 2 : 0)], 1ull);
     }
 #endif
-    // one polynomial pass per warp: the constant-bank series when every lane
-    // is small, else ONE table chain in which small lanes use the series
-    // column with t and middle lanes their piece with u (merged degree when
-    // both occur).  Every chain is computed for all lanes unconditionally (the
-    // NJ chains interleave) and lanes keep their own region's value.
-    const bool vote_m = __any_sync(mask, any_m);
-    if (vote_m) {
+    // one polynomial pass per warp: ONE table chain in which small lanes use
+    // the series column with t and middle lanes their piece with u (merged
+    // degree when both occur).  Every chain is computed for all lanes
+    // unconditionally (the NJ chains interleave) and lanes keep their own
+    // region's value.
+    if (__any_sync(mask, any_m)) {
         const bool vote_s = __any_sync(mask, any_s);
         double v[NJ], q[NJ];
         const double *c[NJ];
@@ -230,13 +246,11 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
             const double fs = series_finish<KIND>(x[j], t[j], ix[j], q[j]);
             r[j] = (KIND >= 4 || small[j]) ? fs : q[j];
         }
-    } else if (__any_sync(mask, any_s)) {
+    } else {
+        // small and huge lanes only: the series for all (huge lanes overwritten)
 #pragma unroll
         for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], ix[j]);
     }
-    bool any_h = false;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) any_h |= huge[j];
     if (__any_sync(mask, any_h)) {
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
