@@ -92,6 +92,21 @@ struct LsLayout {
 template <int OP, int NIJ, int NJ>
 __host__ __device__ constexpr int smem_doubles_per_warp() { return 32 * Layout<OP, NIJ>::PAY + LsLayout<NIJ, NJ>::SIZE; }
 
+// one point's payload (N doubles, 16-byte aligned) as N/2 LDS.128; loads of
+// fields the caller does not use are dead and removed
+template <int N>
+__device__ __forceinline__ void load_payload(const double *p, double (&v)[N])
+{
+    static_assert(N % 2 == 0, "payloads are padded to an even number of doubles");
+    const double2 *p2 = reinterpret_cast<const double2 *>(p);
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+        const double2 d = p2[i];
+        v[2 * i] = d.x;
+        v[2 * i + 1] = d.y;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // per-lane time-gap constants
 // ---------------------------------------------------------------------------
@@ -374,31 +389,30 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                 // (p1 x p1 keeps the explicit select: measured faster there)
                 constexpr bool SEL = NIJ == 9;
                 for (int k = s; k < nlocg; k += 2 * G) {
-                    const double *pp[G];
+                    double pv[G][PAY];
                     double rho[G], a[G], b[G];
                     bool ok[G];
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
                         ok[g] = !SEL || k + 2 * g < nloc;
-                        pp[g] = geo + (ok[g] ? k + 2 * g : 0) * PAY;
-                        rho[g] = pp[g][0];
-                        a[g] = pp[g][1];
-                        b[g] = (OP == 2) ? 0.0 : pp[g][2];
+                        load_payload<PAY>(geo + (ok[g] ? k + 2 * g : 0) * PAY, pv[g]);
+                        rho[g] = pv[g][0];
+                        a[g] = pv[g][1];
+                        b[g] = (OP == 2) ? 0.0 : pv[g][2];
                     }
 #pragma unroll
                     for (int j = 0; j < NJ; ++j) {
-                        double xs[G], ixs[G], fs[G];
+                        double xs[G], fs[G];
 #pragma unroll
-                        for (int g = 0; g < G; ++g) {
-                            xs[g] = __dmul_rn(rho[g], T.cx[j]);
-                            ixs[g] = __dmul_rn(OP == 0 ? b[g] : a[g], T.ic[j]);
-                        }
-                        special::eval_n<OP + 4, G>(xs, ixs, fs, tab, kFull);
+                        for (int g = 0; g < G; ++g) xs[g] = __dmul_rn(rho[g], T.cx[j]);
+                        const double icj = T.ic[j];
+                        special::eval_nf<OP + 4, G>(
+                            xs, [&](int g) { return __dmul_rn(OP == 0 ? b[g] : a[g], icj); }, fs, tab, kFull);
 #pragma unroll
                         for (int g = 0; g < G; ++g) {
                             const double v = ok[g] ? fs[g] : 0.0;
 #pragma unroll
-                            for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, pp[g][HOFF + i], acc[j][i]);
+                            for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, pv[g][HOFF + i], acc[j][i]);
                         }
                     }
                 }
@@ -539,7 +553,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
 // pair is evaluated as its canonical (min, max) orientation whichever output
 // is needed, so the blocks do not depend on the row chunking / rank split.
 // ---------------------------------------------------------------------------
-constexpr int kDualPay = 10;   // rho, 1/rho, 1/rho, Hf[3], Hr[3], pad
+constexpr int kDualPay = 8;   // rho, 1/rho, Wf[3], Wr[3]
 template <int NJ>
 __host__ __device__ constexpr int dual_smem_doubles_per_warp() { return 32 * kDualPay + 2 * LsLayout<3, NJ>::SIZE; }
 
@@ -609,14 +623,13 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             double *p = geo + lane * PAY;
             p[0] = rho;
             p[1] = iq;
-            p[2] = iq;
             double Hf[3], Hr[3];
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 Hf[i] = wq * (1.0 * hs[i]);
                 Hr[i] = wq * (1.0 * ht[i]);
-                p[3 + i] = (Hf[i] * Vf) * A.inv2a;
-                p[6 + i] = (Hr[i] * Vr) * A.inv2a;
+                p[2 + i] = (Hf[i] * Vf) * A.inv2a;
+                p[5 + i] = (Hr[i] * Vr) * A.inv2a;
             }
             if (A.need_special) {
                 const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
@@ -637,29 +650,27 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             static_assert(32 % (2 * G) == 0, "padded group loop must stay inside the warp's 32 payload slots");
             const int nlocg = (nloc + 2 * G - 1) / (2 * G) * (2 * G);
             for (int k = s; k < nlocg; k += 2 * G) {   // padding slots are all zero
-                const double *pp[G];
+                double pv[G][PAY];
                 double rho[G], a[G];
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
-                    pp[gg] = geo + (k + 2 * gg) * PAY;
-                    rho[gg] = pp[gg][0];
-                    a[gg] = pp[gg][1];
+                    load_payload<PAY>(geo + (k + 2 * gg) * PAY, pv[gg]);
+                    rho[gg] = pv[gg][0];
+                    a[gg] = pv[gg][1];
                 }
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
-                    double xs[G], ixs[G], fs[G];
+                    double xs[G], fs[G];
 #pragma unroll
-                    for (int gg = 0; gg < G; ++gg) {
-                        xs[gg] = __dmul_rn(rho[gg], T.cx[j]);
-                        ixs[gg] = __dmul_rn(a[gg], T.ic[j]);
-                    }
-                    special::eval_n<5, G>(xs, ixs, fs, tab, kFull);
+                    for (int gg = 0; gg < G; ++gg) xs[gg] = __dmul_rn(rho[gg], T.cx[j]);
+                    const double icj = T.ic[j];
+                    special::eval_nf<5, G>(xs, [&](int gg) { return __dmul_rn(a[gg], icj); }, fs, tab, kFull);
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
                         for (int i = 0; i < 3; ++i) {
-                            af[j][i] = fma(fs[gg], pp[gg][3 + i], af[j][i]);
-                            ar[j][i] = fma(fs[gg], pp[gg][6 + i], ar[j][i]);
+                            af[j][i] = fma(fs[gg], pv[gg][2 + i], af[j][i]);
+                            ar[j][i] = fma(fs[gg], pv[gg][5 + i], ar[j][i]);
                         }
                     }
                 }
@@ -678,8 +689,8 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
                     const double val = sm ? 0.0 : f;
 #pragma unroll
                     for (int i = 0; i < 3; ++i) {
-                        af[j][i] = fma(val, p[3 + i], af[j][i]);
-                        ar[j][i] = fma(val, p[6 + i], ar[j][i]);
+                        af[j][i] = fma(val, p[2 + i], af[j][i]);
+                        ar[j][i] = fma(val, p[5 + i], ar[j][i]);
                     }
                 }
             }
@@ -943,6 +954,8 @@ __global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_
     special::load_table<OP + 4>(tab);   // factor-free kinds (hb_special.cuh)
     __syncthreads();
     constexpr int kPerWarp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
+    static_assert(special::kTabDoubles % 2 == 0 && kPerWarp % 2 == 0 && Layout<OP, NIJ>::PAY % 2 == 0 &&
+                      kDualPay % 2 == 0, "payload slots must stay 16-byte aligned (LDS.128)");
     double *geo = smem + special::kTabDoubles + warp * kPerWarp;
     double *Ls = geo + 32 * Layout<OP, NIJ>::PAY;
     double *Ls_dual = geo + 32 * kDualPay;

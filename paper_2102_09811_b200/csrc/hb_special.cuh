@@ -155,9 +155,11 @@ __device__ __forceinline__ double series_finish(double x, double t, double ix, d
 
 // NJ evaluations of one lane at once: one region pass for the whole group,
 // so the NJ independent Horner chains interleave (ILP NJ).
-template <int KIND, int NJ>
-__device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)[NJ], double (&r)[NJ],
-                                       const double *__restrict__ tab, unsigned mask)
+// ixf(j) supplies 1/x of evaluation j on demand (the KIND 0 series and the
+// asymptotes only), so the common paths do not form it
+template <int KIND, int NJ, class IXF>
+__device__ __forceinline__ void eval_nf(const double (&x)[NJ], const IXF &ixf, double (&r)[NJ],
+                                        const double *__restrict__ tab, unsigned mask)
 {
     double t[NJ];
     bool small[NJ], any_ns = false;
@@ -180,7 +182,7 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
         if ((threadIdx.x & 31) == (__ffs(mask) - 1)) atomicAdd(&g_branch_count[1], 1ull);
 #endif
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], ix[j]);
+        for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], KIND == 0 ? ixf(j) : 0.0);
         return;
     }
     bool midr[NJ], huge[NJ], any_s = false, any_m = false, any_h = false;
@@ -243,19 +245,26 @@ __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)
             // asymptote below; the factor-free kinds 4-6 finish series and
             // table values alike (x H = 2/sqrt(pi) + t M with M from either,
             // F/x and erf/x are q itself), so they need no select
-            const double fs = series_finish<KIND>(x[j], t[j], ix[j], q[j]);
+            const double fs = series_finish<KIND>(x[j], t[j], KIND == 0 ? ixf(j) : 0.0, q[j]);
             r[j] = (KIND >= 4 || small[j]) ? fs : q[j];
         }
     } else {
         // small and huge lanes only: the series for all (huge lanes overwritten)
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], ix[j]);
+        for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], KIND == 0 ? ixf(j) : 0.0);
     }
     if (__any_sync(mask, any_h)) {
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
-            if (huge[j]) r[j] = asymptote<KIND>(x[j], ix[j]);
+            if (huge[j]) r[j] = asymptote<KIND>(x[j], ixf(j));
     }
+}
+
+template <int KIND, int NJ>
+__device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)[NJ], double (&r)[NJ],
+                                       const double *__restrict__ tab, unsigned mask)
+{
+    eval_nf<KIND, NJ>(x, [&](int j) { return ix[j]; }, r, tab, mask);
 }
 
 // KIND 0: H (single layer), 1: F (double layer), 2: erf (hypersingular D2),
