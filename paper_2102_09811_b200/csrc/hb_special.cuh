@@ -69,7 +69,14 @@ __host__ __device__ constexpr int merged_deg() { return mid_deg<KIND>() > series
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int kMergedDegMax = cmax(cmax(cmax(merged_deg<0>(), merged_deg<1>()), cmax(merged_deg<2>(), merged_deg<3>())),
                                    cmax(cmax(merged_deg<4>(), merged_deg<5>()), merged_deg<6>()));
-constexpr int kTabDoubles = (kMergedDegMax + 1) * kTabStride;   // room for any kind
+constexpr int kTabDoubles = ((kMergedDegMax + 2) & ~1) * kTabStride;   // room for any kind / layout
+
+// the factor-free kinds 4-6 (pair kernels) store coefficients 2m and 2m+1 of a
+// column next to each other, at tab[2 (m kTabStride + p) + (k & 1)]: one
+// LDS.128 feeds two Horner steps (16-byte slots, distinct pieces in
+// consecutive slots)
+template <int KIND>
+__host__ __device__ constexpr bool packed() { return KIND >= 4; }
 
 template <int KIND>
 __device__ __forceinline__ void load_table(double *tab)
@@ -79,12 +86,55 @@ __device__ __forceinline__ void load_table(double *tab)
     const double *ser = (KIND == 0 || KIND == 4) ? kPh : (KIND == 1 || KIND == 5) ? kPf
                       : (KIND == 2 || KIND == 6) ? kPe : kPg;
     constexpr int DM = mid_deg<KIND>(), DS = series_deg<KIND>(), D = merged_deg<KIND>();
-    for (int i = threadIdx.x; i < (D + 1) * kTabStride; i += blockDim.x) {
-        const int k = i / kTabStride, p = i - k * kTabStride;
+    constexpr int ROWS = packed<KIND>() ? ((D + 2) & ~1) : D + 1;
+    for (int i = threadIdx.x; i < ROWS * kTabStride; i += blockDim.x) {
+        int k, p;
+        if (packed<KIND>()) {
+            const int slot = i >> 1, m = slot / kTabStride;
+            p = slot - m * kTabStride;
+            k = 2 * m + (i & 1);
+        } else {
+            k = i / kTabStride;
+            p = i - k * kTabStride;
+        }
         double v;
         if (p < kMidPieces) v = k <= DM ? mid[k * kMidPieces + p] : 0.0;
         else v = k <= DS ? ser[k] : 0.0;
         tab[i] = v;
+    }
+}
+
+// Horner chains q_j = sum_k c_j[k] v_j^k, k = DEG..0, column pointers c_j
+// (element offset of the column in tab); fma order identical in both layouts
+template <int KIND, int DEG, int NJ>
+__device__ __forceinline__ void table_chains(const double *__restrict__ tab, const int (&col)[NJ],
+                                             const double (&v)[NJ], double (&q)[NJ])
+{
+    if constexpr (packed<KIND>()) {
+        const double2 *t2 = reinterpret_cast<const double2 *>(tab);
+        constexpr int MT = DEG / 2;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const double2 w = t2[MT * kTabStride + col[j]];
+            q[j] = (DEG & 1) ? fma(w.y, v[j], w.x) : w.x;
+        }
+#pragma unroll
+        for (int m = MT - 1; m >= 0; --m) {
+            double2 w[NJ];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) w[j] = t2[m * kTabStride + col[j]];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], w[j].y);
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], w[j].x);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) q[j] = tab[DEG * kTabStride + col[j]];
+#pragma unroll
+        for (int k = DEG - 1; k >= 0; --k)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], tab[k * kTabStride + col[j]]);
     }
 }
 
@@ -213,31 +263,16 @@ __device__ __forceinline__ void eval_nf(const double (&x)[NJ], const IXF &ixf, d
     if (__any_sync(mask, any_m)) {
         const bool vote_s = __any_sync(mask, any_s);
         double v[NJ], q[NJ];
-        const double *c[NJ];
+        int col[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             double u;
             const int pc = mid_piece(x[j], u);
-            c[j] = tab + (small[j] ? kMidPieces : pc);
+            col[j] = small[j] ? kMidPieces : pc;
             v[j] = small[j] ? t[j] : u;
         }
-        if (vote_s) {
-            constexpr int DEG = merged_deg<KIND>();
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) q[j] = c[j][DEG * kTabStride];
-#pragma unroll
-            for (int k = DEG - 1; k >= 0; --k)
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], c[j][k * kTabStride]);
-        } else {
-            constexpr int DEG = mid_deg<KIND>();
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) q[j] = c[j][DEG * kTabStride];
-#pragma unroll
-            for (int k = DEG - 1; k >= 0; --k)
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], c[j][k * kTabStride]);
-        }
+        if (vote_s) table_chains<KIND, merged_deg<KIND>(), NJ>(tab, col, v, q);
+        else table_chains<KIND, mid_deg<KIND>(), NJ>(tab, col, v, q);
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             asm volatile("" : "+d"(q[j]));
