@@ -248,6 +248,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
     for (int base = 0; base < nq; base += 32) {
         const int q = base + lane;
         int small = 0;
+        int nzw = OP == 1 ? 0 : 1;   // K: this point's weights are not all zero (r.n_y != 0)
         if (q >= nq) {
             // padding slot of the grouped loop: all zero (x = 0 and 1/x = 0 give
             // finite series values, the zero weights add exact zeros)
@@ -298,6 +299,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                 const double rn = rx * ny[0] + ry * ny[1] + rz * ny[2];
                 const double iq = 1.0 / rho;
                 const double U = small ? 0.0 : -rn * iq, Ur = small ? 0.0 : -rn;
+                nzw = Ur != 0.0;
                 const double P = 1.0 / __dmul_rn(rho, rho);
                 p[1] = HB_FUSED ? iq : P;
                 p[2] = iq;
@@ -325,9 +327,13 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
             }
         }
         const bool any_small = __any_sync(kFull, small);
+        // K: a chunk whose weights are all exactly zero (coplanar triangles:
+        // r.n_y == 0 at every point) adds exact zeros -- skip its evaluations
+        const bool skip = OP == 1 && !__any_sync(kFull, nzw);
         __syncwarp();
         const int nloc = min(32, nq - base);
-        if (!any_small) {
+        if (skip) {
+        } else if (!any_small) {
 #if HB_FUSED
             // two quadrature points of the same parity per iteration, evaluated
             // together per gap slot: their x are close, so the small/large-x
@@ -603,7 +609,7 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
     }
     for (int base = 0; base < nq; base += 32) {
         const int q = base + lane;
-        int small = 0;
+        int small = 0, nzw = 0;
         if (q >= nq) {   // all-zero padding slot (see eval_pair)
             double *p = geo + lane * PAY;
 #pragma unroll
@@ -619,6 +625,7 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             const double iq = 1.0 / rho;
             const double Uf = small ? 0.0 : -rnb * iq, Ur = small ? 0.0 : -rna * iq;
             const double Vf = small ? 0.0 : -rnb, Vr = small ? 0.0 : -rna;   // rho U (factor-free F/x)
+            nzw = Vf != 0.0 || Vr != 0.0;
             const double P = 1.0 / __dmul_rn(rho, rho);
             double *p = geo + lane * PAY;
             p[0] = rho;
@@ -643,9 +650,11 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             }
         }
         const bool any_small = __any_sync(kFull, small);
+        const bool skip = !__any_sync(kFull, nzw);   // both orientations' weights all zero (coplanar pair)
         __syncwarp();
         const int nloc = min(32, nq - base);
-        if (!any_small) {
+        if (skip) {
+        } else if (!any_small) {
             constexpr int G = HB_QGROUP;
             static_assert(32 % (2 * G) == 0, "padded group loop must stay inside the warp's 32 payload slots");
             const int nlocg = (nloc + 2 * G - 1) / (2 * G) * (2 * G);
