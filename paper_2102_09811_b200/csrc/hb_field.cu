@@ -639,36 +639,40 @@ constexpr int kFP = 32;                  // points per CTA
 constexpr int kFT = 4 * kFP;             // threads: (quarter, point)
 constexpr int kFS = kFP + 1;             // G row stride (doubles)
 
-// erf(x) and E(x) of one lane at once (hb_special.cuh regions; one vote set)
+// erf(x) and E(x) of one lane at once (hb_special.cuh regions): one compare
+// and one vote for the common all-small warp, else ONE table chain per
+// function in which small lanes use the series column (values bitwise their
+// own region's, as in special::eval_nf)
 __device__ __forceinline__ void eval_erf_E(double x, const double *__restrict__ tabS, const double *__restrict__ tabD,
                                            double &rs, double &rd)
 {
     const double t = __dmul_rn(x, x);
-    const bool small = x < special::kX0, midr = !small && x < special::kXL, huge = !small && !midr;
-    rs = 0.0;
-    rd = 0.0;
-    if (__any_sync(kFull, small)) {
+    const bool small = x < special::kX0;
+    if (!__any_sync(kFull, !small)) {
         rs = special::series<2>(x, t, 0.0);
         rd = special::series<3>(x, t, 0.0);
+        return;
     }
+    const bool midr = !small && x < special::kXL, huge = !small && !midr;
     if (__any_sync(kFull, midr)) {
         double u;
         const int pc = special::mid_piece(x, u);
-        const double *cs = tabS + pc, *cd = tabD + pc;
-        // erf (degree DS) and E (degree DD >= DS): E's leading steps alone, then both chains
-        constexpr int DS = special::mid_deg<2>(), DD = special::mid_deg<3>();
-        static_assert(DD >= DS, "E's middle-region degree must not be below erf's");
-        double qs = cs[DS * special::kTabStride], qd = cd[DD * special::kTabStride];
-#pragma unroll
-        for (int k = DD - 1; k >= DS; --k) qd = fma(qd, u, cd[k * special::kTabStride]);
-#pragma unroll
-        for (int k = DS - 1; k >= 0; --k) {
-            qs = fma(qs, u, cs[k * special::kTabStride]);
-            qd = fma(qd, u, cd[k * special::kTabStride]);
+        const int col[1] = {small ? special::kMidPieces : pc};
+        const double v[1] = {small ? t : u};
+        double qs[1], qd[1];
+        if (__any_sync(kFull, small)) {
+            special::table_chains<2, special::merged_deg<2>(), 1>(tabS, col, v, qs);
+            special::table_chains<3, special::merged_deg<3>(), 1>(tabD, col, v, qd);
+        } else {
+            special::table_chains<2, special::mid_deg<2>(), 1>(tabS, col, v, qs);
+            special::table_chains<3, special::mid_deg<3>(), 1>(tabD, col, v, qd);
         }
-        asm volatile("" : "+d"(qs), "+d"(qd));
-        rs = midr ? qs : rs;
-        rd = midr ? qd : rd;
+        asm volatile("" : "+d"(qs[0]), "+d"(qd[0]));
+        rs = small ? special::series_finish<2>(x, t, 0.0, qs[0]) : qs[0];
+        rd = small ? special::series_finish<3>(x, t, 0.0, qd[0]) : qd[0];
+    } else {
+        rs = special::series<2>(x, t, 0.0);
+        rd = special::series<3>(x, t, 0.0);
     }
     if (__any_sync(kFull, huge)) {
         if (huge) { rs = 1.0; rd = 1.0; }
