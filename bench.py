@@ -437,10 +437,14 @@ def run_native(args, rank, world, local_rank):
         # K's overlaps D (assemble_all's concurrent streams finish all three
         # together and leave the 265 MB of copies exposed: slower end to end)
         hbdev.drop_device_tables(mesh)              # re-upload inputs from pinned host memory
-        V = hb.assemble_single_layer(mesh, tg, params, q, d_range=(d0, d1))
-        _, ev_v = V.to_host_async(pinV)
-        K = hb.assemble_double_layer(mesh, tg, params, q, d_range=(d0, d1))
-        _, ev_k = K.to_host_async(pinK)
+        # V streams back in work-balanced row slabs as they are assembled
+        # (host_out), K as soon as it is done, D in block chunks as the curl
+        # combine forms them
+        V = hb.assemble_single_layer(mesh, tg, params, q, d_range=(d0, d1), host_out=pinV,
+                                     host_out_slabs=int(os.environ.get("HB_E2E_SLABS", "3")))
+        _, ev_v = V.host_copy
+        K = hb.assemble_double_layer(mesh, tg, params, q, d_range=(d0, d1), host_out=pinK)
+        _, ev_k = K.host_copy
         D = hb.assemble_hypersingular(mesh, tg, params, q, single_layer=V, d_range=(d0, d1), host_out=pinD)
         _, ev_d = D.host_copy                      # D streamed back in block chunks as the curl forms them
         for ev in (ev_v, ev_k, ev_d):
@@ -530,11 +534,12 @@ def run_native(args, rank, world, local_rank):
                      "traffic": traffic},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "public API assemble_single_layer / assemble_double_layer / assemble_hypersingular(host_out), "
-                        "mesh tables re-uploaded from pinned host memory and all blocks copied to pinned host "
-                        "memory every step (each operator copied back on a side stream as soon as it is done -- V's "
-                        "copy overlaps K, K's overlaps D -- and D in 4 block chunks as the curl combine forms "
-                        "them; the step ends when the last copy is done)"},
+                "path": "public API assemble_single_layer / assemble_double_layer / assemble_hypersingular with "
+                        "host_out: mesh tables re-uploaded from pinned host memory and all blocks copied to pinned "
+                        "host memory every step -- V in 3 work-balanced test-row slabs, each slab's copy started "
+                        "on a side stream as soon as its rows are complete, K as soon as it is done, D in 4 block "
+                        "chunks as the "
+                        "curl combine forms them; the step ends when the last copy is done"},
         "clocks": clocks,
         "paths": paths,
         "gpu_launches": int(round(launches_step * args.steps * world)),

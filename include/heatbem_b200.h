@@ -236,6 +236,13 @@ int hb_forward_history(int64_t n_blocks, int64_t R, int64_t C, const double *blo
 int hb_inv_apply(int64_t n, const double *inv_dev, const double *rhs_dev, const double *h_dev,
                  double *x_dev, void *stream);
 
+/* Rows [r0, r1) of every block of a (n_blocks, R, C) float64 device array
+ * copied into the same positions of a page-locked host array of that shape:
+ * one strided asynchronous copy on `stream` (row-slab streaming of V / K,
+ * assembly.py _assemble_streamed). */
+int hb_copy_row_slab_d2h(double *host_dst, const double *dev_src, int64_t n_blocks, int64_t R, int64_t C,
+                         int64_t r0, int64_t r1, void *stream);
+
 /* ---- boundary data (heatbem/field.py:84-119 project_to_space, :193-215
  * relative_error_sigma) for the heat-kernel data family of the study driver
  * (ManufacturedSolution, field.py:20-44):

@@ -84,7 +84,7 @@ EXPORTED = (
     "hb_toeplitz_apply", "hb_forward_subst_step", "hb_fp64_probe", "hb_pair_classes",
     "hb_toeplitz_apply_range", "hb_curl_workspace", "hb_ipc_export", "hb_ipc_import", "hb_ipc_close",
     "hb_forward_solve", "hb_forward_history", "hb_inv_apply", "hb_represent_grid",
-    "hb_project_workspace", "hb_project_data", "hb_p1_mass_solve", "hb_error_sigma",
+    "hb_project_workspace", "hb_project_data", "hb_p1_mass_solve", "hb_error_sigma", "hb_copy_row_slab_d2h",
 )
 
 _lib = None
@@ -146,6 +146,8 @@ def load():
     L.hb_error_sigma.argtypes = [ctypes.POINTER(DataDesc), ctypes.POINTER(HeatDatum), _I64, _D, _P, _INT, _P, _P,
                                  ctypes.c_size_t, _P]
     L.hb_error_sigma.restype = _INT
+    L.hb_copy_row_slab_d2h.argtypes = [_P, _P, _I64, _I64, _I64, _I64, _I64, _P]
+    L.hb_copy_row_slab_d2h.restype = _INT
     _lib = L
     return L
 

@@ -298,6 +298,12 @@ def assemble_single_layer(mesh, timegrid, params: KernelParams, config: Quadratu
     if (test_space, trial_space) not in (("p0", "p0"), ("p1", "p1")):
         raise ValueError("single layer supports p0 x p0 and p1 x p1 only")
     p1 = test_space == "p1"
+    host_out = kw.pop("host_out", None)
+    if host_out is not None and not p1:
+        return _assemble_streamed(_OP_SINGLE, False, False, True, mesh, timegrid, params, config,
+                                  instrumentation, host_out, n_slabs=kw.pop("host_out_slabs", 3), **kw)
+    if host_out is not None:
+        raise ValueError("host_out streaming is for p0 x p0 V and K (V11 rows accumulate)")
     return BlockToeplitzMatrix(_assemble_operator(_OP_SINGLE, p1, p1, True, mesh, timegrid, params,
                                                   config, instrumentation, **kw))
 
@@ -305,9 +311,76 @@ def assemble_single_layer(mesh, timegrid, params: KernelParams, config: Quadratu
 def assemble_double_layer(mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig(),
                           workers: int | None = 1, deterministic: bool = True,
                           instrumentation: AssemblyInstrumentation | None = None, **kw) -> BlockToeplitzMatrix:
-    """Double-layer blocks K, p0 test x p1 trial (assembly.py:272-286)."""
-    return BlockToeplitzMatrix(_assemble_operator(_OP_DOUBLE, False, True, False, mesh, timegrid, params,
-                                                  config, instrumentation, **kw))
+    """Double-layer blocks K, p0 test x p1 trial (assembly.py:272-286).
+    ``host_out`` (page-locked, K's shape): the device->host copy starts on a
+    side stream as soon as K is done (``host_copy`` = (host_out, event)).  K
+    is not split into row slabs: the dual-orientation kernel evaluates a
+    separated pair once for both rows only when both lie in the same call."""
+    host_out = kw.pop("host_out", None)
+    res = BlockToeplitzMatrix(_assemble_operator(_OP_DOUBLE, False, True, False, mesh, timegrid, params,
+                                                 config, instrumentation, **kw))
+    if host_out is not None:
+        if tuple(host_out.shape) != tuple(res.device_blocks.shape) or not host_out.is_pinned():
+            raise ValueError("host_out must be a page-locked tensor of K's (n_blocks, R, C) shape")
+        res.host_copy = res.to_host_async(host_out, kw.get("stream"))
+    return res
+
+
+def _row_slabs(n_rows: int, symmetric: bool, n_slabs: int):
+    """Test-row ranges of equal pair work: upper-triangle rows (f >= e) for a
+    symmetric operator, uniform rows otherwise."""
+    n_slabs = max(1, min(int(n_slabs), n_rows))
+    if symmetric:
+        # work of rows [0, r) ~ r (2E - r): equal-work bounds r_k = E (1 - sqrt(1 - k/n))
+        bounds = [int(round(n_rows * (1.0 - np.sqrt(1.0 - k / n_slabs)))) for k in range(n_slabs + 1)]
+    else:
+        bounds = [int(round(n_rows * k / n_slabs)) for k in range(n_slabs + 1)]
+    bounds[0], bounds[-1] = 0, n_rows
+    return [(a, b) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+
+
+def _assemble_streamed(op, test_p1, trial_p1, symmetric, mesh, timegrid, params, config, instrumentation,
+                       host_out, n_slabs: int = 3, stream=None, **kw):
+    """Assemble a p0-test operator in work-balanced test-row slabs and start
+    each slab's device->host copy (rows [r0, r1) of every block, complete once
+    the slab's rows are done: a symmetric operator's mirrored entries of those
+    rows come from earlier slabs) on a side stream as soon as it is formed, so
+    the copy of a 100+ MB operator overlaps its own assembly.  Same blocks,
+    bitwise, as one call (row ranges write disjoint entries).  The result's
+    ``host_copy`` is (host_out, event of the last copy)."""
+    import torch
+
+    if test_p1:
+        raise ValueError("row-slab streaming needs p0 test rows")
+    E_t = timegrid.n_steps
+    d_range = kw.pop("d_range", None)
+    d0, d1 = (0, E_t) if d_range is None else (int(d_range[0]), int(d_range[1]))
+    R = mesh.n_triangles
+    C = mesh.n_vertices if trial_p1 else mesh.n_triangles
+    out = kw.pop("out", None)
+    dev = device_tables(mesh, config, kw.get("device")).device
+    if out is None:
+        out = torch.empty((d1 - d0, R, C), dtype=torch.float64, device=dev)
+    if (tuple(host_out.shape) != tuple(out.shape) or host_out.dtype != out.dtype or not host_out.is_pinned()
+            or not host_out.is_contiguous() or not out.is_contiguous()):
+        raise ValueError("host_out must be a contiguous page-locked tensor of the operator's (n_blocks, R, C) "
+                         "float64 shape")
+    cur = stream if stream is not None else torch.cuda.current_stream(dev)
+    cs = _copy_stream(dev)
+    for r0, r1 in _row_slabs(R, symmetric, n_slabs):
+        _assemble_operator(op, test_p1, trial_p1, symmetric, mesh, timegrid, params, config, instrumentation,
+                           d_range=(d0, d1), row_range=(r0, r1), out=out, stream=cur, **kw)
+        ready = torch.cuda.Event()
+        ready.record(cur)
+        cs.wait_event(ready)
+        _native.call("hb_copy_row_slab_d2h", _native.ptr(host_out), _native.ptr(out), d1 - d0, R, C, r0, r1,
+                     _native.stream_handle(cs))
+    done = torch.cuda.Event()
+    done.record(cs)
+    out.record_stream(cs)
+    res = BlockToeplitzMatrix(out)
+    res.host_copy = (host_out, done)
+    return res
 
 
 def assemble_hypersingular_d2(mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig(),

@@ -331,3 +331,20 @@ extern "C" int hb_ipc_close(void *ptr_dev, int64_t offset)
     if (!ptr_dev) { set_error("hb_ipc_close: bad arguments"); return HB_ERR_INVALID; }
     return cuda_check(cudaIpcCloseMemHandle((char *)ptr_dev - offset), "cudaIpcCloseMemHandle");
 }
+
+// rows [r0, r1) of every block of a (n_blocks, R, C) float64 array, device ->
+// page-locked host, as ONE strided copy on `stream` (row-slab streaming of an
+// operator while the next slab is assembled)
+extern "C" int hb_copy_row_slab_d2h(double *host_dst, const double *dev_src, int64_t n_blocks, int64_t R, int64_t C,
+                                    int64_t r0, int64_t r1, void *stream)
+{
+    if (!host_dst || !dev_src || n_blocks < 1 || R < 1 || C < 1 || r0 < 0 || r1 > R || r1 <= r0) {
+        set_error("hb_copy_row_slab_d2h: bad arguments");
+        return HB_ERR_INVALID;
+    }
+    const size_t pitch = sizeof(double) * (size_t)(R * C), width = sizeof(double) * (size_t)((r1 - r0) * C);
+    const size_t off = (size_t)(r0 * C);
+    return cuda_check(cudaMemcpy2DAsync(host_dst + off, pitch, dev_src + off, pitch, width, (size_t)n_blocks,
+                                        cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+                      "hb_copy_row_slab_d2h");
+}

@@ -123,3 +123,14 @@ def test_compute_fails_loudly_without_gpu():
 
     with pytest.raises(NativeUnavailable):
         hb.assemble_single_layer(m, tg, hb.KernelParams(1.0, 0.5))
+
+
+def test_row_slabs_cover_rows_with_balanced_work():
+    from paper_2102_09811_b200.assembly import _row_slabs
+
+    for E, sym in ((768, True), (768, False), (5, True), (3, False)):
+        sl = _row_slabs(E, sym, 4)
+        assert sl[0][0] == 0 and sl[-1][1] == E
+        assert all(a < b for a, b in sl) and all(sl[i][1] == sl[i + 1][0] for i in range(len(sl) - 1))
+    work = [sum(768 - e for e in range(a, b)) for a, b in _row_slabs(768, True, 4)]
+    assert max(work) / min(work) < 1.05
