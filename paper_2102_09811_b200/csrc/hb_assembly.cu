@@ -1304,9 +1304,13 @@ static int launch_pairs(const PairArgs &A, cudaStream_t st)
 template <int OP, bool TP1, bool SP1>
 static int dispatch_nj(int nj, const PairArgs &A, cudaStream_t st)
 {
-    if constexpr (OP == 1) {   // K: both orientations of a separated pair per evaluation (HB_K_DUAL=0: off)
-        static const bool dual = !getenv("HB_K_DUAL") || atoi(getenv("HB_K_DUAL")) != 0;
-        if (dual) {
+    if constexpr (OP == 1) {
+        // K: both orientations of a separated pair per evaluation (HB_K_DUAL=0: off).  A pair
+        // whose other row lies outside the launch's rows is evaluated by both row chunks, and
+        // then the dual body (6 accumulators) costs more than the single one; it pays only
+        // when the chunk holds >= 1/3 of the rows (break-even ~0.3 of the pairs inside).
+        static const bool dual_on = !getenv("HB_K_DUAL") || atoi(getenv("HB_K_DUAL")) != 0;
+        if (dual_on && 3 * (A.e1 - A.e0) >= A.m.E_x) {
             if (nj == 1) return launch_pairs<OP, TP1, SP1, 1, true>(A, st);
             return launch_pairs<OP, TP1, SP1, 2, true>(A, st);
         }
