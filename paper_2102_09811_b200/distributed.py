@@ -545,3 +545,50 @@ def gather_blocks(shard: ShardedToeplitz):
         dist.broadcast(buf, src=r, group=shard.group)
         parts.append(buf)
     return torch.cat(parts)
+
+
+# ---------------------------------------------------------------------------
+# potentials: points are independent
+# ---------------------------------------------------------------------------
+def represent_grid_sharded(w, u, xs, mesh, timegrid, params, config=None, group=None, gather: bool = True):
+    """``field.represent_grid`` with the evaluation points split across the
+    ranks: rank r evaluates the contiguous point range block_range(r, world,
+    M) (every rank holds the densities -- 2.4 MB at config 4 -- so there is
+    no collective on the compute path) and, with ``gather``, one all-gather
+    assembles the (M, n_times) result on every rank (rows in point order;
+    over gloo the gather goes through host memory).  Returns the gathered
+    device tensor, or (local rows, (p0, p1)) without ``gather``.  Each
+    point's values are bitwise the 1-GPU ones (a point is evaluated by one
+    rank with the same kernel)."""
+    import torch
+    import torch.distributed as dist
+
+    from .field import represent_grid
+    from .quadrature import QuadratureConfig
+
+    config = config if config is not None else QuadratureConfig()
+    xs = np.ascontiguousarray(np.asarray(xs, dtype=np.float64).reshape(-1, 3))
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    M = xs.shape[0]
+    p0, p1 = block_range(rank, world, M)
+    n_t = timegrid.n_steps
+    if p1 > p0:
+        local = represent_grid(w, u, xs[p0:p1], mesh, timegrid, params, config, return_device=True)
+    else:
+        local = torch.empty((0, n_t), dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+    if not gather:
+        return local, (p0, p1)
+    if world == 1:
+        return local
+    width = -(-M // world)   # block_range sizes differ by at most one: pad to the largest
+    host = dist.get_backend(group) == "gloo"
+    buf = torch.zeros((width, local.shape[1]), dtype=torch.float64, device="cpu" if host else local.device)
+    buf[: p1 - p0] = local.cpu() if host else local
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    rows = []
+    for r in range(world):
+        a, b = block_range(r, world, M)
+        rows.append(parts[r][: b - a])
+    return torch.cat(rows).to(local.device)

@@ -217,3 +217,13 @@ def test_row_sharded_apply_and_forward_solve_gloo(world, n):
         assert np.array_equal(out[f"y{r}"], out["y0"]) and np.array_equal(out[f"x{r}"], out["x0"])
     assert np.allclose(out["y0"].ravel(), dense @ x.ravel(), rtol=1e-13, atol=1e-13)
     assert np.allclose(dense @ out["x0"].ravel(), rhs.ravel(), rtol=1e-12, atol=1e-12)
+
+
+def test_point_ranges_partition_every_point():
+    from paper_2102_09811_b200.distributed import block_range
+
+    for M, world in ((100000, 8), (301, 2), (3, 4)):
+        ranges = [block_range(r, world, M) for r in range(world)]
+        assert ranges[0][0] == 0 and ranges[-1][1] == M
+        assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
+        assert max(b - a for a, b in ranges) <= -(-M // world)
