@@ -592,12 +592,17 @@ __device__ __forceinline__ void combine_store(const PairArgs &A, const double *L
     }
 }
 
-template <int NJ>
+// MODE 0: both outputs; 1: only K(a, b) (forward); 2: only K(b, a) (reverse) --
+// the other row lies outside the launch.  Each output's arithmetic is the same
+// in every mode (same points, order, fs and weights), so a block entry does not
+// depend on which rows share the launch (row chunks, ranks).
+template <int NJ, int MODE = 0>
 __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularGeom &g, int nq, const double nb[3],
                                                const double na[3], double jac, int64_t slot_f, int64_t slot_r,
                                                const Slots<1, NJ> &T, double *geo, double *Ls, int lane,
                                                const double *tab)
 {
+    constexpr bool DF = MODE != 2, DR = MODE != 1;
     constexpr int PAY = kDualPay, SLOTS = LsLayout<3, NJ>::SLOTS, LSZ = LsLayout<3, NJ>::SIZE;
     const int s = lane >> 4, t = lane & 15;
     double af[NJ][3], ar[NJ][3], s0f[3], scf[3], s0r[3], scr[3];
@@ -625,7 +630,7 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             const double iq = 1.0 / rho;
             const double Uf = small ? 0.0 : -rnb * iq, Ur = small ? 0.0 : -rna * iq;
             const double Vf = small ? 0.0 : -rnb, Vr = small ? 0.0 : -rna;   // rho U (factor-free F/x)
-            nzw = Vf != 0.0 || Vr != 0.0;
+            nzw = (DF && Vf != 0.0) || (DR && Vr != 0.0);
             const double P = 1.0 / __dmul_rn(rho, rho);
             double *p = geo + lane * PAY;
             p[0] = rho;
@@ -635,8 +640,8 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             for (int i = 0; i < 3; ++i) {
                 Hf[i] = wq * (1.0 * hs[i]);
                 Hr[i] = wq * (1.0 * ht[i]);
-                p[2 + i] = (Hf[i] * Vf) * A.inv2a;
-                p[5 + i] = (Hr[i] * Vr) * A.inv2a;
+                if (DF) p[2 + i] = (Hf[i] * Vf) * A.inv2a;
+                if (DR) p[5 + i] = (Hr[i] * Vr) * A.inv2a;
             }
             if (A.need_special) {
                 const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
@@ -710,18 +715,22 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            af[j][i] += __shfl_xor_sync(kFull, af[j][i], 16);
-            ar[j][i] += __shfl_xor_sync(kFull, ar[j][i], 16);
+            if (DF) af[j][i] += __shfl_xor_sync(kFull, af[j][i], 16);
+            if (DR) ar[j][i] += __shfl_xor_sync(kFull, ar[j][i], 16);
         }
     if (A.need_special) {
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1)
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
-                s0f[i] += __shfl_xor_sync(kFull, s0f[i], o);
-                scf[i] += __shfl_xor_sync(kFull, scf[i], o);
-                s0r[i] += __shfl_xor_sync(kFull, s0r[i], o);
-                scr[i] += __shfl_xor_sync(kFull, scr[i], o);
+                if (DF) {
+                    s0f[i] += __shfl_xor_sync(kFull, s0f[i], o);
+                    scf[i] += __shfl_xor_sync(kFull, scf[i], o);
+                }
+                if (DR) {
+                    s0r[i] += __shfl_xor_sync(kFull, s0r[i], o);
+                    scr[i] += __shfl_xor_sync(kFull, scr[i], o);
+                }
             }
     }
     const int nslots = A.it_hi - A.it_lo + 1;
@@ -733,8 +742,8 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             if (sl < nslots) {
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    Lf[i * SLOTS + sl] = jac * (af[j][i] * T.sc[j]);
-                    Lr[i * SLOTS + sl] = jac * (ar[j][i] * T.sc[j]);
+                    if (DF) Lf[i * SLOTS + sl] = jac * (af[j][i] * T.sc[j]);
+                    if (DR) Lr[i * SLOTS + sl] = jac * (ar[j][i] * T.sc[j]);
                 }
             }
         }
@@ -742,15 +751,19 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
     if (lane == 0 && A.need_special) {
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            Lf[3 * SLOTS + i] = jac * s0f[i];
-            Lf[3 * SLOTS + 3 + i] = jac * scf[i];
-            Lr[3 * SLOTS + i] = jac * s0r[i];
-            Lr[3 * SLOTS + 3 + i] = jac * scr[i];
+            if (DF) {
+                Lf[3 * SLOTS + i] = jac * s0f[i];
+                Lf[3 * SLOTS + 3 + i] = jac * scf[i];
+            }
+            if (DR) {
+                Lr[3 * SLOTS + i] = jac * s0r[i];
+                Lr[3 * SLOTS + 3 + i] = jac * scr[i];
+            }
         }
     }
     __syncwarp();
-    if (slot_f >= 0) combine_store<3, NJ>(A, Lf, slot_f, lane);
-    if (slot_r >= 0) combine_store<3, NJ>(A, Lr, slot_r, lane);
+    if (DF && slot_f >= 0) combine_store<3, NJ>(A, Lf, slot_f, lane);
+    if (DR && slot_r >= 0) combine_store<3, NJ>(A, Lr, slot_r, lane);
     __syncwarp();
 }
 
@@ -895,7 +908,13 @@ __device__ __forceinline__ void regular_item_dual(const PairArgs &A, int64_t e, 
             nb[c] = __ldg(M.normals_dev + 3 * b + c);
             na[c] = __ldg(M.normals_dev + 3 * a + c);
         }
-        eval_pair_dual<NJ>(A, g, nq1 * nq1, nb, na, pair_jac<1>(A, a, b), slot_f, slot_r, T, geo, Ls, lane, tab);
+        const double jac = pair_jac<1>(A, a, b);
+        if (slot_f >= 0 && slot_r >= 0)
+            eval_pair_dual<NJ, 0>(A, g, nq1 * nq1, nb, na, jac, slot_f, slot_r, T, geo, Ls, lane, tab);
+        else if (slot_f >= 0)
+            eval_pair_dual<NJ, 1>(A, g, nq1 * nq1, nb, na, jac, slot_f, slot_r, T, geo, Ls, lane, tab);
+        else
+            eval_pair_dual<NJ, 2>(A, g, nq1 * nq1, nb, na, jac, slot_f, slot_r, T, geo, Ls, lane, tab);
     }
 }
 
@@ -1306,11 +1325,11 @@ static int dispatch_nj(int nj, const PairArgs &A, cudaStream_t st)
 {
     if constexpr (OP == 1) {
         // K: both orientations of a separated pair per evaluation (HB_K_DUAL=0: off).  A pair
-        // whose other row lies outside the launch's rows is evaluated by both row chunks, and
-        // then the dual body (6 accumulators) costs more than the single one; it pays only
-        // when the chunk holds >= 1/3 of the rows (break-even ~0.3 of the pairs inside).
+        // whose other row lies outside the launch's rows (row chunks, row-parallel ranks) is
+        // evaluated in the same canonical orientation with only the needed output's
+        // accumulators, so the blocks stay independent of the row split.
         static const bool dual_on = !getenv("HB_K_DUAL") || atoi(getenv("HB_K_DUAL")) != 0;
-        if (dual_on && 3 * (A.e1 - A.e0) >= A.m.E_x) {
+        if (dual_on) {
             if (nj == 1) return launch_pairs<OP, TP1, SP1, 1, true>(A, st);
             return launch_pairs<OP, TP1, SP1, 2, true>(A, st);
         }
