@@ -235,40 +235,43 @@ __device__ __forceinline__ void eval_nf(const double (&x)[NJ], const IXF &ixf, d
         for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], KIND == 0 ? ixf(j) : 0.0);
         return;
     }
-    bool midr[NJ], huge[NJ], any_s = false, any_m = false, any_h = false;
+    // region of the other lanes from the integer piece index (one FP64->int
+    // conversion; integer compares instead of FP64 ones) and ONE warp
+    // reduction of the region bits: 1 small, 2 middle, 4 asymptotic
+    bool huge[NJ];
+    int pcl[NJ], code = 0;
+    double y[NJ];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
+        y[j] = __dmul_rn(x[j] - kX0, kMidInvW);
+        const int pi = __double2int_rd(y[j]);   // < 0 for small lanes, >= kMidPieces for asymptotic ones
 #if defined(HB_FORCE_MID)
-        midr[j] = true;
+        huge[j] = false;
 #else
-        midr[j] = !small[j] && x[j] < kXL;
+        huge[j] = !small[j] && pi >= kMidPieces;
 #endif
-        huge[j] = !small[j] && !midr[j];
-        any_s |= small[j];
-        any_m |= midr[j];
-        any_h |= huge[j];
+        pcl[j] = min(max(pi, 0), kMidPieces - 1);
+        code |= small[j] ? 1 : (huge[j] ? 4 : 2);
     }
+    code = __reduce_or_sync(mask, code);
 #ifdef HB_COUNT_BRANCHES   // diagnostics: warp-level region mix of the other eval_n calls
-    {
-        const bool vs = __any_sync(mask, any_s), vm = __any_sync(mask, any_m);
-        if ((threadIdx.x & 31) == (__ffs(mask) - 1))
-            atomicAdd(&g_branch_count[(vs ? 1 : 0) + (vm ? 2 : 0)], 1ull);
-    }
+    if ((threadIdx.x & 31) == (__ffs(mask) - 1))
+        atomicAdd(&g_branch_count[((code & 1) ? 1 : 0) + ((code & 2) ? 2 : 0)], 1ull);
 #endif
     // one polynomial pass per warp: ONE table chain in which small lanes use
     // the series column with t and middle lanes their piece with u (merged
     // degree when both occur).  Every chain is computed for all lanes
     // unconditionally (the NJ chains interleave) and lanes keep their own
     // region's value.
-    if (__any_sync(mask, any_m)) {
-        const bool vote_s = __any_sync(mask, any_s);
+    if (code & 2) {
+        const bool vote_s = code & 1;
         double v[NJ], q[NJ];
         int col[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-            double u;
-            const int pc = mid_piece(x[j], u);
-            col[j] = small[j] ? kMidPieces : pc;
+            // u = 2 (y - piece) - 1, exact within the piece (as mid_piece)
+            const double u = fma(2.0, y[j] - (double)pcl[j], -1.0);
+            col[j] = small[j] ? kMidPieces : pcl[j];
             v[j] = small[j] ? t[j] : u;
         }
         if (vote_s) table_chains<KIND, merged_deg<KIND>(), NJ>(tab, col, v, q);
@@ -288,7 +291,7 @@ __device__ __forceinline__ void eval_nf(const double (&x)[NJ], const IXF &ixf, d
 #pragma unroll
         for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], KIND == 0 ? ixf(j) : 0.0);
     }
-    if (__any_sync(mask, any_h)) {
+    if (code & 4) {
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
             if (huge[j]) r[j] = asymptote<KIND>(x[j], ixf(j));
