@@ -822,6 +822,227 @@ __global__ void __launch_bounds__(kFT, HB_REP_MINB) k_represent_reg(const RepArg
     cl.sync();
 }
 
+// ---------------------------------------------------------------------------
+// k_represent_mma: k_represent_reg with the time contraction on the FP64
+// tensor cores (mma.sync m8n8k4 f64, DMMA).  Per element quadrature node eq
+// and potential, the contraction is a small GEMM over the m (time-gap) axis:
+//   Out[p][k] += sum_m G[p][m] T[m][k],  T[0][k] = A1[k], T[m][k] = B[k - m]
+//   (1 <= m <= k), 0 for m > k
+// with points p as the M dimension (8-point tiles), output steps k = 1..KM as
+// N (8-step tiles) and m = 0..KM (+ zero padding) as K (4-gap steps); tiles
+// that lie entirely above the diagonal (m > k) are skipped at compile time.
+// Warp w owns potential w >> 1 and points 16 (w & 1) .. +15 (two M tiles x
+// KM/8 N tiles of accumulators).  G is stored per point (row stride KM + 4,
+// == 4 mod 16 doubles: conflict-free fragment loads and phase-B stores), B
+// with KM + 4 leading zeros (no index test for k < m).  One DMMA replaces 8
+// DFMA issue slots; the sums run in a fixed order (deterministic).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int KM>
+struct RepMmaLayout {
+    static constexpr int KS = (KM + 4) / 4;   // 4-gap K steps covering m = 0..KM
+    static constexpr int GS = 4 * KS;         // G row stride (== 4 mod 16 for KM in {16, 32, 64})
+    static constexpr int NT = KM / 8;         // 8-step N tiles
+    static constexpr int ZP = GS;             // zeros before each B row
+    static constexpr int BR = ZP + KM + 1;    // B row length
+    static_assert(GS % 16 == 4, "conflict-free G fragment loads need a row stride of 4 mod 16");
+    static constexpr size_t doubles()
+    {
+        return 2 * (size_t)special::kTabDoubles + 2 * kFP * GS + 2 * 2 * BR + 2 * 2 * (KM + 1) + 3 * kFP;
+    }
+};
+
+template <int KM>
+__global__ void __launch_bounds__(kFT, 4) k_represent_mma(const RepArgs P, int n_split)
+{
+    using L = RepMmaLayout<KM>;
+    constexpr int KS = L::KS, GS = L::GS, NT = L::NT, ZP = L::ZP, BR = L::BR;
+    extern __shared__ __align__(16) double fsm[];
+    double *tabS = fsm, *tabD = tabS + special::kTabDoubles;
+    double *Gt = tabD + special::kTabDoubles;   // [2 pot][kFP][GS]
+    double *Bz = Gt + 2 * kFP * GS;             // [2 buf][2 pot][BR]
+    double *A1 = Bz + 2 * 2 * BR;               // [2 buf][2 pot][KM + 1]
+    double *Rs = A1 + 2 * 2 * (KM + 1);         // [kFP]
+    double *L0s = Rs + kFP, *L0d = L0s + kFP;   // [kFP] G at m = 0
+    special::load_table<2>(tabS);
+    special::load_table<3>(tabD);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < 2 * kFP * GS; i += kFT) Gt[i] = 0.0;   // padding rows m > KM stay zero
+    for (int i = tid; i < 2 * 2 * BR; i += kFT) Bz[i] = 0.0;     // leading zeros stay zero
+    const int split = blockIdx.x % n_split;
+    const int64_t pblock = blockIdx.x / n_split;
+    const int pt = tid % kFP;
+    const int64_t g = pblock * kFP + pt;
+    const int64_t gc = g < P.n_points ? g : P.n_points - 1;
+    const double px = P.x[3 * gc], py = P.x[3 * gc + 1], pz = P.x[3 * gc + 2];
+    const int64_t EQ = P.E_x * P.nq;
+    const int64_t eq_lo = EQ * split / n_split, eq_hi = EQ * (split + 1) / n_split;
+    constexpr int kS = KM >= 64 ? 2 : 1;
+    double cm[kS], gsmall[kS];
+    bool gzero[kS];
+#pragma unroll
+    for (int s = 0; s < kS; ++s) {
+        const double gap = (double)(lane + 1 + 32 * s) * P.step;
+        cm[s] = 1.0 / (2.0 * sqrt(P.alpha * gap));
+        gsmall[s] = 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (P.alpha * P.alpha * P.alpha) * gap));
+        gzero[s] = gap <= P.d_eps;
+    }
+    const double inv4pi = 0.25 * kInvPi;
+    const int pot = warp >> 1, mt0 = 2 * (warp & 1);
+    const int gq = lane >> 2, tq = lane & 3;   // fragment row group / thread in group
+    double acc[2][NT][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[a][n][0] = acc[a][n][1] = 0.0;
+    __syncthreads();
+    int64_t e = eq_lo / P.nq, q = eq_lo % P.nq;
+    for (int64_t eq = eq_lo; eq < eq_hi; ++eq) {
+        const int buf = (int)(eq & 1);
+        // ---- A: point geometry (warp 0); the eq's B / A1 rows (warps 1-3) ----
+        if (warp == 0) {
+            const double *y = P.qpts + 3 * eq;
+            const double rx = px - __ldg(y), ry = py - __ldg(y + 1), rz = pz - __ldg(y + 2);
+            const double rho = sqrt(rx * rx + ry * ry + rz * rz);
+            const double rn = rx * __ldg(P.normals + 3 * e) + ry * __ldg(P.normals + 3 * e + 1) +
+                              rz * __ldg(P.normals + 3 * e + 2);
+            Rs[pt] = rho;
+            L0s[pt] = 1.0 / (4.0 * kPi * P.alpha * rho);
+            L0d[pt] = rho <= P.r_eps ? 0.0 : inv4pi * rn / (rho * rho * rho);
+        } else {
+            const double W = 2.0 * __ldg(P.areas + e) * __ldg(P.qw + q);
+            const double *ds = P.dens_s + eq * P.E_t, *dd = P.dens_d + eq * P.E_t;
+            double *bs = Bz + (2 * buf) * BR + ZP, *bd = bs + BR;
+            double *as = A1 + (2 * buf) * (KM + 1), *ad = as + (KM + 1);
+            for (int j = tid - kFP; j <= KM; j += kFT - kFP) {
+                const double s0 = j < P.E_t ? __ldg(ds + j) : 0.0;
+                const double s1 = (j >= 1 && j - 1 < P.E_t) ? __ldg(ds + j - 1) : 0.0;
+                const double d0 = j < P.E_t ? __ldg(dd + j) : 0.0;
+                const double d1 = (j >= 1 && j - 1 < P.E_t) ? __ldg(dd + j - 1) : 0.0;
+                bs[j] = W * (s1 - s0);
+                as[j] = W * s1;
+                bd[j] = -(W * (d1 - d0));
+                ad[j] = -(W * d1);
+            }
+        }
+        if (++q == P.nq) { q = 0; ++e; }
+        __syncthreads();
+        // ---- B: kernel values of both potentials, lanes over m (G rows per point) ----
+#pragma unroll 1
+        for (int p = warp; p < kFP; p += kFT / 32) {
+            const double rho = Rs[p], l0s = L0s[p], l0d = L0d[p];
+            const bool rsmall = rho <= P.r_eps;
+            double *gs = Gt + p * GS, *gd = Gt + (kFP + p) * GS;
+            if (lane == 0) {
+                gs[0] = l0s;
+                gd[0] = l0d;
+            }
+#pragma unroll
+            for (int s = 0; s < kS; ++s) {
+                double fs, fd;
+                eval_erf_E(__dmul_rn(rho, cm[s]), tabS, tabD, fs, fd);
+                const int m = lane + 1 + 32 * s;
+                const double vs = gzero[s] ? l0s : rsmall ? gsmall[s] : __dmul_rn(l0s, fs);
+                const double vd = gzero[s] ? l0d : rsmall ? 0.0 : __dmul_rn(l0d, fd);
+                if (m <= KM) {
+                    gs[m] = vs;
+                    gd[m] = vd;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- C: DMMA contraction (warp: potential `pot`, M tiles mt0, mt0 + 1) ----
+        {
+            const double *gp = Gt + (pot * kFP + 8 * mt0 + gq) * GS + tq;
+            const double *bz = Bz + (2 * buf + pot) * BR + ZP, *a1 = A1 + (2 * buf + pot) * (KM + 1);
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const double a0 = gp[4 * ks], a1f = gp[8 * GS + 4 * ks];
+                const int m = 4 * ks + tq;
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    if (8 * n + 8 < 4 * ks) continue;   // whole tile above the diagonal (m > k)
+                    const int k = 1 + 8 * n + gq;
+                    const double b = (ks == 0 && tq == 0) ? a1[k] : bz[k - m];
+                    dmma884(acc[0][n][0], acc[0][n][1], a0, b);
+                    dmma884(acc[1][n][0], acc[1][n][1], a1f, b);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    double *Os = Gt;   // [2][kFP][KM + 2]: single, negated double (fits in Gt)
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        double *o = Os + (pot * kFP + 8 * (mt0 + a) + gq) * (KM + 2);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            o[1 + 8 * n + 2 * tq] = acc[a][n][0];
+            o[1 + 8 * n + 2 * tq + 1] = acc[a][n][1];
+        }
+        if (tq == 0) o[0] = 0.0;   // u(0) = 0 at eps = 0
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    for (int p = split + n_split * warp; p < kFP; p += n_split * (kFT / 32)) {   // warp per point
+        const int64_t gg = pblock * kFP + p;
+        if (gg >= P.n_points) continue;
+        for (int64_t o = lane; o < P.n_times; o += 32) {
+            const int k = (int)P.k[o];
+            double v = 0.0;
+            for (int s = 0; s < n_split; ++s) {
+                const double *os = cl.map_shared_rank(Os, s);
+                v += os[p * (KM + 2) + k] + os[(kFP + p) * (KM + 2) + k];
+            }
+            P.out[gg * P.n_times + o] = v;
+        }
+    }
+    cl.sync();
+}
+
+template <int KM>
+int launch_represent_mma(const RepArgs &P, cudaStream_t stream)
+{
+    auto kern = k_represent_mma<KM>;
+    const size_t sm = sizeof(double) * RepMmaLayout<KM>::doubles();
+    static_assert(2 * kFP * (KM + 2) <= 2 * kFP * RepMmaLayout<KM>::GS, "output staging must fit in G");
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFT, sm);
+    const int64_t slots = (int64_t)std::max(1, per_sm) * nsm;
+    const int64_t nb = cdiv(P.n_points, kFP);
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 8; ++s) {
+        if ((int64_t)s * 64 > P.E_x * P.nq) break;
+        const double waves = (double)(nb * s) / (double)slots;
+        const double eff = waves / std::ceil(waves);
+        if (eff > best_eff + 1e-3) { best_eff = eff; best = s; }
+    }
+    if (const char *f = getenv("HB_POT_SPLIT")) best = std::max(1, std::min(8, atoi(f)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(nb * best));
+    cfg.blockDim = dim3(kFT);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = best;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, P, best), "hb_represent_grid");
+}
+
 template <int KM>
 int launch_represent_reg(const RepArgs &P, cudaStream_t stream)
 {
@@ -938,6 +1159,13 @@ extern "C" int hb_represent_grid(int64_t n_points, int64_t n_times, int64_t E_t,
     P.qpts = qpts_dev; P.qw = qw_dev; P.areas = areas_dev; P.normals = normals_dev;
     P.step = step; P.alpha = alpha; P.d_eps = d_eps; P.r_eps = r_eps; P.out = out_dev;
     cudaStream_t st = (cudaStream_t)stream;
+    // time contraction on the FP64 tensor cores (HB_REP_MMA=0: the DFMA register-blocked form)
+    static const bool mma = !getenv("HB_REP_MMA") || atoi(getenv("HB_REP_MMA")) != 0;
+    if (mma) {
+        if (kmax <= 16) return launch_represent_mma<16>(P, st);
+        if (kmax <= 32) return launch_represent_mma<32>(P, st);
+        return launch_represent_mma<64>(P, st);
+    }
     if (kmax <= 16) return launch_represent_reg<16>(P, st);
     if (kmax <= 32) return launch_represent_reg<32>(P, st);
     return launch_represent_reg<64>(P, st);
