@@ -85,6 +85,7 @@ EXPORTED = (
     "hb_toeplitz_apply_range", "hb_curl_workspace", "hb_ipc_export", "hb_ipc_import", "hb_ipc_close",
     "hb_forward_solve", "hb_forward_history", "hb_inv_apply", "hb_represent_grid",
     "hb_project_workspace", "hb_project_data", "hb_p1_mass_solve", "hb_error_sigma", "hb_copy_row_slab_d2h",
+    "hb_represent_grid_elem",
 )
 
 _lib = None
@@ -148,6 +149,9 @@ def load():
     L.hb_error_sigma.restype = _INT
     L.hb_copy_row_slab_d2h.argtypes = [_P, _P, _I64, _I64, _I64, _I64, _I64, _P]
     L.hb_copy_row_slab_d2h.restype = _INT
+    L.hb_represent_grid_elem.argtypes = [_I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P,
+                                         _D, _D, _D, _D, _P, _P]
+    L.hb_represent_grid_elem.restype = _INT
     _lib = L
     return L
 

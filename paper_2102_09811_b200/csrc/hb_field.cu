@@ -1043,6 +1043,250 @@ int launch_represent_mma(const RepArgs &P, cudaStream_t stream)
     return cuda_check(cudaLaunchKernelEx(&cfg, kern, P, best), "hb_represent_grid");
 }
 
+// ---------------------------------------------------------------------------
+// k_represent_elem: the representation formula with the time contraction
+// done ONCE PER ELEMENT instead of once per element quadrature node.  The
+// density differences of a node are element data: the p0 density is constant
+// on the element and the p1 density at node q is sum_i hat_i(q) g_{v_i}, so
+//   sum_q G_q[p][m] W_q B_q[k - m]
+//     = sum_m (sum_q W_q G_q[p][m]) Bq[k - m]                       (single)
+//     + sum_i sum_m (sum_q W_q hat_i(q) G_q[p][m]) Bg_i[k - m]      (double)
+// with W_q = 2 area_e qw_q: the kernel values of the nq nodes are first
+// summed into four per-element arrays H (single; double x 3 vertices) and the
+// element then needs 4 Toeplitz products instead of 2 nq (12 at config 4) --
+// on the FP64 tensor cores as in k_represent_mma (warp w: points 8w..8w+7,
+// all four products).  Inputs: the p0 density per element (E_x, E_t) and the
+// p1 density at each element's vertices (E_x, 3, E_t), time fastest.
+// ---------------------------------------------------------------------------
+struct RepElemArgs {
+    int64_t n_points, n_times, E_t, E_x, nq;
+    const double *x;          // (n_points, 3)
+    const int64_t *k;         // (n_times,) ascending, <= KM
+    const double *dens_e;     // (E_x, E_t)
+    const double *dens_v;     // (E_x, 3, E_t)
+    const double *hats;       // (nq, 3)
+    const double *qpts, *qw, *areas, *normals;
+    double step, alpha, d_eps, r_eps;
+    double *out;              // (n_points, n_times)
+};
+
+constexpr int kFTE = 256;   // k_represent_elem threads (8 warps, 32 points)
+
+template <int KM>
+struct RepElemLayout {
+    static constexpr int KS = (KM + 4) / 4, GS = 4 * KS, NT = KM / 8, ZP = GS, BR = ZP + KM + 1;
+    static_assert(GS % 16 == 4, "conflict-free H fragment loads need a row stride of 4 mod 16");
+    static size_t doubles(int64_t nq)
+    {
+        return 2 * (size_t)special::kTabDoubles + 4 * kFP * GS + 3 * (size_t)nq * kFP + 2 * 4 * BR +
+               2 * 4 * (KM + 1);
+    }
+};
+
+template <int KM>
+__global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P, int n_split)
+{
+    using L = RepElemLayout<KM>;
+    constexpr int KS = L::KS, GS = L::GS, NT = L::NT, ZP = L::ZP, BR = L::BR;
+    extern __shared__ __align__(16) double fsm[];
+    const int nq = (int)P.nq;
+    double *tabS = fsm, *tabD = tabS + special::kTabDoubles;
+    double *H = tabD + special::kTabDoubles;    // [4][kFP][GS]: W G (single), W hat_i G (double, i = 0..2)
+    double *Rn = H + 4 * kFP * GS;              // [nq][kFP] rho
+    double *L0s = Rn + nq * kFP, *L0d = L0s + nq * kFP;   // [nq][kFP] G at m = 0
+    double *Tv = L0d + nq * kFP;                // [2 buf][4][BR]: density differences, zeros before
+    double *Av = Tv + 2 * 4 * BR;               // [2 buf][4][KM + 1]: m = 0 row
+    special::load_table<2>(tabS);
+    special::load_table<3>(tabD);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < 4 * kFP * GS; i += kFTE) H[i] = 0.0;   // padding rows m > KM stay zero
+    for (int i = tid; i < 2 * 4 * BR; i += kFTE) Tv[i] = 0.0;    // leading zeros stay zero
+    const int split = blockIdx.x % n_split;
+    const int64_t pblock = blockIdx.x / n_split;
+    const int64_t e_lo = P.E_x * split / n_split, e_hi = P.E_x * (split + 1) / n_split;
+    constexpr int kS = KM >= 64 ? 2 : 1;
+    double cm[kS], gsmall[kS];
+    bool gzero[kS];
+#pragma unroll
+    for (int s = 0; s < kS; ++s) {
+        const double gap = (double)(lane + 1 + 32 * s) * P.step;
+        cm[s] = 1.0 / (2.0 * sqrt(P.alpha * gap));
+        gsmall[s] = 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (P.alpha * P.alpha * P.alpha) * gap));
+        gzero[s] = gap <= P.d_eps;
+    }
+    const double inv4pi = 0.25 * kInvPi;
+    const int gq = lane >> 2, tq = lane & 3;
+    // phase C: warp w owns M tile (points 8 (w & 3) ..) and the N tiles n = 2 j + (w >> 2)
+    // (odd / even interleave balances the skipped upper-triangle tiles)
+    constexpr int NH = (NT + 1) / 2;
+    const int mt = warp & 3, nh = warp >> 2;
+    double accS[NH][2], accD[NH][2];
+#pragma unroll
+    for (int n = 0; n < NH; ++n) accS[n][0] = accS[n][1] = accD[n][0] = accD[n][1] = 0.0;
+    __syncthreads();
+    for (int64_t e = e_lo; e < e_hi; ++e) {
+        const int buf = (int)(e & 1);
+        // ---- A: geometry of every (node, point); the element's density vectors ----
+        const double nx = __ldg(P.normals + 3 * e), ny = __ldg(P.normals + 3 * e + 1), nz = __ldg(P.normals + 3 * e + 2);
+        for (int it = tid; it < nq * kFP; it += kFTE) {
+            const int node = it / kFP, p = it - node * kFP;
+            const int64_t gp = min(pblock * kFP + p, P.n_points - 1);
+            const double *y = P.qpts + 3 * (e * P.nq + node);
+            const double rx = __ldg(P.x + 3 * gp) - __ldg(y), ry = __ldg(P.x + 3 * gp + 1) - __ldg(y + 1),
+                         rz = __ldg(P.x + 3 * gp + 2) - __ldg(y + 2);
+            const double rho = sqrt(rx * rx + ry * ry + rz * rz);
+            const double rn = rx * nx + ry * ny + rz * nz;
+            Rn[it] = rho;
+            L0s[it] = 1.0 / (4.0 * kPi * P.alpha * rho);
+            L0d[it] = rho <= P.r_eps ? 0.0 : inv4pi * rn / (rho * rho * rho);
+        }
+        {
+            double *tv = Tv + buf * 4 * BR + ZP, *av = Av + buf * 4 * (KM + 1);
+            const double *de = P.dens_e + e * P.E_t, *dv = P.dens_v + e * 3 * P.E_t;
+            for (int it = tid; it < 4 * (KM + 1); it += kFTE) {
+                const int v = it / (KM + 1), j = it - v * (KM + 1);
+                const double *d = v == 0 ? de : dv + (v - 1) * P.E_t;
+                const double cur = j < P.E_t ? __ldg(d + j) : 0.0;
+                const double prev = (j >= 1 && j - 1 < P.E_t) ? __ldg(d + j - 1) : 0.0;
+                // single layer: B = s1 - s0, A1 = s1; double layer negated (u = V~q - W g)
+                tv[v * BR + j] = v == 0 ? prev - cur : -(prev - cur);
+                av[v * (KM + 1) + j] = v == 0 ? prev : -prev;
+            }
+        }
+        __syncthreads();
+        // ---- B: kernel values of every node, summed into H (lanes over m) ----
+        const double a2 = 2.0 * __ldg(P.areas + e);
+#pragma unroll 1
+        for (int node = 0; node < nq; ++node) {
+            const double W = a2 * __ldg(P.qw + node);
+            const double wh0 = W * __ldg(P.hats + 3 * node), wh1 = W * __ldg(P.hats + 3 * node + 1),
+                         wh2 = W * __ldg(P.hats + 3 * node + 2);
+            const bool first = node == 0;
+#pragma unroll 1
+            for (int p = warp; p < kFP; p += kFTE / 32) {
+                const double rho = Rn[node * kFP + p], l0s = L0s[node * kFP + p], l0d = L0d[node * kFP + p];
+                const bool rsmall = rho <= P.r_eps;
+                double *hs = H + p * GS, *h0 = hs + kFP * GS, *h1 = h0 + kFP * GS, *h2 = h1 + kFP * GS;
+                if (lane == 0) {
+                    hs[0] = fma(W, l0s, first ? 0.0 : hs[0]);
+                    h0[0] = fma(wh0, l0d, first ? 0.0 : h0[0]);
+                    h1[0] = fma(wh1, l0d, first ? 0.0 : h1[0]);
+                    h2[0] = fma(wh2, l0d, first ? 0.0 : h2[0]);
+                }
+#pragma unroll
+                for (int s = 0; s < kS; ++s) {
+                    double fs, fd;
+                    eval_erf_E(__dmul_rn(rho, cm[s]), tabS, tabD, fs, fd);
+                    const int m = lane + 1 + 32 * s;
+                    const double vs = gzero[s] ? l0s : rsmall ? gsmall[s] : __dmul_rn(l0s, fs);
+                    const double vd = gzero[s] ? l0d : rsmall ? 0.0 : __dmul_rn(l0d, fd);
+                    if (m <= KM) {
+                        hs[m] = fma(W, vs, first ? 0.0 : hs[m]);
+                        h0[m] = fma(wh0, vd, first ? 0.0 : h0[m]);
+                        h1[m] = fma(wh1, vd, first ? 0.0 : h1[m]);
+                        h2[m] = fma(wh2, vd, first ? 0.0 : h2[m]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ---- C: four Toeplitz products per element on the tensor cores ----
+        {
+            const double *hp = H + (8 * mt + gq) * GS + tq;
+            const double *tv = Tv + buf * 4 * BR + ZP, *av = Av + buf * 4 * (KM + 1);
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                double a[4];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) a[v] = hp[v * kFP * GS + 4 * ks];
+                const int m = 4 * ks + tq;
+#pragma unroll
+                for (int j = 0; j < NH; ++j) {
+                    const int n = 2 * j + nh;
+                    if (n >= NT || 8 * n + 8 < 4 * ks) continue;   // whole tile above the diagonal (m > k)
+                    const int k = 1 + 8 * n + gq;
+                    double b[4];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) b[v] = (ks == 0 && tq == 0) ? av[v * (KM + 1) + k] : tv[v * BR + k - m];
+                    dmma884(accS[j][0], accS[j][1], a[0], b[0]);
+                    dmma884(accD[j][0], accD[j][1], a[1], b[1]);
+                    dmma884(accD[j][0], accD[j][1], a[2], b[2]);
+                    dmma884(accD[j][0], accD[j][1], a[3], b[3]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    double *Os = H;   // [2][kFP][KM + 2]: single, negated double
+    {
+        double *os = Os + (8 * mt + gq) * (KM + 2), *od = Os + (kFP + 8 * mt + gq) * (KM + 2);
+#pragma unroll
+        for (int j = 0; j < NH; ++j) {
+            const int n = 2 * j + nh;
+            if (n >= NT) continue;
+            os[1 + 8 * n + 2 * tq] = accS[j][0];
+            os[1 + 8 * n + 2 * tq + 1] = accS[j][1];
+            od[1 + 8 * n + 2 * tq] = accD[j][0];
+            od[1 + 8 * n + 2 * tq + 1] = accD[j][1];
+        }
+        if (tq == 0 && nh == 0) { os[0] = 0.0; od[0] = 0.0; }   // u(0) = 0 at eps = 0
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    for (int p = split + n_split * warp; p < kFP; p += n_split * (kFTE / 32)) {   // warp per point
+        const int64_t gg = pblock * kFP + p;
+        if (gg >= P.n_points) continue;
+        for (int64_t o = lane; o < P.n_times; o += 32) {
+            const int k = (int)P.k[o];
+            double v = 0.0;
+            for (int s = 0; s < n_split; ++s) {
+                const double *os = cl.map_shared_rank(Os, s);
+                v += os[p * (KM + 2) + k] + os[(kFP + p) * (KM + 2) + k];
+            }
+            P.out[gg * P.n_times + o] = v;
+        }
+    }
+    cl.sync();
+}
+
+template <int KM>
+int launch_represent_elem(const RepElemArgs &P, cudaStream_t stream)
+{
+    auto kern = k_represent_elem<KM>;
+    const size_t sm = sizeof(double) * RepElemLayout<KM>::doubles(P.nq);
+    constexpr int kFT = kFTE;
+    static_assert(2 * kFP * (KM + 2) <= 4 * kFP * RepElemLayout<KM>::GS, "output staging must fit in H");
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFT, sm);
+    const int64_t slots = (int64_t)std::max(1, per_sm) * nsm;
+    const int64_t nb = cdiv(P.n_points, kFP);
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 8; ++s) {
+        if ((int64_t)s * 8 > P.E_x) break;
+        const double waves = (double)(nb * s) / (double)slots;
+        const double eff = waves / std::ceil(waves);
+        if (eff > best_eff + 1e-3) { best_eff = eff; best = s; }
+    }
+    if (const char *f = getenv("HB_POT_SPLIT")) best = std::max(1, std::min(8, atoi(f)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(nb * best));
+    cfg.blockDim = dim3(kFT);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = best;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, P, best), "hb_represent_grid_elem");
+}
+
 template <int KM>
 int launch_represent_reg(const RepArgs &P, cudaStream_t stream)
 {
@@ -1169,4 +1413,29 @@ extern "C" int hb_represent_grid(int64_t n_points, int64_t n_times, int64_t E_t,
     if (kmax <= 16) return launch_represent_reg<16>(P, st);
     if (kmax <= 32) return launch_represent_reg<32>(P, st);
     return launch_represent_reg<64>(P, st);
+}
+
+extern "C" int hb_represent_grid_elem(int64_t n_points, int64_t n_times, int64_t E_t, int64_t E_x, int64_t nq,
+                                      const double *x_dev, const int64_t *k_dev, int64_t kmax,
+                                      const double *dens_elem_dev, const double *dens_vert_dev,
+                                      const double *hats_dev, const double *qpts_dev, const double *qw_dev,
+                                      const double *areas_dev, const double *normals_dev, double step, double alpha,
+                                      double d_eps, double r_eps, double *out_dev, void *stream)
+{
+    if (n_points < 0 || n_times < 0 || E_t < 1 || E_x < 1 || nq < 1 || nq > 64 || kmax < 0 || kmax > 64 ||
+        (n_points > 0 && n_times > 0 &&
+         (!x_dev || !k_dev || !dens_elem_dev || !dens_vert_dev || !hats_dev || !out_dev))) {
+        set_error("hb_represent_grid_elem: bad arguments (kmax %lld: at most 64 output steps)", (long long)kmax);
+        return HB_ERR_INVALID;
+    }
+    if (n_points == 0 || n_times == 0) return HB_OK;
+    RepElemArgs P{};
+    P.n_points = n_points; P.n_times = n_times; P.E_t = E_t; P.E_x = E_x; P.nq = nq;
+    P.x = x_dev; P.k = k_dev; P.dens_e = dens_elem_dev; P.dens_v = dens_vert_dev; P.hats = hats_dev;
+    P.qpts = qpts_dev; P.qw = qw_dev; P.areas = areas_dev; P.normals = normals_dev;
+    P.step = step; P.alpha = alpha; P.d_eps = d_eps; P.r_eps = r_eps; P.out = out_dev;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (kmax <= 16) return launch_represent_elem<16>(P, st);
+    if (kmax <= 32) return launch_represent_elem<32>(P, st);
+    return launch_represent_elem<64>(P, st);
 }

@@ -466,6 +466,21 @@ def _represent_grid_fused(w, u, xs, ks, mesh, timegrid, params, config, stream=N
     _native.require_cuda()
     T = _tables(mesh, config, torch.device("cuda", torch.cuda.current_device()))
     dev = T.qw.device
+    if (w.shape[1] == mesh.n_triangles and u.shape[1] == mesh.n_vertices
+            and not os.environ.get("HB_REP_NODES")):
+        # p0 / p1 densities: the contraction runs once per element (hb_represent_grid_elem)
+        de = torch.as_tensor(np.ascontiguousarray(np.asarray(w).T), dtype=torch.float64, device=dev)
+        uu = torch.as_tensor(np.asarray(u), dtype=torch.float64, device=dev)
+        dv = uu[:, T.tri].permute(1, 2, 0).contiguous()          # (E_x, 3, E_t)
+        X = torch.as_tensor(np.ascontiguousarray(xs), dtype=torch.float64, device=dev)
+        K = torch.as_tensor(np.ascontiguousarray(ks, dtype=np.int64), device=dev)
+        out = torch.empty((xs.shape[0], len(ks)), dtype=torch.float64, device=dev)
+        _native.call("hb_represent_grid_elem", xs.shape[0], len(ks), timegrid.n_steps, mesh.n_triangles, T.nq,
+                     _native.ptr(X), _native.ptr(K), int(ks.max()), _native.ptr(de), _native.ptr(dv),
+                     _native.ptr(T.hats), _native.ptr(T.qpts), _native.ptr(T.qw), _native.ptr(T.areas),
+                     _native.ptr(T.normals), timegrid.step, params.alpha, params.delta_eps, params.rho_eps,
+                     _native.ptr(out), _native.stream_handle(stream))
+        return out
     ds = _density(w, mesh, T).permute(1, 2, 0).contiguous()
     dd = _density(u, mesh, T).permute(1, 2, 0).contiguous()
     X = torch.as_tensor(np.ascontiguousarray(xs), dtype=torch.float64, device=dev)
