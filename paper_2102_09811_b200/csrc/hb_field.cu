@@ -1154,38 +1154,49 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
             }
         }
         __syncthreads();
-        // ---- B: kernel values of every node, summed into H (lanes over m) ----
+        // ---- B: kernel values of every node, summed over the nodes in registers
+        //      (lanes over m, node ascending) and stored once into H ----
         const double a2 = 2.0 * __ldg(P.areas + e);
 #pragma unroll 1
-        for (int node = 0; node < nq; ++node) {
-            const double W = a2 * __ldg(P.qw + node);
-            const double wh0 = W * __ldg(P.hats + 3 * node), wh1 = W * __ldg(P.hats + 3 * node + 1),
-                         wh2 = W * __ldg(P.hats + 3 * node + 2);
-            const bool first = node == 0;
+        for (int p = warp; p < kFP; p += kFTE / 32) {
+            double hsum[4][kS], hz[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                hz[v] = 0.0;
+#pragma unroll
+                for (int s = 0; s < kS; ++s) hsum[v][s] = 0.0;
+            }
 #pragma unroll 1
-            for (int p = warp; p < kFP; p += kFTE / 32) {
+            for (int node = 0; node < nq; ++node) {
+                const double W = a2 * __ldg(P.qw + node);
+                const double wh0 = W * __ldg(P.hats + 3 * node), wh1 = W * __ldg(P.hats + 3 * node + 1),
+                             wh2 = W * __ldg(P.hats + 3 * node + 2);
                 const double rho = Rn[node * kFP + p], l0s = L0s[node * kFP + p], l0d = L0d[node * kFP + p];
                 const bool rsmall = rho <= P.r_eps;
-                double *hs = H + p * GS, *h0 = hs + kFP * GS, *h1 = h0 + kFP * GS, *h2 = h1 + kFP * GS;
-                if (lane == 0) {
-                    hs[0] = fma(W, l0s, first ? 0.0 : hs[0]);
-                    h0[0] = fma(wh0, l0d, first ? 0.0 : h0[0]);
-                    h1[0] = fma(wh1, l0d, first ? 0.0 : h1[0]);
-                    h2[0] = fma(wh2, l0d, first ? 0.0 : h2[0]);
-                }
+                hz[0] = fma(W, l0s, hz[0]);
+                hz[1] = fma(wh0, l0d, hz[1]);
+                hz[2] = fma(wh1, l0d, hz[2]);
+                hz[3] = fma(wh2, l0d, hz[3]);
 #pragma unroll
                 for (int s = 0; s < kS; ++s) {
                     double fs, fd;
                     eval_erf_E(__dmul_rn(rho, cm[s]), tabS, tabD, fs, fd);
-                    const int m = lane + 1 + 32 * s;
                     const double vs = gzero[s] ? l0s : rsmall ? gsmall[s] : __dmul_rn(l0s, fs);
                     const double vd = gzero[s] ? l0d : rsmall ? 0.0 : __dmul_rn(l0d, fd);
-                    if (m <= KM) {
-                        hs[m] = fma(W, vs, first ? 0.0 : hs[m]);
-                        h0[m] = fma(wh0, vd, first ? 0.0 : h0[m]);
-                        h1[m] = fma(wh1, vd, first ? 0.0 : h1[m]);
-                        h2[m] = fma(wh2, vd, first ? 0.0 : h2[m]);
-                    }
+                    hsum[0][s] = fma(W, vs, hsum[0][s]);
+                    hsum[1][s] = fma(wh0, vd, hsum[1][s]);
+                    hsum[2][s] = fma(wh1, vd, hsum[2][s]);
+                    hsum[3][s] = fma(wh2, vd, hsum[3][s]);
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                double *h = H + (v * kFP + p) * GS;
+                if (lane == 0) h[0] = hz[v];
+#pragma unroll
+                for (int s = 0; s < kS; ++s) {
+                    const int m = lane + 1 + 32 * s;
+                    if (m <= KM) h[m] = hsum[v][s];
                 }
             }
         }
