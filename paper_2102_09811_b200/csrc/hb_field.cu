@@ -1274,12 +1274,15 @@ int launch_represent_elem(const RepElemArgs &P, cudaStream_t stream)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFT, sm);
     const int64_t slots = (int64_t)std::max(1, per_sm) * nsm;
     const int64_t nb = cdiv(P.n_points, kFP);
+    // element split over a cluster only when the point blocks alone fill the GPU
+    // poorly: the split adds a cluster barrier and the DSMEM reduction
     int best = 1;
     double best_eff = 0.0;
     for (int s = 1; s <= 8; ++s) {
         if ((int64_t)s * 8 > P.E_x) break;
         const double waves = (double)(nb * s) / (double)slots;
         const double eff = waves / std::ceil(waves);
+        if (eff >= 0.9) { best = s; break; }
         if (eff > best_eff + 1e-3) { best_eff = eff; best = s; }
     }
     if (const char *f = getenv("HB_POT_SPLIT")) best = std::max(1, std::min(8, atoi(f)));
