@@ -69,16 +69,19 @@ def test_random_points_vs_oracle(oracle):
         assert np.allclose(got, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max()), kind
 
 
-@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("fused", ["elem", "nodes", False])
 @pytest.mark.parametrize("E_t,steps", [(12, None), (24, None), (64, None), (64, [3, 17, 40, 64]), (40, [0, 1, 2, 40])])
 def test_register_kernel_vs_oracle(oracle, E_t, steps, fused, monkeypatch):
-    """k_represent_reg (fused: both potentials in one pass) and
-    k_potential_reg (one launch per potential, HB_REP_SEPARATE) for
-    time-step-end points, histories of <= 16 / 32 / 64 steps, E_t below the
-    block size, k = 0, vs the oracle, with the eq range split across clusters
-    of 1 and 7 CTAs (HB_POT_SPLIT)."""
+    """represent_grid for time-step-end points -- k_represent_elem (default:
+    per-element contraction on DMMA), k_represent_mma (HB_REP_NODES: per-node
+    contraction) and k_potential_reg (one launch per potential,
+    HB_REP_SEPARATE) -- for histories of <= 16 / 32 / 64 steps, E_t below the
+    block size, k = 0, vs the oracle, with the element / eq range split across
+    clusters of 1 and 7 CTAs (HB_POT_SPLIT)."""
     if not fused:
         monkeypatch.setenv("HB_REP_SEPARATE", "1")
+    elif fused == "nodes":
+        monkeypatch.setenv("HB_REP_NODES", "1")
     from paper_2102_09811_b200.field import _interp_density_np
     from paper_2102_09811_b200.quadrature import rule_tables
 
