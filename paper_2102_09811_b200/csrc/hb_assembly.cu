@@ -1199,16 +1199,38 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
             }
             __syncwarp();
             double x = tile[nl][lane];
+            // stars of <= 32 entries: lanes test the staged bit of entry b (lane b), a ballot
+            // gives the staged entries and only those are loaded (ascending b, as before;
+            // the skipped +0.0 additions were exact identities).  Longer stars: the full loop.
+            const int pb = lane < nb ? myP[lane] : 0;
             for (int a = 0; a < na; ++a) {
                 const double *Qe = F.Q + sQ[a] + dc + lane;
                 const unsigned *om = okm + a * kFinMaxW;
                 double se = 0.0;
+                if (nb <= 32) {
+                    unsigned mask = __ballot_sync(kFull, lane < nb && ((om[pb >> 5] >> (pb & 31)) & 1u));
+                    while (mask) {   // four staged entries per round: their loads are in flight together
+                        int b[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            b[u] = mask ? __ffs(mask) - 1 : -1;
+                            mask &= mask - 1;
+                        }
+                        double qv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) qv[u] = (lok && b[u] >= 0) ? Qe[myFJ[b[u] < 0 ? 0 : b[u]]] : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (b[u] >= 0) se += qv[u];
+                    }
+                } else {
 #pragma unroll 4
-                for (int b = 0; b < nb; ++b) {
-                    const int p = myP[b];
-                    const bool ok = lok && ((om[p >> 5] >> (p & 31)) & 1u);
-                    const double q = ok ? Qe[myFJ[b]] : 0.0;
-                    se += q;
+                    for (int b = 0; b < nb; ++b) {
+                        const int p = myP[b];
+                        const bool ok = lok && ((om[p >> 5] >> (p & 31)) & 1u);
+                        const double q = ok ? Qe[myFJ[b]] : 0.0;
+                        se += q;
+                    }
                 }
                 x += se;
             }
