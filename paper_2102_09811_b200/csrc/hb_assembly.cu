@@ -45,6 +45,9 @@
 #ifndef HB_PAIR_MINB
 #define HB_PAIR_MINB 2
 #endif
+#ifndef HB_PAIR_WARPS   // warps per CTA of the pair kernels
+#define HB_PAIR_WARPS 8
+#endif
 #ifndef HB_SEP
 #define HB_SEP 0     // separable p1 x p1 accumulation (slower at 128 registers; kept for study)
 #endif
@@ -973,7 +976,7 @@ __device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, cons
 // imbalance of upper-triangular / near-diagonal tiles.
 // ---------------------------------------------------------------------------
 template <int OP, bool TP1, bool SP1, int NJ, bool SYM, bool DUAL = false>
-__global__ void __launch_bounds__(kWarps * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_PAIR_MINB) k_pairs(const PairArgs A)
+__global__ void __launch_bounds__(HB_PAIR_WARPS * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_PAIR_MINB) k_pairs(const PairArgs A)
 {
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     extern __shared__ __align__(16) double smem[];
@@ -1320,25 +1323,25 @@ static int launch_pairs(const PairArgs &A, cudaStream_t st)
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     constexpr bool SYM = (OP != 1);
     constexpr int per_warp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
-    const size_t sm = ((size_t)kWarps * per_warp + special::kTabDoubles) * sizeof(double);
+    const size_t sm = ((size_t)HB_PAIR_WARPS * per_warp + special::kTabDoubles) * sizeof(double);
     auto kp = k_pairs<OP, TP1, SP1, NJ, SYM, DUAL>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, kWarps * 32, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, HB_PAIR_WARPS * 32, sm);
     const int64_t rows = A.e1 - A.e0;
     // separated-pair items of 32 trial elements, or shorter when few test rows
     // (a row-parallel rank) would leave fewer than 4 items per resident warp
     PairArgs B = A;
-    const int64_t warps = (int64_t)std::max(1, per_sm) * nsm * kWarps;
+    const int64_t warps = (int64_t)std::max(1, per_sm) * nsm * HB_PAIR_WARPS;
     B.seg_len = 32;
     while (B.seg_len > 4 && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < 4 * warps) B.seg_len /= 2;
     const int64_t items = rows * cdiv(A.m.E_x, (int64_t)B.seg_len) + rows * A.m.sing_max_per_row;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(1, per_sm) * nsm, cdiv(items, kWarps)));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(1, per_sm) * nsm, cdiv(items, HB_PAIR_WARPS)));
     int rc = cuda_check(cudaMemsetAsync(A.counter, 0, sizeof(unsigned long long), st), "counter reset");
     if (rc) return rc;
-    kp<<<(unsigned)grid, kWarps * 32, sm, st>>>(B);
+    kp<<<(unsigned)grid, HB_PAIR_WARPS * 32, sm, st>>>(B);
     return cuda_check(cudaGetLastError(), "pair kernel");
 }
 
