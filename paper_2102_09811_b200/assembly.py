@@ -20,6 +20,8 @@ device path is always deterministic (no atomics; fixed-order reductions).
 from __future__ import annotations
 
 import struct
+import os
+import sys
 import time
 from dataclasses import dataclass, field
 
@@ -205,6 +207,22 @@ def _workspace(tables, desc_m, desc_a, device, cap, stream=None):
     st = stream if stream is not None else torch.cuda.current_stream(device)
     key = (str(device), st.cuda_stream)
     buf = _WS_CACHE.get(key)
+    if cap is None and full > _DEFAULT_WS_CAP:
+        # staging for ALL test rows larger than the cached default: take it transiently when it
+        # fits in the free memory -- one launch instead of row chunks, and for K the
+        # dual-orientation body then evaluates every separated pair once (row chunks evaluate
+        # the pairs that straddle two chunks twice: config 5, K in 30-block chunks 4.1 -> 2.8 s)
+        # free device memory + what torch's caching allocator holds unused (e.g. the previous
+        # call's transient staging, which the next allocation reuses) + the cached buffer
+        free = (torch.cuda.mem_get_info(device)[0] + torch.cuda.memory_reserved(device)
+                - torch.cuda.memory_allocated(device) + (buf.numel() if buf is not None else 0))
+        if os.environ.get("HB_WS_DEBUG"):
+            print(f"[hb workspace] full {full / 1e9:.1f} GB, free {free / 1e9:.1f} GB", file=sys.stderr)
+        if full + (4 << 30) <= free:   # the output is already allocated; keep 4 GiB of headroom
+            if buf is not None:   # hand the cached buffer back to the allocator (reused, not released)
+                _WS_CACHE.pop(key, None)
+                del buf
+            return torch.empty(full, dtype=torch.uint8, device=device)
     if cap is None:   # default: up to 16 GiB, at most a quarter of the free device memory
         want = min(full, _DEFAULT_WS_CAP)
         if buf is not None and buf.numel() >= max(least, want):

@@ -40,13 +40,15 @@ for d0, d1 in aligned_chunks(Et, CH):   # chunk edges on window edges: no extra 
 del bufV, bufD
 torch.cuda.empty_cache()
 # ---- K ----------------------------------------------------------------------
-# default: window-aligned 128-block chunks, rows chunked to a 16 GiB staging
-# budget (single-orientation body).  HB_C5_KCH=14 HB_C5_KWS=56e9 holds ALL
-# test rows of 14-block chunks (one 16-slot window each) so the dual body
-# evaluates each separated pair once -- measured no faster (3.77 vs 3.64 s):
-# 19 windows repeat the pair geometry and NJ = 1 halves the gaps per point load
-CHK = int(os.environ.get("HB_C5_KCH", "128"))
-KWS = float(os.environ.get("HB_C5_KWS", str(16 * 2 ** 30)))
+# default: window-aligned 30-block chunks (one 32-slot window each) whose
+# staging for ALL test rows (109 GB) fits next to the 19 GB output, so one
+# launch per chunk and the dual-orientation body evaluates each separated pair
+# once: 2.8 s.  HB_C5_KCH=128 HB_C5_KWS=16e9: row-chunked 128-block chunks
+# (pairs straddling two row chunks evaluated twice): 4.1 s; 14-block chunks
+# with all rows (one 16-slot window each): 3.8 s (19 windows repeat the pair
+# geometry, NJ = 1 halves the gaps per point load)
+CHK = int(os.environ.get("HB_C5_KCH", "30"))
+KWS = float(os.environ.get("HB_C5_KWS", "0"))   # 0: the library default (all rows when they fit)
 bufK = torch.empty((CHK, E, N), dtype=torch.float64, device="cuda")
 gotK = np.empty((Et, len(rows), N))
 msK = 0.0
@@ -55,7 +57,7 @@ kchunks = aligned_chunks(Et, CHK) if CHK >= 30 else [(a, min(Et, a + CHK)) for a
 for d0, d1 in kchunks:
     n = d1 - d0
     msK += timed(lambda: _assemble_operator(1, False, True, False, m, tg, p, q, None, d_range=(d0, d1), out=bufK[:n],
-                                            stats=stK, workspace_bytes=int(KWS)))
+                                            stats=stK, workspace_bytes=int(KWS) if KWS > 0 else None))
     gotK[d0:d1] = bufK[:n, torch.as_tensor(rows, device="cuda"), :].cpu().numpy()
 del bufK
 for op, ms, st, got in (("V", msV, stV, gotV), ("K", msK, stK, gotK), ("D", msD, stD2, None)):
