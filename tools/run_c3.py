@@ -1,6 +1,6 @@
 """BASELINE config 3 on one B200: icosphere L5 (20480 triangles), alpha=0.5,
-N=64.  V and K (107 / 54 GB per 32-block half) are assembled in two d-chunks
-into a reused device buffer (d-sharding on one GPU: the layout an 8-GPU run
+N=64.  V (107 GB per 32-block half) and K (14-block chunks) are assembled in
+d-chunks into a reused device buffer (d-sharding on one GPU: the layout an 8-GPU run
 uses per rank), timed with CUDA events, and the sampled rows are checked
 against tests/golden/c3_rows.npz (reference rows + exact values)."""
 import json, os, sys, time
@@ -21,17 +21,23 @@ res = {"setup_s": t_setup}
 for op, code in (("V", (0, False, False, True)), ("K", (1, False, True, False))):
     E, N = m.n_triangles, m.n_vertices
     C = E if op == "V" else N
-    buf = torch.empty((32, E, C), dtype=torch.float64, device="cuda")
+    # V: two 32-block halves; K: HB_C3_KCH-block chunks (default 14: one
+    # 16-slot window whose all-rows staging, 141 GB, fits next to the output ->
+    # one launch per chunk and the dual K body: 3.9 s; 32-block row-chunked
+    # halves: 5.0 s; 10-block chunks: 5.2 s)
+    ch = 32 if op == "V" else int(os.environ.get("HB_C3_KCH", "14"))
+    buf = torch.empty((ch, E, C), dtype=torch.float64, device="cuda")
     got = np.empty((64, len(rows), C))
     ms, st = 0.0, AssemblyStats()
-    for d0 in (0, 32):
+    for d0 in range(0, 64, ch):
+        d1 = min(64, d0 + ch)
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        _assemble_operator(*code, m, tg, p, q, None, d_range=(d0, d0 + 32), out=buf, stats=st)
+        _assemble_operator(*code, m, tg, p, q, None, d_range=(d0, d1), out=buf[:d1 - d0], stats=st)
         e.record(); torch.cuda.synchronize()
         ms += s.elapsed_time(e)
-        got[d0:d0 + 32] = buf[:, torch.as_tensor(rows, device="cuda"), :].cpu().numpy()
+        got[d0:d1] = buf[:d1 - d0, torch.as_tensor(rows, device="cuda"), :].cpu().numpy()
     del buf
     torch.cuda.empty_cache()
     w = workload.operator_work(m, op, 64, q)
