@@ -504,7 +504,8 @@ _OP_CODES = {"V": (_OP_SINGLE, False, False, True), "K": (_OP_DOUBLE, False, Tru
 
 
 def apply_assembled(op: str, mesh, timegrid, params: KernelParams, x, config: QuadratureConfig = QuadratureConfig(),
-                    transpose_blocks: bool = False, chunk_blocks: int = 64, writer: BlockFileWriter | None = None):
+                    transpose_blocks: bool = False, chunk_blocks: int | None = None,
+                    writer: BlockFileWriter | None = None):
     """y^k = sum_{d<=k} A^d x^{k-d} for an operator that is never stored whole
     (apply-and-discard): window-aligned d-chunks of A are
     assembled into one reused device buffer, applied with the per-range
@@ -535,6 +536,10 @@ def apply_assembled(op: str, mesh, timegrid, params: KernelParams, x, config: Qu
     if xd.shape[0] > E_t:
         raise ValueError("more time steps than blocks")
     steps = xd.shape[0]
+    if chunk_blocks is None:
+        # K: one 32-slot window per chunk, so its staging for all test rows can fit next to the
+        # chunk (one launch, dual-orientation body); the others: up to two windows
+        chunk_blocks = 30 if op == "K" else 62
     chunks = aligned_chunks(E_t, max(1, int(chunk_blocks)))
     width = max(b - a for a, b in chunks)
     buf = torch.empty((width, R, C), dtype=torch.float64, device=dev)
