@@ -452,10 +452,39 @@ def eval_double_layer_potential(u, points, mesh, timegrid, params: KernelParams,
 
 
 def represent(w, u, points, mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig()):
-    """Representation formula V~w - Wu at EvalPoints (field.py:184-190)."""
-    sv, w1 = eval_single_layer_potential(w, points, mesh, timegrid, params, config)
-    dv, w2 = eval_double_layer_potential(u, points, mesh, timegrid, params, config)
-    return sv - dv, w1 | w2
+    """Representation formula V~w - Wu at EvalPoints (field.py:184-190).
+    Points at time-step ends (eps = 0, k <= 64) with a p0 w and a p1 u go
+    through the fused per-element path of ``represent_grid`` (one history per
+    distinct spatial point); the others through the two potential launches."""
+    import torch
+
+    w_np = w.cpu().numpy() if isinstance(w, torch.Tensor) else np.asarray(w)
+    u_np = u.cpu().numpy() if isinstance(u, torch.Tensor) else np.asarray(u)
+    n = len(points)
+    xs = np.array([np.asarray(p.x, dtype=np.float64) for p in points]).reshape(-1, 3)
+    k, eps = _decompose(np.array([float(p.t) for p in points]), timegrid.step)
+    grid = ((eps == 0.0) & (k <= 64)) if (n and w_np.shape[1] == mesh.n_triangles
+                                          and u_np.shape[1] == mesh.n_vertices
+                                          and not os.environ.get("HB_REP_SEPARATE")) else np.zeros(n, bool)
+    if not grid.any():
+        sv, w1 = eval_single_layer_potential(w, points, mesh, timegrid, params, config)
+        dv, w2 = eval_double_layer_potential(u, points, mesh, timegrid, params, config)
+        return sv - dv, w1 | w2
+    vals = np.empty(n)
+    xu, inv = np.unique(xs[grid], axis=0, return_inverse=True)
+    kg = k[grid]
+    hist = represent_grid(w_np, u_np, xu, mesh, timegrid, params, config,
+                          time_steps=np.arange(0, int(kg.max()) + 1))
+    vals[grid] = hist[inv.reshape(-1), kg]
+    rest = np.flatnonzero(~grid)
+    if len(rest):
+        pts = [points[i] for i in rest]
+        sv, _ = eval_single_layer_potential(w, pts, mesh, timegrid, params, config)
+        dv, _ = eval_double_layer_potential(u, pts, mesh, timegrid, params, config)
+        vals[rest] = sv - dv
+    T = _tables(mesh, config, torch.device("cuda", torch.cuda.current_device()))
+    warn = _boundary_warnings(torch.as_tensor(xs, device=T.qw.device), mesh, T).cpu().numpy()
+    return vals, warn
 
 
 def _represent_grid_fused(w, u, xs, ks, mesh, timegrid, params, config, stream=None):

@@ -41,9 +41,16 @@ def test_c4_subset_vs_reference():
     assert np.max(np.abs(u - ref)) <= 1e-11 * np.abs(ref).max()
     pts = [hb.EvalPoint(X[i], k / 64) for i in g["c4_sel"][:2] for k in range(1, 65)]
     u2, _ = hb.represent(q, gg, pts, m, tg, p)
-    # represent: two k_potential_reg launches; represent_grid: the fused
-    # hb_represent_grid (same sums, the two potentials added per term)
-    assert np.allclose(u2, u[:128], rtol=1e-13, atol=1e-14 * np.abs(ref).max())
+    # represent routes time-step-end points through represent_grid: the same values
+    assert np.array_equal(u2, u[:128])
+    # the two-launch path (HB_REP_SEPARATE: two k_potential_reg launches) agrees to rounding
+    import os
+    os.environ["HB_REP_SEPARATE"] = "1"
+    try:
+        u3, _ = hb.represent(q, gg, pts, m, tg, p)
+    finally:
+        del os.environ["HB_REP_SEPARATE"]
+    assert np.allclose(u3, u[:128], rtol=1e-13, atol=1e-14 * np.abs(ref).max())
 
 
 def test_random_points_vs_oracle(oracle):
