@@ -209,13 +209,15 @@ int hb_represent_grid(int64_t n_points, int64_t n_times, int64_t E_t, int64_t E_
  * the Toeplitz products, which then run on the FP64 tensor cores -- 4 products
  * per element instead of 2 nq.  dens_elem (E_x, E_t): the p0 density per
  * element; dens_vert (E_x, 3, E_t): the p1 density at each element's vertices
- * (tri_nodes order); hats (nq, 3) at the quadrature nodes; time fastest. */
+ * (tri_nodes order); hats (nq, 3) at the quadrature nodes; time fastest.
+ * eps in [0, step): the outputs are u(x_i, k_j h + eps) -- eps > 0 is the
+ * reference's current-interval case (_field_numba.py:53-76; k_j >= 1). */
 int hb_represent_grid_elem(int64_t n_points, int64_t n_times, int64_t E_t, int64_t E_x, int64_t nq,
                            const double *x_dev, const int64_t *k_dev, int64_t kmax,
                            const double *dens_elem_dev, const double *dens_vert_dev, const double *hats_dev,
                            const double *qpts_dev, const double *qw_dev, const double *areas_dev,
                            const double *normals_dev, double step, double alpha, double d_eps, double r_eps,
-                           double *out_dev, void *stream);
+                           double eps, double *out_dev, void *stream);
 
 /* y^k = sum_{d<=k} A^d x^{k-d} (heatbem/solver.py:47-73).  blocks
  * (n_blocks, R, C) row-major; transpose applies A^d^T (input length R,

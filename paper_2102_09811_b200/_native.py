@@ -150,7 +150,7 @@ def load():
     L.hb_copy_row_slab_d2h.argtypes = [_P, _P, _I64, _I64, _I64, _I64, _I64, _P]
     L.hb_copy_row_slab_d2h.restype = _INT
     L.hb_represent_grid_elem.argtypes = [_I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P,
-                                         _D, _D, _D, _D, _P, _P]
+                                         _D, _D, _D, _D, _D, _P, _P]
     L.hb_represent_grid_elem.restype = _INT
     _lib = L
     return L

@@ -1067,6 +1067,7 @@ struct RepElemArgs {
     const double *hats;       // (nq, 3)
     const double *qpts, *qw, *areas, *normals;
     double step, alpha, d_eps, r_eps;
+    double eps;               // evaluation times k h + eps (0: time-step ends)
     double *out;              // (n_points, n_times)
 };
 
@@ -1079,15 +1080,21 @@ struct RepElemLayout {
     static size_t doubles(int64_t nq)
     {
         return 2 * (size_t)special::kTabDoubles + 4 * kFP * GS + 3 * (size_t)nq * kFP + 2 * 4 * BR +
-               2 * 4 * (KM + 1);
+               2 * 2 * 4 * (KM + 1);
     }
 };
 
-template <int KM>
+// EPS (eps > 0, the reference's current-interval case, _field_numba.py:53-76):
+// out[k] = sum_{m=0..k} G(m h + eps) B[k - m] + G(0) W dens[k] -- the m = 0 row
+// is a regular kernel value and the G(0) term rides in the spare K row XR = KM + 1
+// against the element's density vector.
+template <int KM, bool EPS>
 __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P, int n_split)
 {
     using L = RepElemLayout<KM>;
     constexpr int KS = L::KS, GS = L::GS, NT = L::NT, ZP = L::ZP, BR = L::BR;
+    constexpr int MOFS = EPS ? 0 : 1, XR = KM + 1;
+    static_assert(XR < GS, "the G(0) row must fit in the K padding");
     extern __shared__ __align__(16) double fsm[];
     const int nq = (int)P.nq;
     double *tabS = fsm, *tabD = tabS + special::kTabDoubles;
@@ -1096,6 +1103,7 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
     double *L0s = Rn + nq * kFP, *L0d = L0s + nq * kFP;   // [nq][kFP] G at m = 0
     double *Tv = L0d + nq * kFP;                // [2 buf][4][BR]: density differences, zeros before
     double *Av = Tv + 2 * 4 * BR;               // [2 buf][4][KM + 1]: m = 0 row
+    double *Dv = Av + 2 * 4 * (KM + 1);         // [2 buf][4][KM + 1]: density (EPS: the G(0) term)
     special::load_table<2>(tabS);
     special::load_table<3>(tabD);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1104,12 +1112,12 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
     const int split = blockIdx.x % n_split;
     const int64_t pblock = blockIdx.x / n_split;
     const int64_t e_lo = P.E_x * split / n_split, e_hi = P.E_x * (split + 1) / n_split;
-    constexpr int kS = KM >= 64 ? 2 : 1;
+    constexpr int kS = (KM + 1 - MOFS + 31) / 32;   // lane passes over m = MOFS..KM
     double cm[kS], gsmall[kS];
     bool gzero[kS];
 #pragma unroll
     for (int s = 0; s < kS; ++s) {
-        const double gap = (double)(lane + 1 + 32 * s) * P.step;
+        const double gap = (double)(lane + MOFS + 32 * s) * P.step + (EPS ? P.eps : 0.0);
         cm[s] = 1.0 / (2.0 * sqrt(P.alpha * gap));
         gsmall[s] = 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (P.alpha * P.alpha * P.alpha) * gap));
         gzero[s] = gap <= P.d_eps;
@@ -1141,7 +1149,7 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
             L0d[it] = rho <= P.r_eps ? 0.0 : inv4pi * rn / (rho * rho * rho);
         }
         {
-            double *tv = Tv + buf * 4 * BR + ZP, *av = Av + buf * 4 * (KM + 1);
+            double *tv = Tv + buf * 4 * BR + ZP, *av = Av + buf * 4 * (KM + 1), *dd = Dv + buf * 4 * (KM + 1);
             const double *de = P.dens_e + e * P.E_t, *dv = P.dens_v + e * 3 * P.E_t;
             for (int it = tid; it < 4 * (KM + 1); it += kFTE) {
                 const int v = it / (KM + 1), j = it - v * (KM + 1);
@@ -1151,6 +1159,7 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
                 // single layer: B = s1 - s0, A1 = s1; double layer negated (u = V~q - W g)
                 tv[v * BR + j] = v == 0 ? prev - cur : -(prev - cur);
                 av[v * (KM + 1) + j] = v == 0 ? prev : -prev;
+                if (EPS) dd[v * (KM + 1) + j] = v == 0 ? cur : -cur;
             }
         }
         __syncthreads();
@@ -1192,10 +1201,10 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 double *h = H + (v * kFP + p) * GS;
-                if (lane == 0) h[0] = hz[v];
+                if (lane == 0) h[EPS ? XR : 0] = hz[v];   // G(0) sums: the m = 0 row, or row XR
 #pragma unroll
                 for (int s = 0; s < kS; ++s) {
-                    const int m = lane + 1 + 32 * s;
+                    const int m = lane + MOFS + 32 * s;
                     if (m <= KM) h[m] = hsum[v][s];
                 }
             }
@@ -1204,7 +1213,7 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
         // ---- C: four Toeplitz products per element on the tensor cores ----
         {
             const double *hp = H + (8 * mt + gq) * GS + tq;
-            const double *tv = Tv + buf * 4 * BR + ZP, *av = Av + buf * 4 * (KM + 1);
+            const double *tv = Tv + buf * 4 * BR + ZP, *av = Av + buf * 4 * (KM + 1), *dd = Dv + buf * 4 * (KM + 1);
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
                 double a[4];
@@ -1214,11 +1223,14 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
 #pragma unroll
                 for (int j = 0; j < NH; ++j) {
                     const int n = 2 * j + nh;
-                    if (n >= NT || 8 * n + 8 < 4 * ks) continue;   // whole tile above the diagonal (m > k)
+                    // whole tile above the diagonal (m > k) -- except the G(0) row XR (EPS)
+                    if (n >= NT || (8 * n + 8 < 4 * ks && !(EPS && ks == XR / 4))) continue;
                     const int k = 1 + 8 * n + gq;
                     double b[4];
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) b[v] = (ks == 0 && tq == 0) ? av[v * (KM + 1) + k] : tv[v * BR + k - m];
+                    for (int v = 0; v < 4; ++v)
+                        b[v] = (EPS && m == XR) ? dd[v * (KM + 1) + k]
+                             : (!EPS && ks == 0 && tq == 0) ? av[v * (KM + 1) + k] : tv[v * BR + k - m];
                     dmma884(accS[j][0], accS[j][1], a[0], b[0]);
                     dmma884(accD[j][0], accD[j][1], a[1], b[1]);
                     dmma884(accD[j][0], accD[j][1], a[2], b[2]);
@@ -1260,10 +1272,10 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
     cl.sync();
 }
 
-template <int KM>
+template <int KM, bool EPS>
 int launch_represent_elem(const RepElemArgs &P, cudaStream_t stream)
 {
-    auto kern = k_represent_elem<KM>;
+    auto kern = k_represent_elem<KM, EPS>;
     const size_t sm = sizeof(double) * RepElemLayout<KM>::doubles(P.nq);
     constexpr int kFT = kFTE;
     static_assert(2 * kFP * (KM + 2) <= 4 * kFP * RepElemLayout<KM>::GS, "output staging must fit in H");
@@ -1434,9 +1446,10 @@ extern "C" int hb_represent_grid_elem(int64_t n_points, int64_t n_times, int64_t
                                       const double *dens_elem_dev, const double *dens_vert_dev,
                                       const double *hats_dev, const double *qpts_dev, const double *qw_dev,
                                       const double *areas_dev, const double *normals_dev, double step, double alpha,
-                                      double d_eps, double r_eps, double *out_dev, void *stream)
+                                      double d_eps, double r_eps, double eps, double *out_dev, void *stream)
 {
     if (n_points < 0 || n_times < 0 || E_t < 1 || E_x < 1 || nq < 1 || nq > 64 || kmax < 0 || kmax > 64 ||
+        !(eps >= 0.0 && eps < step) ||
         (n_points > 0 && n_times > 0 &&
          (!x_dev || !k_dev || !dens_elem_dev || !dens_vert_dev || !hats_dev || !out_dev))) {
         set_error("hb_represent_grid_elem: bad arguments (kmax %lld: at most 64 output steps)", (long long)kmax);
@@ -1447,9 +1460,14 @@ extern "C" int hb_represent_grid_elem(int64_t n_points, int64_t n_times, int64_t
     P.n_points = n_points; P.n_times = n_times; P.E_t = E_t; P.E_x = E_x; P.nq = nq;
     P.x = x_dev; P.k = k_dev; P.dens_e = dens_elem_dev; P.dens_v = dens_vert_dev; P.hats = hats_dev;
     P.qpts = qpts_dev; P.qw = qw_dev; P.areas = areas_dev; P.normals = normals_dev;
-    P.step = step; P.alpha = alpha; P.d_eps = d_eps; P.r_eps = r_eps; P.out = out_dev;
+    P.step = step; P.alpha = alpha; P.d_eps = d_eps; P.r_eps = r_eps; P.eps = eps; P.out = out_dev;
     cudaStream_t st = (cudaStream_t)stream;
-    if (kmax <= 16) return launch_represent_elem<16>(P, st);
-    if (kmax <= 32) return launch_represent_elem<32>(P, st);
-    return launch_represent_elem<64>(P, st);
+    if (eps > 0.0) {
+        if (kmax <= 16) return launch_represent_elem<16, true>(P, st);
+        if (kmax <= 32) return launch_represent_elem<32, true>(P, st);
+        return launch_represent_elem<64, true>(P, st);
+    }
+    if (kmax <= 16) return launch_represent_elem<16, false>(P, st);
+    if (kmax <= 32) return launch_represent_elem<32, false>(P, st);
+    return launch_represent_elem<64, false>(P, st);
 }

@@ -463,20 +463,35 @@ def represent(w, u, points, mesh, timegrid, params: KernelParams, config: Quadra
     n = len(points)
     xs = np.array([np.asarray(p.x, dtype=np.float64) for p in points]).reshape(-1, 3)
     k, eps = _decompose(np.array([float(p.t) for p in points]), timegrid.step)
-    grid = ((eps == 0.0) & (k <= 64)) if (n and w_np.shape[1] == mesh.n_triangles
-                                          and u_np.shape[1] == mesh.n_vertices
-                                          and not os.environ.get("HB_REP_SEPARATE")) else np.zeros(n, bool)
-    if not grid.any():
+    fused_ok = (n and w_np.shape[1] == mesh.n_triangles and u_np.shape[1] == mesh.n_vertices
+                and not os.environ.get("HB_REP_SEPARATE"))
+    grid = ((eps == 0.0) & (k <= 64)) if fused_ok else np.zeros(n, bool)
+    done = grid.copy()
+    vals = np.empty(n)
+    if grid.any():
+        xu, inv = np.unique(xs[grid], axis=0, return_inverse=True)
+        kg = k[grid]
+        hist = represent_grid(w_np, u_np, xu, mesh, timegrid, params, config,
+                              time_steps=np.arange(0, int(kg.max()) + 1))
+        vals[grid] = hist[inv.reshape(-1), kg]
+    if fused_ok:
+        # eps > 0 (inside a step): one per-element launch per distinct eps with >= 8 points
+        off = (eps > 0.0) & (k >= 1) & (k <= 64)
+        ev, cnt = np.unique(eps[off], return_counts=True)
+        for e_val in ev[cnt >= 8]:
+            sel = off & (eps == e_val)
+            xu, inv = np.unique(xs[sel], axis=0, return_inverse=True)
+            ksel = k[sel]
+            ks_all = np.arange(1, int(ksel.max()) + 1)
+            hist = _represent_grid_fused(w_np, u_np, xu, ks_all, mesh, timegrid, params, config,
+                                         eps=float(e_val)).cpu().numpy()
+            vals[sel] = hist[inv.reshape(-1), ksel - 1]
+            done |= sel
+    if not done.any():
         sv, w1 = eval_single_layer_potential(w, points, mesh, timegrid, params, config)
         dv, w2 = eval_double_layer_potential(u, points, mesh, timegrid, params, config)
         return sv - dv, w1 | w2
-    vals = np.empty(n)
-    xu, inv = np.unique(xs[grid], axis=0, return_inverse=True)
-    kg = k[grid]
-    hist = represent_grid(w_np, u_np, xu, mesh, timegrid, params, config,
-                          time_steps=np.arange(0, int(kg.max()) + 1))
-    vals[grid] = hist[inv.reshape(-1), kg]
-    rest = np.flatnonzero(~grid)
+    rest = np.flatnonzero(~done)
     if len(rest):
         pts = [points[i] for i in rest]
         sv, _ = eval_single_layer_potential(w, pts, mesh, timegrid, params, config)
@@ -487,7 +502,7 @@ def represent(w, u, points, mesh, timegrid, params: KernelParams, config: Quadra
     return vals, warn
 
 
-def _represent_grid_fused(w, u, xs, ks, mesh, timegrid, params, config, stream=None):
+def _represent_grid_fused(w, u, xs, ks, mesh, timegrid, params, config, stream=None, eps: float = 0.0):
     """u = V~w - W u at (x_i, k_j h) in one hb_represent_grid launch: the two
     potentials share the kernel-value evaluation (csrc/hb_field.cu)."""
     import torch
@@ -508,8 +523,10 @@ def _represent_grid_fused(w, u, xs, ks, mesh, timegrid, params, config, stream=N
                      _native.ptr(X), _native.ptr(K), int(ks.max()), _native.ptr(de), _native.ptr(dv),
                      _native.ptr(T.hats), _native.ptr(T.qpts), _native.ptr(T.qw), _native.ptr(T.areas),
                      _native.ptr(T.normals), timegrid.step, params.alpha, params.delta_eps, params.rho_eps,
-                     _native.ptr(out), _native.stream_handle(stream))
+                     float(eps), _native.ptr(out), _native.stream_handle(stream))
         return out
+    if eps:
+        raise ValueError("eps > 0 needs a p0 single-layer and a p1 double-layer density")
     ds = _density(w, mesh, T).permute(1, 2, 0).contiguous()
     dd = _density(u, mesh, T).permute(1, 2, 0).contiguous()
     X = torch.as_tensor(np.ascontiguousarray(xs), dtype=torch.float64, device=dev)

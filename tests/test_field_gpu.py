@@ -53,6 +53,36 @@ def test_c4_subset_vs_reference():
     assert np.allclose(u3, u[:128], rtol=1e-13, atol=1e-14 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("E_t,frac", [(16, 0.3), (40, 0.71), (64, 0.05)])
+def test_represent_inside_steps_vs_oracle(oracle, E_t, frac):
+    """represent() at t = k h + eps with eps > 0 (the current-interval term):
+    groups of >= 8 points sharing eps go through the per-element kernel
+    (k_represent_elem, EPS form), including k = E_t (no current interval)."""
+    from paper_2102_09811_b200.field import _decompose, _interp_density_np
+    from paper_2102_09811_b200.quadrature import rule_tables
+
+    m = hb.unit_cube_mesh(1)
+    tg = hb.TimeGrid(1.0, E_t)
+    p = hb.KernelParams(0.8, tg.step, length_scale=m.diameter)
+    rng = np.random.default_rng(E_t)
+    w = rng.standard_normal((E_t, m.n_triangles))
+    uu = rng.standard_normal((E_t, m.n_vertices))
+    X = rng.uniform(0.05, 0.95, (12, 3))
+    ks = np.array(sorted({1, 2, E_t // 2, E_t - 1, E_t}))
+    T = (np.repeat(ks, len(X)) + frac) * tg.step
+    XX = np.tile(X, (len(ks), 1))
+    pts = [hb.EvalPoint(x, t) for x, t in zip(XX, T)]
+    got, _ = hb.represent(w, uu, pts, m, tg, p)
+    hats, qw, qpts = rule_tables(m, 6)
+    k, eps = _decompose(T, tg.step)
+    assert np.all(eps > 0)
+    cur = (eps > 0) & (k < E_t)
+    refs = [oracle.potential(kind, XX, k, eps, cur, _interp_density_np(c, m, hats), qpts, qw, m.areas, m.normals,
+                             tg.step, p.alpha, p.delta_eps, p.rho_eps) for kind, c in ((0, w), (1, uu))]
+    ref = refs[0] - refs[1]
+    assert np.allclose(got, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max())
+
+
 def test_random_points_vs_oracle(oracle):
     from paper_2102_09811_b200.field import _decompose, _interp_density_np
     from paper_2102_09811_b200.quadrature import rule_tables
