@@ -155,8 +155,10 @@ def fgmres(op, rhs, rel_tol: float = 1e-8, max_iter: int = 500, restart: int = 5
         return out(torch.zeros_like(b)), SolveReport(0, 0.0, True, time.perf_counter() - t0)
     x = torch.zeros_like(b)
     iterations, converged, res = 0, False, float("inf")
+    first = True
     while iterations < max_iter and not converged:
-        r = b - A(x)
+        r = b.clone() if first else b - A(x)   # A(0) = 0 exactly: the first residual is b
+        first = False
         beta = float(torch.linalg.vector_norm(r))
         if beta <= rel_tol * norm_b:
             converged, res = True, beta / norm_b

@@ -23,6 +23,33 @@ def dense(blocks, E_t, transpose=False, diag=False):
     return out
 
 
+@pytest.mark.parametrize("R,C,E_t,d_off", [(2100, 300, 40, 0), (2050, 97, 64, 5), (4096, 64, 9, 0)])
+def test_apply_toeplitz_tensor_core_path(R, C, E_t, d_off):
+    """Operators with >= 2048 rows take the DMMA kernel (k_toep_mma): blockwise
+    products vs numpy, full and d-range (hb_toeplitz_apply_range) forms."""
+    import torch
+
+    from paper_2102_09811_b200 import _native
+
+    rng = np.random.default_rng(R + C)
+    nb = E_t - d_off
+    B = rng.standard_normal((nb, R, C))
+    x = rng.standard_normal((E_t, C))
+    ref = np.zeros((E_t, R))
+    for k in range(E_t):
+        for d in range(d_off, k + 1):
+            ref[k] += B[d - d_off] @ x[k - d]
+    Bd = torch.as_tensor(B, device="cuda")
+    xd = torch.as_tensor(x, device="cuda")
+    y = torch.empty((E_t, R), dtype=torch.float64, device="cuda")
+    _native.call("hb_toeplitz_apply_range", d_off, nb, R, C, _native.ptr(Bd), 0, E_t, _native.ptr(xd),
+                 _native.ptr(y), _native.stream_handle())
+    assert np.allclose(y.cpu().numpy(), ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+    if d_off == 0:
+        got = hb.apply_toeplitz(hb.BlockToeplitzMatrix(Bd), xd).cpu().numpy()
+        assert np.allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
 @pytest.mark.parametrize("R,C,E_t", [(7, 7, 5), (20, 11, 9), (64, 40, 33)])
 def test_apply_toeplitz_vs_dense(R, C, E_t):
     rng = np.random.default_rng(R)
