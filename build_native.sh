@@ -6,6 +6,7 @@ ROOT="$(cd "$(dirname "$0")" && pwd)"
 SRC="$ROOT/paper_2102_09811_b200/csrc"
 OUT="$ROOT/paper_2102_09811_b200/lib"
 mkdir -p "$OUT"
+rm -f "$OUT/libheatbem_b200.so"   # a failed build leaves no stale library behind
 NVCC="${NVCC:-/usr/local/cuda/bin/nvcc}"
 FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC
        -I"$ROOT/include" -I"$SRC" ${HB_NVCC_EXTRA:-})

@@ -197,16 +197,18 @@ __global__ void __launch_bounds__(256) k_inv_apply(const double *__restrict__ in
 using namespace hb;
 
 // ---------------------------------------------------------------------------
-// Large operators (R >= kMmaMinRows rows, <= 64 steps, not transposed): the
-// block-Toeplitz product as one tensor-core GEMM per block d,
+// Large operators (R >= kMmaMinRows rows, not transposed): the block-Toeplitz
+// product as one tensor-core GEMM per block d,
 //   Y[k][r] += sum_c X[k - d][c] A^d[r][c]   (k >= d),
-// with mma.sync m8n8k4 f64 (DMMA): M = steps (8-step tiles), N = 64 rows per
-// CTA (warp w: rows 8w..8w+7), K = the input index in 32-wide chunks staged in
-// shared memory (row stride 36: conflict-free fragment loads).  Every element
-// of A is read from HBM exactly once (the row-per-warp kernel re-reads A once
-// per 8-step tile); sums run in a fixed order (c chunk, d, K step).
+// with mma.sync m8n8k4 f64 (DMMA): M = steps (a CTA owns a 64-step tile,
+// 8-step fragments), N = 64 rows per CTA (warp w: rows 8w..8w+7), K = the
+// input index in 32-wide chunks staged in shared memory (row stride 36:
+// conflict-free fragment loads) -- per (chunk, d) the A^d tile and the 64
+// x rows k - d of the step tile.  Every element of A is read from HBM once per
+// 64-step tile (the warp-per-row kernel re-reads it once per 8-step tile);
+// sums run in a fixed order (chunk, d, K step).
 // ---------------------------------------------------------------------------
-constexpr int kMmaMinRows = 2048;
+constexpr int kMmaMinRows = 1024;
 constexpr int kMR = 64, kMC = 32, kMS = kMC + 4;
 
 __device__ __forceinline__ void dmma884s(double &d0, double &d1, double a, double b)
@@ -220,53 +222,67 @@ __global__ void __launch_bounds__(256) k_toep_mma(const double *__restrict__ blo
                                                   int64_t n_steps, const double *__restrict__ x,
                                                   double *__restrict__ y, int64_t d_off, int64_t n_blocks)
 {
-    __shared__ __align__(16) double Xs[64][kMS];   // x[j][c0 .. c0 + 31], j = 0..63
+    // x window of a group of 32 blocks d in [db, db + 32): the rows k - d for the
+    // tile's steps k_lo + j, i.e. x[k_lo - db - 32 + w], w = 0..95 (row of step j
+    // at block d: w = j - (d - db) + 32)
+    __shared__ __align__(16) double Xw[96][kMS];
     __shared__ __align__(16) double As[kMR][kMS];  // A^d[r0 + r][c0 .. c0 + 31]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
-    const int64_t r0 = (int64_t)blockIdx.x * kMR;
-    const int nst = (int)n_steps, mtiles = (nst + 7) >> 3;
+    const int64_t r0 = (int64_t)blockIdx.x * kMR, k_lo = (int64_t)blockIdx.y * 64;
+    const int nst = (int)min((int64_t)64, n_steps - k_lo), mtiles = (nst + 7) >> 3;
     double acc[8][2];
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
-    const int64_t dmax = min((int64_t)nst - 1, d_off + n_blocks - 1);
+    const int64_t dmax = min(k_lo + nst - 1, d_off + n_blocks - 1);
     for (int64_t c0 = 0; c0 < C; c0 += kMC) {
-        __syncthreads();
-        for (int i = tid; i < 64 * kMC; i += 256) {
-            const int j = i / kMC, cc = i % kMC;
-            Xs[j][cc] = (j < nst && c0 + cc < C) ? __ldg(x + (int64_t)j * C + c0 + cc) : 0.0;
-        }
-        for (int64_t d = d_off; d <= dmax; ++d) {
-            const double *Ad = blocks + (d - d_off) * R * C;
+        for (int64_t db = d_off; db <= dmax; db += 32) {
             __syncthreads();
-            for (int i = tid; i < kMR * kMC; i += 256) {
-                const int rr = i / kMC, cc = i % kMC;
-                As[rr][cc] = (r0 + rr < R && c0 + cc < C) ? __ldg(Ad + (r0 + rr) * C + c0 + cc) : 0.0;
+            for (int i = tid; i < 96 * kMC; i += 256) {
+                const int w = i / kMC, cc = i % kMC;
+                const int64_t xr = k_lo - db - 32 + w;
+                Xw[w][cc] = (xr >= 0 && xr < k_lo + nst && c0 + cc < C) ? __ldg(x + xr * C + c0 + cc) : 0.0;
             }
-            __syncthreads();
-            const int dd = (int)d;
+            const int64_t de = min(dmax, db + 31);
+            for (int64_t d = db; d <= de; ++d) {
+                const double *Ad = blocks + (d - d_off) * R * C;
+                __syncthreads();
+                for (int i = tid; i < kMR * kMC; i += 256) {
+                    const int rr = i / kMC, cc = i % kMC;
+                    As[rr][cc] = (r0 + rr < R && c0 + cc < C) ? __ldg(Ad + (r0 + rr) * C + c0 + cc) : 0.0;
+                }
+                __syncthreads();
+                const int dl = (int)(d - k_lo);      // steps j < dl of the tile have no term (k < d)
+                const int wo = 32 - (int)(d - db);   // window row of step j: j + wo
 #pragma unroll
-            for (int ks = 0; ks < kMC / 4; ++ks) {
-                const double b = As[8 * warp + gq][4 * ks + tq];   // B[k = c][n = row]
+                for (int ks = 0; ks < kMC / 4; ++ks) {
+                    const double b = As[8 * warp + gq][4 * ks + tq];   // B[k = c][n = row]
 #pragma unroll
-                for (int mt = 0; mt < 8; ++mt) {
-                    if (mt >= mtiles || 8 * mt + 7 < dd) continue;   // steps k < d: no term
-                    const int j = 8 * mt + gq - dd;                   // x row k - d
-                    const double a = j >= 0 ? Xs[j][4 * ks + tq] : 0.0;
-                    dmma884s(acc[mt][0], acc[mt][1], a, b);
+                    for (int mt = 0; mt < 8; ++mt) {
+                        if (mt >= mtiles || 8 * mt + 7 < dl) continue;
+                        dmma884s(acc[mt][0], acc[mt][1], Xw[8 * mt + gq + wo][4 * ks + tq], b);
+                    }
                 }
             }
         }
     }
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
-        const int k = 8 * mt + gq;
-        if (k >= nst) continue;
+        const int j = 8 * mt + gq;
+        if (j >= nst) continue;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int64_t r = r0 + 8 * warp + 2 * tq + h;
-            if (r < R) y[(int64_t)k * R + r] = acc[mt][h];
+            if (r < R) y[(k_lo + j) * R + r] = acc[mt][h];
         }
     }
+}
+
+static int launch_toep_mma(const double *blocks, int64_t R, int64_t C, int64_t n_steps, const double *x, double *y,
+                           int64_t d_off, int64_t n_blocks, cudaStream_t st, const char *what)
+{
+    dim3 g((unsigned)cdiv(R, kMR), (unsigned)cdiv(n_steps, 64));
+    k_toep_mma<<<g, 256, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks);
+    return cuda_check(cudaGetLastError(), what);
 }
 
 extern "C" int hb_toeplitz_apply(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int transpose,
@@ -283,11 +299,9 @@ extern "C" int hb_toeplitz_apply(int64_t n_blocks, int64_t R, int64_t C, const d
         return HB_ERR_INVALID;
     }
     const int64_t n_out = transpose ? C : R;
-    if (!transpose && !diagonal_only && n_steps <= kRowsMaxSteps && R >= kMmaMinRows) {   // tensor-core GEMMs
-        k_toep_mma<<<(unsigned)cdiv(R, kMR), 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, n_steps, x_dev, y_dev,
-                                                                           0, n_blocks);
-        return cuda_check(cudaGetLastError(), "hb_toeplitz_apply");
-    }
+    if (!transpose && !diagonal_only && R >= kMmaMinRows)   // tensor-core GEMMs
+        return launch_toep_mma(blocks_dev, R, C, n_steps, x_dev, y_dev, 0, n_blocks, (cudaStream_t)stream,
+                               "hb_toeplitz_apply");
     if (!transpose && !diagonal_only && n_steps <= kRowsMaxSteps) {   // warp per (row, kMK-step tile)
         const int64_t warps = n_out * cdiv(n_steps, kMK);
         k_toep_rows<<<(unsigned)cdiv(warps * 32, 256), 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, n_steps,
@@ -309,11 +323,9 @@ extern "C" int hb_toeplitz_apply_range(int64_t d_off, int64_t n_blocks, int64_t 
         return HB_ERR_INVALID;
     }
     const int64_t n_out = transpose ? C : R;
-    if (!transpose && n_steps <= kRowsMaxSteps && R >= kMmaMinRows) {
-        k_toep_mma<<<(unsigned)cdiv(R, kMR), 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, n_steps, x_dev, y_dev,
-                                                                           d_off, n_blocks);
-        return cuda_check(cudaGetLastError(), "hb_toeplitz_apply_range");
-    }
+    if (!transpose && R >= kMmaMinRows)
+        return launch_toep_mma(blocks_dev, R, C, n_steps, x_dev, y_dev, d_off, n_blocks, (cudaStream_t)stream,
+                               "hb_toeplitz_apply_range");
     if (!transpose && n_steps <= kRowsMaxSteps) {
         const int64_t warps = n_out * cdiv(n_steps, kMK);
         k_toep_rows<<<(unsigned)cdiv(warps * 32, 256), 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, n_steps,

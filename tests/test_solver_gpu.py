@@ -23,10 +23,12 @@ def dense(blocks, E_t, transpose=False, diag=False):
     return out
 
 
-@pytest.mark.parametrize("R,C,E_t,d_off", [(2100, 300, 40, 0), (2050, 97, 64, 5), (4096, 64, 9, 0)])
+@pytest.mark.parametrize("R,C,E_t,d_off", [(2100, 300, 40, 0), (2050, 97, 64, 5), (4096, 64, 9, 0),
+                                           (1100, 70, 150, 0), (1030, 40, 130, 70)])
 def test_apply_toeplitz_tensor_core_path(R, C, E_t, d_off):
-    """Operators with >= 2048 rows take the DMMA kernel (k_toep_mma): blockwise
-    products vs numpy, full and d-range (hb_toeplitz_apply_range) forms."""
+    """Operators with >= 1024 rows take the DMMA kernel (k_toep_mma, 64-step
+    tiles): blockwise products vs numpy, full and d-range
+    (hb_toeplitz_apply_range) forms, histories longer than one step tile."""
     import torch
 
     from paper_2102_09811_b200 import _native
