@@ -218,15 +218,20 @@ __device__ __forceinline__ void dmma884s(double &d0, double &d1, double a, doubl
                  : "d"(a), "d"(b));
 }
 
+// TR: the transposed product Y[k][c] += sum_r X[k - d][r] A^d[r][c] (A tile staged
+// as [r][c], B fragment B[k = r][n = c]).
+template <bool TR>
 __global__ void __launch_bounds__(256) k_toep_mma(const double *__restrict__ blocks, int64_t R, int64_t C,
                                                   int64_t n_steps, const double *__restrict__ x,
                                                   double *__restrict__ y, int64_t d_off, int64_t n_blocks)
 {
+    const int64_t n_in = TR ? R : C, n_out = TR ? C : R;
     // x window of a group of 32 blocks d in [db, db + 32): the rows k - d for the
     // tile's steps k_lo + j, i.e. x[k_lo - db - 32 + w], w = 0..95 (row of step j
     // at block d: w = j - (d - db) + 32)
     __shared__ __align__(16) double Xw[96][kMS];
-    __shared__ __align__(16) double As[kMR][kMS];  // A^d[r0 + r][c0 .. c0 + 31]
+    // A^d tile: [out 64][in 32] (row stride 36) or, transposed, [in 32][out 64] (stride 68)
+    __shared__ __align__(16) double As[kMR * kMS > kMC * (kMR + 4) ? kMR * kMS : kMC * (kMR + 4)];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
     const int64_t r0 = (int64_t)blockIdx.x * kMR, k_lo = (int64_t)blockIdx.y * 64;
     const int nst = (int)min((int64_t)64, n_steps - k_lo), mtiles = (nst + 7) >> 3;
@@ -234,28 +239,35 @@ __global__ void __launch_bounds__(256) k_toep_mma(const double *__restrict__ blo
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
     const int64_t dmax = min(k_lo + nst - 1, d_off + n_blocks - 1);
-    for (int64_t c0 = 0; c0 < C; c0 += kMC) {
+    for (int64_t c0 = 0; c0 < n_in; c0 += kMC) {
         for (int64_t db = d_off; db <= dmax; db += 32) {
             __syncthreads();
             for (int i = tid; i < 96 * kMC; i += 256) {
                 const int w = i / kMC, cc = i % kMC;
                 const int64_t xr = k_lo - db - 32 + w;
-                Xw[w][cc] = (xr >= 0 && xr < k_lo + nst && c0 + cc < C) ? __ldg(x + xr * C + c0 + cc) : 0.0;
+                Xw[w][cc] = (xr >= 0 && xr < k_lo + nst && c0 + cc < n_in) ? __ldg(x + xr * n_in + c0 + cc) : 0.0;
             }
             const int64_t de = min(dmax, db + 31);
             for (int64_t d = db; d <= de; ++d) {
                 const double *Ad = blocks + (d - d_off) * R * C;
                 __syncthreads();
                 for (int i = tid; i < kMR * kMC; i += 256) {
-                    const int rr = i / kMC, cc = i % kMC;
-                    As[rr][cc] = (r0 + rr < R && c0 + cc < C) ? __ldg(Ad + (r0 + rr) * C + c0 + cc) : 0.0;
+                    if (TR) {   // rows c0 + ii of A, 64 output columns r0.. (coalesced along the row)
+                        const int ii = i / kMR, oo = i % kMR;
+                        As[ii * (kMR + 4) + oo] =
+                            (c0 + ii < n_in && r0 + oo < n_out) ? __ldg(Ad + (c0 + ii) * C + r0 + oo) : 0.0;
+                    } else {
+                        const int rr = i / kMC, cc = i % kMC;
+                        As[rr * kMS + cc] = (r0 + rr < R && c0 + cc < C) ? __ldg(Ad + (r0 + rr) * C + c0 + cc) : 0.0;
+                    }
                 }
                 __syncthreads();
                 const int dl = (int)(d - k_lo);      // steps j < dl of the tile have no term (k < d)
                 const int wo = 32 - (int)(d - db);   // window row of step j: j + wo
 #pragma unroll
                 for (int ks = 0; ks < kMC / 4; ++ks) {
-                    const double b = As[8 * warp + gq][4 * ks + tq];   // B[k = c][n = row]
+                    const double b = TR ? As[(4 * ks + tq) * (kMR + 4) + 8 * warp + gq]   // B[k = in][n = out]
+                                        : As[(8 * warp + gq) * kMS + 4 * ks + tq];
 #pragma unroll
                     for (int mt = 0; mt < 8; ++mt) {
                         if (mt >= mtiles || 8 * mt + 7 < dl) continue;
@@ -272,16 +284,17 @@ __global__ void __launch_bounds__(256) k_toep_mma(const double *__restrict__ blo
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int64_t r = r0 + 8 * warp + 2 * tq + h;
-            if (r < R) y[(k_lo + j) * R + r] = acc[mt][h];
+            if (r < n_out) y[(k_lo + j) * n_out + r] = acc[mt][h];
         }
     }
 }
 
-static int launch_toep_mma(const double *blocks, int64_t R, int64_t C, int64_t n_steps, const double *x, double *y,
-                           int64_t d_off, int64_t n_blocks, cudaStream_t st, const char *what)
+static int launch_toep_mma(const double *blocks, int64_t R, int64_t C, int tr, int64_t n_steps, const double *x,
+                           double *y, int64_t d_off, int64_t n_blocks, cudaStream_t st, const char *what)
 {
-    dim3 g((unsigned)cdiv(R, kMR), (unsigned)cdiv(n_steps, 64));
-    k_toep_mma<<<g, 256, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks);
+    dim3 g((unsigned)cdiv(tr ? C : R, kMR), (unsigned)cdiv(n_steps, 64));
+    if (tr) k_toep_mma<true><<<g, 256, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks);
+    else k_toep_mma<false><<<g, 256, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks);
     return cuda_check(cudaGetLastError(), what);
 }
 
@@ -299,8 +312,8 @@ extern "C" int hb_toeplitz_apply(int64_t n_blocks, int64_t R, int64_t C, const d
         return HB_ERR_INVALID;
     }
     const int64_t n_out = transpose ? C : R;
-    if (!transpose && !diagonal_only && R >= kMmaMinRows)   // tensor-core GEMMs
-        return launch_toep_mma(blocks_dev, R, C, n_steps, x_dev, y_dev, 0, n_blocks, (cudaStream_t)stream,
+    if (!diagonal_only && n_out >= kMmaMinRows)   // tensor-core GEMMs
+        return launch_toep_mma(blocks_dev, R, C, transpose, n_steps, x_dev, y_dev, 0, n_blocks, (cudaStream_t)stream,
                                "hb_toeplitz_apply");
     if (!transpose && !diagonal_only && n_steps <= kRowsMaxSteps) {   // warp per (row, kMK-step tile)
         const int64_t warps = n_out * cdiv(n_steps, kMK);
@@ -323,9 +336,9 @@ extern "C" int hb_toeplitz_apply_range(int64_t d_off, int64_t n_blocks, int64_t 
         return HB_ERR_INVALID;
     }
     const int64_t n_out = transpose ? C : R;
-    if (!transpose && R >= kMmaMinRows)
-        return launch_toep_mma(blocks_dev, R, C, n_steps, x_dev, y_dev, d_off, n_blocks, (cudaStream_t)stream,
-                               "hb_toeplitz_apply_range");
+    if (n_out >= kMmaMinRows)
+        return launch_toep_mma(blocks_dev, R, C, transpose, n_steps, x_dev, y_dev, d_off, n_blocks,
+                               (cudaStream_t)stream, "hb_toeplitz_apply_range");
     if (!transpose && n_steps <= kRowsMaxSteps) {
         const int64_t warps = n_out * cdiv(n_steps, kMK);
         k_toep_rows<<<(unsigned)cdiv(warps * 32, 256), 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, n_steps,

@@ -50,6 +50,12 @@ def test_apply_toeplitz_tensor_core_path(R, C, E_t, d_off):
     if d_off == 0:
         got = hb.apply_toeplitz(hb.BlockToeplitzMatrix(Bd), xd).cpu().numpy()
         assert np.allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+    # transposed blocks (K', D^T): y[k] = sum_d A^d^T x[k - d], output length R -> run with B^T stored
+    Bt = torch.as_tensor(np.ascontiguousarray(B.transpose(0, 2, 1)), device="cuda")   # (nb, C, R)
+    yt = torch.empty((E_t, R), dtype=torch.float64, device="cuda")
+    _native.call("hb_toeplitz_apply_range", d_off, nb, C, R, _native.ptr(Bt), 1, E_t, _native.ptr(xd),
+                 _native.ptr(yt), _native.stream_handle())
+    assert np.allclose(yt.cpu().numpy(), ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
 
 
 @pytest.mark.parametrize("R,C,E_t", [(7, 7, 5), (20, 11, 9), (64, 40, 33)])
