@@ -201,7 +201,7 @@ using namespace hb;
 // product as one tensor-core GEMM per block d,
 //   Y[k][r] += sum_c X[k - d][c] A^d[r][c]   (k >= d),
 // with mma.sync m8n8k4 f64 (DMMA): M = steps (a CTA owns a 64-step tile,
-// 8-step fragments), N = 64 rows per CTA (warp w: rows 8w..8w+7), K = the
+// 8-step fragments), N = 32 rows per CTA (warp w: rows 8w..8w+7), K = the
 // input index in 32-wide chunks staged in shared memory (row stride 36:
 // conflict-free fragment loads) -- per (chunk, d) the A^d tile and the 64
 // x rows k - d of the step tile.  Every element of A is read from HBM once per
@@ -209,7 +209,7 @@ using namespace hb;
 // sums run in a fixed order (chunk, d, K step).
 // ---------------------------------------------------------------------------
 constexpr int kMmaMinRows = 1024;
-constexpr int kMR = 64, kMC = 32, kMS = kMC + 4;
+constexpr int kMR = 32, kMC = 32, kMS = kMC + 4, kMT = 4 * kMR;   // kMT threads: warp w owns rows 8w..8w+7
 
 __device__ __forceinline__ void dmma884s(double &d0, double &d1, double a, double b)
 {
@@ -221,7 +221,7 @@ __device__ __forceinline__ void dmma884s(double &d0, double &d1, double a, doubl
 // TR: the transposed product Y[k][c] += sum_r X[k - d][r] A^d[r][c] (A tile staged
 // as [r][c], B fragment B[k = r][n = c]).
 template <bool TR>
-__global__ void __launch_bounds__(256) k_toep_mma(const double *__restrict__ blocks, int64_t R, int64_t C,
+__global__ void __launch_bounds__(kMT) k_toep_mma(const double *__restrict__ blocks, int64_t R, int64_t C,
                                                   int64_t n_steps, const double *__restrict__ x,
                                                   double *__restrict__ y, int64_t d_off, int64_t n_blocks)
 {
@@ -242,26 +242,41 @@ __global__ void __launch_bounds__(256) k_toep_mma(const double *__restrict__ blo
     for (int64_t c0 = 0; c0 < n_in; c0 += kMC) {
         for (int64_t db = d_off; db <= dmax; db += 32) {
             __syncthreads();
-            for (int i = tid; i < 96 * kMC; i += 256) {
+            for (int i = tid; i < 96 * kMC; i += kMT) {
                 const int w = i / kMC, cc = i % kMC;
                 const int64_t xr = k_lo - db - 32 + w;
                 Xw[w][cc] = (xr >= 0 && xr < k_lo + nst && c0 + cc < n_in) ? __ldg(x + xr * n_in + c0 + cc) : 0.0;
             }
             const int64_t de = min(dmax, db + 31);
-            for (int64_t d = db; d <= de; ++d) {
+            // A^d tiles pass through registers: the loads of tile d + 1 are issued
+            // before the DMMAs of tile d, so HBM latency overlaps the tensor work
+            constexpr int PT = kMR * kMC / kMT;   // elements per thread
+            auto fetch = [&](int64_t d, double (&v)[PT]) {
                 const double *Ad = blocks + (d - d_off) * R * C;
-                __syncthreads();
-                for (int i = tid; i < kMR * kMC; i += 256) {
+#pragma unroll
+                for (int u = 0; u < PT; ++u) {
+                    const int i = tid + kMT * u;
                     if (TR) {   // rows c0 + ii of A, 64 output columns r0.. (coalesced along the row)
                         const int ii = i / kMR, oo = i % kMR;
-                        As[ii * (kMR + 4) + oo] =
-                            (c0 + ii < n_in && r0 + oo < n_out) ? __ldg(Ad + (c0 + ii) * C + r0 + oo) : 0.0;
+                        v[u] = (c0 + ii < n_in && r0 + oo < n_out) ? __ldg(Ad + (c0 + ii) * C + r0 + oo) : 0.0;
                     } else {
                         const int rr = i / kMC, cc = i % kMC;
-                        As[rr * kMS + cc] = (r0 + rr < R && c0 + cc < C) ? __ldg(Ad + (r0 + rr) * C + c0 + cc) : 0.0;
+                        v[u] = (r0 + rr < R && c0 + cc < C) ? __ldg(Ad + (r0 + rr) * C + c0 + cc) : 0.0;
                     }
                 }
+            };
+            double nxt[PT];
+            fetch(db, nxt);
+            for (int64_t d = db; d <= de; ++d) {
                 __syncthreads();
+#pragma unroll
+                for (int u = 0; u < PT; ++u) {
+                    const int i = tid + kMT * u;
+                    if (TR) As[(i / kMR) * (kMR + 4) + i % kMR] = nxt[u];
+                    else As[(i / kMC) * kMS + i % kMC] = nxt[u];
+                }
+                __syncthreads();
+                if (d < de) fetch(d + 1, nxt);
                 const int dl = (int)(d - k_lo);      // steps j < dl of the tile have no term (k < d)
                 const int wo = 32 - (int)(d - db);   // window row of step j: j + wo
 #pragma unroll
@@ -293,8 +308,8 @@ static int launch_toep_mma(const double *blocks, int64_t R, int64_t C, int tr, i
                            double *y, int64_t d_off, int64_t n_blocks, cudaStream_t st, const char *what)
 {
     dim3 g((unsigned)cdiv(tr ? C : R, kMR), (unsigned)cdiv(n_steps, 64));
-    if (tr) k_toep_mma<true><<<g, 256, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks);
-    else k_toep_mma<false><<<g, 256, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks);
+    if (tr) k_toep_mma<true><<<g, kMT, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks);
+    else k_toep_mma<false><<<g, kMT, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks);
     return cuda_check(cudaGetLastError(), what);
 }
 
