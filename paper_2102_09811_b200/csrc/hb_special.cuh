@@ -71,12 +71,12 @@ constexpr int kMergedDegMax = cmax(cmax(cmax(merged_deg<0>(), merged_deg<1>()), 
                                    cmax(cmax(merged_deg<4>(), merged_deg<5>()), merged_deg<6>()));
 constexpr int kTabDoubles = ((kMergedDegMax + 2) & ~1) * kTabStride;   // room for any kind / layout
 
-// the factor-free kinds 4-6 (pair kernels) store coefficients 2m and 2m+1 of a
+// the kinds 2-6 (pair kernels, potentials) store coefficients 2m and 2m+1 of a
 // column next to each other, at tab[2 (m kTabStride + p) + (k & 1)]: one
 // LDS.128 feeds two Horner steps (16-byte slots, distinct pieces in
 // consecutive slots)
 template <int KIND>
-__host__ __device__ constexpr bool packed() { return KIND >= 4; }
+__host__ __device__ constexpr bool packed() { return KIND >= 2; }   // all but the unused H / F forms
 
 template <int KIND>
 __device__ __forceinline__ void load_table(double *tab)
