@@ -40,6 +40,7 @@
 #include <vector>
 
 #include "hb_common.cuh"
+#include "hb_moment_coeffs.h"
 #include "hb_special.cuh"
 
 #ifndef HB_PAIR_MINB
@@ -48,17 +49,11 @@
 #ifndef HB_PAIR_WARPS   // warps per CTA of the pair kernels
 #define HB_PAIR_WARPS 8
 #endif
-#ifndef HB_SEP
-#define HB_SEP 0     // separable p1 x p1 accumulation (slower at 128 registers; kept for study)
-#endif
-#ifndef HB_P1P1_GROUPED   // p1 x p1 through the G-point grouped loop (1, default: D2 pair kernel -4 %
-#define HB_P1P1_GROUPED 1  // with the per-kind degrees); 0 = one point per iteration
-#endif
 #ifndef HB_P1P1_MINB
 #define HB_P1P1_MINB HB_PAIR_MINB
 #endif
-#ifndef HB_FUSED
-#define HB_FUSED 1   // fused special-function evaluation (hb_special.cuh); 0 = CUDA erf/exp path
+#ifndef HB_QGROUP
+#define HB_QGROUP 2   // quadrature points of the same parity per evaluation group (independent chains)
 #endif
 
 namespace hb {
@@ -67,12 +62,15 @@ struct PairArgs {
     hb_mesh_desc m;
     double step, alpha, d_eps, r_eps;
     double inv2a, inv2a2, inva, kconst;
+    double inv_u2;                 // 1 / u^2 = 1 / (4 alpha h): rho~^2 = rho^2 / u^2
+    double mom_S, mom_q0;          // moment form: L(i) = jac S sum_k a_k M_k i^(q0 - k)
     int64_t e0, e1;
-    int d0, d1, it_lo, it_hi, need_special, nd;
+    int d0, d1, need_special, nd;   // blocks [d0, d1) of this launch, nd = d1 - d0
+    int moments;                    // 1: moment form for the blocks d >= dmom of a pair; 0: all gaps per point
+    const double *Tm;              // moment table [kNK][nd] + term thresholds (k_moment_table)
     int halve_diag;
     double *Q;
     unsigned long long *counter;   // work-item counter (zeroed per launch)
-    int debug_class;               // 0 all pairs; 1 / 2 touching / separated only (HB_DEBUG_CLASS)
     int seg_len;                   // trial elements per separated-pair work item (32, or fewer for few rows)
 };
 
@@ -92,8 +90,13 @@ struct LsLayout {
     static constexpr int SIZE = NIJ * SLOTS + 2 * NIJ;   // + L0 and Lcomb0
 };
 
+constexpr int kPwDoubles = 32 * 17;   // per-warp moment scratch (kPwStride = 17, below)
+
 template <int OP, int NIJ, int NJ>
-__host__ __device__ constexpr int smem_doubles_per_warp() { return 32 * Layout<OP, NIJ>::PAY + LsLayout<NIJ, NJ>::SIZE; }
+__host__ __device__ constexpr int smem_doubles_per_warp_base()
+{
+    return 32 * Layout<OP, NIJ>::PAY + LsLayout<NIJ, NJ>::SIZE + kPwDoubles;
+}
 
 // one point's payload (N doubles, 16-byte aligned) as N/2 LDS.128; loads of
 // fields the caller does not use are dead and removed
@@ -111,24 +114,30 @@ __device__ __forceinline__ void load_payload(const double *p, double (&v)[N])
 }
 
 // ---------------------------------------------------------------------------
-// per-lane time-gap constants
+// per-point gap window of a pair: gaps it_lo..it_hi feed the blocks
+// [w0, w1) (it_lo = max(1, w0 - 1), it_hi = w1, <= 32 gap slots)
 // ---------------------------------------------------------------------------
+struct Win {
+    int w0, w1, it_lo, it_hi;
+};
+
+// a lane's NJ gap slots sl = t + 16 j of window W: cx = 1/(2 sqrt(a delta))
+// (x = rho cx), ic = 1/cx, kk (rho <= r_eps limits), sc (per-gap factor of
+// the factor-free kinds: V = (x H) ic / (2a^2), K = (F/x) (-rn/(2a)) cx,
+// D2 = (erf/x) cx).  Slots past it_hi are clamped (finite values, never stored).
 template <int OP, int NJ>
 struct Slots {
-    double dl[NJ], cx[NJ], ic[NJ], kk[NJ], sc[NJ];   // sc: per-gap factor of the factor-free kinds
-    __device__ void init(const PairArgs &A, int t)
+    double cx[NJ], ic[NJ], kk[NJ], sc[NJ];
+    __device__ __forceinline__ void init(const PairArgs &A, const Win &W, int t)
     {
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-            int it = A.it_lo + t + 16 * j;
-            if (it > A.it_hi) it = A.it_hi;   // clamped slots compute finite values, never stored
+            int it = W.it_lo + t + 16 * j;
+            if (it > W.it_hi) it = W.it_hi;
             const double delta = (double)it * A.step;
-            dl[j] = delta;
-            ic[j] = 2.0 * sqrt(A.alpha * delta);     // 1 / cx: x = rho cx, 1/x = (1/rho) ic
+            ic[j] = 2.0 * sqrt(A.alpha * delta);
             cx[j] = 1.0 / ic[j];
-            if (OP == 2) kk[j] = 1.0 / sqrt(kPi * A.alpha * delta);
-            else kk[j] = sqrt(delta) * A.kconst;
-            // V = (x H) ic / (2a^2), K = (F/x) (-rn/(2a)) cx, D2 = (erf/x) cx
+            kk[j] = (OP == 2) ? 1.0 / sqrt(kPi * A.alpha * delta) : sqrt(delta) * A.kconst;
             sc[j] = OP == 0 ? ic[j] * A.inv2a2 : cx[j];
         }
     }
@@ -143,7 +152,9 @@ struct RegularGeom {
     int nq1;
     __device__ void point(int q, double x[3], double y[3], double &wq, double ht[3], double hs[3]) const
     {
-        const int p = q / nq1, r = q - p * nq1;
+        // p = q / nq1 without the integer division: (q + 1/2) / nq1 is at least
+        // 1/(2 nq1) away from an integer, far above the float rounding
+        const int p = __float2int_rz(((float)q + 0.5f) * __frcp_rn((float)nq1)), r = q - p * nq1;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             x[c] = __ldg(xp + 3 * p + c);
@@ -183,377 +194,521 @@ struct DuffyGeom {
 };
 
 // ---------------------------------------------------------------------------
-// kernel value at one (point pair, gap) in the general branch (scaled by 4 pi):
-//   op 0: (rho/(2a^2) + delta/(a rho)) erf(x) + sqrt(delta/(pi a^3)) exp(-x^2)
-//   op 1: -(rn/rho) [(1/(2a) - delta/rho^2) erf(x) + sqrt(delta/(pi a)) exp(-x^2)/rho]
-//         (the -(rn/rho) factor lives in the hat weights)
-//   op 2: erf(x) / rho
-// Every product/sum is pinned (fma / __dmul_rn): after unrolling the gap
-// slots the compiler must not contract the same expression differently per
-// slot, or a gap's value would depend on the slot it lands in.
+// Moment form.  At gaps where every quadrature point of a pair has
+// t = x^2 <= kTM, the factor-free kernel value is a power series in
+// t = rho~^2 / i (rho~ = rho / u, u = 2 sqrt(alpha h), gap i = delta / h):
+//   L(i) = jac S sum_k a_k M_k i^(q0 - k),   M_k = sum_p W_p rho~_p^(2k)
+//   B^d  = jac sum_k M_k Tm_k(d),            Tm_k(d) = S a_k D2[i^(q0 - k)](d)
+// with the pair's gap-independent moments M_k and the time second
+// difference D2[g](d) = -g(d-1) + 2 g(d) - g(d+1) of the powers taken in
+// closed form.  The reference's B^d = -L(d-1) + 2 L(d) - L(d+1) cancels like
+// 1/(4 d^2) and amplifies the rounding of every L; here the rounding errors of
+// the moments do not depend on d and are not amplified.
+// V: S = u / (2 a^2), q0 = 1/2 (x H); K: S = 1/u, q0 = -1/2 (F/x);
+// D2: S = 1/u, q0 = -1/2 (erf/x).  Coefficients: hb_moment_coeffs.h.
+// A pair's moment gap istar = ceil(max_p rho~_p^2 / kTM) follows from its own
+// points; blocks d >= max(2, istar + 1) come from the moments, blocks below
+// from L(i) evaluated point by point (gaps <= istar + 1).  The split and
+// the per-point lane layout depend on the pair only -- never on the launch's
+// d range, the row chunk or the rank -- so every block entry is bitwise
+// independent of how the work is cut.  Terms beyond the t-dependent count of
+// kMom*Thr are below 2^-56 of the leading one.
 // ---------------------------------------------------------------------------
-template <int OP, int NJ>
-__device__ __forceinline__ double eval_general(const PairArgs &A, const Slots<OP, NJ> &T, int j, double rho,
-                                               double s1, double s2)
+constexpr int kNK = moments::kNK;    // 32: lane k of a warp owns moment k
+constexpr int kPwStride = 17;        // per-warp scratch: powers [32 points][16 (+1 pad)], then moments
+static_assert(kPwDoubles == 32 * kPwStride, "moment scratch size");
+static_assert(kNK == 32, "one moment per lane");
+
+template <int OP>
+__device__ __forceinline__ double mom_coef(int k)
 {
-    const double x = __dmul_rn(rho, T.cx[j]);
-    const double e1 = erf(x);
-    if (OP == 2) return __dmul_rn(e1, s1);
-    const double e2 = exp(-__dmul_rn(x, x));
-    if (OP == 0) return fma(fma(T.dl[j], s2, s1), e1, __dmul_rn(T.kk[j], e2));
-    return fma(fma(-T.dl[j], s1, A.inv2a), e1, __dmul_rn(__dmul_rn(T.kk[j], s2), e2));
+    return OP == 0 ? moments::kMomV[k] : OP == 1 ? moments::kMomK[k] : moments::kMomE[k];
 }
 
-// ---------------------------------------------------------------------------
-// one element pair, all time gaps of the window
-// ---------------------------------------------------------------------------
-template <int OP, bool TP1, bool SP1, int NJ, class Geom>
-__device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq, const double ny[3],
-                                          double jac, int64_t slot, const Slots<OP, NJ> &T,
-                                          double *geo, double *Ls, int lane, const double *tab)
+template <int OP>
+__device__ __forceinline__ double mom_thr(int k)
 {
-    constexpr int NT = TP1 ? 3 : 1, NS = SP1 ? 3 : 1, NIJ = NT * NS;
-    using L = Layout<OP, NIJ>;
-    constexpr int PAY = L::PAY, HOFF = L::HOFF;
-    constexpr int SLOTS = LsLayout<NIJ, NJ>::SLOTS;
-    const int s = lane >> 4, t = lane & 15;
+    return OP == 0 ? moments::kMomVThr[k] : OP == 1 ? moments::kMomKThr[k] : moments::kMomEThr[k];
+}
 
-    // p1 x p1 product rules factor: sum_q v w_p w_r ht_i(p) hs_j(r) =
-    // sum_p (w_p ht_i(p)) [sum_r v (w_r hs_j(r))] -- 3 FMA per evaluation
-    // instead of 9, the row sums flushed when the test point p changes
-    constexpr bool SEP = (NIJ == 9) && Geom::kSeparable && HB_FUSED && HB_SEP;
-    double acc[NJ][NIJ];
-    double inner[NJ][3], arow[3] = {0.0, 0.0, 0.0};
-    int prow = -1;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j)
-        for (int c = 0; c < 3; ++c) inner[j][c] = 0.0;
-    auto flush = [&]() {
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) acc[j][3 * i + c] = fma(arow[i], inner[j][c], acc[j][3 * i + c]);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) inner[j][c] = 0.0;
+// D2[i^q](d) = -(d-1)^q + 2 d^q - (d+1)^q = -2 d^q (expm1(m) cosh(dl) + 2 sinh^2(dl/2)),
+// m = (q/2) log1p(-1/d^2), dl = q atanh(1/d): no cancellation beyond a factor ~2
+__device__ __forceinline__ double second_diff_pow(double d, double q)
+{
+    const double r = 1.0 / d;
+    const double m = 0.5 * q * log1p(-r * r);
+    const double dl = q * atanh(r);
+    const double sh = sinh(0.5 * dl);
+    return -2.0 * pow(d, q) * (expm1(m) * cosh(dl) + 2.0 * sh * sh);
+}
+
+// moment table of a launch: Tm[k][dd] = S a_k D2[i^(q0-k)](d0 + dd) for d >= 2
+// (0 below), then the kNK + 1 term-count thresholds
+template <int OP>
+__global__ void k_moment_table(double *Tm, int d0, int nd, double S, double q0)
+{
+    const int n = kNK * nd;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n + kNK + 1; i += gridDim.x * blockDim.x) {
+        if (i < n) {
+            const int k = i / nd, dd = i - k * nd, d = d0 + dd;
+            Tm[i] = d >= 2 ? (S * mom_coef<OP>(k)) * second_diff_pow((double)d, q0 - k) : 0.0;
+        } else {
+            Tm[i] = mom_thr<OP>(i - n);
         }
-    };
-    double s0[NIJ], sc[NIJ];
-#pragma unroll
-    for (int i = 0; i < NIJ; ++i) {
-        s0[i] = 0.0;
-        sc[i] = 0.0;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) acc[j][i] = 0.0;
     }
+}
 
-    for (int base = 0; base < nq; base += 32) {
-        const int q = base + lane;
-        int small = 0;
-        int nzw = OP == 1 ? 0 : 1;   // K: this point's weights are not all zero (r.n_y != 0)
-        if (q >= nq) {
-            // padding slot of the grouped loop: all zero (x = 0 and 1/x = 0 give
-            // finite series values, the zero weights add exact zeros)
-            double *p = geo + lane * PAY;
+// moments of one chunk of nloc points: lane p writes rt2_p^k, k in
+// [16c, 16c + 16), to Pw[p][k - 16c]; lane (k16, h) = (lane & 15, lane >> 4)
+// then adds sum_{p in [16h, 16h + 16), p < nloc} Pw[p][k16] W_p[i] to
+// mom[c][i], p ascending.
+template <int PAY, int WOFF, int NW>
+__device__ __forceinline__ void chunk_moments(const double *geo, double *Pw, double rt2, int nloc,
+                                              double (&mom)[2][NW], int lane)
+{
+    const int k16 = lane & 15, h = lane >> 4;
+    const int pend = min(16 * h + 16, nloc);
+    double pw = 1.0;
 #pragma unroll
-            for (int i = 0; i < PAY; ++i) p[i] = 0.0;
-        } else {
-            double x[3], y[3], wq, ht[3], hs[3];
-            g.point(q, x, y, wq, ht, hs);
-            const double rx = x[0] - y[0], ry = x[1] - y[1], rz = x[2] - y[2];
-            const double rho = sqrt(rx * rx + ry * ry + rz * rz);
-            small = rho <= A.r_eps;
-            double H[NIJ];
+    for (int c = 0; c < 2; ++c) {
 #pragma unroll
-            for (int i = 0; i < NT; ++i)
-#pragma unroll
-                for (int j = 0; j < NS; ++j)
-                    H[i * NS + j] = (TP1 || SP1) ? wq * ((TP1 ? ht[i] : 1.0) * (SP1 ? hs[j] : 1.0)) : wq;
-            double *p = geo + lane * PAY;
-            p[0] = rho;
-            if constexpr (SEP) {   // [HOFF..+2] = w_r hs(r), [HOFF+3..+5] = w_p ht(p)
-                const int pr = q / g.nq1, rr = q - pr * g.nq1;
-                const double wp = __ldg(g.w + pr), wr = __ldg(g.w + rr);
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    p[HOFF + c] = wr * hs[c];
-                    p[HOFF + 3 + c] = wp * ht[c];
-                }
-            }
-            if (OP == 0) {
-                const double iq = 1.0 / rho;
-                const double Aq = rho * A.inv2a2, Bq = A.inva * iq;
-                p[1] = Aq;
-                p[2] = HB_FUSED ? iq : Bq;
-                if constexpr (!SEP) {
-#pragma unroll
-                    for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
-                }
-                if (A.need_special) {
-                    const double cq = A.step * Bq + Aq;
-#pragma unroll
-                    for (int i = 0; i < NIJ; ++i) {
-                        s0[i] = fma(H[i], Aq, s0[i]);
-                        sc[i] = fma(H[i], cq, sc[i]);
-                    }
-                }
-            } else if (OP == 1) {
-                const double rn = rx * ny[0] + ry * ny[1] + rz * ny[2];
-                const double iq = 1.0 / rho;
-                const double U = small ? 0.0 : -rn * iq, Ur = small ? 0.0 : -rn;
-                nzw = Ur != 0.0;
-                const double P = 1.0 / __dmul_rn(rho, rho);
-                p[1] = HB_FUSED ? iq : P;
-                p[2] = iq;
-#pragma unroll
-                for (int i = 0; i < NIJ; ++i) p[HOFF + i] = HB_FUSED ? (H[i] * Ur) * A.inv2a : H[i] * U;
-                if (A.need_special) {
-                    const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
-#pragma unroll
-                    for (int i = 0; i < NIJ; ++i) {
-                        s0[i] = fma(H[i] * U, c0, s0[i]);
-                        sc[i] = fma(H[i] * U, cc, sc[i]);
-                    }
-                }
-            } else {
-                const double iq = 1.0 / rho;
-                p[1] = iq;
-                if constexpr (!SEP) {
-#pragma unroll
-                    for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
-                }
-                if (A.need_special) {
-#pragma unroll
-                    for (int i = 0; i < NIJ; ++i) s0[i] = fma(H[i], iq, s0[i]);
-                }
-            }
+        for (int k = 0; k < 16; ++k) {
+            Pw[lane * kPwStride + k] = pw;
+            pw = __dmul_rn(pw, rt2);
         }
-        const bool any_small = __any_sync(kFull, small);
-        // K: a chunk whose weights are all exactly zero (coplanar triangles:
-        // r.n_y == 0 at every point) adds exact zeros -- skip its evaluations
-        const bool skip = OP == 1 && !__any_sync(kFull, nzw);
         __syncwarp();
-        const int nloc = min(32, nq - base);
-        if (skip) {
-        } else if (!any_small) {
-#if HB_FUSED
-            // two quadrature points of the same parity per iteration, evaluated
-            // together per gap slot: their x are close, so the small/large-x
-            // branch skipping survives, and the two Horner chains interleave
-            // uniform trip count for both point-parity halves (tail points of
-            // an odd chunk get zero weight), so the branch votes below span the
-            // full warp and compile to uniform branches
-            const int nloc4 = (nloc + 3) & ~3;
-            if constexpr (SEP) {
-                for (int k = s; k < nloc4; k += 2) {
-                    const bool ok = k < nloc;
-                    const double *p = geo + (ok ? k : 0) * PAY;
-                    const int pr = (base + k) / g.nq1;
-                    if (ok && pr != prow) {
-                        if (prow >= 0) flush();
-                        prow = pr;
+#pragma unroll 2
+        for (int p = 16 * h; p < pend; ++p) {
+            const double P = Pw[p * kPwStride + k16];
+            const double *w = geo + p * PAY + WOFF;
 #pragma unroll
-                        for (int i = 0; i < 3; ++i) arow[i] = p[HOFF + 3 + i];
-                    }
-                    const double rho = p[0], s1 = p[1];
-                    const double s2 = (OP == 2) ? 0.0 : p[2];
-#pragma unroll
-                    for (int j = 0; j < NJ; ++j) {
-                        const double x = __dmul_rn(rho, T.cx[j]);
-                        const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                        const double f = special::eval<OP + 4>(x, ix, tab, kFull);
-                        const double v = ok ? f : 0.0;
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) inner[j][c] = fma(v, p[HOFF + c], inner[j][c]);
-                    }
-                }
-            } else if constexpr (NIJ == 9 && !HB_P1P1_GROUPED) {
-                // p1 x p1: nine hat weights per point -- one point per iteration
-                for (int k = s; k < nloc4; k += 2) {
-                    const bool ok = k < nloc;
-                    const double *p = geo + (ok ? k : 0) * PAY;
-                    const double rho = p[0], s1 = p[1];
-                    const double s2 = (OP == 2) ? 0.0 : p[2];
-#pragma unroll
-                    for (int j = 0; j < NJ; ++j) {
-                        const double x = __dmul_rn(rho, T.cx[j]);
-                        const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                        const double f = special::eval<OP + 4>(x, ix, tab, kFull);
-                        const double v = ok ? f : 0.0;
-#pragma unroll
-                        for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, p[HOFF + i], acc[j][i]);
-                    }
-                }
-            } else {
-#ifndef HB_QGROUP
-#define HB_QGROUP 2
-#endif
-                // G points of the same parity per branch region (x close -> the
-                // small/large-x skipping survives; G independent Horner chains)
-                constexpr int G = HB_QGROUP;
-                static_assert(32 % (2 * G) == 0, "padded group loop must stay inside the warp's 32 payload slots");
-                const int nlocg = (nloc + 2 * G - 1) / (2 * G) * (2 * G);
-                // (slots nloc..nlocg-1 hold the all-zero padding payload)
-                // (p1 x p1 keeps the explicit select: measured faster there)
-                constexpr bool SEL = NIJ == 9;
-                for (int k = s; k < nlocg; k += 2 * G) {
-                    double pv[G][PAY];
-                    double rho[G], a[G], b[G];
-                    bool ok[G];
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        ok[g] = !SEL || k + 2 * g < nloc;
-                        load_payload<PAY>(geo + (ok[g] ? k + 2 * g : 0) * PAY, pv[g]);
-                        rho[g] = pv[g][0];
-                        a[g] = pv[g][1];
-                        b[g] = (OP == 2) ? 0.0 : pv[g][2];
-                    }
-#pragma unroll
-                    for (int j = 0; j < NJ; ++j) {
-                        double xs[G], fs[G];
-#pragma unroll
-                        for (int g = 0; g < G; ++g) xs[g] = __dmul_rn(rho[g], T.cx[j]);
-                        const double icj = T.ic[j];
-                        special::eval_nf<OP + 4, G>(
-                            xs, [&](int g) { return __dmul_rn(OP == 0 ? b[g] : a[g], icj); }, fs, tab, kFull);
-#pragma unroll
-                        for (int g = 0; g < G; ++g) {
-                            const double v = ok[g] ? fs[g] : 0.0;
-#pragma unroll
-                            for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, pv[g][HOFF + i], acc[j][i]);
-                        }
-                    }
-                }
-            }
-#else
-#pragma unroll 1
-            for (int k = s; k < nloc; k += 2) {
-                const double *p = geo + k * PAY;
-                const double rho = p[0], s1 = p[1];
-                const double s2 = (OP == 2) ? 0.0 : p[2];
-                double val[NJ];
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) val[j] = eval_general<OP>(A, T, j, rho, s1, s2);
-#pragma unroll
-                for (int i = 0; i < NIJ; ++i) {
-                    const double h = p[HOFF + i];
-#pragma unroll
-                    for (int j = 0; j < NJ; ++j) acc[j][i] = fma(val[j], h, acc[j][i]);
-                }
-            }
-#endif
-        } else {
-            if constexpr (SEP) {
-                if (prow >= 0) flush();
-                prow = -1;
-            }
-            for (int k = s; k < nloc; k += 2) {
-                const double *p = geo + k * PAY;
-                const double rho = p[0], s1 = p[1];
-                const double s2 = (OP == 2) ? 0.0 : p[2];
-                const bool sm = rho <= A.r_eps;
-#if HB_FUSED
-                const unsigned mask = __activemask();
-#endif
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    double val;
-#if HB_FUSED
-                    const double x = __dmul_rn(rho, T.cx[j]);
-                    const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                    const double f = special::eval<OP + 4>(x, ix, tab, mask);
-                    // rho <= r_eps limits, divided by the per-gap factor applied at the end
-                    if (OP == 0) val = sm ? 2.0 * T.kk[j] / T.sc[j] : f;
-                    else if (OP == 1) val = sm ? 0.0 : f;
-                    else val = sm ? T.kk[j] / T.sc[j] : f;
-#else
-                    if (OP == 0) val = sm ? 2.0 * T.kk[j] : eval_general<OP>(A, T, j, rho, s1, s2);
-                    else if (OP == 1) val = sm ? 0.0 : eval_general<OP>(A, T, j, rho, s1, s2);
-                    else val = sm ? T.kk[j] : eval_general<OP>(A, T, j, rho, s1, s2);
-#endif
-                    if constexpr (SEP) {
-#pragma unroll
-                        for (int i = 0; i < 3; ++i)
-#pragma unroll
-                            for (int c = 0; c < 3; ++c)
-                                acc[j][3 * i + c] = fma(val, p[HOFF + 3 + i] * p[HOFF + c], acc[j][3 * i + c]);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(val, p[HOFF + i], acc[j][i]);
-                    }
-                }
-            }
+            for (int i = 0; i < NW; ++i) mom[c][i] = fma(P, w[i], mom[c][i]);
         }
         __syncwarp();
     }
-    if constexpr (SEP) {
-        if (prow >= 0) flush();
-    }
+}
 
-    // fold the two point-parity halves (commutative: both halves get equal bits)
+// fold the two point halves of the moments and park them in Pw as Ms[i][k]
+template <int NW>
+__device__ __forceinline__ void store_moments(double (&mom)[2][NW], double *Pw, int lane)
+{
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
+    for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int i = 0; i < NIJ; ++i) acc[j][i] += __shfl_xor_sync(kFull, acc[j][i], 16);
-    if (A.need_special) {
+        for (int i = 0; i < NW; ++i) mom[c][i] += __shfl_xor_sync(kFull, mom[c][i], 16);   // commutative
+    __syncwarp();
+    if (lane < 16) {
 #pragma unroll
-        for (int o = 16; o >= 1; o >>= 1)
-#pragma unroll
-            for (int i = 0; i < NIJ; ++i) {
-                s0[i] += __shfl_xor_sync(kFull, s0[i], o);
-                if (OP != 2) sc[i] += __shfl_xor_sync(kFull, sc[i], o);
-            }
-    }
-    const int nslots = A.it_hi - A.it_lo + 1;
-    if (s == 0) {
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const int sl = t + 16 * j;
-            if (sl < nslots) {
-#pragma unroll
-                for (int i = 0; i < NIJ; ++i) Ls[i * SLOTS + sl] = jac * (HB_FUSED ? acc[j][i] * T.sc[j] : acc[j][i]);
-            }
-        }
-    }
-    double *L0 = Ls + NIJ * SLOTS, *Lc = L0 + NIJ;
-    if (lane == 0 && A.need_special) {
-#pragma unroll
-        for (int i = 0; i < NIJ; ++i) {
-            L0[i] = jac * s0[i];
-            Lc[i] = jac * (OP == 2 ? s0[i] : sc[i]);
+        for (int i = 0; i < NW; ++i) {
+            Pw[i * kNK + lane] = mom[0][i];
+            Pw[i * kNK + 16 + lane] = mom[1][i];
         }
     }
     __syncwarp();
-    // 3-term combination (AssemblyPlan.targets) with lanes over blocks d
+}
+
+// blocks [dmom, d1) of the launch from the moments Ms, lanes over d; the
+// series is cut at the lane's own term count (t = rmax / (d - 1))
+template <int NIJ>
+__device__ __forceinline__ void combine_moments(const PairArgs &A, int64_t slot, int lane, const double *Ms,
+                                                double jac, int dmom, double rmax)
+{
     double *dst = A.Q + slot * (int64_t)(NIJ * A.nd);
-    for (int dd = lane; dd < A.nd; dd += 32) {
-        const int d = A.d0 + dd;
+    const double *thr = A.Tm + kNK * A.nd;
+    for (int dd0 = max(dmom, A.d0) - A.d0; dd0 < A.nd; dd0 += 32) {
+        const int dd = dd0 + lane;
+        const bool an = dd < A.nd;
+        int nk = 0;
+        if (an) {   // smallest term count whose threshold covers t (thresholds ascending, thr[kNK] = kTM)
+            const double t = rmax / (double)(A.d0 + dd - 1);
+            int lo = 1, hi = kNK;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (t <= __ldg(thr + mid)) hi = mid;
+                else lo = mid + 1;
+            }
+            nk = lo;
+        }
+        const int nkw = __reduce_max_sync(kFull, nk);
+        double b[NIJ];
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) b[i] = 0.0;
+        const double *tm = A.Tm + (an ? dd : 0);
+        for (int k = 0; k < nkw; ++k) {
+            const double tk = __ldg(tm + k * A.nd);
+            if (k < nk) {
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) b[i] = fma(Ms[i * kNK + k], tk, b[i]);
+            }
+        }
+        if (an) {
+#pragma unroll
+            for (int i = 0; i < NIJ; ++i) dst[i * A.nd + dd] = jac * b[i];
+        }
+    }
+}
+
+// blocks [W.w0, W.w1) by the 3-term combination of the staged L row of the
+// window (Ls: [NIJ][SLOTS], then L0[NIJ], Lcomb0[NIJ]), lanes over d
+template <int NIJ, int SLOTS>
+__device__ __forceinline__ void combine_window(const PairArgs &A, const Win &W, const double *Ls, int64_t slot,
+                                               int lane)
+{
+    const double *L0 = Ls + NIJ * SLOTS, *Lc = L0 + NIJ;
+    double *dst = A.Q + slot * (int64_t)(NIJ * A.nd);
+    for (int d = W.w0 + lane; d < W.w1; d += 32) {
+        const int dd = d - A.d0;
 #pragma unroll
         for (int i = 0; i < NIJ; ++i) {
             const double *Li = Ls + i * SLOTS;
             double b;
             if (d == 0) {
-                const double l1 = Li[1 - A.it_lo];
+                const double l1 = Li[1 - W.it_lo];
                 b = Lc[i] + (-l1);
             } else {
-                const double lm = (d - 1 == 0) ? L0[i] : Li[d - 1 - A.it_lo];
-                const double lc = Li[d - A.it_lo];
-                const double lp = Li[d + 1 - A.it_lo];
+                const double lm = (d - 1 == 0) ? L0[i] : Li[d - 1 - W.it_lo];
+                const double lc = Li[d - W.it_lo];
+                const double lp = Li[d + 1 - W.it_lo];
                 b = -lm + 2.0 * lc;
                 b = b + (-lp);
             }
             dst[i * A.nd + dd] = b;
         }
     }
+}
+
+// pair's moment gap from its largest rho~^2 (warp-uniform)
+__device__ __forceinline__ int moment_istar(double rmax)
+{
+    const double is = ceil(rmax / moments::kTM);
+    return is < 1.0 ? 1 : (is > 1e9 ? 1000000000 : (int)is);
+}
+
+// lanes per point group of the per-point evaluation: the pair's per-point
+// gaps are 1..istar+1, so GW = 4 / 8 lanes cover them with 8 / 4 point
+// groups; larger istar use 16 lanes x NJ slots (2 point groups)
+__device__ __forceinline__ int pair_gw(int istar) { return istar + 1 <= 4 ? 4 : (istar + 1 <= 8 ? 8 : 16); }
+
+// ---------------------------------------------------------------------------
+// per-point evaluation of one chunk of nloc points for the lane's nje gap
+// slots; gw lanes per point group, npg = 32 / gw point groups (lane's group
+// pg = lane / gw takes points pg, pg + npg, ...; with G points per step).
+// gw and nje are warp-uniform runtime values (one code copy for all layouts).
+// ---------------------------------------------------------------------------
+template <int OP, int NIJ, int PAY, int HOFF, int NJ>
+__device__ __forceinline__ void eval_points(const PairArgs &A, const Slots<OP, NJ> &T, const double *geo, int nloc,
+                                            bool any_small, int pg, int npg, int nje, double (&acc)[NJ][NIJ],
+                                            const double *tab)
+{
+    const int NPG = npg;
+    if (!any_small) {
+        // G points of one group per step (x close -> the small/large-x
+        // skipping survives; G independent Horner chains); uniform trip count
+        // for all groups (padding slots hold the all-zero payload), so the
+        // branch votes span the full warp
+        constexpr int G = HB_QGROUP;
+        const int STEP = NPG * G;   // divides 32: the padded loop stays inside the warp's 32 payload slots
+        const int nlocg = (nloc + STEP - 1) / STEP * STEP;
+        constexpr bool SEL = NIJ == 9;   // p1 x p1 keeps the explicit select: measured faster there
+        for (int k = pg; k < nlocg; k += STEP) {
+            double pv[G][PAY];
+            double rho[G], a[G], b[G];
+            bool ok[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                ok[g] = !SEL || k + NPG * g < nloc;
+                load_payload<PAY>(geo + (ok[g] ? k + NPG * g : 0) * PAY, pv[g]);
+                rho[g] = pv[g][0];
+                a[g] = pv[g][1];
+                b[g] = (OP == 2) ? 0.0 : pv[g][2];
+            }
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                if (j >= nje) break;
+                double xs[G], fs[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) xs[g] = __dmul_rn(rho[g], T.cx[j]);
+                const double icj = T.ic[j];
+                special::eval_nf<OP + 4, G>(
+                    xs, [&](int g) { return __dmul_rn(OP == 0 ? b[g] : a[g], icj); }, fs, tab, kFull);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const double v = ok[g] ? fs[g] : 0.0;
+#pragma unroll
+                    for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, pv[g][HOFF + i], acc[j][i]);
+                }
+            }
+        }
+    } else {
+        for (int k = pg; k < nloc; k += NPG) {
+            const double *p = geo + k * PAY;
+            const double rho = p[0], s1 = p[1];
+            const double s2 = (OP == 2) ? 0.0 : p[2];
+            const bool sm = rho <= A.r_eps;
+            const unsigned mask = __activemask();
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                if (j >= nje) break;
+                const double x = __dmul_rn(rho, T.cx[j]);
+                const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
+                const double f = special::eval<OP + 4>(x, ix, tab, mask);
+                // rho <= r_eps limits, divided by the per-gap factor applied at the end
+                double val;
+                if (OP == 0) val = sm ? 2.0 * T.kk[j] / T.sc[j] : f;
+                else if (OP == 1) val = sm ? 0.0 : f;
+                else val = sm ? T.kk[j] / T.sc[j] : f;
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(val, p[HOFF + i], acc[j][i]);
+            }
+        }
+    }
+}
+
+// sum the point groups (butterfly over the lane bits >= log2(gw); every lane
+// ends with the same bits) and stage L for the window slots of gaps < gend
+template <int OP, int NIJ, int NJ, int SLOTS>
+__device__ __forceinline__ void stage_L(const Win &W, const Slots<OP, NJ> &T, double (&acc)[NJ][NIJ], double jac,
+                                        int gend, int gw, int nje, double *Ls, int lane)
+{
+    for (int o = 16; o >= gw; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            if (j >= nje) break;
+#pragma unroll
+            for (int i = 0; i < NIJ; ++i) acc[j][i] += __shfl_xor_sync(kFull, acc[j][i], o);
+        }
+    const int t = lane & (gw - 1), nslots = W.it_hi - W.it_lo + 1;
+    if (lane < gw) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int sl = t + 16 * j;
+            if (j < nje && sl < nslots && W.it_lo + sl < gend) {
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) Ls[i * SLOTS + sl] = jac * (acc[j][i] * T.sc[j]);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// payload of quadrature point q (lane's slot): rho, per-op scalars, weights;
+// returns rho~^2 and the small / nonzero-weight flags; SPECIAL adds the
+// delta = 0 sums (closed-form limits) of the point
+// ---------------------------------------------------------------------------
+template <int OP, bool TP1, bool SP1, class Geom>
+__device__ __forceinline__ void point_payload(const PairArgs &A, const Geom &g, int q, int nq, const double ny[3],
+                                              bool SPECIAL, double *p, double &rt2, int &small, int &nzw,
+                                              double (&s0)[(TP1 ? 3 : 1) * (SP1 ? 3 : 1)],
+                                              double (&sc)[(TP1 ? 3 : 1) * (SP1 ? 3 : 1)])
+{
+    constexpr int NT = TP1 ? 3 : 1, NS = SP1 ? 3 : 1, NIJ = NT * NS;
+    using L = Layout<OP, NIJ>;
+    constexpr int PAY = L::PAY, HOFF = L::HOFF;
+    small = 0;
+    nzw = OP == 1 ? 0 : 1;   // K: this point's weights are not all zero (r.n_y != 0)
+    rt2 = 0.0;
+    if (q >= nq) {
+        // padding slot of the grouped loop: all zero (x = 0 and 1/x = 0 give
+        // finite series values, the zero weights add exact zeros)
+#pragma unroll
+        for (int i = 0; i < PAY; ++i) p[i] = 0.0;
+        return;
+    }
+    double x[3], y[3], wq, ht[3], hs[3];
+    g.point(q, x, y, wq, ht, hs);
+    const double rx = x[0] - y[0], ry = x[1] - y[1], rz = x[2] - y[2];
+    const double r2 = rx * rx + ry * ry + rz * rz;
+    const double rho = sqrt(r2);
+    rt2 = r2 * A.inv_u2;
+    small = rho <= A.r_eps;
+    double H[NIJ];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+            H[i * NS + j] = (TP1 || SP1) ? wq * ((TP1 ? ht[i] : 1.0) * (SP1 ? hs[j] : 1.0)) : wq;
+    p[0] = rho;
+    if (OP == 0) {
+        const double iq = 1.0 / rho;
+        const double Aq = rho * A.inv2a2, Bq = A.inva * iq;
+        p[1] = Aq;
+        p[2] = iq;
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
+        if (SPECIAL) {
+            const double cq = A.step * Bq + Aq;
+#pragma unroll
+            for (int i = 0; i < NIJ; ++i) {
+                s0[i] = fma(H[i], Aq, s0[i]);
+                sc[i] = fma(H[i], cq, sc[i]);
+            }
+        }
+    } else if (OP == 1) {
+        const double rn = rx * ny[0] + ry * ny[1] + rz * ny[2];
+        const double iq = 1.0 / rho;
+        const double U = small ? 0.0 : -rn * iq, Ur = small ? 0.0 : -rn;
+        nzw = Ur != 0.0;
+        const double P = 1.0 / __dmul_rn(rho, rho);
+        p[1] = iq;
+        p[2] = iq;
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) p[HOFF + i] = (H[i] * Ur) * A.inv2a;
+        if (SPECIAL) {
+            const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
+#pragma unroll
+            for (int i = 0; i < NIJ; ++i) {
+                s0[i] = fma(H[i] * U, c0, s0[i]);
+                sc[i] = fma(H[i] * U, cc, sc[i]);
+            }
+        }
+    } else {
+        const double iq = 1.0 / rho;
+        p[1] = iq;
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) p[HOFF + i] = H[i];
+        if (SPECIAL) {
+#pragma unroll
+            for (int i = 0; i < NIJ; ++i) s0[i] = fma(H[i], iq, s0[i]);
+        }
+    }
+}
+
+// per-point L of one window for one lane layout: gap slots [it_lo, gend)
+// over all point chunks, staged into Ls
+template <int OP, bool TP1, bool SP1, int NJ, class Geom>
+__device__ __noinline__ void pair_points(const PairArgs &A, const Win &W, const Geom &g, int nq, const double ny[3],
+                                         double jac, int gend, int gw, int nje, double *geo, double *Ls, int lane,
+                                         const double *tab)
+{
+    constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
+    using L = Layout<OP, NIJ>;
+    constexpr int PAY = L::PAY, HOFF = L::HOFF;
+    constexpr int SLOTS = LsLayout<NIJ, NJ>::SLOTS;
+    Slots<OP, NJ> T;
+    T.init(A, W, lane & (gw - 1));
+    const int pg = lane / gw, npg = 32 / gw;
+    double acc[NJ][NIJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) acc[j][i] = 0.0;
+    double dummy[NIJ];
+    for (int base = 0; base < nq; base += 32) {
+        double rt2;
+        int small, nzw;
+        point_payload<OP, TP1, SP1>(A, g, base + lane, nq, ny, false, geo + lane * PAY, rt2, small, nzw, dummy, dummy);
+        const bool any_small = __any_sync(kFull, small);
+        const bool skip = OP == 1 && !__any_sync(kFull, nzw);   // all-zero K chunk: exact zeros
+        __syncwarp();
+        if (!skip) eval_points<OP, NIJ, PAY, HOFF, NJ>(A, T, geo, min(32, nq - base), any_small, pg, npg, nje, acc, tab);
+        __syncwarp();
+    }
+    stage_L<OP, NIJ, NJ, SLOTS>(W, T, acc, jac, gend, gw, nje, Ls, lane);
+}
+
+// the per-point windows of a pair: blocks [d0, dend) in windows of <= 32 gap
+// slots (the first from block 0 or 1 holds 32 blocks, later ones 30); per
+// window the gaps up to istar + 1, then the 3-term combination
+template <int NIJ, int SLOTS, class PointsFn>
+__device__ __forceinline__ void per_point_windows(const PairArgs &A, int dend, int istar, double *Ls, int64_t slot,
+                                                  int lane, const PointsFn &points)
+{
+    int w0 = A.d0;
+    while (w0 < dend) {
+        Win W;
+        W.w0 = w0;
+        W.w1 = min(dend, w0 <= 1 ? 32 : w0 + 30);
+        W.it_lo = max(1, w0 - 1);
+        W.it_hi = W.w1;
+        const int npp = min(W.it_hi, istar + 1) - W.it_lo + 1;
+        if (npp > 0) points(W, npp);
+        __syncwarp();
+        combine_window<NIJ, SLOTS>(A, W, Ls, slot, lane);
+        __syncwarp();
+        w0 = W.w1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// one element pair, all blocks [d0, d1) of the launch.  Phase 1: payload over
+// all point chunks -> the pair's largest rho~^2 (hence istar), the delta = 0
+// sums and (when the launch may hold moment blocks) the moments.  Phase 2:
+// point-by-point L for the gaps below istar + 2, window by window (payload
+// recomputed: same bits; the phases never hold their registers at the same
+// time), 3-term blocks below dmom = max(2, istar + 1), moment blocks above.
+// rt2_lo: a lower bound of the pair's rho~^2 (squared centroid distance).
+// ---------------------------------------------------------------------------
+template <int OP, bool TP1, bool SP1, int NJ, class Geom>
+__device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq, const double ny[3],
+                                          double jac, double rt2_lo, int64_t slot, double *geo, double *Ls,
+                                          double *Pw, int lane, const double *tab)
+{
+    constexpr int NT = TP1 ? 3 : 1, NS = SP1 ? 3 : 1, NIJ = NT * NS;
+    using L = Layout<OP, NIJ>;
+    constexpr int PAY = L::PAY, HOFF = L::HOFF;
+    constexpr int SLOTS = LsLayout<NIJ, NJ>::SLOTS;
+    double *p_lane = geo + lane * PAY;
+    double *L0 = Ls + NIJ * SLOTS, *Lc = L0 + NIJ;
+    const bool try_mom = A.moments && A.d1 - 1 >= max(2, moment_istar(rt2_lo) + 1);
+
+    // ---- phase 1 ----
+    double rmax = 0.0;
+    {
+        double mom[2][NIJ], s0[NIJ], sc[NIJ];
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) s0[i] = sc[i] = mom[0][i] = mom[1][i] = 0.0;
+        for (int base = 0; base < nq; base += 32) {
+            double rt2;
+            int small, nzw;
+            point_payload<OP, TP1, SP1>(A, g, base + lane, nq, ny, A.need_special, p_lane, rt2, small, nzw, s0, sc);
+            rmax = fmax(rmax, rt2);
+            const bool skip = OP == 1 && !__any_sync(kFull, nzw);   // all-zero K chunk: exact zeros
+            __syncwarp();
+            if (try_mom && !skip) chunk_moments<PAY, HOFF, NIJ>(geo, Pw, rt2, min(32, nq - base), mom, lane);
+            __syncwarp();
+        }
+        if (A.need_special) {
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) {
+                    s0[i] += __shfl_xor_sync(kFull, s0[i], o);
+                    if (OP != 2) sc[i] += __shfl_xor_sync(kFull, sc[i], o);
+                }
+            if (lane == 0) {
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) {
+                    L0[i] = jac * s0[i];
+                    Lc[i] = jac * (OP == 2 ? s0[i] : sc[i]);
+                }
+            }
+        }
+        if (try_mom) store_moments<NIJ>(mom, Pw, lane);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(kFull, rmax, o));
+    // without the moment form every gap is evaluated point by point
+    const int istar = A.moments ? moment_istar(rmax) : (1 << 29);
+    const int dmom = max(2, istar + 1);
+    const bool use_mom = try_mom && A.d1 > dmom;
+
+    // ---- phase 2: per-point windows below dmom, moment blocks from dmom ----
+    const int gend = istar + 2;
+    const int gw = pair_gw(istar);
+    per_point_windows<NIJ, SLOTS>(A, use_mom ? min(A.d1, dmom) : A.d1, istar, Ls, slot, lane,
+                                  [&](const Win &W, int npp) {
+        pair_points<OP, TP1, SP1, NJ>(A, W, g, nq, ny, jac, gend, gw, (gw == 16 && npp > 16) ? NJ : 1, geo, Ls, lane,
+                                      tab);
+    });
+    if (use_mom) combine_moments<NIJ>(A, slot, lane, Pw, jac, dmom, rmax);
     __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
 // K (p0 test x p1 trial) for both orientations of one separated pair.
 // The product rule of a separated pair (a, b) uses the same point pairs for
-// K(a, b) and K(b, a): rho -- hence x and F(x) at every gap -- is shared, and
-// only the per-point weights differ:
+// K(a, b) and K(b, a): rho -- hence x and F(x) at every gap, and the powers
+// of the moment form -- is shared, and only the per-point weights differ:
 //   K(a, b): -(r . n_b)/rho * w hs_j(y_r)      (test a, trial hats on b)
 //   K(b, a): +(r . n_a)/rho * w ht_j(x_p)      (test b, trial hats on a)
 // with r = x_p - y_r (the reverse orientation's r is -r, exactly).  Each
@@ -564,99 +719,81 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
 // ---------------------------------------------------------------------------
 constexpr int kDualPay = 8;   // rho, 1/rho, Wf[3], Wr[3]
 template <int NJ>
-__host__ __device__ constexpr int dual_smem_doubles_per_warp() { return 32 * kDualPay + 2 * LsLayout<3, NJ>::SIZE; }
+__host__ __device__ constexpr int dual_smem_doubles_per_warp_base() { return 32 * kDualPay + 2 * LsLayout<3, NJ>::SIZE + kPwDoubles; }
 
-// 3-term time combination of one staged row of L values (Ls: [NIJ][SLOTS],
-// then L0[NIJ], Lcomb0[NIJ]) into Q slot `slot`, lanes over blocks d
-template <int NIJ, int NJ>
-__device__ __forceinline__ void combine_store(const PairArgs &A, const double *Ls, int64_t slot, int lane)
+// payload of one point of the dual K pair (both orientations' weights);
+// `special` adds the delta = 0 sums of both orientations
+__device__ __forceinline__ void dual_payload(const PairArgs &A, const RegularGeom &g, int q, int nq, const double nb[3],
+                                             const double na[3], bool special, double *p, double &rt2, int &small,
+                                             int &nzw, double (&s0f)[3], double (&scf)[3], double (&s0r)[3],
+                                             double (&scr)[3])
 {
-    constexpr int SLOTS = LsLayout<NIJ, NJ>::SLOTS;
-    const double *L0 = Ls + NIJ * SLOTS, *Lc = L0 + NIJ;
-    double *dst = A.Q + slot * (int64_t)(NIJ * A.nd);
-    for (int dd = lane; dd < A.nd; dd += 32) {
-        const int d = A.d0 + dd;
+    small = 0;
+    nzw = 0;
+    rt2 = 0.0;
+    if (q >= nq) {   // all-zero padding slot (see point_payload)
 #pragma unroll
-        for (int i = 0; i < NIJ; ++i) {
-            const double *Li = Ls + i * SLOTS;
-            double b;
-            if (d == 0) {
-                const double l1 = Li[1 - A.it_lo];
-                b = Lc[i] + (-l1);
-            } else {
-                const double lm = (d - 1 == 0) ? L0[i] : Li[d - 1 - A.it_lo];
-                const double lc = Li[d - A.it_lo];
-                const double lp = Li[d + 1 - A.it_lo];
-                b = -lm + 2.0 * lc;
-                b = b + (-lp);
-            }
-            dst[i * A.nd + dd] = b;
+        for (int i = 0; i < kDualPay; ++i) p[i] = 0.0;
+        return;
+    }
+    double x[3], y[3], wq, ht[3], hs[3];
+    g.point(q, x, y, wq, ht, hs);
+    const double rx = x[0] - y[0], ry = x[1] - y[1], rz = x[2] - y[2];
+    const double r2 = rx * rx + ry * ry + rz * rz;
+    const double rho = sqrt(r2);
+    rt2 = r2 * A.inv_u2;
+    small = rho <= A.r_eps;
+    const double rnb = rx * nb[0] + ry * nb[1] + rz * nb[2];
+    const double rna = (-rx) * na[0] + (-ry) * na[1] + (-rz) * na[2];   // reverse: r' = -r
+    const double iq = 1.0 / rho;
+    const double Vf = small ? 0.0 : -rnb, Vr = small ? 0.0 : -rna;   // rho U (factor-free F/x)
+    nzw = Vf != 0.0 || Vr != 0.0;
+    p[0] = rho;
+    p[1] = iq;
+    double Hf[3], Hr[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        Hf[i] = wq * (1.0 * hs[i]);
+        Hr[i] = wq * (1.0 * ht[i]);
+        p[2 + i] = (Hf[i] * Vf) * A.inv2a;
+        p[5 + i] = (Hr[i] * Vr) * A.inv2a;
+    }
+    if (special) {
+        const double Uf = small ? 0.0 : -rnb * iq, Ur = small ? 0.0 : -rna * iq;
+        const double P = 1.0 / __dmul_rn(rho, rho);
+        const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            s0f[i] = fma(Hf[i] * Uf, c0, s0f[i]);
+            scf[i] = fma(Hf[i] * Uf, cc, scf[i]);
+            s0r[i] = fma(Hr[i] * Ur, c0, s0r[i]);
+            scr[i] = fma(Hr[i] * Ur, cc, scr[i]);
         }
     }
 }
 
-// MODE 0: both outputs; 1: only K(a, b) (forward); 2: only K(b, a) (reverse) --
-// the other row lies outside the launch.  Each output's arithmetic is the same
-// in every mode (same points, order, fs and weights), so a block entry does not
-// depend on which rows share the launch (row chunks, ranks).
-template <int NJ, int MODE = 0>
-__device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularGeom &g, int nq, const double nb[3],
-                                               const double na[3], double jac, int64_t slot_f, int64_t slot_r,
-                                               const Slots<1, NJ> &T, double *geo, double *Ls, int lane,
-                                               const double *tab)
+// per-point L of one window of the dual pair (both orientations; stage_f /
+// stage_r: which staged rows are needed), runtime lane layout gw / nje
+template <int NJ>
+__device__ __noinline__ void dual_points(const PairArgs &A, const Win &W, const RegularGeom &g, int nq,
+                                         const double nb[3], const double na[3], double jac, int gend, int gw,
+                                         int nje, bool stage_f, bool stage_r, double *geo, double *Lf, double *Lr,
+                                         int lane, const double *tab)
 {
-    constexpr bool DF = MODE != 2, DR = MODE != 1;
-    constexpr int PAY = kDualPay, SLOTS = LsLayout<3, NJ>::SLOTS, LSZ = LsLayout<3, NJ>::SIZE;
-    const int s = lane >> 4, t = lane & 15;
-    double af[NJ][3], ar[NJ][3], s0f[3], scf[3], s0r[3], scr[3];
+    constexpr int PAY = kDualPay, SLOTS = LsLayout<3, NJ>::SLOTS;
+    Slots<1, NJ> T;
+    T.init(A, W, lane & (gw - 1));
+    const int pg = lane / gw, NPG = 32 / gw;
+    double af[NJ][3], ar[NJ][3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        s0f[i] = scf[i] = s0r[i] = scr[i] = 0.0;
+    for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < NJ; ++j) af[j][i] = ar[j][i] = 0.0;
-    }
+    double d3[3];
     for (int base = 0; base < nq; base += 32) {
-        const int q = base + lane;
-        int small = 0, nzw = 0;
-        if (q >= nq) {   // all-zero padding slot (see eval_pair)
-            double *p = geo + lane * PAY;
-#pragma unroll
-            for (int i = 0; i < PAY; ++i) p[i] = 0.0;
-        } else {
-            double x[3], y[3], wq, ht[3], hs[3];
-            g.point(q, x, y, wq, ht, hs);
-            const double rx = x[0] - y[0], ry = x[1] - y[1], rz = x[2] - y[2];
-            const double rho = sqrt(rx * rx + ry * ry + rz * rz);
-            small = rho <= A.r_eps;
-            const double rnb = rx * nb[0] + ry * nb[1] + rz * nb[2];
-            const double rna = (-rx) * na[0] + (-ry) * na[1] + (-rz) * na[2];   // reverse: r' = -r
-            const double iq = 1.0 / rho;
-            const double Uf = small ? 0.0 : -rnb * iq, Ur = small ? 0.0 : -rna * iq;
-            const double Vf = small ? 0.0 : -rnb, Vr = small ? 0.0 : -rna;   // rho U (factor-free F/x)
-            nzw = (DF && Vf != 0.0) || (DR && Vr != 0.0);
-            const double P = 1.0 / __dmul_rn(rho, rho);
-            double *p = geo + lane * PAY;
-            p[0] = rho;
-            p[1] = iq;
-            double Hf[3], Hr[3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                Hf[i] = wq * (1.0 * hs[i]);
-                Hr[i] = wq * (1.0 * ht[i]);
-                if (DF) p[2 + i] = (Hf[i] * Vf) * A.inv2a;
-                if (DR) p[5 + i] = (Hr[i] * Vr) * A.inv2a;
-            }
-            if (A.need_special) {
-                const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    s0f[i] = fma(Hf[i] * Uf, c0, s0f[i]);
-                    scf[i] = fma(Hf[i] * Uf, cc, scf[i]);
-                    s0r[i] = fma(Hr[i] * Ur, c0, s0r[i]);
-                    scr[i] = fma(Hr[i] * Ur, cc, scr[i]);
-                }
-            }
-        }
+        double rt2;
+        int small, nzw;
+        dual_payload(A, g, base + lane, nq, nb, na, false, geo + lane * PAY, rt2, small, nzw, d3, d3, d3, d3);
         const bool any_small = __any_sync(kFull, small);
         const bool skip = !__any_sync(kFull, nzw);   // both orientations' weights all zero (coplanar pair)
         __syncwarp();
@@ -664,19 +801,20 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
         if (skip) {
         } else if (!any_small) {
             constexpr int G = HB_QGROUP;
-            static_assert(32 % (2 * G) == 0, "padded group loop must stay inside the warp's 32 payload slots");
-            const int nlocg = (nloc + 2 * G - 1) / (2 * G) * (2 * G);
-            for (int k = s; k < nlocg; k += 2 * G) {   // padding slots are all zero
+            const int STEP = NPG * G;   // divides 32
+            const int nlocg = (nloc + STEP - 1) / STEP * STEP;
+            for (int k = pg; k < nlocg; k += STEP) {   // padding slots are all zero
                 double pv[G][PAY];
                 double rho[G], a[G];
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
-                    load_payload<PAY>(geo + (k + 2 * gg) * PAY, pv[gg]);
+                    load_payload<PAY>(geo + (k + NPG * gg) * PAY, pv[gg]);
                     rho[gg] = pv[gg][0];
                     a[gg] = pv[gg][1];
                 }
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
+                    if (j >= nje) break;
                     double xs[G], fs[G];
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) xs[gg] = __dmul_rn(rho[gg], T.cx[j]);
@@ -693,13 +831,14 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
                 }
             }
         } else {
-            for (int k = s; k < nloc; k += 2) {
+            for (int k = pg; k < nloc; k += NPG) {
                 const double *p = geo + k * PAY;
                 const double rho = p[0], s1 = p[1];
                 const bool sm = rho <= A.r_eps;
                 const unsigned mask = __activemask();
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
+                    if (j >= nje) break;
                     const double x = __dmul_rn(rho, T.cx[j]);
                     const double ix = __dmul_rn(s1, T.ic[j]);
                     const double f = special::eval<5>(x, ix, tab, mask);
@@ -714,59 +853,112 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
         }
         __syncwarp();
     }
+    if (stage_f) stage_L<1, 3, NJ, SLOTS>(W, T, af, jac, gend, gw, nje, Lf, lane);
+    if (stage_r) stage_L<1, 3, NJ, SLOTS>(W, T, ar, jac, gend, gw, nje, Lr, lane);
+}
+
+// delta = 0 sums of the dual pair (L0 / Lc of both staged rows)
+template <int NJ>
+__device__ __forceinline__ void dual_specials_reduce(double (&s0f)[3], double (&scf)[3], double (&s0r)[3],
+                                                     double (&scr)[3], double jac, double *Lf, double *Lr, int lane)
+{
+    constexpr int SLOTS = LsLayout<3, NJ>::SLOTS;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
+    for (int o = 16; o >= 1; o >>= 1)
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            if (DF) af[j][i] += __shfl_xor_sync(kFull, af[j][i], 16);
-            if (DR) ar[j][i] += __shfl_xor_sync(kFull, ar[j][i], 16);
+            s0f[i] += __shfl_xor_sync(kFull, s0f[i], o);
+            scf[i] += __shfl_xor_sync(kFull, scf[i], o);
+            s0r[i] += __shfl_xor_sync(kFull, s0r[i], o);
+            scr[i] += __shfl_xor_sync(kFull, scr[i], o);
         }
-    if (A.need_special) {
+    if (lane == 0) {
 #pragma unroll
-        for (int o = 16; o >= 1; o >>= 1)
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                if (DF) {
-                    s0f[i] += __shfl_xor_sync(kFull, s0f[i], o);
-                    scf[i] += __shfl_xor_sync(kFull, scf[i], o);
-                }
-                if (DR) {
-                    s0r[i] += __shfl_xor_sync(kFull, s0r[i], o);
-                    scr[i] += __shfl_xor_sync(kFull, scr[i], o);
-                }
-            }
+        for (int i = 0; i < 3; ++i) {
+            Lf[3 * SLOTS + i] = jac * s0f[i];
+            Lf[3 * SLOTS + 3 + i] = jac * scf[i];
+            Lr[3 * SLOTS + i] = jac * s0r[i];
+            Lr[3 * SLOTS + 3 + i] = jac * scr[i];
+        }
     }
-    const int nslots = A.it_hi - A.it_lo + 1;
+}
+
+// blocks [d0, dend) of the dual pair from per-point L, window by window
+template <int NJ>
+__device__ __forceinline__ void dual_point_blocks(const PairArgs &A, const RegularGeom &g, int nq, const double nb[3],
+                                                  const double na[3], double jac, int istar, int dend, int64_t slot_f,
+                                                  int64_t slot_r, double *geo, double *Ls, int lane, const double *tab)
+{
+    constexpr int SLOTS = LsLayout<3, NJ>::SLOTS, LSZ = LsLayout<3, NJ>::SIZE;
     double *Lf = Ls, *Lr = Ls + LSZ;
-    if (s == 0) {
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const int sl = t + 16 * j;
-            if (sl < nslots) {
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    if (DF) Lf[i * SLOTS + sl] = jac * (af[j][i] * T.sc[j]);
-                    if (DR) Lr[i * SLOTS + sl] = jac * (ar[j][i] * T.sc[j]);
-                }
-            }
-        }
+    const int gend = istar + 2;
+    const int gw = pair_gw(istar);
+    int w0 = A.d0;
+    while (w0 < dend) {
+        Win W;
+        W.w0 = w0;
+        W.w1 = min(dend, w0 <= 1 ? 32 : w0 + 30);
+        W.it_lo = max(1, w0 - 1);
+        W.it_hi = W.w1;
+        const int npp = min(W.it_hi, istar + 1) - W.it_lo + 1;
+        if (npp > 0)
+            dual_points<NJ>(A, W, g, nq, nb, na, jac, gend, gw, (gw == 16 && npp > 16) ? NJ : 1, slot_f >= 0,
+                            slot_r >= 0, geo, Lf, Lr, lane, tab);
+        __syncwarp();
+        if (slot_f >= 0) combine_window<3, SLOTS>(A, W, Lf, slot_f, lane);
+        if (slot_r >= 0) combine_window<3, SLOTS>(A, W, Lr, slot_r, lane);
+        __syncwarp();
+        w0 = W.w1;
     }
-    if (lane == 0 && A.need_special) {
+}
+
+// One dual pair, warp per pair (near pairs): phase 1 (rmax, delta = 0 sums,
+// moments rows 0..2 forward, 3..5 reverse), per-point blocks below dmom,
+// moment blocks from dmom.  Both orientations are always evaluated (each
+// output's arithmetic is the same whichever rows the launch holds); only the
+// outputs with a slot (>= 0) are stored.
+template <int NJ>
+__device__ __noinline__ void eval_pair_dual(const PairArgs &A, const RegularGeom &g, int nq, const double nb[3],
+                                            const double na[3], double jac, double rt2_lo, int64_t slot_f,
+                                            int64_t slot_r, double *geo, double *Ls, double *Pw, int lane,
+                                            const double *tab)
+{
+    constexpr int PAY = kDualPay, LSZ = LsLayout<3, NJ>::SIZE;
+    double *p_lane = geo + lane * PAY;
+    double *Lf = Ls, *Lr = Ls + LSZ;
+    const bool try_mom = A.moments && A.d1 - 1 >= max(2, moment_istar(rt2_lo) + 1);
+    double rmax = 0.0;
+    {
+        double mom[2][6], s0f[3], scf[3], s0r[3], scr[3];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            if (DF) {
-                Lf[3 * SLOTS + i] = jac * s0f[i];
-                Lf[3 * SLOTS + 3 + i] = jac * scf[i];
-            }
-            if (DR) {
-                Lr[3 * SLOTS + i] = jac * s0r[i];
-                Lr[3 * SLOTS + 3 + i] = jac * scr[i];
-            }
+        for (int i = 0; i < 3; ++i) s0f[i] = scf[i] = s0r[i] = scr[i] = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) mom[0][i] = mom[1][i] = 0.0;
+        for (int base = 0; base < nq; base += 32) {
+            double rt2;
+            int small, nzw;
+            dual_payload(A, g, base + lane, nq, nb, na, A.need_special, p_lane, rt2, small, nzw, s0f, scf, s0r, scr);
+            rmax = fmax(rmax, rt2);
+            const bool skip = !__any_sync(kFull, nzw);
+            __syncwarp();
+            if (try_mom && !skip) chunk_moments<PAY, 2, 6>(geo, Pw, rt2, min(32, nq - base), mom, lane);
+            __syncwarp();
         }
+        if (A.need_special) dual_specials_reduce<NJ>(s0f, scf, s0r, scr, jac, Lf, Lr, lane);
+        if (try_mom) store_moments<6>(mom, Pw, lane);
     }
-    __syncwarp();
-    if (DF && slot_f >= 0) combine_store<3, NJ>(A, Lf, slot_f, lane);
-    if (DR && slot_r >= 0) combine_store<3, NJ>(A, Lr, slot_r, lane);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(kFull, rmax, o));
+    // without the moment form every gap is evaluated point by point
+    const int istar = A.moments ? moment_istar(rmax) : (1 << 29);
+    const int dmom = max(2, istar + 1);
+    const bool use_mom = try_mom && A.d1 > dmom;
+    dual_point_blocks<NJ>(A, g, nq, nb, na, jac, istar, use_mom ? min(A.d1, dmom) : A.d1, slot_f, slot_r, geo, Ls,
+                          lane, tab);
+    if (use_mom) {
+        if (slot_f >= 0) combine_moments<3>(A, slot_f, lane, Pw, jac, dmom, rmax);
+        if (slot_r >= 0) combine_moments<3>(A, slot_r, lane, Pw + 3 * kNK, jac, dmom, rmax);
+    }
     __syncwarp();
 }
 
@@ -819,6 +1011,26 @@ __device__ __forceinline__ bool near_test(const hb_mesh_desc &M, const double ce
     return dist < 2.0 * fmax(de, __ldg(M.diameters_dev + f));
 }
 
+// lower bound of a separated pair's largest rho~^2: the symmetric triangle
+// rules have the centroid as weighted mean, so by convexity the largest point
+// distance is at least the centroid distance (1 - 1e-12 covers rounding)
+__device__ __forceinline__ double rt2_lower(const PairArgs &A, int64_t e, int64_t f)
+{
+    double q = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double d = __ldg(A.m.centroids_dev + 3 * e + c) - __ldg(A.m.centroids_dev + 3 * f + c);
+        q = fma(d, d, q);
+    }
+    return q * A.inv_u2 * (1.0 - 1e-12);
+}
+
+// per-warp shared-memory areas of the pair kernels
+struct WarpMem {
+    double *geo, *Ls, *Pw;
+    const double *rw, *rh;   // regular rule weights / hats (CTA copy, far batches)
+};
+
 // class codes: 0 far, 1 near, 2 identical, 3 common edge, 4 common vertex
 __global__ void k_pair_classes(const hb_mesh_desc M, int64_t e0, int64_t e1, int8_t *out)
 {
@@ -837,12 +1049,462 @@ __global__ void k_pair_classes(const hb_mesh_desc M, int64_t e0, int64_t e1, int
 }
 
 // ---------------------------------------------------------------------------
-// K1 body: separated pairs of one (test row e, 32-column segment) work item.
+// Far-pair batches (separated pairs on the regular product rule).  The
+// moments of a batch are computed lane-parallel with FMA-dense register loops
+// -- lane (pair ps, k-group g) runs over the pair's point pairs and owns the
+// moments k in [KPL g, KPL g + KPL) -- instead of the warp-per-pair transposes
+// through shared memory, and the moment blocks of the whole batch come from
+// ONE small GEMM on the FP64 tensor cores,
+//   B[d][n] = sum_k Tm[k][d] M[k][n],   n = output i * PB + pair ps,
+// with mma.sync m8n8k4 f64 (8 k-steps of the 32 terms per 8 x 8 tile).  The
+// blocks below a pair's dmom keep the warp-per-pair per-point path.  The
+// moments of a far pair are always formed this way, so a block entry still
+// depends on the pair only.
+//   V (NW 1): KPL 16, PB 16      K dual (NW 6): KPL 4, PB 4
+//   p1 x p1 (NW 9, separable hat weights): KPL 4, PB 4
 // ---------------------------------------------------------------------------
-template <int OP, bool TP1, bool SP1, int NJ, bool SYM>
-__device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64_t seg, const Slots<OP, NJ> &T,
-                                             double *geo, double *Ls, int lane, const double *tab)
+template <int NW>
+struct FarCfg;
+template <>
+struct FarCfg<1> {
+    static constexpr int KPL = 16, PB = 16;
+};
+template <>
+struct FarCfg<6> {
+    static constexpr int KPL = 4, PB = 4;
+};
+template <>
+struct FarCfg<9> {
+    static constexpr int KPL = 4, PB = 4;
+};
+template <int NW>
+__host__ __device__ constexpr int far_ntile() { return (NW * FarCfg<NW>::PB + 7) / 8; }
+// row stride of Ms[k][n]: 8 ntile + 4 (= 4 or 12 mod 16: conflict-free B fragments)
+template <int NW>
+__host__ __device__ constexpr int far_nstr() { return 8 * far_ntile<NW>() + 4; }
+template <int NW>
+__host__ __device__ constexpr int far_smem_doubles() { return kNK * far_nstr<NW>() + 5 * FarCfg<NW>::PB; }
+
+// per-pair data of a batch (shared memory, after Ms)
+template <int NW>
+struct FarPairs {
+    double *jac, *rmax;
+    int64_t *slot_f, *slot_r;
+    int *dmom, *lane;   // first moment block; lane (segment position) of the pair
+    __device__ FarPairs(double *base)
+        : jac(base + kNK * far_nstr<NW>()), rmax(jac + FarCfg<NW>::PB),
+          slot_f(reinterpret_cast<int64_t *>(rmax + FarCfg<NW>::PB)), slot_r(slot_f + FarCfg<NW>::PB),
+          dmom(reinterpret_cast<int *>(slot_r + FarCfg<NW>::PB)), lane(dmom + FarCfg<NW>::PB) {}
+};
+
+// a far pair's points staged in shared memory (x: test element a, y: trial
+// element b, 3 coordinates each) and the regular rule's weights and hats
+// (CTA copy): plain shared-memory loads in the lane loops
+struct FarGeom {
+    const double *xp, *yp, *w, *hats;
+    int nq1;
+};
+constexpr int kFarMaxRule = 7;    // far batches when the regular rule has <= 7 points
+constexpr int kRuleDoubles = 4 * 16;
+
+// copy the batch's point coordinates: lane (ps, g) copies entries g, g + LPP, ...
+// of its pair into Xs[ps][0..6 nq1) (stride 6 nq1 + 1)
+template <int LPP>
+__device__ __forceinline__ void stage_far_points(const hb_mesh_desc &M, int64_t a, int64_t b, double *Xs, int g)
 {
+    const int n3 = 3 * (int)M.n_reg;
+    const double *pa = M.reg_pts_dev + a * n3, *pb = M.reg_pts_dev + b * n3;
+    for (int c = g; c < 2 * n3; c += LPP) Xs[c] = c < n3 ? __ldg(pa + c) : __ldg(pb + c - n3);
+}
+
+// t^(KPL g): the first power of the lane's k-group (KPL a power of two)
+template <int KPL>
+__device__ __forceinline__ double group_start_pow(double t, int g)
+{
+    double s = t;
+#pragma unroll
+    for (int q = 1; q < KPL; q <<= 1) s = __dmul_rn(s, s);   // t^KPL
+    double p = 1.0;
+#pragma unroll
+    for (int b = 1; b < 32 / KPL; b <<= 1) {
+        if (g & b) p = __dmul_rn(p, s);
+        s = __dmul_rn(s, s);
+    }
+    return p;
+}
+
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// DMMA combine of a batch: blocks d in [dlo, d1) of all its pairs; entries
+// below a pair's dmom are left to the per-point path
+template <int NW, int NIJ>
+__device__ __forceinline__ void far_combine(const PairArgs &A, const double *Ms, const FarPairs<NW> &P, int npairs,
+                                            int dlo, int lane)
+{
+    constexpr int PB = FarCfg<NW>::PB, NT = far_ntile<NW>(), NSTR = far_nstr<NW>();
+    const int gq = lane >> 2, tq = lane & 3;
+    // per output column (2 per lane per tile): pair, output, dmom
+    for (int dt = dlo; dt < A.d1; dt += 8) {
+        const int d = dt + gq;
+        double acc[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+        const bool drow = d < A.d1;
+#pragma unroll
+        for (int ks = 0; ks < kNK / 4; ++ks) {
+            const double a = drow ? __ldg(A.Tm + (4 * ks + tq) * A.nd + (d - A.d0)) : 0.0;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt][0], acc[nt][1], a, Ms[(4 * ks + tq) * NSTR + 8 * nt + gq]);
+        }
+        if (!drow) continue;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int n = 8 * nt + 2 * tq + h;
+                const int i = n / PB, ps = n - i * PB;
+                if (i >= NW || ps >= npairs) continue;
+                if (d < P.dmom[ps]) continue;
+                int64_t slot;
+                int io;
+                if (NW == 6) {   // K dual: outputs 0..2 forward (slot_f), 3..5 reverse (slot_r)
+                    slot = i < 3 ? P.slot_f[ps] : P.slot_r[ps];
+                    io = i < 3 ? i : i - 3;
+                } else {
+                    slot = P.slot_f[ps];
+                    io = i;
+                }
+                if (slot < 0) continue;
+                A.Q[slot * (int64_t)(NIJ * A.nd) + io * A.nd + (d - A.d0)] = P.jac[ps] * acc[nt][h];
+            }
+    }
+}
+
+// moments of a V pair (p0 x p0) on the regular rule: lane (ps, g) = (lane >> 1, lane & 1)
+__device__ __forceinline__ void far_moments_v(const PairArgs &A, const FarGeom &G, double (&mom)[16], double &rmax,
+                                              int g)
+{
+    const double *xp = G.xp, *yp = G.yp, *w = G.w;
+    const int nq1 = G.nq1;
+    rmax = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) mom[k] = 0.0;
+    for (int p = 0; p < nq1; ++p) {
+        const double x0 = (xp + 3 * p)[0], x1 = (xp + 3 * p + 1)[0], x2 = (xp + 3 * p + 2)[0];
+        const double wp = (w + p)[0];
+#pragma unroll 2
+        for (int r = 0; r < nq1; ++r) {
+            const double rx = x0 - (yp + 3 * r)[0], ry = x1 - (yp + 3 * r + 1)[0], rz = x2 - (yp + 3 * r + 2)[0];
+            const double t = (rx * rx + ry * ry + rz * rz) * A.inv_u2;
+            rmax = fmax(rmax, t);
+            const double W = wp * (w + r)[0];
+            double pw = group_start_pow<16>(t, g);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                mom[k] = fma(W, pw, mom[k]);
+                pw = __dmul_rn(pw, t);
+            }
+        }
+    }
+}
+
+// moments of a K pair, both orientations (canonical a < b): lane (ps, g) = (lane >> 2, lane & 3)
+__device__ __forceinline__ void far_moments_k(const PairArgs &A, const FarGeom &G, const double nb[3],
+                                              const double na[3], double (&mom)[6][FarCfg<6>::KPL], int g)
+{
+    constexpr int KPL = FarCfg<6>::KPL;
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) mom[i][k] = 0.0;
+    const int nq1 = G.nq1;
+    for (int p = 0; p < nq1; ++p) {
+        const double x0 = G.xp[3 * p], x1 = G.xp[3 * p + 1], x2 = G.xp[3 * p + 2];
+        const double wp = G.w[p];
+        double ht[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ht[c] = G.hats[3 * p + c];
+        for (int r = 0; r < nq1; ++r) {
+            const double rx = x0 - G.yp[3 * r], ry = x1 - G.yp[3 * r + 1], rz = x2 - G.yp[3 * r + 2];
+            const double t = (rx * rx + ry * ry + rz * rz) * A.inv_u2;
+            const double rnb = rx * nb[0] + ry * nb[1] + rz * nb[2];
+            const double rna = (-rx) * na[0] + (-ry) * na[1] + (-rz) * na[2];
+            const double wq = wp * G.w[r];
+            double Wt[6];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                Wt[i] = ((wq * (1.0 * G.hats[3 * r + i])) * (-rnb)) * A.inv2a;
+                Wt[3 + i] = ((wq * (1.0 * ht[i])) * (-rna)) * A.inv2a;
+            }
+            double pw = group_start_pow<KPL>(t, g);
+#pragma unroll
+            for (int k = 0; k < KPL; ++k) {
+#pragma unroll
+                for (int i = 0; i < 6; ++i) mom[i][k] = fma(Wt[i], pw, mom[i][k]);
+                pw = __dmul_rn(pw, t);
+            }
+        }
+    }
+}
+
+// moments of a p1 x p1 pair (separable hat weights (w_p ht_i(p)) (w_r hs_j(r))):
+// lane (ps, g) = (lane >> 3, lane & 7)
+__device__ __forceinline__ void far_moments_p1p1(const PairArgs &A, const FarGeom &G, double (&mom)[9][4],
+                                                 double &rmax, int g)
+{
+    rmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mom[i][k] = 0.0;
+    const int nq1 = G.nq1;
+    for (int p = 0; p < nq1; ++p) {
+        const double x0 = (G.xp + 3 * p)[0], x1 = (G.xp + 3 * p + 1)[0], x2 = (G.xp + 3 * p + 2)[0];
+        const double wp = (G.w + p)[0];
+        double N[3][4];
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) N[j][k] = 0.0;
+        for (int r = 0; r < nq1; ++r) {
+            const double rx = x0 - (G.yp + 3 * r)[0], ry = x1 - (G.yp + 3 * r + 1)[0],
+                         rz = x2 - (G.yp + 3 * r + 2)[0];
+            const double t = (rx * rx + ry * ry + rz * rz) * A.inv_u2;
+            rmax = fmax(rmax, t);
+            const double wr = (G.w + r)[0];
+            double b[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) b[j] = wr * (G.hats + 3 * r + j)[0];
+            double pw = group_start_pow<4>(t, g);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) N[j][k] = fma(b[j], pw, N[j][k]);
+                pw = __dmul_rn(pw, t);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double a = wp * (G.hats + 3 * p + i)[0];
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) mom[3 * i + j][k] = fma(a, N[j][k], mom[3 * i + j][k]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused lane-level K far path.  For far pairs whose per-point gaps
+// 1..istar+1 number at most 8 (the common case at moderate E_t), lane
+// (ps, g) of the batch forms from the pair's point pairs the moments k in
+// [4g, 4g + 4) of both orientations and the kernel value F/x at its gap
+// g + 1 -- no per-pair warp-serial phase.  The blocks d < dmom follow from the 3-term combination of those L
+// values, the blocks d >= dmom from the moments (DMMA combine).
+// ---------------------------------------------------------------------------
+constexpr int kFusedMaxGap = 8;   // per-point gaps 1..8: one per lane of a pair
+
+// largest rho~^2 of a far pair: lane g of the pair takes the point pairs q = g mod LPP
+template <int LPP>
+__device__ __forceinline__ double far_rmax(const PairArgs &A, const FarGeom &G, int g)
+{
+    const int nq1 = G.nq1, nq = nq1 * nq1;
+    double rmax = 0.0;
+    for (int q = g; q < nq; q += LPP) {
+        const int p = q / nq1, r = q - p * nq1;
+        const double rx = G.xp[3 * p] - G.yp[3 * r], ry = G.xp[3 * p + 1] - G.yp[3 * r + 1],
+                     rz = G.xp[3 * p + 2] - G.yp[3 * r + 2];
+        rmax = fmax(rmax, (rx * rx + ry * ry + rz * rz) * A.inv_u2);
+    }
+#pragma unroll
+    for (int o = 1; o < LPP; o <<= 1) rmax = fmax(rmax, __shfl_xor_sync(kFull, rmax, o));
+    return rmax;
+}
+
+// gap constants of gap i (as Slots::init): cx = 1/(2 sqrt(a delta)), ic = 1/cx, sc = cx (K)
+__device__ __forceinline__ void gap_consts(const PairArgs &A, int i, double &cx, double &ic)
+{
+    const double delta = (double)max(i, 1) * A.step;
+    ic = 2.0 * sqrt(A.alpha * delta);
+    cx = 1.0 / ic;
+}
+
+// lane (ps, g) of a K dual batch (4 pairs x 8 lanes), second walk over the
+// pair's point pairs (the moments are formed by far_moments_k first): when
+// `pp`, the per-point sum of gap g + 1 (acc[o], o: 3 forward, 3 reverse
+// outputs); `spec`: the delta = 0 sums of the point pairs q = g mod 8.  Called
+// warp-uniformly (every lane takes part in the region votes).
+__device__ __forceinline__ void far_pp_k(const PairArgs &A, const FarGeom &G, const double nb[3], const double na[3],
+                                         int g, bool pp, bool spec, double (&acc)[6], double (&s0f)[3],
+                                         double (&scf)[3], double (&s0r)[3], double (&scr)[3], const double *tab)
+{
+    constexpr int LPP = 32 / FarCfg<6>::PB;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s0f[i] = scf[i] = s0r[i] = scr[i] = 0.0;
+    double cx, ic;
+    gap_consts(A, g + 1, cx, ic);
+    const int nq1 = G.nq1;
+    int q = 0;
+    for (int p = 0; p < nq1; ++p) {
+        const double x0 = G.xp[3 * p], x1 = G.xp[3 * p + 1], x2 = G.xp[3 * p + 2];
+        const double wp = G.w[p];
+        for (int r = 0; r < nq1; ++r, ++q) {
+            const double rx = x0 - G.yp[3 * r], ry = x1 - G.yp[3 * r + 1], rz = x2 - G.yp[3 * r + 2];
+            const double r2 = rx * rx + ry * ry + rz * rz;
+            const double rnb = rx * nb[0] + ry * nb[1] + rz * nb[2];
+            const double rna = (-rx) * na[0] + (-ry) * na[1] + (-rz) * na[2];
+            const double wq = wp * G.w[r];
+            const double rho = sqrt(r2);
+            const double iq = 1.0 / rho;
+            double xs[1] = {__dmul_rn(rho, cx)}, fs[1];
+            special::eval_nf<5, 1>(xs, [&](int) { return __dmul_rn(iq, ic); }, fs, tab, kFull);
+            if (pp) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const double wf = ((wq * (1.0 * G.hats[3 * r + i])) * (-rnb)) * A.inv2a;
+                    const double wr = ((wq * (1.0 * G.hats[3 * p + i])) * (-rna)) * A.inv2a;
+                    acc[i] = fma(fs[0], wf, acc[i]);
+                    acc[3 + i] = fma(fs[0], wr, acc[3 + i]);
+                }
+            }
+            if (spec && (q % LPP) == g) {
+                const double Uf = -rnb * iq, Ur = -rna * iq;
+                const double P = 1.0 / __dmul_rn(rho, rho);
+                const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const double hf = wq * (1.0 * G.hats[3 * r + i]), hr = wq * (1.0 * G.hats[3 * p + i]);
+                    s0f[i] = fma(hf * Uf, c0, s0f[i]);
+                    scf[i] = fma(hf * Uf, cc, scf[i]);
+                    s0r[i] = fma(hr * Ur, c0, s0r[i]);
+                    scr[i] = fma(hr * Ur, cc, scr[i]);
+                }
+            }
+        }
+    }
+}
+
+// blocks d in [d0, min(d1, dmom)) of a fused K pair from its staged L row
+// Lrow[o][0..9] (o: 6 outputs; index 0 = L0, 1..8 = gaps, 9 = Lcomb0),
+// lane (ps, g): block g
+__device__ __forceinline__ void fused_blocks_k(const PairArgs &A, const double *Lrow, int dmom, int64_t slot_f,
+                                               int64_t slot_r, int g)
+{
+    {
+        const int d = g;
+        if (d < A.d0 || d >= A.d1 || d >= dmom) return;
+#pragma unroll
+        for (int o = 0; o < 6; ++o) {
+            const int64_t slot = o < 3 ? slot_f : slot_r;
+            if (slot < 0) continue;
+            const double *Li = Lrow + o * 10;
+            double b;
+            if (d == 0) {
+                b = Li[9] + (-Li[1]);
+            } else {
+                b = -Li[d - 1] + 2.0 * Li[d];
+                b = b + (-Li[d + 1]);
+            }
+            A.Q[slot * (int64_t)(3 * A.nd) + (o % 3) * A.nd + (d - A.d0)] = b;
+        }
+    }
+}
+
+// delta = 0 sums of a pair without moments (far-batch pairs): L0 / Lc of the staged row
+template <int OP, bool TP1, bool SP1, int NJ, class Geom>
+__device__ __forceinline__ void pair_specials(const PairArgs &A, const Geom &g, int nq, const double ny[3],
+                                              double jac, double *geo, double *Ls, int lane)
+{
+    constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
+    constexpr int PAY = Layout<OP, NIJ>::PAY, SLOTS = LsLayout<NIJ, NJ>::SLOTS;
+    double s0[NIJ], sc[NIJ];
+#pragma unroll
+    for (int i = 0; i < NIJ; ++i) s0[i] = sc[i] = 0.0;
+    for (int base = 0; base < nq; base += 32) {
+        double rt2;
+        int small, nzw;
+        point_payload<OP, TP1, SP1>(A, g, base + lane, nq, ny, true, geo + lane * PAY, rt2, small, nzw, s0, sc);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) {
+            s0[i] += __shfl_xor_sync(kFull, s0[i], o);
+            if (OP != 2) sc[i] += __shfl_xor_sync(kFull, sc[i], o);
+        }
+    if (lane == 0) {
+        double *L0 = Ls + NIJ * SLOTS, *Lc = L0 + NIJ;
+#pragma unroll
+        for (int i = 0; i < NIJ; ++i) {
+            L0[i] = jac * s0[i];
+            Lc[i] = jac * (OP == 2 ? s0[i] : sc[i]);
+        }
+    }
+    __syncwarp();
+}
+
+
+// blocks [d0, dend) of a pair from per-point L (windows), given its istar
+template <int OP, bool TP1, bool SP1, int NJ, class Geom>
+__device__ __forceinline__ void pair_point_blocks(const PairArgs &A, const Geom &g, int nq, const double ny[3],
+                                                  double jac, int istar, int dend, int64_t slot, double *geo,
+                                                  double *Ls, int lane, const double *tab)
+{
+    constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
+    constexpr int SLOTS = LsLayout<NIJ, NJ>::SLOTS;
+    const int gend = istar + 2;
+    const int gw = pair_gw(istar);
+    per_point_windows<NIJ, SLOTS>(A, dend, istar, Ls, slot, lane, [&](const Win &W, int npp) {
+        pair_points<OP, TP1, SP1, NJ>(A, W, g, nq, ny, jac, gend, gw, (gw == 16 && npp > 16) ? NJ : 1, geo, Ls, lane,
+                                      tab);
+    });
+}
+
+
+__device__ __forceinline__ RegularGeom regular_geom(const hb_mesh_desc &M, int64_t a, int64_t b, bool near)
+{
+    RegularGeom g;
+    const int nq1 = near ? (int)M.n_near : (int)M.n_reg;
+    const double *pts = near ? M.near_pts_dev : M.reg_pts_dev;
+    g.xp = pts + 3 * a * nq1;
+    g.yp = pts + 3 * b * nq1;
+    g.w = near ? M.near_w_dev : M.reg_w_dev;
+    g.hats = near ? M.near_hats_dev : M.reg_hats_dev;
+    g.nq1 = nq1;
+    return g;
+}
+
+// lane of the n-th set bit of m (n < popc(m)), warp-uniform inputs
+__device__ __forceinline__ int nth_bit(unsigned m, int n)
+{
+    for (int k = 0; k < n; ++k) m &= m - 1;
+    return __ffs(m) - 1;
+}
+
+// smallest first moment block over the batch's pairs (lanes of pair ps: ps < npairs)
+__device__ __forceinline__ int batch_dlo(const PairArgs &A, double rmax, bool valid)
+{
+    const int dm = valid ? max(2, moment_istar(rmax) + 1) : 0x7fffffff;
+    return max(A.d0, __reduce_min_sync(kFull, dm));
+}
+
+// ---------------------------------------------------------------------------
+// K1 body: separated pairs of one (test row e, 32-column segment) work item.
+// The segment is classified lane-parallel; near pairs run warp per pair,
+// far pairs in batches (V, V11, D2: moments in registers, DMMA combine).
+// ---------------------------------------------------------------------------
+template <int OP, bool TP1, bool SP1, int NJ, bool SYM, int CLS>
+__device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64_t seg, const WarpMem &W, int lane,
+                                             const double *tab)
+{
+    constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     const hb_mesh_desc &M = A.m;
     int64_t fb = seg * A.seg_len;
     const int64_t fe = min(fb + A.seg_len, M.E_x);
@@ -853,24 +1515,98 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
     for (int c = 0; c < 3; ++c) ce[c] = __ldg(M.centroids_dev + 3 * e + c);
     const double de = __ldg(M.diameters_dev + e);
 
-    for (int64_t f = fb; f < fe; ++f) {
-        // touching pairs belong to the singular path
-        if (touching_pos(M, t_lo, t_hi, f) >= 0) continue;
-        const int64_t slot = (e - A.e0) * M.E_x + f;
-        const double jac = pair_jac<OP>(A, e, f);
-        if (OP == 2 && jac == 0.0) continue;   // n_x.n_y == 0: no contribution (finalize skips it)
-        const bool near = near_test(M, ce, de, f);
-        RegularGeom g;
-        const int nq1 = near ? (int)M.n_near : (int)M.n_reg;
-        const double *pts = near ? M.near_pts_dev : M.reg_pts_dev;
-        g.xp = pts + 3 * e * nq1;
-        g.yp = pts + 3 * f * nq1;
-        g.w = near ? M.near_w_dev : M.reg_w_dev;
-        g.hats = near ? M.near_hats_dev : M.reg_hats_dev;
-        g.nq1 = nq1;
+    // lane l classifies f = fb + l (touching pairs belong to the singular path;
+    // D2 pairs with n_x.n_y == 0 contribute nothing and are not staged)
+    const int64_t f = fb + lane;
+    bool ok = f < fe && touching_pos(M, t_lo, t_hi, f) < 0;
+    double jac = 0.0;
+    if (ok) {
+        jac = pair_jac<OP>(A, e, f);
+        if (OP == 2 && jac == 0.0) ok = false;
+    }
+    const bool near = ok && near_test(M, ce, de, f);
+    constexpr bool FARC = NIJ == 1 || NIJ == 9;
+    const bool FAR = FARC && A.moments && M.n_reg <= kFarMaxRule;
+    // CLS 2: far pairs only (batches), 3: the rest (near pairs, warp per pair)
+    const unsigned nearm = CLS == 2 ? 0u : __ballot_sync(kFull, ok && (near || !FAR));
+    const unsigned farm = CLS == 3 ? 0u : __ballot_sync(kFull, ok && !near && FAR);
+
+    for (unsigned m = nearm; m; m &= m - 1) {
+        const int l = __ffs(m) - 1;
+        const int64_t ff = fb + l;
+        const double jf = __shfl_sync(kFull, jac, l);
+        const bool nf = (__shfl_sync(kFull, (int)near, l)) != 0;
+        const RegularGeom g = regular_geom(M, e, ff, nf);
         double ny[3];
-        for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * f + c);
-        eval_pair<OP, TP1, SP1, NJ>(A, g, nq1 * nq1, ny, jac, slot, T, geo, Ls, lane, tab);
+        for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * ff + c);
+        eval_pair<OP, TP1, SP1, NJ>(A, g, g.nq1 * g.nq1, ny, jf, rt2_lower(A, e, ff), (e - A.e0) * M.E_x + ff, W.geo,
+                                    W.Ls, W.Pw, lane, tab);
+    }
+    if constexpr (FARC) {
+        constexpr int PB = FarCfg<NIJ>::PB, KPL = FarCfg<NIJ>::KPL, LPP = 32 / PB, NSTR = far_nstr<NIJ>();
+        double *Ms = W.geo;
+        FarPairs<NIJ> P(W.geo);
+        unsigned m = farm;
+        while (m) {
+            const int npairs = min(PB, __popc(m));
+            const int ps = lane / LPP, gk = lane % LPP;
+            const bool pv = ps < npairs;
+            const int l = pv ? nth_bit(m, ps) : 0;
+            const int64_t ff = fb + l;
+            double rmax;
+            __syncwarp();
+            const int n3 = 3 * (int)M.n_reg;
+            double *Xs = W.geo + ps * (2 * n3 + 1);
+            stage_far_points<LPP>(M, e, ff, Xs, gk);
+            __syncwarp();
+            const FarGeom fg{Xs, Xs + n3, W.rw, W.rh, (int)M.n_reg};
+            if constexpr (NIJ == 1) {
+                double mom[16];
+                far_moments_v(A, fg, mom, rmax, gk);
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < KPL; ++k) Ms[(KPL * gk + k) * NSTR + ps] = pv ? mom[k] : 0.0;
+            } else {
+                double mom[9][4];
+                far_moments_p1p1(A, fg, mom, rmax, gk);
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < KPL; ++k)
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) Ms[(KPL * gk + k) * NSTR + i * PB + ps] = pv ? mom[i][k] : 0.0;
+            }
+            const double jf = __shfl_sync(kFull, jac, l);
+            if (gk == 0 && pv) {
+                P.jac[ps] = jf;
+                P.rmax[ps] = rmax;
+                P.dmom[ps] = max(2, moment_istar(rmax) + 1);
+                P.lane[ps] = l;
+                P.slot_f[ps] = (e - A.e0) * M.E_x + ff;
+                P.slot_r[ps] = -1;
+            }
+            const int dlo = batch_dlo(A, rmax, pv);
+            __syncwarp();
+            far_combine<NIJ, NIJ>(A, Ms, P, npairs, dlo, lane);
+            __syncwarp();
+            // blocks below each pair's dmom: per-point L, warp per pair
+            for (int q = 0; q < npairs; ++q) {
+                const int dmom = P.dmom[q];
+                if (A.d0 >= dmom) continue;
+                const int istar = moment_istar(P.rmax[q]);
+                const int lq = P.lane[q];
+                const int64_t fq = fb + lq;
+                const double jq = P.jac[q];
+                const RegularGeom gq = regular_geom(M, e, fq, false);
+                double ny[3];
+                for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * fq + c);
+                const int64_t slot = (e - A.e0) * M.E_x + fq;
+                if (A.need_special) pair_specials<OP, TP1, SP1, NJ>(A, gq, gq.nq1 * gq.nq1, ny, jq, W.geo, W.Ls, lane);
+                pair_point_blocks<OP, TP1, SP1, NJ>(A, gq, gq.nq1 * gq.nq1, ny, jq, istar, min(A.d1, dmom), slot, W.geo,
+                                                    W.Ls, lane, tab);
+                __syncwarp();
+            }
+            for (int q = 0; q < npairs; ++q) m &= m - 1;
+        }
     }
 }
 
@@ -878,47 +1614,193 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
 // (test row e, segment) item, evaluated as the canonical pair (min, max).
 // Pairs with both rows in the chunk are produced once (by the smaller row);
 // a pair whose other row lies outside the chunk is still evaluated in its
-// canonical orientation and only this row's output is stored.
-template <int NJ>
-__device__ __forceinline__ void regular_item_dual(const PairArgs &A, int64_t e, int64_t seg, const Slots<1, NJ> &T,
-                                                  double *geo, double *Ls, int lane, const double *tab)
+// canonical orientation and only this row's output is stored.  Near pairs
+// run warp per pair, far pairs in batches (moments of both orientations in
+// registers, DMMA combine).
+template <int NJ, int CLS>
+__device__ __forceinline__ void regular_item_dual(const PairArgs &A, int64_t e, int64_t seg, const WarpMem &W,
+                                                  int lane, const double *tab)
 {
     const hb_mesh_desc &M = A.m;
     const int64_t fb = seg * A.seg_len;
     const int64_t fe = min(fb + A.seg_len, M.E_x);
     if (fb >= fe) return;
     const int64_t t_lo = __ldg(M.tn_indptr_dev + e), t_hi = __ldg(M.tn_indptr_dev + e + 1);
-    for (int64_t f = fb; f < fe; ++f) {
-        const bool f_in = f >= A.e0 && f < A.e1;
-        if (f < e && f_in) continue;                           // the canonical pair (f, e) belongs to row f
-        if (touching_pos(M, t_lo, t_hi, f) >= 0) continue;     // touching pairs: singular path (f == e too)
-        const int64_t a = f > e ? e : f, b = f > e ? f : e;
-        const int64_t slot_f = (a >= A.e0 && a < A.e1) ? (a - A.e0) * M.E_x + b : -1;   // test a, trial b
-        const int64_t slot_r = (b >= A.e0 && b < A.e1) ? (b - A.e0) * M.E_x + a : -1;   // test b, trial a
+    const int64_t f = fb + lane;
+    const bool f_in = f >= A.e0 && f < A.e1;
+    // the canonical pair (f, e) of f < e in the chunk belongs to row f; touching pairs (f == e
+    // too) belong to the singular path
+    const bool ok = f < fe && !(f < e && f_in) && touching_pos(M, t_lo, t_hi, f) < 0;
+    const int64_t a = f > e ? e : f, b = f > e ? f : e;
+    bool near = false;
+    if (ok) {
         double ca[3];
         for (int c = 0; c < 3; ++c) ca[c] = __ldg(M.centroids_dev + 3 * a + c);
-        const bool near = near_test(M, ca, __ldg(M.diameters_dev + a), b);
-        RegularGeom g;
-        const int nq1 = near ? (int)M.n_near : (int)M.n_reg;
-        const double *pts = near ? M.near_pts_dev : M.reg_pts_dev;
-        g.xp = pts + 3 * a * nq1;
-        g.yp = pts + 3 * b * nq1;
-        g.w = near ? M.near_w_dev : M.reg_w_dev;
-        g.hats = near ? M.near_hats_dev : M.reg_hats_dev;
-        g.nq1 = nq1;
+        near = near_test(M, ca, __ldg(M.diameters_dev + a), b);
+    }
+    // CLS 2: far pairs only (batches), 3: the rest (near pairs, warp per pair)
+    const bool FAR = A.moments && M.n_reg <= kFarMaxRule;
+    const unsigned nearm = CLS == 2 ? 0u : __ballot_sync(kFull, ok && (near || !FAR));
+    const unsigned farm = CLS == 3 ? 0u : __ballot_sync(kFull, ok && !near && FAR);
+    auto slots = [&](int64_t aa, int64_t bb, int64_t &sf, int64_t &sr) {
+        sf = (aa >= A.e0 && aa < A.e1) ? (aa - A.e0) * M.E_x + bb : -1;   // test a, trial b
+        sr = (bb >= A.e0 && bb < A.e1) ? (bb - A.e0) * M.E_x + aa : -1;   // test b, trial a
+    };
+    for (unsigned m = nearm; m; m &= m - 1) {
+        const int l = __ffs(m) - 1;
+        const int64_t ff = fb + l;
+        const int64_t aa = ff > e ? e : ff, bb = ff > e ? ff : e;
+        int64_t slot_f, slot_r;
+        slots(aa, bb, slot_f, slot_r);
+        const RegularGeom g = regular_geom(M, aa, bb, __shfl_sync(kFull, (int)near, l) != 0);
         double nb[3], na[3];
         for (int c = 0; c < 3; ++c) {
-            nb[c] = __ldg(M.normals_dev + 3 * b + c);
-            na[c] = __ldg(M.normals_dev + 3 * a + c);
+            nb[c] = __ldg(M.normals_dev + 3 * bb + c);
+            na[c] = __ldg(M.normals_dev + 3 * aa + c);
         }
-        const double jac = pair_jac<1>(A, a, b);
-        if (slot_f >= 0 && slot_r >= 0)
-            eval_pair_dual<NJ, 0>(A, g, nq1 * nq1, nb, na, jac, slot_f, slot_r, T, geo, Ls, lane, tab);
-        else if (slot_f >= 0)
-            eval_pair_dual<NJ, 1>(A, g, nq1 * nq1, nb, na, jac, slot_f, slot_r, T, geo, Ls, lane, tab);
-        else
-            eval_pair_dual<NJ, 2>(A, g, nq1 * nq1, nb, na, jac, slot_f, slot_r, T, geo, Ls, lane, tab);
+        const double jac = pair_jac<1>(A, aa, bb);
+        const double rlo = rt2_lower(A, aa, bb);
+        const int nq = g.nq1 * g.nq1;
+        eval_pair_dual<NJ>(A, g, nq, nb, na, jac, rlo, slot_f, slot_r, W.geo, W.Ls, W.Pw, lane, tab);
     }
+    constexpr int PB = FarCfg<6>::PB, KPL = FarCfg<6>::KPL, LPP = 32 / PB, NSTR = far_nstr<6>();
+    double *Ms = W.geo;
+    FarPairs<6> P(W.geo);
+    unsigned m = farm;
+    while (m) {
+        const int npairs = min(PB, __popc(m));
+        const int ps = lane / LPP, gk = lane % LPP;
+        const bool pv = ps < npairs;
+        const int l = pv ? nth_bit(m, ps) : 0;
+        const int64_t ff = fb + l;
+        const int64_t aa = ff > e ? e : ff, bb = ff > e ? ff : e;
+        double nb[3], na[3];
+        for (int c = 0; c < 3; ++c) {
+            nb[c] = __ldg(M.normals_dev + 3 * bb + c);
+            na[c] = __ldg(M.normals_dev + 3 * aa + c);
+        }
+        double mom[6][KPL], acc[6], s0f[3], scf[3], s0r[3], scr[3];
+        __syncwarp();
+        const int n3 = 3 * (int)M.n_reg;
+        double *Xs = W.geo + ps * (2 * n3 + 1);
+        stage_far_points<LPP>(M, aa, bb, Xs, gk);
+        __syncwarp();
+        const FarGeom g{Xs, Xs + n3, W.rw, W.rh, (int)M.n_reg};
+        // the pair's largest rho~^2 first: it decides istar, dmom and whether the
+        // per-point gaps fit the fused lane path
+        const double rmax = far_rmax<LPP>(A, g, gk);
+        const int istar = moment_istar(rmax), dmom = max(2, istar + 1);
+        const bool fused = pv && istar + 1 <= kFusedMaxGap;
+        const bool pp = fused && A.d0 < dmom;
+        const bool pp_any = __any_sync(kFull, pp);
+        int64_t sf = -1, sr = -1;
+        slots(aa, bb, sf, sr);
+        const double jac = pair_jac<1>(A, aa, bb);
+        far_moments_k(A, g, nb, na, mom, gk);
+        if (pp_any) far_pp_k(A, g, nb, na, gk, pp, pp && A.need_special, acc, s0f, scf, s0r, scr, tab);
+        __syncwarp();   // the staged points are overwritten from here on
+        if (pp_any) {
+            // staged L row per pair: [o][0] = L0, [o][1..8] = gaps, [o][9] = Lcomb0
+            double *Lrow = W.geo + ps * 60;
+            if (A.need_special) {
+#pragma unroll
+                for (int o = 1; o < LPP; o <<= 1)
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        s0f[i] += __shfl_xor_sync(kFull, s0f[i], o);
+                        scf[i] += __shfl_xor_sync(kFull, scf[i], o);
+                        s0r[i] += __shfl_xor_sync(kFull, s0r[i], o);
+                        scr[i] += __shfl_xor_sync(kFull, scr[i], o);
+                    }
+            }
+            if (pp) {
+                double cxh, ich;
+                gap_consts(A, gk + 1, cxh, ich);
+#pragma unroll
+                for (int o = 0; o < 6; ++o) Lrow[o * 10 + gk + 1] = jac * (acc[o] * cxh);
+                if (A.need_special && gk == 0) {
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        Lrow[i * 10] = jac * s0f[i];
+                        Lrow[i * 10 + 9] = jac * scf[i];
+                        Lrow[(3 + i) * 10] = jac * s0r[i];
+                        Lrow[(3 + i) * 10 + 9] = jac * scr[i];
+                    }
+                }
+            }
+            __syncwarp();
+            if (pp) fused_blocks_k(A, Lrow, dmom, sf, sr, gk);
+            __syncwarp();
+        }
+#pragma unroll
+        for (int k = 0; k < KPL; ++k)
+#pragma unroll
+            for (int i = 0; i < 6; ++i) Ms[(KPL * gk + k) * NSTR + i * PB + ps] = pv ? mom[i][k] : 0.0;
+        if (gk == 0 && pv) {
+            P.jac[ps] = jac;
+            P.rmax[ps] = fused ? -1.0 : rmax;   // < 0: no warp-path per-point work left
+            P.dmom[ps] = dmom;
+            P.lane[ps] = l;
+            P.slot_f[ps] = sf;
+            P.slot_r[ps] = sr;
+        }
+        const int dlo = max(A.d0, __reduce_min_sync(kFull, pv ? dmom : 0x7fffffff));
+        __syncwarp();
+        far_combine<6, 3>(A, Ms, P, npairs, dlo, lane);
+        __syncwarp();
+        // pairs outside the fused path: per-point blocks warp per pair
+        for (int q = 0; q < npairs; ++q) {
+            const int dmom = P.dmom[q];
+            if (A.d0 >= dmom || P.rmax[q] < 0.0) continue;
+            const int istar = moment_istar(P.rmax[q]);
+            const int lq = P.lane[q];
+            const int64_t fq = fb + lq;
+            const int64_t aq = fq > e ? e : fq, bq = fq > e ? fq : e;
+            const double jq = P.jac[q];
+            const int64_t sf = P.slot_f[q], sr = P.slot_r[q];
+            const RegularGeom gq = regular_geom(M, aq, bq, false);
+            double nbq[3], naq[3];
+            for (int c = 0; c < 3; ++c) {
+                nbq[c] = __ldg(M.normals_dev + 3 * bq + c);
+                naq[c] = __ldg(M.normals_dev + 3 * aq + c);
+            }
+            const int nq = gq.nq1 * gq.nq1, dend = min(A.d1, dmom);
+            if (A.need_special) {
+                double s0f[3] = {0, 0, 0}, scf[3] = {0, 0, 0}, s0r[3] = {0, 0, 0}, scr[3] = {0, 0, 0};
+                for (int base = 0; base < nq; base += 32) {
+                    double rt2;
+                    int small, nzw;
+                    dual_payload(A, gq, base + lane, nq, nbq, naq, true, W.geo + lane * kDualPay, rt2, small, nzw,
+                                 s0f, scf, s0r, scr);
+                }
+                dual_specials_reduce<NJ>(s0f, scf, s0r, scr, jq, W.Ls, W.Ls + LsLayout<3, NJ>::SIZE, lane);
+                __syncwarp();
+            }
+            dual_point_blocks<NJ>(A, gq, nq, nbq, naq, jq, istar, dend, sf, sr, W.geo, W.Ls, lane, tab);
+            __syncwarp();
+        }
+        for (int q = 0; q < npairs; ++q) m &= m - 1;
+    }
+}
+
+// per-warp shared memory: the warp-per-pair layout (payload, staged L row,
+// moment scratch), or the far batch's Ms + pair data where larger (they are
+// never live at the same time)
+template <int OP, int NIJ, int NJ>
+__host__ __device__ constexpr int smem_doubles_per_warp()
+{
+    if constexpr (NIJ == 1 || NIJ == 9) {
+        return smem_doubles_per_warp_base<OP, NIJ, NJ>() > far_smem_doubles<NIJ>()
+                   ? smem_doubles_per_warp_base<OP, NIJ, NJ>() : far_smem_doubles<NIJ>();
+    } else {
+        return smem_doubles_per_warp_base<OP, NIJ, NJ>();
+    }
+}
+template <int NJ>
+__host__ __device__ constexpr int dual_smem_doubles_per_warp()
+{
+    return dual_smem_doubles_per_warp_base<NJ>() > far_smem_doubles<6>() ? dual_smem_doubles_per_warp_base<NJ>()
+                                                                         : far_smem_doubles<6>();
 }
 
 // ---------------------------------------------------------------------------
@@ -926,8 +1808,8 @@ __device__ __forceinline__ void regular_item_dual(const PairArgs &A, int64_t e, 
 // Sauter-Schwab rule on the permuted charts of classify_pair.
 // ---------------------------------------------------------------------------
 template <int OP, bool TP1, bool SP1, int NJ>
-__device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, const Slots<OP, NJ> &T,
-                                              double *geo, double *Ls, int lane, const double *tab)
+__device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, const WarpMem &W, int lane,
+                                              const double *tab)
 {
     const hb_mesh_desc &M = A.m;
     const int64_t tpos = __ldg(M.sing_pos_dev + k);
@@ -964,7 +1846,8 @@ __device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, cons
     if (OP == 2 && jac == 0.0) return;   // n_x.n_y == 0: no contribution (finalize skips it)
     double ny[3];
     for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * f + c);
-    eval_pair<OP, TP1, SP1, NJ>(A, g, off1 - off0, ny, jac, slot, T, geo, Ls, lane, tab);
+    // touching pairs: no lower bound of rho~^2 (0)
+    eval_pair<OP, TP1, SP1, NJ>(A, g, off1 - off0, ny, jac, 0.0, slot, W.geo, W.Ls, W.Pw, lane, tab);
 }
 
 // ---------------------------------------------------------------------------
@@ -975,7 +1858,7 @@ __device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, cons
 // two quadrature families never share a warp; dynamic fetching removes the
 // imbalance of upper-triangular / near-diagonal tiles.
 // ---------------------------------------------------------------------------
-template <int OP, bool TP1, bool SP1, int NJ, bool SYM, bool DUAL = false>
+template <int OP, bool TP1, bool SP1, int NJ, bool SYM, bool DUAL, int CLS>
 __global__ void __launch_bounds__(HB_PAIR_WARPS * 32, (TP1 && SP1) ? HB_P1P1_MINB : HB_PAIR_MINB) k_pairs(const PairArgs A)
 {
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
@@ -983,33 +1866,40 @@ __global__ void __launch_bounds__(HB_PAIR_WARPS * 32, (TP1 && SP1) ? HB_P1P1_MIN
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *tab = smem;
     special::load_table<OP + 4>(tab);   // factor-free kinds (hb_special.cuh)
+    double *rule = smem + special::kTabDoubles;
+    if (A.m.n_reg <= kFarMaxRule) {
+        for (int i = threadIdx.x; i < 4 * (int)A.m.n_reg; i += blockDim.x)
+            rule[i] = i < A.m.n_reg ? __ldg(A.m.reg_w_dev + i) : __ldg(A.m.reg_hats_dev + i - A.m.n_reg);
+    }
     __syncthreads();
     constexpr int kPerWarp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
     static_assert(special::kTabDoubles % 2 == 0 && kPerWarp % 2 == 0 && Layout<OP, NIJ>::PAY % 2 == 0 &&
                       kDualPay % 2 == 0, "payload slots must stay 16-byte aligned (LDS.128)");
-    double *geo = smem + special::kTabDoubles + warp * kPerWarp;
-    double *Ls = geo + 32 * Layout<OP, NIJ>::PAY;
-    double *Ls_dual = geo + 32 * kDualPay;
+    double *geo = smem + special::kTabDoubles + kRuleDoubles + warp * kPerWarp;
+    WarpMem W;
+    W.geo = geo;
+    W.Ls = geo + 32 * (DUAL ? kDualPay : Layout<OP, NIJ>::PAY);
+    W.Pw = W.Ls + (DUAL ? 2 * LsLayout<3, NJ>::SIZE : LsLayout<NIJ, NJ>::SIZE);
+    W.rw = rule;
+    W.rh = rule + A.m.n_reg;
     const hb_mesh_desc &M = A.m;
     const int64_t s_lo = __ldg(M.sing_rowptr_dev + A.e0), s_hi = __ldg(M.sing_rowptr_dev + A.e1);
     int64_t n_sing = s_hi - s_lo;
     const int64_t nseg = cdiv(M.E_x, (int64_t)A.seg_len);
     int64_t n_reg = (A.e1 - A.e0) * nseg;
-    if (A.debug_class == 1) n_reg = 0;      // study hook: touching pairs only
-    if (A.debug_class == 2) n_sing = 0;     // study hook: separated pairs only
-    Slots<OP, NJ> T;
-    T.init(A, lane & 15);
+    if (CLS == 1) n_reg = 0;    // touching pairs only
+    if (CLS >= 2) n_sing = 0;   // separated pairs: far (2) / near (3)
     for (;;) {
         unsigned long long it = 0;
         if (lane == 0) it = atomicAdd(A.counter, 1ull);
         it = __shfl_sync(kFull, it, 0);
         const int64_t item = (int64_t)it;
         if (item < n_sing) {
-            singular_item<OP, TP1, SP1, NJ>(A, s_lo + item, T, geo, Ls, lane, tab);
+            singular_item<OP, TP1, SP1, NJ>(A, s_lo + item, W, lane, tab);
         } else if (item - n_sing < n_reg) {
             const int64_t r = item - n_sing;
-            if constexpr (DUAL) regular_item_dual<NJ>(A, A.e0 + r / nseg, r % nseg, T, geo, Ls_dual, lane, tab);
-            else regular_item<OP, TP1, SP1, NJ, SYM>(A, A.e0 + r / nseg, r % nseg, T, geo, Ls, lane, tab);
+            if constexpr (DUAL) regular_item_dual<NJ, CLS>(A, A.e0 + r / nseg, r % nseg, W, lane, tab);
+            else regular_item<OP, TP1, SP1, NJ, SYM, CLS>(A, A.e0 + r / nseg, r % nseg, W, lane, tab);
         } else {
             break;
         }
@@ -1282,22 +2172,10 @@ __global__ void __launch_bounds__(256) k_symmetrize(double *out, int64_t N, int6
 // ---------------------------------------------------------------------------
 // host orchestration
 // ---------------------------------------------------------------------------
-struct OpShape {
-    int NIJ, NJmax;
-};
+// gap slots per per-point window: 16 lanes x NJ = 2
+constexpr int kNJ = 2;
 
-static OpShape op_shape(const hb_assembly_desc *a)
-{
-    const int nij = (a->test_p1 ? 3 : 1) * (a->trial_p1 ? 3 : 1);
-    return {nij, 2};
-}
-
-static int choose_nj(const hb_assembly_desc *a)
-{
-    const OpShape s = op_shape(a);
-    int nj = (int)cdiv(a->E_t, 16);
-    return std::max(1, std::min(nj, s.NJmax));
-}
+static int op_nij(const hb_assembly_desc *a) { return (a->test_p1 ? 3 : 1) * (a->trial_p1 ? 3 : 1); }
 
 static bool combo_ok(const hb_assembly_desc *a)
 {
@@ -1310,21 +2188,47 @@ static bool combo_ok(const hb_assembly_desc *a)
 
 constexpr size_t kCounterBytes = 256;
 
-static size_t row_bytes(const hb_mesh_desc *m, const hb_assembly_desc *a)
+// moment form: always for the single layer (its accuracy at large d carries
+// into D through the curl transform); for K and D2 when the time grid has
+// enough steps (E_t >= 64) for the per-pair moments to replace many cheap
+// per-point gaps -- below that the direct kernel (hb_pairs_direct.cu) is
+// faster.  Decided by (op, E_t) only, so d-sharded calls of one operator
+// agree bitwise.  HB_MOMENTS=0/1 overrides.
+static int use_moments(const hb_assembly_desc *a)
 {
-    const int nj = choose_nj(a);
-    const int64_t W = std::min<int64_t>(16 * nj, a->d_end - a->d_begin);
-    return (size_t)m->E_x * op_shape(a).NIJ * W * sizeof(double);
+    static const int env = getenv("HB_MOMENTS") ? (atoi(getenv("HB_MOMENTS")) != 0) : -1;
+    if (env >= 0) return env;
+    return (a->op == HB_OP_SINGLE_LAYER || a->E_t >= 64) ? 1 : 0;
 }
 
-template <int OP, bool TP1, bool SP1, int NJ, bool DUAL = false>
-static int launch_pairs(const PairArgs &A, cudaStream_t st)
+// staging of one test row: every trial element x NIJ x the blocks of one
+// launch (all blocks of the call in the moment form, a 32-gap window direct)
+static size_t row_bytes(const hb_mesh_desc *m, const hb_assembly_desc *a)
+{
+    const int64_t nd = a->d_end - a->d_begin;
+    return (size_t)m->E_x * op_nij(a) * (size_t)(use_moments(a) ? nd : std::min<int64_t>(nd, 32)) * sizeof(double);
+}
+
+// moment table of the call (k_moment_table), 256-byte rounded
+static size_t tm_bytes(const hb_assembly_desc *a)
+{
+    if (!use_moments(a)) return 0;
+    const size_t n = (size_t)kNK * (size_t)(a->d_end - a->d_begin) + kNK + 1;
+    return (n * sizeof(double) + 255) & ~(size_t)255;
+}
+
+// one class of pair items: CLS 1 touching pairs (Sauter-Schwab), 3 separated
+// near pairs (warp per pair), 2 separated far pairs (batches).  The classes
+// run as separate launches so that each kernel's working set of instructions
+// is one path.
+template <int OP, bool TP1, bool SP1, int NJ, bool DUAL, int CLS>
+static int launch_class(const PairArgs &A, cudaStream_t st)
 {
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     constexpr bool SYM = (OP != 1);
     constexpr int per_warp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
-    const size_t sm = ((size_t)HB_PAIR_WARPS * per_warp + special::kTabDoubles) * sizeof(double);
-    auto kp = k_pairs<OP, TP1, SP1, NJ, SYM, DUAL>;
+    const size_t sm = ((size_t)HB_PAIR_WARPS * per_warp + special::kTabDoubles + kRuleDoubles) * sizeof(double);
+    auto kp = k_pairs<OP, TP1, SP1, NJ, SYM, DUAL, CLS>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
@@ -1337,7 +2241,9 @@ static int launch_pairs(const PairArgs &A, cudaStream_t st)
     const int64_t warps = (int64_t)std::max(1, per_sm) * nsm * HB_PAIR_WARPS;
     B.seg_len = 32;
     while (B.seg_len > 4 && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < 4 * warps) B.seg_len /= 2;
-    const int64_t items = rows * cdiv(A.m.E_x, (int64_t)B.seg_len) + rows * A.m.sing_max_per_row;
+    const int64_t items = CLS == 1 ? rows * A.m.sing_max_per_row : rows * cdiv(A.m.E_x, (int64_t)B.seg_len);
+    // (near-pair items: most segments hold none and exit after the classification)
+    if (items == 0) return HB_OK;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(1, per_sm) * nsm, cdiv(items, HB_PAIR_WARPS)));
     int rc = cuda_check(cudaMemsetAsync(A.counter, 0, sizeof(unsigned long long), st), "counter reset");
     if (rc) return rc;
@@ -1345,30 +2251,44 @@ static int launch_pairs(const PairArgs &A, cudaStream_t st)
     return cuda_check(cudaGetLastError(), "pair kernel");
 }
 
-template <int OP, bool TP1, bool SP1>
-static int dispatch_nj(int nj, const PairArgs &A, cudaStream_t st)
+template <int OP, bool TP1, bool SP1, int NJ, bool DUAL = false>
+static int launch_pairs(const PairArgs &A, cudaStream_t st)
 {
-    if constexpr (OP == 1) {
+    int rc = launch_class<OP, TP1, SP1, NJ, DUAL, 1>(A, st);
+    if (!rc) rc = launch_class<OP, TP1, SP1, NJ, DUAL, 3>(A, st);
+    if (!rc && A.moments) rc = launch_class<OP, TP1, SP1, NJ, DUAL, 2>(A, st);   // far batches
+    return rc;
+}
+
+static int run_pairs(const hb_assembly_desc *a, const PairArgs &A, cudaStream_t st)
+{
+    if (a->op == 0 && !a->test_p1) return launch_pairs<0, false, false, kNJ>(A, st);
+    if (a->op == 0 && a->test_p1) return launch_pairs<0, true, true, kNJ>(A, st);
+    if (a->op == 1) {
         // K: both orientations of a separated pair per evaluation (HB_K_DUAL=0: off).  A pair
         // whose other row lies outside the launch's rows (row chunks, row-parallel ranks) is
         // evaluated in the same canonical orientation with only the needed output's
         // accumulators, so the blocks stay independent of the row split.
         static const bool dual_on = !getenv("HB_K_DUAL") || atoi(getenv("HB_K_DUAL")) != 0;
-        if (dual_on) {
-            if (nj == 1) return launch_pairs<OP, TP1, SP1, 1, true>(A, st);
-            return launch_pairs<OP, TP1, SP1, 2, true>(A, st);
-        }
+        if (dual_on) return launch_pairs<1, false, true, kNJ, true>(A, st);
+        return launch_pairs<1, false, true, kNJ>(A, st);
     }
-    if (nj == 1) return launch_pairs<OP, TP1, SP1, 1>(A, st);
-    return launch_pairs<OP, TP1, SP1, 2>(A, st);
+    return launch_pairs<2, true, true, kNJ>(A, st);
 }
 
-static int run_pairs(const hb_assembly_desc *a, int nj, const PairArgs &A, cudaStream_t st)
+// the direct pair kernel (csrc/hb_pairs_direct.cu): one 32-gap window
+int direct_pairs(const hb_mesh_desc *m, const hb_assembly_desc *a, int64_t e0, int64_t e1, int d0, int d1,
+                 double *Q, unsigned long long *counter, cudaStream_t st);
+
+static int moment_table(const hb_assembly_desc *a, const PairArgs &A, double *Tm, cudaStream_t st)
 {
-    if (a->op == 0 && !a->test_p1) return dispatch_nj<0, false, false>(nj, A, st);
-    if (a->op == 0 && a->test_p1) return dispatch_nj<0, true, true>(nj, A, st);
-    if (a->op == 1) return dispatch_nj<1, false, true>(nj, A, st);
-    return dispatch_nj<2, true, true>(nj, A, st);
+    const int nd = (int)(a->d_end - a->d_begin);
+    const int n = kNK * nd + kNK + 1;
+    const unsigned grid = (unsigned)std::max(1, std::min(148, (n + 255) / 256));
+    if (a->op == HB_OP_SINGLE_LAYER) k_moment_table<0><<<grid, 256, 0, st>>>(Tm, (int)a->d_begin, nd, A.mom_S, A.mom_q0);
+    else if (a->op == HB_OP_DOUBLE_LAYER) k_moment_table<1><<<grid, 256, 0, st>>>(Tm, (int)a->d_begin, nd, A.mom_S, A.mom_q0);
+    else k_moment_table<2><<<grid, 256, 0, st>>>(Tm, (int)a->d_begin, nd, A.mom_S, A.mom_q0);
+    return cuda_check(cudaGetLastError(), "moment table");
 }
 
 }  // namespace hb
@@ -1378,13 +2298,13 @@ using namespace hb;
 extern "C" size_t hb_assemble_min_workspace(const hb_mesh_desc *m, const hb_assembly_desc *a)
 {
     if (!m || !a) return 0;
-    return row_bytes(m, a) + kCounterBytes;
+    return row_bytes(m, a) + tm_bytes(a) + kCounterBytes;
 }
 
 extern "C" size_t hb_assemble_full_workspace(const hb_mesh_desc *m, const hb_assembly_desc *a)
 {
     if (!m || !a) return 0;
-    return row_bytes(m, a) * (size_t)m->E_x + kCounterBytes;
+    return row_bytes(m, a) * (size_t)m->E_x + tm_bytes(a) + kCounterBytes;
 }
 
 namespace hb {
@@ -1458,14 +2378,14 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
         return HB_ERR_UNSUPPORTED;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    const int nj = choose_nj(a);
-    const int W = 16 * nj;
-    const size_t rb = row_bytes(m, a);
-    if (!a->workspace_dev || a->workspace_bytes < rb + kCounterBytes) {
-        set_error("hb_assemble: workspace %zu bytes < one row chunk (%zu bytes)", a->workspace_bytes, rb);
+    const size_t rb = row_bytes(m, a), tb = tm_bytes(a);
+    if (!a->workspace_dev || a->workspace_bytes < rb + tb + kCounterBytes) {
+        set_error("hb_assemble: workspace %zu bytes < one row chunk (%zu bytes)", a->workspace_bytes,
+                  rb + tb + kCounterBytes);
         return HB_ERR_WORKSPACE;
     }
-    const size_t q_bytes = (a->workspace_bytes - kCounterBytes) & ~(size_t)255;
+    // workspace: [staging Q: row chunks][moment table][counter]
+    const size_t q_bytes = (a->workspace_bytes - kCounterBytes - tb) & ~(size_t)255;
     const int64_t rows_per_chunk = std::max<int64_t>(1, std::min<int64_t>(m->E_x, (int64_t)(q_bytes / rb)));
     const int64_t R = a->test_p1 ? m->N_x : m->E_x, C = a->trial_p1 ? m->N_x : m->E_x;
     const int64_t nb = a->d_end - a->d_begin;
@@ -1485,44 +2405,64 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
     A.inv2a2 = 1.0 / (2.0 * a->alpha * a->alpha);
     A.inva = 1.0 / a->alpha;
     A.kconst = (a->op == 0) ? 1.0 / sqrt(kPi * a->alpha * a->alpha * a->alpha) : 1.0 / sqrt(kPi * a->alpha);
+    {   // moment form: u = 2 sqrt(alpha h); V: S = u / (2 a^2), q0 = 1/2; K, D2: S = 1/u, q0 = -1/2
+        const double u = 2.0 * sqrt(a->alpha * a->step);
+        A.inv_u2 = 1.0 / (u * u);
+        A.mom_S = (a->op == HB_OP_SINGLE_LAYER) ? u * A.inv2a2 : 1.0 / u;
+        A.mom_q0 = (a->op == HB_OP_SINGLE_LAYER) ? 0.5 : -0.5;
+    }
     A.halve_diag = p1p1 ? 1 : 0;
-#ifdef HB_DIAGNOSTICS   // timing study only: restrict the pair classes (results incomplete)
-    if (const char *dc = getenv("HB_DEBUG_CLASS")) A.debug_class = atoi(dc);
-#endif
     A.Q = (double *)a->workspace_dev;
-    A.counter = (unsigned long long *)((char *)a->workspace_dev + q_bytes);
+    double *Tm = (double *)((char *)a->workspace_dev + q_bytes);
+    A.Tm = Tm;
+    A.counter = (unsigned long long *)((char *)a->workspace_dev + q_bytes + tb);
+    // one launch per test-row chunk covers all blocks [d_begin, d_end): each pair
+    // computes its moments once and its per-point gap windows inside the kernel
+    A.d0 = (int)a->d_begin;
+    A.d1 = (int)a->d_end;
+    A.nd = (int)nb;
+    A.need_special = a->d_begin <= 1;
+    A.moments = use_moments(a);
 
     LaunchTimer LT{a->stats, st};
-    if (p1p1) LT.launches += 0;   // memset is not a kernel
-    int64_t d0 = a->d_begin;
-    while (d0 < a->d_end) {
-        // slots i_t in [max(1, d0-1), d1] must fit the W lanes-x-slots of a warp
-        const int64_t d1 = std::min<int64_t>(a->d_end, (d0 <= 1) ? (int64_t)W : d0 + W - 2);
-        A.d0 = (int)d0;
-        A.d1 = (int)d1;
-        A.nd = (int)(d1 - d0);
-        A.it_lo = (int)std::max<int64_t>(1, d0 - 1);
-        A.it_hi = (int)d1;
-        A.need_special = d0 <= 1;
-        // a short (tail) window needs only the lanes-x-slots its gaps occupy
-        const int nj_w = std::min(nj, (int)cdiv(A.it_hi - A.it_lo + 1, 16));
+    if (A.moments) {
+        cudaEvent_t ev = LT.begin(st);
+        int rc = moment_table(a, A, Tm, st);
+        if (rc) return rc;
+        LT.end(ev, false, st);
+        LT.launches += 1;
+    }
+    // moment form: one launch per row chunk for all blocks; direct form: windows
+    // of <= 32 gap slots (the first from block 0 or 1 holds 32 blocks, later 30)
+    const int64_t W = 32;
+    for (int64_t d0 = a->d_begin; d0 < a->d_end;) {
+        const int64_t d1 = A.moments ? a->d_end : std::min<int64_t>(a->d_end, (d0 <= 1) ? W : d0 + W - 2);
+        const int nd_w = (int)(d1 - d0);
+        // staging rows of this window: rows_per_chunk from the full row size is a lower bound
         for (int64_t e0 = r0; e0 < r1; e0 += rows_per_chunk) {
             const int64_t e1 = std::min(r1, e0 + rows_per_chunk);
             A.e0 = e0;
             A.e1 = e1;
             cudaEvent_t ev = LT.begin(st);
-            int rc = run_pairs(a, nj_w, A, st);
+            int rc;
+            if (A.moments) {
+                rc = run_pairs(a, A, st);   // three launches: touching, near, far pairs
+                LT.launches += 3;
+                LT.pair_launches += 3;
+            } else {
+                rc = direct_pairs(m, a, e0, e1, (int)d0, (int)d1, A.Q, A.counter, st);
+                LT.launches += 1;
+                LT.pair_launches += 1;
+            }
             if (rc) return rc;
             LT.end(ev, true, st);
-            LT.launches += 1;
-            LT.pair_launches += 1;
             ev = LT.begin(st);
             FinArgs F{};
             F.Q = A.Q;
             F.out = a->blocks_dev;
             F.bptr = a->block_ptrs_dev;
             F.E_x = m->E_x; F.N_x = m->N_x; F.R = R; F.C = C; F.e0 = e0; F.e1 = e1;
-            F.d0 = (int)d0; F.nd = A.nd; F.d_begin = (int)a->d_begin;
+            F.d0 = (int)d0; F.nd = nd_w; F.d_begin = (int)a->d_begin;
             F.star_indptr = m->star_indptr_dev; F.star_elem = m->star_elem_dev;
             F.star_local = m->star_local_dev; F.tri_nodes = m->tri_nodes_dev;
             F.normals = m->normals_dev; F.skip_zero_dot = a->op == HB_OP_HYPERSINGULAR2;
@@ -1545,17 +2485,19 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
             LT.end(ev, false, st);
             LT.launches += 1;
         }
-        if (p1p1) {
-            const int64_t nt = cdiv(R, 32);
-            dim3 g((unsigned)(nt * (nt + 1) / 2), (unsigned)(d1 - d0));
+        d0 = d1;
+    }
+    if (p1p1) {
+        const int64_t nt = cdiv(R, 32);
+        for (int64_t b0 = 0; b0 < nb; b0 += 65535) {
+            dim3 g((unsigned)(nt * (nt + 1) / 2), (unsigned)std::min<int64_t>(65535, nb - b0));
             cudaEvent_t ev = LT.begin(st);
-            k_symmetrize<<<g, 256, 0, st>>>(a->blocks_dev, R, d0 - a->d_begin);
+            k_symmetrize<<<g, 256, 0, st>>>(a->blocks_dev, R, b0);
             int rc = cuda_check(cudaGetLastError(), "symmetrize");
             if (rc) return rc;
             LT.end(ev, false, st);
             LT.launches += 1;
         }
-        d0 = d1;
     }
     return LT.finish();
 }
