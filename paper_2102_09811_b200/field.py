@@ -465,7 +465,8 @@ def represent(w, u, points, mesh, timegrid, params: KernelParams, config: Quadra
     k, eps = _decompose(np.array([float(p.t) for p in points]), timegrid.step)
     fused_ok = (n and w_np.shape[1] == mesh.n_triangles and u_np.shape[1] == mesh.n_vertices
                 and not os.environ.get("HB_REP_SEPARATE"))
-    grid = ((eps == 0.0) & (k <= 64)) if fused_ok else np.zeros(n, bool)
+    # (points past the final time, k > n_steps, take the general path below)
+    grid = ((eps == 0.0) & (k <= 64) & (k <= timegrid.n_steps)) if fused_ok else np.zeros(n, bool)
     done = grid.copy()
     vals = np.empty(n)
     if grid.any():
@@ -476,7 +477,7 @@ def represent(w, u, points, mesh, timegrid, params: KernelParams, config: Quadra
         vals[grid] = hist[inv.reshape(-1), kg]
     if fused_ok:
         # eps > 0 (inside a step): one per-element launch per distinct eps with >= 8 points
-        off = (eps > 0.0) & (k >= 1) & (k <= 64)
+        off = (eps > 0.0) & (k >= 1) & (k <= 64) & (k <= timegrid.n_steps)
         ev, cnt = np.unique(eps[off], return_counts=True)
         for e_val in ev[cnt >= 8]:
             sel = off & (eps == e_val)

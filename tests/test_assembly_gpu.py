@@ -3,17 +3,20 @@
 Tolerances (north star: <= 1e-11 of each block's max-abs entry):
 * bit-exact: pair classification, exact-zero pattern, symmetry, Toeplitz
   block reuse, d-sharding / row-chunking invariance, run-to-run determinism;
-* values: per block d, |gpu - ref| / max|ref| <= max(1e-11, 3 eps_ref(d)),
-  where eps_ref(d) is the reference's OWN deviation from the exact value of
-  the same quadrature (quad-precision oracle, tests/golden/exact.npz).  The
-  time second difference B^d = -L(d-1) + 2L(d) - L(d+1) and the curl
-  transform of D amplify last-bit libm differences beyond 1e-11 at large d
-  (the reference itself is 2.5e-11 off exact for c2 V, 4.6e-9 for c2 D);
-* accuracy: |gpu - exact| <= ACC[op] eps_ref(d) + 1e-13 -- the GPU blocks are
-  about as close to the exact quadrature as the reference's own fp64 blocks
-  (measured: V 1.1-1.7x, V11 0.8x, D2 1.5x, D 2.0-2.2x, K 0.7x -- the fused
-  evaluation F(x) of csrc/hb_special.cuh removes the 1/x^2 cancellation of the
-  reference's K bracket, so the GPU K is closer to exact than the reference).
+* values: per block d, |gpu - ref| / max|ref| <= 1e-11 wherever the
+  reference's OWN deviation from the exact value of the same quadrature,
+  eps_ref(d) (quad-precision oracle, tests/golden/exact.npz), is <= 3.3e-12;
+  above that <= 3 eps_ref(d): the time second difference
+  B^d = -L(d-1) + 2L(d) - L(d+1) and the curl transform of D amplify the
+  reference's last-bit libm errors beyond 1e-11 at large d (2.5e-11 off exact
+  for c2 V, 4.6e-9 for c2 D) -- a GPU result closer to exact than that
+  cannot also be within 1e-11 of the reference;
+* accuracy: |gpu - exact| <= eps_ref(d) + 1e-13 -- the GPU blocks are at
+  least as close to the exact quadrature as the reference's own fp64 blocks
+  (measured on the golden rows, profiles/r02_parity_c1_c2.json: <= 0.98
+  eps_ref; the moment form makes the large-d blocks of V, and through the
+  curl D, nearly exact, and F(x) removes the 1/x^2 cancellation of the
+  reference's K bracket).
 """
 import numpy as np
 import pytest
@@ -23,7 +26,14 @@ from _hb_util import golden, rel_block_err
 
 pytestmark = pytest.mark.gpu
 Q4 = hb.QuadratureConfig(4, 4)
-ACC = {"V": 2.0, "V11": 2.0, "D2": 2.0, "D": 2.5, "K": 1.5}
+ACC = {"V": 1.0, "V11": 1.0, "D2": 1.0, "D": 1.0, "K": 1.0}
+
+
+def gate(eps_ref):
+    """|gpu - ref| bar per block: the literal 1e-11 where the reference is
+    well conditioned (eps_ref <= 3.3e-12), 3 eps_ref above."""
+    eps_ref = np.asarray(eps_ref)
+    return np.where(eps_ref <= 3.3e-12, 1e-11, 3 * eps_ref)
 OPS = {
     "V": lambda m, tg, p, **k: hb.assemble_single_layer(m, tg, p, Q4, **k),
     "K": lambda m, tg, p, **k: hb.assemble_double_layer(m, tg, p, Q4, **k),
@@ -78,7 +88,7 @@ def test_c1_parity_and_accuracy(c1_ops):
         ref_rows, ex_rows, bmax = g[f"{op}_rows"], ex[f"c1_{op}_exact_rows"], g[f"{op}_maxabs"]
         eps_ref = ex[f"c1_{op}_eps_ref"]
         par = np.abs(B[:, rows, :] - ref_rows).max(axis=(1, 2)) / bmax
-        assert np.all(par <= np.maximum(1e-11, 3 * eps_ref)), (op, par, eps_ref)
+        assert np.all(par <= gate(eps_ref)), (op, par, eps_ref)
         acc = np.abs(B[:, rows, :] - ex_rows).max(axis=(1, 2)) / bmax
         assert np.all(acc <= ACC[op] * eps_ref + 1e-13), (op, acc, eps_ref)
         assert np.array_equal(np.packbits(B[0] == 0.0), g[f"{op}_zeros"]), op
@@ -90,7 +100,7 @@ def test_c1_full_blocks_vs_oracle(oracle, c1_ops):
     for op in ("V", "K", "D2", "V11"):
         ref = oracle.assemble(m, tg, p, Q4, op)
         err = rel_block_err(c1_ops[op], ref)
-        assert np.all(err <= np.maximum(1e-11, 3 * ex[f"c1_{op}_eps_ref"])), (op, err)
+        assert np.all(err <= gate(ex[f"c1_{op}_eps_ref"])), (op, err)
         assert np.array_equal(c1_ops[op] == 0.0, ref == 0.0), op
         if op != "K":
             assert all(np.array_equal(c1_ops[op][d], c1_ops[op][d].T) for d in range(16)), op
@@ -148,6 +158,12 @@ def test_long_history_windows_match_single_window():
 
 
 def test_long_history_vs_oracle(oracle):
+    """80 blocks on the reference's [-1, 1]^3 cube (alpha = 0.5): rho~^2 reaches
+    480 here, so most pairs stay in the point-by-point form for all 80 gaps
+    (istar = rho~^2 / 3 > E_t) -- the same second-difference amplification of
+    per-point rounding as the reference; measured |gpu - exact| <= 1.14
+    eps_ref (V, d = 58), hence the 1.5 bar on this synthetic case (BASELINE
+    configs: <= 1.0, tests above and below)."""
     m = hb.generate_cube_surface(2)
     tg = hb.TimeGrid(1.0, 80)
     p = hb.KernelParams(0.5, tg.step, length_scale=m.diameter)
@@ -156,8 +172,8 @@ def test_long_history_vs_oracle(oracle):
         got = OPS[op](m, tg, p).blocks
         x = oracle.assemble(m, tg, p, Q4, op, exact=True)
         eps_ref = rel_block_err(ref, x)
-        assert np.all(rel_block_err(got, ref) <= np.maximum(1e-11, 3 * eps_ref)), op
-        assert np.all(rel_block_err(got, x) <= ACC[op] * eps_ref + 1e-13), op
+        assert np.all(rel_block_err(got, ref) <= gate(eps_ref)), op
+        assert np.all(rel_block_err(got, x) <= 1.5 * eps_ref + 1e-13), op
 
 
 def test_c2_rows_vs_reference():
@@ -173,7 +189,7 @@ def test_c2_rows_vs_reference():
         par = np.abs(B[:, rows, :] - g[f"{op}_rows"]).max(axis=(1, 2)) / g[f"{op}_maxabs"]
         if f"c2_{op}_eps_ref" in ex:
             eps_ref = ex[f"c2_{op}_eps_ref"]
-            assert np.all(par <= np.maximum(1e-11, 3 * eps_ref)), (op, par)
+            assert np.all(par <= gate(eps_ref)), (op, par)
             acc = np.abs(B[:, rows, :] - ex[f"c2_{op}_exact_rows"]).max(axis=(1, 2)) / g[f"{op}_maxabs"]
             assert np.all(acc <= ACC[op] * eps_ref + 1e-13), (op, acc, eps_ref)
         else:   # D2: well conditioned, plain bar
@@ -241,11 +257,10 @@ def test_c5_sampled_rows_vs_reference():
     extra gap slots; 39 / 19 GB per chunk), three sampled rows per block
     compared with the reference's single-row oracle (tests/golden/c5_rows.npz,
     exact values from the quad build).  At d ~ 255 the reference's own V rows
-    are up to 2.4e-9 of block max from exact (the -L + 2L - L cancellation),
-    and ours suffer the same cancellation with different rounding, so both
-    gates use 3 eps_ref(d): |gpu - ref| <= max(1e-11, 3 eps_ref) and
-    |gpu - exact| <= 3 eps_ref + 1e-13.  Structural zeros (coplanar K
-    columns) must be exact zeros."""
+    are up to 2.4e-9 of block max from exact (the -L + 2L - L cancellation);
+    the GPU's moment form does not cancel there, so |gpu - ref| ~ eps_ref:
+    |gpu - ref| <= gate(eps_ref) and |gpu - exact| <= eps_ref + 1e-13.
+    Structural zeros (coplanar K columns) must be exact zeros."""
     import torch
 
     from paper_2102_09811_b200.assembly import _assemble_operator
@@ -271,8 +286,8 @@ def test_c5_sampled_rows_vs_reference():
         gs = got[:, :, ::stride]
         par = np.abs(gs - g[f"{op}_ref"]).max(axis=(1, 2)) / mx
         acc = np.abs(gs - g[f"{op}_exact"]).max(axis=(1, 2)) / mx
-        assert np.all(par <= np.maximum(1e-11, 3 * eps)), (op, par.max())
-        assert np.all(acc <= 3 * eps + 1e-13), (op, np.max(acc / eps))
+        assert np.all(par <= gate(eps)), (op, par.max())
+        assert np.all(acc <= ACC[op] * eps + 1e-13), (op, np.max(acc / eps))
         # structural zeros -- exactly zero in the quad build at every d (the
         # coplanar K columns) -- must be exact zeros at every d; the other
         # zeros (far pairs at d <= 5, roundings of the -L + 2L - L second
@@ -291,7 +306,7 @@ def test_c3_sampled_rows_vs_reference():
     with the reference's single-row oracle (tests/golden/c3_rows.npz, with
     exact values from the quad build).  The reference's own V rows are up to
     6.3e-11 of block max from exact at large d, so the gate is
-    max(1e-11, 3 eps_ref(d)) and |gpu - exact| <= ACC eps_ref(d) + 1e-13."""
+    gate(eps_ref(d)) and |gpu - exact| <= ACC eps_ref(d) + 1e-13."""
     import torch
 
     from paper_2102_09811_b200.assembly import _assemble_operator
@@ -316,7 +331,7 @@ def test_c3_sampled_rows_vs_reference():
         gs = got[:, :, ::stride]
         par = np.abs(gs - g[f"{op}_ref"]).max(axis=(1, 2)) / mx
         acc = np.abs(gs - g[f"{op}_exact"]).max(axis=(1, 2)) / mx
-        assert np.all(par <= np.maximum(1e-11, 3 * eps)), (op, par.max())
+        assert np.all(par <= gate(eps)), (op, par.max())
         assert np.all(acc <= ACC[op] * eps + 1e-13), (op, np.max(acc / eps))
         # no structural zeros on the sphere (no coplanar pairs): the reference's
         # exact zeros at large d are rounding cancellations of -L + 2L - L,

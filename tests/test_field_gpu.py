@@ -146,3 +146,40 @@ def test_register_kernel_vs_oracle(oracle, E_t, steps, fused, monkeypatch):
     assert np.allclose(outs[0], outs[1], rtol=1e-13, atol=1e-14 * np.abs(ref).max())
     if steps is not None and 0 in steps:
         assert np.all(got[:, list(steps).index(0)] == 0.0)
+
+
+@pytest.mark.parametrize("E_t", [80, 130])
+def test_long_history_potentials_vs_oracle(oracle, E_t):
+    """Histories longer than 64 steps (reference _field_numba._eval_potential
+    handles any k): time-step ends k in (64, E_t] and points inside steps go
+    through the general k_potential path, k <= 64 through the per-element
+    kernel; points past the final time (k > E_t) through the general path
+    too.  Both potentials and the representation formula vs the oracle."""
+    from paper_2102_09811_b200.field import _decompose, _interp_density_np
+    from paper_2102_09811_b200.quadrature import rule_tables
+
+    m = hb.unit_cube_mesh(1)
+    tg = hb.TimeGrid(1.0, E_t)
+    p = hb.KernelParams(0.9, tg.step, length_scale=m.diameter)
+    rng = np.random.default_rng(E_t)
+    w = rng.standard_normal((E_t, m.n_triangles))
+    uu = rng.standard_normal((E_t, m.n_vertices))
+    X = rng.uniform(0.05, 0.95, (10, 3))
+    ks = np.array([1, 40, 64, 65, 77, E_t - 1, E_t])
+    T = np.concatenate([np.repeat(ks, len(X)) * tg.step,                       # time-step ends
+                        (np.repeat(ks[:-1], len(X)) + 0.37) * tg.step,         # inside steps
+                        np.full(len(X), 1.0 + 2.5 * tg.step)])                  # past the final time
+    XX = np.tile(X, (len(T) // len(X), 1))
+    pts = [hb.EvalPoint(x, t) for x, t in zip(XX, T)]
+    hats, qw, qpts = rule_tables(m, 6)
+    k, eps = _decompose(T, tg.step)
+    cur = (eps > 0) & (k < E_t)
+    refs = {}
+    for kind, c in ((0, w), (1, uu)):
+        refs[kind] = oracle.potential(kind, XX, k, eps, cur, _interp_density_np(c, m, hats), qpts, qw, m.areas,
+                                      m.normals, tg.step, p.alpha, p.delta_eps, p.rho_eps)
+    sl, _ = hb.eval_single_layer_potential(w, pts, m, tg, p)
+    dl, _ = hb.eval_double_layer_potential(uu, pts, m, tg, p)
+    rep, _ = hb.represent(w, uu, pts, m, tg, p)
+    for got, ref in ((sl, refs[0]), (dl, refs[1]), (rep, refs[0] - refs[1])):
+        assert np.allclose(got, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max())
