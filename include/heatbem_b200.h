@@ -211,7 +211,9 @@ int hb_represent_grid(int64_t n_points, int64_t n_times, int64_t E_t, int64_t E_
  * element; dens_vert (E_x, 3, E_t): the p1 density at each element's vertices
  * (tri_nodes order); hats (nq, 3) at the quadrature nodes; time fastest.
  * eps in [0, step): the outputs are u(x_i, k_j h + eps) -- eps > 0 is the
- * reference's current-interval case (_field_numba.py:53-76; k_j >= 1). */
+ * reference's current-interval case (_field_numba.py:53-76) and requires
+ * k_j >= 1 (k_j = 0 outputs are written as NaN; field.py routes such points
+ * through hb_potential). */
 int hb_represent_grid_elem(int64_t n_points, int64_t n_times, int64_t E_t, int64_t E_x, int64_t nq,
                            const double *x_dev, const int64_t *k_dev, int64_t kmax,
                            const double *dens_elem_dev, const double *dens_vert_dev, const double *hats_dev,

@@ -36,58 +36,143 @@ _OP_SINGLE, _OP_DOUBLE, _OP_HYPER2 = 0, 1, 2
 _DEFAULT_WS_CAP = 16 << 30
 
 
+class _HostBlocks(np.ndarray):
+    """Host view of a BlockToeplitzMatrix's blocks that records writes.
+
+    The reference mutates operators through their ``.blocks`` array
+    (heatbem/assembly.py:328-333: ``out = D2.blocks; out[d] += ...``).  Item
+    assignment and in-place ufuncs on this array -- or on any view taken from
+    it -- mark the owning storage host-dirty, so the next device use uploads
+    the edited blocks and drops the cached (A^0)^{-1}."""
+
+    def __array_finalize__(self, obj):
+        self._hb_store = getattr(obj, "_hb_store", None)
+
+    def _hb_touch(self):
+        st = getattr(self, "_hb_store", None)
+        if st is not None:
+            st.host_written()
+
+    def __setitem__(self, key, value):
+        super().__setitem__(key, value)
+        self._hb_touch()
+
+    def __array_ufunc__(self, ufunc, method, *inputs, out=None, **kwargs):
+        args = [np.asarray(x) if isinstance(x, _HostBlocks) else x for x in inputs]
+        outs = None
+        if out is not None:
+            outs = tuple(np.asarray(o) if isinstance(o, _HostBlocks) else o for o in out)
+            kwargs["out"] = outs
+        res = getattr(ufunc, method)(*args, **kwargs)
+        if out is not None:
+            for o in out:
+                if isinstance(o, _HostBlocks):
+                    o._hb_touch()
+            return out[0] if len(out) == 1 else out
+        return res
+
+
+class _BlockStorage:
+    """Blocks of one operator (shared by its transposed() twins): host array,
+    device tensor, which side is current, and caches derived from the blocks."""
+
+    def __init__(self, host=None, dev=None):
+        self.host, self.dev = host, dev
+        self.host_dirty = False     # host edited after the device copy was made
+        self.version = 0            # bumped on every change of the blocks
+        self.inv_cache = {}         # (A^0)^{-1} per transpose flag (solver.py)
+
+    def changed(self):
+        self.version += 1
+        self.inv_cache = {}
+
+    def host_written(self):
+        if self.dev is not None:
+            self.host_dirty = True
+        self.changed()
+
+    def device_written(self):
+        """The device blocks were changed in place: the host copy is stale."""
+        self.host = None
+        self.host_dirty = False
+        self.changed()
+
+
 class BlockToeplitzMatrix:
     """Block (k, i) = blocks[k - i] for k >= i, zero above (never stored).
 
     Construct from a numpy array (host) or a torch tensor (device); the
-    other side is created on first use.  ``transposed()`` shares storage."""
+    other side is created on first use.  ``transposed()`` shares storage.
+    Host and device stay coherent: ``.blocks`` hands out a host array whose
+    in-place edits (the reference's idiom) reach the device on its next use,
+    assigning ``.blocks`` replaces both sides, and in-place device writes by
+    the library (e.g. ``hypersingular_from_single_layer(overwrite_d2=True)``)
+    drop the host copy; every change drops the cached (A^0)^{-1}."""
 
     def __init__(self, blocks, transpose_blocks_on_apply: bool = False, diagonal_only: bool = False):
-        self._host = None
-        self._dev = None
         if _is_torch(blocks):
-            self._dev = blocks
+            self._store = _BlockStorage(dev=blocks)
         else:
-            self._host = np.asarray(blocks, dtype=np.float64)
+            self._store = _BlockStorage(host=np.asarray(blocks, dtype=np.float64))
         self.transpose_blocks_on_apply = bool(transpose_blocks_on_apply)
         self.diagonal_only = bool(diagonal_only)
-        self._share = None   # storage shared with transposed() twins
         self.host_copy = None  # (page-locked host tensor, event) when streamed to the host
 
     # ---- storage ---------------------------------------------------------
     @property
     def shape(self):
-        return tuple(self._dev.shape) if self._dev is not None else self._host.shape
+        st = self._store
+        if st.host is not None and (st.host_dirty or st.dev is None):
+            return st.host.shape
+        return tuple(st.dev.shape) if st.dev is not None else st.host.shape
 
     @property
     def blocks(self) -> np.ndarray:
-        if self._host is None:
-            self._host = self._dev.detach().cpu().numpy()
-            if self._share is not None:
-                self._share._host = self._host
-        return self._host
+        st = self._store
+        if st.host is None:
+            st.host = st.dev.detach().cpu().numpy()
+        if not isinstance(st.host, _HostBlocks) and st.host.flags.writeable:
+            st.host = st.host.view(_HostBlocks)
+        if isinstance(st.host, _HostBlocks):
+            st.host._hb_store = st
+        return st.host
 
     @blocks.setter
     def blocks(self, value):
-        self._host = np.asarray(value, dtype=np.float64)
-        self._dev = None
-        self._lu_cache = None
+        st = self._store
+        st.host = np.asarray(value, dtype=np.float64)
+        st.dev = None
+        st.host_dirty = False
+        st.changed()
 
     @property
     def device_blocks(self):
-        """(n_blocks, rows, cols) float64 CUDA tensor."""
-        if self._dev is None:
+        """(n_blocks, rows, cols) float64 CUDA tensor (uploads host edits first)."""
+        st = self._store
+        if st.dev is None or st.host_dirty:
             import torch
 
             _native.require_cuda()
-            self._dev = torch.from_numpy(np.ascontiguousarray(self._host)).cuda()
-            if self._share is not None:
-                self._share._dev = self._dev
-        return self._dev
+            src = np.ascontiguousarray(np.asarray(st.host))
+            if st.dev is not None and tuple(st.dev.shape) == src.shape:
+                st.dev.copy_(torch.from_numpy(src))
+            else:
+                st.dev = torch.from_numpy(src).cuda()
+            st.host_dirty = False
+        return st.dev
 
     @property
     def on_device(self) -> bool:
-        return self._dev is not None
+        return self._store.dev is not None
+
+    @property
+    def version(self) -> int:
+        """Counts the changes of the blocks (host edits, assignments, in-place device writes)."""
+        return self._store.version
+
+    def mark_device_written(self):
+        """Declare an in-place change of ``device_blocks`` (drops the host copy and caches)."""
+        self._store.device_written()
 
     # ---- reference properties -------------------------------------------
     @property
@@ -126,10 +211,10 @@ class BlockToeplitzMatrix:
     def transposed(self) -> "BlockToeplitzMatrix":
         """Blockwise transpose (K' from K), sharing the block storage."""
         t = BlockToeplitzMatrix.__new__(BlockToeplitzMatrix)
-        t._host, t._dev = self._host, self._dev
+        t._store = self._store
         t.transpose_blocks_on_apply = not self.transpose_blocks_on_apply
         t.diagonal_only = self.diagonal_only
-        t._share, self._share = self, t
+        t.host_copy = None
         return t
 
 
@@ -462,7 +547,7 @@ def hypersingular_from_single_layer(V: BlockToeplitzMatrix, D2: BlockToeplitzMat
         out.record_stream(cs)
         host_copy = (host_out, done)
     if overwrite_d2:
-        D2._host = None
+        D2.mark_device_written()
         D2.host_copy = host_copy
         return D2
     res = BlockToeplitzMatrix(out)

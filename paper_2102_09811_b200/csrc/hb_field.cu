@@ -1266,6 +1266,9 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
                 const double *os = cl.map_shared_rank(Os, s);
                 v += os[p * (KM + 2) + k] + os[(kFP + p) * (KM + 2) + k];
             }
+            // k = 0 inside the first step (eps > 0) is not this kernel's case
+            // (header: k >= 1 when eps > 0): NaN, never a silent 0
+            if (EPS && k == 0) v = __longlong_as_double(0x7ff8000000000000ll);
             P.out[gg * P.n_times + o] = v;
         }
     }

@@ -197,14 +197,15 @@ __global__ void __launch_bounds__(256) k_inv_apply(const double *__restrict__ in
 using namespace hb;
 
 // ---------------------------------------------------------------------------
-// Large operators (R >= kMmaMinRows rows, not transposed): the block-Toeplitz
+// Large operators (>= kMmaMinRows output rows; plain or transposed): the block-Toeplitz
 // product as one tensor-core GEMM per block d,
 //   Y[k][r] += sum_c X[k - d][c] A^d[r][c]   (k >= d),
 // with mma.sync m8n8k4 f64 (DMMA): M = steps (a CTA owns a 64-step tile,
-// 8-step fragments), N = 32 rows per CTA (warp w: rows 8w..8w+7), K = the
-// input index in 32-wide chunks staged in shared memory (row stride 36:
-// conflict-free fragment loads) -- per (chunk, d) the A^d tile and the 64
-// x rows k - d of the step tile.  Every element of A is read from HBM once per
+// 8-step fragments), N = 32 output rows per CTA (4 warps; warp w: rows
+// 8w..8w+7), K = the input index in 32-wide chunks staged in shared memory
+// (row stride 36: conflict-free fragment loads) -- per (chunk, d) the A^d tile
+// and the 96-row x window of the step tile.  TR (K', D^T): the A^d tile is
+// staged as [in 32][out 32] and read as the B fragment B[k = in][n = out].  Every element of A is read from HBM once per
 // 64-step tile (the warp-per-row kernel re-reads it once per 8-step tile);
 // sums run in a fixed order (chunk, d, K step).
 // ---------------------------------------------------------------------------
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(kMT) k_toep_mma(const double *__restrict__ blo
     // tile's steps k_lo + j, i.e. x[k_lo - db - 32 + w], w = 0..95 (row of step j
     // at block d: w = j - (d - db) + 32)
     __shared__ __align__(16) double Xw[96][kMS];
-    // A^d tile: [out 64][in 32] (row stride 36) or, transposed, [in 32][out 64] (stride 68)
+    // A^d tile: [out 32][in 32] (row stride 36) or, transposed, [in 32][out 32] (stride 36)
     __shared__ __align__(16) double As[kMR * kMS > kMC * (kMR + 4) ? kMR * kMS : kMC * (kMR + 4)];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
     const int64_t r0 = (int64_t)blockIdx.x * kMR, k_lo = (int64_t)blockIdx.y * 64;
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(kMT) k_toep_mma(const double *__restrict__ blo
 #pragma unroll
                 for (int u = 0; u < PT; ++u) {
                     const int i = tid + kMT * u;
-                    if (TR) {   // rows c0 + ii of A, 64 output columns r0.. (coalesced along the row)
+                    if (TR) {   // rows c0 + ii of A, 32 output columns r0.. (coalesced along the row)
                         const int ii = i / kMR, oo = i % kMR;
                         v[u] = (c0 + ii < n_in && r0 + oo < n_out) ? __ldg(Ad + (c0 + ii) * C + r0 + oo) : 0.0;
                     } else {

@@ -159,15 +159,24 @@ class PeerShardTable:
 
         self._L = _native.load()
         rank = dist.get_rank(group) if dist.is_initialized() else 0
-        block_bytes = int(local[0].numel()) * 8 if local.shape[0] else 0
-        h = (ctypes.c_char * 64)()
-        off = ctypes.c_int64()
-        _native.call("hb_ipc_export", local.data_ptr(), h, ctypes.byref(off))
-        metas = exchange_shard_meta((bytes(h), off.value, d0, d1), group)
+        block_bytes = int(np.prod(tuple(local.shape[1:]))) * 8   # valid for an empty shard too
+        if d1 > d0 and local.numel() > 0:
+            h = (ctypes.c_char * 64)()
+            off = ctypes.c_int64()
+            _native.call("hb_ipc_export", local.data_ptr(), h, ctypes.byref(off))
+            meta = (bytes(h), off.value, d0, d1)
+        else:
+            # an empty d-shard (more ranks than blocks): nothing to map, but the
+            # collective below still runs on every rank
+            meta = (None, 0, d0, d1)
+        metas = exchange_shard_meta(meta, group)
         bases, self._opened = [], []
         for r, (hr, o, a, b) in enumerate(metas):
             if r == rank:
-                bases.append((local.data_ptr(), a, b))
+                bases.append((local.data_ptr() if meta[0] is not None else 0, a, b))
+                continue
+            if hr is None or b <= a:
+                bases.append((0, a, b))
                 continue
             p = ctypes.c_void_p()
             _native.call("hb_ipc_import", hr, o, ctypes.byref(p))

@@ -77,19 +77,16 @@ def apply_toeplitz(matrix: BlockToeplitzMatrix, x, transpose_blocks: bool = Fals
 
 
 def _inverse(matrix, tr):
-    """(A^0)^{-1} (of A^0^T when transposed), cached on the matrix: the
-    reference refactors A^0 on every call (solver.py:176)."""
+    """(A^0)^{-1} (of A^0^T when transposed), cached with the matrix's block
+    storage and dropped on any change of the blocks (host edits through
+    ``.blocks``, assignment, in-place device writes): the reference refactors
+    A^0 on every call (solver.py:176)."""
     import torch
 
-    cache = getattr(matrix, "_inv_cache", None)
-    if cache is None:
-        cache = {}
-        try:
-            matrix._inv_cache = cache
-        except AttributeError:
-            pass
+    A0 = matrix.device_blocks[0]   # uploads pending host edits (and drops the cache) first
+    store = getattr(matrix, "_store", None)
+    cache = store.inv_cache if store is not None else {}
     if tr not in cache:
-        A0 = matrix.device_blocks[0]
         cache[tr] = torch.linalg.inv(A0.T.contiguous() if tr else A0).contiguous()
     return cache[tr]
 

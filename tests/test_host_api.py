@@ -134,3 +134,33 @@ def test_row_slabs_cover_rows_with_balanced_work():
         assert all(a < b for a, b in sl) and all(sl[i][1] == sl[i + 1][0] for i in range(len(sl) - 1))
     work = [sum(768 - e for e in range(a, b)) for a, b in _row_slabs(768, True, 4)]
     assert max(work) / min(work) < 1.05
+
+
+def test_blocks_host_edits_are_tracked():
+    """The reference edits operators through .blocks (assembly.py:328-333:
+    out = D2.blocks; out[d] += ...): item assignment, in-place ufuncs and
+    writes through views bump the shared storage version (which drops the
+    cached (A^0)^-1 and makes the next device use upload the edit); the
+    transposed twin shares it; assigning .blocks replaces the blocks."""
+    rng = np.random.default_rng(3)
+    M = hb.BlockToeplitzMatrix(rng.standard_normal((3, 4, 4)))
+    Mt = M.transposed()
+    v0 = M.version
+    out = M.blocks
+    out[1] += 1.0                       # reference idiom
+    assert M.version > v0 and Mt.version == M.version
+    v1 = M.version
+    out += 0.5                          # in-place ufunc
+    assert M.version > v1
+    v2 = M.version
+    view = out[2]
+    view[0, 0] = 7.0                    # write through a view
+    assert M.version > v2 and M.blocks[2, 0, 0] == 7.0 and Mt.blocks[2, 0, 0] == 7.0
+    v3 = M.version
+    np.multiply(out, 2.0, out=out)
+    assert M.version > v3
+    v4 = M.version
+    s = out.sum() + float((out[0] * 2.0).max())   # reads do not count as edits
+    assert M.version == v4 and np.isfinite(s)
+    M.blocks = np.zeros((2, 4, 4))
+    assert M.version > v4 and M.n_blocks == 2 and Mt.n_blocks == 2

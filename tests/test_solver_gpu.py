@@ -209,3 +209,39 @@ def test_row_sharded_kernels_bitwise(world):
         xf, rep1 = hb.fgmres(hb.toeplitz_operator(M), rhs, rel_tol=1e-12,
                              right_precond=lambda v: hb.forward_block_solve(M, v))
         assert rep.converged and torch.equal(torch.as_tensor(xr), torch.as_tensor(xf))
+
+
+def test_host_edits_reach_device_and_drop_cached_inverse():
+    """Reference idiom (assembly.py:328-333): edit .blocks in place, then
+    apply_toeplitz / forward_block_solve must see the edited operator --
+    including a new (A^0)^-1 after A^0 itself changed -- and so must the
+    blockwise-transposed twin; assigning .blocks and overwrite_d2 likewise."""
+    rng = np.random.default_rng(11)
+    n, nb = 6, 4
+    B = rng.standard_normal((nb, n, n)) * 0.1
+    B[0] += 4.0 * np.eye(n)
+    M = hb.BlockToeplitzMatrix(B.copy())
+    Mt = M.transposed()
+    x = rng.standard_normal((nb, n))
+    hb.forward_block_solve(M, x)                    # caches (A^0)^-1 and puts the blocks on the device
+    hb.apply_toeplitz(Mt, x)
+    out = M.blocks
+    out[0] += 2.0 * np.eye(n)                       # edit A^0 in place
+    out[2] *= -1.0
+    Bn = np.asarray(out).copy()
+    assert np.allclose(hb.apply_toeplitz(M, x), _dense_apply(Bn, x), rtol=1e-12, atol=1e-12)
+    assert np.allclose(hb.apply_toeplitz(Mt, x), _dense_apply(np.transpose(Bn, (0, 2, 1)), x), rtol=1e-12, atol=1e-12)
+    y = hb.forward_block_solve(M, x)
+    assert np.allclose(_dense_apply(Bn, y), x, rtol=1e-10, atol=1e-10)
+    M.blocks = B.copy()                             # assignment replaces both sides
+    y = hb.forward_block_solve(M, x)
+    assert np.allclose(_dense_apply(B, y), x, rtol=1e-10, atol=1e-10)
+
+
+def _dense_apply(blocks, x):
+    nb = blocks.shape[0]
+    y = np.zeros((x.shape[0], blocks.shape[1]))
+    for k in range(x.shape[0]):
+        for d in range(min(k + 1, nb)):
+            y[k] += blocks[d] @ x[k - d]
+    return y
