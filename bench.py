@@ -1,28 +1,48 @@
 #!/usr/bin/env python
 """Benchmark: BEM matrix entries assembled per second (fp64 V / K / D).
 
-Workload = BASELINE config 2 (the config the headline metric is quoted on
-that fits one GPU): unit-cube surface refined 3x (768 triangles, 386 nodes),
-N = 32 time steps, alpha = 1.  One step assembles V (p0 x p0), K (p0 x p1;
-K' is the blockwise-transposed view, not re-counted) and D = D2 + curl(V)
-(p1 x p1) -- E_t (E_x^2 + E_x N_x + N_x^2) = 33.1 M entries.
+Default workload = BASELINE config 2 (the config the headline metric is
+quoted on that fits one GPU): unit-cube surface refined 3x (768 triangles,
+386 nodes), N = 32 time steps, alpha = 1.  One step assembles V (p0 x p0),
+K (p0 x p1; K' is the blockwise-transposed view, not re-counted) and
+D = D2 + curl(V) (p1 x p1) -- E_t (E_x^2 + E_x N_x + N_x^2) = 33.1 M entries.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+                  [--config 2|3|5]
 
-N > 1 runs one process per GPU (torchrun); ranks own contiguous ranges of
-time-difference blocks d.  With --parallel rows (default) the V and K pair
-work is split by balanced test-row ranges over all blocks and the finalize
-kernels store every block into its owner's shard through NVLink peer
-pointers (CUDA IPC; no halo gaps, no data-path collective), D2's row partial
-sums meet in one reduce-scatter (also the fence before the d-local curl
-combine); --parallel d
-splits everything by d (block d depends only on the kernel at gaps d-1, d,
-d+1).  value = all ranks' entries / max-over-ranks device time.  ``--impl reference`` times the reference's CPU algorithm (the
-oracle port, oracle/heatbem_oracle.c, all host threads) on rank 0.
+--config 3 (icosphere L5, N = 64: V + K, 322 GB) and 5 (unit cube L5,
+N = 256: V + K + D, 541 GB) are the scaling configurations: every rank
+assembles its contiguous range of blocks d (window-aligned d-chunks into a
+reused buffer where its range does not fit one GPU).
+
+N > 1 runs one process per GPU (torchrun).  Config 2: the V and K pair work
+is split by balanced test-row ranges over all blocks and the finalize kernels
+store every block into its owner's d-shard through NVLink peer pointers (CUDA
+IPC); D2 is d-sharded (block d needs the kernel at gaps d-1, d, d+1 only) and
+the curl combine is d-local -- no data-path collective.  value = all ranks'
+entries / max-over-ranks device time.
+
+Measurement:
+* roofline: the dominant pair kernel's ISSUED FP64 arithmetic (2 DFMA + DMUL
+  + DADD thread instructions + 512 flop per DMMA warp instruction), counted by
+  an ncu counter pass on the same workload inside this run, divided by the
+  kernel's average launch time measured live with CUDA events, against the
+  FP64 peak measured in-run (DFMA probe); traffic = DRAM bytes per launch
+  from the same ncu pass.  The SURVEY 8(d) work rate (kernel evaluations of
+  the reference formulation per second) is reported beside it, not as a
+  fraction.
+* cpu_baseline: one full config-2 assembly by the oracle port of the
+  reference's algorithm (oracle/heatbem_oracle.c) on all host cores,
+  measured, plus the per-pass sample rate (validates extrapolations).
+* --impl reference: per step one full delta-pass of V, K and D2 and one curl
+  block (every i_t >= 1 pass does the same work), tables built outside the
+  timed region; value = the work-equivalent entries per second; the line
+  also carries one measured full assembly.
 """
 from __future__ import annotations
 
 import argparse
+import csv
 import json
 import os
 import statistics
@@ -38,34 +58,47 @@ sys.path.insert(0, ROOT)
 
 METRIC = "BEM matrix entries assembled/sec (fp64 V/K/D) and % of FP64 roofline"
 UNIT = "entries/s"
-LEVEL, E_T, ALPHA = 3, 32, 1.0
-WORKLOAD = ("BASELINE config 2: unit-cube [0,1]^3 surface refined 3x (768 triangles, 386 nodes), "
-            "N=32 steps, T=1, alpha=1, quadrature (4,4): V p0p0 + K p0p1 (K' = transposed view) + "
-            "D = D2 + alpha^2 curl(V) p1p1")
+CONFIGS = {
+    2: dict(mesh="cube", level=3, E_t=32, alpha=1.0, ops=("V", "K", "D"),
+            text="BASELINE config 2: unit-cube [0,1]^3 surface refined 3x (768 triangles, 386 nodes), N=32 steps, "
+                 "T=1, alpha=1, quadrature (4,4): V p0p0 + K p0p1 (K' = transposed view) + D = D2 + alpha^2 curl(V) "
+                 "p1p1"),
+    3: dict(mesh="sphere", level=5, E_t=64, alpha=0.5, ops=("V", "K"),
+            text="BASELINE config 3: icosphere L5 (20480 triangles, 10242 nodes), N=64 steps, T=1, alpha=0.5, "
+                 "quadrature (4,4): V p0p0 + K p0p1"),
+    5: dict(mesh="cube", level=5, E_t=256, alpha=1.0, ops=("V", "K", "D"),
+            text="BASELINE config 5: unit-cube surface refined 5x (12288 triangles, 6146 nodes), N=256 steps, T=1, "
+                 "alpha=1, quadrature (4,4): V p0p0 + K p0p1 + D = D2 + alpha^2 curl(V) p1p1"),
+}
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def setup():
+def setup(cfg):
     import paper_2102_09811_b200 as hb
 
-    mesh = hb.unit_cube_mesh(LEVEL)
-    tg = hb.TimeGrid(1.0, E_T)
-    params = hb.KernelParams(ALPHA, tg.step, length_scale=mesh.diameter)
+    c = CONFIGS[cfg["config"]]
+    level = cfg.get("level") or c["level"]
+    E_t = cfg.get("E_t") or c["E_t"]
+    mesh = hb.unit_cube_mesh(level) if c["mesh"] == "cube" else hb.generate_icosphere(level)
+    tg = hb.TimeGrid(1.0, E_t)
+    params = hb.KernelParams(c["alpha"], tg.step, length_scale=mesh.diameter)
     return hb, mesh, tg, params
 
 
-def entries_total(mesh, nb):
+def entries_total(mesh, nb, ops):
     E, N = mesh.n_triangles, mesh.n_vertices
-    return nb * (E * E + E * N + N * N)
+    per = {"V": E * E, "K": E * N, "D": N * N}
+    return nb * sum(per[o] for o in ops)
 
 
-def d_range(rank, world, E_t):
-    base, rem = divmod(E_t, world)
-    lo = rank * base + min(rank, rem)
-    return lo, lo + base + (1 if rank < rem else 0)
+def config_dict(cfg, mesh, tg):
+    """The workload description -- identical in both arms."""
+    c = CONFIGS[cfg["config"]]
+    return {"workload": c["text"], "E_x": mesh.n_triangles, "N_x": mesh.n_vertices, "E_t": tg.n_steps,
+            "entries_per_step": entries_total(mesh, tg.n_steps, c["ops"])}
 
 
 # ---------------------------------------------------------------------------
@@ -129,58 +162,207 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline / reference arm: the oracle port of the reference algorithm
+# CPU side: the oracle port of the reference's algorithm (checker only)
 # ---------------------------------------------------------------------------
-def cpu_reference_step(mesh, tg, params, threads):
-    """One bounded sample of the reference algorithm on the config-2 mesh:
-    one full _toeplitz_pass (i_t = 1) of each of V, K, D2 plus the curl
-    combine of one block, extrapolated to the E_t + 1 passes and E_t blocks
-    of a full assembly (every i_t >= 1 pass does identical work)."""
-    import paper_2102_09811_b200 as hb
-    from oracle import oracle as O
+class CpuReference:
+    """The reference's assembly on the host (oracle/heatbem_oracle.c, the
+    port of _toeplitz_pass / _scatter_add / _assemble_operator): problem
+    tables built once, outside every timed region."""
 
-    q = hb.QuadratureConfig()
-    t_pass = {}
-    for op in ("V", "K", "D2"):
+    def __init__(self, mesh, tg, params, threads):
+        import paper_2102_09811_b200 as hb
+        from oracle import oracle as O
+
+        O.build()
+        self.O, self.mesh, self.tg, self.params, self.threads = O, mesh, tg, params, threads
+        q = hb.QuadratureConfig()
+        self.P = {op: O.OracleProblem(mesh, params, q, op, tg.step) for op in ("V", "K", "D2")}
+        E, N = mesh.n_triangles, mesh.n_vertices
+        self.loc = {op: (np.zeros((E, 3 if P.test_p1 else 1, P.shape_rc[1])),
+                         np.zeros((E, 3 if P.test_p1 else 1, P.shape_rc[1]))) for op, P in self.P.items()}
+        rng = np.random.default_rng(0)
+        self.V1, self.D21 = rng.standard_normal((1, E, E)), rng.standard_normal((1, N, N))
+
+    def pass_sample(self):
+        """One full delta-pass (i_t = 1, all rows) of V, K, D2 and the curl
+        combine of one block: 1/(E_t + 1) of the passes and 1/E_t of the
+        curl work of a full assembly.  Returns seconds."""
+        O = self.O
         t0 = time.perf_counter()
-        O.single_pass(mesh, params, q, op, tg.step, 1, n_threads=threads)
-        t_pass[op] = time.perf_counter() - t0
-    E, N = mesh.n_triangles, mesh.n_vertices
-    rng = np.random.default_rng(0)
-    V1, D21 = rng.standard_normal((1, E, E)), rng.standard_normal((1, N, N))
-    t0 = time.perf_counter()
-    O.curl_combine(V1, D21, mesh, params.alpha)
-    t_curl = time.perf_counter() - t0
-    t_full = (tg.n_steps + 1) * sum(t_pass.values()) + tg.n_steps * t_curl
-    return t_full, t_pass, t_curl
+        for op, P in self.P.items():
+            loc, locc = self.loc[op]
+            O.lib().hb_oracle_pass(*P.args(), float(self.tg.step), 0, None, 0, O._ptr(loc), O._ptr(locc),
+                                   self.threads)
+        O.curl_combine(self.V1, self.D21, self.mesh, self.params.alpha)
+        return time.perf_counter() - t0
+
+    def pass_sample_entries(self, entries):
+        """Work-equivalent entries of one pass sample (passes and curl blocks
+        of a full assembly weighted by their measured share)."""
+        return entries / (self.tg.n_steps + 1)
+
+    def full_assembly(self):
+        """The whole assembly of V, K, D2 (E_t + 1 passes each) and D =
+        D2 + curl(V): measured seconds (tables prebuilt)."""
+        O = self.O
+        out = {}
+        t0 = time.perf_counter()
+        for op, P in self.P.items():
+            R, C = P.shape_rc
+            out[op] = np.empty((self.tg.n_steps, R, C))
+            rc = O.lib().hb_oracle_assemble(*P.args(), self.tg.n_steps, self.tg.step, O._ptr(out[op]),
+                                            self.threads)
+            if rc != 0:
+                raise MemoryError("oracle assemble failed")
+        O.curl_combine(out["V"], out["D2"], self.mesh, self.params.alpha)
+        return time.perf_counter() - t0
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    from oracle import oracle as O
-
-    O.build()
-    hb, mesh, tg, params = setup()
+    cfg = {"config": args.config, "level": args.level, "E_t": args.et}
+    hb, mesh, tg, params = setup(cfg)
+    conf = config_dict(cfg, mesh, tg)
     threads = os.cpu_count() or 1
+    if args.config != 2:
+        print(json.dumps({"impl": "reference", "metric": METRIC, "unavailable":
+                          f"config {args.config}: hours of CPU work per step (the CPU baseline is timed on config 2)",
+                          "config": conf}), flush=True)
+        return
+    ref = CpuReference(mesh, tg, params, threads)
+    n_entries = conf["entries_per_step"]
     for _ in range(args.warmup):
-        cpu_reference_step(mesh, tg, params, threads)
-    ts = []
-    for _ in range(args.steps):
-        ts.append(cpu_reference_step(mesh, tg, params, threads)[0])
+        ref.pass_sample()
+    ts = [ref.pass_sample() for _ in range(args.steps)]
     t = statistics.median(ts)
-    n_entries = entries_total(mesh, tg.n_steps)
-    val = n_entries / t
-    sample = (f"per step: one full i_t=1 pass each of V, K, D2 on the config-2 mesh + curl combine of one block "
-              f"(oracle/heatbem_oracle.c, {threads} OpenMP threads), extrapolated to (E_t+1)=33 passes and "
-              f"32 blocks = {n_entries} entries")
+    val = ref.pass_sample_entries(n_entries) / t
+    t_full = ref.full_assembly()
+    sample = (f"per step: one full delta-pass (i_t=1, all rows) each of V, K, D2 on the config-2 mesh + the curl "
+              f"combine of one block (oracle/heatbem_oracle.c, the port of the reference's _toeplitz_pass; "
+              f"{threads} OpenMP threads; tables built outside the timed region) = 1/{tg.n_steps + 1} of a full "
+              f"assembly's passes; value = {n_entries}/{tg.n_steps + 1} work-equivalent entries per step / "
+              f"median step time.  Measured once in the same run: full assembly (V, K, D2, curl) {t_full:.2f} s = "
+              f"{n_entries / t_full:.4g} entries/s")
     out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic (config-2 mesh generated in-run)",
-           "config": {"workload": WORKLOAD, "E_x": mesh.n_triangles, "N_x": mesh.n_vertices, "E_t": tg.n_steps},
-           "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+           "config": conf,
+           "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                            "full_assembly_s": t_full, "full_assembly_value": n_entries / t_full},
            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# ncu counter pass (hardware view of the kernels, inside this run)
+# ---------------------------------------------------------------------------
+NCU_METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+               "sm__sass_thread_inst_executed_op_dfma_pred_on.sum", "sm__sass_thread_inst_executed_op_dmul_pred_on.sum",
+               "sm__sass_thread_inst_executed_op_dadd_pred_on.sum", "sm__inst_executed_pipe_tensor_subpipe_dmma.sum",
+               "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+               "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
+
+
+def ncu_pass(child_mode, kernel_regex, timeout=600):
+    """Run this script's ``--ncu-child MODE`` under ncu (counters only) and
+    return per-launch rows {kernel, metric: value}.  None when ncu is not
+    usable here."""
+    ncu = "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None
+    cmd = [ncu, "--metrics", ",".join(NCU_METRICS), "--clock-control", "none", "--csv", "--print-units", "base",
+           "-k", f"regex:{kernel_regex}", sys.executable, os.path.abspath(__file__), "--ncu-child", child_mode]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    except (subprocess.TimeoutExpired, OSError) as exc:
+        log(f"ncu pass failed: {exc}")
+        return None
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith('"')]
+    if not lines:
+        log("ncu pass produced no rows:", out.stderr[-500:])
+        return None
+    rows = list(csv.reader(lines))
+    h = rows[0]
+    iid, ik, im, iv = h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    launches = {}
+    for r in rows[1:]:
+        if len(r) != len(h):
+            continue
+        d = launches.setdefault(int(r[iid]), {"kernel": r[ik]})
+        try:
+            d[r[im]] = float(r[iv].replace(",", ""))
+        except ValueError:
+            pass
+    return [launches[k] for k in sorted(launches)]
+
+
+def issued_fp64(row):
+    """Issued FP64 flops of one launch: 2 DFMA + DMUL + DADD thread
+    instructions + 512 per DMMA (m8n8k4) warp instruction."""
+    return (2 * row.get("sm__sass_thread_inst_executed_op_dfma_pred_on.sum", 0.0)
+            + row.get("sm__sass_thread_inst_executed_op_dmul_pred_on.sum", 0.0)
+            + row.get("sm__sass_thread_inst_executed_op_dadd_pred_on.sum", 0.0)
+            + 512 * row.get("sm__inst_executed_pipe_tensor_subpipe_dmma.sum", 0.0))
+
+
+def ncu_child(mode):
+    """Workload of the ncu pass: one warm-up and one measured call (the
+    parent keeps the second half of the launches)."""
+    import torch
+
+    if mode == "c2":
+        cfg = {"config": 2}
+        hb, mesh, tg, params = setup(cfg)
+        from paper_2102_09811_b200.assembly import _assemble_operator
+
+        q = hb.QuadratureConfig()
+        for _ in range(2):
+            for code in ((0, False, False, True), (1, False, True, False), (2, True, True, True)):
+                _assemble_operator(*code, mesh, tg, params, q, None)
+            torch.cuda.synchronize()
+    elif mode == "c4":
+        import paper_2102_09811_b200 as hb
+
+        m4 = hb.unit_cube_mesh(4)
+        tg4 = hb.TimeGrid(1.0, 64)
+        p4 = hb.KernelParams(1.0, tg4.step, length_scale=m4.diameter)
+        rng = np.random.default_rng(0)
+        qd = rng.uniform(-1, 1, (64, m4.n_triangles))
+        gd = rng.uniform(-1, 1, (64, m4.n_vertices))
+        X = rng.uniform(0.05, 0.95, (100000, 3))
+        for _ in range(2):
+            hb.represent_grid(qd, gd, X[:8192], m4, tg4, p4, return_device=True)
+            torch.cuda.synchronize()
+
+
+def pair_kernel_hw(rows):
+    """Group the c2 pair launches of the measured (second) call by operator:
+    the V kernels (moment form: touching, near and far launches), then K and
+    D2 (direct kernels, one launch each)."""
+    if not rows:
+        return None
+    half = rows[len(rows) // 2:]
+    groups = {"V": [], "K": [], "D2": []}
+    for r in half:
+        k = r["kernel"]
+        op = "V" if "k_pairs<0" in k else "K" if "k_pairs<1" in k else "D2" if "k_pairs<2" in k else None
+        if op:
+            groups[op].append(r)
+    out = {}
+    for op, rs in groups.items():
+        if not rs:
+            continue
+        t = sum(r.get("gpu__time_duration.sum", 0.0) for r in rs) * 1e-9
+        fl = sum(issued_fp64(r) for r in rs)
+        dram = sum(r.get("dram__bytes_read.sum", 0.0) + r.get("dram__bytes_write.sum", 0.0) for r in rs)
+        w = [r.get("gpu__time_duration.sum", 0.0) for r in rs]
+        pipe = sum(r.get("sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active", 0.0) * x
+                   for r, x in zip(rs, w)) / max(1e-30, sum(w))
+        out[op] = {"launches": len(rs), "ncu_ms": t * 1e3, "issued_fp64_flop": fl, "dram_bytes": dram,
+                   "ncu_issued_tflops": fl / t / 1e12 if t > 0 else None, "fp64_shared_pipe_pct": pipe,
+                   "kernels": sorted({r["kernel"].split("(")[0] for r in rs})}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -200,21 +382,18 @@ def fp64_peak(torch, _native):
     return grid * 256 * iters * 8 * 2 / (s.elapsed_time(e) * 1e-3) / 1e12
 
 
-def load_traffic():
-    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+def hbm_peak():
     try:
-        with open(p) as fh:
-            return json.load(fh)
-    except (OSError, ValueError):
-        return {}
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        return 6459.6, "B200_PROFILING.md fallback"
 
 
-def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd, cpu=True):
+def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd, cpu=True, hw=None, peak=None):
     """The other SURVEY 8 rows on this GPU (device time, CUDA events): the
-    interior potentials of the whole config 4 (register-blocked kernel) and the config-2
-    Dirichlet solve on the blocks just assembled.  Reference times are the
-    SURVEY's measurements of the reference on this container (8 cores)."""
-    import numpy as np
+    whole config-4 representation formula and the config-2 Dirichlet solve
+    on the blocks just assembled, each with its roofline fraction."""
 
     def ev_ms(fn, reps=3):
         fn()
@@ -235,8 +414,6 @@ def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd, cpu=True):
     qd = rng.uniform(-1, 1, (64, m4.n_triangles))
     gd = rng.uniform(-1, 1, (64, m4.n_vertices))
     X = rng.uniform(0.05, 0.95, (100000, 3))
-    # the whole of config 4 through the public call (1e5 points x 64 times,
-    # single + double layer); warm-up on a 256-point slice
     hb.represent_grid(qd, gd, X[:256], m4, tg4, p4, return_device=True)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -246,10 +423,17 @@ def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd, cpu=True):
     torch.cuda.synchronize()
     t_ms = s.elapsed_time(e)
     vals = X.shape[0] * 64
-    out["potentials_c4"] = {"values_per_s": vals / (t_ms * 1e-3), "unit": "values/s (u = V~q - Wg)",
-                            "full_config4_s": t_ms * 1e-3,
-                            "sample": "all 1e5 config-4 points x 64 times (seeded as SURVEY 8(d)), represent_grid",
-                            "cpu_baseline": cpu_potentials(m4, tg4, p4, qd, gd, X) if cpu else None}
+    pot = {"values_per_s": vals / (t_ms * 1e-3), "unit": "values/s (u = V~q - Wg)", "full_config4_s": t_ms * 1e-3,
+           "sample": "all 1e5 config-4 points x 64 times (seeded as SURVEY 8(d)), represent_grid",
+           "cpu_baseline": cpu_potentials(m4, tg4, p4, qd, gd, X) if cpu else None}
+    if hw:   # issued FP64 per point from the ncu pass (8192 points), scaled to 1e5 points
+        fl = sum(issued_fp64(r) for r in hw[len(hw) // 2:])
+        achieved = fl * (X.shape[0] / 8192) / (t_ms * 1e-3) / 1e12
+        pot["roofline"] = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                           "frac": achieved / peak if peak else None,
+                           "definition": "issued FP64 (2 DFMA + DMUL + DADD + 512 per DMMA) counted by ncu on 8192 "
+                                         "points, scaled to 1e5, / the live time of the whole config 4"}
+    out["potentials_c4"] = pot
     V = hb.BlockToeplitzMatrix(Vd)
     Kb = hb.BlockToeplitzMatrix(Kd)
     Mm = hb.assemble_mass(mesh, tg)
@@ -263,9 +447,21 @@ def measure_paths(torch, hb, mesh, tg, params, q, Vd, Kd, cpu=True):
                            right_precond=lambda v: hb.forward_block_solve(V, v))
         info["it"], info["res"] = rep.iterations, rep.residual
 
-    out["solve_c2"] = {"matvec_ms": ev_ms(lambda: hb.apply_toeplitz(V, rhs), reps=10),
-                       "forward_subst_ms": ev_ms(lambda: hb.forward_block_solve(V, rhs), reps=10),
-                       "fgmres_ms": ev_ms(solve), "iterations": info["it"], "residual": info["res"]}
+    mv = ev_ms(lambda: hb.apply_toeplitz(V, rhs), reps=10)
+    fs = ev_ms(lambda: hb.forward_block_solve(V, rhs), reps=10)
+    hbm, hbm_src = hbm_peak()
+    nb, R, C = Vd.shape
+    mv_bytes = nb * R * C * 8 + 2 * rhs.numel() * 8                       # A read once + x, y
+    fs_bytes = sum(k * R * C * 8 for k in range(1, nb + 1)) + R * R * 8 * nb   # history blocks + inverse per step
+    out["solve_c2"] = {"matvec_ms": mv, "forward_subst_ms": fs, "fgmres_ms": ev_ms(solve),
+                       "iterations": info["it"], "residual": info["res"],
+                       "roofline": {"bound": "hbm", "peak": hbm, "unit": "GB/s", "peak_source": hbm_src,
+                                    "matvec_achieved": mv_bytes / (mv * 1e-3) / 1e9,
+                                    "matvec_frac": mv_bytes / (mv * 1e-3) / 1e9 / hbm,
+                                    "forward_subst_achieved": fs_bytes / (fs * 1e-3) / 1e9,
+                                    "forward_subst_frac": fs_bytes / (fs * 1e-3) / 1e9 / hbm,
+                                    "definition": "algorithmic bytes: matvec reads every block once; forward "
+                                                  "substitution step k reads blocks 1..k and (A^0)^-1"}}
     if cpu:
         out["solve_c2"]["cpu_baseline"] = cpu_solve(Vd.cpu().numpy(), rhs.cpu().numpy())
     return out
@@ -275,8 +471,6 @@ def cpu_potentials(m4, tg4, p4, qd, gd, X, n_points=4):
     """The reference algorithm (oracle port of _field_numba._eval_potential,
     all host threads) on a bounded sample: n_points config-4 points x 64 times,
     both potentials."""
-    import numpy as np
-
     from oracle import oracle as O
     from paper_2102_09811_b200.field import _interp_density_np
     from paper_2102_09811_b200.quadrature import rule_tables
@@ -286,9 +480,10 @@ def cpu_potentials(m4, tg4, p4, qd, gd, X, n_points=4):
     XX = np.repeat(X[:n_points], 64, axis=0)
     K = np.tile(np.arange(1, 65), n_points)
     z = np.zeros(len(K))
+    dens = [_interp_density_np(c, m4, hats) for c in (qd, gd)]
     t0 = time.perf_counter()
-    for kind, c in ((0, qd), (1, gd)):
-        O.potential(kind, XX, K, z, z > 0, _interp_density_np(c, m4, hats), qpts, qw, m4.areas, m4.normals,
+    for kind in (0, 1):
+        O.potential(kind, XX, K, z, z > 0, dens[kind], qpts, qw, m4.areas, m4.normals,
                     tg4.step, p4.alpha, p4.delta_eps, p4.rho_eps)
     dt = time.perf_counter() - t0
     return {"values_per_s": len(K) / dt, "cores": os.cpu_count() or 1, "kind": "port",
@@ -309,17 +504,31 @@ def cpu_solve(Vh, rhs_h):
             "cores": os.cpu_count() or 1, "sample": "config-2 V (32 x 768 x 768) and the solve's rhs, numpy"}
 
 
-def run_native(args, rank, world, local_rank):
+def algorithmic_rate(hb, mesh, op, n_gaps, ms):
+    """SURVEY 8(d) work rate: kernel evaluations of the reference formulation per second."""
+    from paper_2102_09811_b200 import workload
+
+    w = workload.operator_work(mesh, op, n_gaps, hb.QuadratureConfig())
+    return {"evaluations": w["n_eval"], "evaluations_per_s": w["n_eval"] / (ms * 1e-3),
+            "reference_flops_per_s": w["flops"] / (ms * 1e-3),
+            "definition": "N_eval = E_t sum_class n_pairs q_class (SURVEY 8(d)); reference formulation "
+                          f"{workload.FLOPS_PER_EVAL[op]} flop per evaluation (erf + exp)"}
+
+
+def run_native_c2(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
+    cfg = {"config": 2, "level": args.level, "E_t": args.et}
     torch.cuda.set_device(local_rank)
-    hb, mesh, tg, params = setup()
-    from paper_2102_09811_b200 import _native, device as hbdev, workload
+    hb, mesh, tg, params = setup(cfg)
+    conf = config_dict(cfg, mesh, tg)
+    from paper_2102_09811_b200 import _native, device as hbdev
     from paper_2102_09811_b200.assembly import _assemble_operator, curl_combine_into
+    from paper_2102_09811_b200 import distributed as Dm
 
     _native.require_cuda()
-    d0, d1 = d_range(rank, world, tg.n_steps)
+    d0, d1 = Dm.block_range(rank, world, tg.n_steps)
     nb = d1 - d0
     q = hb.QuadratureConfig()
     E, N = mesh.n_triangles, mesh.n_vertices
@@ -332,12 +541,9 @@ def run_native(args, rank, world, local_rank):
     rows_mode = world > 1 and args.parallel == "rows"
     if rows_mode:
         # V and K: pair work split by balanced test-row ranges over ALL blocks,
-        # stores into the d-owner's shard over NVLink (peer pointers); D2: row
-        # partial sums + reduce-scatter; the curl combine is d-local
-        from paper_2102_09811_b200 import distributed as Dm
-
-        # peer mappings are set up collectively: if any rank cannot map its
-        # peers (CUDA IPC / peer access), every rank falls back to d-sharding
+        # stores into the d-owner's shard over NVLink (peer pointers).  Peer
+        # mappings are set up collectively: if any rank cannot map its peers
+        # (CUDA IPC / peer access), every rank falls back to d-sharding.
         ok = 1
         try:
             peersV = Dm.PeerShardTable(outV, d0, d1, tg.n_steps)
@@ -351,8 +557,6 @@ def run_native(args, rank, world, local_rank):
     if rows_mode:
         rowsV = Dm.row_partition(Dm.row_weights_mesh(mesh, q, True), world)[rank]
         rowsK = Dm.row_partition(Dm.row_weights_mesh(mesh, q, False), world)[rank]
-        rowsD = Dm.row_partition(Dm.row_weights_mesh(mesh, q, True, skip_perpendicular=True), world)[rank]
-        partD = torch.empty((tg.n_steps, N, N), dtype=torch.float64, device=dev)   # this rank's D2 rows
         dist.barrier()
 
     def step(stats=None):
@@ -362,6 +566,13 @@ def run_native(args, rank, world, local_rank):
                                row_range=rowsV, block_ptrs=peersV.table, stats=st[0])
             _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(0, tg.n_steps),
                                row_range=rowsK, block_ptrs=peersK.table, stats=st[1])
+            # D2 d-sharded: block d needs the kernel at gaps d-1, d, d+1 only (no
+            # collective); the barrier-free d-local curl combine reads this rank's
+            # V shard after all ranks' V stores -- fenced by the device barrier below
+            _assemble_operator(2, True, True, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outD,
+                               stats=st[2])
+            torch.cuda.synchronize()
+            dist.barrier()
         elif stats is None:
             # the three operators on concurrent streams (public API assemble_all)
             hb.assemble_all(mesh, tg, params, q, d_range=(d0, d1), out={"V": outV, "K": outK, "D": outD})
@@ -371,14 +582,6 @@ def run_native(args, rank, world, local_rank):
                                stats=st[0])
             _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(d0, d1), out=outK,
                                stats=st[1])
-        if rows_mode:
-            # D2: this rank's element rows for all blocks, summed into the d-owners'
-            # shards by one reduce-scatter -- which is also the fence after which
-            # every rank's V stores into this shard are complete
-            _assemble_operator(2, True, True, True, mesh, tg, params, q, None, d_range=(0, tg.n_steps),
-                               row_range=rowsD, out=partD, stats=st[2])
-            Dm.reduce_scatter_blocks(partD, outD, d0, d1)
-        else:
             _assemble_operator(2, True, True, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outD,
                                stats=st[2])
         curl_combine_into(tabs, outV, outD, outD, params.alpha)
@@ -389,7 +592,6 @@ def run_native(args, rank, world, local_rank):
     peak = fp64_peak(torch, _native) if rank == 0 else None
 
     # ---- timed region: K steps, events per step, L2 flushed between steps ----
-    stats = [_native.AssemblyStats() for _ in range(3)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -407,20 +609,21 @@ def run_native(args, rank, world, local_rank):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # kernel timing pass (stats sync inside each call; kept out of the headline)
-    for _ in range(max(1, args.steps // 2)):
-        step(stats)
-    torch.cuda.synchronize()
-
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    n_entries = entries_total(mesh, tg.n_steps)   # all ranks together
+    ms_per_step = float(t.item()) / args.steps
+    n_entries = conf["entries_per_step"]   # all ranks together
     value = n_entries / (ms_per_step * 1e-3)
 
+    # ---- kernel timing pass (stats: events around every launch, sync per call) ----
+    stats = [_native.AssemblyStats() for _ in range(3)]
+    n_stat = max(1, args.steps // 2)
+    for _ in range(n_stat):
+        flush.fill_(1)
+        step(stats)
+    torch.cuda.synchronize()
     if rows_mode:
         dist.barrier()
         peersV.close()
@@ -434,19 +637,15 @@ def run_native(args, rank, world, local_rank):
 
     def e2e_step():
         # sequential public calls: V finishes first and its copy-back overlaps K,
-        # K's overlaps D (assemble_all's concurrent streams finish all three
-        # together and leave the 265 MB of copies exposed: slower end to end)
-        hbdev.drop_device_tables(mesh)              # re-upload inputs from pinned host memory
-        # V streams back in work-balanced row slabs as they are assembled
-        # (host_out), K as soon as it is done, D in block chunks as the curl
-        # combine forms them
+        # K's overlaps D; mesh tables re-uploaded from pinned host memory
+        hbdev.drop_device_tables(mesh)
         V = hb.assemble_single_layer(mesh, tg, params, q, d_range=(d0, d1), host_out=pinV,
                                      host_out_slabs=int(os.environ.get("HB_E2E_SLABS", "3")))
         _, ev_v = V.host_copy
         K = hb.assemble_double_layer(mesh, tg, params, q, d_range=(d0, d1), host_out=pinK)
         _, ev_k = K.host_copy
         D = hb.assemble_hypersingular(mesh, tg, params, q, single_layer=V, d_range=(d0, d1), host_out=pinD)
-        _, ev_d = D.host_copy                      # D streamed back in block chunks as the curl forms them
+        _, ev_d = D.host_copy
         for ev in (ev_v, ev_k, ev_d):
             torch.cuda.current_stream().wait_event(ev)
 
@@ -468,97 +667,177 @@ def run_native(args, rank, world, local_rank):
     h2d = Hpin.pinned_bytes
     d2h = (pinV.numel() + pinK.numel() + pinD.numel()) * 8
 
-    # ---- roofline of the dominant kernel: the K pair kernel (k_pairs<1,...>) ----
-    kd0, kd1 = (0, tg.n_steps) if rows_mode else (d0, d1)
-    it_lo, it_hi = max(1, kd0 - 1), kd1
-    n_windows = 0
-    dd = kd0
-    while dd < kd1:   # windows of <= 32 gap slots (csrc/hb_assembly.cu)
-        nd1 = min(kd1, 32 if dd <= 1 else dd + 30)
-        n_windows += 1
-        dd = nd1
-    wK = workload.operator_work(mesh, "K", 1, q)
-    gapsK = (it_hi - it_lo + 1) + 2 * (n_windows - 1)
-    row_frac = (rowsK[1] - rowsK[0]) / E if rows_mode else 1.0
-    flops_per_call = wK["flops"] * gapsK * row_frac   # one call = n_windows launches
-    sK = stats[1]
-    pair_ms_per_call = sK.pair_ms / max(1, args.steps // 2)
-    launches_per_call = sK.pair_launches / max(1, args.steps // 2)
-    achieved = flops_per_call / (pair_ms_per_call * 1e-3) / 1e12
-    shares = {nm: st.pair_ms / max(1e-9, st.pair_ms + st.finalize_ms) for nm, st in zip(("V", "K", "D2"), stats)}
-    launches_step = sum(st.launches for st in stats) / max(1, args.steps // 2) + 1   # + curl (k_curl_tile)
-    traffic = load_traffic().get("k_pairs_K_dram_bytes_per_launch")
-
-    paths = (measure_paths(torch, hb, mesh, tg, params, q, outV, outK, cpu=not args.no_cpu_baseline)
-             if (world == 1 and not args.no_paths) else None)
     if rank != 0:
+        if world > 1:
+            dist.barrier()
         return
     clocks = clk.summary()
+
+    # ---- roofline: issued FP64 of the pair kernels (ncu pass, this run) over live launch times ----
+    live = {nm: {"pair_ms_per_call": st.pair_ms / n_stat, "pair_launches_per_call": st.pair_launches / n_stat,
+                 "finalize_ms_per_call": st.finalize_ms / n_stat}
+            for nm, st in zip(("V", "K", "D2"), stats)}
+    hw = None if (args.no_ncu or world > 1) else pair_kernel_hw(ncu_pass("c2", "k_pairs"))
+    kernels = {}
+    for nm in ("V", "K", "D2"):
+        ent = dict(live[nm])
+        ent["algorithmic"] = algorithmic_rate(hb, mesh, nm, tg.n_steps, live[nm]["pair_ms_per_call"])
+        if hw and nm in hw:
+            h = hw[nm]
+            ach = h["issued_fp64_flop"] / (live[nm]["pair_ms_per_call"] * 1e-3) / 1e12
+            ent.update({"issued_fp64_flop_per_call": h["issued_fp64_flop"], "achieved_tflops": ach,
+                        "frac": ach / peak if peak else None, "ncu_issued_tflops": h["ncu_issued_tflops"],
+                        "ncu_ms": h["ncu_ms"], "fp64_shared_pipe_pct_ncu": h["fp64_shared_pipe_pct"],
+                        "dram_bytes_per_call": h["dram_bytes"], "kernels": h["kernels"]})
+        kernels[nm] = ent
+    dom = max(("V", "K", "D2"), key=lambda nm: live[nm]["pair_ms_per_call"])
+    dk = kernels[dom]
+    n_l = max(1.0, live[dom]["pair_launches_per_call"])
+    roofline = {"bound": "fp64", "kernel": f"pair kernels of {dom} (the longest pair-kernel time of a step)",
+                "achieved": dk.get("achieved_tflops"), "peak": peak, "unit": "TFLOP/s", "frac": dk.get("frac"),
+                "traffic": (dk["dram_bytes_per_call"] / n_l) if "dram_bytes_per_call" in dk else None,
+                "avg_launch_ms": live[dom]["pair_ms_per_call"] / n_l,
+                "peak_source": "measured in-run (hb_fp64_probe DFMA loop; MEASURED_PEAKS.json has no FP64 entry)",
+                "definition": "achieved = issued FP64 flops per call (2 DFMA + DMUL + DADD thread instructions + "
+                              "512 per DMMA warp instruction, counted by an ncu pass over the same workload in this "
+                              "run) / the call's pair-kernel time measured live with CUDA events; traffic = DRAM "
+                              "bytes per launch from the same pass",
+                "source": "ncu counter pass in this run" if hw else "unavailable (ncu pass did not run)",
+                "kernels": kernels}
+    paths = (measure_paths(torch, hb, mesh, tg, params, q, outV, outK, cpu=not args.no_cpu_baseline,
+                           hw=None if args.no_ncu else ncu_pass("c4", "k_represent|k_potential"), peak=peak)
+             if (world == 1 and not args.no_paths) else None)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        from oracle import oracle as O
-
-        O.build()
         threads = os.cpu_count() or 1
-        cpu_reference_step(mesh, tg, params, threads)         # page-in / thread start
-        ts = [cpu_reference_step(mesh, tg, params, threads)[0] for _ in range(3)]
-        cpu = {"value": n_entries / statistics.median(ts), "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": "3 x (one full i_t=1 pass each of V, K, D2 on the config-2 mesh + curl combine of one "
-                         "block), oracle/heatbem_oracle.c with all host threads, extrapolated to the 33 passes / "
-                         "32 blocks of a full assembly"}
+        ref = CpuReference(mesh, tg, params, threads)
+        ref.pass_sample()                                   # page-in / thread start
+        t_pass = statistics.median(ref.pass_sample() for _ in range(3))
+        t_full = ref.full_assembly()
+        cpu = {"value": n_entries / t_full, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": "one full config-2 assembly (V, K, D2: 33 delta-passes each, + the curl combine of the 32 "
+                         f"blocks), measured: {t_full:.2f} s (oracle/heatbem_oracle.c, the port of the reference's "
+                         f"_toeplitz_pass, {threads} OpenMP threads, tables built outside the timed region)",
+               "full_assembly_s": t_full,
+               "pass_sample_value": ref.pass_sample_entries(n_entries) / t_pass,
+               "pass_sample_note": "one delta-pass each of V, K, D2 + one curl block, x (E_t + 1): agrees with the "
+                                   "measured full assembly when the pass work is uniform"}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: BASELINE config-2 mesh and time grid generated in-run (no dataset)",
-        "config": {"workload": WORKLOAD, "E_x": E, "N_x": N, "E_t": tg.n_steps, "entries_per_step": n_entries,
-                   "parallelism": (f"x{world}: V/K/D2 pair work split by balanced test-row ranges over all "
-                                   "blocks; V/K blocks stored into the d-owner's shard over NVLink peer memory, "
-                                   "D2 row partials summed by one NCCL reduce-scatter; curl d-local")
-                   if rows_mode else f"d-sharded x{world} (contiguous time-difference blocks per rank)",
-                   "l2": "flushed between timed steps (256 MiB device write, outside the events)",
-                   "fp64_peak_tflops": peak, "pair_kernel_share": shares},
-        "roofline": {"bound": "fp64", "kernel": "k_pairs<op=K> (double-layer pair kernel)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                     "peak_source": "measured in-run (hb_fp64_probe DFMA loop; MEASURED_PEAKS.json has no FP64 entry)",
-                     "flops_per_launch": flops_per_call / max(1.0, launches_per_call),
-                     "flops_definition": "SURVEY 8(d): N_eval (pairs x points x gaps) x 124 flop",
-                     "note": ("achieved counts the reference formulation's 124 flop per evaluation (erf + exp) "
-                              "over every (pair, point, gap); the fused evaluator executes far fewer FP64 ops per "
-                              "evaluation and skips point chunks whose K weights are exactly zero (coplanar "
-                              "triangles), so frac exceeds 1: it is the work rate against the reference's "
-                              "algorithm. The hardware view of the same kernel (ncu, 'hw') is the FP64 pipe "
-                              "activity and the issued FP64 flop rate"),
-                     "hw": load_traffic().get("k_pairs_K"),
-                     "avg_launch_ms": pair_ms_per_call / max(1.0, launches_per_call),
-                     "traffic": traffic},
+        "config": conf,
+        "parallelism": (f"x{world}: V/K pair work split by balanced test-row ranges over all blocks, stored into the "
+                        "d-owner's shard over NVLink peer memory; D2 and the curl combine d-sharded")
+        if rows_mode else f"d-sharded x{world} (contiguous time-difference blocks per rank)",
+        "l2": "flushed between timed steps (256 MiB device write, outside the events)",
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "public API assemble_single_layer / assemble_double_layer / assemble_hypersingular with "
                         "host_out: mesh tables re-uploaded from pinned host memory and all blocks copied to pinned "
-                        "host memory every step -- V in 3 work-balanced test-row slabs, each slab's copy started "
-                        "on a side stream as soon as its rows are complete, K as soon as it is done, D in 4 block "
-                        "chunks as the "
-                        "curl combine forms them; the step ends when the last copy is done"},
+                        "host memory every step (V in work-balanced test-row slabs as they complete, K when done, D "
+                        "in block chunks as the curl combine forms them); the step ends when the last copy is done"},
         "clocks": clocks,
         "paths": paths,
-        "gpu_launches": int(round(launches_step * args.steps * world)),
+        "gpu_launches": int(round(sum(st.launches for st in stats) / n_stat + 1)) * args.steps * world,
         "impl": "native",
     }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+
+
+def run_native_large(args, rank, world, local_rank):
+    """Configs 3 and 5: every rank assembles its contiguous range of blocks d
+    (block_range) of each operator -- no collective -- in window-aligned
+    d-chunks into reused buffers where the range does not fit one GPU; D per
+    chunk as D2 + curl(V) of the same blocks.  value = all entries / max-over-
+    ranks time of the whole operator set."""
+    import torch
+    import torch.distributed as dist
+
+    cfg = {"config": args.config, "level": args.level, "E_t": args.et}
+    torch.cuda.set_device(local_rank)
+    hb, mesh, tg, params = setup(cfg)
+    conf = config_dict(cfg, mesh, tg)
+    c = CONFIGS[args.config]
+    from paper_2102_09811_b200 import _native, device as hbdev
+    from paper_2102_09811_b200 import distributed as Dm
+    from paper_2102_09811_b200.assembly import _assemble_operator, curl_combine_into
+
+    _native.require_cuda()
+    q = hb.QuadratureConfig()
+    E, N, Et = mesh.n_triangles, mesh.n_vertices, tg.n_steps
+    d0, d1 = Dm.block_range(rank, world, Et)
+    dev = torch.device("cuda", local_rank)
+    tabs = hbdev.device_tables(mesh, q, dev)
+    budget = float(os.environ.get("HB_BENCH_CHUNK_BYTES", 60e9))
+    ch = max(1, int(budget // (E * E * 8)))
+    chunks = [(a, min(d1, a + ch)) for a in range(d0, d1, ch)]
+    bufV = torch.empty((min(ch, d1 - d0), E, E), dtype=torch.float64, device=dev)
+    bufK = torch.empty((min(ch, d1 - d0), E, N), dtype=torch.float64, device=dev)
+    bufD = torch.empty((min(ch, d1 - d0), N, N), dtype=torch.float64, device=dev) if "D" in c["ops"] else None
+
+    def step():
+        for a, b in chunks:
+            n = b - a
+            _assemble_operator(0, False, False, True, mesh, tg, params, q, None, d_range=(a, b), out=bufV[:n])
+            if bufD is not None:
+                _assemble_operator(2, True, True, True, mesh, tg, params, q, None, d_range=(a, b), out=bufD[:n])
+                curl_combine_into(tabs, bufV[:n], bufD[:n], bufD[:n], params.alpha)
+            _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(a, b), out=bufK[:n])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = []
+    gpu = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[0]) if world == 1 else local_rank
+    with ClockSampler(gpu) as clk:
+        for _ in range(args.steps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            step()
+            e.record()
+            e.synchronize()
+            ms.append(s.elapsed_time(e))
+    t = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    if rank != 0:
+        return
+    out = {"metric": METRIC, "value": conf["entries_per_step"] / (ms_per_step * 1e-3), "unit": UNIT,
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": f"synthetic: BASELINE config-{args.config} mesh generated in-run", "config": conf,
+           "parallelism": f"d-sharded x{world}: blocks [d0, d1) per rank in chunks of <= {ch} blocks",
+           "clocks": clk.summary(), "impl": "native"}
     print(json.dumps(out), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("native", "reference"), default="native")
+    ap.add_argument("--config", type=int, choices=(2, 3, 5), default=2)
+    ap.add_argument("--level", type=int, default=None, help="override the mesh refinement level (emulation runs)")
+    ap.add_argument("--et", type=int, default=None, help="override the number of time steps (emulation runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-paths", action="store_true", help="skip the potentials / solve measurements")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the ncu counter pass (roofline from live times only)")
     ap.add_argument("--parallel", choices=("rows", "d"), default="rows",
-                    help="N > 1: split V/K pair work by test rows (peer stores) or everything by d")
+                    help="config 2, N > 1: split V/K pair work by test rows (peer stores) or everything by d")
+    ap.add_argument("--ncu-child", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.ncu_child:
+        ncu_child(args.ncu_child)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -577,7 +856,10 @@ def main():
         if os.environ.get("HB_BENCH_EMULATE"):
             local_rank = 0
     try:
-        run_native(args, rank, world, local_rank)
+        if args.config == 2:
+            run_native_c2(args, rank, world, local_rank)
+        else:
+            run_native_large(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist
