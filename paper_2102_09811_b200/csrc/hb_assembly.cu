@@ -1417,6 +1417,80 @@ __device__ __forceinline__ void fused_blocks_k(const PairArgs &A, const double *
     }
 }
 
+// Fused lane-level V far path (2 lanes per pair): lane (ps, g) evaluates
+// x H at the pair's gaps g + 1, g + 3, g + 5, g + 7 (four interleaved Horner
+// chains) over its point pairs and, when `spec`, the delta = 0 sums of the
+// point pairs q = g mod 2.  Called warp-uniformly.
+__device__ __forceinline__ void far_pp_v(const PairArgs &A, const FarGeom &G, int g, bool pp, bool spec,
+                                         double (&acc)[4], double &s0, double &sc, const double *tab)
+{
+    double cmp[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = cmp[j] = 0.0;
+    s0 = sc = 0.0;
+    double cx[4], ic[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) gap_consts(A, g + 1 + 2 * j, cx[j], ic[j]);
+    const int nq1 = G.nq1;
+    int q = 0;
+    for (int p = 0; p < nq1; ++p) {
+        const double x0 = G.xp[3 * p], x1 = G.xp[3 * p + 1], x2 = G.xp[3 * p + 2];
+        const double wp = G.w[p];
+        for (int r = 0; r < nq1; ++r, ++q) {
+            const double rx = x0 - G.yp[3 * r], ry = x1 - G.yp[3 * r + 1], rz = x2 - G.yp[3 * r + 2];
+            const double rho = sqrt(rx * rx + ry * ry + rz * rz);
+            const double iq = 1.0 / rho;
+            const double wq = wp * G.w[r];
+            double xs[4], fs[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) xs[j] = __dmul_rn(rho, cx[j]);
+            special::eval_nf<4, 4>(xs, [&](int j) { return __dmul_rn(iq, ic[j]); }, fs, tab, kFull);
+            if (pp) {
+                // compensated sum (TwoProd by fma + TwoSum): the point sum of a gap
+                // carries no rounding of its own, so the time second difference
+                // below dmom amplifies only the per-point evaluation errors
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double pr = __dmul_rn(fs[j], wq);
+                    const double pe = fma(fs[j], wq, -pr);
+                    const double sm = __dadd_rn(acc[j], pr);
+                    const double bp = __dsub_rn(sm, acc[j]);
+                    const double er = __dadd_rn(__dsub_rn(acc[j], __dsub_rn(sm, bp)), __dsub_rn(pr, bp));
+                    cmp[j] = __dadd_rn(cmp[j], __dadd_rn(er, pe));
+                    acc[j] = sm;
+                }
+            }
+            if (spec && (q & 1) == g) {
+                const double Aq = rho * A.inv2a2, Bq = A.inva * iq;
+                const double cq = A.step * Bq + Aq;
+                s0 = fma(wq, Aq, s0);
+                sc = fma(wq, cq, sc);
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = __dadd_rn(acc[j], cmp[j]);
+}
+
+// blocks d in [d0, min(d1, dmom)) of a fused V pair from its staged L row
+// Lrow[0] = L0, [1..8] = gaps, [9] = Lcomb0; lane (ps, g): blocks g, g + 2, g + 4, g + 6
+__device__ __forceinline__ void fused_blocks_v(const PairArgs &A, const double *Lrow, int dmom, int64_t slot, int g)
+{
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const int d = g + 2 * h;
+        if (d < A.d0 || d >= A.d1 || d >= dmom) continue;
+        double b;
+        if (d == 0) {
+            b = Lrow[9] + (-Lrow[1]);
+        } else {
+            b = -Lrow[d - 1] + 2.0 * Lrow[d];
+            b = b + (-Lrow[d + 1]);
+        }
+        A.Q[slot * (int64_t)A.nd + (d - A.d0)] = b;
+    }
+}
+
 // delta = 0 sums of a pair without moments (far-batch pairs): L0 / Lc of the staged row
 template <int OP, bool TP1, bool SP1, int NJ, class Geom>
 __device__ __forceinline__ void pair_specials(const PairArgs &A, const Geom &g, int nq, const double ny[3],
@@ -1560,10 +1634,44 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
             stage_far_points<LPP>(M, e, ff, Xs, gk);
             __syncwarp();
             const FarGeom fg{Xs, Xs + n3, W.rw, W.rh, (int)M.n_reg};
+            bool fused = false;
             if constexpr (NIJ == 1) {
-                double mom[16];
-                far_moments_v(A, fg, mom, rmax, gk);
-                __syncwarp();
+                // the pair's largest rho~^2 first: it decides istar, dmom and whether
+                // its per-point gaps fit the fused lane path (<= 8 gaps, 4 per lane)
+                rmax = far_rmax<LPP>(A, fg, gk);
+                const int istar = moment_istar(rmax), dmom = max(2, istar + 1);
+                fused = pv && istar + 1 <= kFusedMaxGap;
+                const bool pp = fused && A.d0 < dmom;
+                const bool pp_any = __any_sync(kFull, pp);
+                double mom[16], rdummy;
+                far_moments_v(A, fg, mom, rdummy, gk);
+                double acc[4], s0, sc;
+                if (pp_any) far_pp_v(A, fg, gk, pp, pp && A.need_special, acc, s0, sc, tab);
+                __syncwarp();   // the staged points are overwritten from here on
+                if (pp_any) {
+                    const double jq = __shfl_sync(kFull, jac, l);
+                    double *Lrow = W.geo + ps * 10;
+                    if (A.need_special) {
+                        s0 += __shfl_xor_sync(kFull, s0, 1);
+                        sc += __shfl_xor_sync(kFull, sc, 1);
+                    }
+                    if (pp) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int i = gk + 1 + 2 * j;
+                            double cxj, icj;
+                            gap_consts(A, i, cxj, icj);
+                            Lrow[i] = jq * (acc[j] * (icj * A.inv2a2));
+                        }
+                        if (A.need_special && gk == 0) {
+                            Lrow[0] = jq * s0;
+                            Lrow[9] = jq * sc;
+                        }
+                    }
+                    __syncwarp();
+                    if (pp) fused_blocks_v(A, Lrow, dmom, (e - A.e0) * M.E_x + ff, gk);
+                    __syncwarp();
+                }
 #pragma unroll
                 for (int k = 0; k < KPL; ++k) Ms[(KPL * gk + k) * NSTR + ps] = pv ? mom[k] : 0.0;
             } else {
@@ -1578,7 +1686,7 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
             const double jf = __shfl_sync(kFull, jac, l);
             if (gk == 0 && pv) {
                 P.jac[ps] = jf;
-                P.rmax[ps] = rmax;
+                P.rmax[ps] = fused ? -1.0 : rmax;   // < 0: no warp-path per-point work left
                 P.dmom[ps] = max(2, moment_istar(rmax) + 1);
                 P.lane[ps] = l;
                 P.slot_f[ps] = (e - A.e0) * M.E_x + ff;
@@ -1591,7 +1699,7 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
             // blocks below each pair's dmom: per-point L, warp per pair
             for (int q = 0; q < npairs; ++q) {
                 const int dmom = P.dmom[q];
-                if (A.d0 >= dmom) continue;
+                if (A.d0 >= dmom || P.rmax[q] < 0.0) continue;
                 const int istar = moment_istar(P.rmax[q]);
                 const int lq = P.lane[q];
                 const int64_t fq = fb + lq;
