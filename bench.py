@@ -640,7 +640,7 @@ def run_native_c2(args, rank, world, local_rank):
         # K's overlaps D; mesh tables re-uploaded from pinned host memory
         hbdev.drop_device_tables(mesh)
         V = hb.assemble_single_layer(mesh, tg, params, q, d_range=(d0, d1), host_out=pinV,
-                                     host_out_slabs=int(os.environ.get("HB_E2E_SLABS", "3")))
+                                     host_out_slabs=int(os.environ.get("HB_E2E_SLABS", "2")))
         _, ev_v = V.host_copy
         K = hb.assemble_double_layer(mesh, tg, params, q, d_range=(d0, d1), host_out=pinK)
         _, ev_k = K.host_copy
