@@ -230,6 +230,17 @@ int hb_toeplitz_apply(int64_t n_blocks, int64_t R, int64_t C, const double *bloc
                       int transpose, int diagonal_only, int64_t n_steps,
                       const double *x_dev, double *y_dev, void *stream);
 
+/* hb_toeplitz_apply with a caller workspace: operators with few output rows
+ * split the tensor-core product over groups of blocks d (partial products
+ * in the workspace, summed in group order -- deterministic) so that the GPU
+ * is full; bytes needed from hb_toeplitz_apply_workspace (0: no split, the
+ * plain hb_toeplitz_apply runs). */
+size_t hb_toeplitz_apply_workspace(int64_t n_blocks, int64_t R, int64_t C, int transpose, int diagonal_only,
+                                   int64_t n_steps);
+int hb_toeplitz_apply_ws(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev,
+                         int transpose, int diagonal_only, int64_t n_steps, const double *x_dev,
+                         double *y_dev, void *workspace_dev, size_t workspace_bytes, void *stream);
+
 /* Partial product of a d-sharded operator: y^k = sum over the LOCAL blocks
  * d in [d_off, d_off + n_blocks), d <= k, of A^d x^{k-d}; summing y over the
  * ranks (one all-reduce) gives apply_toeplitz of the full operator. */

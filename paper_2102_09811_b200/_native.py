@@ -85,7 +85,7 @@ EXPORTED = (
     "hb_toeplitz_apply_range", "hb_curl_workspace", "hb_ipc_export", "hb_ipc_import", "hb_ipc_close",
     "hb_forward_solve", "hb_forward_history", "hb_inv_apply", "hb_represent_grid",
     "hb_project_workspace", "hb_project_data", "hb_p1_mass_solve", "hb_error_sigma", "hb_copy_row_slab_d2h",
-    "hb_represent_grid_elem",
+    "hb_represent_grid_elem", "hb_toeplitz_apply_workspace", "hb_toeplitz_apply_ws",
 )
 
 _lib = None
@@ -117,6 +117,10 @@ def load():
     L.hb_potential.restype = _INT
     L.hb_toeplitz_apply.argtypes = [_I64, _I64, _I64, _P, _INT, _INT, _I64, _P, _P, _P]
     L.hb_toeplitz_apply.restype = _INT
+    L.hb_toeplitz_apply_workspace.argtypes = [_I64, _I64, _I64, _INT, _INT, _I64]
+    L.hb_toeplitz_apply_workspace.restype = ctypes.c_size_t
+    L.hb_toeplitz_apply_ws.argtypes = [_I64, _I64, _I64, _P, _INT, _INT, _I64, _P, _P, _P, ctypes.c_size_t, _P]
+    L.hb_toeplitz_apply_ws.restype = _INT
     L.hb_toeplitz_apply_range.argtypes = [_I64, _I64, _I64, _I64, _P, _INT, _I64, _P, _P, _P]
     L.hb_toeplitz_apply_range.restype = _INT
     L.hb_forward_subst_step.argtypes = [_I64, _I64, _I64, _P, _INT, _I64, _P, _P, _P]

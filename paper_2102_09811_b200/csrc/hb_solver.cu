@@ -5,6 +5,9 @@
 // output rows x 16 time steps and walks the (d, column) space in 32-wide
 // chunks staged through shared memory; every output is a fixed-order sum
 // (d ascending, column ascending), so results are bitwise deterministic.
+#include <algorithm>
+#include <cstdlib>
+
 #include "hb_common.cuh"
 
 namespace hb {
@@ -221,12 +224,22 @@ __device__ __forceinline__ void dmma884s(double &d0, double &d1, double a, doubl
 
 // TR: the transposed product Y[k][c] += sum_r X[k - d][r] A^d[r][c] (A tile staged
 // as [r][c], B fragment B[k = r][n = c]).
+// grid.z > 1 (split-K of operators with few output rows): CTA z takes the
+// input columns [z csz, (z + 1) csz) and writes its partial product to
+// y + z ystride; k_sum_partials adds the partials in z order (deterministic).
 template <bool TR>
 __global__ void __launch_bounds__(kMT) k_toep_mma(const double *__restrict__ blocks, int64_t R, int64_t C,
                                                   int64_t n_steps, const double *__restrict__ x,
-                                                  double *__restrict__ y, int64_t d_off, int64_t n_blocks)
+                                                  double *__restrict__ y, int64_t d_off, int64_t n_blocks,
+                                                  int64_t csz, int64_t ystride)
 {
     const int64_t n_in = TR ? R : C, n_out = TR ? C : R;
+    int64_t c_begin = 0, c_end = n_in;
+    if (gridDim.z > 1) {
+        c_begin = (int64_t)blockIdx.z * csz;
+        c_end = min(n_in, c_begin + csz);
+        y += (int64_t)blockIdx.z * ystride;
+    }
     // x window of a group of 32 blocks d in [db, db + 32): the rows k - d for the
     // tile's steps k_lo + j, i.e. x[k_lo - db - 32 + w], w = 0..95 (row of step j
     // at block d: w = j - (d - db) + 32)
@@ -240,7 +253,7 @@ __global__ void __launch_bounds__(kMT) k_toep_mma(const double *__restrict__ blo
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
     const int64_t dmax = min(k_lo + nst - 1, d_off + n_blocks - 1);
-    for (int64_t c0 = 0; c0 < n_in; c0 += kMC) {
+    for (int64_t c0 = c_begin; c0 < c_end; c0 += kMC) {
         for (int64_t db = d_off; db <= dmax; db += 32) {
             __syncthreads();
             for (int i = tid; i < 96 * kMC; i += kMT) {
@@ -306,12 +319,73 @@ __global__ void __launch_bounds__(kMT) k_toep_mma(const double *__restrict__ blo
 }
 
 static int launch_toep_mma(const double *blocks, int64_t R, int64_t C, int tr, int64_t n_steps, const double *x,
-                           double *y, int64_t d_off, int64_t n_blocks, cudaStream_t st, const char *what)
+                           double *y, int64_t d_off, int64_t n_blocks, cudaStream_t st, const char *what,
+                           int64_t groups = 1, int64_t csz = 0)
 {
-    dim3 g((unsigned)cdiv(tr ? C : R, kMR), (unsigned)cdiv(n_steps, 64));
-    if (tr) k_toep_mma<true><<<g, kMT, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks);
-    else k_toep_mma<false><<<g, kMT, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks);
+    dim3 g((unsigned)cdiv(tr ? C : R, kMR), (unsigned)cdiv(n_steps, 64), (unsigned)groups);
+    const int64_t ystride = n_steps * (tr ? C : R);
+    if (tr) k_toep_mma<true><<<g, kMT, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks, csz, ystride);
+    else k_toep_mma<false><<<g, kMT, 0, st>>>(blocks, R, C, n_steps, x, y, d_off, n_blocks, csz, ystride);
     return cuda_check(cudaGetLastError(), what);
+}
+
+__global__ void k_sum_partials(const double *__restrict__ part, int64_t groups, int64_t n, double *__restrict__ y)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = part[i];
+        for (int64_t z = 1; z < groups; ++z) v += part[z * n + i];
+        y[i] = v;
+    }
+}
+
+// split-K of the tensor-core product for operators with few output rows
+// (< kMmaMinRows, whose row tiles alone cannot fill the GPU): groups of
+// 32-column chunks of the input index, about 12 groups; the split depends on
+// the input length only, so row shards of an operator (RowShardedToeplitz)
+// sum in the same order as the whole operator.  Returns the group count and
+// the columns per group.
+static int64_t toep_groups(int64_t n_in, int64_t n_out, int64_t n_steps, int64_t *csz)
+{
+    (void)n_steps;
+    const int64_t chunks = cdiv(n_in, kMC);
+    *csz = chunks * kMC;
+    if (n_out >= kMmaMinRows || chunks < 2) return 1;
+    static const int64_t target = getenv("HB_TOEP_GROUPS") ? atoll(getenv("HB_TOEP_GROUPS")) : 12;
+    const int64_t per = cdiv(chunks, std::max<int64_t>(1, target));
+    *csz = per * kMC;
+    return cdiv(chunks, per);
+}
+
+extern "C" size_t hb_toeplitz_apply_workspace(int64_t n_blocks, int64_t R, int64_t C, int transpose,
+                                              int diagonal_only, int64_t n_steps)
+{
+    if (diagonal_only || n_blocks < 1 || R < 1 || C < 1 || n_steps < 1) return 0;
+    const int64_t n_out = transpose ? C : R, n_in = transpose ? R : C;
+    int64_t csz;
+    const int64_t groups = toep_groups(n_in, n_out, n_steps, &csz);
+    return groups > 1 ? (size_t)groups * (size_t)(n_steps * n_out) * sizeof(double) : 0;
+}
+
+extern "C" int hb_toeplitz_apply_ws(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int transpose,
+                                    int diagonal_only, int64_t n_steps, const double *x_dev, double *y_dev,
+                                    void *workspace_dev, size_t workspace_bytes, void *stream)
+{
+    const size_t need = hb_toeplitz_apply_workspace(n_blocks, R, C, transpose, diagonal_only, n_steps);
+    if (need == 0 || !workspace_dev || workspace_bytes < need || (!diagonal_only && n_steps > n_blocks) || !blocks_dev ||
+        !x_dev || !y_dev)
+        return hb_toeplitz_apply(n_blocks, R, C, blocks_dev, transpose, diagonal_only, n_steps, x_dev, y_dev, stream);
+    // tensor-core product split over groups of input columns into partials, summed in group order
+    const int64_t n_out = transpose ? C : R, n_in = transpose ? R : C;
+    int64_t csz;
+    const int64_t groups = toep_groups(n_in, n_out, n_steps, &csz);
+    double *part = (double *)workspace_dev;
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = launch_toep_mma(blocks_dev, R, C, transpose, n_steps, x_dev, part, 0, n_blocks, st,
+                             "hb_toeplitz_apply_ws", groups, csz);
+    if (rc) return rc;
+    const int64_t n = n_steps * n_out;
+    k_sum_partials<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 8), 256, 0, st>>>(part, groups, n, y_dev);
+    return cuda_check(cudaGetLastError(), "hb_toeplitz_apply_ws");
 }
 
 extern "C" int hb_toeplitz_apply(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int transpose,

@@ -440,10 +440,16 @@ class RowShardedToeplitz:
     def local_apply(self, x):
         import torch
 
+        from .solver import _workspace
+
         E_t = x.shape[0]
-        y = torch.empty((E_t, self.r1 - self.r0), dtype=torch.float64, device=x.device)
-        _native.call("hb_toeplitz_apply", self.n_blocks, self.r1 - self.r0, self.C, _native.ptr(self.local), 0, 0,
-                     E_t, _native.ptr(x), _native.ptr(y), _native.stream_handle())
+        R = self.r1 - self.r0
+        y = torch.empty((E_t, R), dtype=torch.float64, device=x.device)
+        need = _native.load().hb_toeplitz_apply_workspace(self.n_blocks, R, self.C, 0, 0, E_t)
+        ws = _workspace(x.device, need)
+        _native.call("hb_toeplitz_apply_ws", self.n_blocks, R, self.C, _native.ptr(self.local), 0, 0, E_t,
+                     _native.ptr(x), _native.ptr(y), _native.ptr(ws) if need else None, int(need),
+                     _native.stream_handle())
         return y
 
     def local_history(self, x, k: int):

@@ -71,9 +71,29 @@ def apply_toeplitz(matrix: BlockToeplitzMatrix, x, transpose_blocks: bool = Fals
     if not matrix.diagonal_only and E_t > nb:
         raise ValueError("more time steps than stored blocks")
     y = torch.empty((E_t, n_out), dtype=torch.float64, device=xd.device)
-    _native.call("hb_toeplitz_apply", nb, R, C, _native.ptr(B), int(tr), int(matrix.diagonal_only), E_t,
-                 _native.ptr(xd), _native.ptr(y), _native.stream_handle())
+    L = _native.load()
+    need = L.hb_toeplitz_apply_workspace(nb, R, C, int(tr), int(matrix.diagonal_only), E_t)
+    ws = _workspace(xd.device, need)
+    _native.call("hb_toeplitz_apply_ws", nb, R, C, _native.ptr(B), int(tr), int(matrix.diagonal_only), E_t,
+                 _native.ptr(xd), _native.ptr(y), _native.ptr(ws) if need else None, int(need),
+                 _native.stream_handle())
     return y if was_torch else y.cpu().numpy()
+
+
+_WS: dict = {}
+
+
+def _workspace(device, nbytes: int):
+    """Cached device scratch (grows on demand) for the split Toeplitz product."""
+    import torch
+
+    if nbytes <= 0:
+        return None
+    buf = _WS.get(device)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _WS[device] = buf
+    return buf
 
 
 def _inverse(matrix, tr):
