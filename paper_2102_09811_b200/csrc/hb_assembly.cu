@@ -2297,16 +2297,20 @@ static bool combo_ok(const hb_assembly_desc *a)
 constexpr size_t kCounterBytes = 256;
 
 // moment form: always for the single layer (its accuracy at large d carries
-// into D through the curl transform); for K and D2 when the time grid has
-// enough steps (E_t >= 64) for the per-pair moments to replace many cheap
-// per-point gaps -- below that the direct kernel (hb_pairs_direct.cu) is
-// faster.  Decided by (op, E_t) only, so d-sharded calls of one operator
-// agree bitwise.  HB_MOMENTS=0/1 overrides.
+// into D through the curl transform); for D2 when the time grid has enough
+// steps (E_t >= 64) for the per-pair moments to replace many cheap per-point
+// gaps -- below that the direct kernel (hb_pairs_direct.cu) is faster.  K
+// keeps the direct dual-orientation kernel at every E_t: one F evaluation
+// feeds both orientations there, while its moment form needs the 6 moment
+// sets and 6 combines per pair (B200: c2 1.64 vs 2.97 ms, level 4 / E_t 64
+// 47.1 vs 50.6 ms).  Decided by (op, E_t) only, so d-sharded calls of one
+// operator agree bitwise.  HB_MOMENTS=0/1 overrides for every operator.
 static int use_moments(const hb_assembly_desc *a)
 {
     static const int env = getenv("HB_MOMENTS") ? (atoi(getenv("HB_MOMENTS")) != 0) : -1;
     if (env >= 0) return env;
-    return (a->op == HB_OP_SINGLE_LAYER || a->E_t >= 64) ? 1 : 0;
+    if (a->op == HB_OP_SINGLE_LAYER) return 1;
+    return (a->op == HB_OP_HYPERSINGULAR2 && a->E_t >= 64) ? 1 : 0;
 }
 
 // staging of one test row: every trial element x NIJ x the blocks of one

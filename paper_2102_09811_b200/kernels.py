@@ -6,7 +6,7 @@ antiderivatives (heatbem/kernels.py:27-50):
 
     delta_eps = 1e-14 * h_t        rho_eps = 1e-12 * length_scale
 
-The device kernels (csrc/hb_kernels.cuh) evaluate the same antiderivatives;
+The device kernels (csrc/hb_special.cuh, csrc/hb_assembly.cu) evaluate the same antiderivatives;
 the numpy versions here serve host-side data (projection of boundary data,
 manufactured solutions) and tests.  G^{dtau} and G^{dtau dt} denote the first
 and second temporal antiderivatives of the heat kernel G_alpha.
