@@ -808,6 +808,9 @@ def run_native_large(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
+    del bufV, bufK, bufD
+    torch.cuda.empty_cache()
+    solve = large_solve(args, torch, dist, hb, mesh, tg, params, q, world, dev) if args.config == 5 else None
     if rank != 0:
         return
     out = {"metric": METRIC, "value": conf["entries_per_step"] / (ms_per_step * 1e-3), "unit": UNIT,
@@ -816,7 +819,40 @@ def run_native_large(args, rank, world, local_rank):
            "data": f"synthetic: BASELINE config-{args.config} mesh generated in-run", "config": conf,
            "parallelism": f"d-sharded x{world}: blocks [d0, d1) per rank in chunks of <= {ch} blocks",
            "clocks": clk.summary(), "impl": "native"}
+    if solve is not None:
+        out["solve"] = solve
     print(json.dumps(out), flush=True)
+
+
+def large_solve(args, torch, dist, hb, mesh, tg, params, q, world, dev):
+    """Config 5's Dirichlet solve (distributed.dirichlet_solve_row_sharded):
+    V and K row-sharded across the ranks (peer stores), rhs = 1/2 M g + K g
+    with one all-gather, FGMRES + forward substitution with the density
+    all-gathers (NCCL).  Needs the V and K row shards resident: skipped when
+    they do not fit (one GPU: 309 + 155 GB).  Times are device times, max over
+    ranks; one run (the assembly inside is the same work as the timed step)."""
+    from paper_2102_09811_b200 import distributed as Dm
+
+    E, N, Et = mesh.n_triangles, mesh.n_vertices, tg.n_steps
+    need = Et * E * (E + N) * 8 / world * 1.08 + 20e9      # shards + staging / tables headroom
+    total = torch.cuda.get_device_properties(dev).total_memory
+    if need > total and not os.environ.get("HB_BENCH_EMULATE"):
+        return {"skipped": f"V + K row shards need {need / 1e9:.0f} GB per rank at N={world} "
+                           f"(device: {total / 1e9:.0f} GB); run with --gpus >= 4"}
+    datum = hb.HeatKernelDatum((1.5, 1.5, 1.5), 1.0, 0.1)   # G(x - y0, t + 0.1): BASELINE config 2/5 data
+    tm = {}
+    if world > 1:
+        dist.barrier()
+    x, rep, _ = Dm.dirichlet_solve_row_sharded(mesh, tg, params, q, datum, rel_tol=1e-10, timings=tm)
+    keys = ("assemble_V", "assemble_K", "rhs", "solve")
+    t = torch.tensor([tm[k] for k in keys], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    res = {k + "_ms": float(v) for k, v in zip(keys, t.tolist())}
+    res.update({"iterations": rep.iterations, "residual": rep.residual, "converged": rep.converged,
+                "layout": f"V, K row-sharded x{world} (rows block_range(rank)); rhs and density all-gathers",
+                "x_norm": float(torch.linalg.norm(x))})
+    return res
 
 
 def main():

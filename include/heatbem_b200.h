@@ -128,6 +128,21 @@ typedef struct {
      * reduce-scatter); contiguous blocks only. */
     int64_t row_begin, row_end;
     double *const *block_ptrs_dev;
+    /* Row-sharded destination (the solve operator's layout, SURVEY 8(e):
+     * rank k holds rows [bounds[k], bounds[k+1]) of every block).  With
+     * n_row_shards > 0 (p0 test functions only; exclusive with
+     * block_ptrs_dev) entry (d, r, c) is written at
+     *   row_shard_ptrs_dev[k] + ((d - d_begin) (bounds[k+1] - bounds[k])
+     *                            + r - bounds[k]) C + c,
+     * bounds = row_shard_bounds_dev (n_row_shards + 1 ascending device
+     * int64 values, bounds[0] = 0, bounds[n] = R), pointers typically the
+     * peers' shards mapped with hb_ipc_import.  The finalize stores ARE the
+     * exchange: V's mirrored entries land in the owner of their row, so
+     * ranks splitting the pair work by any row ranges fill the row shards
+     * bitwise as one GPU fills the whole blocks. */
+    int64_t n_row_shards;
+    const int64_t *row_shard_bounds_dev;
+    double *const *row_shard_ptrs_dev;
 } hb_assembly_desc;
 
 /* bytes of staging for one test-row chunk (the minimum) and for all rows */

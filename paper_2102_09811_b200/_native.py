@@ -61,6 +61,7 @@ class AssemblyDesc(ctypes.Structure):
         ("blocks_dev", _P), ("workspace_dev", _P), ("workspace_bytes", ctypes.c_size_t),
         ("stats", ctypes.POINTER(AssemblyStats)),
         ("row_begin", _I64), ("row_end", _I64), ("block_ptrs_dev", _P),
+        ("n_row_shards", _I64), ("row_shard_bounds_dev", _P), ("row_shard_ptrs_dev", _P),
     ]
 
 

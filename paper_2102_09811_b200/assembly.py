@@ -332,7 +332,7 @@ def release_workspaces():
 def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, mesh, timegrid,
                        params: KernelParams, config: QuadratureConfig, instrumentation,
                        d_range=None, device=None, workspace_bytes=None, stream=None, stats=None, out=None,
-                       row_range=None, block_ptrs=None):
+                       row_range=None, block_ptrs=None, row_shards=None):
     """Blocks [d0, d1) of one operator.  ``row_range`` restricts the test rows
     and ``block_ptrs`` (int64 device tensor of d1 - d0 addresses) redirects
     block d to block_ptrs[d - d0] (row-parallel assembly, distributed.py);
@@ -349,7 +349,15 @@ def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, 
     R = N_x if test_p1 else E_x
     C = N_x if trial_p1 else E_x
     dev = tabs.device
-    if block_ptrs is not None:
+    if row_shards is not None:
+        if out is not None or block_ptrs is not None or test_p1:
+            raise ValueError("row_shards: p0 test functions, no out / block_ptrs")
+        bounds, ptrs = row_shards
+        if (bounds.dtype != torch.int64 or ptrs.dtype != torch.int64 or bounds.device != dev
+                or ptrs.device != dev or bounds.numel() != ptrs.numel() + 1):
+            raise ValueError("row_shards = (bounds (n + 1,), ptrs (n,)) int64 device tensors")
+        blocks = None
+    elif block_ptrs is not None:
         if out is not None:
             raise ValueError("out and block_ptrs are exclusive")
         if tuple(block_ptrs.shape) != (d1 - d0,) or block_ptrs.dtype != torch.int64 or block_ptrs.device != dev:
@@ -369,6 +377,9 @@ def _assemble_operator(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, 
     a.blocks_dev = blocks.data_ptr() if blocks is not None else None
     if block_ptrs is not None:
         a.block_ptrs_dev = block_ptrs.data_ptr()
+    if row_shards is not None:
+        a.n_row_shards = row_shards[1].numel()
+        a.row_shard_bounds_dev, a.row_shard_ptrs_dev = row_shards[0].data_ptr(), row_shards[1].data_ptr()
     if row_range is not None:
         r0, r1 = int(row_range[0]), int(row_range[1])
         if not (0 <= r0 < r1 <= E_x):

@@ -2029,13 +2029,23 @@ struct FinArgs {
     int star_max;
     const int64_t *tile_eptr, *tile_elem;   // curl tile plan (32-node tiles)
     const int32_t *star_pos;
+    int nrs;                                // row-sharded destination: shards, bounds, base pointers
+    const int64_t *rs_bounds;
+    double *const *rs_ptrs;
 };
 
-// destination of block d - d_begin = b: the caller's per-block pointer (another
-// GPU's memory over NVLink in a row-parallel run) or the contiguous blocks
-__device__ __forceinline__ double *fin_block(const FinArgs &F, int64_t b)
+// address of entry (row, col) of block d - d_begin = b: the caller's per-block
+// pointer (another GPU's memory over NVLink in a d-sharded row-parallel run),
+// the owner of the row in a row-sharded run, or the contiguous blocks
+__device__ __forceinline__ double *fin_addr(const FinArgs &F, int64_t b, int64_t row, int64_t col)
 {
-    return F.bptr ? F.bptr[b] : F.out + b * F.R * F.C;
+    if (F.nrs > 0) {
+        int k = 0;   // owner of the row: <= 8-ish shards, linear scan of cached bounds
+        while (k + 1 < F.nrs && row >= __ldg(F.rs_bounds + k + 1)) ++k;
+        const int64_t lo = __ldg(F.rs_bounds + k), rows = __ldg(F.rs_bounds + k + 1) - lo;
+        return F.rs_ptrs[k] + (b * rows + (row - lo)) * F.C + col;
+    }
+    return (F.bptr ? F.bptr[b] : F.out + b * F.R * F.C) + row * F.C + col;
 }
 
 // V (p0 x p0, symmetric): tile of 4 rows x 32 columns x 32 blocks through smem;
@@ -2060,7 +2070,7 @@ __global__ void __launch_bounds__(256) k_fin_p0p0(const FinArgs F)
             const int64_t e = eb + el, f = f0 + fl;
             if (e < F.e1 && f < F.E_x && f >= e && dl < ndc) {
                 const int64_t b = F.d0 + dc + dl - F.d_begin;
-                fin_block(F, b)[e * F.C + f] = tile[el][fl][dl];
+                *fin_addr(F, b, e, f) = tile[el][fl][dl];
             }
         }
         for (int idx = tid; idx < 4 * 32 * 32; idx += 256) {
@@ -2068,7 +2078,7 @@ __global__ void __launch_bounds__(256) k_fin_p0p0(const FinArgs F)
             const int64_t e = eb + el, f = f0 + fl;
             if (e < F.e1 && f < F.E_x && f > e && dl < ndc) {
                 const int64_t b = F.d0 + dc + dl - F.d_begin;
-                fin_block(F, b)[f * F.C + e] = tile[el][fl][dl];
+                *fin_addr(F, b, f, e) = tile[el][fl][dl];
             }
         }
         __syncthreads();
@@ -2101,7 +2111,7 @@ __global__ void __launch_bounds__(256) k_fin_p0p1(const FinArgs F)
             const int64_t n = n0 + lane;
             if (n < F.N_x) {
                 const int64_t b = F.d0 + dc + dl - F.d_begin;
-                fin_block(F, b)[e * F.C + n] = tile[lane][dl];
+                *fin_addr(F, b, e, n) = tile[lane][dl];
             }
         }
         __syncthreads();
@@ -2479,8 +2489,15 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
                   (long long)r1);
         return HB_ERR_INVALID;
     }
-    if (!a->blocks_dev && !a->block_ptrs_dev) {
-        set_error("hb_assemble: no output (blocks_dev and block_ptrs_dev are NULL)");
+    if (a->n_row_shards < 0 ||
+        (a->n_row_shards > 0 && (a->test_p1 || a->block_ptrs_dev || !a->row_shard_bounds_dev ||
+                                 !a->row_shard_ptrs_dev))) {
+        set_error("hb_assemble: row-sharded output needs p0 test functions, bounds and pointers, and no "
+                  "block_ptrs_dev");
+        return HB_ERR_INVALID;
+    }
+    if (!a->blocks_dev && !a->block_ptrs_dev && a->n_row_shards == 0) {
+        set_error("hb_assemble: no output (blocks_dev, block_ptrs_dev and row shards all absent)");
         return HB_ERR_INVALID;
     }
     if (a->test_p1 && a->trial_p1 &&
@@ -2573,6 +2590,9 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
             F.Q = A.Q;
             F.out = a->blocks_dev;
             F.bptr = a->block_ptrs_dev;
+            F.nrs = (int)a->n_row_shards;
+            F.rs_bounds = a->row_shard_bounds_dev;
+            F.rs_ptrs = a->row_shard_ptrs_dev;
             F.E_x = m->E_x; F.N_x = m->N_x; F.R = R; F.C = C; F.e0 = e0; F.e1 = e1;
             F.d0 = (int)d0; F.nd = nd_w; F.d_begin = (int)a->d_begin;
             F.star_indptr = m->star_indptr_dev; F.star_elem = m->star_elem_dev;

@@ -144,6 +144,68 @@ def exchange_shard_meta(meta, group=None):
     return out
 
 
+def map_peer_shards(local, extent, group=None):
+    """Every rank's shard address in this process: each rank exports its
+    shard (CUDA IPC, hb_ipc_export), the handles and ``extent`` (the shard's
+    (lo, hi) range) are all-gathered, and peer shards are mapped
+    (hb_ipc_import; peer access over NVLink).  Returns (addresses by rank --
+    0 for an empty shard --, extents by rank, [(mapped address, offset)] to
+    hand to hb_ipc_close).  Collective: every rank calls it, empty shards
+    (more ranks than blocks or rows) included."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if extent[1] > extent[0] and local.numel() > 0:
+        h = (ctypes.c_char * 64)()
+        off = ctypes.c_int64()
+        _native.call("hb_ipc_export", local.data_ptr(), h, ctypes.byref(off))
+        meta = (bytes(h), off.value) + tuple(extent)
+    else:
+        meta = (None, 0) + tuple(extent)
+    metas = exchange_shard_meta(meta, group)
+    addrs, opened = [], []
+    for r, (hr, o, a, b) in enumerate(metas):
+        if r == rank:
+            addrs.append(local.data_ptr() if meta[0] is not None else 0)
+        elif hr is None or b <= a:
+            addrs.append(0)
+        else:
+            p = ctypes.c_void_p()
+            _native.call("hb_ipc_import", hr, o, ctypes.byref(p))
+            opened.append((p.value, o))
+            addrs.append(p.value)
+    return addrs, [(m[2], m[3]) for m in metas], opened
+
+
+class PeerRowShards:
+    """Row-sharded destination of an assembly (hb_assembly_desc.row_shard_*):
+    rank k holds rows [bounds[k], bounds[k+1]) of every block; ``bounds`` and
+    ``ptrs`` (int64 device tensors) are what the finalize kernels store
+    through -- peer shards mapped by CUDA IPC.  ``close()`` unmaps."""
+
+    def __init__(self, local, r0: int, r1: int, n_rows: int, group=None):
+        import torch
+
+        self._L = _native.load()
+        addrs, ranges, self._opened = map_peer_shards(local, (r0, r1), group)
+        bounds = [0]
+        for a, b in ranges:
+            if a != bounds[-1]:
+                raise ValueError("row shards must be contiguous and in rank order")
+            bounds.append(b)
+        if bounds[-1] != n_rows:
+            raise ValueError("row shards do not cover every row")
+        self.bounds = torch.as_tensor(np.array(bounds, dtype=np.int64), device=local.device)
+        self.ptrs = torch.as_tensor(np.array(addrs, dtype=np.int64), device=local.device)
+
+    def close(self):
+        for pv, o in self._opened:
+            self._L.hb_ipc_close(pv, o)
+        self._opened = []
+
+
 class PeerShardTable:
     """Per-block addresses of a d-sharded operator across ranks: every rank
     exports its shard (CUDA IPC, hb_ipc_export), the metadata is all-gathered
@@ -158,30 +220,9 @@ class PeerShardTable:
         import torch.distributed as dist
 
         self._L = _native.load()
-        rank = dist.get_rank(group) if dist.is_initialized() else 0
         block_bytes = int(np.prod(tuple(local.shape[1:]))) * 8   # valid for an empty shard too
-        if d1 > d0 and local.numel() > 0:
-            h = (ctypes.c_char * 64)()
-            off = ctypes.c_int64()
-            _native.call("hb_ipc_export", local.data_ptr(), h, ctypes.byref(off))
-            meta = (bytes(h), off.value, d0, d1)
-        else:
-            # an empty d-shard (more ranks than blocks): nothing to map, but the
-            # collective below still runs on every rank
-            meta = (None, 0, d0, d1)
-        metas = exchange_shard_meta(meta, group)
-        bases, self._opened = [], []
-        for r, (hr, o, a, b) in enumerate(metas):
-            if r == rank:
-                bases.append((local.data_ptr() if meta[0] is not None else 0, a, b))
-                continue
-            if hr is None or b <= a:
-                bases.append((0, a, b))
-                continue
-            p = ctypes.c_void_p()
-            _native.call("hb_ipc_import", hr, o, ctypes.byref(p))
-            self._opened.append((p.value, o))
-            bases.append((p.value, a, b))
+        addrs, ranges, self._opened = map_peer_shards(local, (d0, d1), group)
+        bases = [(addr, a, b) for addr, (a, b) in zip(addrs, ranges)]
         self.table = torch.as_tensor(block_pointer_table(bases, n_blocks, block_bytes), device=local.device)
 
     def close(self):
@@ -231,6 +272,50 @@ def assemble_row_parallel(op: int, test_p1: bool, trial_p1: bool, symmetric: boo
     finally:
         peers.close()
     return ShardedToeplitz(local, d0, d1, E_t, group)
+
+
+def assemble_row_sharded(op: int, test_p1: bool, trial_p1: bool, symmetric: bool, mesh, timegrid, params,
+                         config, group=None, workspace_bytes=None, d_range=None):
+    """The solve operator's layout: rank r holds rows
+    block_range(r, world, R) of every block, as a RowShardedToeplitz.  The
+    pair work is split by balanced test-row ranges (upper-triangle weights for
+    symmetric V) and the finalize kernels store every entry into the owner of
+    its row -- V's mirrored entries into peer shards over NVLink (CUDA IPC):
+    no halo, no data-path collective, and the shards are bitwise the rows of
+    the 1-GPU blocks.  p0 test functions (V, K)."""
+    import torch
+    import torch.distributed as dist
+
+    from .assembly import _assemble_operator
+
+    if test_p1:
+        raise ValueError("row-sharded assembly needs p0 test functions (p1 rows accumulate over elements)")
+    E_t = timegrid.n_steps
+    d0, d1 = (0, E_t) if d_range is None else (int(d_range[0]), int(d_range[1]))
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    E_x, N_x = mesh.n_triangles, mesh.n_vertices
+    R, C = E_x, (N_x if trial_p1 else E_x)
+    r0, r1 = block_range(rank, world, R)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    local = torch.empty((d1 - d0, r1 - r0, C), dtype=torch.float64, device=dev)
+    if world == 1:
+        _assemble_operator(op, test_p1, trial_p1, symmetric, mesh, timegrid, params, config, None,
+                           d_range=(d0, d1), out=local, workspace_bytes=workspace_bytes)
+        return RowShardedToeplitz(local, 0, R, R, group)
+    peers = PeerRowShards(local, r0, r1, R, group)
+    work = (row_partition(row_weights_mesh(mesh, config, symmetric), world)[rank] if symmetric else (r0, r1))
+    dist.barrier(group)                      # every shard allocated and mapped
+    try:
+        if work[1] > work[0]:
+            _assemble_operator(op, test_p1, trial_p1, symmetric, mesh, timegrid, params, config, None,
+                               d_range=(d0, d1), row_range=work, row_shards=(peers.bounds, peers.ptrs),
+                               workspace_bytes=workspace_bytes)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group)                  # every rank's stores into every shard are done
+    finally:
+        peers.close()
+    return RowShardedToeplitz(local, r0, r1, R, group)
 
 
 def reduce_scatter_blocks(partial, local, d0: int, d1: int, group=None):
@@ -607,3 +692,48 @@ def represent_grid_sharded(w, u, xs, mesh, timegrid, params, config=None, group=
         a, b = block_range(r, world, M)
         rows.append(parts[r][: b - a])
     return torch.cat(rows).to(local.device)
+
+
+def dirichlet_solve_row_sharded(mesh, timegrid, params, config, datum, group=None, rel_tol: float = 1e-10,
+                                workspace_bytes=None, timings=None):
+    """The Dirichlet problem of BASELINE config 2/5 across the ranks of
+    ``group`` (reference study.py:96-136, solver.py:47-73 / 165-184):
+
+      1. V and K row-sharded (``assemble_row_sharded``: balanced pair work,
+         finalize stores into the row owners' shards over NVLink);
+      2. g = the X10 projection of ``datum`` (device, replicated: every rank
+         projects the same data), rhs rows = 1/2 (M g)[rows] + K[rows] g,
+         ONE all-gather of the rhs rows; K is dropped;
+      3. FGMRES right-preconditioned by forward substitution on the row
+         shards: one all-gather of the density rows per matvec and one of
+         h^k (R values) per forward-substitution step -- the only
+         collectives of the data path.
+
+    Returns (x, SolveReport, V rows); ``timings`` (dict) receives the device
+    times (ms, max over ranks is the caller's business) of the phases."""
+    import torch
+
+    from .assembly import assemble_mass
+    from .field import project_to_space
+    from .solver import apply_toeplitz
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)   # noqa: E731
+    marks = [ev()]
+    marks[0].record()
+    V = assemble_row_sharded(0, False, False, True, mesh, timegrid, params, config, group, workspace_bytes)
+    marks.append(ev()); marks[-1].record()
+    K = assemble_row_sharded(1, False, True, False, mesh, timegrid, params, config, group, workspace_bytes)
+    marks.append(ev()); marks[-1].record()
+    g = project_to_space(datum, mesh, timegrid, "X10", return_device=True)
+    Mg = apply_toeplitz(assemble_mass(mesh, timegrid), g)
+    rhs_rows = 0.5 * Mg[:, K.r0:K.r1] + K.local_apply(g.contiguous())
+    rhs = V.gather_rows(rhs_rows.contiguous())
+    del K
+    marks.append(ev()); marks[-1].record()
+    x, rep = V.solve(rhs, rel_tol=rel_tol)
+    marks.append(ev()); marks[-1].record()
+    if timings is not None:
+        torch.cuda.synchronize()
+        for name, a, b in (("assemble_V", 0, 1), ("assemble_K", 1, 2), ("rhs", 2, 3), ("solve", 3, 4)):
+            timings[name] = marks[a].elapsed_time(marks[b])
+    return x, rep, V
