@@ -121,7 +121,9 @@ struct RegularGeom {
     int nq1;
     __device__ void point(int q, double x[3], double y[3], double &wq, double ht[3], double hs[3]) const
     {
-        const int p = q / nq1, r = q - p * nq1;
+        // p = q / nq1 without the integer division: (q + 1/2) / nq1 is at least
+        // 1/(2 nq1) away from an integer, far above the float rounding
+        const int p = __float2int_rz(((float)q + 0.5f) * __frcp_rn((float)nq1)), r = q - p * nq1;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             x[c] = __ldg(xp + 3 * p + c);
@@ -810,17 +812,29 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
     if (SYM) fb = max(fb, e);
     if (fb >= fe) return;
     const int64_t t_lo = __ldg(M.tn_indptr_dev + e), t_hi = __ldg(M.tn_indptr_dev + e + 1);
-    double ce[3];
-    for (int c = 0; c < 3; ++c) ce[c] = __ldg(M.centroids_dev + 3 * e + c);
-    const double de = __ldg(M.diameters_dev + e);
-
-    for (int64_t f = fb; f < fe; ++f) {
-        // touching pairs belong to the singular path
-        if (touching_pos(M, t_lo, t_hi, f) >= 0) continue;
+    // classify the segment lane-parallel (lane l: trial fb + l): touching pairs
+    // belong to the singular path; near/far by the exact IEEE test
+    unsigned todo, nearm;
+    {
+        const int64_t f = fb + lane;
+        bool ok = false, nr = false;
+        if (f < fe) {
+            double ce[3];
+            for (int c = 0; c < 3; ++c) ce[c] = __ldg(M.centroids_dev + 3 * e + c);
+            ok = touching_pos(M, t_lo, t_hi, f) < 0;
+            nr = ok && near_test(M, ce, __ldg(M.diameters_dev + e), f);
+        }
+        todo = __ballot_sync(kFull, ok);
+        nearm = __ballot_sync(kFull, nr);
+    }
+    while (todo) {
+        const int bit = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t f = fb + bit;
         const int64_t slot = (e - A.e0) * M.E_x + f;
         const double jac = pair_jac<OP>(A, e, f);
         if (OP == 2 && jac == 0.0) continue;   // n_x.n_y == 0: no contribution (finalize skips it)
-        const bool near = near_test(M, ce, de, f);
+        const bool near = (nearm >> bit) & 1u;
         RegularGeom g;
         const int nq1 = near ? (int)M.n_near : (int)M.n_reg;
         const double *pts = near ? M.near_pts_dev : M.reg_pts_dev;
@@ -849,16 +863,35 @@ __device__ __forceinline__ void regular_item_dual(const PairArgs &A, int64_t e, 
     const int64_t fe = min(fb + A.seg_len, M.E_x);
     if (fb >= fe) return;
     const int64_t t_lo = __ldg(M.tn_indptr_dev + e), t_hi = __ldg(M.tn_indptr_dev + e + 1);
-    for (int64_t f = fb; f < fe; ++f) {
-        const bool f_in = f >= A.e0 && f < A.e1;
-        if (f < e && f_in) continue;                           // the canonical pair (f, e) belongs to row f
-        if (touching_pos(M, t_lo, t_hi, f) >= 0) continue;     // touching pairs: singular path (f == e too)
+    // classify the segment lane-parallel (lane l: trial fb + l); the near test
+    // of the canonical pair (a, b) equals that of (e, f) bitwise (squares of
+    // negated differences, symmetric max)
+    unsigned todo, nearm;
+    {
+        const int64_t f = fb + lane;
+        bool ok = false, nr = false;
+        if (f < fe) {
+            const bool f_in = f >= A.e0 && f < A.e1;
+            ok = !(f < e && f_in)                              // the canonical pair (f, e) belongs to row f
+                 && touching_pos(M, t_lo, t_hi, f) < 0;        // touching pairs: singular path (f == e too)
+            if (ok) {
+                const int64_t a = f > e ? e : f, b = f > e ? f : e;
+                double ca[3];
+                for (int c = 0; c < 3; ++c) ca[c] = __ldg(M.centroids_dev + 3 * a + c);
+                nr = near_test(M, ca, __ldg(M.diameters_dev + a), b);
+            }
+        }
+        todo = __ballot_sync(kFull, ok);
+        nearm = __ballot_sync(kFull, nr);
+    }
+    while (todo) {
+        const int bit = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t f = fb + bit;
         const int64_t a = f > e ? e : f, b = f > e ? f : e;
         const int64_t slot_f = (a >= A.e0 && a < A.e1) ? (a - A.e0) * M.E_x + b : -1;   // test a, trial b
         const int64_t slot_r = (b >= A.e0 && b < A.e1) ? (b - A.e0) * M.E_x + a : -1;   // test b, trial a
-        double ca[3];
-        for (int c = 0; c < 3; ++c) ca[c] = __ldg(M.centroids_dev + 3 * a + c);
-        const bool near = near_test(M, ca, __ldg(M.diameters_dev + a), b);
+        const bool near = (nearm >> bit) & 1u;
         RegularGeom g;
         const int nq1 = near ? (int)M.n_near : (int)M.n_reg;
         const double *pts = near ? M.near_pts_dev : M.reg_pts_dev;
