@@ -149,6 +149,27 @@ typedef struct {
 size_t hb_assemble_min_workspace(const hb_mesh_desc *mesh, const hb_assembly_desc *a);
 size_t hb_assemble_full_workspace(const hb_mesh_desc *mesh, const hb_assembly_desc *a);
 
+/* Fused single layer + hypersingular operator (heatbem assembly.py:337-361,
+ * assemble_hypersingular without a given single_layer; replaces the
+ * assemble_single_layer + hypersingular_from_single_layer sequence,
+ * assembly.py:314-334).  d2 describes D2 (op HB_OP_HYPERSINGULAR2, p1 x p1,
+ * symmetric, all rows, contiguous blocks); its blocks_dev receives
+ * D = D2 + alpha^2 sum_o T_o^T V T_o, its workspace holds the staging of
+ * BOTH operators for a test-row chunk (>= hb_assemble_vd_min_workspace).
+ * V and D2 are assembled in the same row chunks and the p1 x p1 finalize
+ * adds alpha^2 (curl_ei . curl_fj) V_ef to each pair (e, f >= e) as it
+ * accumulates D2, so V is never re-read for the curl transform.
+ * V_blocks_dev (nullable): V of the same blocks, p0 x p0 -- bitwise the
+ * blocks hb_assemble gives.  curls_dev: (E_x, 3, 3) surface curls,
+ * curl of hat i on e = (v_{i+1} - v_{i+2}) / (2 area_e).
+ * The memory-lean path (D without V's blocks: NULL V_blocks_dev); when V is
+ * kept anyway, hb_assemble + hb_curl_combine on separate streams is faster
+ * (the fused finalize loads twice as much as the plain p1 x p1 one). */
+size_t hb_assemble_vd_min_workspace(const hb_mesh_desc *mesh, const hb_assembly_desc *d2);
+size_t hb_assemble_vd_full_workspace(const hb_mesh_desc *mesh, const hb_assembly_desc *d2);
+int hb_assemble_vd(const hb_mesh_desc *mesh, const hb_assembly_desc *d2, double *V_blocks_dev,
+                   const double *curls_dev, void *stream);
+
 /* Assemble blocks [d_begin, d_end) of one operator.  Writes every entry of
  * blocks_dev; results are bitwise deterministic run to run and independent
  * of d_begin/d_end (so d-sharded ranks reproduce the 1-GPU blocks). */

@@ -87,6 +87,7 @@ EXPORTED = (
     "hb_forward_solve", "hb_forward_history", "hb_inv_apply", "hb_represent_grid",
     "hb_project_workspace", "hb_project_data", "hb_p1_mass_solve", "hb_error_sigma", "hb_copy_row_slab_d2h",
     "hb_represent_grid_elem", "hb_toeplitz_apply_workspace", "hb_toeplitz_apply_ws",
+    "hb_assemble_vd", "hb_assemble_vd_min_workspace", "hb_assemble_vd_full_workspace",
 )
 
 _lib = None
@@ -106,7 +107,10 @@ def load():
     L.hb_last_error.restype = ctypes.c_char_p
     L.hb_assemble.argtypes = [ctypes.POINTER(MeshDesc), ctypes.POINTER(AssemblyDesc), _P]
     L.hb_assemble.restype = _INT
-    for fn in ("hb_assemble_min_workspace", "hb_assemble_full_workspace"):
+    L.hb_assemble_vd.argtypes = [ctypes.POINTER(MeshDesc), ctypes.POINTER(AssemblyDesc), _P, _P, _P]
+    L.hb_assemble_vd.restype = _INT
+    for fn in ("hb_assemble_min_workspace", "hb_assemble_full_workspace", "hb_assemble_vd_min_workspace",
+               "hb_assemble_vd_full_workspace"):
         getattr(L, fn).argtypes = [ctypes.POINTER(MeshDesc), ctypes.POINTER(AssemblyDesc)]
         getattr(L, fn).restype = ctypes.c_size_t
     L.hb_curl_combine.argtypes = [ctypes.POINTER(MeshDesc), _I64, _D, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]

@@ -278,7 +278,7 @@ class AssemblyInstrumentation:
 _WS_CACHE: dict = {}
 
 
-def _workspace(tables, desc_m, desc_a, device, cap, stream=None):
+def _workspace(tables, desc_m, desc_a, device, cap, stream=None, fused_vd: bool = False):
     """Staging buffer for one hb_assemble call.  One buffer per (device,
     stream) is kept and grown on demand: calls on a stream run in order, so
     reusing it is safe, and consecutive calls of different operators do not
@@ -287,8 +287,12 @@ def _workspace(tables, desc_m, desc_a, device, cap, stream=None):
     import torch
 
     L = _native.load()
-    full = L.hb_assemble_full_workspace(desc_m, desc_a)
-    least = L.hb_assemble_min_workspace(desc_m, desc_a)
+    if fused_vd:
+        full = L.hb_assemble_vd_full_workspace(desc_m, desc_a)
+        least = L.hb_assemble_vd_min_workspace(desc_m, desc_a)
+    else:
+        full = L.hb_assemble_full_workspace(desc_m, desc_a)
+        least = L.hb_assemble_min_workspace(desc_m, desc_a)
     st = stream if stream is not None else torch.cuda.current_stream(device)
     key = (str(device), st.cuda_stream)
     buf = _WS_CACHE.get(key)
@@ -585,14 +589,86 @@ def assemble_hypersingular(mesh, timegrid, params: KernelParams, config: Quadrat
                            instrumentation: AssemblyInstrumentation | None = None,
                            single_layer: BlockToeplitzMatrix | None = None, host_out=None,
                            **kw) -> BlockToeplitzMatrix:
-    """D = T^T (alpha^2 V) T + D2, p1 x p1 (assembly.py:337-361).  ``host_out``:
-    stream D to page-locked host memory chunk by chunk (hypersingular_from_single_layer)."""
+    """D = T^T (alpha^2 V) T + D2, p1 x p1 (assembly.py:337-361).
+
+    Without ``single_layer`` (the reference then assembles V itself) V and D2
+    are assembled together and the curl transform is folded into D2's p1 x p1
+    finalize (hb_assemble_vd: no pass of its own over V).  With a given
+    ``single_layer`` the curl combine reads it (hypersingular_from_single_layer).
+    ``host_out``: stream D to page-locked host memory (chunk by chunk on the
+    curl path, after the call on the fused path)."""
+    if single_layer is None and _fused_vd() and not kw.get("row_range") and kw.get("block_ptrs") is None:
+        _, D = _assemble_vd(mesh, timegrid, params, config, instrumentation, keep_v=False, **kw)
+        if host_out is not None:
+            if tuple(host_out.shape) != tuple(D.device_blocks.shape) or not host_out.is_pinned():
+                raise ValueError("host_out must be a page-locked tensor of D's (n_blocks, R, C) shape")
+            D.host_copy = D.to_host_async(host_out, kw.get("stream"))
+        return D
     if single_layer is None:
         single_layer = assemble_single_layer(mesh, timegrid, params, config, "p0", "p0", workers,
                                              deterministic, instrumentation, **kw)
     D2 = assemble_hypersingular_d2(mesh, timegrid, params, config, workers, instrumentation, **kw)
     return hypersingular_from_single_layer(single_layer, D2, mesh, params, overwrite_d2=True, config=config,
                                            host_out=host_out)
+
+
+def _fused_vd() -> bool:
+    """HB_FUSED_VD=1: V + D in one call (hb_assemble_vd) where the API allows
+    it.  Off by default: the fused finalize does twice the loads of the plain
+    p1 x p1 one, and at config 2 the separate curl combine overlaps K's pair
+    kernel on another stream (B200: 4.09 ms per V + K + D step separate vs
+    4.30 fused; a config-5 64-block chunk 481 vs 560 ms).  What it saves is
+    memory: D without V's blocks (config 5: 309 GB)."""
+    return os.environ.get("HB_FUSED_VD", "0") == "1"
+
+
+def _assemble_vd(mesh, timegrid, params: KernelParams, config: QuadratureConfig, instrumentation=None,
+                 d_range=None, device=None, workspace_bytes=None, stream=None, stats=None, out=None, out_v=None,
+                 keep_v: bool = True):
+    """V and D = D2 + alpha^2 curl^T V curl of blocks d_range in one
+    hb_assemble_vd call (V and D2 staged in the same test-row chunks, the curl
+    transform folded into the p1 x p1 finalize).  Returns (V or None, D)."""
+    import torch
+
+    _native.require_cuda()
+    tabs = device_tables(mesh, config, device)
+    E_t = timegrid.n_steps
+    d0, d1 = (0, E_t) if d_range is None else (int(d_range[0]), int(d_range[1]))
+    if not (0 <= d0 < d1 <= E_t):
+        raise ValueError(f"d_range {d_range} outside [0, {E_t}]")
+    E_x, N_x = mesh.n_triangles, mesh.n_vertices
+    dev = tabs.device
+    for t, shape in ((out, (d1 - d0, N_x, N_x)), (out_v, (d1 - d0, E_x, E_x))):
+        if t is not None and (tuple(t.shape) != shape or t.dtype != torch.float64 or not t.is_contiguous()):
+            raise ValueError(f"out tensors must be contiguous float64 of shape {shape}")
+    D = out if out is not None else torch.empty((d1 - d0, N_x, N_x), dtype=torch.float64, device=dev)
+    V = out_v if out_v is not None else (
+        torch.empty((d1 - d0, E_x, E_x), dtype=torch.float64, device=dev) if keep_v else None)
+    a = _native.AssemblyDesc()
+    a.op, a.test_p1, a.trial_p1, a.symmetric = _OP_HYPER2, 1, 1, 1
+    a.E_t, a.step = E_t, timegrid.step
+    a.alpha, a.d_eps, a.r_eps = params.alpha, params.delta_eps, params.rho_eps
+    a.d_begin, a.d_end = d0, d1
+    a.blocks_dev = D.data_ptr()
+    m = tabs.desc(True)
+    ws = _workspace(tabs, m, a, dev, None if workspace_bytes is None else int(workspace_bytes), stream,
+                    fused_vd=True)
+    a.workspace_dev, a.workspace_bytes = ws.data_ptr(), ws.numel()
+    if stats is not None:
+        import ctypes
+
+        a.stats = ctypes.pointer(stats)
+    t0 = time.perf_counter()
+    with torch.cuda.device(dev):
+        _native.call("hb_assemble_vd", m, a, V.data_ptr() if V is not None else None,
+                     _native.ptr(tabs.t["curls"]), _native.stream_handle(stream))
+        if instrumentation is not None:
+            torch.cuda.synchronize(dev)
+    if instrumentation is not None:
+        instrumentation.kernel_batch_passes += 2 * (E_t + 1)
+        instrumentation.seconds += time.perf_counter() - t0
+    del ws
+    return (BlockToeplitzMatrix(V) if V is not None else None), BlockToeplitzMatrix(D)
 
 
 _OP_CODES = {"V": (_OP_SINGLE, False, False, True), "K": (_OP_DOUBLE, False, True, False),
@@ -695,30 +771,39 @@ def assemble_all(mesh, timegrid, params: KernelParams, config: QuadratureConfig 
         st.wait_stream(cur)
     host_out = host_out or {}
     out = out or {}
-    with torch.cuda.stream(sD):
-        D2 = BlockToeplitzMatrix(_assemble_operator(_OP_HYPER2, True, True, True, mesh, timegrid, params, config,
-                                                    None, d_range=d_range, out=out.get("D")))
-    with torch.cuda.stream(sV):
-        V = BlockToeplitzMatrix(_assemble_operator(_OP_SINGLE, False, False, True, mesh, timegrid, params, config,
-                                                   None, d_range=d_range, out=out.get("V")))
-        v_done = torch.cuda.Event()
-        v_done.record(sV)
-        if "V" in host_out:
-            V.host_copy = V.to_host_async(host_out["V"])
+    if _fused_vd():
+        with torch.cuda.stream(sV):   # V and D together: D2's finalize adds the curl transform of V
+            V, D = _assemble_vd(mesh, timegrid, params, config, None, d_range=d_range, out=out.get("D"),
+                                out_v=out.get("V"))
+            if "V" in host_out:
+                V.host_copy = V.to_host_async(host_out["V"])
+            if "D" in host_out:
+                D.host_copy = D.to_host_async(host_out["D"])
+    else:
+        with torch.cuda.stream(sD):
+            D2 = BlockToeplitzMatrix(_assemble_operator(_OP_HYPER2, True, True, True, mesh, timegrid, params,
+                                                        config, None, d_range=d_range, out=out.get("D")))
+        with torch.cuda.stream(sV):
+            V = BlockToeplitzMatrix(_assemble_operator(_OP_SINGLE, False, False, True, mesh, timegrid, params,
+                                                       config, None, d_range=d_range, out=out.get("V")))
+            v_done = torch.cuda.Event()
+            v_done.record(sV)
+            if "V" in host_out:
+                V.host_copy = V.to_host_async(host_out["V"])
+        with torch.cuda.stream(sD):
+            sD.wait_event(v_done)
+            D = hypersingular_from_single_layer(V, D2, mesh, params, overwrite_d2=True, config=config,
+                                                host_out=host_out.get("D"))
+        V.device_blocks.record_stream(sD)    # read by the curl combine
     with torch.cuda.stream(sK):
         K = BlockToeplitzMatrix(_assemble_operator(_OP_DOUBLE, False, True, False, mesh, timegrid, params, config,
                                                    None, d_range=d_range, out=out.get("K")))
         if "K" in host_out:
             K.host_copy = K.to_host_async(host_out["K"])
-    with torch.cuda.stream(sD):
-        sD.wait_event(v_done)
-        D = hypersingular_from_single_layer(V, D2, mesh, params, overwrite_d2=True, config=config,
-                                            host_out=host_out.get("D"))
     for st in (sD, sV, sK):
         cur.wait_stream(st)
-    for M, st in ((V, sV), (K, sK), (D, sD)):
+    for M in (V, K, D):
         M.device_blocks.record_stream(cur)   # allocated on a side stream, used on the caller's
-    V.device_blocks.record_stream(sD)        # read by the curl combine
     return {"V": V, "K": K, "D": D}
 
 

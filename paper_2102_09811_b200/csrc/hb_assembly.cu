@@ -2032,6 +2032,13 @@ struct FinArgs {
     int nrs;                                // row-sharded destination: shards, bounds, base pointers
     const int64_t *rs_bounds;
     double *const *rs_ptrs;
+    // fused curl transform (k_fin_p1p1_accum<true>): the single layer's staging
+    // Qv[(e - e0) E_x + f][ndv] of the same row chunk, the window's offset in
+    // it, alpha^2 and the surface curls (E_x, 3, 3)
+    const double *Qv;
+    int ndv, dv_off;
+    double a2;
+    const double *curls;
 };
 
 // address of entry (row, col) of block d - d_begin = b: the caller's per-block
@@ -2127,6 +2134,15 @@ __global__ void __launch_bounds__(256) k_fin_p0p1(const FinArgs F)
 // a predicated load -- unstaged pairs add +0.0, which leaves the sum as is.
 constexpr int kFinMaxW = 8;   // bitmask words per star entry (tile lists <= 256 elements)
 
+// FUSE: D = D2 + alpha^2 curl^T V curl in the same pass (hb_assemble_vd).  Every
+// pair (e, f >= e) of the chunk adds alpha^2 (c_ei . c_fj) V_ef to X[m][n]
+// beside its staged D2 value (c: surface curl of hat i on e; V_ef from the
+// single layer's staging of the same rows, halved for e == f like D2's
+// diagonal), so X + X^T is D: sum over (e, i) in star(m), (f, j) in star(n) of
+// D2 + alpha^2 (c_ei . c_fj) V_ef -- the curl transform of
+// hypersingular_from_single_layer (heatbem/assembly.py:314-334) without a
+// pass of its own over V.
+template <bool FUSE>
 __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
 {
     __shared__ double tile[32][33];
@@ -2149,6 +2165,9 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
     int64_t *wFJ = sE + smax;                              // [kWarps][star_max] (9f + j) nd of node n's star
     unsigned *okm = (unsigned *)(wFJ + kWarps * smax);     // [star_max][kFinMaxW]
     int *wP = (int *)(okm + smax * kFinMaxW);              // [kWarps][star_max] tile position of f
+    // FUSE only: [star_max][4] curl of (e, i) | [kWarps][star_max][4] alpha^2 curl of (f, j), f
+    double *sC = (double *)(wP + kWarps * smax + (smax * kWarps & 1));
+    double *wC = sC + 4 * smax;
     __shared__ int na_s;
     if (threadIdx.x == 0) {
         int na = 0;
@@ -2157,6 +2176,12 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
             if (e < F.e0 || e >= F.e1) continue;
             sE[na] = e;
             sQ[na] = (e - F.e0) * F.E_x * 9 * (int64_t)F.nd + 3 * __ldg(F.star_local + a) * F.nd;
+            if (FUSE) {
+                const double *c = F.curls + 9 * e + 3 * __ldg(F.star_local + a);
+                sC[4 * na] = __ldg(c);
+                sC[4 * na + 1] = __ldg(c + 1);
+                sC[4 * na + 2] = __ldg(c + 2);
+            }
             ++na;
         }
         na_s = na;
@@ -2164,7 +2189,12 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
     __syncthreads();
     const int na = na_s;
     const int64_t tB0 = F.tile_eptr[blockIdx.y], tB = F.tile_eptr[blockIdx.y + 1] - tB0;
-    {   // staged-pair bitmask: warp w owns word w (tile positions 32w..32w+31)
+    // staged-pair bitmasks: warp w owns word w (tile positions 32w..32w+31);
+    // okm: D2 staged (f >= e, n_e . n_f != 0); FUSE: okv, every f >= e (V staged)
+    unsigned *okv = okm;
+    __shared__ unsigned okv_s[FUSE ? 64 * kFinMaxW : 1];
+    if (FUSE) okv = okv_s;
+    {
         const int p = 32 * warp + lane;
         int64_t f = -1;
         double nf[3] = {0.0, 0.0, 0.0};
@@ -2175,6 +2205,10 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
         for (int a = 0; a < na; ++a) {
             const int64_t e = sE[a];
             bool ok = p < tB && f >= e;
+            if (FUSE) {
+                const unsigned wv = __ballot_sync(kFull, ok);
+                if (lane == 0) okv[a * kFinMaxW + warp] = wv;
+            }
             if (F.skip_zero_dot) {
                 const double ne[3] = {__ldg(F.normals + 3 * e), __ldg(F.normals + 3 * e + 1),
                                       __ldg(F.normals + 3 * e + 2)};
@@ -2204,9 +2238,18 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
             const int64_t n = n0 + nl;
             if (n >= F.N_x) break;
             const int sn0 = (int)__ldg(F.star_indptr + n), nb = (int)__ldg(F.star_indptr + n + 1) - sn0;
+            double *myC = wC + warp * 4 * smax;
             for (int b = lane; b < nb; b += 32) {
-                myFJ[b] = (9 * __ldg(F.star_elem + sn0 + b) + __ldg(F.star_local + sn0 + b)) * F.nd;
+                const int64_t fb = __ldg(F.star_elem + sn0 + b), jb = __ldg(F.star_local + sn0 + b);
+                myFJ[b] = (9 * fb + jb) * F.nd;
                 myP[b] = F.star_pos[sn0 + b];
+                if (FUSE) {
+                    const double *c = F.curls + 9 * fb + 3 * jb;
+                    myC[4 * b] = F.a2 * __ldg(c);
+                    myC[4 * b + 1] = F.a2 * __ldg(c + 1);
+                    myC[4 * b + 2] = F.a2 * __ldg(c + 2);
+                    myC[4 * b + 3] = __longlong_as_double(fb);
+                }
             }
             __syncwarp();
             double x = tile[nl][lane];
@@ -2218,7 +2261,64 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
                 const double *Qe = F.Q + sQ[a] + dc + lane;
                 const unsigned *om = okm + a * kFinMaxW;
                 double se = 0.0;
-                if (nb <= 32) {
+                if (FUSE && nb <= 32) {
+                    // every (f, j) of star(n) with f >= e: staged D2 value (0 where D2
+                    // skipped the pair) + (alpha^2 c_ei . c_fj) V_ef, in star order.
+                    // Lane b holds entry b's coefficient; four entries per round
+                    // with their eight loads in flight together
+                    const int64_t e = sE[a];
+                    const double *Qve = F.Qv + (e - F.e0) * F.E_x * (int64_t)F.ndv + F.dv_off + dc + lane;
+                    const unsigned *ov = okv + a * kFinMaxW;
+                    bool vb = false, db = false;
+                    double sb = 0.0;
+                    int64_t fbl = 0;
+                    if (lane < nb) {
+                        vb = (ov[pb >> 5] >> (pb & 31)) & 1u;
+                        db = (om[pb >> 5] >> (pb & 31)) & 1u;
+                        fbl = __double_as_longlong(myC[4 * lane + 3]);
+                        sb = fma(sC[4 * a + 2], myC[4 * lane + 2], fma(sC[4 * a + 1], myC[4 * lane + 1],
+                                                                       sC[4 * a] * myC[4 * lane]));
+                        if (fbl == e) sb *= 0.5;
+                    }
+                    unsigned mask = __ballot_sync(kFull, vb);
+                    const unsigned dmask = __ballot_sync(kFull, db);
+                    while (mask) {
+                        int b[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            b[u] = mask ? __ffs(mask) - 1 : -1;
+                            mask &= mask - 1;
+                        }
+                        double su[4], qd[4], qv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int bu = b[u] < 0 ? 0 : b[u];
+                            su[u] = __shfl_sync(kFull, sb, bu);
+                            const int64_t fu = __shfl_sync(kFull, fbl, bu);
+                            qd[u] = (lok && b[u] >= 0 && ((dmask >> bu) & 1u)) ? Qe[myFJ[bu]] : 0.0;
+                            qv[u] = (lok && b[u] >= 0) ? Qve[fu * F.ndv] : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (b[u] >= 0) se += fma(su[u], qv[u], qd[u]);
+                    }
+                } else if (FUSE) {
+                    const int64_t e = sE[a];
+                    const double ce0 = sC[4 * a], ce1 = sC[4 * a + 1], ce2 = sC[4 * a + 2];
+                    const double *Qve = F.Qv + (e - F.e0) * F.E_x * (int64_t)F.ndv + F.dv_off + dc + lane;
+                    const unsigned *ov = okv + a * kFinMaxW;
+                    for (int b = 0; b < nb; ++b) {
+                        const int p = myP[b];
+                        if (!((ov[p >> 5] >> (p & 31)) & 1u)) continue;   // f < e: the mirrored half
+                        const int64_t fb = __double_as_longlong(myC[4 * b + 3]);
+                        double s = fma(ce2, myC[4 * b + 2], fma(ce1, myC[4 * b + 1], ce0 * myC[4 * b]));
+                        if (fb == e) s *= 0.5;
+                        const bool d2 = (om[p >> 5] >> (p & 31)) & 1u;
+                        const double qd = (lok && d2) ? Qe[myFJ[b]] : 0.0;
+                        const double qv = lok ? Qve[fb * F.ndv] : 0.0;
+                        se += fma(s, qv, qd);
+                    }
+                } else if (nb <= 32) {
                     unsigned mask = __ballot_sync(kFull, lane < nb && ((om[pb >> 5] >> (pb & 31)) & 1u));
                     while (mask) {   // four staged entries per round: their loads are in flight together
                         int b[4];
@@ -2467,20 +2567,180 @@ struct LaunchTimer {
 };
 }  // namespace hb
 
-extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, void *stream)
+namespace hb {
+// pair-kernel arguments of one operator call (everything but the staging
+// pointers and the row range)
+static PairArgs make_pair_args(const hb_mesh_desc *m, const hb_assembly_desc *a)
 {
-    if (!m || !a) { set_error("hb_assemble: null descriptor"); return HB_ERR_INVALID; }
+    PairArgs A{};
+    A.m = *m;
+    A.step = a->step;
+    A.alpha = a->alpha;
+    A.d_eps = a->d_eps;
+    A.r_eps = a->r_eps;
+    A.inv2a = 1.0 / (2.0 * a->alpha);
+    A.inv2a2 = 1.0 / (2.0 * a->alpha * a->alpha);
+    A.inva = 1.0 / a->alpha;
+    A.kconst = (a->op == 0) ? 1.0 / sqrt(kPi * a->alpha * a->alpha * a->alpha) : 1.0 / sqrt(kPi * a->alpha);
+    {   // moment form: u = 2 sqrt(alpha h); V: S = u / (2 a^2), q0 = 1/2; K, D2: S = 1/u, q0 = -1/2
+        const double u = 2.0 * sqrt(a->alpha * a->step);
+        A.inv_u2 = 1.0 / (u * u);
+        A.mom_S = (a->op == HB_OP_SINGLE_LAYER) ? u * A.inv2a2 : 1.0 / u;
+        A.mom_q0 = (a->op == HB_OP_SINGLE_LAYER) ? 0.5 : -0.5;
+    }
+    A.halve_diag = (a->test_p1 && a->trial_p1) ? 1 : 0;
+    // one launch per test-row chunk covers all blocks [d_begin, d_end) in the
+    // moment form: each pair computes its moments once and its per-point gap
+    // windows inside the kernel
+    A.d0 = (int)a->d_begin;
+    A.d1 = (int)a->d_end;
+    A.nd = (int)(a->d_end - a->d_begin);
+    A.need_special = a->d_begin <= 1;
+    A.moments = use_moments(a);
+    return A;
+}
+
+// gap windows of a call: the moment form covers all blocks in one; the direct
+// form windows of <= 32 gap slots (the first from block 0 or 1 holds 32 blocks,
+// later ones 30)
+static int64_t window_end(const hb_assembly_desc *a, bool moments, int64_t d0)
+{
+    return moments ? a->d_end : std::min<int64_t>(a->d_end, (d0 <= 1) ? 32 : d0 + 30);
+}
+
+// the pair kernels of rows [e0, e1) and blocks [d0, d1) into staging A.Q
+static int pairs_window(const hb_mesh_desc *m, const hb_assembly_desc *a, PairArgs &A, int64_t e0, int64_t e1,
+                        int64_t d0, int64_t d1, LaunchTimer &LT, cudaStream_t st)
+{
+    A.e0 = e0;
+    A.e1 = e1;
+    cudaEvent_t ev = LT.begin(st);
+    int rc;
+    if (A.moments) {
+        rc = run_pairs(a, A, st);   // three launches: touching, near, far pairs
+        LT.launches += 3;
+        LT.pair_launches += 3;
+    } else {
+        rc = direct_pairs(m, a, e0, e1, (int)d0, (int)d1, A.Q, A.counter, st);
+        LT.launches += 1;
+        LT.pair_launches += 1;
+    }
+    if (rc) return rc;
+    LT.end(ev, true, st);
+    return HB_OK;
+}
+
+static FinArgs fin_args(const hb_mesh_desc *m, const hb_assembly_desc *a, const double *Q, int64_t e0, int64_t e1,
+                        int64_t d0, int nd_w)
+{
+    FinArgs F{};
+    F.Q = Q;
+    F.out = a->blocks_dev;
+    F.bptr = a->block_ptrs_dev;
+    F.nrs = (int)a->n_row_shards;
+    F.rs_bounds = a->row_shard_bounds_dev;
+    F.rs_ptrs = a->row_shard_ptrs_dev;
+    F.E_x = m->E_x; F.N_x = m->N_x;
+    F.R = a->test_p1 ? m->N_x : m->E_x;
+    F.C = a->trial_p1 ? m->N_x : m->E_x;
+    F.e0 = e0; F.e1 = e1;
+    F.d0 = (int)d0; F.nd = nd_w; F.d_begin = (int)a->d_begin;
+    F.star_indptr = m->star_indptr_dev; F.star_elem = m->star_elem_dev;
+    F.star_local = m->star_local_dev; F.tri_nodes = m->tri_nodes_dev;
+    F.normals = m->normals_dev; F.skip_zero_dot = a->op == HB_OP_HYPERSINGULAR2;
+    F.star_max = (int)m->star_max;
+    F.tile_eptr = m->curl_tile_eptr_dev; F.tile_elem = m->curl_tile_elem_dev; F.star_pos = m->curl_star_pos_dev;
+    return F;
+}
+
+static size_t fin_p1p1_smem(const hb_mesh_desc *m, bool fuse)
+{
+    const size_t sm = (size_t)m->star_max;
+    size_t b = sm * ((2 + kWarps) * sizeof(int64_t) + kFinMaxW * sizeof(unsigned) + kWarps * sizeof(int));
+    if (fuse) b += sizeof(double) * 4 * sm * (1 + kWarps);
+    return b;
+}
+
+// staging -> blocks for one window of one row chunk
+static int finalize_window(const hb_mesh_desc *m, const hb_assembly_desc *a, const FinArgs &F, LaunchTimer &LT,
+                           cudaStream_t st)
+{
+    cudaEvent_t ev = LT.begin(st);
+    const int64_t rows = F.e1 - F.e0;
+    if (!a->test_p1 && !a->trial_p1) {
+        dim3 g((unsigned)cdiv(m->E_x, 32), (unsigned)cdiv(rows, 4));
+        k_fin_p0p0<<<g, 256, 0, st>>>(F);
+    } else if (!a->test_p1) {
+        dim3 g((unsigned)rows, (unsigned)cdiv(m->N_x, 32));
+        k_fin_p0p1<<<g, 256, 0, st>>>(F);
+    } else {
+        dim3 g((unsigned)(3 * rows), (unsigned)cdiv(m->N_x, 32));
+        if (F.Qv) k_fin_p1p1_accum<true><<<g, 256, fin_p1p1_smem(m, true), st>>>(F);
+        else k_fin_p1p1_accum<false><<<g, 256, fin_p1p1_smem(m, false), st>>>(F);
+    }
+    int rc = cuda_check(cudaGetLastError(), "finalize");
+    if (rc) return rc;
+    LT.end(ev, false, st);
+    LT.launches += 1;
+    return HB_OK;
+}
+
+// X <- X + X^T on every block of a p1 x p1 call
+static int symmetrize_blocks(double *blocks, int64_t R, int64_t nb, LaunchTimer &LT, cudaStream_t st)
+{
+    const int64_t nt = cdiv(R, 32);
+    for (int64_t b0 = 0; b0 < nb; b0 += 65535) {
+        dim3 g((unsigned)(nt * (nt + 1) / 2), (unsigned)std::min<int64_t>(65535, nb - b0));
+        cudaEvent_t ev = LT.begin(st);
+        k_symmetrize<<<g, 256, 0, st>>>(blocks, R, b0);
+        int rc = cuda_check(cudaGetLastError(), "symmetrize");
+        if (rc) return rc;
+        LT.end(ev, false, st);
+        LT.launches += 1;
+    }
+    return HB_OK;
+}
+
+static int check_desc(const hb_mesh_desc *m, const hb_assembly_desc *a, const char *who)
+{
     if (!combo_ok(a)) {
-        set_error("hb_assemble: unsupported op/space combination (op=%d test_p1=%d trial_p1=%d sym=%d)",
-                  a->op, a->test_p1, a->trial_p1, a->symmetric);
+        set_error("%s: unsupported op/space combination (op=%d test_p1=%d trial_p1=%d sym=%d)", who, a->op,
+                  a->test_p1, a->trial_p1, a->symmetric);
         return HB_ERR_UNSUPPORTED;
     }
     if (a->E_t < 1 || a->d_begin < 0 || a->d_end > a->E_t || a->d_begin >= a->d_end || m->E_x < 1 ||
         m->N_x < 3 || !(a->step > 0) || !(a->alpha > 0)) {
-        set_error("hb_assemble: invalid sizes or parameters (E_t=%lld d=[%lld,%lld) E_x=%lld)",
-                  (long long)a->E_t, (long long)a->d_begin, (long long)a->d_end, (long long)m->E_x);
+        set_error("%s: invalid sizes or parameters (E_t=%lld d=[%lld,%lld) E_x=%lld)", who, (long long)a->E_t,
+                  (long long)a->d_begin, (long long)a->d_end, (long long)m->E_x);
         return HB_ERR_INVALID;
     }
+    if (a->test_p1 && a->trial_p1 &&
+        (!m->curl_tile_eptr_dev || !m->curl_tile_elem_dev || !m->curl_star_pos_dev ||
+         m->curl_tile_emax > 32 * kFinMaxW)) {
+        set_error("%s: p1 x p1 needs the mesh tile plan with <= %d elements per 32-node tile", who, 32 * kFinMaxW);
+        return HB_ERR_UNSUPPORTED;
+    }
+    return HB_OK;
+}
+
+// the single layer's descriptor of a fused V + D call
+static hb_assembly_desc vd_single_layer(const hb_assembly_desc *d2, double *V_blocks_dev)
+{
+    hb_assembly_desc v = *d2;
+    v.op = HB_OP_SINGLE_LAYER;
+    v.test_p1 = v.trial_p1 = 0;
+    v.symmetric = 1;
+    v.blocks_dev = V_blocks_dev;
+    v.stats = nullptr;
+    return v;
+}
+}  // namespace hb
+
+extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, void *stream)
+{
+    if (!m || !a) { set_error("hb_assemble: null descriptor"); return HB_ERR_INVALID; }
+    int rc = check_desc(m, a, "hb_assemble");
+    if (rc) return rc;
     const int64_t r0 = a->row_end > a->row_begin ? a->row_begin : 0;
     const int64_t r1 = a->row_end > a->row_begin ? a->row_end : m->E_x;
     if (r0 < 0 || r1 > m->E_x || r0 >= r1 || (a->test_p1 && a->trial_p1 && a->block_ptrs_dev)) {
@@ -2500,12 +2760,6 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
         set_error("hb_assemble: no output (blocks_dev, block_ptrs_dev and row shards all absent)");
         return HB_ERR_INVALID;
     }
-    if (a->test_p1 && a->trial_p1 &&
-        (!m->curl_tile_eptr_dev || !m->curl_tile_elem_dev || !m->curl_star_pos_dev ||
-         m->curl_tile_emax > 32 * kFinMaxW)) {
-        set_error("hb_assemble: p1 x p1 needs the mesh tile plan with <= %d elements per 32-node tile", 32 * kFinMaxW);
-        return HB_ERR_UNSUPPORTED;
-    }
     cudaStream_t st = (cudaStream_t)stream;
     const size_t rb = row_bytes(m, a), tb = tm_bytes(a);
     if (!a->workspace_dev || a->workspace_bytes < rb + tb + kCounterBytes) {
@@ -2516,121 +2770,147 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
     // workspace: [staging Q: row chunks][moment table][counter]
     const size_t q_bytes = (a->workspace_bytes - kCounterBytes - tb) & ~(size_t)255;
     const int64_t rows_per_chunk = std::max<int64_t>(1, std::min<int64_t>(m->E_x, (int64_t)(q_bytes / rb)));
-    const int64_t R = a->test_p1 ? m->N_x : m->E_x, C = a->trial_p1 ? m->N_x : m->E_x;
+    const int64_t R = a->test_p1 ? m->N_x : m->E_x;
     const int64_t nb = a->d_end - a->d_begin;
     const bool p1p1 = a->test_p1 && a->trial_p1;
     if (p1p1) {
-        int rc = cuda_check(cudaMemsetAsync(a->blocks_dev, 0, (size_t)nb * R * C * sizeof(double), st), "memset");
+        rc = cuda_check(cudaMemsetAsync(a->blocks_dev, 0, (size_t)nb * R * R * sizeof(double), st), "memset");
         if (rc) return rc;
     }
-
-    PairArgs A{};
-    A.m = *m;
-    A.step = a->step;
-    A.alpha = a->alpha;
-    A.d_eps = a->d_eps;
-    A.r_eps = a->r_eps;
-    A.inv2a = 1.0 / (2.0 * a->alpha);
-    A.inv2a2 = 1.0 / (2.0 * a->alpha * a->alpha);
-    A.inva = 1.0 / a->alpha;
-    A.kconst = (a->op == 0) ? 1.0 / sqrt(kPi * a->alpha * a->alpha * a->alpha) : 1.0 / sqrt(kPi * a->alpha);
-    {   // moment form: u = 2 sqrt(alpha h); V: S = u / (2 a^2), q0 = 1/2; K, D2: S = 1/u, q0 = -1/2
-        const double u = 2.0 * sqrt(a->alpha * a->step);
-        A.inv_u2 = 1.0 / (u * u);
-        A.mom_S = (a->op == HB_OP_SINGLE_LAYER) ? u * A.inv2a2 : 1.0 / u;
-        A.mom_q0 = (a->op == HB_OP_SINGLE_LAYER) ? 0.5 : -0.5;
-    }
-    A.halve_diag = p1p1 ? 1 : 0;
+    PairArgs A = make_pair_args(m, a);
     A.Q = (double *)a->workspace_dev;
     double *Tm = (double *)((char *)a->workspace_dev + q_bytes);
     A.Tm = Tm;
     A.counter = (unsigned long long *)((char *)a->workspace_dev + q_bytes + tb);
-    // one launch per test-row chunk covers all blocks [d_begin, d_end): each pair
-    // computes its moments once and its per-point gap windows inside the kernel
-    A.d0 = (int)a->d_begin;
-    A.d1 = (int)a->d_end;
-    A.nd = (int)nb;
-    A.need_special = a->d_begin <= 1;
-    A.moments = use_moments(a);
 
     LaunchTimer LT{a->stats, st};
     if (A.moments) {
         cudaEvent_t ev = LT.begin(st);
-        int rc = moment_table(a, A, Tm, st);
+        rc = moment_table(a, A, Tm, st);
         if (rc) return rc;
         LT.end(ev, false, st);
         LT.launches += 1;
     }
-    // moment form: one launch per row chunk for all blocks; direct form: windows
-    // of <= 32 gap slots (the first from block 0 or 1 holds 32 blocks, later 30)
-    const int64_t W = 32;
     for (int64_t d0 = a->d_begin; d0 < a->d_end;) {
-        const int64_t d1 = A.moments ? a->d_end : std::min<int64_t>(a->d_end, (d0 <= 1) ? W : d0 + W - 2);
-        const int nd_w = (int)(d1 - d0);
-        // staging rows of this window: rows_per_chunk from the full row size is a lower bound
+        const int64_t d1 = window_end(a, A.moments, d0);
         for (int64_t e0 = r0; e0 < r1; e0 += rows_per_chunk) {
             const int64_t e1 = std::min(r1, e0 + rows_per_chunk);
-            A.e0 = e0;
-            A.e1 = e1;
-            cudaEvent_t ev = LT.begin(st);
-            int rc;
-            if (A.moments) {
-                rc = run_pairs(a, A, st);   // three launches: touching, near, far pairs
-                LT.launches += 3;
-                LT.pair_launches += 3;
-            } else {
-                rc = direct_pairs(m, a, e0, e1, (int)d0, (int)d1, A.Q, A.counter, st);
-                LT.launches += 1;
-                LT.pair_launches += 1;
-            }
+            rc = pairs_window(m, a, A, e0, e1, d0, d1, LT, st);
             if (rc) return rc;
-            LT.end(ev, true, st);
-            ev = LT.begin(st);
-            FinArgs F{};
-            F.Q = A.Q;
-            F.out = a->blocks_dev;
-            F.bptr = a->block_ptrs_dev;
-            F.nrs = (int)a->n_row_shards;
-            F.rs_bounds = a->row_shard_bounds_dev;
-            F.rs_ptrs = a->row_shard_ptrs_dev;
-            F.E_x = m->E_x; F.N_x = m->N_x; F.R = R; F.C = C; F.e0 = e0; F.e1 = e1;
-            F.d0 = (int)d0; F.nd = nd_w; F.d_begin = (int)a->d_begin;
-            F.star_indptr = m->star_indptr_dev; F.star_elem = m->star_elem_dev;
-            F.star_local = m->star_local_dev; F.tri_nodes = m->tri_nodes_dev;
-            F.normals = m->normals_dev; F.skip_zero_dot = a->op == HB_OP_HYPERSINGULAR2;
-            F.star_max = (int)m->star_max;
-            F.tile_eptr = m->curl_tile_eptr_dev; F.tile_elem = m->curl_tile_elem_dev; F.star_pos = m->curl_star_pos_dev;
-            if (!a->test_p1 && !a->trial_p1) {
-                dim3 g((unsigned)cdiv(m->E_x, 32), (unsigned)cdiv(e1 - e0, 4));
-                k_fin_p0p0<<<g, 256, 0, st>>>(F);
-            } else if (!a->test_p1) {
-                dim3 g((unsigned)(e1 - e0), (unsigned)cdiv(m->N_x, 32));
-                k_fin_p0p1<<<g, 256, 0, st>>>(F);
-            } else {
-                dim3 g((unsigned)(3 * (e1 - e0)), (unsigned)cdiv(m->N_x, 32));
-                const size_t fsm = (size_t)m->star_max * ((2 + kWarps) * sizeof(int64_t) + kFinMaxW * sizeof(unsigned) +
-                                                          kWarps * sizeof(int));
-                k_fin_p1p1_accum<<<g, 256, fsm, st>>>(F);
-            }
-            rc = cuda_check(cudaGetLastError(), "finalize");
+            rc = finalize_window(m, a, fin_args(m, a, A.Q, e0, e1, d0, (int)(d1 - d0)), LT, st);
             if (rc) return rc;
-            LT.end(ev, false, st);
-            LT.launches += 1;
         }
         d0 = d1;
     }
     if (p1p1) {
-        const int64_t nt = cdiv(R, 32);
-        for (int64_t b0 = 0; b0 < nb; b0 += 65535) {
-            dim3 g((unsigned)(nt * (nt + 1) / 2), (unsigned)std::min<int64_t>(65535, nb - b0));
-            cudaEvent_t ev = LT.begin(st);
-            k_symmetrize<<<g, 256, 0, st>>>(a->blocks_dev, R, b0);
-            int rc = cuda_check(cudaGetLastError(), "symmetrize");
+        rc = symmetrize_blocks(a->blocks_dev, R, nb, LT, st);
+        if (rc) return rc;
+    }
+    return LT.finish();
+}
+
+// fused V + D (hb_assemble_vd): staging of one test row for both operators
+static size_t vd_row_bytes(const hb_mesh_desc *m, const hb_assembly_desc *d2)
+{
+    const hb_assembly_desc v = vd_single_layer(d2, nullptr);
+    return row_bytes(m, &v) + row_bytes(m, d2);
+}
+
+static size_t vd_fixed_bytes(const hb_assembly_desc *d2)
+{
+    const hb_assembly_desc v = vd_single_layer(d2, nullptr);
+    return tm_bytes(&v) + tm_bytes(d2) + kCounterBytes;
+}
+
+extern "C" size_t hb_assemble_vd_min_workspace(const hb_mesh_desc *m, const hb_assembly_desc *d2)
+{
+    if (!m || !d2) return 0;
+    return vd_row_bytes(m, d2) + vd_fixed_bytes(d2) + 512;
+}
+
+extern "C" size_t hb_assemble_vd_full_workspace(const hb_mesh_desc *m, const hb_assembly_desc *d2)
+{
+    if (!m || !d2) return 0;
+    return vd_row_bytes(m, d2) * (size_t)m->E_x + vd_fixed_bytes(d2) + 512;
+}
+
+extern "C" int hb_assemble_vd(const hb_mesh_desc *m, const hb_assembly_desc *d2, double *V_blocks_dev,
+                              const double *curls_dev, void *stream)
+{
+    if (!m || !d2 || !curls_dev || !d2->blocks_dev) {
+        set_error("hb_assemble_vd: null descriptor, curls or D blocks");
+        return HB_ERR_INVALID;
+    }
+    if (d2->op != HB_OP_HYPERSINGULAR2 || d2->row_end > d2->row_begin || d2->block_ptrs_dev || d2->n_row_shards) {
+        set_error("hb_assemble_vd: needs the hypersingular (D2) descriptor over all rows, contiguous blocks");
+        return HB_ERR_INVALID;
+    }
+    int rc = check_desc(m, d2, "hb_assemble_vd");
+    if (rc) return rc;
+    if (m->star_max > 64) {
+        set_error("hb_assemble_vd: node stars of more than 64 elements");
+        return HB_ERR_UNSUPPORTED;
+    }
+    const hb_assembly_desc v = vd_single_layer(d2, V_blocks_dev);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t rbv = row_bytes(m, &v), rbd = row_bytes(m, d2), tbv = tm_bytes(&v), tbd = tm_bytes(d2);
+    if (!d2->workspace_dev || d2->workspace_bytes < hb_assemble_vd_min_workspace(m, d2)) {
+        set_error("hb_assemble_vd: workspace %zu bytes < one row chunk (%zu bytes)", d2->workspace_bytes,
+                  hb_assemble_vd_min_workspace(m, d2));
+        return HB_ERR_WORKSPACE;
+    }
+    // workspace: [Q_V: row chunk][Q_D2: row chunk][Tm_V][Tm_D2][counter]
+    const size_t avail = d2->workspace_bytes - tbv - tbd - kCounterBytes - 512;
+    const int64_t rows_per_chunk = std::max<int64_t>(1, std::min<int64_t>(m->E_x, (int64_t)(avail / (rbv + rbd))));
+    char *ws = (char *)d2->workspace_dev;
+    const size_t qv_bytes = ((size_t)rows_per_chunk * rbv + 255) & ~(size_t)255;
+    const size_t qd_bytes = ((size_t)rows_per_chunk * rbd + 255) & ~(size_t)255;
+    PairArgs AV = make_pair_args(m, &v), AD = make_pair_args(m, d2);
+    if (!AV.moments && AD.moments) {
+        set_error("hb_assemble_vd: direct single layer with a moment-form D2 (HB_MOMENTS override) is not fused");
+        return HB_ERR_UNSUPPORTED;
+    }
+    AV.Q = (double *)ws;
+    AD.Q = (double *)(ws + qv_bytes);
+    AV.Tm = (double *)(ws + qv_bytes + qd_bytes);
+    AD.Tm = (double *)(ws + qv_bytes + qd_bytes + tbv);
+    AV.counter = AD.counter = (unsigned long long *)(ws + qv_bytes + qd_bytes + tbv + tbd);
+    const int64_t N = m->N_x, nb = d2->d_end - d2->d_begin;
+    rc = cuda_check(cudaMemsetAsync(d2->blocks_dev, 0, (size_t)nb * N * N * sizeof(double), st), "memset");
+    if (rc) return rc;
+    LaunchTimer LT{d2->stats, st};
+    if (AV.moments) { rc = moment_table(&v, AV, const_cast<double *>(AV.Tm), st); if (rc) return rc; LT.launches += 1; }
+    if (AD.moments) { rc = moment_table(d2, AD, const_cast<double *>(AD.Tm), st); if (rc) return rc; LT.launches += 1; }
+    for (int64_t e0 = 0; e0 < m->E_x; e0 += rows_per_chunk) {
+        const int64_t e1 = std::min(m->E_x, e0 + rows_per_chunk);
+        if (AV.moments) {   // V staging of all blocks of the call
+            rc = pairs_window(m, &v, AV, e0, e1, v.d_begin, v.d_end, LT, st);
+            if (!rc && V_blocks_dev) rc = finalize_window(m, &v, fin_args(m, &v, AV.Q, e0, e1, v.d_begin, (int)nb), LT, st);
             if (rc) return rc;
-            LT.end(ev, false, st);
-            LT.launches += 1;
+        }
+        for (int64_t d0 = d2->d_begin; d0 < d2->d_end;) {
+            const int64_t d1 = window_end(d2, AD.moments, d0);
+            if (!AV.moments) {   // direct V: the same windows as the direct D2
+                rc = pairs_window(m, &v, AV, e0, e1, d0, d1, LT, st);
+                if (!rc && V_blocks_dev)
+                    rc = finalize_window(m, &v, fin_args(m, &v, AV.Q, e0, e1, d0, (int)(d1 - d0)), LT, st);
+                if (rc) return rc;
+            }
+            rc = pairs_window(m, d2, AD, e0, e1, d0, d1, LT, st);
+            if (rc) return rc;
+            FinArgs F = fin_args(m, d2, AD.Q, e0, e1, d0, (int)(d1 - d0));
+            F.Qv = AV.Q;
+            F.ndv = AV.moments ? (int)nb : (int)(d1 - d0);
+            F.dv_off = AV.moments ? (int)(d0 - d2->d_begin) : 0;
+            F.a2 = d2->alpha * d2->alpha;
+            F.curls = curls_dev;
+            rc = finalize_window(m, d2, F, LT, st);
+            if (rc) return rc;
+            d0 = d1;
         }
     }
+    rc = symmetrize_blocks(d2->blocks_dev, N, nb, LT, st);
+    if (rc) return rc;
     return LT.finish();
 }
 

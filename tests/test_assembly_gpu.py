@@ -18,6 +18,8 @@ Tolerances (north star: <= 1e-11 of each block's max-abs entry):
   curl D, nearly exact, and F(x) removes the 1/x^2 cancellation of the
   reference's K bracket).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -195,6 +197,42 @@ def test_c2_rows_vs_reference():
         else:   # D2: well conditioned, plain bar
             assert np.all(par <= 1e-11), (op, par)
         assert np.array_equal(np.packbits(B[0] == 0.0), g[f"{op}_zeros"]), op
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_fused_single_layer_and_hypersingular(cfg):
+    """hb_assemble_vd (assemble_hypersingular without a given single layer,
+    assemble_all): V and D2 in the same row chunks, the curl transform folded
+    into D2's p1 x p1 finalize.  V is bitwise the standalone V; D meets the
+    same parity / accuracy gates as the curl-combine D, is exactly symmetric,
+    and differs from it only by summation order."""
+    g, ex = golden(cfg), golden("exact")
+    m, tg, p = c1() if cfg == "c1" else c2()
+    from paper_2102_09811_b200.assembly import _assemble_vd
+
+    V, D = _assemble_vd(m, tg, p, Q4)
+    V_ref = hb.assemble_single_layer(m, tg, p, Q4)
+    assert np.array_equal(V.blocks, V_ref.blocks)
+    B = D.blocks
+    assert all(np.array_equal(B[d], B[d].T) for d in range(B.shape[0]))
+    rows = g["rows_p1"]
+    eps_ref = ex[f"{cfg}_D_eps_ref"]
+    par = np.abs(B[:, rows, :] - g["D_rows"]).max(axis=(1, 2)) / g["D_maxabs"]
+    assert np.all(par <= gate(eps_ref)), (par, eps_ref)
+    acc = np.abs(B[:, rows, :] - ex[f"{cfg}_D_exact_rows"]).max(axis=(1, 2)) / g["D_maxabs"]
+    assert np.all(acc <= ACC["D"] * eps_ref + 1e-13), (acc, eps_ref)
+    assert np.array_equal(np.packbits(B[0] == 0.0), g["D_zeros"])
+    D_curl = hb.hypersingular_from_single_layer(V_ref, hb.assemble_hypersingular_d2(m, tg, p, Q4), m, p).blocks
+    assert np.abs(B - D_curl).max() <= 1e-13 * np.abs(D_curl).max()
+    os.environ["HB_FUSED_VD"] = "1"                                # the public path, fused
+    try:
+        D_api = hb.assemble_hypersingular(m, tg, p, Q4).blocks
+    finally:
+        del os.environ["HB_FUSED_VD"]
+    assert np.array_equal(D_api, B)
+    # a small staging budget: several row chunks, same blocks bitwise
+    V2, D2c = _assemble_vd(m, tg, p, Q4, workspace_bytes=1 << 22)
+    assert np.array_equal(V2.blocks, V.blocks) and np.array_equal(D2c.blocks, B)
 
 
 def test_instrumentation_and_api_variants():
