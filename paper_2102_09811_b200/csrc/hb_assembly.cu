@@ -1995,8 +1995,9 @@ __global__ void __launch_bounds__(HB_PAIR_WARPS * 32, (TP1 && SP1) ? HB_P1P1_MIN
     int64_t n_sing = s_hi - s_lo;
     const int64_t nseg = cdiv(M.E_x, (int64_t)A.seg_len);
     int64_t n_reg = (A.e1 - A.e0) * nseg;
-    if (CLS == 1) n_reg = 0;    // touching pairs only
-    if (CLS >= 2) n_sing = 0;   // separated pairs: far (2) / near (3)
+    if (CLS == 1) n_reg = 0;                 // touching pairs only
+    if (CLS == 2 || CLS == 3) n_sing = 0;    // separated pairs: far (2) / near (3); 4: touching, then near
+    constexpr int RCLS = CLS == 4 ? 3 : CLS;
     for (;;) {
         unsigned long long it = 0;
         if (lane == 0) it = atomicAdd(A.counter, 1ull);
@@ -2006,8 +2007,8 @@ __global__ void __launch_bounds__(HB_PAIR_WARPS * 32, (TP1 && SP1) ? HB_P1P1_MIN
             singular_item<OP, TP1, SP1, NJ>(A, s_lo + item, W, lane, tab);
         } else if (item - n_sing < n_reg) {
             const int64_t r = item - n_sing;
-            if constexpr (DUAL) regular_item_dual<NJ, CLS>(A, A.e0 + r / nseg, r % nseg, W, lane, tab);
-            else regular_item<OP, TP1, SP1, NJ, SYM, CLS>(A, A.e0 + r / nseg, r % nseg, W, lane, tab);
+            if constexpr (DUAL) regular_item_dual<NJ, RCLS>(A, A.e0 + r / nseg, r % nseg, W, lane, tab);
+            else regular_item<OP, TP1, SP1, NJ, SYM, RCLS>(A, A.e0 + r / nseg, r % nseg, W, lane, tab);
         } else {
             break;
         }
@@ -2463,7 +2464,8 @@ static int launch_class(const PairArgs &A, cudaStream_t st)
     const int64_t warps = (int64_t)std::max(1, per_sm) * nsm * HB_PAIR_WARPS;
     B.seg_len = 32;
     while (B.seg_len > 4 && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < 4 * warps) B.seg_len /= 2;
-    const int64_t items = CLS == 1 ? rows * A.m.sing_max_per_row : rows * cdiv(A.m.E_x, (int64_t)B.seg_len);
+    const int64_t items = (CLS == 1 || CLS == 4 ? rows * A.m.sing_max_per_row : 0) +
+                          (CLS == 1 ? 0 : rows * cdiv(A.m.E_x, (int64_t)B.seg_len));
     // (near-pair items: most segments hold none and exit after the classification)
     if (items == 0) return HB_OK;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(1, per_sm) * nsm, cdiv(items, HB_PAIR_WARPS)));
@@ -2473,11 +2475,28 @@ static int launch_class(const PairArgs &A, cudaStream_t st)
     return cuda_check(cudaGetLastError(), "pair kernel");
 }
 
+static bool merge_tn()
+{
+    static const bool merge = !getenv("HB_MERGE_TN") || atoi(getenv("HB_MERGE_TN")) != 0;
+    return merge;
+}
+
 template <int OP, bool TP1, bool SP1, int NJ, bool DUAL = false>
 static int launch_pairs(const PairArgs &A, cudaStream_t st)
 {
-    int rc = launch_class<OP, TP1, SP1, NJ, DUAL, 1>(A, st);
-    if (!rc) rc = launch_class<OP, TP1, SP1, NJ, DUAL, 3>(A, st);
+    // touching and near pairs (warp per pair) in one launch: the cheap segment
+    // items fill in behind the heavy touching ones (one kernel tail instead of
+    // two); HB_MERGE_TN=0: separate launches
+    // (all three classes in one launch: measured slower -- V 1.38 vs 1.10 ms at
+    // config 2 -- the far batches' register-heavy path and the warp-per-pair
+    // path then share SMs)
+    int rc;
+    if (merge_tn()) {
+        rc = launch_class<OP, TP1, SP1, NJ, DUAL, 4>(A, st);
+    } else {
+        rc = launch_class<OP, TP1, SP1, NJ, DUAL, 1>(A, st);
+        if (!rc) rc = launch_class<OP, TP1, SP1, NJ, DUAL, 3>(A, st);
+    }
     if (!rc && A.moments) rc = launch_class<OP, TP1, SP1, NJ, DUAL, 2>(A, st);   // far batches
     return rc;
 }
@@ -2617,9 +2636,9 @@ static int pairs_window(const hb_mesh_desc *m, const hb_assembly_desc *a, PairAr
     cudaEvent_t ev = LT.begin(st);
     int rc;
     if (A.moments) {
-        rc = run_pairs(a, A, st);   // three launches: touching, near, far pairs
-        LT.launches += 3;
-        LT.pair_launches += 3;
+        rc = run_pairs(a, A, st);   // touching + near pairs, far batches (or three launches)
+        LT.launches += merge_tn() ? 2 : 3;
+        LT.pair_launches += merge_tn() ? 2 : 3;
     } else {
         rc = direct_pairs(m, a, e0, e1, (int)d0, (int)d1, A.Q, A.counter, st);
         LT.launches += 1;

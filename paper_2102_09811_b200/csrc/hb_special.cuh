@@ -113,20 +113,30 @@ __device__ __forceinline__ void table_chains(const double *__restrict__ tab, con
     if constexpr (packed<KIND>()) {
         const double2 *t2 = reinterpret_cast<const double2 *>(tab);
         constexpr int MT = DEG / 2;
+        // coefficient pairs prefetched HB_TAB_PREFETCH steps ahead of the chain
+        // (the loads do not depend on it): the LDS.128 latency hides behind the
+        // previous steps' FMAs instead of stalling every step
+#ifndef HB_TAB_PREFETCH
+#define HB_TAB_PREFETCH 3
+#endif
+        constexpr int PF = HB_TAB_PREFETCH < 1 ? 1 : HB_TAB_PREFETCH;
+        double2 w[MT + 1][NJ];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const double2 w = t2[MT * kTabStride + col[j]];
-            q[j] = (DEG & 1) ? fma(w.y, v[j], w.x) : w.x;
-        }
+        for (int m = MT; m >= 0 && m > MT - PF - 1; --m)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) w[m][j] = t2[m * kTabStride + col[j]];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) q[j] = (DEG & 1) ? fma(w[MT][j].y, v[j], w[MT][j].x) : w[MT][j].x;
 #pragma unroll
         for (int m = MT - 1; m >= 0; --m) {
-            double2 w[NJ];
+            if (m - PF >= 0) {
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) w[j] = t2[m * kTabStride + col[j]];
+                for (int j = 0; j < NJ; ++j) w[m - PF][j] = t2[(m - PF) * kTabStride + col[j]];
+            }
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], w[j].y);
+            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], w[m][j].y);
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], w[j].x);
+            for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], v[j], w[m][j].x);
         }
     } else {
 #pragma unroll
