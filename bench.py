@@ -635,18 +635,26 @@ def run_native_c2(args, rank, world, local_rank):
     pinK = torch.empty(outK.shape, dtype=torch.float64).pin_memory()
     pinD = torch.empty(outD.shape, dtype=torch.float64).pin_memory()
 
+    e2e_mode = os.environ.get("HB_E2E_MODE", "seq")   # "all": assemble_all(host_out) -- measured slower (6.4 vs 6.0 ms)
+    e2e_slabs = int(os.environ.get("HB_E2E_SLABS", "2"))
+
     def e2e_step():
-        # sequential public calls: V finishes first and its copy-back overlaps K,
-        # K's overlaps D; mesh tables re-uploaded from pinned host memory
+        # mesh tables re-uploaded from pinned host memory every step
         hbdev.drop_device_tables(mesh)
-        V = hb.assemble_single_layer(mesh, tg, params, q, d_range=(d0, d1), host_out=pinV,
-                                     host_out_slabs=int(os.environ.get("HB_E2E_SLABS", "2")))
-        _, ev_v = V.host_copy
-        K = hb.assemble_double_layer(mesh, tg, params, q, d_range=(d0, d1), host_out=pinK)
-        _, ev_k = K.host_copy
-        D = hb.assemble_hypersingular(mesh, tg, params, q, single_layer=V, d_range=(d0, d1), host_out=pinD)
-        _, ev_d = D.host_copy
-        for ev in (ev_v, ev_k, ev_d):
+        if e2e_mode == "all":
+            # public assemble_all: V, K, D on concurrent streams (V's at high priority, in
+            # row slabs), every output copied back as soon as it (or its slab / chunk) is formed
+            ops = hb.assemble_all(mesh, tg, params, q, d_range=(d0, d1), host_out={"V": pinV, "K": pinK, "D": pinD},
+                                  v_slabs=e2e_slabs)
+            evs = [ops[n].host_copy[1] for n in ("V", "K", "D")]
+        else:
+            # sequential public calls: V's copy-back overlaps K, K's overlaps D
+            V = hb.assemble_single_layer(mesh, tg, params, q, d_range=(d0, d1), host_out=pinV,
+                                         host_out_slabs=e2e_slabs)
+            K = hb.assemble_double_layer(mesh, tg, params, q, d_range=(d0, d1), host_out=pinK)
+            D = hb.assemble_hypersingular(mesh, tg, params, q, single_layer=V, d_range=(d0, d1), host_out=pinD)
+            evs = [V.host_copy[1], K.host_copy[1], D.host_copy[1]]
+        for ev in evs:
             torch.cuda.current_stream().wait_event(ev)
 
     for _ in range(2):
@@ -735,10 +743,13 @@ def run_native_c2(args, rank, world, local_rank):
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "public API assemble_single_layer / assemble_double_layer / assemble_hypersingular with "
-                        "host_out: mesh tables re-uploaded from pinned host memory and all blocks copied to pinned "
-                        "host memory every step (V in work-balanced test-row slabs as they complete, K when done, D "
-                        "in block chunks as the curl combine forms them); the step ends when the last copy is done"},
+                "path": ("public API assemble_all(host_out=...): V, K, D on concurrent streams (V's at high "
+                         "priority)" if e2e_mode == "all" else
+                         "public API assemble_single_layer / assemble_double_layer / assemble_hypersingular with "
+                         "host_out") + "; mesh tables re-uploaded from pinned host memory and all blocks copied to "
+                        "pinned host memory every step (V in work-balanced test-row slabs as they complete, K when "
+                        "done, D in block chunks as the curl combine forms them); the step ends when the last copy "
+                        "is done"},
         "clocks": clocks,
         "paths": paths,
         "gpu_launches": int(round(sum(st.launches for st in stats) / n_stat + 1)) * args.steps * world,

@@ -221,10 +221,12 @@ class BlockToeplitzMatrix:
 _COPY_STREAMS: dict = {}
 
 
-def _copy_stream(device):
+def _copy_stream(device, name: str = ""):
+    """Side stream for device->host copies (one per (device, name): copies of
+    different operators on different streams do not queue behind each other)."""
     import torch
 
-    key = str(device)
+    key = (str(device), name)
     if key not in _COPY_STREAMS:
         _COPY_STREAMS[key] = torch.cuda.Stream(device=device)
     return _COPY_STREAMS[key]
@@ -458,7 +460,7 @@ def _row_slabs(n_rows: int, symmetric: bool, n_slabs: int):
 
 
 def _assemble_streamed(op, test_p1, trial_p1, symmetric, mesh, timegrid, params, config, instrumentation,
-                       host_out, n_slabs: int = 3, stream=None, **kw):
+                       host_out, n_slabs: int = 3, stream=None, copy_stream=None, **kw):
     """Assemble a p0-test operator in work-balanced test-row slabs and start
     each slab's device->host copy (rows [r0, r1) of every block, complete once
     the slab's rows are done: a symmetric operator's mirrored entries of those
@@ -484,7 +486,7 @@ def _assemble_streamed(op, test_p1, trial_p1, symmetric, mesh, timegrid, params,
         raise ValueError("host_out must be a contiguous page-locked tensor of the operator's (n_blocks, R, C) "
                          "float64 shape")
     cur = stream if stream is not None else torch.cuda.current_stream(dev)
-    cs = _copy_stream(dev)
+    cs = copy_stream if copy_stream is not None else _copy_stream(dev)
     for r0, r1 in _row_slabs(R, symmetric, n_slabs):
         _assemble_operator(op, test_p1, trial_p1, symmetric, mesh, timegrid, params, config, instrumentation,
                            d_range=(d0, d1), row_range=(r0, r1), out=out, stream=cur, **kw)
@@ -525,7 +527,8 @@ def curl_transform(mesh) -> CurlTransform:
 
 def hypersingular_from_single_layer(V: BlockToeplitzMatrix, D2: BlockToeplitzMatrix, mesh, params: KernelParams,
                                     overwrite_d2: bool = False, config: QuadratureConfig = QuadratureConfig(),
-                                    stream=None, host_out=None, copy_chunks: int = 4) -> BlockToeplitzMatrix:
+                                    stream=None, host_out=None, copy_chunks: int = 4,
+                                    copy_stream=None) -> BlockToeplitzMatrix:
     """D = D2 + alpha^2 sum_o T_o^T V T_o blockwise (assembly.py:314-334), on the device.
 
     ``host_out`` (page-locked, D's shape): the combine runs in ``copy_chunks``
@@ -549,7 +552,7 @@ def hypersingular_from_single_layer(V: BlockToeplitzMatrix, D2: BlockToeplitzMat
         n = Vd.shape[0]
         bounds = np.linspace(0, n, max(1, min(int(copy_chunks), n)) + 1).astype(int)
         cur = stream if stream is not None else torch.cuda.current_stream(Vd.device)
-        cs = _copy_stream(Vd.device)
+        cs = copy_stream if copy_stream is not None else _copy_stream(Vd.device)
         for a, b in zip(bounds[:-1], bounds[1:]):
             curl_combine_into(tabs, Vd[a:b], D2d[a:b], out[a:b], float(params.alpha), cur)
             ready = torch.cuda.Event()
@@ -740,24 +743,30 @@ _OP_STREAMS: dict = {}
 
 
 def _op_streams(device):
+    """(D, V, K) streams of assemble_all; V's has the highest priority, so
+    with host outputs its row slabs finish first and the device->host copies
+    (the end-to-end bound) start as early as possible."""
     import torch
 
     key = str(device)
     if key not in _OP_STREAMS:
-        _OP_STREAMS[key] = tuple(torch.cuda.Stream(device=device) for _ in range(3))
+        lo, hi = torch.cuda.Stream.priority_range()   # (least, greatest): greatest is numerically lowest
+        _OP_STREAMS[key] = (torch.cuda.Stream(device=device), torch.cuda.Stream(device=device, priority=hi),
+                            torch.cuda.Stream(device=device))
     return _OP_STREAMS[key]
 
 
 def assemble_all(mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig(),
-                 d_range=None, host_out=None, out=None) -> dict:
+                 d_range=None, host_out=None, out=None, v_slabs: int = 2) -> dict:
     """V (p0 x p0), K (p0 x p1) and D = D2 + alpha^2 curl(V) (p1 x p1) of one
     space-time problem, assembled concurrently on three CUDA streams: the
     persistent pair kernels of one operator run while another's finalize /
     curl kernels (memory-bound) and kernel tails drain -- 8 % faster than three
     sequential calls at config 2, bitwise the same blocks.  ``host_out``
     (dict of page-locked tensors "V", "K", "D"): each operator is copied back
-    on a side stream as soon as it is done (D in block chunks as the curl
-    forms them); the returned matrices' ``host_copy`` hold (tensor, event).
+    on a side stream as soon as it is done (V in ``v_slabs`` work-balanced row
+    slabs on the high-priority stream, D in block chunks as the curl forms
+    them); the returned matrices' ``host_copy`` hold (tensor, event).
     ``out``: dict of preallocated device tensors "V", "K", "D" to assemble into.
     Returns {"V", "K", "D"}; the caller's stream waits for all of them."""
     import torch
@@ -780,21 +789,49 @@ def assemble_all(mesh, timegrid, params: KernelParams, config: QuadratureConfig 
             if "D" in host_out:
                 D.host_copy = D.to_host_async(host_out["D"])
     else:
-        with torch.cuda.stream(sD):
-            D2 = BlockToeplitzMatrix(_assemble_operator(_OP_HYPER2, True, True, True, mesh, timegrid, params,
-                                                        config, None, d_range=d_range, out=out.get("D")))
+        streamed = bool(host_out)
+        if not streamed:   # D2 first: its finalize and the curl overlap the other pair kernels
+            with torch.cuda.stream(sD):
+                D2 = BlockToeplitzMatrix(_assemble_operator(_OP_HYPER2, True, True, True, mesh, timegrid, params,
+                                                            config, None, d_range=d_range, out=out.get("D")))
         with torch.cuda.stream(sV):
-            V = BlockToeplitzMatrix(_assemble_operator(_OP_SINGLE, False, False, True, mesh, timegrid, params,
-                                                       config, None, d_range=d_range, out=out.get("V")))
+            if "V" in host_out:   # work-balanced row slabs, each copied back as soon as it is formed
+                V = _assemble_streamed(_OP_SINGLE, False, False, True, mesh, timegrid, params, config, None,
+                                       host_out["V"], n_slabs=v_slabs, stream=sV, d_range=d_range,
+                                       out=out.get("V"))
+            else:
+                V = BlockToeplitzMatrix(_assemble_operator(_OP_SINGLE, False, False, True, mesh, timegrid,
+                                                           params, config, None, d_range=d_range,
+                                                           out=out.get("V")))
             v_done = torch.cuda.Event()
             v_done.record(sV)
-            if "V" in host_out:
-                V.host_copy = V.to_host_async(host_out["V"])
+        if streamed:
+            # host outputs: V alone first (its row slabs start the copies early: the
+            # device->host copies are the end-to-end bound), then K and D2 concurrently,
+            # then the curl; the copies queue on one copy stream in the order the
+            # outputs form (persistent pair kernels launched together would let K
+            # hold the SMs and delay V's later slabs)
+            with torch.cuda.stream(sK):
+                sK.wait_event(v_done)
+                K = BlockToeplitzMatrix(_assemble_operator(_OP_DOUBLE, False, True, False, mesh, timegrid, params,
+                                                           config, None, d_range=d_range, out=out.get("K")))
+                if "K" in host_out:
+                    K.host_copy = K.to_host_async(host_out["K"])
+            with torch.cuda.stream(sD):
+                sD.wait_event(v_done)
+                D2 = BlockToeplitzMatrix(_assemble_operator(_OP_HYPER2, True, True, True, mesh, timegrid, params,
+                                                            config, None, d_range=d_range, out=out.get("D")))
         with torch.cuda.stream(sD):
             sD.wait_event(v_done)
             D = hypersingular_from_single_layer(V, D2, mesh, params, overwrite_d2=True, config=config,
                                                 host_out=host_out.get("D"))
         V.device_blocks.record_stream(sD)    # read by the curl combine
+        if streamed:
+            for st in (sD, sV, sK):
+                cur.wait_stream(st)
+            for M in (V, K, D):
+                M.device_blocks.record_stream(cur)
+            return {"V": V, "K": K, "D": D}
     with torch.cuda.stream(sK):
         K = BlockToeplitzMatrix(_assemble_operator(_OP_DOUBLE, False, True, False, mesh, timegrid, params, config,
                                                    None, d_range=d_range, out=out.get("K")))
