@@ -52,6 +52,9 @@
 #ifndef HB_P1P1_MINB
 #define HB_P1P1_MINB HB_PAIR_MINB
 #endif
+#ifndef HB_FUSE1
+#define HB_FUSE1 1   // p0 x p0 touching / near pairs: moments and per-point gaps in one payload pass
+#endif
 #ifndef HB_QGROUP
 #define HB_QGROUP 2   // quadrature points of the same parity per evaluation group (independent chains)
 #endif
@@ -640,8 +643,8 @@ __device__ __forceinline__ void per_point_windows(const PairArgs &A, int dend, i
 // ---------------------------------------------------------------------------
 template <int OP, bool TP1, bool SP1, int NJ, class Geom>
 __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq, const double ny[3],
-                                          double jac, double rt2_lo, int64_t slot, double *geo, double *Ls,
-                                          double *Pw, int lane, const double *tab)
+                                          double jac, double rt2_lo, double rt2_hi, int64_t slot, double *geo,
+                                          double *Ls, double *Pw, int lane, const double *tab)
 {
     constexpr int NT = TP1 ? 3 : 1, NS = SP1 ? 3 : 1, NIJ = NT * NS;
     using L = Layout<OP, NIJ>;
@@ -650,6 +653,72 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
     double *p_lane = geo + lane * PAY;
     double *L0 = Ls + NIJ * SLOTS, *Lc = L0 + NIJ;
     const bool try_mom = A.moments && A.d1 - 1 >= max(2, moment_istar(rt2_lo) + 1);
+
+    // Single pass (p0 x p0, HB_FUSE1): with the moment split taken from the
+    // vertex bound rt2_hi the per-point gaps are known before the payload pass,
+    // so each point chunk feeds the moments AND the per-point gaps at once
+    // (no second payload pass); taken when those gaps fit the first window.
+    if constexpr (NIJ == 1 && HB_FUSE1) {
+        const int istar_f = moment_istar(rt2_hi), dmom_f = max(2, istar_f + 1);
+        if (try_mom && rt2_hi > 0.0 && A.d0 <= 1 && A.d1 > dmom_f && dmom_f <= 32) {
+            Win W;
+            W.w0 = A.d0;
+            W.w1 = dmom_f;
+            W.it_lo = max(1, A.d0 - 1);
+            W.it_hi = W.w1;
+            const int gw = pair_gw(istar_f);
+            const int npp = min(W.it_hi, istar_f + 1) - W.it_lo + 1;
+            const int nje = (gw == 16 && npp > 16) ? NJ : 1;
+            Slots<OP, NJ> T;
+            T.init(A, W, lane & (gw - 1));
+            const int pg = lane / gw, npg = 32 / gw;
+            double acc[NJ][NIJ], mom[2][NIJ], s0[NIJ], sc[NIJ];
+#pragma unroll
+            for (int i = 0; i < NIJ; ++i) {
+                s0[i] = sc[i] = mom[0][i] = mom[1][i] = 0.0;
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) acc[j][i] = 0.0;
+            }
+            for (int base = 0; base < nq; base += 32) {
+                double rt2;
+                int small, nzw;
+                point_payload<OP, TP1, SP1>(A, g, base + lane, nq, ny, A.need_special, p_lane, rt2, small, nzw, s0,
+                                            sc);
+                const bool any_small = __any_sync(kFull, small);
+                __syncwarp();
+                const int nloc = min(32, nq - base);
+                chunk_moments<PAY, HOFF, NIJ>(geo, Pw, rt2, nloc, mom, lane);
+                __syncwarp();
+                eval_points<OP, NIJ, PAY, HOFF, NJ>(A, T, geo, nloc, any_small, pg, npg, nje, acc, tab);
+                __syncwarp();
+            }
+            if (A.need_special) {
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+                    for (int i = 0; i < NIJ; ++i) {
+                        s0[i] += __shfl_xor_sync(kFull, s0[i], o);
+                        sc[i] += __shfl_xor_sync(kFull, sc[i], o);
+                    }
+                if (lane == 0) {
+#pragma unroll
+                    for (int i = 0; i < NIJ; ++i) {
+                        L0[i] = jac * s0[i];
+                        Lc[i] = jac * sc[i];
+                    }
+                }
+            }
+            store_moments<NIJ>(mom, Pw, lane);
+            stage_L<OP, NIJ, NJ, SLOTS>(W, T, acc, jac, istar_f + 2, gw, nje, Ls, lane);
+            __syncwarp();
+            combine_window<NIJ, SLOTS>(A, W, Ls, slot, lane);
+            __syncwarp();
+            // the bound: every term count the series cut needs is covered
+            combine_moments<NIJ>(A, slot, lane, Pw, jac, dmom_f, rt2_hi);
+            __syncwarp();
+            return;
+        }
+    }
 
     // ---- phase 1 ----
     double rmax = 0.0;
@@ -687,6 +756,9 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(kFull, rmax, o));
+    // p0 x p0 with the single-pass path: the split always comes from the vertex
+    // bound, so the blocks do not depend on which path a launch takes
+    if (NIJ == 1 && HB_FUSE1 && rt2_hi > 0.0) rmax = rt2_hi;
     // without the moment form every gap is evaluated point by point
     const int istar = A.moments ? moment_istar(rmax) : (1 << 29);
     const int dmom = max(2, istar + 1);
@@ -1014,6 +1086,29 @@ __device__ __forceinline__ bool near_test(const hb_mesh_desc &M, const double ce
 // lower bound of a separated pair's largest rho~^2: the symmetric triangle
 // rules have the centroid as weighted mean, so by convexity the largest point
 // distance is at least the centroid distance (1 - 1e-12 covers rounding)
+// an upper bound of a pair's rho~^2 from its vertices (every quadrature point
+// lies in its triangle): max over the 9 vertex pairs, rounded up by 1e-12 --
+// a function of the pair alone, so a moment split taken from it is the same
+// whatever the launch
+__device__ __forceinline__ double rt2_upper(const PairArgs &A, int64_t e, int64_t f)
+{
+    const double *ve = A.m.verts_tri_dev + 9 * e, *vf = A.m.verts_tri_dev + 9 * f;
+    double q = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double d = __ldg(ve + 3 * i + c) - __ldg(vf + 3 * j + c);
+                s = fma(d, d, s);
+            }
+            q = fmax(q, s);
+        }
+    return q * A.inv_u2 * (1.0 + 1e-12);
+}
+
 __device__ __forceinline__ double rt2_lower(const PairArgs &A, int64_t e, int64_t f)
 {
     double q = 0.0;
@@ -1613,7 +1708,8 @@ __device__ __forceinline__ void regular_item(const PairArgs &A, int64_t e, int64
         const RegularGeom g = regular_geom(M, e, ff, nf);
         double ny[3];
         for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * ff + c);
-        eval_pair<OP, TP1, SP1, NJ>(A, g, g.nq1 * g.nq1, ny, jf, rt2_lower(A, e, ff), (e - A.e0) * M.E_x + ff, W.geo,
+        eval_pair<OP, TP1, SP1, NJ>(A, g, g.nq1 * g.nq1, ny, jf, rt2_lower(A, e, ff), rt2_upper(A, e, ff),
+                                    (e - A.e0) * M.E_x + ff, W.geo,
                                     W.Ls, W.Pw, lane, tab);
     }
     if constexpr (FARC) {
@@ -1955,7 +2051,8 @@ __device__ __forceinline__ void singular_item(const PairArgs &A, int64_t k, cons
     double ny[3];
     for (int c = 0; c < 3; ++c) ny[c] = __ldg(M.normals_dev + 3 * f + c);
     // touching pairs: no lower bound of rho~^2 (0)
-    eval_pair<OP, TP1, SP1, NJ>(A, g, off1 - off0, ny, jac, 0.0, slot, W.geo, W.Ls, W.Pw, lane, tab);
+    eval_pair<OP, TP1, SP1, NJ>(A, g, off1 - off0, ny, jac, 0.0, rt2_upper(A, e, f), slot, W.geo, W.Ls, W.Pw, lane,
+                                tab);
 }
 
 // ---------------------------------------------------------------------------
