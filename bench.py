@@ -508,6 +508,8 @@ def algorithmic_rate(hb, mesh, op, n_gaps, ms):
     """SURVEY 8(d) work rate: kernel evaluations of the reference formulation per second."""
     from paper_2102_09811_b200 import workload
 
+    if not ms > 0:
+        return None
     w = workload.operator_work(mesh, op, n_gaps, hb.QuadratureConfig())
     return {"evaluations": w["n_eval"], "evaluations_per_s": w["n_eval"] / (ms * 1e-3),
             "reference_flops_per_s": w["flops"] / (ms * 1e-3),
@@ -557,22 +559,36 @@ def run_native_c2(args, rank, world, local_rank):
     if rows_mode:
         rowsV = Dm.row_partition(Dm.row_weights_mesh(mesh, q, True), world)[rank]
         rowsK = Dm.row_partition(Dm.row_weights_mesh(mesh, q, False), world)[rank]
+        # D2 split by element rows, partials read over peer memory by each rank's curl kernel
+        rpd = Dm.RowPartialD(mesh, tg, params, q, d0, d1, device=dev)
+        from paper_2102_09811_b200.assembly import _op_streams
+        sD, sV, sK = _op_streams(dev)
         dist.barrier()
 
     def step(stats=None):
         st = stats if stats is not None else [None, None, None]
         if rows_mode:
-            _assemble_operator(0, False, False, True, mesh, tg, params, q, None, d_range=(0, tg.n_steps),
-                               row_range=rowsV, block_ptrs=peersV.table, stats=st[0])
-            _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(0, tg.n_steps),
-                               row_range=rowsK, block_ptrs=peersK.table, stats=st[1])
-            # D2 d-sharded: block d needs the kernel at gaps d-1, d, d+1 only (no
-            # collective); the barrier-free d-local curl combine reads this rank's
-            # V shard after all ranks' V stores -- fenced by the device barrier below
-            _assemble_operator(2, True, True, True, mesh, tg, params, q, None, d_range=(d0, d1), out=outD,
-                               stats=st[2])
+            # the rank's V and K rows (stores into the d-owners' shards over NVLink) and
+            # its element rows' D2 partial, on three streams
+            cur = torch.cuda.current_stream()
+            for s_ in (sD, sV, sK):
+                s_.wait_stream(cur)
+            with torch.cuda.stream(sV):
+                _assemble_operator(0, False, False, True, mesh, tg, params, q, None, d_range=(0, tg.n_steps),
+                                   row_range=rowsV, block_ptrs=peersV.table, stats=st[0], stream=sV)
+            with torch.cuda.stream(sK):
+                _assemble_operator(1, False, True, False, mesh, tg, params, q, None, d_range=(0, tg.n_steps),
+                                   row_range=rowsK, block_ptrs=peersK.table, stats=st[1], stream=sK)
+            with torch.cuda.stream(sD):
+                rpd.assemble_partial(stream=sD, stats=st[2])
             torch.cuda.synchronize()
-            dist.barrier()
+            dist.barrier()   # every rank's V stores and D2 partial are complete
+            # the cross-rank sum of D2 and the curl transform of this rank's blocks in one
+            # kernel (partials read over peer memory)
+            rpd.combine(outV, outD)
+            torch.cuda.synchronize()
+            dist.barrier()   # no rank reads a partial any more
+            return
         elif stats is None:
             # the three operators on concurrent streams (public API assemble_all)
             hb.assemble_all(mesh, tg, params, q, d_range=(d0, d1), out={"V": outV, "K": outK, "D": outD})
@@ -628,6 +644,7 @@ def run_native_c2(args, rank, world, local_rank):
         dist.barrier()
         peersV.close()
         peersK.close()
+        rpd.close()
 
     # ---- e2e: public API, host buffers, copies inside the timed region ----
     Hpin = hbdev.pin_host_tables(hbdev.host_tables(mesh, q))
@@ -737,7 +754,8 @@ def run_native_c2(args, rank, world, local_rank):
         "data": "synthetic: BASELINE config-2 mesh and time grid generated in-run (no dataset)",
         "config": conf,
         "parallelism": (f"x{world}: V/K pair work split by balanced test-row ranges over all blocks, stored into the "
-                        "d-owner's shard over NVLink peer memory; D2 and the curl combine d-sharded")
+                        "d-owner's shard over NVLink peer memory; D2 split by element rows into full-size partials "
+                        "that each rank's curl kernel reads over peer memory and sums for its own blocks")
         if rows_mode else f"d-sharded x{world} (contiguous time-difference blocks per rank)",
         "l2": "flushed between timed steps (256 MiB device write, outside the events)",
         "roofline": roofline,

@@ -209,6 +209,16 @@ int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha,
                     const double *curls_dev, const double *V_dev, const double *D2_dev,
                     double *D_dev, void *workspace_dev, size_t workspace_bytes, void *stream);
 
+/* hb_curl_combine with D2 given as the sum of n_parts full-size partials
+ * (parts_dev: device array of n_parts pointers to (n_blocks_total, N, N)
+ * blocks; block d of this call is block part_d_offset + d of every part),
+ * summed in part order -- the row-parallel ranks' p1 x p1 partials read over
+ * NVLink peer memory (hb_ipc_import): the cross-rank sum of D2 and the curl
+ * transform in one kernel, no collective (distributed.hypersingular_rows_peer). */
+int hb_curl_combine_parts(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha, const double *curls_dev,
+                          const double *V_dev, int64_t n_parts, const double *const *parts_dev,
+                          int64_t part_d_offset, double *D_dev, void *stream);
+
 /* Interior potential, heatbem/_field_numba.py:15-79 (kind 0: single layer,
  * kind 1: double layer).  Evaluation outputs are grouped by spatial point and
  * time offset: group g = (gx[g], geps[g]) owns outputs gptr[g]..gptr[g+1]-1,

@@ -87,7 +87,7 @@ EXPORTED = (
     "hb_forward_solve", "hb_forward_history", "hb_inv_apply", "hb_represent_grid",
     "hb_project_workspace", "hb_project_data", "hb_p1_mass_solve", "hb_error_sigma", "hb_copy_row_slab_d2h",
     "hb_represent_grid_elem", "hb_toeplitz_apply_workspace", "hb_toeplitz_apply_ws",
-    "hb_assemble_vd", "hb_assemble_vd_min_workspace", "hb_assemble_vd_full_workspace",
+    "hb_assemble_vd", "hb_assemble_vd_min_workspace", "hb_assemble_vd_full_workspace", "hb_curl_combine_parts",
 )
 
 _lib = None
@@ -117,6 +117,8 @@ def load():
     L.hb_curl_workspace.argtypes = [ctypes.POINTER(MeshDesc), _I64]
     L.hb_curl_workspace.restype = ctypes.c_size_t
     L.hb_curl_combine.restype = _INT
+    L.hb_curl_combine_parts.argtypes = [ctypes.POINTER(MeshDesc), _I64, _D, _P, _P, _I64, _P, _I64, _P, _P]
+    L.hb_curl_combine_parts.restype = _INT
     L.hb_potential.argtypes = [_INT, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _I64,
                                _P, _P, _P, _P, _P, _D, _D, _D, _D, _P, _P]
     L.hb_potential.restype = _INT

@@ -69,7 +69,23 @@ struct CurlArgs {
     double *D;
     int64_t n_blocks;
     int dpc, ldv, smax, emax;
+    // D2 as the sum of nparts full-size partials (row-parallel ranks' p1 x p1
+    // contributions, read over NVLink peer memory): parts[p] + (part_doff + d) N^2
+    int nparts;
+    const double *const *parts;
+    int64_t part_doff;
 };
+
+// D2[d][m][n] of the combine: the contiguous D2 blocks, or the partials summed
+// in part order (deterministic)
+__device__ __forceinline__ double curl_d2(const CurlArgs &C, int64_t d, int64_t idx)
+{
+    if (C.nparts == 0) return C.D2[d * C.M.N_x * C.M.N_x + idx];
+    const int64_t off = (C.part_doff + d) * C.M.N_x * C.M.N_x + idx;
+    double s = C.parts[0][off];
+    for (int p = 1; p < C.nparts; ++p) s += C.parts[p][off];
+    return s;
+}
 
 // star entry of a tile: curl vector of (element, local hat) and the element's
 // position in the tile's element list (two 16-byte broadcast loads)
@@ -186,7 +202,7 @@ __global__ void __launch_bounds__(256) k_curl_tile(const CurlArgs C)
             }
             __syncthreads();
         }
-        const double *D2d = C.D2 + d * N * N;
+
         double *Dd = C.D + d * N * N;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -194,7 +210,7 @@ __global__ void __launch_bounds__(256) k_curl_tile(const CurlArgs C)
             const int64_t m = mm0 + ml, n = nn0 + lane;
             double val = 0.0;
             if (ml < nmr && lane < nnc && n >= m) {
-                val = fma(C.a2, acc[q], D2d[m * N + n]);
+                val = fma(C.a2, acc[q], curl_d2(C, d, m * N + n));
                 Dd[m * N + n] = val;
             }
             Dt[ml * 33 + lane] = val;
@@ -229,6 +245,10 @@ extern "C" size_t hb_curl_workspace(const hb_mesh_desc *mesh, int64_t blocks_per
     return 0;   // the tile kernel keeps its intermediates on chip
 }
 
+static int curl_launch(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha, const double *curls_dev,
+                       const double *V_dev, const double *D2_dev, double *D_dev, int nparts,
+                       const double *const *parts, int64_t part_doff, void *stream);
+
 extern "C" int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha, const double *curls_dev,
                                const double *V_dev, const double *D2_dev, double *D_dev, void *workspace_dev,
                                size_t workspace_bytes, void *stream)
@@ -238,6 +258,27 @@ extern "C" int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, doubl
         set_error("hb_curl_combine: bad arguments");
         return HB_ERR_INVALID;
     }
+    return curl_launch(mesh, n_blocks, alpha, curls_dev, V_dev, D2_dev, D_dev, 0, nullptr, 0, stream);
+}
+
+extern "C" int hb_curl_combine_parts(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha,
+                                     const double *curls_dev, const double *V_dev, int64_t n_parts,
+                                     const double *const *parts_dev, int64_t part_d_offset, double *D_dev,
+                                     void *stream)
+{
+    if (!mesh || n_blocks < 1 || !curls_dev || !V_dev || n_parts < 1 || n_parts > 64 || !parts_dev || !D_dev ||
+        part_d_offset < 0) {
+        set_error("hb_curl_combine_parts: bad arguments");
+        return HB_ERR_INVALID;
+    }
+    return curl_launch(mesh, n_blocks, alpha, curls_dev, V_dev, nullptr, D_dev, (int)n_parts, parts_dev,
+                       part_d_offset, stream);
+}
+
+static int curl_launch(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha, const double *curls_dev,
+                       const double *V_dev, const double *D2_dev, double *D_dev, int nparts,
+                       const double *const *parts, int64_t part_doff, void *stream)
+{
     if (!mesh->curl_tile_eptr_dev || !mesh->curl_tile_elem_dev || !mesh->curl_star_pos_dev ||
         mesh->curl_tile_emax < 1 || mesh->curl_tile_smax < 1) {
         set_error("hb_curl_combine: mesh descriptor has no curl tile plan");
@@ -245,6 +286,7 @@ extern "C" int hb_curl_combine(const hb_mesh_desc *mesh, int64_t n_blocks, doubl
     }
     CurlArgs C{};
     C.M = *mesh; C.a2 = alpha * alpha; C.curls = curls_dev; C.V = V_dev; C.D2 = D2_dev; C.D = D_dev;
+    C.nparts = nparts; C.parts = parts; C.part_doff = part_doff;
     C.n_blocks = n_blocks;
     C.emax = (int)mesh->curl_tile_emax;
     C.smax = (int)mesh->curl_tile_smax;

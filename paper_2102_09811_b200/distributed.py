@@ -374,6 +374,88 @@ def assemble_p1p1_row_parallel(op: int, mesh, timegrid, params, config, group=No
     return ShardedToeplitz(local, d0, d1, E_t, group)
 
 
+class RowPartialD:
+    """D = D2 + alpha^2 curl^T V curl on this rank's blocks [d0, d1) with the
+    D2 pair work split by balanced element rows: every rank
+    assembles its rows' (symmetrised) p1 x p1 contribution to ALL blocks into
+    a full-size partial (``assemble_partial``), the partials are mapped into
+    every rank over NVLink (CUDA IPC, once), and the curl kernel of each rank
+    reads and sums them in rank order for its own blocks (``combine``,
+    hb_curl_combine_parts) -- the cross-rank sum of D2 and the curl transform
+    in one kernel: no collective, no halo gaps, and every rank touches only
+    1/N of the pairs (the d split makes every rank evaluate every pair).
+    Equal to the 1-GPU D to rounding (the partial sums associate
+    differently).  Between ``assemble_partial`` and ``combine`` every rank's
+    partial must be complete, after ``combine`` no rank may overwrite its
+    partial before every rank's combine is done (host barriers)."""
+
+    def __init__(self, mesh, timegrid, params, config, d0: int, d1: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        self.mesh, self.timegrid, self.params, self.config = mesh, timegrid, params, config
+        self.d0, self.d1, self.group = d0, d1, group
+        E_t, N_x = timegrid.n_steps, mesh.n_vertices
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = world
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.rows = row_partition(row_weights_mesh(mesh, config, True, skip_perpendicular=True), world)[rank]
+        self.partial = torch.zeros((E_t, N_x, N_x), dtype=torch.float64, device=dev)
+        addrs, _, self._opened = map_peer_shards(self.partial, (0, E_t), group)
+        self.ptrs = torch.as_tensor(np.array(addrs, dtype=np.int64), device=dev)
+        self._L = _native.load()
+
+    def assemble_partial(self, workspace_bytes=None, stream=None, stats=None):
+        from .assembly import _assemble_operator
+
+        if self.rows[1] > self.rows[0]:
+            _assemble_operator(2, True, True, True, self.mesh, self.timegrid, self.params, self.config, None,
+                               d_range=(0, self.timegrid.n_steps), row_range=self.rows, out=self.partial,
+                               workspace_bytes=workspace_bytes, stream=stream, stats=stats)
+
+    def combine(self, V_local, out, stream=None):
+        from .device import device_tables
+
+        if self.d1 <= self.d0:
+            return out
+        tabs = device_tables(self.mesh, self.config, V_local.device)
+        _native.call("hb_curl_combine_parts", tabs.desc(True), self.d1 - self.d0, float(self.params.alpha),
+                     _native.ptr(tabs.t["curls"]), _native.ptr(V_local), self.world, _native.ptr(self.ptrs),
+                     self.d0, _native.ptr(out), _native.stream_handle(stream))
+        return out
+
+    def close(self):
+        for pv, o in self._opened:
+            self._L.hb_ipc_close(pv, o)
+        self._opened = []
+
+
+def hypersingular_rows_peer(mesh, timegrid, params, config, V_local, d0: int, d1: int, group=None, out=None,
+                            workspace_bytes=None):
+    """One-shot RowPartialD: D's blocks [d0, d1) on this rank.  ``V_local``:
+    V's blocks [d0, d1), complete (after the V stores of every rank)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = V_local.device
+    R = RowPartialD(mesh, timegrid, params, config, d0, d1, group, dev)
+    D = out if out is not None else torch.empty((d1 - d0, mesh.n_vertices, mesh.n_vertices), dtype=torch.float64,
+                                                device=dev)
+    try:
+        R.assemble_partial(workspace_bytes)
+        torch.cuda.synchronize(dev)
+        if R.world > 1:
+            dist.barrier(group)                  # every rank's partial is complete
+        R.combine(V_local, D)
+        torch.cuda.synchronize(dev)
+        if R.world > 1:
+            dist.barrier(group)                  # no rank reads a partial any more
+    finally:
+        R.close()
+    return D
+
+
 def gap_slots(d0: int, d1: int, window: int = 32):
     """Time gaps i_t >= 1 a rank evaluates for blocks [d0, d1) (incl. halo
     slots at window edges): the redundant work of d-sharding."""

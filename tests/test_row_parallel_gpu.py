@@ -121,3 +121,51 @@ def test_row_sharded_dirichlet_solve_three_processes():
         assert out[r]["conv"] and out[r]["res"] <= 1e-10
         assert np.array_equal(out[r]["x"], out[0]["x"])          # replicated iterates
     assert np.linalg.norm(out[0]["x"] - g["x"]) / np.linalg.norm(g["x"]) <= 1e-9
+
+
+def _d_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2102_09811_b200 as hb
+    from paper_2102_09811_b200 import distributed as D
+    from paper_2102_09811_b200.assembly import _assemble_operator
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        m = hb.unit_cube_mesh(2)
+        tg = hb.TimeGrid(1.0, 16)
+        p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
+        q = hb.QuadratureConfig()
+        d0, d1 = D.block_range(rank, world, 16)
+        V = _assemble_operator(0, False, False, True, m, tg, p, q, None, d_range=(d0, d1))
+        Dl = D.hypersingular_rows_peer(m, tg, p, q, V, d0, d1)
+        out[rank] = (d0, d1, Dl.cpu().numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_hypersingular_rows_peer_three_processes():
+    """D2 split by element rows over three ranks, the partials read over peer
+    memory (CUDA IPC on one device) and summed inside the curl kernel of each
+    rank's blocks: D equals the 1-GPU D to rounding and is exactly symmetric."""
+    import torch.multiprocessing as mp
+
+    import paper_2102_09811_b200 as hb
+
+    world = 3
+    out = mp.get_context("spawn").Manager().dict()
+    mp.start_processes(_d_worker, args=(world, _free_port(), out), nprocs=world, join=True, start_method="spawn")
+    m = hb.unit_cube_mesh(2)
+    tg = hb.TimeGrid(1.0, 16)
+    p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
+    q = hb.QuadratureConfig()
+    V = hb.assemble_single_layer(m, tg, p, q)
+    ref = hb.hypersingular_from_single_layer(V, hb.assemble_hypersingular_d2(m, tg, p, q), m, p).blocks
+    got = np.concatenate([out[r][2] for r in range(world)])
+    assert [out[r][:2] for r in range(world)] == [(0, 6), (6, 11), (11, 16)]
+    for d in range(16):
+        assert np.array_equal(got[d], got[d].T)
+        assert np.abs(got[d] - ref[d]).max() <= 1e-13 * np.abs(ref[d]).max(), d
