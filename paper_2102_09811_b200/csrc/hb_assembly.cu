@@ -2560,7 +2560,13 @@ static int launch_class(const PairArgs &A, cudaStream_t st)
     PairArgs B = A;
     const int64_t warps = (int64_t)std::max(1, per_sm) * nsm * HB_PAIR_WARPS;
     B.seg_len = 32;
-    while (B.seg_len > 4 && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < 4 * warps) B.seg_len /= 2;
+    // far batches (CLS 2) keep 32 trial elements per item: a batch combines up to
+    // 16 pairs of one item on the tensor cores (floor 4 for a rank of 8 at config 2:
+    // V 0.49 ms, floor 32: 0.37 ms)
+    static const int min_seg = getenv("HB_MIN_SEG") ? atoi(getenv("HB_MIN_SEG")) : 4;
+    static const int min_far = getenv("HB_MIN_SEG_FAR") ? atoi(getenv("HB_MIN_SEG_FAR")) : 32;
+    const int seg_floor = std::max(1, std::min(32, CLS == 2 ? min_far : min_seg));
+    while (B.seg_len > seg_floor && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < 4 * warps) B.seg_len /= 2;
     const int64_t items = (CLS == 1 || CLS == 4 ? rows * A.m.sing_max_per_row : 0) +
                           (CLS == 1 ? 0 : rows * cdiv(A.m.E_x, (int64_t)B.seg_len));
     // (near-pair items: most segments hold none and exit after the classification)

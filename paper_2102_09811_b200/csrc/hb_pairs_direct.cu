@@ -1045,7 +1045,9 @@ static int launch_pairs(const PairArgs &A, cudaStream_t st)
     PairArgs B = A;
     const int64_t warps = (int64_t)std::max(1, per_sm) * nsm * HB_PAIR_WARPS;
     B.seg_len = 32;
-    while (B.seg_len > 4 && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < 4 * warps) B.seg_len /= 2;
+    static const int min_seg = getenv("HB_MIN_SEG") ? atoi(getenv("HB_MIN_SEG")) : 4;
+    const int seg_floor = std::max(1, std::min(32, min_seg));
+    while (B.seg_len > seg_floor && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < 4 * warps) B.seg_len /= 2;
     const int64_t items = rows * cdiv(A.m.E_x, (int64_t)B.seg_len) + rows * A.m.sing_max_per_row;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(1, per_sm) * nsm, cdiv(items, HB_PAIR_WARPS)));
     int rc = cuda_check(cudaMemsetAsync(A.counter, 0, sizeof(unsigned long long), st), "counter reset");
