@@ -48,6 +48,37 @@ def window_edges(n_blocks: int):
     return edges
 
 
+def cost_balanced_ranges(costs, n_blocks: int, world: int, edges=None):
+    """Contiguous d-ranges of near-equal measured cost, one per rank.
+
+    ``costs``: (d0, d1, ms) pieces covering [0, n_blocks) (e.g. the chunk
+    times of a first step on block_range's split, gathered from every rank);
+    the cost of a piece is spread evenly over its blocks.  Boundaries snap to
+    the nearest of ``edges`` (window edges: a range edge inside a window
+    costs extra gap slots) when that keeps the range non-empty.  With the
+    moment form the low blocks are the expensive ones (per-point gaps below
+    each pair's moment block), so equal block counts leave rank 0 with the
+    most work (config 5, N = 8: balance 0.60)."""
+    dens = np.zeros(n_blocks)
+    for d0, d1, ms in costs:
+        if d1 > d0:
+            dens[int(d0):int(d1)] += float(ms) / (int(d1) - int(d0))
+    if not np.all(dens > 0):
+        dens = np.where(dens > 0, dens, dens[dens > 0].mean() if np.any(dens > 0) else 1.0)
+    cum = np.concatenate([[0.0], np.cumsum(dens)])
+    cuts = [0]
+    for r in range(1, world):
+        c = int(np.searchsorted(cum, cum[-1] * r / world))
+        c = min(max(c, cuts[-1] + 1), n_blocks - (world - r))
+        if edges is not None:
+            e = min(edges, key=lambda x: abs(x - c))
+            if cuts[-1] < e < n_blocks - (world - r) + 1 and abs(e - c) <= 8:
+                c = e
+        cuts.append(c)
+    cuts.append(n_blocks)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
 def aligned_chunks(n_blocks: int, max_blocks: int):
     """Contiguous d-chunks of at most ``max_blocks`` blocks that start and
     end on window edges (so chunked assembly evaluates no extra gap slots);

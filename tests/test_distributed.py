@@ -26,6 +26,25 @@ def test_block_ranges_cover_exactly_once():
             assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
 
 
+def test_cost_balanced_ranges_equalise_measured_cost():
+    """Front-loaded block costs (the moment form's low blocks): the measured
+    split gives contiguous, covering ranges of near-equal cost, where the
+    equal-count split leaves rank 0 with the most work."""
+    VD = [824, 395, 298, 297, 421, 297, 297, 351]   # B200, config 5, ms per 32-block chunk
+    costs = [(32 * i, 32 * i + 32, c) for i, c in enumerate(VD)]
+    dens = np.repeat(np.array(VD) / 32.0, 32)
+    for world in (2, 4, 8):
+        r = D.cost_balanced_ranges(costs, 256, world)
+        assert r[0][0] == 0 and r[-1][1] == 256 and all(a < b for a, b in r)
+        assert all(r[i][1] == r[i + 1][0] for i in range(world - 1))
+        per = [dens[a:b].sum() for a, b in r]
+        uni = [dens[a:b].sum() for a, b in (D.block_range(k, world, 256) for k in range(world))]
+        assert max(per) < max(uni) and sum(per) / (world * max(per)) > 0.9
+    edges = D.window_edges(256)
+    r = D.cost_balanced_ranges(costs, 256, 8, edges)
+    assert r[0][0] == 0 and r[-1][1] == 256 and all(a < b for a, b in r)
+
+
 def test_gap_slots_halo_accounting():
     assert D.gap_slots(0, 32) == 32
     assert D.gap_slots(0, 16) + D.gap_slots(16, 32) == 34        # one extra halo pair
