@@ -1512,6 +1512,122 @@ __device__ __forceinline__ void fused_blocks_k(const PairArgs &A, const double *
     }
 }
 
+// ---------------------------------------------------------------------------
+// K far batches from a per-point payload (HB_KFAR_PAYLOAD): the geometry of a
+// pair's point pairs -- t = rho~^2, rho, 1/rho and both orientations' six
+// weights -- is formed ONCE per point pair by the pair's 8 lanes into shared
+// memory, and the moment loop (lane: 4 moments x 6 outputs) and the per-point
+// gap loop (lane: one gap) read it back, instead of every lane recomputing
+// sqrt, 1/rho, the normal products and the weights per point pair.
+// Payload of point pair q of pair ps: Pk[(ps nq + q) kKPay + .] =
+//   [t, rho, 1/rho, -, Wf0, Wf1, Wf2, Wr0, Wr1, Wr2]   (LDS.128-aligned pairs)
+// ---------------------------------------------------------------------------
+#ifndef HB_KFAR_PAYLOAD
+#define HB_KFAR_PAYLOAD 1
+#endif
+constexpr int kKPay = 10;
+constexpr int kKFarPts = 36;   // payload room: regular rules of <= 6 points (the default order 4)
+
+// lane (ps, g) of the batch forms the payload of point pairs q = g, g + 8, ...;
+// returns the pair's largest t (reduced over its 8 lanes)
+__device__ __forceinline__ double far_payload_k(const PairArgs &A, const FarGeom &G, const double nb[3],
+                                                const double na[3], double *Pk, int g)
+{
+    constexpr int LPP = 32 / FarCfg<6>::PB;
+    const int nq1 = G.nq1, nq = nq1 * nq1;
+    double tmax = 0.0;
+    for (int q = g; q < nq; q += LPP) {
+        const int p = q / nq1, r = q - p * nq1;
+        const double rx = G.xp[3 * p] - G.yp[3 * r], ry = G.xp[3 * p + 1] - G.yp[3 * r + 1],
+                     rz = G.xp[3 * p + 2] - G.yp[3 * r + 2];
+        const double r2 = rx * rx + ry * ry + rz * rz;
+        const double t = r2 * A.inv_u2;
+        tmax = fmax(tmax, t);
+        const double rho = sqrt(r2);
+        const double rnb = rx * nb[0] + ry * nb[1] + rz * nb[2];
+        const double rna = (-rx) * na[0] + (-ry) * na[1] + (-rz) * na[2];
+        const double wq = G.w[p] * G.w[r];
+        double *o = Pk + q * kKPay;
+        o[0] = t;
+        o[1] = rho;
+        o[2] = 1.0 / rho;
+        o[3] = 0.0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            o[4 + i] = ((wq * (1.0 * G.hats[3 * r + i])) * (-rnb)) * A.inv2a;
+            o[7 + i] = ((wq * (1.0 * G.hats[3 * p + i])) * (-rna)) * A.inv2a;
+        }
+    }
+#pragma unroll
+    for (int o = 1; o < LPP; o <<= 1) tmax = fmax(tmax, __shfl_xor_sync(kFull, tmax, o));
+    return tmax;
+}
+
+// moments k in [KPL g, KPL g + KPL) of both orientations from the payload
+__device__ __forceinline__ void far_moments_k2(const double *Pk, int nq, double (&mom)[6][FarCfg<6>::KPL], int g)
+{
+    constexpr int KPL = FarCfg<6>::KPL;
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) mom[i][k] = 0.0;
+#pragma unroll 2
+    for (int q = 0; q < nq; ++q) {
+        const double2 *o = reinterpret_cast<const double2 *>(Pk + q * kKPay);
+        const double t = o[0].x;
+        const double2 w01 = o[2], w23 = o[3], w45 = o[4];
+        const double Wt[6] = {w01.x, w01.y, w23.x, w23.y, w45.x, w45.y};
+        double pw = group_start_pow<KPL>(t, g);
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) {
+#pragma unroll
+            for (int i = 0; i < 6; ++i) mom[i][k] = fma(Wt[i], pw, mom[i][k]);
+            pw = __dmul_rn(pw, t);
+        }
+    }
+}
+
+// lane (ps, g): when `pp`, the per-point sum of gap g + 1 (acc[o]); `spec`: the
+// delta = 0 sums of the point pairs q = g mod 8 -- from the payload.  Called
+// warp-uniformly (every lane takes part in the region votes).
+__device__ __forceinline__ void far_pp_k2(const PairArgs &A, const double *Pk, int nq, int g, bool pp, bool spec,
+                                          double (&acc)[6], double (&s0f)[3], double (&scf)[3], double (&s0r)[3],
+                                          double (&scr)[3], const double *tab)
+{
+    constexpr int LPP = 32 / FarCfg<6>::PB;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s0f[i] = scf[i] = s0r[i] = scr[i] = 0.0;
+    double cx, ic;
+    gap_consts(A, g + 1, cx, ic);
+    const double k2 = 2.0 * A.alpha * A.step;   // cc / c0 = 1 - step P / inv2a
+    for (int q = 0; q < nq; ++q) {
+        const double2 *o = reinterpret_cast<const double2 *>(Pk + q * kKPay);
+        const double2 tr = o[0], ii = o[1], w01 = o[2], w23 = o[3], w45 = o[4];
+        const double rho = tr.y, iq = ii.x;
+        const double W[6] = {w01.x, w01.y, w23.x, w23.y, w45.x, w45.y};
+        double xs[1] = {__dmul_rn(rho, cx)}, fs[1];
+        special::eval_nf<5, 1>(xs, [&](int) { return __dmul_rn(iq, ic); }, fs, tab, kFull);
+        if (pp) {
+#pragma unroll
+            for (int i = 0; i < 6; ++i) acc[i] = fma(fs[0], W[i], acc[i]);
+        }
+        if (spec && (q % LPP) == g) {
+            // (w hs (-r.n) / rho) c0 = W iq, (...) cc = W iq (1 - 2 a h / rho^2)
+            const double f = 1.0 - k2 * __dmul_rn(iq, iq);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const double af = W[i] * iq, ar = W[3 + i] * iq;
+                s0f[i] += af;
+                scf[i] = fma(af, f, scf[i]);
+                s0r[i] += ar;
+                scr[i] = fma(ar, f, scr[i]);
+            }
+        }
+    }
+}
+
 // Fused lane-level V far path (2 lanes per pair): lane (ps, g) evaluates
 // x H at the pair's gaps g + 1, g + 3, g + 5, g + 7 (four interleaved Horner
 // chains) over its point pairs and, when `spec`, the delta = 0 sums of the
@@ -1890,9 +2006,17 @@ __device__ __forceinline__ void regular_item_dual(const PairArgs &A, int64_t e, 
         stage_far_points<LPP>(M, aa, bb, Xs, gk);
         __syncwarp();
         const FarGeom g{Xs, Xs + n3, W.rw, W.rh, (int)M.n_reg};
-        // the pair's largest rho~^2 first: it decides istar, dmom and whether the
-        // per-point gaps fit the fused lane path
+        const int nqf = (int)(M.n_reg * M.n_reg);
+#if HB_KFAR_PAYLOAD
+        const bool kpay = nqf <= kKFarPts;   // warp-uniform
+        double *Pk = W.geo + ((PB * (2 * n3 + 1) + 1) & ~1) + ps * nqf * kKPay;
+        // the payload, with the pair's largest rho~^2: it decides istar, dmom and
+        // whether the per-point gaps fit the fused lane path
+        const double rmax = kpay ? far_payload_k(A, g, nb, na, Pk, gk) : far_rmax<LPP>(A, g, gk);
+        __syncwarp();
+#else
         const double rmax = far_rmax<LPP>(A, g, gk);
+#endif
         const int istar = moment_istar(rmax), dmom = max(2, istar + 1);
         const bool fused = pv && istar + 1 <= kFusedMaxGap;
         const bool pp = fused && A.d0 < dmom;
@@ -1900,8 +2024,18 @@ __device__ __forceinline__ void regular_item_dual(const PairArgs &A, int64_t e, 
         int64_t sf = -1, sr = -1;
         slots(aa, bb, sf, sr);
         const double jac = pair_jac<1>(A, aa, bb);
+#if HB_KFAR_PAYLOAD
+        if (kpay) {
+            far_moments_k2(Pk, nqf, mom, gk);
+            if (pp_any) far_pp_k2(A, Pk, nqf, gk, pp, pp && A.need_special, acc, s0f, scf, s0r, scr, tab);
+        } else {
+            far_moments_k(A, g, nb, na, mom, gk);
+            if (pp_any) far_pp_k(A, g, nb, na, gk, pp, pp && A.need_special, acc, s0f, scf, s0r, scr, tab);
+        }
+#else
         far_moments_k(A, g, nb, na, mom, gk);
         if (pp_any) far_pp_k(A, g, nb, na, gk, pp, pp && A.need_special, acc, s0f, scf, s0r, scr, tab);
+#endif
         __syncwarp();   // the staged points are overwritten from here on
         if (pp_any) {
             // staged L row per pair: [o][0] = L0, [o][1..8] = gaps, [o][9] = Lcomb0
@@ -2000,11 +2134,20 @@ __host__ __device__ constexpr int smem_doubles_per_warp()
         return smem_doubles_per_warp_base<OP, NIJ, NJ>();
     }
 }
+// K far batches from a payload: the staged points of the batch + PB x 36 x kKPay
+// payload doubles (the regular rule of <= kFarMaxRule points: 49 point pairs)
+__host__ __device__ constexpr int kfar_payload_doubles()
+{
+    return HB_KFAR_PAYLOAD ? ((FarCfg<6>::PB * (6 * kFarMaxRule + 1) + 1) & ~1) + FarCfg<6>::PB * kKFarPts * kKPay
+                           : 0;
+}
+
 template <int NJ>
 __host__ __device__ constexpr int dual_smem_doubles_per_warp()
 {
-    return dual_smem_doubles_per_warp_base<NJ>() > far_smem_doubles<6>() ? dual_smem_doubles_per_warp_base<NJ>()
-                                                                         : far_smem_doubles<6>();
+    constexpr int a = dual_smem_doubles_per_warp_base<NJ>() > far_smem_doubles<6>()
+                          ? dual_smem_doubles_per_warp_base<NJ>() : far_smem_doubles<6>();
+    return a > kfar_payload_doubles() ? a : kfar_payload_doubles();
 }
 
 // ---------------------------------------------------------------------------
