@@ -679,6 +679,52 @@ __device__ __forceinline__ void eval_erf_E(double x, const double *__restrict__ 
     }
 }
 
+// factor-free forms for k_represent_elem (HB_REP_FF): erf(x)/x and E(x)/x^3
+// (kinds 6, 7) -- the per-point factors 1/rho and rn/rho^3 of the two
+// potentials turn into per-gap constants cm/(4 pi alpha) and cm^3 applied
+// once to the node sums; no finishing multiplies or region selects per value
+__device__ __forceinline__ void eval_ex_Ex3(double x, double ix, const double *__restrict__ tabS,
+                                            const double *__restrict__ tabD, double &rs, double &rd)
+{
+    const double t = __dmul_rn(x, x);
+    const bool small = x < special::kX0;
+    if (!__any_sync(kFull, !small)) {
+        rs = special::series<6>(x, t, 0.0);
+        rd = special::series<7>(x, t, 0.0);
+        return;
+    }
+    const bool midr = !small && x < special::kXL, huge = !small && !midr;
+    if (__any_sync(kFull, midr)) {
+        double u;
+        const int pc = special::mid_piece(x, u);
+        const int col[1] = {small ? special::kMidPieces : pc};
+        const double v[1] = {small ? t : u};
+        double qs[1], qd[1];
+        if (__any_sync(kFull, small)) {
+            special::table_chains<6, special::merged_deg<6>(), 1>(tabS, col, v, qs);
+            special::table_chains<7, special::merged_deg<7>(), 1>(tabD, col, v, qd);
+        } else {
+            special::table_chains<6, special::mid_deg<6>(), 1>(tabS, col, v, qs);
+            special::table_chains<7, special::mid_deg<7>(), 1>(tabD, col, v, qd);
+        }
+        rs = qs[0];
+        rd = qd[0];
+    } else {
+        rs = special::series<6>(x, t, 0.0);
+        rd = special::series<7>(x, t, 0.0);
+    }
+    if (__any_sync(kFull, huge)) {
+        if (huge) {
+            rs = ix;
+            rd = __dmul_rn(__dmul_rn(ix, ix), ix);
+        }
+    }
+}
+
+#ifndef HB_REP_FF
+#define HB_REP_FF 1
+#endif
+
 struct RepArgs {
     int64_t n_points, n_times, E_t, E_x, nq;
     const double *x;        // (n_points, 3)
@@ -1079,7 +1125,7 @@ struct RepElemLayout {
     static_assert(GS % 16 == 4, "conflict-free H fragment loads need a row stride of 4 mod 16");
     static size_t doubles(int64_t nq)
     {
-        return 2 * (size_t)special::kTabDoubles + 4 * kFP * GS + 3 * (size_t)nq * kFP + 2 * 4 * BR +
+        return 2 * (size_t)special::kTabDoubles + 4 * kFP * GS + (HB_REP_FF ? 5 : 3) * (size_t)nq * kFP + 2 * 4 * BR +
                2 * 2 * 4 * (KM + 1);
     }
 };
@@ -1104,8 +1150,15 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
     double *Tv = L0d + nq * kFP;                // [2 buf][4][BR]: density differences, zeros before
     double *Av = Tv + 2 * 4 * BR;               // [2 buf][4][KM + 1]: m = 0 row
     double *Dv = Av + 2 * 4 * (KM + 1);         // [2 buf][4][KM + 1]: density (EPS: the G(0) term)
+    double *Ri = Dv + 2 * 4 * (KM + 1);         // HB_REP_FF: [nq][kFP] 1/rho
+    double *Rq = Ri + nq * kFP;                 // HB_REP_FF: [nq][kFP] rn / (4 pi) (0 for rho <= r_eps)
+#if HB_REP_FF
+    special::load_table<6>(tabS);
+    special::load_table<7>(tabD);
+#else
     special::load_table<2>(tabS);
     special::load_table<3>(tabD);
+#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < 4 * kFP * GS; i += kFTE) H[i] = 0.0;   // padding rows m > KM stay zero
     for (int i = tid; i < 2 * 4 * BR; i += kFTE) Tv[i] = 0.0;    // leading zeros stay zero
@@ -1113,12 +1166,13 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
     const int64_t pblock = blockIdx.x / n_split;
     const int64_t e_lo = P.E_x * split / n_split, e_hi = P.E_x * (split + 1) / n_split;
     constexpr int kS = (KM + 1 - MOFS + 31) / 32;   // lane passes over m = MOFS..KM
-    double cm[kS], gsmall[kS];
+    double cm[kS], gsmall[kS], icm[kS];
     bool gzero[kS];
 #pragma unroll
     for (int s = 0; s < kS; ++s) {
         const double gap = (double)(lane + MOFS + 32 * s) * P.step + (EPS ? P.eps : 0.0);
-        cm[s] = 1.0 / (2.0 * sqrt(P.alpha * gap));
+        icm[s] = 2.0 * sqrt(P.alpha * gap);
+        cm[s] = 1.0 / icm[s];
         gsmall[s] = 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (P.alpha * P.alpha * P.alpha) * gap));
         gzero[s] = gap <= P.d_eps;
     }
@@ -1147,6 +1201,10 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
             Rn[it] = rho;
             L0s[it] = 1.0 / (4.0 * kPi * P.alpha * rho);
             L0d[it] = rho <= P.r_eps ? 0.0 : inv4pi * rn / (rho * rho * rho);
+            if (HB_REP_FF) {
+                Ri[it] = 1.0 / rho;
+                Rq[it] = rho <= P.r_eps ? 0.0 : inv4pi * rn;
+            }
         }
         {
             double *tv = Tv + buf * 4 * BR + ZP, *av = Av + buf * 4 * (KM + 1), *dd = Dv + buf * 4 * (KM + 1);
@@ -1186,6 +1244,23 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
                 hz[1] = fma(wh0, l0d, hz[1]);
                 hz[2] = fma(wh1, l0d, hz[2]);
                 hz[3] = fma(wh2, l0d, hz[3]);
+#if HB_REP_FF
+                const double ri = Ri[node * kFP + p], rq = Rq[node * kFP + p];
+                (void)rsmall;
+#pragma unroll
+                for (int s = 0; s < kS; ++s) {
+                    double fs, fd;
+                    eval_ex_Ex3(__dmul_rn(rho, cm[s]), __dmul_rn(ri, icm[s]), tabS, tabD, fs, fd);
+                    // (scaled by cm / (4 pi a) and cm^3 after the node sum; rho <= r_eps:
+                    // erf(x)/x -> 2/sqrt(pi), the reference's limit, and rq = 0)
+                    const double vs = gzero[s] ? l0s : fs;
+                    const double vd = gzero[s] ? l0d : __dmul_rn(rq, fd);
+                    hsum[0][s] = fma(W, vs, hsum[0][s]);
+                    hsum[1][s] = fma(wh0, vd, hsum[1][s]);
+                    hsum[2][s] = fma(wh1, vd, hsum[2][s]);
+                    hsum[3][s] = fma(wh2, vd, hsum[3][s]);
+                }
+#else
 #pragma unroll
                 for (int s = 0; s < kS; ++s) {
                     double fs, fd;
@@ -1197,7 +1272,19 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
                     hsum[2][s] = fma(wh1, vd, hsum[2][s]);
                     hsum[3][s] = fma(wh2, vd, hsum[3][s]);
                 }
+#endif
             }
+#if HB_REP_FF
+#pragma unroll
+            for (int s = 0; s < kS; ++s) {
+                if (!gzero[s]) {
+                    const double cs = cm[s] * (0.25 * kInvPi / P.alpha), cd = cm[s] * cm[s] * cm[s];
+                    hsum[0][s] *= cs;
+#pragma unroll
+                    for (int v = 1; v < 4; ++v) hsum[v][s] *= cd;
+                }
+            }
+#endif
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 double *h = H + (v * kFP + p) * GS;

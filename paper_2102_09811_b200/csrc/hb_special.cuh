@@ -61,6 +61,7 @@ __host__ __device__ constexpr int series_deg()
     return (KIND == 0 || KIND == 4 ? (int)(sizeof(kPh) / sizeof(double))
             : KIND == 1 || KIND == 5 ? (int)(sizeof(kPf) / sizeof(double))
             : KIND == 2 || KIND == 6 ? (int)(sizeof(kPe) / sizeof(double)) : (int)(sizeof(kPg) / sizeof(double))) - 1;
+    // (kinds 3 E and 7 E/x^3 share Pg: E = x^3 Pg(t))
 }
 
 template <int KIND>
@@ -68,7 +69,7 @@ __host__ __device__ constexpr int merged_deg() { return mid_deg<KIND>() > series
 
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int kMergedDegMax = cmax(cmax(cmax(merged_deg<0>(), merged_deg<1>()), cmax(merged_deg<2>(), merged_deg<3>())),
-                                   cmax(cmax(merged_deg<4>(), merged_deg<5>()), merged_deg<6>()));
+                                   cmax(cmax(merged_deg<4>(), merged_deg<5>()), cmax(merged_deg<6>(), merged_deg<7>())));
 constexpr int kTabDoubles = ((kMergedDegMax + 2) & ~1) * kTabStride;   // room for any kind / layout
 
 // the kinds 2-6 (pair kernels, potentials) store coefficients 2m and 2m+1 of a
@@ -82,7 +83,7 @@ template <int KIND>
 __device__ __forceinline__ void load_table(double *tab)
 {
     const double *mid = KIND == 0 ? kMid0 : KIND == 1 ? kMid1 : KIND == 2 ? kMid2 : KIND == 3 ? kMid3
-                      : KIND == 4 ? kMid4 : KIND == 5 ? kMid5 : kMid6;
+                      : KIND == 4 ? kMid4 : KIND == 5 ? kMid5 : KIND == 6 ? kMid6 : kMid7;
     const double *ser = (KIND == 0 || KIND == 4) ? kPh : (KIND == 1 || KIND == 5) ? kPf
                       : (KIND == 2 || KIND == 6) ? kPe : kPg;
     constexpr int DM = mid_deg<KIND>(), DS = series_deg<KIND>(), D = merged_deg<KIND>();
@@ -167,6 +168,7 @@ __device__ __forceinline__ double series(double x, double t, double ix)
     if (KIND == 3) return __dmul_rn(__dmul_rn(x, t), horner(kPg, t));
     if (KIND == 4) return fma(t, horner(kPh, t), kTwoInvSqrtPi);   // x H = 2/sqrt(pi) + t Ph(t)
     if (KIND == 5) return horner(kPf, t);                          // F / x
+    if (KIND == 7) return horner(kPg, t);                          // E / x^3
     return horner(kPe, t);                                         // erf / x
 }
 
@@ -176,6 +178,7 @@ __device__ __forceinline__ double asymptote(double x, double ix)
 {
     if (KIND == 2 || KIND == 3) return 1.0;
     if (KIND == 6) return ix;                            // erf / x
+    if (KIND == 7) return __dmul_rn(__dmul_rn(ix, ix), ix);   // E / x^3
     if (KIND == 4) return fma(0.5, ix, x);               // x H = x + 1/(2x)
     const double hx = __dmul_rn(0.5 * ix, ix);
     if (KIND == 5) return __dmul_rn(ix, 1.0 - hx);       // F / x = (1 - 1/(2x^2)) / x

@@ -33,7 +33,7 @@ MID_W = mp.mpf(os.environ.get("HB_MID_W", "0.25"))
 MID_PIECES = int(os.environ.get("HB_MID_PIECES", "21"))
 DEG_M = {k: int(os.environ.get(f"HB_DEGM_{k}", os.environ.get("HB_DEGM", d)))
          for k, d in (("H", "12"), ("F", "10"), ("erf", "10"), ("E", "11"), ("xH", "9"), ("Fx", "9"),
-                      ("ex", "10"))}
+                      ("ex", "10"), ("Ex3", "11"))}
 
 
 def F_H(x):
@@ -63,6 +63,10 @@ def F_Fx(x):
 
 def F_ex(x):
     return mp.erf(x) / x
+
+
+def F_Ex3(x):   # E(x) / x^3 (double-layer potential, factor-free: E rn / rho^3 = [E / x^3] rn cx^3)
+    return F_E(x) / (x * x * x)
 
 
 def S_e(t):
@@ -164,14 +168,14 @@ def main():
     XL = X0 + MID_W * MID_PIECES
     out.append(f"constexpr double kXL = {hexd(XL)};   // middle / asymptotic switch")
     out.append(f"constexpr int kMidPieces = {MID_PIECES};")
-    names = ("H", "F", "erf", "E", "xH", "Fx", "ex")
-    out.append("// degree of the middle-region pieces per kind (0 H, 1 F, 2 erf, 3 E, 4 xH, 5 F/x, 6 erf/x)")
-    out.append("constexpr int kMidDegK[7] = {" + ", ".join(str(DEG_M[n]) for n in names) + "};")
+    names = ("H", "F", "erf", "E", "xH", "Fx", "ex", "Ex3")
+    out.append("// degree of the middle-region pieces per kind (0 H, 1 F, 2 erf, 3 E, 4 xH, 5 F/x, 6 erf/x, 7 E/x^3)")
+    out.append("constexpr int kMidDegK[8] = {" + ", ".join(str(DEG_M[n]) for n in names) + "};")
     out.append(f"constexpr int kMidDegMax = {max(DEG_M.values())};")
     out.append(f"constexpr double kMidInvW = {hexd(1 / MID_W)};")
     out.append(f"constexpr double kMidInvHalf = {hexd(2 / MID_W)};")
     for kind, (fname, f) in enumerate((("H", F_H), ("F", F_F), ("erf", mp.erf), ("E", F_E), ("xH", F_xH),
-                                       ("Fx", F_Fx), ("ex", F_ex))):
+                                       ("Fx", F_Fx), ("ex", F_ex), ("Ex3", F_Ex3))):
         worst, tab = 0, []
         for pc in range(MID_PIECES):
             a = X0 + MID_W * pc
@@ -186,7 +190,7 @@ def main():
         asym = {"H": lambda x: 1 + 1 / (2 * x * x), "F": lambda x: 1 - 1 / (2 * x * x),
                 "erf": lambda x: mp.mpf(1), "E": lambda x: mp.mpf(1),
                 "xH": lambda x: (x + 1 / (2 * x) - 2 / SQPI) / (x * x), "Fx": lambda x: 1 / x - 1 / (2 * x * x * x),
-                "ex": lambda x: 1 / x}[fname]
+                "ex": lambda x: 1 / x, "Ex3": lambda x: 1 / (x * x * x)}[fname]
         tail = max(abs(asym(XL + k / mp.mpf(8)) - f(XL + k / mp.mpf(8))) / abs(f(XL + k / mp.mpf(8))) for k in range(40))
         report.append(f"mid {fname}: {MID_PIECES} pieces x degree {DEG_M[fname]} on [{float(X0)}, {float(XL)}), "
                       f"max rel err (double Horner) {float(worst):.2e}; asymptote rel err for x >= XL {float(tail):.1e}")
