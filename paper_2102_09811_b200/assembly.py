@@ -582,8 +582,6 @@ def curl_combine_into(tabs, Vd, D2d, out, alpha: float, stream=None, workspace_c
     per = L.hb_curl_workspace(m, 1)
     nb = Vd.shape[0]
     ws = torch.empty(max(per, min(per * nb, workspace_cap)), dtype=torch.uint8, device=Vd.device)
-    if os.environ.get("HB_DEBUG_SKIP_CURL"):   # timing experiments only: D = D2 (wrong values)
-        return
     with torch.cuda.device(Vd.device):
         _native.call("hb_curl_combine", m, nb, alpha, _native.ptr(tabs.t["curls"]), _native.ptr(Vd),
                      _native.ptr(D2d), _native.ptr(out), _native.ptr(ws), ws.numel(), _native.stream_handle(stream))
