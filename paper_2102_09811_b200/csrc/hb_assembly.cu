@@ -2647,37 +2647,72 @@ static bool combo_ok(const hb_assembly_desc *a)
 
 constexpr size_t kCounterBytes = 256;
 
-// moment form: always for the single layer (its accuracy at large d carries
-// into D through the curl transform); for D2 when the time grid has enough
-// steps (E_t >= 64) for the per-pair moments to replace many cheap per-point
-// gaps -- below that the direct kernel (hb_pairs_direct.cu) is faster.  K
-// keeps the direct dual-orientation kernel at every E_t: one F evaluation
-// feeds both orientations there, while its moment form needs the 6 moment
-// sets and 6 combines per pair (B200: c2 1.64 vs 2.97 ms, level 4 / E_t 64
-// 47.1 vs 50.6 ms).  Decided by (op, E_t) only, so d-sharded calls of one
-// operator agree bitwise.  HB_MOMENTS=0/1 overrides for every operator.
-static int use_moments(const hb_assembly_desc *a)
+// Which blocks the moment form computes: blocks d >= moment_from(op, E_t).
+// * E_t < 64 (config 2 size): V throughout (its moments beat the per-point
+//   gaps there: 1.03 vs 1.23 ms), K and D2 never (direct kernel: K's
+//   dual-orientation body feeds both orientations from one F evaluation).
+// * E_t >= 64: V and D2 direct below block 32 and moments from block 32; K
+//   (E_t >= 128) from block 62 (a direct-window edge).
+//   At small gaps each pair's moment block lies high (many per-point gaps below
+//   it) and the direct kernel is faster; above, the moments win (B200, config
+//   5, pair ms per block range direct / moments: V [0,32) 282 / 383,
+//   [32,62) 212 / 88, [62,92) 175 / 41; D2 174 / 318, 134 / 115, 121 / 83;
+//   K 393 / 923, 296 / 267, 244 / 176).
+// A function of (op, E_t) only, so a block is computed the same way whatever
+// d-range a call (chunk, rank) covers: d-sharded calls agree bitwise.
+// HB_MOMENTS=0/1 overrides (never / always), HB_MOMENT_FROM the switch block.
+static int64_t moment_from(const hb_assembly_desc *a)
 {
     static const int env = getenv("HB_MOMENTS") ? (atoi(getenv("HB_MOMENTS")) != 0) : -1;
-    if (env >= 0) return env;
-    if (a->op == HB_OP_SINGLE_LAYER) return 1;
-    return (a->op == HB_OP_HYPERSINGULAR2 && a->E_t >= 64) ? 1 : 0;
+    static const int64_t sw = getenv("HB_MOMENT_FROM") ? atoll(getenv("HB_MOMENT_FROM")) : 32;
+    const int64_t never = INT64_MAX / 4;
+    if (env == 1) return 0;
+    if (env == 0) return never;
+    if (a->op == HB_OP_DOUBLE_LAYER)   // K: the moment form pays only far out (config 3, E_t 64: it does not)
+        return a->E_t >= 128 ? std::max<int64_t>(sw, 62) : never;
+    if (a->E_t >= 64) return sw;
+    return a->op == HB_OP_SINGLE_LAYER ? 0 : never;
+}
+
+// the moment form for a call (a part of one) that starts at d_begin
+static int use_moments(const hb_assembly_desc *a) { return a->d_begin >= moment_from(a) ? 1 : 0; }
+
+// the direct and moment parts of a call's blocks [d_begin, d_end)
+struct CallPart {
+    int64_t lo, hi;
+    bool mom;
+};
+static int call_parts(const hb_assembly_desc *a, CallPart (&p)[2])
+{
+    const int64_t sw = std::max(a->d_begin, std::min(a->d_end, moment_from(a)));
+    int n = 0;
+    if (a->d_begin < sw) p[n++] = {a->d_begin, sw, false};
+    if (sw < a->d_end) p[n++] = {sw, a->d_end, true};
+    return n;
 }
 
 // staging of one test row: every trial element x NIJ x the blocks of one
-// launch (all blocks of the call in the moment form, a 32-gap window direct)
+// launch (all blocks of the moment part, a 32-gap window of the direct part)
 static size_t row_bytes(const hb_mesh_desc *m, const hb_assembly_desc *a)
 {
-    const int64_t nd = a->d_end - a->d_begin;
-    return (size_t)m->E_x * op_nij(a) * (size_t)(use_moments(a) ? nd : std::min<int64_t>(nd, 32)) * sizeof(double);
+    CallPart p[2];
+    const int n = call_parts(a, p);
+    int64_t nd = 1;
+    for (int i = 0; i < n; ++i) nd = std::max(nd, p[i].mom ? p[i].hi - p[i].lo : std::min<int64_t>(p[i].hi - p[i].lo, 32));
+    return (size_t)m->E_x * op_nij(a) * (size_t)nd * sizeof(double);
 }
 
-// moment table of the call (k_moment_table), 256-byte rounded
+// moment table of the moment part (k_moment_table), 256-byte rounded
 static size_t tm_bytes(const hb_assembly_desc *a)
 {
-    if (!use_moments(a)) return 0;
-    const size_t n = (size_t)kNK * (size_t)(a->d_end - a->d_begin) + kNK + 1;
-    return (n * sizeof(double) + 255) & ~(size_t)255;
+    CallPart p[2];
+    const int n = call_parts(a, p);
+    for (int i = 0; i < n; ++i)
+        if (p[i].mom) {
+            const size_t k = (size_t)kNK * (size_t)(p[i].hi - p[i].lo) + kNK + 1;
+            return (k * sizeof(double) + 255) & ~(size_t)255;
+        }
+    return 0;
 }
 
 // one class of pair items: CLS 1 touching pairs (Sauter-Schwab), 3 separated
@@ -3042,30 +3077,38 @@ extern "C" int hb_assemble(const hb_mesh_desc *m, const hb_assembly_desc *a, voi
         rc = cuda_check(cudaMemsetAsync(a->blocks_dev, 0, (size_t)nb * R * R * sizeof(double), st), "memset");
         if (rc) return rc;
     }
-    PairArgs A = make_pair_args(m, a);
-    A.Q = (double *)a->workspace_dev;
     double *Tm = (double *)((char *)a->workspace_dev + q_bytes);
-    A.Tm = Tm;
-    A.counter = (unsigned long long *)((char *)a->workspace_dev + q_bytes + tb);
-
     LaunchTimer LT{a->stats, st};
-    if (A.moments) {
-        cudaEvent_t ev = LT.begin(st);
-        rc = moment_table(a, A, Tm, st);
-        if (rc) return rc;
-        LT.end(ev, false, st);
-        LT.launches += 1;
-    }
-    for (int64_t d0 = a->d_begin; d0 < a->d_end;) {
-        const int64_t d1 = window_end(a, A.moments, d0);
-        for (int64_t e0 = r0; e0 < r1; e0 += rows_per_chunk) {
-            const int64_t e1 = std::min(r1, e0 + rows_per_chunk);
-            rc = pairs_window(m, a, A, e0, e1, d0, d1, LT, st);
+    CallPart parts[2];
+    const int nparts = call_parts(a, parts);
+    for (int ip = 0; ip < nparts; ++ip) {
+        // the part's blocks: its own pair arguments and windows; the finalize
+        // stores through the call's descriptor (block offsets from d_begin)
+        hb_assembly_desc ap = *a;
+        ap.d_begin = parts[ip].lo;
+        ap.d_end = parts[ip].hi;
+        PairArgs A = make_pair_args(m, &ap);
+        A.Q = (double *)a->workspace_dev;
+        A.Tm = Tm;
+        A.counter = (unsigned long long *)((char *)a->workspace_dev + q_bytes + tb);
+        if (A.moments) {
+            cudaEvent_t ev = LT.begin(st);
+            rc = moment_table(&ap, A, Tm, st);
             if (rc) return rc;
-            rc = finalize_window(m, a, fin_args(m, a, A.Q, e0, e1, d0, (int)(d1 - d0)), LT, st);
-            if (rc) return rc;
+            LT.end(ev, false, st);
+            LT.launches += 1;
         }
-        d0 = d1;
+        for (int64_t d0 = ap.d_begin; d0 < ap.d_end;) {
+            const int64_t d1 = window_end(&ap, A.moments, d0);
+            for (int64_t e0 = r0; e0 < r1; e0 += rows_per_chunk) {
+                const int64_t e1 = std::min(r1, e0 + rows_per_chunk);
+                rc = pairs_window(m, &ap, A, e0, e1, d0, d1, LT, st);
+                if (rc) return rc;
+                rc = finalize_window(m, a, fin_args(m, a, A.Q, e0, e1, d0, (int)(d1 - d0)), LT, st);
+                if (rc) return rc;
+            }
+            d0 = d1;
+        }
     }
     if (p1p1) {
         rc = symmetrize_blocks(a->blocks_dev, R, nb, LT, st);
@@ -3117,6 +3160,14 @@ extern "C" int hb_assemble_vd(const hb_mesh_desc *m, const hb_assembly_desc *d2,
         return HB_ERR_UNSUPPORTED;
     }
     const hb_assembly_desc v = vd_single_layer(d2, V_blocks_dev);
+    {
+        CallPart pv[2], pd[2];
+        if (call_parts(&v, pv) != 1 || call_parts(d2, pd) != 1) {
+            set_error("hb_assemble_vd: calls whose blocks straddle the direct / moment switch (E_t >= 64) are not "
+                      "fused; use hb_assemble + hb_curl_combine");
+            return HB_ERR_UNSUPPORTED;
+        }
+    }
     cudaStream_t st = (cudaStream_t)stream;
     const size_t rbv = row_bytes(m, &v), rbd = row_bytes(m, d2), tbv = tm_bytes(&v), tbd = tm_bytes(d2);
     if (!d2->workspace_dev || d2->workspace_bytes < hb_assemble_vd_min_workspace(m, d2)) {

@@ -47,13 +47,13 @@ torch.cuda.empty_cache()
 # (pairs straddling two row chunks evaluated twice): 4.1 s; 14-block chunks
 # with all rows (one 16-slot window each): 3.8 s (19 windows repeat the pair
 # geometry, NJ = 1 halves the gaps per point load)
-CHK = int(os.environ.get("HB_C5_KCH", "30"))
+CHK = int(os.environ.get("HB_C5_KCH", "32"))
 KWS = float(os.environ.get("HB_C5_KWS", "0"))   # 0: the library default (all rows when they fit)
 bufK = torch.empty((CHK, E, N), dtype=torch.float64, device="cuda")
 gotK = np.empty((Et, len(rows), N))
 msK = 0.0
 stK = AssemblyStats()
-kchunks = aligned_chunks(Et, CHK) if CHK >= 30 else [(a, min(Et, a + CHK)) for a in range(0, Et, CHK)]
+kchunks = aligned_chunks(Et, CHK) if CHK >= 32 else [(a, min(Et, a + CHK)) for a in range(0, Et, CHK)]
 for d0, d1 in kchunks:
     n = d1 - d0
     msK += timed(lambda: _assemble_operator(1, False, True, False, m, tg, p, q, None, d_range=(d0, d1), out=bufK[:n],
