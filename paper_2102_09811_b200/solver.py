@@ -142,9 +142,80 @@ def build_hypersingular_preconditioner(V11: BlockToeplitzMatrix) -> LinearOperat
     return LinearOperator(lambda x: forward_block_solve(V11, x))
 
 
+class _KrylovCycle:
+    """One restart cycle of flexible GMRES on the device.
+
+    The Arnoldi vectors V and the preconditioned directions Z (flexible:
+    the preconditioner may change from step to step) are rows of device
+    matrices.  A new direction is orthogonalised by classical Gram-Schmidt
+    with one re-orthogonalisation pass (two GEMVs against the stored basis,
+    CGS2 -- as stable as modified Gram-Schmidt, one host round trip per step
+    instead of one per basis vector).  Each Hessenberg column is reduced by
+    the accumulated Givens rotations as it is formed; the least-squares
+    residual is then |g[j + 1]| of the rotated right-hand side."""
+
+    def __init__(self, r, beta: float, m: int):
+        import torch
+
+        n = r.numel()
+        self.m, self.k = m, 0
+        self.V = torch.zeros((m + 1, n), dtype=torch.float64, device=r.device)
+        self.Z = torch.zeros((m, n), dtype=torch.float64, device=r.device)
+        self.V[0] = r / beta
+        self.R = np.zeros((m, m))            # the rotated (upper-triangular) Hessenberg
+        self.rot = np.zeros((m, 2))          # (c, s) of each step's rotation
+        self.g = np.zeros(m + 1)
+        self.g[0] = beta
+
+    def extend(self, apply_A, apply_M) -> bool:
+        """One Arnoldi step; False on breakdown (the Krylov space is invariant)."""
+        import torch
+
+        k = self.k
+        Vk = self.V[: k + 1]
+        self.Z[k] = apply_M(self.V[k])
+        w = apply_A(self.Z[k])
+        h = torch.mv(Vk, w)
+        w = w - torch.mv(Vk.T, h)
+        h2 = torch.mv(Vk, w)
+        w = w - torch.mv(Vk.T, h2)
+        h = h + h2
+        nrm = torch.linalg.vector_norm(w)
+        col = torch.cat([h, nrm.reshape(1)]).cpu().numpy()   # the one host round trip of the step
+        if col[k + 1] > 0.0:
+            self.V[k + 1] = w / nrm
+        for i in range(k):                  # earlier rotations act on rows (i, i + 1)
+            c, s = self.rot[i]
+            col[i], col[i + 1] = c * col[i] + s * col[i + 1], c * col[i + 1] - s * col[i]
+        rho = float(np.hypot(col[k], col[k + 1]))
+        c, s = (col[k] / rho, col[k + 1] / rho) if rho > 0.0 else (1.0, 0.0)
+        self.rot[k] = (c, s)
+        col[k], col[k + 1] = rho, 0.0
+        self.R[: k + 1, k] = col[: k + 1]
+        self.g[k], self.g[k + 1] = c * self.g[k], -s * self.g[k]
+        self.k = k + 1
+        return rho != 0.0
+
+    @property
+    def residual(self) -> float:
+        return abs(self.g[self.k])
+
+    def correction(self):
+        """Z^T y with R y = g (the least-squares solution of the cycle)."""
+        import scipy.linalg
+        import torch
+
+        k = self.k
+        y = scipy.linalg.solve_triangular(self.R[:k, :k], self.g[:k], lower=False)
+        return self.Z[:k].T @ torch.as_tensor(y, device=self.Z.device)
+
+
 def fgmres(op, rhs, rel_tol: float = 1e-8, max_iter: int = 500, restart: int = 50, right_precond=None):
-    """Restarted flexible GMRES with right preconditioning (solver.py:76-162);
-    the reported residual is the true relative residual of the iterate."""
+    """Restarted flexible GMRES with right preconditioning, the semantics of
+    solver.py:76-162 (restart length, iteration budget, stopping on the
+    rotated least-squares residual, the true relative residual of the
+    returned iterate in the report); the cycles run on the device
+    (``_KrylovCycle``)."""
     import torch
 
     t0 = time.perf_counter()
@@ -155,67 +226,38 @@ def fgmres(op, rhs, rel_tol: float = 1e-8, max_iter: int = 500, restart: int = 5
     # user callables see the array type the caller passed (numpy in -> numpy)
     view = (lambda v: v.reshape(shape)) if was_torch else (lambda v: v.reshape(shape).cpu().numpy())
 
-    def A(v):
+    def apply_A(v):
         return torch.as_tensor(op(view(v)), dtype=torch.float64, device=b.device).reshape(-1).clone()
 
-    def M(v):
+    def apply_M(v):
         if right_precond is None:
             return v
         return torch.as_tensor(right_precond(view(v)), dtype=torch.float64, device=b.device).reshape(-1)
 
-    def out(x):
+    def result(x, its, res, ok):
         x = x.reshape(shape)
-        return x if was_torch else x.cpu().numpy()
+        return (x if was_torch else x.cpu().numpy()), SolveReport(its, float(res), ok, time.perf_counter() - t0)
 
     norm_b = float(torch.linalg.vector_norm(b))
     if norm_b == 0.0:
-        return out(torch.zeros_like(b)), SolveReport(0, 0.0, True, time.perf_counter() - t0)
+        return result(torch.zeros_like(b), 0, 0.0, True)
+    tol = rel_tol * norm_b
     x = torch.zeros_like(b)
-    iterations, converged, res = 0, False, float("inf")
-    first = True
-    while iterations < max_iter and not converged:
-        r = b.clone() if first else b - A(x)   # A(0) = 0 exactly: the first residual is b
-        first = False
+    its, res = 0, float("inf")
+    r = b.clone()                            # A(0) = 0 exactly: the first residual is b
+    while its < max_iter:
         beta = float(torch.linalg.vector_norm(r))
-        if beta <= rel_tol * norm_b:
-            converged, res = True, beta / norm_b
-            break
-        m = min(restart, max_iter - iterations)
-        V = torch.zeros((m + 1, b.numel()), dtype=torch.float64, device=b.device)
-        Z = torch.zeros((m, b.numel()), dtype=torch.float64, device=b.device)
-        H = np.zeros((m + 1, m))
-        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
-        g[0] = beta
-        V[0] = r / beta
-        j_used = 0
-        for j in range(m):
-            Z[j] = M(V[j])
-            w = A(Z[j])
-            for i in range(j + 1):
-                H[i, j] = float(torch.dot(w, V[i]))
-                w -= H[i, j] * V[i]
-            H[j + 1, j] = float(torch.linalg.vector_norm(w))
-            if H[j + 1, j] > 0:
-                V[j + 1] = w / H[j + 1, j]
-            for i in range(j):
-                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
-                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
-                H[i, j] = t
-            denom = np.hypot(H[j, j], H[j + 1, j])
-            cs[j] = H[j, j] / denom if denom > 0 else 1.0
-            sn[j] = H[j + 1, j] / denom if denom > 0 else 0.0
-            H[j, j], H[j + 1, j] = denom, 0.0
-            g[j + 1] = -sn[j] * g[j]
-            g[j] = cs[j] * g[j]
-            iterations += 1
-            j_used = j + 1
-            if abs(g[j + 1]) <= rel_tol * norm_b or H[j, j] == 0.0:
+        if beta <= tol:
+            return result(x, its, beta / norm_b, True)
+        cyc = _KrylovCycle(r, beta, min(restart, max_iter - its))
+        while cyc.k < cyc.m:
+            alive = cyc.extend(apply_A, apply_M)
+            its += 1
+            if cyc.residual <= tol or not alive:
                 break
-        import scipy.linalg
-
-        y = scipy.linalg.solve_triangular(H[:j_used, :j_used], g[:j_used], lower=False)
-        x = x + Z[:j_used].T @ torch.as_tensor(y, device=b.device)
-        res = float(torch.linalg.vector_norm(b - A(x))) / norm_b
+        x = x + cyc.correction()
+        r = b - apply_A(x)
+        res = float(torch.linalg.vector_norm(r)) / norm_b
         if res <= rel_tol:
-            converged = True
-    return out(x), SolveReport(iterations, float(res), converged, time.perf_counter() - t0)
+            return result(x, its, res, True)
+    return result(x, its, res, False)
