@@ -2374,6 +2374,7 @@ __global__ void __launch_bounds__(256) k_fin_p0p1(const FinArgs F)
 // (the mesh's curl tile plan); the star product loop is then a bit test and
 // a predicated load -- unstaged pairs add +0.0, which leaves the sum as is.
 constexpr int kFinMaxW = 8;   // bitmask words per star entry (tile lists <= 256 elements)
+constexpr int kFlatMax = 96;  // flat (a, b) lists of the p1 x p1 finalize: star sizes up to ~9 x 9
 
 // FUSE: D = D2 + alpha^2 curl^T V curl in the same pass (hb_assemble_vd).  Every
 // pair (e, f >= e) of the chunk adds alpha^2 (c_ei . c_fj) V_ef to X[m][n]
@@ -2410,6 +2411,8 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
     double *sC = (double *)(wP + kWarps * smax + (smax * kWarps & 1));
     double *wC = sC + 4 * smax;
     __shared__ int na_s;
+    __shared__ int64_t fOff[FUSE ? 1 : kWarps][FUSE ? 1 : kFlatMax];   // flat (a, b) list per warp
+    __shared__ int fA[FUSE ? 1 : kWarps][FUSE ? 1 : kFlatMax];
     if (threadIdx.x == 0) {
         int na = 0;
         for (int64_t a = sm0; a < sm1; ++a) {
@@ -2498,7 +2501,48 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
             // gives the staged entries and only those are loaded (ascending b, as before;
             // the skipped +0.0 additions were exact identities).  Longer stars: the full loop.
             const int pb = lane < nb ? myP[lane] : 0;
-            for (int a = 0; a < na; ++a) {
+            // flat list of the staged (a, b) entries in (a, b) order, loaded eight at a
+            // time: the same additions in the same order as the per-a loop (se over b,
+            // then x += se for every a, empty ones included), with more loads in flight
+            const bool flat_ok = !FUSE && nb <= 32 && na * nb <= kFlatMax;
+            if (flat_ok) {
+                int cnt = 0;
+                for (int a = 0; a < na; ++a) {
+                    const unsigned *om = okm + a * kFinMaxW;
+                    const bool st = lane < nb && ((om[pb >> 5] >> (pb & 31)) & 1u);
+                    const unsigned mask = __ballot_sync(kFull, st);
+                    if (st) {
+                        const int slot = cnt + __popc(mask & ((1u << lane) - 1u));
+                        fOff[warp][slot] = sQ[a] + myFJ[lane];
+                        fA[warp][slot] = a;
+                    }
+                    cnt += __popc(mask);
+                }
+                __syncwarp();
+                double se = 0.0;
+                int cur = 0;
+                for (int i = 0; i < cnt; i += 8) {
+                    double qv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) qv[u] = (lok && i + u < cnt) ? F.Q[fOff[warp][i + u] + dc + lane] : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (i + u >= cnt) break;
+                        const int a = fA[warp][i + u];
+                        for (; cur < a; ++cur) {
+                            x += se;
+                            se = 0.0;
+                        }
+                        se += qv[u];
+                    }
+                }
+                for (; cur < na; ++cur) {
+                    x += se;
+                    se = 0.0;
+                }
+                __syncwarp();
+            }
+            for (int a = 0; a < (flat_ok ? 0 : na); ++a) {
                 const double *Qe = F.Q + sQ[a] + dc + lane;
                 const unsigned *om = okm + a * kFinMaxW;
                 double se = 0.0;
