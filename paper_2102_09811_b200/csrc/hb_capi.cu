@@ -61,6 +61,10 @@ __global__ void __launch_bounds__(256) k_fp64_probe(int64_t iters, double *sink)
 constexpr int kCT = 32;    // nodes per tile
 constexpr int kRC = 32;    // staged V rows per chunk (one per lane)
 constexpr int kMaxJ = 8;   // column elements per tile <= 32 kMaxJ
+#ifndef HB_CURL_WARPS
+#define HB_CURL_WARPS 16   // warps per CTA sharing one tile pair's shared-memory stages (latency hiding)
+#endif
+constexpr int kCW = HB_CURL_WARPS, kCQ = kCT / kCW;   // output rows per warp in the D stage
 
 struct CurlArgs {
     hb_mesh_desc M;
@@ -94,7 +98,7 @@ struct __align__(16) CurlEnt {
     int pos, pad;
 };
 
-__global__ void __launch_bounds__(256) k_curl_tile(const CurlArgs C)
+__global__ void __launch_bounds__(32 * kCW) k_curl_tile(const CurlArgs C)
 {
     extern __shared__ __align__(16) double csm[];
     const int64_t N = C.M.N_x, E = C.M.E_x;
@@ -146,14 +150,17 @@ __global__ void __launch_bounds__(256) k_curl_tile(const CurlArgs C)
     const double *vrow = Vs + lane * C.ldv;
     for (int64_t d = d_lo; d < d_hi; ++d) {
         const double *Vd = C.V + d * E * E;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        int sp[4];
+        double acc[kCQ];
+        int sp[kCQ];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) sp[q] = rPtr[min(warp + 8 * q, kCT)];
+        for (int q = 0; q < kCQ; ++q) {
+            acc[q] = 0.0;
+            sp[q] = rPtr[min(warp + kCW * q, kCT)];
+        }
         for (int r0 = 0; r0 < (int)A; r0 += kRC) {
             const int rc = (int)A - r0 < kRC ? (int)A - r0 : kRC;
             // gather the chunk with async copies: all of its loads in flight at once
-            for (int r = warp; r < rc; r += 8) {
+            for (int r = warp; r < rc; r += kCW) {
                 const double *Vr = Vd + rowE[r0 + r] * E;
                 const unsigned sa = (unsigned)__cvta_generic_to_shared(Vs + r * C.ldv + lane);
 #pragma unroll
@@ -166,7 +173,7 @@ __global__ void __launch_bounds__(256) k_curl_tile(const CurlArgs C)
             __syncthreads();
             // T stage: warp per node (uniform star loop, broadcast entries), lane per staged row
             // (rows >= rc compute unused values)
-            for (int nl = warp; nl < nnc; nl += 8) {
+            for (int nl = warp; nl < nnc; nl += kCW) {
                 double w0 = 0.0, w1 = 0.0, w2 = 0.0;
                 for (int s = cPtr[nl]; s < cPtr[nl + 1]; ++s) {
                     const CurlEnt ce = cE[s];
@@ -184,8 +191,8 @@ __global__ void __launch_bounds__(256) k_curl_tile(const CurlArgs C)
             // entries in this chunk are the next ones (element-sorted stars)
             const int rend = r0 + rc;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int ml = warp + 8 * q;
+            for (int q = 0; q < kCQ; ++q) {
+                const int ml = warp + kCW * q;
                 if (ml < nmr) {
                     const int se = rPtr[ml + 1];
                     int s = sp[q];
@@ -205,8 +212,8 @@ __global__ void __launch_bounds__(256) k_curl_tile(const CurlArgs C)
 
         double *Dd = C.D + d * N * N;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int ml = warp + 8 * q;
+        for (int q = 0; q < kCQ; ++q) {
+            const int ml = warp + kCW * q;
             const int64_t m = mm0 + ml, n = nn0 + lane;
             double val = 0.0;
             if (ml < nmr && lane < nnc && n >= m) {
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(256) k_curl_tile(const CurlArgs C)
             Dt[ml * 33 + lane] = val;
         }
         __syncthreads();
-        for (int r = warp; r < kCT; r += 8) {   // D[n][m] = D[m][n] for n > m
+        for (int r = warp; r < kCT; r += kCW) {   // D[n][m] = D[m][n] for n > m
             const int64_t n = nn0 + r, m = mm0 + lane;
             if (r < nnc && lane < nmr && n > m) Dd[n * N + m] = Dt[lane * 33 + r];
         }
@@ -305,13 +312,13 @@ static int curl_launch(const hb_mesh_desc *mesh, int64_t n_blocks, double alpha,
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_curl_tile, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_curl_tile, 32 * kCW, smem);
     const int64_t nt = cdiv(mesh->N_x, kCT), npairs = nt * (nt + 1) / 2;
     // blocks per CTA: enough CTAs for ~4 waves, the rest loops on chip (plan reuse)
     const int64_t want = (int64_t)std::max(1, per_sm) * nsm * 4;
     C.dpc = (int)std::max<int64_t>(1, std::min<int64_t>(n_blocks, npairs * n_blocks / std::max<int64_t>(1, want)));
     const int64_t gy = cdiv(n_blocks, C.dpc);
-    k_curl_tile<<<dim3((unsigned)npairs, (unsigned)gy), 256, smem, (cudaStream_t)stream>>>(C);
+    k_curl_tile<<<dim3((unsigned)npairs, (unsigned)gy), 32 * kCW, smem, (cudaStream_t)stream>>>(C);
     return cuda_check(cudaGetLastError(), "hb_curl_combine");
 }
 
