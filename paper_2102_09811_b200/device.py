@@ -92,12 +92,14 @@ class DeviceTables:
 
         self.host = H = host if host is not None else host_tables(mesh, config)
         self.device = device
-        pin = getattr(H, "pinned", None)
+        # every array in one buffer: one allocation and one host->device copy
+        # (asynchronous from the page-locked blob of pin_host_tables)
+        blob, where = _packed(H)
+        self._blob = blob.to(device, non_blocking=True)
 
         def up(a):
-            if pin is not None:
-                return pin[id(a)].to(device, non_blocking=True)
-            return torch.from_numpy(np.ascontiguousarray(a)).to(device)
+            off, n, dt, shape = where[id(a)]
+            return self._blob[off:off + n].view(dt).view(shape)
         self.t = {
             "tri_nodes": up(H.tri_nodes), "verts_tri": up(H.verts_tri), "normals": up(H.normals),
             "centroids": up(H.centroids), "diameters": up(H.diameters), "areas": up(H.areas),
@@ -161,16 +163,41 @@ def host_tables(mesh, config: QuadratureConfig) -> HostTables:
     return per_mesh[key]
 
 
-def pin_host_tables(H: HostTables):
-    """Page-locked copies of every host array (uploads become async DMA)."""
-    import torch
-
+def _table_arrays(H: HostTables) -> list:
     arrays = [H.tri_nodes, H.verts_tri, H.normals, H.centroids, H.diameters, H.areas, *H.reg, *H.near,
               *H.tn, *H.duf, H.sing_row, *H.star, H.curls, *H.curl_plan[:3]]
     for sym in (False, True):
         arrays += list(H.sing[sym][:2])
-    H.pinned = {id(a): torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays}
-    H.pinned_bytes = sum(t.numel() * t.element_size() for t in H.pinned.values())
+    return arrays
+
+
+def _packed(H: HostTables):
+    """The host tables as one byte blob (256-byte aligned sections) and, per
+    array id, (offset, bytes, torch dtype, shape); cached on ``H`` (the
+    page-locked blob of pin_host_tables when pinned)."""
+    import torch
+
+    if getattr(H, "_blob", None) is None:
+        arrays = _table_arrays(H)
+        where, off = {}, 0
+        for a in arrays:   # keyed by the attribute objects DeviceTables looks up
+            where[id(a)] = (off, a.nbytes, torch.from_numpy(np.ascontiguousarray(a[:0])).dtype, tuple(a.shape))
+            off += -(-a.nbytes // 256) * 256
+        blob = np.zeros(max(off, 256), dtype=np.uint8)
+        for a in arrays:
+            o, n, _, _ = where[id(a)]
+            blob[o:o + n] = np.ascontiguousarray(a).reshape(-1).view(np.uint8)
+        H._blob, H._where = torch.from_numpy(blob), where
+    return H._blob, H._where
+
+
+def pin_host_tables(H: HostTables):
+    """Page-locked copy of the packed host tables (the upload becomes one
+    async DMA)."""
+    blob, _ = _packed(H)
+    if not blob.is_pinned():
+        H._blob = blob.pin_memory()
+    H.pinned_bytes = H._blob.numel()
     return H
 
 

@@ -387,7 +387,7 @@ def test_hypersingular_streamed_to_host_matches():
     p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
     V = hb.assemble_single_layer(m, tg, p, Q4)
     ref = hb.assemble_hypersingular(m, tg, p, Q4, single_layer=V).device_blocks.cpu()
-    pin = torch.empty(ref.shape, dtype=torch.float64).pin_memory()
+    pin = torch.full(ref.shape, float("nan"), dtype=torch.float64).pin_memory()
     D = hb.assemble_hypersingular(m, tg, p, Q4, single_layer=V, host_out=pin)
     host, ev = D.host_copy
     ev.synchronize()
@@ -451,12 +451,12 @@ def test_host_out_row_slab_streaming_is_bitwise(op):
     p = hb.KernelParams(1.0, tg.step, length_scale=m.diameter)
     f = hb.assemble_single_layer if op == "V" else hb.assemble_double_layer
     ref = f(m, tg, p).blocks
-    pin = torch.empty(ref.shape, dtype=torch.float64).pin_memory()
+    pin = torch.full(ref.shape, float("nan"), dtype=torch.float64).pin_memory()   # every entry must be written
     res = f(m, tg, p, host_out=pin)
     res.host_copy[1].synchronize()
     assert np.array_equal(pin.numpy(), ref)
     assert np.array_equal(res.blocks, ref)
     # a d-range streams the same way
-    pin2 = torch.empty((5,) + ref.shape[1:], dtype=torch.float64).pin_memory()
+    pin2 = torch.full((5,) + ref.shape[1:], float("nan"), dtype=torch.float64).pin_memory()
     f(m, tg, p, d_range=(3, 8), host_out=pin2).host_copy[1].synchronize()
     assert np.array_equal(pin2.numpy(), ref[3:8])
