@@ -185,6 +185,39 @@ __device__ __forceinline__ double eval_general(const PairArgs &A, const Slots<OP
 }
 
 // ---------------------------------------------------------------------------
+// Warp sums of N per-lane values, value v returned in lane v (v < N): the two
+// 16-lane halves folded by one shuffle each, the 16 partials of every value
+// summed by one lane through shared memory (`buf`: 16 (N | 1) doubles, odd
+// stride: conflict-free) -- N shuffles + 16 loads instead of 5 N shuffles.
+// ---------------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ double warp_sums_to_lanes(double (&v)[N], double *buf, int lane)
+{
+    constexpr int S = N | 1;
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] += __shfl_xor_sync(kFull, v[i], 16);
+    __syncwarp();
+    if (lane < 16) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) buf[lane * S + i] = v[i];
+    }
+    __syncwarp();
+    double r = 0.0;
+    if (lane < N) {
+        double p[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p[k] = buf[k * S + lane];
+#pragma unroll
+        for (int l = 4; l < 16; l += 4)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) p[k] += buf[(l + k) * S + lane];
+        r = (p[0] + p[1]) + (p[2] + p[3]);
+    }
+    __syncwarp();
+    return r;
+}
+
+// ---------------------------------------------------------------------------
 // one element pair, all time gaps of the window
 // ---------------------------------------------------------------------------
 template <int OP, bool TP1, bool SP1, int NJ, class Geom>
@@ -476,14 +509,28 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int i = 0; i < NIJ; ++i) acc[j][i] += __shfl_xor_sync(kFull, acc[j][i], 16);
+    constexpr int NSP = (OP == 2 ? 1 : 2) * NIJ;   // special sums: s0 (and sc)
+    constexpr bool SCATTER = NSP >= 6;
+    static_assert(!SCATTER || 16 * (NSP | 1) <= 32 * PAY, "special-sum buffer must fit the payload area");
+    double spec = 0.0;   // SCATTER: value `lane` of (s0, sc)
     if (A.need_special) {
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1)
+        if constexpr (SCATTER) {
+            double v[NSP];
 #pragma unroll
             for (int i = 0; i < NIJ; ++i) {
-                s0[i] += __shfl_xor_sync(kFull, s0[i], o);
-                if (OP != 2) sc[i] += __shfl_xor_sync(kFull, sc[i], o);
+                v[i] = s0[i];
+                if (OP != 2) v[NIJ + i] = sc[i];
             }
+            spec = warp_sums_to_lanes<NSP>(v, geo, lane);
+        } else {
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+                for (int i = 0; i < NIJ; ++i) {
+                    s0[i] += __shfl_xor_sync(kFull, s0[i], o);
+                    if (OP != 2) sc[i] += __shfl_xor_sync(kFull, sc[i], o);
+                }
+        }
     }
     const int nslots = A.it_hi - A.it_lo + 1;
     if (s == 0) {
@@ -497,7 +544,12 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
         }
     }
     double *L0 = Ls + NIJ * SLOTS, *Lc = L0 + NIJ;
-    if (lane == 0 && A.need_special) {
+    if constexpr (SCATTER) {   // L0 = s0, Lc = sc (D2: s0): lane v holds value v
+        if (A.need_special && lane < NSP) {
+            L0[lane] = jac * spec;
+            if (OP == 2) Lc[lane] = jac * spec;
+        }
+    } else if (lane == 0 && A.need_special) {
 #pragma unroll
         for (int i = 0; i < NIJ; ++i) {
             L0[i] = jac * s0[i];
@@ -701,20 +753,24 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             if (DF) af[j][i] += __shfl_xor_sync(kFull, af[j][i], 16);
             if (DR) ar[j][i] += __shfl_xor_sync(kFull, ar[j][i], 16);
         }
+    // special sums, value v in lane v: (s0, sc) of the forward output, then of the reverse one
+    constexpr int NSP = (DF ? 6 : 0) + (DR ? 6 : 0);
+    static_assert(16 * (NSP | 1) <= 32 * PAY, "special-sum buffer must fit the payload area");
+    double spec = 0.0;
     if (A.need_special) {
+        double v[NSP];
 #pragma unroll
-        for (int o = 16; o >= 1; o >>= 1)
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                if (DF) {
-                    s0f[i] += __shfl_xor_sync(kFull, s0f[i], o);
-                    scf[i] += __shfl_xor_sync(kFull, scf[i], o);
-                }
-                if (DR) {
-                    s0r[i] += __shfl_xor_sync(kFull, s0r[i], o);
-                    scr[i] += __shfl_xor_sync(kFull, scr[i], o);
-                }
+        for (int i = 0; i < 3; ++i) {
+            if (DF) {
+                v[i] = s0f[i];
+                v[3 + i] = scf[i];
             }
+            if (DR) {
+                v[(DF ? 6 : 0) + i] = s0r[i];
+                v[(DF ? 9 : 3) + i] = scr[i];
+            }
+        }
+        spec = warp_sums_to_lanes<NSP>(v, geo, lane);
     }
     const int nslots = A.it_hi - A.it_lo + 1;
     double *Lf = Ls, *Lr = Ls + LSZ;
@@ -731,18 +787,9 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
             }
         }
     }
-    if (lane == 0 && A.need_special) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            if (DF) {
-                Lf[3 * SLOTS + i] = jac * s0f[i];
-                Lf[3 * SLOTS + 3 + i] = jac * scf[i];
-            }
-            if (DR) {
-                Lr[3 * SLOTS + i] = jac * s0r[i];
-                Lr[3 * SLOTS + 3 + i] = jac * scr[i];
-            }
-        }
+    if (A.need_special && lane < NSP) {   // [3 SLOTS + 0..2] = s0, [+3..5] = sc
+        const bool fwd = DF && lane < 6;
+        (fwd ? Lf : Lr)[3 * SLOTS + (fwd ? lane : lane - (DF ? 6 : 0))] = jac * spec;
     }
     __syncwarp();
     if (DF && slot_f >= 0) combine_store<3, NJ>(A, Lf, slot_f, lane);
