@@ -183,6 +183,27 @@ int hb_forward_solve(int64_t n_blocks, int64_t n, const double *blocks_dev, int 
                      int64_t n_steps, const double *inv_dev, const double *rhs_dev, double *x_dev,
                      double *h_work_dev, void *stream);
 
+/* The same substitution blocked in tiles of 8 steps: per tile, the history
+ * terms from earlier tiles of all 8 steps in one pass over the blocks (each
+ * block read once per tile), then per step only the near terms d < 8 and the
+ * inverse apply -- about E_t^2 / 16 block reads instead of E_t^2 / 2.
+ * workspace: hb_forward_solve_workspace(n) bytes of device memory.  The
+ * transposed and diagonal-only forms run the per-step path. */
+size_t hb_forward_solve_workspace(int64_t n);
+/* The two history kernels of the blocked substitution on R rows (a row
+ * shard) x C columns, the same per-row sums as hb_forward_solve_ws:
+ * _far: H[i][r] = sum_d A^d(r, :) x[k0 + i - d] over 0 <= k0 + i - d < k0,
+ *       i < nk <= 8, k0 >= 1 (H: nk x R);
+ * _near: h[r] = Hk[r] (if Hk) + sum_{d=1..min(k-k0, n_blocks-1)} A^d(r, :) x[k-d],
+ *       k0 <= k < k0 + 8 (the near terms of step k of its tile). */
+int hb_forward_history_far(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int64_t k0, int64_t nk,
+                           const double *x_dev, double *H_dev, void *stream);
+int hb_forward_history_near(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int64_t k, int64_t k0,
+                            const double *x_dev, const double *Hk_dev, double *h_dev, void *stream);
+int hb_forward_solve_ws(int64_t n_blocks, int64_t n, const double *blocks_dev, int transpose, int diagonal_only,
+                        int64_t n_steps, const double *inv_dev, const double *rhs_dev, double *x_dev,
+                        void *workspace_dev, size_t workspace_bytes, void *stream);
+
 /* CUDA IPC for row-parallel assembly: export a device pointer (anywhere
  * inside an allocation) as a 64-byte handle of its allocation plus the byte
  * offset; import opens the handle in this process (peer access enabled

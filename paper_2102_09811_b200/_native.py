@@ -84,7 +84,7 @@ EXPORTED = (
     "hb_assemble_full_workspace", "hb_curl_combine", "hb_potential",
     "hb_toeplitz_apply", "hb_forward_subst_step", "hb_fp64_probe", "hb_pair_classes",
     "hb_toeplitz_apply_range", "hb_curl_workspace", "hb_ipc_export", "hb_ipc_import", "hb_ipc_close",
-    "hb_forward_solve", "hb_forward_history", "hb_inv_apply", "hb_represent_grid",
+    "hb_forward_solve", "hb_forward_solve_workspace", "hb_forward_solve_ws", "hb_forward_history_far", "hb_forward_history_near", "hb_forward_history", "hb_inv_apply", "hb_represent_grid",
     "hb_project_workspace", "hb_project_data", "hb_p1_mass_solve", "hb_error_sigma", "hb_copy_row_slab_d2h",
     "hb_represent_grid_elem", "hb_toeplitz_apply_workspace", "hb_toeplitz_apply_ws",
     "hb_assemble_vd", "hb_assemble_vd_min_workspace", "hb_assemble_vd_full_workspace", "hb_curl_combine_parts",
@@ -140,6 +140,14 @@ def load():
     L.hb_ipc_close.argtypes = [_P, _I64]
     L.hb_forward_solve.argtypes = [_I64, _I64, _P, _INT, _INT, _I64, _P, _P, _P, _P, _P]
     L.hb_forward_solve.restype = _INT
+    L.hb_forward_solve_workspace.argtypes = [_I64]
+    L.hb_forward_solve_workspace.restype = ctypes.c_size_t
+    L.hb_forward_solve_ws.argtypes = [_I64, _I64, _P, _INT, _INT, _I64, _P, _P, _P, _P, ctypes.c_size_t, _P]
+    L.hb_forward_solve_ws.restype = _INT
+    L.hb_forward_history_far.argtypes = [_I64, _I64, _I64, _P, _I64, _I64, _P, _P, _P]
+    L.hb_forward_history_far.restype = _INT
+    L.hb_forward_history_near.argtypes = [_I64, _I64, _I64, _P, _I64, _I64, _P, _P, _P, _P]
+    L.hb_forward_history_near.restype = _INT
     L.hb_fp64_probe.restype = _INT
     L.hb_forward_history.argtypes = [_I64, _I64, _I64, _P, _I64, _P, _P, _P]
     L.hb_forward_history.restype = _INT

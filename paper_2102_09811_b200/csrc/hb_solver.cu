@@ -177,22 +177,131 @@ __global__ void __launch_bounds__(256) k_hist_cols(const double *__restrict__ bl
     }
 }
 
-// x_k[i] = sum_j inv[i][j] (rhs_k[j] - h[j]); one warp per row i
+// x_k[i] = sum_j inv[i][j] (rhs_k[j] - h[j]); kHW warps per row i (the j range
+// split in interleaved quarters, partials added in warp order)
 __global__ void __launch_bounds__(256) k_inv_apply(const double *__restrict__ inv, int64_t n,
                                                    const double *__restrict__ rhs_k, const double *__restrict__ h,
                                                    int has_h, double *__restrict__ x_k)
 {
-    const int lane = threadIdx.x & 31;
-    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (i >= n) return;
-    const double *a = inv + i * n;
+    __shared__ double part[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = warp % kHW;
+    const int64_t i = (int64_t)blockIdx.x * (8 / kHW) + warp / kHW;
     double acc = 0.0;
-    for (int64_t j = lane; j < n; j += 32) {
-        const double v = has_h ? __ldg(rhs_k + j) - __ldg(h + j) : __ldg(rhs_k + j);
-        acc = fma(__ldg(a + j), v, acc);
+    if (i < n) {
+        const double *a = inv + i * n;
+#pragma unroll 4
+        for (int64_t j = lane + 32 * sub; j < n; j += 32 * kHW) {
+            const double v = has_h ? __ldg(rhs_k + j) - __ldg(h + j) : __ldg(rhs_k + j);
+            acc = fma(__ldg(a + j), v, acc);
+        }
     }
     acc = warp_sum(acc);
-    if (lane == 0) x_k[i] = acc;
+    if (lane == 0) part[warp] = acc;
+    __syncthreads();
+    if (sub == 0 && lane == 0 && i < n) {
+        double v = 0.0;
+        for (int w = 0; w < kHW; ++w) v += part[warp + w];
+        x_k[i] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Blocked forward substitution: the steps in tiles of kFT.  Per tile [k0,
+// k0 + nk) the history from earlier tiles (the "far" terms, k - d < k0) of
+// all nk steps in one pass that reads each block once (k_hist_far); inside
+// the tile, per step, only the near terms d <= k - k0 (blocks 1..kFT-1,
+// L2-resident) and the inverse apply.  Block reads per solve: about
+// E_t^2 / (2 kFT) instead of E_t^2 / 2.
+// ---------------------------------------------------------------------------
+constexpr int kFT = 8;
+
+// H[i][r] = sum_{d >= 1} A^d(r, :) x[k0 + i - d] over the terms with
+// 0 <= k0 + i - d < k0, i < nk; 4 warps per row split the columns, each lane
+// keeps x[k0 + i - d][c] (i < kFT) of the current d in registers -- one new x
+// load per element of A as d grows; sums in fixed order (column, d, lanes, warps)
+// (R output rows -- all of a square operator or one rank's row shard -- by C columns)
+__global__ void __launch_bounds__(256) k_hist_far(const double *__restrict__ blocks, int64_t R, int64_t C,
+                                                  int64_t n_blocks, int64_t k0, int nk, const double *__restrict__ x,
+                                                  double *__restrict__ H)
+{
+    __shared__ double part[8][kFT];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = warp % kHW;
+    const int64_t r = (int64_t)blockIdx.x * (8 / kHW) + warp / kHW;
+    double acc[kFT];
+#pragma unroll
+    for (int i = 0; i < kFT; ++i) acc[i] = 0.0;
+    if (r < R) {
+        const int64_t dmax = min(k0 + nk - 1, n_blocks - 1);
+        for (int64_t c = lane + 32 * sub; c < C; c += 32 * kHW) {
+            double xw[kFT];   // xw[i] = x[k0 + i - d][c], 0 unless 0 <= k0 + i - d < k0
+#pragma unroll
+            for (int i = 0; i < kFT; ++i) xw[i] = 0.0;
+            const double *a = blocks + r * C + c;
+            for (int64_t db = 1; db <= dmax; db += kFT) {
+                // the loads of kFT blocks d first (independent: in flight together), then the FMAs
+                double av[kFT], xn[kFT];
+#pragma unroll
+                for (int u = 0; u < kFT; ++u) {
+                    const int64_t d = db + u;
+                    av[u] = d <= dmax ? __ldg(a + d * R * C) : 0.0;
+                    xn[u] = (d <= dmax && k0 - d >= 0) ? __ldg(x + (k0 - d) * C + c) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kFT; ++u) {
+#pragma unroll
+                    for (int i = kFT - 1; i > 0; --i) xw[i] = xw[i - 1];
+                    xw[0] = xn[u];
+#pragma unroll
+                    for (int i = 0; i < kFT; ++i) acc[i] = fma(av[u], xw[i], acc[i]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kFT; ++i) acc[i] = warp_sum(acc[i]);
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < kFT; ++i) part[warp][i] = acc[i];
+    }
+    __syncthreads();
+    if (sub == 0 && lane < nk && r < R) {
+        double v = 0.0;
+        for (int w = 0; w < kHW; ++w) v += part[warp + w][lane];
+        H[lane * R + r] = v;
+    }
+}
+
+// h[r] = Hk[r] (far terms, if any) + sum_{d=1..dn} A^d(r, :) x[k - d] (near terms)
+__global__ void __launch_bounds__(256) k_hist_near(const double *__restrict__ blocks, int64_t R, int64_t C,
+                                                   int64_t k, int64_t dn, const double *__restrict__ x,
+                                                   const double *__restrict__ Hk, double *__restrict__ h)
+{
+    __shared__ double part[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = warp % kHW;
+    const int64_t r = (int64_t)blockIdx.x * (8 / kHW) + warp / kHW;
+    double acc = 0.0;
+    if (r < R) {
+        // column-outer, d-inner (dn < kFT): the dn loads of a column are in flight together
+        for (int64_t c = lane + 32 * sub; c < C; c += 32 * kHW) {
+            double av[kFT - 1], xv[kFT - 1];
+#pragma unroll
+            for (int d = 1; d < kFT; ++d) {
+                av[d - 1] = d <= dn ? __ldg(blocks + (d * R + r) * C + c) : 0.0;
+                xv[d - 1] = d <= dn ? __ldg(x + (k - d) * C + c) : 0.0;
+            }
+#pragma unroll
+            for (int d = 1; d < kFT; ++d)
+                if (d <= dn) acc = fma(av[d - 1], xv[d - 1], acc);
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) part[warp] = acc;
+    __syncthreads();
+    if (sub == 0 && lane == 0 && r < R) {
+        double v = Hk ? Hk[r] : 0.0;
+        for (int w = 0; w < kHW; ++w) v += part[warp + w];
+        h[r] = v;
+    }
 }
 
 }  // namespace hb
@@ -220,6 +329,24 @@ __device__ __forceinline__ void dmma884s(double &d0, double &d1, double a, doubl
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
+}
+
+// the DMMAs of one staged (A^d tile, x window): m-tiles LO..7 (those below
+// mtiles), k-steps outer so the live tiles' accumulators interleave; bs: this
+// lane's B element of k-step 0 (k-step ks at + 4 ks rows (TR) / columns), xw:
+// its x window element of m-tile 0, k-step 0 (m-tile mt at + 8 mt rows)
+template <int LO, bool TR>
+__device__ __forceinline__ void mma_live(double (&acc)[8][2], const double *bs, const double *xw, int mtiles)
+{
+#pragma unroll
+    for (int ks = 0; ks < kMC / 4; ++ks) {
+        const double b = TR ? bs[4 * ks * (kMR + 4)] : bs[4 * ks];
+#pragma unroll
+        for (int mt = LO; mt < 8; ++mt) {
+            if (mt >= mtiles) continue;
+            dmma884s(acc[mt][0], acc[mt][1], xw[8 * mt * kMS + 4 * ks], b);
+        }
+    }
 }
 
 // TR: the transposed product Y[k][c] += sum_r X[k - d][r] A^d[r][c] (A tile staged
@@ -293,15 +420,22 @@ __global__ void __launch_bounds__(kMT) k_toep_mma(const double *__restrict__ blo
                 if (d < de) fetch(d + 1, nxt);
                 const int dl = (int)(d - k_lo);      // steps j < dl of the tile have no term (k < d)
                 const int wo = 32 - (int)(d - db);   // window row of step j: j + wo
-#pragma unroll
-                for (int ks = 0; ks < kMC / 4; ++ks) {
-                    const double b = TR ? As[(4 * ks + tq) * (kMR + 4) + 8 * warp + gq]   // B[k = in][n = out]
-                                        : As[(8 * warp + gq) * kMS + 4 * ks + tq];
-#pragma unroll
-                    for (int mt = 0; mt < 8; ++mt) {
-                        if (mt >= mtiles || 8 * mt + 7 < dl) continue;
-                        dmma884s(acc[mt][0], acc[mt][1], Xw[8 * mt + gq + wo][4 * ks + tq], b);
-                    }
+                // m-tiles with every step below dl are skipped: a predicated DMMA
+                // still takes its tensor-pipe slot, so the live range [mt_lo, 8)
+                // selects a loop whose start is a compile-time constant (the live
+                // tiles' DMMAs interleave, independent accumulators)
+                const int mt_lo = dl > 0 ? dl >> 3 : 0;
+                const double *bs = TR ? &As[tq * (kMR + 4) + 8 * warp + gq] : &As[(8 * warp + gq) * kMS + tq];
+                const double *xw = &Xw[gq + wo][tq];
+                switch (mt_lo) {
+                case 0: mma_live<0, TR>(acc, bs, xw, mtiles); break;
+                case 1: mma_live<1, TR>(acc, bs, xw, mtiles); break;
+                case 2: mma_live<2, TR>(acc, bs, xw, mtiles); break;
+                case 3: mma_live<3, TR>(acc, bs, xw, mtiles); break;
+                case 4: mma_live<4, TR>(acc, bs, xw, mtiles); break;
+                case 5: mma_live<5, TR>(acc, bs, xw, mtiles); break;
+                case 6: mma_live<6, TR>(acc, bs, xw, mtiles); break;
+                default: mma_live<7, TR>(acc, bs, xw, mtiles); break;
                 }
             }
         }
@@ -344,12 +478,24 @@ __global__ void k_sum_partials(const double *__restrict__ part, int64_t groups, 
 // the input length only, so row shards of an operator (RowShardedToeplitz)
 // sum in the same order as the whole operator.  Returns the group count and
 // the columns per group.
+// Large operators (>= kMmaMinRows rows) split too, in groups of 64 chunks
+// (2048 input columns): the row tiles alone give one CTA wave or less
+// (12288 rows: 384 CTAs over 148 SMs, 2.6 per SM -- the SMs with 3 set the
+// time); 12288 columns -> 6 groups, 2304 CTAs.  Again a function of the
+// input length only (within the large-operator regime).
 static int64_t toep_groups(int64_t n_in, int64_t n_out, int64_t n_steps, int64_t *csz)
 {
     (void)n_steps;
     const int64_t chunks = cdiv(n_in, kMC);
     *csz = chunks * kMC;
-    if (n_out >= kMmaMinRows || chunks < 2) return 1;
+    if (chunks < 2) return 1;
+    if (n_out >= kMmaMinRows) {
+        static const int64_t per_big = getenv("HB_TOEP_CHUNKS_BIG") ? atoll(getenv("HB_TOEP_CHUNKS_BIG")) : 64;
+        if (per_big <= 0 || chunks <= per_big) return 1;
+        const int64_t g = cdiv(chunks, per_big), per = cdiv(chunks, g);
+        *csz = per * kMC;
+        return cdiv(chunks, per);
+    }
     static const int64_t target = getenv("HB_TOEP_GROUPS") ? atoll(getenv("HB_TOEP_GROUPS")) : 12;
     const int64_t per = cdiv(chunks, std::max<int64_t>(1, target));
     *csz = per * kMC;
@@ -467,7 +613,7 @@ extern "C" int hb_forward_solve(int64_t n_blocks, int64_t n, const double *block
         return HB_ERR_INVALID;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    const unsigned g_rows = (unsigned)cdiv(n * 32, 256), g_cols = (unsigned)cdiv(n, 32);
+    const unsigned g_rows = (unsigned)cdiv(n, 8 / kHW), g_cols = (unsigned)cdiv(n, 32);
     const unsigned g_hist = (unsigned)cdiv(n, 8 / kHW);
     for (int64_t k = 0; k < n_steps; ++k) {
         const bool hist = !diagonal_only && k > 0;
@@ -478,6 +624,38 @@ extern "C" int hb_forward_solve(int64_t n_blocks, int64_t n, const double *block
         k_inv_apply<<<g_rows, 256, 0, st>>>(inv_dev, n, rhs_dev + k * n, h_work_dev, hist ? 1 : 0, x_dev + k * n);
     }
     return cuda_check(cudaGetLastError(), "hb_forward_solve");
+}
+
+extern "C" size_t hb_forward_solve_workspace(int64_t n) { return n < 1 ? 0 : (size_t)(kFT + 1) * (size_t)n * sizeof(double); }
+
+extern "C" int hb_forward_solve_ws(int64_t n_blocks, int64_t n, const double *blocks_dev, int transpose,
+                                   int diagonal_only, int64_t n_steps, const double *inv_dev, const double *rhs_dev,
+                                   double *x_dev, void *workspace_dev, size_t workspace_bytes, void *stream)
+{
+    if (n_blocks < 1 || n < 1 || n_steps < 1 || !blocks_dev || !inv_dev || !rhs_dev || !x_dev || !workspace_dev ||
+        workspace_bytes < hb_forward_solve_workspace(n) || (!diagonal_only && n_steps > n_blocks)) {
+        set_error("hb_forward_solve_ws: bad arguments");
+        return HB_ERR_INVALID;
+    }
+    double *h = (double *)workspace_dev, *H = h + n;
+    if (transpose || diagonal_only)   // the per-step form (transposed history kernel / no history)
+        return hb_forward_solve(n_blocks, n, blocks_dev, transpose, diagonal_only, n_steps, inv_dev, rhs_dev, x_dev,
+                                h, stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g_rows = (unsigned)cdiv(n, 8 / kHW), g_hist = (unsigned)cdiv(n, 8 / kHW);
+    for (int64_t k0 = 0; k0 < n_steps; k0 += kFT) {
+        const int nk = (int)std::min<int64_t>(kFT, n_steps - k0);
+        if (k0 > 0) k_hist_far<<<g_hist, 256, 0, st>>>(blocks_dev, n, n, n_blocks, k0, nk, x_dev, H);
+        for (int64_t k = k0; k < k0 + nk; ++k) {
+            const int64_t dn = std::min(k - k0, n_blocks - 1);
+            const bool hist = k > 0;
+            if (hist)
+                k_hist_near<<<g_hist, 256, 0, st>>>(blocks_dev, n, n, k, dn, x_dev,
+                                                    k0 > 0 ? H + (k - k0) * n : nullptr, h);
+            k_inv_apply<<<g_rows, 256, 0, st>>>(inv_dev, n, rhs_dev + k * n, h, hist ? 1 : 0, x_dev + k * n);
+        }
+    }
+    return cuda_check(cudaGetLastError(), "hb_forward_solve_ws");
 }
 
 extern "C" int hb_forward_history(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int64_t k,
@@ -492,6 +670,35 @@ extern "C" int hb_forward_history(int64_t n_blocks, int64_t R, int64_t C, const 
     return cuda_check(cudaGetLastError(), "hb_forward_history");
 }
 
+extern "C" int hb_forward_history_far(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int64_t k0,
+                                      int64_t nk, const double *x_dev, double *H_dev, void *stream)
+{
+    if (n_blocks < 1 || R < 1 || C < 1 || k0 < 1 || nk < 1 || nk > kFT || !blocks_dev || !x_dev || !H_dev) {
+        set_error("hb_forward_history_far: bad arguments");
+        return HB_ERR_INVALID;
+    }
+    k_hist_far<<<(unsigned)cdiv(R, 8 / kHW), 256, 0, (cudaStream_t)stream>>>(blocks_dev, R, C, n_blocks, k0, (int)nk,
+                                                                           x_dev, H_dev);
+    return cuda_check(cudaGetLastError(), "hb_forward_history_far");
+}
+
+extern "C" int hb_forward_history_near(int64_t n_blocks, int64_t R, int64_t C, const double *blocks_dev, int64_t k,
+                                       int64_t k0, const double *x_dev, const double *Hk_dev, double *h_dev,
+                                       void *stream)
+{
+    if (n_blocks < 1 || R < 1 || C < 1 || k < 1 || k0 < 0 || k0 > k || !blocks_dev || !x_dev || !h_dev) {
+        set_error("hb_forward_history_near: bad arguments");
+        return HB_ERR_INVALID;
+    }
+    if (k - k0 >= kFT) {
+        set_error("hb_forward_history_near: k - k0 must be below the tile length 8");
+        return HB_ERR_INVALID;
+    }
+    k_hist_near<<<(unsigned)cdiv(R, 8 / kHW), 256, 0, (cudaStream_t)stream>>>(
+        blocks_dev, R, C, k, std::min(k - k0, n_blocks - 1), x_dev, Hk_dev, h_dev);
+    return cuda_check(cudaGetLastError(), "hb_forward_history_near");
+}
+
 extern "C" int hb_inv_apply(int64_t n, const double *inv_dev, const double *rhs_dev, const double *h_dev,
                             double *x_dev, void *stream)
 {
@@ -499,7 +706,7 @@ extern "C" int hb_inv_apply(int64_t n, const double *inv_dev, const double *rhs_
         set_error("hb_inv_apply: bad arguments");
         return HB_ERR_INVALID;
     }
-    k_inv_apply<<<(unsigned)cdiv(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(inv_dev, n, rhs_dev, h_dev,
+    k_inv_apply<<<(unsigned)cdiv(n, 8 / kHW), 256, 0, (cudaStream_t)stream>>>(inv_dev, n, rhs_dev, h_dev,
                                                                              h_dev ? 1 : 0, x_dev);
     return cuda_check(cudaGetLastError(), "hb_inv_apply");
 }

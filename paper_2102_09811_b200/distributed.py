@@ -21,6 +21,8 @@ import numpy as np
 
 from . import _native
 
+FORWARD_TILE = 8   # steps per tile of the blocked forward substitution (hb_solver.cu kFT)
+
 
 def block_range(rank: int, world: int, n_blocks: int):
     """Contiguous balanced split of [0, n_blocks): (d0, d1) for ``rank``."""
@@ -586,13 +588,14 @@ class RowShardedToeplitz:
 
     * ``apply``: the local rows of y = A x from the replicated x, then ONE
       all-gather of the row pieces -- the density all-gather of the solve.
-    * ``forward_solve``: per step the local rows of the history
-      h^k = sum_{d>=1} A^d x^{k-d} (hb_forward_history), one all-gather of h^k
-      (R values) and x^k = (A^0)^{-1} (rhs^k - h^k) on every rank (the
-      inverse is replicated: A^0's rows are gathered once).
+    * ``forward_solve``: in tiles of 8 steps as hb_forward_solve_ws -- per tile
+      the local rows of the far history (one pass over the local blocks), per
+      step the near terms, one all-gather of h^k (R values) and
+      x^k = (A^0)^{-1} (rhs^k - h^k) on every rank (the inverse is
+      replicated: A^0's rows are gathered once).
 
-    The per-rank kernels are the methods ``local_apply`` / ``local_history``
-    / ``inv_apply`` (tests on CPU replace them by numpy stand-ins)."""
+    The per-rank kernels are the methods ``local_apply`` / ``local_history_far``
+    / ``local_history`` / ``inv_apply`` (tests on CPU replace them by numpy stand-ins)."""
 
     def __init__(self, local, r0: int, r1: int, n_rows: int, group=None):
         if local.shape[1] != r1 - r0:
@@ -650,12 +653,26 @@ class RowShardedToeplitz:
                      _native.stream_handle())
         return y
 
-    def local_history(self, x, k: int):
+    def local_history_far(self, x, k0: int, nk: int):
+        """Local rows of the far history of the step tile [k0, k0 + nk): terms
+        with k - d < k0, (nk, r1 - r0) (hb_forward_history_far)."""
+        import torch
+
+        H = torch.empty((nk, self.r1 - self.r0), dtype=torch.float64, device=x.device)
+        _native.call("hb_forward_history_far", self.n_blocks, self.r1 - self.r0, self.C, _native.ptr(self.local), k0,
+                     nk, _native.ptr(x), _native.ptr(H), _native.stream_handle())
+        return H
+
+    def local_history(self, x, k: int, k0: int = 0, Hk=None):
+        """Local rows of h^k: Hk (the far terms, if given) + the near terms
+        d = 1..k - k0 of step k of the tile starting at k0 (k - k0 < 8,
+        hb_forward_history_near)."""
         import torch
 
         h = torch.empty(self.r1 - self.r0, dtype=torch.float64, device=x.device)
-        _native.call("hb_forward_history", self.n_blocks, self.r1 - self.r0, self.C, _native.ptr(self.local), k,
-                     _native.ptr(x), _native.ptr(h), _native.stream_handle())
+        _native.call("hb_forward_history_near", self.n_blocks, self.r1 - self.r0, self.C, _native.ptr(self.local), k,
+                     k0, _native.ptr(x), _native.ptr(Hk) if Hk is not None else None, _native.ptr(h),
+                     _native.stream_handle())
         return h
 
     def inv_apply(self, inv, rhs_k, h):
@@ -700,9 +717,13 @@ class RowShardedToeplitz:
             raise ValueError("more time steps than stored blocks")
         rhs = rhs.contiguous()
         x = torch.zeros((E_t, self.C), dtype=torch.float64, device=rhs.device)
-        for k in range(E_t):
-            h = self.gather_rows(self.local_history(x, k)) if k > 0 else None
-            x[k] = self.inv_apply(inv, rhs[k], h)
+        for k0 in range(0, E_t, FORWARD_TILE):   # the tiles of hb_forward_solve_ws, same per-row sums
+            nk = min(FORWARD_TILE, E_t - k0)
+            H = self.local_history_far(x, k0, nk) if k0 > 0 else None
+            for k in range(k0, k0 + nk):
+                h = (self.gather_rows(self.local_history(x, k, k0, H[k - k0] if H is not None else None))
+                     if k > 0 else None)
+                x[k] = self.inv_apply(inv, rhs[k], h)
         return x
 
     def solve(self, rhs, rel_tol: float = 1e-10, max_iter: int = 500, restart: int = 50):

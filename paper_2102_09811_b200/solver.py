@@ -113,7 +113,8 @@ def _inverse(matrix, tr):
 
 def forward_block_solve(matrix: BlockToeplitzMatrix, rhs, transpose_blocks: bool = False):
     """Causal time marching A^0 x^k = rhs^k - sum_{d>=1} A^d x^{k-d} (solver.py:165-184):
-    one hb_forward_solve call (history and inverse-apply kernels per step)."""
+    one hb_forward_solve_ws call (steps in tiles of 8: one history pass over
+    the blocks per tile, then the near terms and the inverse apply per step)."""
     import torch
 
     _native.require_cuda()
@@ -131,9 +132,10 @@ def forward_block_solve(matrix: BlockToeplitzMatrix, rhs, transpose_blocks: bool
         raise ValueError("more time steps than stored blocks")
     inv = _inverse(matrix, tr)
     x = torch.empty((E_t, R), dtype=torch.float64, device=r.device)
-    h = torch.empty(R, dtype=torch.float64, device=r.device)
-    _native.call("hb_forward_solve", nb, R, _native.ptr(B), int(tr), int(matrix.diagonal_only), E_t,
-                 _native.ptr(inv), _native.ptr(r), _native.ptr(x), _native.ptr(h), _native.stream_handle())
+    need = _native.load().hb_forward_solve_workspace(R)
+    ws = _workspace(r.device, need)
+    _native.call("hb_forward_solve_ws", nb, R, _native.ptr(B), int(tr), int(matrix.diagonal_only), E_t,
+                 _native.ptr(inv), _native.ptr(r), _native.ptr(x), _native.ptr(ws), int(need), _native.stream_handle())
     out = x.reshape(-1) if squeeze else x
     return out if was_torch else out.cpu().numpy()
 

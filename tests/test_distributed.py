@@ -179,10 +179,19 @@ def _np_local_apply(self, x):
     return torch.from_numpy(y)
 
 
-def _np_local_history(self, x, k):
+def _np_local_history_far(self, x, k0, nk):
     A = self.local.numpy()
-    h = np.zeros(A.shape[1])
-    for d in range(1, min(k, A.shape[0] - 1) + 1):
+    H = np.zeros((nk, A.shape[1]))
+    for i in range(nk):
+        for d in range(i + 1, min(k0 + i, A.shape[0] - 1) + 1):   # k0 + i - d < k0
+            H[i] += A[d] @ x[k0 + i - d].numpy()
+    return torch.from_numpy(H)
+
+
+def _np_local_history(self, x, k, k0=0, Hk=None):
+    A = self.local.numpy()
+    h = np.zeros(A.shape[1]) if Hk is None else Hk.numpy().copy()
+    for d in range(1, min(k - k0, A.shape[0] - 1) + 1):
         h += A[d] @ x[k - d].numpy()
     return torch.from_numpy(h)
 
@@ -198,6 +207,7 @@ def _row_worker(rank, world, port, B, x, rhs, out):
     try:
         D.RowShardedToeplitz.local_apply = _np_local_apply
         D.RowShardedToeplitz.local_history = _np_local_history
+        D.RowShardedToeplitz.local_history_far = _np_local_history_far
         D.RowShardedToeplitz.inv_apply = _np_inv_apply
         n_blocks, R, _ = B.shape
         d0, d1 = D.block_range(rank, world, n_blocks)
@@ -221,7 +231,7 @@ def test_row_sharded_apply_and_forward_solve_gloo(world, n):
     identical on every rank and equal to the dense expansion; row ranges of
     unequal length (n = 7 over 2 ranks, 8 over 3)."""
     rng = np.random.default_rng(n)
-    E_t = 7
+    E_t = 19   # three step tiles of the blocked substitution (8, 8, 3)
     B = 0.2 * rng.standard_normal((E_t, n, n))
     B[0] += 3 * np.eye(n)
     x = rng.standard_normal((E_t, n))

@@ -198,9 +198,13 @@ def test_row_sharded_kernels_bitwise(world):
     assert torch.equal(y, hb.apply_toeplitz(M, x))
     inv = torch.linalg.inv(Bd[0]).contiguous()
     xs = torch.zeros_like(rhs)
-    for k in range(E_t):
-        h = torch.cat([s.local_history(xs, k) for s in shards]) if k else None
-        xs[k] = shards[0].inv_apply(inv, rhs[k], h)
+    for k0 in range(0, E_t, D.FORWARD_TILE):   # the step tiles of the blocked substitution
+        nk = min(D.FORWARD_TILE, E_t - k0)
+        H = [s.local_history_far(xs, k0, nk) for s in shards] if k0 else None
+        for k in range(k0, k0 + nk):
+            h = (torch.cat([s.local_history(xs, k, k0, H[i][k - k0] if H else None) for i, s in enumerate(shards)])
+                 if k else None)
+            xs[k] = shards[0].inv_apply(inv, rhs[k], h)
     assert torch.equal(xs, hb.forward_block_solve(M, rhs))
     if world == 1:
         assert torch.equal(shards[0].apply(x), y)
