@@ -220,7 +220,7 @@ constexpr int kFT = 8;
 // keeps x[k0 + i - d][c] (i < kFT) of the current d in registers -- one new x
 // load per element of A as d grows; sums in fixed order (column, d, lanes, warps)
 // (R output rows -- all of a square operator or one rank's row shard -- by C columns)
-__global__ void __launch_bounds__(256) k_hist_far(const double *__restrict__ blocks, int64_t R, int64_t C,
+__global__ void __launch_bounds__(256, 3) k_hist_far(const double *__restrict__ blocks, int64_t R, int64_t C,
                                                   int64_t n_blocks, int64_t k0, int nk, const double *__restrict__ x,
                                                   double *__restrict__ H)
 {
@@ -271,7 +271,8 @@ __global__ void __launch_bounds__(256) k_hist_far(const double *__restrict__ blo
     }
 }
 
-// h[r] = Hk[r] (far terms, if any) + sum_{d=1..dn} A^d(r, :) x[k - d] (near terms)
+// h[r] = Hk[r] (far terms, if any) + sum_{d=1..dn} A^d(r, :) x[k - d] (near
+// terms, dn < kFT; the blocks are L2-resident across the tile's steps)
 __global__ void __launch_bounds__(256) k_hist_near(const double *__restrict__ blocks, int64_t R, int64_t C,
                                                    int64_t k, int64_t dn, const double *__restrict__ x,
                                                    const double *__restrict__ Hk, double *__restrict__ h)
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(256) k_hist_near(const double *__restrict__ bl
     const int64_t r = (int64_t)blockIdx.x * (8 / kHW) + warp / kHW;
     double acc = 0.0;
     if (r < R) {
-        // column-outer, d-inner (dn < kFT): the dn loads of a column are in flight together
+        // column-outer, d-inner: the dn loads of a column are in flight together
         for (int64_t c = lane + 32 * sub; c < C; c += 32 * kHW) {
             double av[kFT - 1], xv[kFT - 1];
 #pragma unroll
@@ -301,6 +302,34 @@ __global__ void __launch_bounds__(256) k_hist_near(const double *__restrict__ bl
         double v = Hk ? Hk[r] : 0.0;
         for (int w = 0; w < kHW; ++w) v += part[warp + w];
         h[r] = v;
+    }
+}
+
+constexpr int kNW = 8;
+// x_k[i] = sum_j inv[i][j] (rhs_k[j] - h[j]) for the blocked substitution: one
+// row per CTA, 8 warps over interleaved 32-column slices, partials in warp order
+__global__ void __launch_bounds__(256) k_inv_apply_row(const double *__restrict__ inv, int64_t n,
+                                                       const double *__restrict__ rhs_k,
+                                                       const double *__restrict__ h, int has_h,
+                                                       double *__restrict__ x_k)
+{
+    __shared__ double part[kNW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x;
+    const double *a = inv + i * n;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int64_t j = lane + 32 * warp; j < n; j += 32 * kNW) {
+        const double v = has_h ? __ldg(rhs_k + j) - __ldg(h + j) : __ldg(rhs_k + j);
+        acc = fma(__ldg(a + j), v, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) part[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < kNW; ++w) v += part[w];
+        x_k[i] = v;
     }
 }
 
@@ -642,7 +671,7 @@ extern "C" int hb_forward_solve_ws(int64_t n_blocks, int64_t n, const double *bl
         return hb_forward_solve(n_blocks, n, blocks_dev, transpose, diagonal_only, n_steps, inv_dev, rhs_dev, x_dev,
                                 h, stream);
     cudaStream_t st = (cudaStream_t)stream;
-    const unsigned g_rows = (unsigned)cdiv(n, 8 / kHW), g_hist = (unsigned)cdiv(n, 8 / kHW);
+    const unsigned g_hist = (unsigned)cdiv(n, 8 / kHW);
     for (int64_t k0 = 0; k0 < n_steps; k0 += kFT) {
         const int nk = (int)std::min<int64_t>(kFT, n_steps - k0);
         if (k0 > 0) k_hist_far<<<g_hist, 256, 0, st>>>(blocks_dev, n, n, n_blocks, k0, nk, x_dev, H);
@@ -652,7 +681,8 @@ extern "C" int hb_forward_solve_ws(int64_t n_blocks, int64_t n, const double *bl
             if (hist)
                 k_hist_near<<<g_hist, 256, 0, st>>>(blocks_dev, n, n, k, dn, x_dev,
                                                     k0 > 0 ? H + (k - k0) * n : nullptr, h);
-            k_inv_apply<<<g_rows, 256, 0, st>>>(inv_dev, n, rhs_dev + k * n, h, hist ? 1 : 0, x_dev + k * n);
+            k_inv_apply_row<<<(unsigned)n, 256, 0, st>>>(inv_dev, n, rhs_dev + k * n, h, hist ? 1 : 0,
+                                                         x_dev + k * n);
         }
     }
     return cuda_check(cudaGetLastError(), "hb_forward_solve_ws");
@@ -706,7 +736,7 @@ extern "C" int hb_inv_apply(int64_t n, const double *inv_dev, const double *rhs_
         set_error("hb_inv_apply: bad arguments");
         return HB_ERR_INVALID;
     }
-    k_inv_apply<<<(unsigned)cdiv(n, 8 / kHW), 256, 0, (cudaStream_t)stream>>>(inv_dev, n, rhs_dev, h_dev,
+    k_inv_apply_row<<<(unsigned)n, 256, 0, (cudaStream_t)stream>>>(inv_dev, n, rhs_dev, h_dev,
                                                                              h_dev ? 1 : 0, x_dev);
     return cuda_check(cudaGetLastError(), "hb_inv_apply");
 }
