@@ -2845,6 +2845,7 @@ static int run_pairs(const hb_assembly_desc *a, const PairArgs &A, cudaStream_t 
 // the direct pair kernel (csrc/hb_pairs_direct.cu): one 32-gap window
 int direct_pairs(const hb_mesh_desc *m, const hb_assembly_desc *a, int64_t e0, int64_t e1, int d0, int d1,
                  double *Q, unsigned long long *counter, cudaStream_t st);
+void direct_window(int64_t E_t, int64_t d, int &w0, int &w1);   // hb_pairs_direct.cu
 
 static int moment_table(const hb_assembly_desc *a, const PairArgs &A, double *Tm, cudaStream_t st)
 {
@@ -2947,9 +2948,15 @@ static PairArgs make_pair_args(const hb_mesh_desc *m, const hb_assembly_desc *a)
 // gap windows of a call: the moment form covers all blocks in one; the direct
 // form windows of <= 32 gap slots (the first from block 0 or 1 holds 32 blocks,
 // later ones 30)
+// direct windows are the global ones of direct_window ([0, 32), [32, 62), ...)
+// clipped to the call's range: a call's blocks are computed in the same warps
+// whatever its d-range (d-sharded ranks, chunks reproduce the 1-GPU blocks)
 static int64_t window_end(const hb_assembly_desc *a, bool moments, int64_t d0)
 {
-    return moments ? a->d_end : std::min<int64_t>(a->d_end, (d0 <= 1) ? 32 : d0 + 30);
+    if (moments) return a->d_end;
+    int w0, w1;
+    direct_window(a->E_t, d0, w0, w1);
+    return std::min<int64_t>(a->d_end, w1);
 }
 
 // the pair kernels of rows [e0, e1) and blocks [d0, d1) into staging A.Q

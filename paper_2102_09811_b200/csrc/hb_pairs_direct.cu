@@ -375,7 +375,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                     for (int j = 0; j < NJ; ++j) {
                         const double x = __dmul_rn(rho, T.cx[j]);
                         const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                        const double f = special::eval<OP + 4>(x, ix, tab, kFull);
+                        const double f = special::eval_u<OP + 4>(x, ix, tab, kFull);
                         const double v = ok ? f : 0.0;
 #pragma unroll
                         for (int c = 0; c < 3; ++c) inner[j][c] = fma(v, p[HOFF + c], inner[j][c]);
@@ -392,7 +392,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
                     for (int j = 0; j < NJ; ++j) {
                         const double x = __dmul_rn(rho, T.cx[j]);
                         const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                        const double f = special::eval<OP + 4>(x, ix, tab, kFull);
+                        const double f = special::eval_u<OP + 4>(x, ix, tab, kFull);
                         const double v = ok ? f : 0.0;
 #pragma unroll
                         for (int i = 0; i < NIJ; ++i) acc[j][i] = fma(v, p[HOFF + i], acc[j][i]);
@@ -428,7 +428,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
 #pragma unroll
                         for (int g = 0; g < G; ++g) xs[g] = __dmul_rn(rho[g], T.cx[j]);
                         const double icj = T.ic[j];
-                        special::eval_nf<OP + 4, G>(
+                        special::eval_unf<OP + 4, G>(
                             xs, [&](int g) { return __dmul_rn(OP == 0 ? b[g] : a[g], icj); }, fs, tab, kFull);
 #pragma unroll
                         for (int g = 0; g < G; ++g) {
@@ -475,7 +475,7 @@ __device__ __forceinline__ void eval_pair(const PairArgs &A, const Geom &g, int 
 #if HB_FUSED
                     const double x = __dmul_rn(rho, T.cx[j]);
                     const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                    const double f = special::eval<OP + 4>(x, ix, tab, mask);
+                    const double f = special::eval_u<OP + 4>(x, ix, tab, mask);
                     // rho <= r_eps limits, divided by the per-gap factor applied at the end
                     if (OP == 0) val = sm ? 2.0 * T.kk[j] / T.sc[j] : f;
                     else if (OP == 1) val = sm ? 0.0 : f;
@@ -713,7 +713,7 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) xs[gg] = __dmul_rn(rho[gg], T.cx[j]);
                     const double icj = T.ic[j];
-                    special::eval_nf<5, G>(xs, [&](int gg) { return __dmul_rn(a[gg], icj); }, fs, tab, kFull);
+                    special::eval_unf<5, G>(xs, [&](int gg) { return __dmul_rn(a[gg], icj); }, fs, tab, kFull);
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
@@ -734,7 +734,7 @@ __device__ __forceinline__ void eval_pair_dual(const PairArgs &A, const RegularG
                 for (int j = 0; j < NJ; ++j) {
                     const double x = __dmul_rn(rho, T.cx[j]);
                     const double ix = __dmul_rn(s1, T.ic[j]);
-                    const double f = special::eval<5>(x, ix, tab, mask);
+                    const double f = special::eval_u<5>(x, ix, tab, mask);
                     const double val = sm ? 0.0 : f;
 #pragma unroll
                     for (int i = 0; i < 3; ++i) {
@@ -1023,12 +1023,12 @@ __global__ void __launch_bounds__(HB_PAIR_WARPS * 32, (TP1 && SP1) ? HB_P1P1_MIN
     extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *tab = smem;
-    special::load_table<OP + 4>(tab);   // factor-free kinds (hb_special.cuh)
+    special::load_utable<OP + 4>(tab);   // factor-free kinds, uniform pieces (hb_special.cuh)
     __syncthreads();
     constexpr int kPerWarp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
-    static_assert(special::kTabDoubles % 2 == 0 && kPerWarp % 2 == 0 && Layout<OP, NIJ>::PAY % 2 == 0 &&
+    static_assert(special::kUTabDoubles % 2 == 0 && kPerWarp % 2 == 0 && Layout<OP, NIJ>::PAY % 2 == 0 &&
                       kDualPay % 2 == 0, "payload slots must stay 16-byte aligned (LDS.128)");
-    double *geo = smem + special::kTabDoubles + warp * kPerWarp;
+    double *geo = smem + special::kUTabDoubles + warp * kPerWarp;
     double *Ls = geo + 32 * Layout<OP, NIJ>::PAY;
     double *Ls_dual = geo + 32 * kDualPay;
     const hb_mesh_desc &M = A.m;
@@ -1079,7 +1079,7 @@ static int launch_pairs(const PairArgs &A, cudaStream_t st)
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     constexpr bool SYM = (OP != 1);
     constexpr int per_warp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
-    const size_t sm = ((size_t)HB_PAIR_WARPS * per_warp + special::kTabDoubles) * sizeof(double);
+    const size_t sm = ((size_t)HB_PAIR_WARPS * per_warp + special::kUTabDoubles) * sizeof(double);
     auto kp = k_pairs<OP, TP1, SP1, NJ, SYM, DUAL>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int dev = 0, nsm = 0, per_sm = 0;
@@ -1132,6 +1132,14 @@ static int run_pairs(const hb_assembly_desc *a, int nj, const PairArgs &A, cudaS
 }  // namespace direct
 
 // one 32-gap window [d0, d1) of test rows [e0, e1): pair kernel into the staging Q
+// the global direct window [w0, w1) holding block d: [0, 32), then 30 blocks
+// each ([32, 62), [62, 92), ...), clipped at E_t -- 32 gaps each
+void direct_window(int64_t E_t, int64_t d, int &w0, int &w1)
+{
+    w0 = d < 32 ? 0 : 32 + 30 * (int)((d - 32) / 30);
+    w1 = (int)std::min<int64_t>(E_t, w0 == 0 ? 32 : w0 + 30);
+}
+
 int direct_pairs(const hb_mesh_desc *m, const hb_assembly_desc *a, int64_t e0, int64_t e1, int d0, int d1,
                  double *Q, unsigned long long *counter, cudaStream_t st)
 {
@@ -1151,11 +1159,18 @@ int direct_pairs(const hb_mesh_desc *m, const hb_assembly_desc *a, int64_t e0, i
     A.counter = counter;
     A.e0 = e0;
     A.e1 = e1;
+    // gaps of the whole global window holding [d0, d1) (direct_window(): [0, 32),
+    // [32, 62), [62, 92), ...), whatever part of it the call stores: which
+    // evaluations share a warp -- and so every value -- does not depend on the
+    // call's d-range (the all-series vote of hb_special.cuh eval_unf)
+    int w0, w1;
+    direct_window(a->E_t, d0, w0, w1);
+    if (d1 > w1) return HB_ERR_INVALID;
     A.d0 = d0;
     A.d1 = d1;
     A.nd = d1 - d0;
-    A.it_lo = std::max(1, d0 - 1);
-    A.it_hi = d1;
+    A.it_lo = std::max(1, w0 - 1);
+    A.it_hi = w1;
     A.need_special = d0 <= 1;
     const int nj = std::min(choose_nj(a), (int)cdiv(A.it_hi - A.it_lo + 1, 16));
     return run_pairs(a, std::max(1, nj), A, st);

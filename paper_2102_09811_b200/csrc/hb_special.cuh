@@ -311,6 +311,98 @@ __device__ __forceinline__ void eval_nf(const double (&x)[NJ], const IXF &ixf, d
     }
 }
 
+// ---------------------------------------------------------------------------
+// Uniform pieces (the direct pair kernels, kinds 4-6).  A warp whose
+// evaluations all lie in the series region (x < X0) takes the constant-bank
+// series; any other warp evaluates EVERY lane on the uniform pieces of
+// [0, XL) -- piece p = floor(16 x) of width 1/16, degree 7 in
+// u = 2 (16 x - p) - 1 (exact) -- with no series / middle select, merged
+// chain or region reduction; lanes at or above XL take the asymptote.  A
+// lane's form thus depends on the other lanes' x through the all-series vote:
+// the direct kernels fix which evaluations share a warp by evaluating whole
+// global gap windows (hb_pairs_direct.cu direct_pairs), so blocks stay
+// independent of the d-range / row chunk / rank of a call.
+// Table: coefficients 2m, 2m+1 of piece p side by side at double2 index
+// m kUPieces + p (one LDS.128 per two Horner steps).
+// ---------------------------------------------------------------------------
+constexpr int kUTabDoubles = (kUDeg + 1) * kUPieces;
+static_assert((kUDeg & 1) == 1 && kUTabDoubles % 2 == 0, "uniform pieces: coefficient pairs");
+
+template <int KIND>
+__device__ __forceinline__ void load_utable(double *utab)
+{
+    static_assert(KIND >= 4 && KIND <= 6, "uniform pieces exist for the factor-free kinds 4-6");
+    const double *src = KIND == 4 ? kU4 : KIND == 5 ? kU5 : kU6;
+    for (int i = threadIdx.x; i < kUTabDoubles; i += blockDim.x) {
+        const int slot = i >> 1, m = slot / kUPieces, p = slot - m * kUPieces;
+        utab[i] = src[(2 * m + (i & 1)) * kUPieces + p];
+    }
+}
+
+template <int KIND, int NJ, class IXF>
+__device__ __forceinline__ void eval_unf(const double (&x)[NJ], const IXF &ixf, double (&r)[NJ],
+                                         const double *__restrict__ utab, unsigned mask)
+{
+    double t[NJ];
+    bool any_ns = false;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        t[j] = __dmul_rn(x[j], x[j]);
+        any_ns |= !(x[j] < kX0);
+    }
+    if (!__any_sync(mask, any_ns)) {   // every evaluation of the warp in the series region
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) r[j] = series<KIND>(x[j], t[j], 0.0);
+        return;
+    }
+    const double2 *t2 = reinterpret_cast<const double2 *>(utab);
+    constexpr int MT = kUDeg / 2;
+    int p[NJ];
+    double u[NJ];
+    bool huge[NJ], any_h = false;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const double y = __dmul_rn(x[j], kUInvH);   // exact (power of two)
+        const int pi = __double2int_rz(y);          // x >= 0: the floor; INT_MAX for inf
+        huge[j] = pi >= kUPieces;
+        any_h |= huge[j];
+        p[j] = min(pi, kUPieces - 1);
+        u[j] = fma(2.0, y - (double)p[j], -1.0);    // exact within the piece
+    }
+    double2 w[MT + 1][NJ];
+#pragma unroll
+    for (int m = MT; m >= 0; --m)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) w[m][j] = t2[m * kUPieces + p[j]];
+    double q[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) q[j] = fma(w[MT][j].y, u[j], w[MT][j].x);
+#pragma unroll
+    for (int m = MT - 1; m >= 0; --m) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], u[j], w[m][j].y);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], u[j], w[m][j].x);
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)   // kinds 4-6 finish like the series (x H = 2/sqrt(pi) + x^2 M)
+        r[j] = KIND == 4 ? fma(t[j], q[j], kTwoInvSqrtPi) : q[j];
+    if (__any_sync(mask, any_h)) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            if (huge[j]) r[j] = asymptote<KIND>(x[j], ixf(j));
+    }
+}
+
+template <int KIND>
+__device__ __forceinline__ double eval_u(double x, double ix, const double *__restrict__ utab, unsigned mask)
+{
+    double r[1];
+    const double xs[1] = {x};
+    eval_unf<KIND, 1>(xs, [&](int) { return ix; }, r, utab, mask);
+    return r[0];
+}
+
 template <int KIND, int NJ>
 __device__ __forceinline__ void eval_n(const double (&x)[NJ], const double (&ix)[NJ], double (&r)[NJ],
                                        const double *__restrict__ tab, unsigned mask)

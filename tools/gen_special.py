@@ -16,6 +16,8 @@ function of x = rho / (2 sqrt(alpha delta)):
   width 1/4, degree 12 in u = (x - mid) / half; all four are analytic there).
 * x >= XL = 6.25: the asymptotes erf = E = 1, H/F = 1 +- 1/(2x^2), which the
   exact values round to (e^{-x^2}(...) < 2^-53 relative; reported below).
+* the direct pair kernels' factor-free kinds (x H as M, F/x, erf/x) also as
+  uniform pieces of [0, XL): width 1/16, degree 7.
 """
 import os
 import sys
@@ -198,6 +200,35 @@ def main():
         out.append(f"static __device__ __constant__ double kMid{kind}[(kMidDegK[{kind}] + 1) * kMidPieces] = {{")
         for k in range(DEG_M[fname] + 1):
             out.append("    " + ", ".join(hexd(tab[pc][k]) for pc in range(MID_PIECES)) + ",")
+        out.append("};")
+    # ---- uniform pieces for the pair kernels' factor-free kinds (4 xH, 5 F/x, 6 erf/x) ----
+    # [0, XL) in pieces of width 1/16, degree 7 in u = 2 (16 x - p) - 1: ONE
+    # polynomial form for every lane below XL that is not in an all-series
+    # warp (no series / middle select), 4 LDS.128 + 7 FMA per value
+    U_INV_H, U_DEG = int(os.environ.get("HB_U_INV_H", "16")), int(os.environ.get("HB_U_DEG", "7"))
+    U_PIECES = int(XL * U_INV_H)
+    out.append("")
+    out.append(f"constexpr int kUPieces = {U_PIECES};   // uniform pieces of [0, XL), width 1/{U_INV_H}")
+    out.append(f"constexpr int kUDeg = {U_DEG};")
+    out.append(f"constexpr double kUInvH = {hexd(mp.mpf(U_INV_H))};")
+    for kind, (fname, f) in ((4, ("xH", F_xH)), (5, ("Fx", F_Fx)), (6, ("ex", F_ex))):
+        worst, tab = 0, []
+        for pc in range(U_PIECES):
+            a = mp.mpf(pc) / U_INV_H
+            b = a + mp.mpf(1) / U_INV_H
+            mono_u = cheb_interp_monomial(f, a, b, U_DEG)
+            for j in range(25):
+                x = mp.mpf(float(a + (b - a) * (j + mp.mpf(1) / 2) / 25))
+                y = mp.mpf(float(x * U_INV_H))
+                u = mp.mpf(float(2 * (y - int(mp.floor(y))) - 1))
+                worst = max(worst, abs(horner_double(mono_u, u) - f(x)) / abs(f(x)))
+            tab.append(mono_u)
+        report.append(f"uniform {fname}: {U_PIECES} pieces x degree {U_DEG} on [0, {float(XL)}), "
+                      f"max rel err (double Horner) {float(worst):.2e}")
+        out.append(f"// {report[-1]}")
+        out.append(f"static __device__ __constant__ double kU{kind}[(kUDeg + 1) * kUPieces] = {{")
+        for k in range(U_DEG + 1):
+            out.append("    " + ", ".join(hexd(tab[pc][k]) for pc in range(U_PIECES)) + ",")
         out.append("};")
     out += ["", "}  // namespace special", "}  // namespace hb", ""]
     path = os.environ.get("HB_SPECIAL_OUT") or os.path.join(

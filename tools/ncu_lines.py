@@ -1,23 +1,27 @@
-"""Per-CUDA-source-line instruction counts and stall samples of an .ncu-rep
-(source/SASS correlation page)."""
-import csv, subprocess, sys, collections
+"""Per-source-line instruction and stall-sample shares of one kernel from an
+ncu report (ncu --page source --print-source cuda,sass; needs -lineinfo):
+python tools/ncu_lines.py REPORT [kernel-regex] [top]"""
+import csv, subprocess, sys
+
 rep = sys.argv[1]
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
-rows = list(csv.reader(out.splitlines()))
-hdr = next(r for r in rows if r and r[0] == "Line No")
-ie, ss = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
-lines, cur, src = collections.Counter(), None, {}
-stall = collections.Counter()
-for r in rows:
-    if len(r) < len(hdr) or r[0] == "Line No":
+args = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+if len(sys.argv) > 2 and sys.argv[2]:
+    args += ["-k", "regex:" + sys.argv[2]]
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+out = subprocess.run(args, capture_output=True, text=True).stdout
+fname, rows = "?", []
+for r in csv.reader(out.splitlines()):
+    if not r:
         continue
-    if r[0]:
-        cur = int(r[0]); src[cur] = r[1]
-    try:
-        lines[cur] += int(r[ie] or 0); stall[cur] += int(r[ss] or 0)
-    except ValueError:
-        pass
-tot, tst = sum(lines.values()) or 1, sum(stall.values()) or 1
-for ln, c in sorted(lines.items(), key=lambda kv: -kv[1])[: int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
-    print(f"{ln:5d} {100*c/tot:5.1f}% instr {100*stall[ln]/tst:5.1f}% stall | {src.get(ln,'').strip()[:90]}")
+    if r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+    elif r[0].isdigit() and len(r) > 8 and r[2] == "-":
+        try:
+            rows.append((fname, int(r[0]), float(r[7] or 0), float(r[4] or 0), r[1].strip()[:100]))
+        except ValueError:
+            pass
+ti = sum(x[2] for x in rows) or 1
+ts = sum(x[3] for x in rows) or 1
+print(f"total warp instructions {ti:.3e}")
+for f, ln, ie, sm, src in sorted(rows, key=lambda x: -x[2])[:top]:
+    print(f"{f[:16]:16s}{ln:5d} inst {100 * ie / ti:5.1f}% stall {100 * sm / ts:5.1f}%  {src}")
