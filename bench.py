@@ -34,10 +34,9 @@ Measurement (DESIGN.md "Measurement"):
 * cpu_baseline: one full config-2 assembly by the oracle port of the
   reference's algorithm (oracle/heatbem_oracle.c) on all host cores,
   measured, plus the per-pass sample rate (validates extrapolations).
-* --impl reference: per step one full delta-pass of V, K and D2 and one curl
-  block (every i_t >= 1 pass does the same work), tables built outside the
-  timed region; value = the work-equivalent entries per second; the line
-  also carries one measured full assembly.
+* --impl reference: per step one full config-2 assembly (V, K, D2 over all
+  E_t + 1 delta-passes, then D = D2 + curl V) by the oracle port on all host
+  cores, tables built outside the timed region; value = entries / median step.
 """
 from __future__ import annotations
 
