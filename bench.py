@@ -661,7 +661,8 @@ def run_native_c2(args, rank, world, local_rank):
     pinD = torch.empty(outD.shape, dtype=torch.float64).pin_memory()
 
     e2e_mode = os.environ.get("HB_E2E_MODE", "seq")   # "all": assemble_all(host_out) -- measured slower (6.4 vs 6.0 ms)
-    e2e_slabs = int(os.environ.get("HB_E2E_SLABS", "2"))
+    _sl = os.environ.get("HB_E2E_SLABS", "4")   # a count of equal-work slabs, or work fractions "a,b,c"
+    e2e_slabs = [float(x) for x in _sl.split(",")] if "," in _sl else int(_sl)
 
     def e2e_step():
         # mesh tables re-uploaded from pinned host memory every step

@@ -446,21 +446,30 @@ def assemble_double_layer(mesh, timegrid, params: KernelParams, config: Quadratu
     return res
 
 
-def _row_slabs(n_rows: int, symmetric: bool, n_slabs: int):
-    """Test-row ranges of equal pair work: upper-triangle rows (f >= e) for a
+def _row_slabs(n_rows: int, symmetric: bool, n_slabs):
+    """Test-row ranges of given shares of the pair work (``n_slabs``: a count
+    of equal shares, or a sequence of work fractions -- a small first slab
+    starts the device->host copies early): upper-triangle rows (f >= e) for a
     symmetric operator, uniform rows otherwise."""
-    n_slabs = max(1, min(int(n_slabs), n_rows))
-    if symmetric:
-        # work of rows [0, r) ~ r (2E - r): equal-work bounds r_k = E (1 - sqrt(1 - k/n))
-        bounds = [int(round(n_rows * (1.0 - np.sqrt(1.0 - k / n_slabs)))) for k in range(n_slabs + 1)]
+    if isinstance(n_slabs, (int, np.integer)):
+        n = max(1, min(int(n_slabs), n_rows))
+        cum = [k / n for k in range(n + 1)]
     else:
-        bounds = [int(round(n_rows * k / n_slabs)) for k in range(n_slabs + 1)]
+        fr = np.asarray(list(n_slabs), dtype=np.float64)
+        if fr.size < 1 or not np.all(fr > 0.0):
+            raise ValueError("slab work fractions must be positive")
+        cum = [0.0] + list(np.cumsum(fr) / fr.sum())
+    if symmetric:
+        # work of rows [0, r) ~ r (2E - r): bounds r = E (1 - sqrt(1 - share))
+        bounds = [int(round(n_rows * (1.0 - np.sqrt(max(0.0, 1.0 - c))))) for c in cum]
+    else:
+        bounds = [int(round(n_rows * c)) for c in cum]
     bounds[0], bounds[-1] = 0, n_rows
     return [(a, b) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
 
 
 def _assemble_streamed(op, test_p1, trial_p1, symmetric, mesh, timegrid, params, config, instrumentation,
-                       host_out, n_slabs: int = 3, stream=None, copy_stream=None, **kw):
+                       host_out, n_slabs=3, stream=None, copy_stream=None, **kw):
     """Assemble a p0-test operator in work-balanced test-row slabs and start
     each slab's device->host copy (rows [r0, r1) of every block, complete once
     the slab's rows are done: a symmetric operator's mirrored entries of those

@@ -2777,8 +2777,10 @@ static int launch_class(const PairArgs &A, cudaStream_t st)
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, HB_PAIR_WARPS * 32, sm);
     const int64_t rows = A.e1 - A.e0;
-    // separated-pair items of 32 trial elements, or shorter when few test rows
-    // (a row-parallel rank) would leave fewer than 4 items per resident warp
+    // separated-pair items of 32 trial elements, halved while the launch holds
+    // fewer than 16 items per resident warp (the persistent grid's tail is about
+    // one item per warp: config 2 V pair kernels 1.02 -> 0.975 ms; a row-parallel
+    // rank's few rows likewise)
     PairArgs B = A;
     const int64_t warps = (int64_t)std::max(1, per_sm) * nsm * HB_PAIR_WARPS;
     B.seg_len = 32;
@@ -2788,7 +2790,8 @@ static int launch_class(const PairArgs &A, cudaStream_t st)
     static const int min_seg = getenv("HB_MIN_SEG") ? atoi(getenv("HB_MIN_SEG")) : 4;
     static const int min_far = getenv("HB_MIN_SEG_FAR") ? atoi(getenv("HB_MIN_SEG_FAR")) : 32;
     const int seg_floor = std::max(1, std::min(32, CLS == 2 ? min_far : min_seg));
-    while (B.seg_len > seg_floor && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < 4 * warps) B.seg_len /= 2;
+    static const int ipw = getenv("HB_ITEMS_PER_WARP_M") ? std::max(1, atoi(getenv("HB_ITEMS_PER_WARP_M"))) : 16;
+    while (B.seg_len > seg_floor && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < ipw * warps) B.seg_len /= 2;
     const int64_t items = (CLS == 1 || CLS == 4 ? rows * A.m.sing_max_per_row : 0) +
                           (CLS == 1 ? 0 : rows * cdiv(A.m.E_x, (int64_t)B.seg_len));
     // (near-pair items: most segments hold none and exit after the classification)

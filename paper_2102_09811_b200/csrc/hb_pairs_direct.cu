@@ -1087,14 +1087,19 @@ static int launch_pairs(const PairArgs &A, cudaStream_t st)
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, HB_PAIR_WARPS * 32, sm);
     const int64_t rows = A.e1 - A.e0;
-    // separated-pair items of 32 trial elements, or shorter when few test rows
-    // (a row-parallel rank) would leave fewer than 4 items per resident warp
+    // separated-pair items of 32 trial elements, halved while the launch holds
+    // fewer than 16 items per resident warp (HB_ITEMS_PER_WARP): the persistent grid's
+    // tail is about one item per warp, so few large items leave SMs idle at the
+    // end (config 2: 8 items per warp at 32 -> 31 at 8 elements: K 1.36 -> 1.25 ms,
+    // D2 1.00 -> 0.89 ms; the values do not depend on the grouping: warp per pair)
     PairArgs B = A;
     const int64_t warps = (int64_t)std::max(1, per_sm) * nsm * HB_PAIR_WARPS;
-    B.seg_len = 32;
+    static const int seg0 = getenv("HB_SEG_LEN") ? std::max(1, std::min(32, atoi(getenv("HB_SEG_LEN")))) : 32;
+    static const int ipw = getenv("HB_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("HB_ITEMS_PER_WARP"))) : 16;
+    B.seg_len = seg0;
     static const int min_seg = getenv("HB_MIN_SEG") ? atoi(getenv("HB_MIN_SEG")) : 4;
     const int seg_floor = std::max(1, std::min(32, min_seg));
-    while (B.seg_len > seg_floor && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < 4 * warps) B.seg_len /= 2;
+    while (B.seg_len > seg_floor && rows * cdiv(A.m.E_x, (int64_t)B.seg_len) < ipw * warps) B.seg_len /= 2;
     const int64_t items = rows * cdiv(A.m.E_x, (int64_t)B.seg_len) + rows * A.m.sing_max_per_row;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(1, per_sm) * nsm, cdiv(items, HB_PAIR_WARPS)));
     int rc = cuda_check(cudaMemsetAsync(A.counter, 0, sizeof(unsigned long long), st), "counter reset");

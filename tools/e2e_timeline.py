@@ -21,7 +21,8 @@ Hpin = hbdev.pin_host_tables(hbdev.host_tables(m, q))
 pinV = torch.empty((32, E, E), dtype=torch.float64).pin_memory()
 pinK = torch.empty((32, E, N), dtype=torch.float64).pin_memory()
 pinD = torch.empty((32, N, N), dtype=torch.float64).pin_memory()
-slabs = int(os.environ.get("HB_E2E_SLABS", "2"))
+_sl = os.environ.get("HB_E2E_SLABS", "2")
+slabs = [float(x) for x in _sl.split(",")] if "," in _sl else int(_sl)
 def step(marks):
     cur = torch.cuda.current_stream()
     def mark(name):
