@@ -82,6 +82,24 @@ def curl_tile_plan(star_indptr, star_elem, n_nodes: int, tile: int = CURL_TILE):
     return eptr, elem, pos, int(np.diff(eptr).max()) if nt else 0, int(smax)
 
 
+class _LazyViews:
+    """``tables.t[name]``: the device view of one table, made on first use."""
+
+    def __init__(self, owner):
+        self._o, self._v = owner, {}
+
+    def __getitem__(self, name):
+        v = self._v.get(name)
+        if v is None:
+            o = self._o
+            off, n, dt, shape = o._where[id(o._names[name])]
+            v = self._v[name] = o._blob[off:off + n].view(dt).view(shape)
+        return v
+
+    def __contains__(self, name):
+        return name in self._o._names
+
+
 class DeviceTables:
     """Device copies of :class:`HostTables` plus ready-made C descriptors.
     With ``pinned`` host staging the uploads are async copies from page-locked
@@ -97,31 +115,37 @@ class DeviceTables:
         blob, where = _packed(H)
         self._blob = blob.to(device, non_blocking=True)
 
-        def up(a):
-            off, n, dt, shape = where[id(a)]
-            return self._blob[off:off + n].view(dt).view(shape)
-        self.t = {
-            "tri_nodes": up(H.tri_nodes), "verts_tri": up(H.verts_tri), "normals": up(H.normals),
-            "centroids": up(H.centroids), "diameters": up(H.diameters), "areas": up(H.areas),
-            "reg_hats": up(H.reg[0]), "reg_w": up(H.reg[1]), "reg_pts": up(H.reg[2]),
-            "near_hats": up(H.near[0]), "near_w": up(H.near[1]), "near_pts": up(H.near[2]),
-            "tn_indptr": up(H.tn[0]), "tn_idx": up(H.tn[1]), "tn_case": up(H.tn[2]),
-            "tn_permt": up(H.tn[3]), "tn_perms": up(H.tn[4]),
-            "duf_off": up(H.duf[0]), "duf_t": up(H.duf[1]), "duf_s": up(H.duf[2]), "duf_w": up(H.duf[3]),
-            "sing_row": up(H.sing_row),
-            "star_indptr": up(H.star[0]), "star_elem": up(H.star[1]), "star_local": up(H.star[2]),
-            "curls": up(H.curls),
-            "curl_tile_eptr": up(H.curl_plan[0]), "curl_tile_elem": up(H.curl_plan[1]),
-            "curl_star_pos": up(H.curl_plan[2]),
+        # name -> host array; device views are made on first use (``t[name]``),
+        # the descriptors take base + offset directly (no per-table tensor ops
+        # on the upload path: the cold-table call stays one async copy)
+        self._where = where
+        self._names = {
+            "tri_nodes": H.tri_nodes, "verts_tri": H.verts_tri, "normals": H.normals,
+            "centroids": H.centroids, "diameters": H.diameters, "areas": H.areas,
+            "reg_hats": H.reg[0], "reg_w": H.reg[1], "reg_pts": H.reg[2],
+            "near_hats": H.near[0], "near_w": H.near[1], "near_pts": H.near[2],
+            "tn_indptr": H.tn[0], "tn_idx": H.tn[1], "tn_case": H.tn[2],
+            "tn_permt": H.tn[3], "tn_perms": H.tn[4],
+            "duf_off": H.duf[0], "duf_t": H.duf[1], "duf_s": H.duf[2], "duf_w": H.duf[3],
+            "sing_row": H.sing_row,
+            "star_indptr": H.star[0], "star_elem": H.star[1], "star_local": H.star[2],
+            "curls": H.curls,
+            "curl_tile_eptr": H.curl_plan[0], "curl_tile_elem": H.curl_plan[1],
+            "curl_star_pos": H.curl_plan[2],
         }
         for sym in (False, True):
             pos, rp, _ = H.sing[sym]
-            self.t[f"sing_pos_{int(sym)}"] = up(pos)
-            self.t[f"sing_rowptr_{int(sym)}"] = up(rp)
+            self._names[f"sing_pos_{int(sym)}"] = pos
+            self._names[f"sing_rowptr_{int(sym)}"] = rp
+        self.t = _LazyViews(self)
         self._desc = {sym: self._make_desc(sym) for sym in (False, True)}
 
     def _make_desc(self, symmetric: bool) -> _native.MeshDesc:
-        t, H, p = self.t, self.host, _native.ptr
+        H = self.host
+        base, where, t = self._blob.data_ptr(), self._where, self._names
+
+        def p(a):   # device address of a table: blob base + its section offset
+            return base + where[id(a)][0]
         d = _native.MeshDesc()
         d.E_x, d.N_x = H.E_x, H.N_x
         d.tri_nodes_dev, d.verts_tri_dev = p(t["tri_nodes"]), p(t["verts_tri"])
