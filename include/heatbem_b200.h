@@ -280,7 +280,11 @@ int hb_represent_grid(int64_t n_points, int64_t n_times, int64_t E_t, int64_t E_
  * eps in [0, step): the outputs are u(x_i, k_j h + eps) -- eps > 0 is the
  * reference's current-interval case (_field_numba.py:53-76) and requires
  * k_j >= 1 (k_j = 0 outputs are written as NaN; field.py routes such points
- * through hb_potential). */
+ * through hb_potential).  kmax <= 64 for eps > 0; at time-step ends (eps = 0)
+ * kmax <= 512: histories longer than 64 steps run one launch per block of 64
+ * output steps, each contracting the gap windows below it as full Toeplitz
+ * tiles (the reference's _eval_potential handles any k, _field_numba.py:33-76;
+ * longer histories still go through hb_potential). */
 int hb_represent_grid_elem(int64_t n_points, int64_t n_times, int64_t E_t, int64_t E_x, int64_t nq,
                            const double *x_dev, const int64_t *k_dev, int64_t kmax,
                            const double *dens_elem_dev, const double *dens_vert_dev, const double *hats_dev,

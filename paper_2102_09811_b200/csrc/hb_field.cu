@@ -1115,6 +1115,7 @@ struct RepElemArgs {
     double step, alpha, d_eps, r_eps;
     double eps;               // evaluation times k h + eps (0: time-step ends)
     double *out;              // (n_points, n_times)
+    int kblock;               // LONG kernels: this launch forms the outputs k in (KM kblock, KM kblock + KM]
 };
 
 constexpr int kFTE = 256;   // k_represent_elem threads (8 warps, 32 points)
@@ -1123,10 +1124,11 @@ template <int KM>
 struct RepElemLayout {
     static constexpr int KS = (KM + 4) / 4, GS = 4 * KS, NT = KM / 8, ZP = GS, BR = ZP + KM + 1;
     static_assert(GS % 16 == 4, "conflict-free H fragment loads need a row stride of 4 mod 16");
-    static size_t doubles(int64_t nq)
+    // kt: time steps held per density vector (KM, or KM (kblock + 1) for the LONG kernels)
+    static size_t doubles(int64_t nq, int64_t kt = KM)
     {
-        return 2 * (size_t)special::kTabDoubles + 4 * kFP * GS + (HB_REP_FF ? 5 : 3) * (size_t)nq * kFP + 2 * 4 * BR +
-               2 * 2 * 4 * (KM + 1);
+        return 2 * (size_t)special::kTabDoubles + 4 * kFP * GS + (HB_REP_FF ? 5 : 3) * (size_t)nq * kFP +
+               2 * 4 * (size_t)(ZP + kt + 1) + 2 * 2 * 4 * (size_t)(kt + 1);
     }
 };
 
@@ -1134,13 +1136,27 @@ struct RepElemLayout {
 // out[k] = sum_{m=0..k} G(m h + eps) B[k - m] + G(0) W dens[k] -- the m = 0 row
 // is a regular kernel value and the G(0) term rides in the spare K row XR = KM + 1
 // against the element's density vector.
-template <int KM, bool EPS>
+//
+// LONG (histories longer than KM steps, eps = 0): the launch forms the output
+// block J = kblock, k = KM J + k', k' in 1..KM, from the gap windows
+// w = 0..J (gaps m = KM w + m', m' in 1..KM; G(0) in window 0):
+//   out[k] = sum_w sum_m' H_w[m'] T[KM (J - w) + k' - m']
+// -- window J is the triangular product of the short kernel, the windows below
+// are full tiles.  Each window's kernel values are evaluated into the same H
+// rows and contracted on the tensor cores before the next one; one launch per
+// output block (hb_represent_grid_elem loops J), so gap window w is evaluated
+// by the launches J >= w.
+template <int KM, bool EPS, bool LONG = false>
 __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P, int n_split)
 {
     using L = RepElemLayout<KM>;
-    constexpr int KS = L::KS, GS = L::GS, NT = L::NT, ZP = L::ZP, BR = L::BR;
+    constexpr int KS = L::KS, GS = L::GS, NT = L::NT, ZP = L::ZP;
     constexpr int MOFS = EPS ? 0 : 1, XR = KM + 1;
     static_assert(XR < GS, "the G(0) row must fit in the K padding");
+    static_assert(!(EPS && LONG), "long histories: time-step ends only");
+    const int J = LONG ? P.kblock : 0;
+    const int KT = KM * (J + 1);            // time steps held per density vector
+    const int BR = ZP + KT + 1, AS = KT + 1;
     extern __shared__ __align__(16) double fsm[];
     const int nq = (int)P.nq;
     double *tabS = fsm, *tabD = tabS + special::kTabDoubles;
@@ -1148,9 +1164,9 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
     double *Rn = H + 4 * kFP * GS;              // [nq][kFP] rho
     double *L0s = Rn + nq * kFP, *L0d = L0s + nq * kFP;   // [nq][kFP] G at m = 0
     double *Tv = L0d + nq * kFP;                // [2 buf][4][BR]: density differences, zeros before
-    double *Av = Tv + 2 * 4 * BR;               // [2 buf][4][KM + 1]: m = 0 row
-    double *Dv = Av + 2 * 4 * (KM + 1);         // [2 buf][4][KM + 1]: density (EPS: the G(0) term)
-    double *Ri = Dv + 2 * 4 * (KM + 1);         // HB_REP_FF: [nq][kFP] 1/rho
+    double *Av = Tv + 2 * 4 * BR;               // [2 buf][4][AS]: m = 0 row
+    double *Dv = Av + 2 * 4 * AS;               // [2 buf][4][AS]: density (EPS: the G(0) term)
+    double *Ri = Dv + 2 * 4 * AS;               // HB_REP_FF: [nq][kFP] 1/rho
     double *Rq = Ri + nq * kFP;                 // HB_REP_FF: [nq][kFP] rn / (4 pi) (0 for rho <= r_eps)
 #if HB_REP_FF
     special::load_table<6>(tabS);
@@ -1168,14 +1184,17 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
     constexpr int kS = (KM + 1 - MOFS + 31) / 32;   // lane passes over m = MOFS..KM
     double cm[kS], gsmall[kS], icm[kS];
     bool gzero[kS];
+    auto gap_constants = [&](int w) {   // gaps KM w + m', m' = lane + MOFS + 32 s
 #pragma unroll
-    for (int s = 0; s < kS; ++s) {
-        const double gap = (double)(lane + MOFS + 32 * s) * P.step + (EPS ? P.eps : 0.0);
-        icm[s] = 2.0 * sqrt(P.alpha * gap);
-        cm[s] = 1.0 / icm[s];
-        gsmall[s] = 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (P.alpha * P.alpha * P.alpha) * gap));
-        gzero[s] = gap <= P.d_eps;
-    }
+        for (int s = 0; s < kS; ++s) {
+            const double gap = (double)(KM * w + lane + MOFS + 32 * s) * P.step + (EPS ? P.eps : 0.0);
+            icm[s] = 2.0 * sqrt(P.alpha * gap);
+            cm[s] = 1.0 / icm[s];
+            gsmall[s] = 1.0 / (4.0 * sqrt((kPi * kPi * kPi) * (P.alpha * P.alpha * P.alpha) * gap));
+            gzero[s] = gap <= P.d_eps;
+        }
+    };
+    if (!LONG) gap_constants(0);
     const double inv4pi = 0.25 * kInvPi;
     const int gq = lane >> 2, tq = lane & 3;
     // phase C: warp w owns M tile (points 8 (w & 3) ..) and the N tiles n = 2 j + (w >> 2)
@@ -1207,23 +1226,29 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
             }
         }
         {
-            double *tv = Tv + buf * 4 * BR + ZP, *av = Av + buf * 4 * (KM + 1), *dd = Dv + buf * 4 * (KM + 1);
+            double *tv = Tv + buf * 4 * BR + ZP, *av = Av + buf * 4 * AS, *dd = Dv + buf * 4 * AS;
             const double *de = P.dens_e + e * P.E_t, *dv = P.dens_v + e * 3 * P.E_t;
-            for (int it = tid; it < 4 * (KM + 1); it += kFTE) {
-                const int v = it / (KM + 1), j = it - v * (KM + 1);
+            for (int it = tid; it < 4 * AS; it += kFTE) {
+                const int v = it / AS, j = it - v * AS;
                 const double *d = v == 0 ? de : dv + (v - 1) * P.E_t;
                 const double cur = j < P.E_t ? __ldg(d + j) : 0.0;
                 const double prev = (j >= 1 && j - 1 < P.E_t) ? __ldg(d + j - 1) : 0.0;
                 // single layer: B = s1 - s0, A1 = s1; double layer negated (u = V~q - W g)
                 tv[v * BR + j] = v == 0 ? prev - cur : -(prev - cur);
-                av[v * (KM + 1) + j] = v == 0 ? prev : -prev;
-                if (EPS) dd[v * (KM + 1) + j] = v == 0 ? cur : -cur;
+                av[v * AS + j] = v == 0 ? prev : -prev;
+                if (EPS) dd[v * AS + j] = v == 0 ? cur : -cur;
             }
         }
         __syncthreads();
+        const double a2 = 2.0 * __ldg(P.areas + e);
+#pragma unroll 1
+        for (int w = 0; w <= J; ++w) {   // gap windows (one, w = 0, unless LONG)
+        if (LONG) {
+            if (w > 0) __syncthreads();   // the previous window's products have read H
+            gap_constants(w);
+        }
         // ---- B: kernel values of every node, summed over the nodes in registers
         //      (lanes over m, node ascending) and stored once into H ----
-        const double a2 = 2.0 * __ldg(P.areas + e);
 #pragma unroll 1
         for (int p = warp; p < kFP; p += kFTE / 32) {
             double hsum[4][kS], hz[4];
@@ -1288,7 +1313,8 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 double *h = H + (v * kFP + p) * GS;
-                if (lane == 0) h[EPS ? XR : 0] = hz[v];   // G(0) sums: the m = 0 row, or row XR
+                // G(0) sums: the m = 0 row (of window 0), or row XR
+                if (lane == 0) h[EPS ? XR : 0] = (LONG && w > 0) ? 0.0 : hz[v];
 #pragma unroll
                 for (int s = 0; s < kS; ++s) {
                     const int m = lane + MOFS + 32 * s;
@@ -1300,7 +1326,11 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
         // ---- C: four Toeplitz products per element on the tensor cores ----
         {
             const double *hp = H + (8 * mt + gq) * GS + tq;
-            const double *tv = Tv + buf * 4 * BR + ZP, *av = Av + buf * 4 * (KM + 1), *dd = Dv + buf * 4 * (KM + 1);
+            // window w against the densities KM (J - w) steps back; the m = 0 row of
+            // window 0 against the previous step's density of the output k = KM J + k'
+            const double *tv = Tv + buf * 4 * BR + ZP + KM * (J - w), *av = Av + buf * 4 * AS + KM * J,
+                         *dd = Dv + buf * 4 * AS;
+            const bool diag = !LONG || w == J;   // the triangular window: tiles above the diagonal are empty
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
                 double a[4];
@@ -1311,13 +1341,13 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
                 for (int j = 0; j < NH; ++j) {
                     const int n = 2 * j + nh;
                     // whole tile above the diagonal (m > k) -- except the G(0) row XR (EPS)
-                    if (n >= NT || (8 * n + 8 < 4 * ks && !(EPS && ks == XR / 4))) continue;
+                    if (n >= NT || (diag && 8 * n + 8 < 4 * ks && !(EPS && ks == XR / 4))) continue;
                     const int k = 1 + 8 * n + gq;
                     double b[4];
 #pragma unroll
                     for (int v = 0; v < 4; ++v)
-                        b[v] = (EPS && m == XR) ? dd[v * (KM + 1) + k]
-                             : (!EPS && ks == 0 && tq == 0) ? av[v * (KM + 1) + k] : tv[v * BR + k - m];
+                        b[v] = (EPS && m == XR) ? dd[v * AS + k]
+                             : (!EPS && ks == 0 && tq == 0 && (!LONG || w == 0)) ? av[v * AS + k] : tv[v * BR + k - m];
                     dmma884(accS[j][0], accS[j][1], a[0], b[0]);
                     dmma884(accD[j][0], accD[j][1], a[1], b[1]);
                     dmma884(accD[j][0], accD[j][1], a[2], b[2]);
@@ -1325,6 +1355,7 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
                 }
             }
         }
+        }   // gap windows
     }
     __syncthreads();
     double *Os = H;   // [2][kFP][KM + 2]: single, negated double
@@ -1347,7 +1378,11 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
         const int64_t gg = pblock * kFP + p;
         if (gg >= P.n_points) continue;
         for (int64_t o = lane; o < P.n_times; o += 32) {
-            const int k = (int)P.k[o];
+            int k = (int)P.k[o];
+            if (LONG) {   // this launch's output block only (k = 0 belongs to block 0)
+                k -= KM * J;
+                if (k > KM || k < (J == 0 ? 0 : 1)) continue;
+            }
             double v = 0.0;
             for (int s = 0; s < n_split; ++s) {
                 const double *os = cl.map_shared_rank(Os, s);
@@ -1362,11 +1397,15 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
     cl.sync();
 }
 
-template <int KM, bool EPS>
+template <int KM, bool EPS, bool LONG = false>
 int launch_represent_elem(const RepElemArgs &P, cudaStream_t stream)
 {
-    auto kern = k_represent_elem<KM, EPS>;
-    const size_t sm = sizeof(double) * RepElemLayout<KM>::doubles(P.nq);
+    auto kern = k_represent_elem<KM, EPS, LONG>;
+    const size_t sm = sizeof(double) * RepElemLayout<KM>::doubles(P.nq, LONG ? (int64_t)KM * (P.kblock + 1) : KM);
+    if (sm > 227 * 1024) {
+        set_error("hb_represent_grid_elem: %d output blocks of %d steps do not fit shared memory", P.kblock + 1, KM);
+        return HB_ERR_UNSUPPORTED;
+    }
     constexpr int kFT = kFTE;
     static_assert(2 * kFP * (KM + 2) <= 4 * kFP * RepElemLayout<KM>::GS, "output staging must fit in H");
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1531,6 +1570,8 @@ extern "C" int hb_represent_grid(int64_t n_points, int64_t n_times, int64_t E_t,
     return launch_represent_reg<64>(P, st);
 }
 
+constexpr int kRepMaxBlocks = 8;   // histories up to 512 steps on the per-element kernel
+
 extern "C" int hb_represent_grid_elem(int64_t n_points, int64_t n_times, int64_t E_t, int64_t E_x, int64_t nq,
                                       const double *x_dev, const int64_t *k_dev, int64_t kmax,
                                       const double *dens_elem_dev, const double *dens_vert_dev,
@@ -1538,11 +1579,12 @@ extern "C" int hb_represent_grid_elem(int64_t n_points, int64_t n_times, int64_t
                                       const double *areas_dev, const double *normals_dev, double step, double alpha,
                                       double d_eps, double r_eps, double eps, double *out_dev, void *stream)
 {
-    if (n_points < 0 || n_times < 0 || E_t < 1 || E_x < 1 || nq < 1 || nq > 64 || kmax < 0 || kmax > 64 ||
-        !(eps >= 0.0 && eps < step) ||
+    if (n_points < 0 || n_times < 0 || E_t < 1 || E_x < 1 || nq < 1 || nq > 64 || kmax < 0 ||
+        (kmax > 64 && (eps > 0.0 || kmax > 64 * kRepMaxBlocks)) || !(eps >= 0.0 && eps < step) ||
         (n_points > 0 && n_times > 0 &&
          (!x_dev || !k_dev || !dens_elem_dev || !dens_vert_dev || !hats_dev || !out_dev))) {
-        set_error("hb_represent_grid_elem: bad arguments (kmax %lld: at most 64 output steps)", (long long)kmax);
+        set_error("hb_represent_grid_elem: bad arguments (kmax %lld: at most 64 output steps inside a step, "
+                  "%d at time-step ends)", (long long)kmax, 64 * kRepMaxBlocks);
         return HB_ERR_INVALID;
     }
     if (n_points == 0 || n_times == 0) return HB_OK;
@@ -1559,5 +1601,12 @@ extern "C" int hb_represent_grid_elem(int64_t n_points, int64_t n_times, int64_t
     }
     if (kmax <= 16) return launch_represent_elem<16, false>(P, st);
     if (kmax <= 32) return launch_represent_elem<32, false>(P, st);
-    return launch_represent_elem<64, false>(P, st);
+    if (kmax <= 64) return launch_represent_elem<64, false>(P, st);
+    // longer histories: one launch per block of 64 output steps, each over the gap windows below it
+    for (int J = 0; 64 * J < kmax; ++J) {
+        P.kblock = J;
+        const int rc = launch_represent_elem<64, false, true>(P, st);
+        if (rc) return rc;
+    }
+    return HB_OK;
 }

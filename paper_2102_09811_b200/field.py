@@ -451,9 +451,12 @@ def eval_double_layer_potential(u, points, mesh, timegrid, params: KernelParams,
     return _eval_potential(1, u, points, mesh, timegrid, params, config)
 
 
+_ELEM_MAX_STEPS = 512   # longest history of hb_represent_grid_elem at time-step ends (8 blocks of 64)
+
+
 def represent(w, u, points, mesh, timegrid, params: KernelParams, config: QuadratureConfig = QuadratureConfig()):
     """Representation formula V~w - Wu at EvalPoints (field.py:184-190).
-    Points at time-step ends (eps = 0, k <= 64) with a p0 w and a p1 u go
+    Points at time-step ends (eps = 0, k <= 512) with a p0 w and a p1 u go
     through the fused per-element path of ``represent_grid`` (one history per
     distinct spatial point); the others through the two potential launches."""
     import torch
@@ -466,7 +469,7 @@ def represent(w, u, points, mesh, timegrid, params: KernelParams, config: Quadra
     fused_ok = (n and w_np.shape[1] == mesh.n_triangles and u_np.shape[1] == mesh.n_vertices
                 and not os.environ.get("HB_REP_SEPARATE"))
     # (points past the final time, k > n_steps, take the general path below)
-    grid = ((eps == 0.0) & (k <= 64) & (k <= timegrid.n_steps)) if fused_ok else np.zeros(n, bool)
+    grid = ((eps == 0.0) & (k <= _ELEM_MAX_STEPS) & (k <= timegrid.n_steps)) if fused_ok else np.zeros(n, bool)
     done = grid.copy()
     vals = np.empty(n)
     if grid.any():
@@ -556,7 +559,11 @@ def represent_grid(w, u, xs, mesh, timegrid, params: KernelParams, config: Quadr
         raise ValueError("time_steps must lie in [0, n_steps]")
     if nt > 1 and np.any(np.diff(ks) < 0):
         raise ValueError("time_steps must be ascending")
-    if nt and int(ks.max()) <= 64 and not os.environ.get("HB_REP_SEPARATE"):
+    elem_ok = (np.asarray(w).shape[1] == mesh.n_triangles and np.asarray(u).shape[1] == mesh.n_vertices
+               and not os.environ.get("HB_REP_NODES"))
+    # histories up to 64 steps: the fused kernels; up to 512 with p0 / p1 densities: the
+    # per-element kernel, one launch per 64 output steps (csrc/hb_field.cu k_represent_elem LONG)
+    if nt and int(ks.max()) <= (_ELEM_MAX_STEPS if elem_ok else 64) and not os.environ.get("HB_REP_SEPARATE"):
         res = _represent_grid_fused(np.asarray(w), np.asarray(u), xs, ks, mesh, timegrid, params, config)
         return res if return_device else res.cpu().numpy()
     groups = _grid_groups(xs, ks)

@@ -183,3 +183,53 @@ def test_long_history_potentials_vs_oracle(oracle, E_t):
     rep, _ = hb.represent(w, uu, pts, m, tg, p)
     for got, ref in ((sl, refs[0]), (dl, refs[1]), (rep, refs[0] - refs[1])):
         assert np.allclose(got, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("E_t", [70, 128, 200, 300])
+def test_long_history_grid_per_element_kernel(oracle, E_t, monkeypatch):
+    """represent_grid with histories longer than 64 steps runs the per-element
+    kernel once per block of 64 output steps (k_represent_elem LONG: gap
+    windows below the block as full Toeplitz tiles).  Checked against the
+    general k_potential path on every (point, step) and against the oracle
+    (reference _field_numba._eval_potential, any k) on sampled steps; cluster
+    splits give the same values; a step subset with k = 0 returns exact zeros."""
+    from paper_2102_09811_b200.field import _interp_density_np
+    from paper_2102_09811_b200.quadrature import rule_tables
+
+    m = hb.unit_cube_mesh(1)
+    tg = hb.TimeGrid(1.0, E_t)
+    p = hb.KernelParams(0.8, tg.step, length_scale=m.diameter)
+    rng = np.random.default_rng(1000 + E_t)
+    w = rng.standard_normal((E_t, m.n_triangles))
+    uu = rng.standard_normal((E_t, m.n_vertices))
+    X = rng.uniform(0.05, 0.95, (40, 3))
+    got = hb.represent_grid(w, uu, X, m, tg, p)
+    assert got.shape == (40, E_t) and np.all(np.isfinite(got))
+    # the oracle on sampled steps (block ends, block starts, the last step)
+    ks = np.unique(np.array([1, 63, 64, 65, 66, min(E_t, 127), min(E_t, 128), min(E_t, 129), E_t - 1, E_t]))
+    Xs = X[::7]
+    XX = np.repeat(Xs, len(ks), axis=0)
+    kk = np.tile(ks, len(Xs))
+    hats, qw, qpts = rule_tables(m, 6)
+    zero = np.zeros(len(kk))
+    cur = np.zeros(len(kk), dtype=bool)
+    ref = (oracle.potential(0, XX, kk, zero, cur, _interp_density_np(w, m, hats), qpts, qw, m.areas, m.normals,
+                            tg.step, p.alpha, p.delta_eps, p.rho_eps)
+           - oracle.potential(1, XX, kk, zero, cur, _interp_density_np(uu, m, hats), qpts, qw, m.areas, m.normals,
+                              tg.step, p.alpha, p.delta_eps, p.rho_eps)).reshape(len(Xs), len(ks))
+    sub = got[::7][:, ks - 1]
+    assert np.allclose(sub, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max())
+    # a step subset including k = 0, two cluster splits
+    steps = np.array([0, 1, 64, 65, E_t])
+    outs = []
+    for split in ("1", "3"):
+        monkeypatch.setenv("HB_POT_SPLIT", split)
+        part = hb.represent_grid(w, uu, X, m, tg, p, time_steps=steps)
+        assert np.all(part[:, 0] == 0.0)
+        assert np.allclose(part[:, 1:], got[:, steps[1:] - 1], rtol=1e-13, atol=1e-14 * np.abs(got).max())
+        outs.append(part)
+    monkeypatch.delenv("HB_POT_SPLIT")
+    # the general path (two potential launches) on every (point, step)
+    monkeypatch.setenv("HB_REP_SEPARATE", "1")
+    gen = hb.represent_grid(w, uu, X, m, tg, p)
+    assert np.allclose(got, gen, rtol=1e-12, atol=1e-13 * np.abs(gen).max())
