@@ -280,12 +280,25 @@ __device__ __forceinline__ void chunk_moments(const double *geo, double *Pw, dou
             pw = __dmul_rn(pw, rt2);
         }
         __syncwarp();
-#pragma unroll 2
-        for (int p = 16 * h; p < pend; ++p) {
-            const double P = Pw[p * kPwStride + k16];
-            const double *w = geo + p * PAY + WOFF;
+        if (NW <= 3 && nloc == 32) {
+            // full chunk (every touching-pair chunk): straight-line, the 16 points'
+            // loads at immediate offsets from two bases -- same additions, same order
+            const double *col = Pw + 16 * h * kPwStride + k16;
+            const double *wb = geo + 16 * h * PAY + WOFF;
 #pragma unroll
-            for (int i = 0; i < NW; ++i) mom[c][i] = fma(P, w[i], mom[c][i]);
+            for (int q = 0; q < 16; ++q) {
+                const double P = col[q * kPwStride];
+#pragma unroll
+                for (int i = 0; i < NW; ++i) mom[c][i] = fma(P, wb[q * PAY + i], mom[c][i]);
+            }
+        } else {
+#pragma unroll 2
+            for (int p = 16 * h; p < pend; ++p) {
+                const double P = Pw[p * kPwStride + k16];
+                const double *w = geo + p * PAY + WOFF;
+#pragma unroll
+                for (int i = 0; i < NW; ++i) mom[c][i] = fma(P, w[i], mom[c][i]);
+            }
         }
         __syncwarp();
     }
