@@ -2281,6 +2281,7 @@ struct FinArgs {
     const double *normals;
     int skip_zero_dot;    // D2: pairs with n_e . n_f == 0 were not staged
     int star_max;
+    int node_grid;        // p1 x p1 finalize: grid x = node (rows cover most of the mesh) instead of (chunk element, local node)
     const int64_t *tile_eptr, *tile_elem;   // curl tile plan (32-node tiles)
     const int32_t *star_pos;
     int nrs;                                // row-sharded destination: shards, bounds, base pointers
@@ -2404,16 +2405,25 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
     extern __shared__ __align__(16) double fsm[];
     // CTA x = (element of the chunk, local node): node m is handled by the
     // CTA of the first chunk element in its (element-sorted) star only
-    const int64_t n0 = (int64_t)blockIdx.y * 32, eo = F.e0 + blockIdx.x / 3;
-    const int64_t m = __ldg(F.tri_nodes + 3 * eo + blockIdx.x % 3);
+    const int64_t n0 = (int64_t)blockIdx.y * 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t sm0 = __ldg(F.star_indptr + m), sm1 = __ldg(F.star_indptr + m + 1);
-    int64_t first = -1;
-    for (int64_t a = sm0; a < sm1 && first < 0; ++a) {
-        const int64_t e = __ldg(F.star_elem + a);
-        if (e >= F.e0) first = e;
+    int64_t m;
+    if (F.node_grid) {
+        // one CTA column per node (row ranges covering most of the mesh: fewer CTAs
+        // than three candidates per chunk element, none of them empty-handed)
+        m = blockIdx.x;
+    } else {
+        const int64_t eo = F.e0 + blockIdx.x / 3;
+        m = __ldg(F.tri_nodes + 3 * eo + blockIdx.x % 3);
+        const int64_t a0 = __ldg(F.star_indptr + m), a1 = __ldg(F.star_indptr + m + 1);
+        int64_t first = -1;
+        for (int64_t a = a0; a < a1 && first < 0; ++a) {
+            const int64_t e = __ldg(F.star_elem + a);
+            if (e >= F.e0) first = e;
+        }
+        if (first != eo) return;
     }
-    if (first != eo) return;
+    const int64_t sm0 = __ldg(F.star_indptr + m), sm1 = __ldg(F.star_indptr + m + 1);
     const int smax = F.star_max;
     int64_t *sQ = (int64_t *)fsm;                          // [star_max] Q offset of (e - e0, 3i)
     int64_t *sE = sQ + smax;                               // [star_max] e
@@ -2445,6 +2455,7 @@ __global__ void __launch_bounds__(256) k_fin_p1p1_accum(const FinArgs F)
     }
     __syncthreads();
     const int na = na_s;
+    if (na == 0) return;   // (node grid: no element of the node's star in this row range)
     const int64_t tB0 = F.tile_eptr[blockIdx.y], tB = F.tile_eptr[blockIdx.y + 1] - tB0;
     // staged-pair bitmasks: warp w owns word w (tile positions 32w..32w+31);
     // okm: D2 staged (f >= e, n_e . n_f != 0); FUSE: okv, every f >= e (V staged)
@@ -3041,9 +3052,12 @@ static int finalize_window(const hb_mesh_desc *m, const hb_assembly_desc *a, con
         dim3 g((unsigned)rows, (unsigned)cdiv(m->N_x, 32));
         k_fin_p0p1<<<g, 256, 0, st>>>(F);
     } else {
-        dim3 g((unsigned)(3 * rows), (unsigned)cdiv(m->N_x, 32));
-        if (F.Qv) k_fin_p1p1_accum<true><<<g, 256, fin_p1p1_smem(m, true), st>>>(F);
-        else k_fin_p1p1_accum<false><<<g, 256, fin_p1p1_smem(m, false), st>>>(F);
+        FinArgs G = F;
+        static const int ng_env = getenv("HB_FIN_NODE_GRID") ? atoi(getenv("HB_FIN_NODE_GRID")) : -1;
+        G.node_grid = ng_env >= 0 ? ng_env : (3 * rows >= m->N_x ? 1 : 0);
+        dim3 g((unsigned)(G.node_grid ? m->N_x : 3 * rows), (unsigned)cdiv(m->N_x, 32));
+        if (G.Qv) k_fin_p1p1_accum<true><<<g, 256, fin_p1p1_smem(m, true), st>>>(G);
+        else k_fin_p1p1_accum<false><<<g, 256, fin_p1p1_smem(m, false), st>>>(G);
     }
     int rc = cuda_check(cudaGetLastError(), "finalize");
     if (rc) return rc;

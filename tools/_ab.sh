@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT
-for db in 0 1; do echo "== c2 HB_CURL_DB=$db"; HB_CURL_DB=$db python tools/time_ops.py 2>&1 | tail -1; HB_CURL_DB=$db LVL=4 ET=64 python tools/time_ops.py 2>&1 | tail -1; done
-for db in 0 1; do echo "== c5 chunk HB_CURL_DB=$db"; HB_CURL_DB=$db python tools/prof_c5_d.py 2>&1 | tail -1; done
-python -m pytest tests/test_assembly_gpu.py -x -q -k "curl or hypersingular or D_ or c1 or c2" 2>&1 | tail -3
+for ng in 0 1; do echo "== HB_FIN_NODE_GRID=$ng"; HB_FIN_NODE_GRID=$ng python tools/time_ops.py 2>&1 | head -1; HB_FIN_NODE_GRID=$ng LVL=4 ET=64 python tools/time_ops.py 2>&1 | head -1; HB_FIN_NODE_GRID=$ng python tools/hash_ops.py > gpurun_out/hash_ng$ng.txt 2>&1; done
+diff gpurun_out/hash_ng0.txt gpurun_out/hash_ng1.txt && echo "hashes identical"
