@@ -811,7 +811,11 @@ def run_native_large(args, rank, world, local_rank):
     d0, d1 = Dm.block_range(rank, world, Et)
     dev = torch.device("cuda", local_rank)
     tabs = hbdev.device_tables(mesh, q, dev)
-    budget = float(os.environ.get("HB_BENCH_CHUNK_BYTES", 40e9))
+    # V chunk buffer: 40 GB where D shares the pool (config 5: 33-block chunks; larger ones
+    # squeeze the staging workspace: 57 / 82 blocks measured 4.74 / 5.99 s against 4.55 s),
+    # 110 GB for V and K alone (config 3: whole 32-block windows, 5.03 s against 6.71 s
+    # with 11-block chunks that re-evaluate the window's gaps)
+    budget = float(os.environ.get("HB_BENCH_CHUNK_BYTES", 40e9 if "D" in c["ops"] else 110e9))
     ch = max(1, int(budget // (E * E * 8)))
 
     def rank_chunks(max_blocks):
