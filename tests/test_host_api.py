@@ -136,6 +136,21 @@ def test_row_slabs_cover_rows_with_balanced_work():
     assert max(work) / min(work) < 1.05
 
 
+def test_row_slabs_from_work_fractions():
+    """A sequence of work fractions instead of a count: contiguous cover of the
+    rows, each slab's share of the upper-triangle pair work as requested."""
+    from paper_2102_09811_b200.assembly import _row_slabs
+
+    fr = (0.1, 0.3, 0.6)
+    sl = _row_slabs(768, True, fr)
+    assert sl[0][0] == 0 and sl[-1][1] == 768 and all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
+    work = np.array([sum(768 - e for e in range(a, b)) for a, b in sl], dtype=float)
+    assert np.allclose(work / work.sum(), fr, atol=0.01)
+    assert _row_slabs(100, False, (1, 1)) == [(0, 50), (50, 100)]
+    with pytest.raises(ValueError):
+        _row_slabs(100, True, (0.5, 0.0))
+
+
 def test_blocks_host_edits_are_tracked():
     """The reference edits operators through .blocks (assembly.py:328-333:
     out = D2.blocks; out[d] += ...): item assignment, in-place ufuncs and
