@@ -61,6 +61,17 @@
 
 namespace hb {
 
+// one factor-free kernel value on the lane-local uniform pieces (hb_special.cuh eval_ulocal)
+template <int KIND>
+__device__ __forceinline__ double eval_one(double x, double ix, const double *__restrict__ utab)
+{
+    double r[1];
+    const double xs[1] = {x};
+    special::eval_ulocal<KIND, 1>(xs, [&](int) { return ix; }, r, utab);
+    return r[0];
+}
+
+
 struct PairArgs {
     hb_mesh_desc m;
     double step, alpha, d_eps, r_eps;
@@ -445,8 +456,8 @@ __device__ __forceinline__ void eval_points(const PairArgs &A, const Slots<OP, N
 #pragma unroll
                 for (int g = 0; g < G; ++g) xs[g] = __dmul_rn(rho[g], T.cx[j]);
                 const double icj = T.ic[j];
-                special::eval_nf<OP + 4, G>(
-                    xs, [&](int g) { return __dmul_rn(OP == 0 ? b[g] : a[g], icj); }, fs, tab, kFull);
+                special::eval_ulocal<OP + 4, G>(
+                    xs, [&](int g) { return __dmul_rn(OP == 0 ? b[g] : a[g], icj); }, fs, tab);
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const double v = ok[g] ? fs[g] : 0.0;
@@ -461,13 +472,12 @@ __device__ __forceinline__ void eval_points(const PairArgs &A, const Slots<OP, N
             const double rho = p[0], s1 = p[1];
             const double s2 = (OP == 2) ? 0.0 : p[2];
             const bool sm = rho <= A.r_eps;
-            const unsigned mask = __activemask();
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
                 if (j >= nje) break;
                 const double x = __dmul_rn(rho, T.cx[j]);
                 const double ix = __dmul_rn(OP == 0 ? s2 : s1, T.ic[j]);
-                const double f = special::eval<OP + 4>(x, ix, tab, mask);
+                const double f = eval_one<OP + 4>(x, ix, tab);
                 // rho <= r_eps limits, divided by the per-gap factor applied at the end
                 double val;
                 if (OP == 0) val = sm ? 2.0 * T.kk[j] / T.sc[j] : f;
@@ -904,7 +914,7 @@ __device__ __noinline__ void dual_points(const PairArgs &A, const Win &W, const 
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) xs[gg] = __dmul_rn(rho[gg], T.cx[j]);
                     const double icj = T.ic[j];
-                    special::eval_nf<5, G>(xs, [&](int gg) { return __dmul_rn(a[gg], icj); }, fs, tab, kFull);
+                    special::eval_ulocal<5, G>(xs, [&](int gg) { return __dmul_rn(a[gg], icj); }, fs, tab);
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
@@ -920,13 +930,12 @@ __device__ __noinline__ void dual_points(const PairArgs &A, const Win &W, const 
                 const double *p = geo + k * PAY;
                 const double rho = p[0], s1 = p[1];
                 const bool sm = rho <= A.r_eps;
-                const unsigned mask = __activemask();
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
                     if (j >= nje) break;
                     const double x = __dmul_rn(rho, T.cx[j]);
                     const double ix = __dmul_rn(s1, T.ic[j]);
-                    const double f = special::eval<5>(x, ix, tab, mask);
+                    const double f = eval_one<5>(x, ix, tab);
                     const double val = sm ? 0.0 : f;
 #pragma unroll
                     for (int i = 0; i < 3; ++i) {
@@ -1472,7 +1481,7 @@ __device__ __forceinline__ void far_pp_k(const PairArgs &A, const FarGeom &G, co
             const double rho = sqrt(r2);
             const double iq = 1.0 / rho;
             double xs[1] = {__dmul_rn(rho, cx)}, fs[1];
-            special::eval_nf<5, 1>(xs, [&](int) { return __dmul_rn(iq, ic); }, fs, tab, kFull);
+            special::eval_ulocal<5, 1>(xs, [&](int) { return __dmul_rn(iq, ic); }, fs, tab);
             if (pp) {
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
@@ -1621,7 +1630,7 @@ __device__ __forceinline__ void far_pp_k2(const PairArgs &A, const double *Pk, i
         const double rho = tr.y, iq = ii.x;
         const double W[6] = {w01.x, w01.y, w23.x, w23.y, w45.x, w45.y};
         double xs[1] = {__dmul_rn(rho, cx)}, fs[1];
-        special::eval_nf<5, 1>(xs, [&](int) { return __dmul_rn(iq, ic); }, fs, tab, kFull);
+        special::eval_ulocal<5, 1>(xs, [&](int) { return __dmul_rn(iq, ic); }, fs, tab);
         if (pp) {
 #pragma unroll
             for (int i = 0; i < 6; ++i) acc[i] = fma(fs[0], W[i], acc[i]);
@@ -1668,7 +1677,7 @@ __device__ __forceinline__ void far_pp_v(const PairArgs &A, const FarGeom &G, in
             double xs[4], fs[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) xs[j] = __dmul_rn(rho, cx[j]);
-            special::eval_nf<4, 4>(xs, [&](int j) { return __dmul_rn(iq, ic[j]); }, fs, tab, kFull);
+            special::eval_ulocal<4, 4>(xs, [&](int j) { return __dmul_rn(iq, ic[j]); }, fs, tab);
             if (pp) {
                 // compensated sum (TwoProd by fma + TwoSum): the point sum of a gap
                 // carries no rounding of its own, so the time second difference
@@ -2226,17 +2235,17 @@ __global__ void __launch_bounds__(HB_PAIR_WARPS * 32, (TP1 && SP1) ? HB_P1P1_MIN
     extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *tab = smem;
-    special::load_table<OP + 4>(tab);   // factor-free kinds (hb_special.cuh)
-    double *rule = smem + special::kTabDoubles;
+    special::load_utable<OP + 4>(tab);   // factor-free kinds, uniform pieces (hb_special.cuh)
+    double *rule = smem + special::kUTabDoubles;
     if (A.m.n_reg <= kFarMaxRule) {
         for (int i = threadIdx.x; i < 4 * (int)A.m.n_reg; i += blockDim.x)
             rule[i] = i < A.m.n_reg ? __ldg(A.m.reg_w_dev + i) : __ldg(A.m.reg_hats_dev + i - A.m.n_reg);
     }
     __syncthreads();
     constexpr int kPerWarp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
-    static_assert(special::kTabDoubles % 2 == 0 && kPerWarp % 2 == 0 && Layout<OP, NIJ>::PAY % 2 == 0 &&
+    static_assert(special::kUTabDoubles % 2 == 0 && kPerWarp % 2 == 0 && Layout<OP, NIJ>::PAY % 2 == 0 &&
                       kDualPay % 2 == 0, "payload slots must stay 16-byte aligned (LDS.128)");
-    double *geo = smem + special::kTabDoubles + kRuleDoubles + warp * kPerWarp;
+    double *geo = smem + special::kUTabDoubles + kRuleDoubles + warp * kPerWarp;
     WarpMem W;
     W.geo = geo;
     W.Ls = geo + 32 * (DUAL ? kDualPay : Layout<OP, NIJ>::PAY);
@@ -2793,7 +2802,7 @@ static int launch_class(const PairArgs &A, cudaStream_t st)
     constexpr int NIJ = (TP1 ? 3 : 1) * (SP1 ? 3 : 1);
     constexpr bool SYM = (OP != 1);
     constexpr int per_warp = DUAL ? dual_smem_doubles_per_warp<NJ>() : smem_doubles_per_warp<OP, NIJ, NJ>();
-    const size_t sm = ((size_t)HB_PAIR_WARPS * per_warp + special::kTabDoubles + kRuleDoubles) * sizeof(double);
+    const size_t sm = ((size_t)HB_PAIR_WARPS * per_warp + special::kUTabDoubles + kRuleDoubles) * sizeof(double);
     auto kp = k_pairs<OP, TP1, SP1, NJ, SYM, DUAL, CLS>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int dev = 0, nsm = 0, per_sm = 0;

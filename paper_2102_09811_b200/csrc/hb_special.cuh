@@ -394,6 +394,51 @@ __device__ __forceinline__ void eval_unf(const double (&x)[NJ], const IXF &ixf, 
     }
 }
 
+// Lane-local form of the uniform pieces: every value below XL from its piece,
+// whatever the other lanes hold (no votes at all), the asymptote above.  For
+// callers whose x is never small -- the per-point gaps of the moment form
+// (t = x^2 > kTM) -- where the all-series shortcut of eval_unf cannot fire;
+// a value depends on its own x only, so it is independent of the warp's
+// composition (d-range, row chunk, rank) by construction.
+template <int KIND, int NJ, class IXF>
+__device__ __forceinline__ void eval_ulocal(const double (&x)[NJ], const IXF &ixf, double (&r)[NJ],
+                                            const double *__restrict__ utab)
+{
+    const double2 *t2 = reinterpret_cast<const double2 *>(utab);
+    constexpr int MT = kUDeg / 2;
+    int p[NJ];
+    double u[NJ];
+    bool huge[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const double y = __dmul_rn(x[j], kUInvH);   // exact (power of two)
+        const int pi = __double2int_rz(y);          // x >= 0: the floor; INT_MAX for inf
+        huge[j] = pi >= kUPieces;
+        p[j] = min(pi, kUPieces - 1);
+        u[j] = fma(2.0, y - (double)p[j], -1.0);    // exact within the piece
+    }
+    double2 w[MT + 1][NJ];
+#pragma unroll
+    for (int m = MT; m >= 0; --m)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) w[m][j] = t2[m * kUPieces + p[j]];
+    double q[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) q[j] = fma(w[MT][j].y, u[j], w[MT][j].x);
+#pragma unroll
+    for (int m = MT - 1; m >= 0; --m) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], u[j], w[m][j].y);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], u[j], w[m][j].x);
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        r[j] = KIND == 4 ? fma(__dmul_rn(x[j], x[j]), q[j], kTwoInvSqrtPi) : q[j];
+        if (huge[j]) r[j] = asymptote<KIND>(x[j], ixf(j));
+    }
+}
+
 template <int KIND>
 __device__ __forceinline__ double eval_u(double x, double ix, const double *__restrict__ utab, unsigned mask)
 {
