@@ -721,6 +721,47 @@ __device__ __forceinline__ void eval_ex_Ex3(double x, double ix, const double *_
     }
 }
 
+// The same two values from the uniform pieces of [0, XL) (kinds 6 and 7: width
+// 1/16, degree 7, one shared piece index; hb_special.cuh): a warp whose lanes
+// -- the gaps m of one (point, node) -- all lie in the series region takes the
+// constant-bank series, any other warp evaluates every lane on its piece with
+// no series / middle select or merged chain (two chains of 7 steps instead of
+// two merged ones of 11).  Which lanes share a warp is fixed by (point, node,
+// lane pass), so a value does not depend on the launch split.
+__device__ __forceinline__ void eval_ex_Ex3_u(double x, double ix, const double *__restrict__ utabS,
+                                              const double *__restrict__ utabD, double &rs, double &rd)
+{
+    const double t = __dmul_rn(x, x);
+    if (!__any_sync(kFull, !(x < special::kX0))) {
+        rs = special::series<6>(x, t, 0.0);
+        rd = special::series<7>(x, t, 0.0);
+        return;
+    }
+    const double2 *s2 = reinterpret_cast<const double2 *>(utabS), *d2 = reinterpret_cast<const double2 *>(utabD);
+    constexpr int MT = special::kUDeg / 2, NP = special::kUPieces;
+    const double y = __dmul_rn(x, special::kUInvH);   // exact (power of two)
+    const int pi = __double2int_rz(y);
+    const bool huge = pi >= NP;
+    const int p = min(pi, NP - 1);
+    const double u = fma(2.0, y - (double)p, -1.0);   // exact within the piece
+    double2 ws[MT + 1], wd[MT + 1];
+#pragma unroll
+    for (int m = MT; m >= 0; --m) {
+        ws[m] = s2[m * NP + p];
+        wd[m] = d2[m * NP + p];
+    }
+    double qs = fma(ws[MT].y, u, ws[MT].x), qd = fma(wd[MT].y, u, wd[MT].x);
+#pragma unroll
+    for (int m = MT - 1; m >= 0; --m) {
+        qs = fma(qs, u, ws[m].y);
+        qd = fma(qd, u, wd[m].y);
+        qs = fma(qs, u, ws[m].x);
+        qd = fma(qd, u, wd[m].x);
+    }
+    rs = huge ? ix : qs;
+    rd = huge ? __dmul_rn(__dmul_rn(ix, ix), ix) : qd;
+}
+
 #ifndef HB_REP_FF
 #define HB_REP_FF 1
 #endif
@@ -1119,6 +1160,8 @@ struct RepElemArgs {
 };
 
 constexpr int kFTE = 256;   // k_represent_elem threads (8 warps, 32 points)
+// shared-memory doubles per special-function table of k_represent_elem (uniform pieces with HB_REP_FF)
+constexpr int kRepTab = special::kUTabDoubles > special::kTabDoubles ? special::kUTabDoubles : special::kTabDoubles;
 
 template <int KM>
 struct RepElemLayout {
@@ -1127,7 +1170,7 @@ struct RepElemLayout {
     // kt: time steps held per density vector (KM, or KM (kblock + 1) for the LONG kernels)
     static size_t doubles(int64_t nq, int64_t kt = KM)
     {
-        return 2 * (size_t)special::kTabDoubles + 4 * kFP * GS + (HB_REP_FF ? 5 : 3) * (size_t)nq * kFP +
+        return 2 * (size_t)kRepTab + 4 * kFP * GS + (HB_REP_FF ? 5 : 3) * (size_t)nq * kFP +
                2 * 4 * (size_t)(ZP + kt + 1) + 2 * 2 * 4 * (size_t)(kt + 1);
     }
 };
@@ -1159,8 +1202,8 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
     const int BR = ZP + KT + 1, AS = KT + 1;
     extern __shared__ __align__(16) double fsm[];
     const int nq = (int)P.nq;
-    double *tabS = fsm, *tabD = tabS + special::kTabDoubles;
-    double *H = tabD + special::kTabDoubles;    // [4][kFP][GS]: W G (single), W hat_i G (double, i = 0..2)
+    double *tabS = fsm, *tabD = tabS + kRepTab;
+    double *H = tabD + kRepTab;                 // [4][kFP][GS]: W G (single), W hat_i G (double, i = 0..2)
     double *Rn = H + 4 * kFP * GS;              // [nq][kFP] rho
     double *L0s = Rn + nq * kFP, *L0d = L0s + nq * kFP;   // [nq][kFP] G at m = 0
     double *Tv = L0d + nq * kFP;                // [2 buf][4][BR]: density differences, zeros before
@@ -1169,8 +1212,8 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
     double *Ri = Dv + 2 * 4 * AS;               // HB_REP_FF: [nq][kFP] 1/rho
     double *Rq = Ri + nq * kFP;                 // HB_REP_FF: [nq][kFP] rn / (4 pi) (0 for rho <= r_eps)
 #if HB_REP_FF
-    special::load_table<6>(tabS);
-    special::load_table<7>(tabD);
+    special::load_utable<6>(tabS);
+    special::load_utable<7>(tabD);
 #else
     special::load_table<2>(tabS);
     special::load_table<3>(tabD);
@@ -1275,7 +1318,7 @@ __global__ void __launch_bounds__(kFTE, 2) k_represent_elem(const RepElemArgs P,
 #pragma unroll
                 for (int s = 0; s < kS; ++s) {
                     double fs, fd;
-                    eval_ex_Ex3(__dmul_rn(rho, cm[s]), __dmul_rn(ri, icm[s]), tabS, tabD, fs, fd);
+                    eval_ex_Ex3_u(__dmul_rn(rho, cm[s]), __dmul_rn(ri, icm[s]), tabS, tabD, fs, fd);
                     // (scaled by cm / (4 pi a) and cm^3 after the node sum; rho <= r_eps:
                     // erf(x)/x -> 2/sqrt(pi), the reference's limit, and rq = 0)
                     const double vs = gzero[s] ? l0s : fs;

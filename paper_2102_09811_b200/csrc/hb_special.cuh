@@ -331,8 +331,8 @@ static_assert((kUDeg & 1) == 1 && kUTabDoubles % 2 == 0, "uniform pieces: coeffi
 template <int KIND>
 __device__ __forceinline__ void load_utable(double *utab)
 {
-    static_assert(KIND >= 4 && KIND <= 6, "uniform pieces exist for the factor-free kinds 4-6");
-    const double *src = KIND == 4 ? kU4 : KIND == 5 ? kU5 : kU6;
+    static_assert(KIND >= 4 && KIND <= 7, "uniform pieces exist for the factor-free kinds 4-7");
+    const double *src = KIND == 4 ? kU4 : KIND == 5 ? kU5 : KIND == 6 ? kU6 : kU7;
     for (int i = threadIdx.x; i < kUTabDoubles; i += blockDim.x) {
         const int slot = i >> 1, m = slot / kUPieces, p = slot - m * kUPieces;
         utab[i] = src[(2 * m + (i & 1)) * kUPieces + p];

@@ -201,7 +201,7 @@ def main():
         for k in range(DEG_M[fname] + 1):
             out.append("    " + ", ".join(hexd(tab[pc][k]) for pc in range(MID_PIECES)) + ",")
         out.append("};")
-    # ---- uniform pieces for the pair kernels' factor-free kinds (4 xH, 5 F/x, 6 erf/x) ----
+    # ---- uniform pieces for the factor-free kinds (pair kernels: 4 xH, 5 F/x, 6 erf/x; potentials: 6, 7 E/x^3) ----
     # [0, XL) in pieces of width 1/16, degree 7 in u = 2 (16 x - p) - 1: ONE
     # polynomial form for every lane below XL that is not in an all-series
     # warp (no series / middle select), 4 LDS.128 + 7 FMA per value
@@ -211,7 +211,7 @@ def main():
     out.append(f"constexpr int kUPieces = {U_PIECES};   // uniform pieces of [0, XL), width 1/{U_INV_H}")
     out.append(f"constexpr int kUDeg = {U_DEG};")
     out.append(f"constexpr double kUInvH = {hexd(mp.mpf(U_INV_H))};")
-    for kind, (fname, f) in ((4, ("xH", F_xH)), (5, ("Fx", F_Fx)), (6, ("ex", F_ex))):
+    for kind, (fname, f) in ((4, ("xH", F_xH)), (5, ("Fx", F_Fx)), (6, ("ex", F_ex)), (7, ("Ex3", F_Ex3))):
         worst, tab = 0, []
         for pc in range(U_PIECES):
             a = mp.mpf(pc) / U_INV_H
