@@ -1,5 +1,9 @@
 cd $GRAFT_REPO_ROOT
-NPTS=20000 python tools/time_represent.py 2>&1 | tail -1
-NPTS=20000 HB_LIB_PATH=variants_tmp/old/libheatbem_b200.so python tools/time_represent.py 2>&1 | tail -1
-python tools/time_represent_long.py 2>&1 | tail -1
-python -m pytest tests/test_field_gpu.py tests/test_study_gpu.py -x -q 2>&1 | tail -3
+for env in "X=1" "HB_MOMENT_FROM=0" "HB_MOMENTS=1"; do
+  echo "== c3 $env"; env $env python bench.py --config 3 --no-cpu-baseline --steps 2 --warmup 1 2>/dev/null | python -c "
+import json,sys
+r=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(r['ms_per_step'])"
+  echo "== c5 $env"; env $env python bench.py --config 5 --no-cpu-baseline --steps 2 --warmup 1 2>/dev/null | python -c "
+import json,sys
+r=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(r['ms_per_step'])"
+done

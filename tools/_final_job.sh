@@ -6,6 +6,9 @@ ncu --set full --clock-control none --import-source on --kernel-name-base demang
 python tools/ncu_roofline.py /tmp/pairs_all.ncu-rep > gpurun_out/final_pairs_roofline.txt 2>&1
 python tools/ncu_summary.py /tmp/pairs_all.ncu-rep > gpurun_out/final_pairs_summary.txt 2>&1
 python tools/ncu_mix.py /tmp/pairs_all.ncu-rep > gpurun_out/final_pairs_mix.txt 2>&1
-cp /tmp/pairs_all.ncu-rep gpurun_out/
+ncu --set full --clock-control none --kernel-name-base demangled -k regex:"k_fin|k_curl|k_symm" -c 6 -o /tmp/fin_all -f python tools/prof_c2.py > gpurun_out/ncu_fin.log 2>&1
+python tools/ncu_roofline.py /tmp/fin_all.ncu-rep > gpurun_out/final_fin_roofline.txt 2>&1
+python tools/parity_report.py gpurun_out/final_parity.json > gpurun_out/final_parity.txt 2>&1
 python tools/rank_work2.py > gpurun_out/final_rank_c2.json 2> gpurun_out/final_rank_c2.err
 python bench.py --config 5 --no-cpu-baseline > gpurun_out/final_bench_c5.json 2> gpurun_out/final_bench_c5.err
+python bench.py --config 3 --no-cpu-baseline --steps 5 > gpurun_out/final_bench_c3.json 2> gpurun_out/final_bench_c3.err
