@@ -2742,11 +2742,12 @@ static int64_t moment_from(const hb_assembly_desc *a)
 {
     static const int env = getenv("HB_MOMENTS") ? (atoi(getenv("HB_MOMENTS")) != 0) : -1;
     static const int64_t sw = getenv("HB_MOMENT_FROM") ? atoll(getenv("HB_MOMENT_FROM")) : 32;
+    static const int64_t ksw = getenv("HB_K_MOMENT_FROM") ? atoll(getenv("HB_K_MOMENT_FROM")) : 62;
     const int64_t never = INT64_MAX / 4;
     if (env == 1) return 0;
     if (env == 0) return never;
     if (a->op == HB_OP_DOUBLE_LAYER)   // K: the moment form pays only far out (config 3, E_t 64: it does not)
-        return a->E_t >= 128 ? std::max<int64_t>(sw, 62) : never;
+        return a->E_t >= 128 ? std::max<int64_t>(sw, ksw) : never;
     if (a->E_t >= 64) return sw;
     return a->op == HB_OP_SINGLE_LAYER ? 0 : never;
 }
