@@ -952,7 +952,11 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         # HB_BENCH_EMULATE=1: every rank on cuda:0 over gloo -- a control-flow
         # check of the N > 1 path on a one-GPU box, never a measurement
-        dist.init_process_group("gloo" if os.environ.get("HB_BENCH_EMULATE") else "nccl")
+        import datetime
+
+        # (a rank that dies must not leave the others in a collective for NCCL's default 10 minutes)
+        dist.init_process_group("gloo" if os.environ.get("HB_BENCH_EMULATE") else "nccl",
+                                timeout=datetime.timedelta(seconds=int(os.environ.get("HB_BENCH_TIMEOUT_S", "300"))))
         if os.environ.get("HB_BENCH_EMULATE"):
             local_rank = 0
     try:
