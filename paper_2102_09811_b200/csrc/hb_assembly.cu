@@ -315,6 +315,65 @@ __device__ __forceinline__ void chunk_moments(const double *geo, double *Pw, dou
     }
 }
 
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b);
+
+// One weight per point (p0 x p0): the 32 moments of a chunk as ONE rank-32
+// product on the FP64 tensor cores.  With k = 8 n + g,
+//   M_k = sum_p r_p^g (W_p r_p^(8 n))  =  (A B)[g][n],
+// A[g][p] = r_p^g (g < 8), B[p][n] = W_p r_p^(8 n) (n < 4; columns 4-7 zero):
+// lane p forms its point's 8 + 4 values with 11 multiplications (instead of 32
+// powers and 32 stores), eight m8n8k4 DMMAs (4 points each) accumulate into the
+// C fragment cf (lane (g, t): columns 2t, 2t + 1) across the pair's chunks.
+// Scratch Pw: A rows at stride 36 (conflict-free stores, 2-wavefront fragment
+// loads), then the four B rows.  Padding points (all-zero payload, r = 0)
+// contribute exact zeros.
+constexpr int kMmStride = 36;
+static_assert(12 * kMmStride <= kPwDoubles, "DMMA moment scratch must fit the per-warp moment scratch");
+
+template <int PAY, int WOFF>
+__device__ __forceinline__ void chunk_moments_mma(const double *geo, double *Pw, double r, double (&cf)[2], int lane)
+{
+    const double W = geo[lane * PAY + WOFF];
+    const double r2 = __dmul_rn(r, r), r3 = __dmul_rn(r2, r), r4 = __dmul_rn(r2, r2);
+    const double r5 = __dmul_rn(r4, r), r6 = __dmul_rn(r4, r2), r7 = __dmul_rn(r4, r3), r8 = __dmul_rn(r4, r4);
+    const double w8 = __dmul_rn(W, r8), r16 = __dmul_rn(r8, r8), w16 = __dmul_rn(W, r16), w24 = __dmul_rn(w16, r8);
+    double *Ar = Pw + lane, *Br = Pw + 8 * kMmStride + lane;
+    Ar[0] = 1.0;
+    Ar[kMmStride] = r;
+    Ar[2 * kMmStride] = r2;
+    Ar[3 * kMmStride] = r3;
+    Ar[4 * kMmStride] = r4;
+    Ar[5 * kMmStride] = r5;
+    Ar[6 * kMmStride] = r6;
+    Ar[7 * kMmStride] = r7;
+    Br[0] = W;
+    Br[kMmStride] = w8;
+    Br[2 * kMmStride] = w16;
+    Br[3 * kMmStride] = w24;
+    __syncwarp();
+    const int g = lane >> 2, t = lane & 3;
+    const double *af = Pw + g * kMmStride + t, *bf = Pw + (8 + (g & 3)) * kMmStride + t;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const double a = af[4 * q];
+        const double b = g < 4 ? bf[4 * q] : 0.0;
+        dmma884(cf[0], cf[1], a, b);
+    }
+    __syncwarp();
+}
+
+// park the DMMA moments in Pw as Ms[k], k = 8 n + g (lane (g, t): n = 2t, 2t + 1 < 4)
+__device__ __forceinline__ void store_moments_mma(const double (&cf)[2], double *Pw, int lane)
+{
+    const int g = lane >> 2, t = lane & 3;
+    __syncwarp();
+    if (t < 2) {
+        Pw[8 * (2 * t) + g] = cf[0];
+        Pw[8 * (2 * t + 1) + g] = cf[1];
+    }
+    __syncwarp();
+}
+
 // fold the two point halves of the moments and park them in Pw as Ms[i][k]
 template <int NW>
 __device__ __forceinline__ void store_moments(double (&mom)[2][NW], double *Pw, int lane)
@@ -695,10 +754,10 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
             Slots<OP, NJ> T;
             T.init(A, W, lane & (gw - 1));
             const int pg = lane / gw, npg = 32 / gw;
-            double acc[NJ][NIJ], mom[2][NIJ], s0[NIJ], sc[NIJ];
+            double acc[NJ][NIJ], mom[1][2] = {{0.0, 0.0}}, s0[NIJ], sc[NIJ];   // mom: the DMMA C fragment
 #pragma unroll
             for (int i = 0; i < NIJ; ++i) {
-                s0[i] = sc[i] = mom[0][i] = mom[1][i] = 0.0;
+                s0[i] = sc[i] = 0.0;
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) acc[j][i] = 0.0;
             }
@@ -710,7 +769,7 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
                 const bool any_small = __any_sync(kFull, small);
                 __syncwarp();
                 const int nloc = min(32, nq - base);
-                chunk_moments<PAY, HOFF, NIJ>(geo, Pw, rt2, nloc, mom, lane);
+                chunk_moments_mma<PAY, HOFF>(geo, Pw, rt2, mom[0], lane);   // (NIJ == 1: mom[0] = the C fragment)
                 __syncwarp();
                 eval_points<OP, NIJ, PAY, HOFF, NJ>(A, T, geo, nloc, any_small, pg, npg, nje, acc, tab);
                 __syncwarp();
@@ -731,7 +790,7 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
                     }
                 }
             }
-            store_moments<NIJ>(mom, Pw, lane);
+            store_moments_mma(mom[0], Pw, lane);
             stage_L<OP, NIJ, NJ, SLOTS>(W, T, acc, jac, istar_f + 2, gw, nje, Ls, lane);
             __syncwarp();
             combine_window<NIJ, SLOTS>(A, W, Ls, slot, lane);
@@ -746,7 +805,7 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
     // ---- phase 1 ----
     double rmax = 0.0;
     {
-        double mom[2][NIJ], s0[NIJ], sc[NIJ];
+        double mom[2][NIJ], s0[NIJ], sc[NIJ], cf[2] = {0.0, 0.0};
 #pragma unroll
         for (int i = 0; i < NIJ; ++i) s0[i] = sc[i] = mom[0][i] = mom[1][i] = 0.0;
         for (int base = 0; base < nq; base += 32) {
@@ -756,7 +815,11 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
             rmax = fmax(rmax, rt2);
             const bool skip = OP == 1 && !__any_sync(kFull, nzw);   // all-zero K chunk: exact zeros
             __syncwarp();
-            if (try_mom && !skip) chunk_moments<PAY, HOFF, NIJ>(geo, Pw, rt2, min(32, nq - base), mom, lane);
+            if (try_mom && !skip) {
+                // p0 x p0: the same tensor-core moments as the single-pass path (same bits)
+                if constexpr (NIJ == 1) chunk_moments_mma<PAY, HOFF>(geo, Pw, rt2, cf, lane);
+                else chunk_moments<PAY, HOFF, NIJ>(geo, Pw, rt2, min(32, nq - base), mom, lane);
+            }
             __syncwarp();
         }
         if (A.need_special) {
@@ -775,7 +838,10 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
                 }
             }
         }
-        if (try_mom) store_moments<NIJ>(mom, Pw, lane);
+        if (try_mom) {
+            if constexpr (NIJ == 1) store_moments_mma(cf, Pw, lane);
+            else store_moments<NIJ>(mom, Pw, lane);
+        }
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(kFull, rmax, o));
