@@ -374,6 +374,68 @@ __device__ __forceinline__ void store_moments_mma(const double (&cf)[2], double 
     __syncwarp();
 }
 
+// NW weights per point (p0 x p1, p1 x p1, K's two orientations): the same
+// product with B[p][(i, n)] = W_i(p) r_p^(8 n), column c = 4 i + n, in
+// ceil(4 NW / 8) column tiles; the B element is formed in registers from the
+// payload weight and the staged power r_p^(8 n) (rows 8..11 of the scratch).
+template <int NW>
+__host__ __device__ constexpr int mom_tiles() { return (4 * NW + 7) / 8; }
+
+template <int PAY, int WOFF, int NW>
+__device__ __forceinline__ void chunk_moments_mma_n(const double *geo, double *Pw, double r,
+                                                    double (&cf)[mom_tiles<NW>()][2], int lane)
+{
+    constexpr int NT = mom_tiles<NW>();
+    const double r2 = __dmul_rn(r, r), r3 = __dmul_rn(r2, r), r4 = __dmul_rn(r2, r2);
+    const double r5 = __dmul_rn(r4, r), r6 = __dmul_rn(r4, r2), r7 = __dmul_rn(r4, r3), r8 = __dmul_rn(r4, r4);
+    const double r16 = __dmul_rn(r8, r8), r24 = __dmul_rn(r16, r8);
+    double *Ar = Pw + lane;
+    Ar[0] = 1.0;
+    Ar[kMmStride] = r;
+    Ar[2 * kMmStride] = r2;
+    Ar[3 * kMmStride] = r3;
+    Ar[4 * kMmStride] = r4;
+    Ar[5 * kMmStride] = r5;
+    Ar[6 * kMmStride] = r6;
+    Ar[7 * kMmStride] = r7;
+    Ar[8 * kMmStride] = 1.0;
+    Ar[9 * kMmStride] = r8;
+    Ar[10 * kMmStride] = r16;
+    Ar[11 * kMmStride] = r24;
+    __syncwarp();
+    const int g = lane >> 2, t = lane & 3;
+    const double *af = Pw + g * kMmStride + t, *rf = Pw + (8 + (g & 3)) * kMmStride + t;
+    const double *wf = geo + t * PAY + WOFF + (g >> 2);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const double a = af[4 * q], rb = rf[4 * q];
+#pragma unroll
+        for (int tau = 0; tau < NT; ++tau) {
+            // column c = 8 tau + g = 4 i + n: weight i = 2 tau + (g >> 2), power n = g & 3
+            const bool live = 2 * tau + (g >> 2) < NW;
+            const double b = live ? __dmul_rn(wf[4 * q * PAY + 2 * tau], rb) : 0.0;
+            dmma884(cf[tau][0], cf[tau][1], a, b);
+        }
+    }
+    __syncwarp();
+}
+
+// park them in Pw as Ms[i][k], k = 8 n + g (lane (g, t): columns 8 tau + 2t, + 1)
+template <int NW>
+__device__ __forceinline__ void store_moments_mma_n(const double (&cf)[mom_tiles<NW>()][2], double *Pw, int lane)
+{
+    const int g = lane >> 2, t = lane & 3;
+    __syncwarp();
+#pragma unroll
+    for (int tau = 0; tau < mom_tiles<NW>(); ++tau)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = 8 * tau + 2 * t + h, i = c >> 2, n = c & 3;
+            if (i < NW) Pw[i * kNK + 8 * n + g] = cf[tau][h];
+        }
+    __syncwarp();
+}
+
 // fold the two point halves of the moments and park them in Pw as Ms[i][k]
 template <int NW>
 __device__ __forceinline__ void store_moments(double (&mom)[2][NW], double *Pw, int lane)
@@ -805,9 +867,11 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
     // ---- phase 1 ----
     double rmax = 0.0;
     {
-        double mom[2][NIJ], s0[NIJ], sc[NIJ], cf[2] = {0.0, 0.0};
+        double s0[NIJ], sc[NIJ], cf[2] = {0.0, 0.0}, cfn[mom_tiles<NIJ>()][2];   // DMMA C fragments of the moments
 #pragma unroll
-        for (int i = 0; i < NIJ; ++i) s0[i] = sc[i] = mom[0][i] = mom[1][i] = 0.0;
+        for (int i = 0; i < NIJ; ++i) s0[i] = sc[i] = 0.0;
+#pragma unroll
+        for (int tau = 0; tau < mom_tiles<NIJ>(); ++tau) cfn[tau][0] = cfn[tau][1] = 0.0;
         for (int base = 0; base < nq; base += 32) {
             double rt2;
             int small, nzw;
@@ -818,7 +882,7 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
             if (try_mom && !skip) {
                 // p0 x p0: the same tensor-core moments as the single-pass path (same bits)
                 if constexpr (NIJ == 1) chunk_moments_mma<PAY, HOFF>(geo, Pw, rt2, cf, lane);
-                else chunk_moments<PAY, HOFF, NIJ>(geo, Pw, rt2, min(32, nq - base), mom, lane);
+                else chunk_moments_mma_n<PAY, HOFF, NIJ>(geo, Pw, rt2, cfn, lane);
             }
             __syncwarp();
         }
@@ -840,7 +904,7 @@ __device__ __noinline__ void eval_pair(const PairArgs &A, const Geom &g, int nq,
         }
         if (try_mom) {
             if constexpr (NIJ == 1) store_moments_mma(cf, Pw, lane);
-            else store_moments<NIJ>(mom, Pw, lane);
+            else store_moments_mma_n<NIJ>(cfn, Pw, lane);
         }
     }
 #pragma unroll
@@ -1089,11 +1153,11 @@ __device__ __noinline__ void eval_pair_dual(const PairArgs &A, const RegularGeom
     const bool try_mom = A.moments && A.d1 - 1 >= max(2, moment_istar(rt2_lo) + 1);
     double rmax = 0.0;
     {
-        double mom[2][6], s0f[3], scf[3], s0r[3], scr[3];
+        double cfn[mom_tiles<6>()][2], s0f[3], scf[3], s0r[3], scr[3];   // cfn: DMMA C fragments of the moments
 #pragma unroll
         for (int i = 0; i < 3; ++i) s0f[i] = scf[i] = s0r[i] = scr[i] = 0.0;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) mom[0][i] = mom[1][i] = 0.0;
+        for (int tau = 0; tau < mom_tiles<6>(); ++tau) cfn[tau][0] = cfn[tau][1] = 0.0;
         for (int base = 0; base < nq; base += 32) {
             double rt2;
             int small, nzw;
@@ -1101,11 +1165,11 @@ __device__ __noinline__ void eval_pair_dual(const PairArgs &A, const RegularGeom
             rmax = fmax(rmax, rt2);
             const bool skip = !__any_sync(kFull, nzw);
             __syncwarp();
-            if (try_mom && !skip) chunk_moments<PAY, 2, 6>(geo, Pw, rt2, min(32, nq - base), mom, lane);
+            if (try_mom && !skip) chunk_moments_mma_n<PAY, 2, 6>(geo, Pw, rt2, cfn, lane);
             __syncwarp();
         }
         if (A.need_special) dual_specials_reduce<NJ>(s0f, scf, s0r, scr, jac, Lf, Lr, lane);
-        if (try_mom) store_moments<6>(mom, Pw, lane);
+        if (try_mom) store_moments_mma_n<6>(cfn, Pw, lane);
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(kFull, rmax, o));
