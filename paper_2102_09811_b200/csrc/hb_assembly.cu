@@ -104,7 +104,7 @@ struct LsLayout {
     static constexpr int SIZE = NIJ * SLOTS + 2 * NIJ;   // + L0 and Lcomb0
 };
 
-constexpr int kPwDoubles = 32 * 17;   // per-warp moment scratch (kPwStride = 17, below)
+constexpr int kPwDoubles = 32 * 17;   // per-warp moment scratch: DMMA fragments (12 rows of stride 36), then the moments Ms
 
 template <int OP, int NIJ, int NJ>
 __host__ __device__ constexpr int smem_doubles_per_warp_base()
@@ -229,8 +229,7 @@ struct DuffyGeom {
 // kMom*Thr are below 2^-56 of the leading one.
 // ---------------------------------------------------------------------------
 constexpr int kNK = moments::kNK;    // 32: lane k of a warp owns moment k
-constexpr int kPwStride = 17;        // per-warp scratch: powers [32 points][16 (+1 pad)], then moments
-static_assert(kPwDoubles == 32 * kPwStride, "moment scratch size");
+static_assert(kPwDoubles >= 9 * kNK, "moment scratch holds the moments of nine weights");
 static_assert(kNK == 32, "one moment per lane");
 
 template <int OP>
@@ -269,49 +268,6 @@ __global__ void k_moment_table(double *Tm, int d0, int nd, double S, double q0)
         } else {
             Tm[i] = mom_thr<OP>(i - n);
         }
-    }
-}
-
-// moments of one chunk of nloc points: lane p writes rt2_p^k, k in
-// [16c, 16c + 16), to Pw[p][k - 16c]; lane (k16, h) = (lane & 15, lane >> 4)
-// then adds sum_{p in [16h, 16h + 16), p < nloc} Pw[p][k16] W_p[i] to
-// mom[c][i], p ascending.
-template <int PAY, int WOFF, int NW>
-__device__ __forceinline__ void chunk_moments(const double *geo, double *Pw, double rt2, int nloc,
-                                              double (&mom)[2][NW], int lane)
-{
-    const int k16 = lane & 15, h = lane >> 4;
-    const int pend = min(16 * h + 16, nloc);
-    double pw = 1.0;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            Pw[lane * kPwStride + k] = pw;
-            pw = __dmul_rn(pw, rt2);
-        }
-        __syncwarp();
-        if (NW <= 3 && nloc == 32) {
-            // full chunk (every touching-pair chunk): straight-line, the 16 points'
-            // loads at immediate offsets from two bases -- same additions, same order
-            const double *col = Pw + 16 * h * kPwStride + k16;
-            const double *wb = geo + 16 * h * PAY + WOFF;
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const double P = col[q * kPwStride];
-#pragma unroll
-                for (int i = 0; i < NW; ++i) mom[c][i] = fma(P, wb[q * PAY + i], mom[c][i]);
-            }
-        } else {
-#pragma unroll 2
-            for (int p = 16 * h; p < pend; ++p) {
-                const double P = Pw[p * kPwStride + k16];
-                const double *w = geo + p * PAY + WOFF;
-#pragma unroll
-                for (int i = 0; i < NW; ++i) mom[c][i] = fma(P, w[i], mom[c][i]);
-            }
-        }
-        __syncwarp();
     }
 }
 
@@ -433,25 +389,6 @@ __device__ __forceinline__ void store_moments_mma_n(const double (&cf)[mom_tiles
             const int c = 8 * tau + 2 * t + h, i = c >> 2, n = c & 3;
             if (i < NW) Pw[i * kNK + 8 * n + g] = cf[tau][h];
         }
-    __syncwarp();
-}
-
-// fold the two point halves of the moments and park them in Pw as Ms[i][k]
-template <int NW>
-__device__ __forceinline__ void store_moments(double (&mom)[2][NW], double *Pw, int lane)
-{
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int i = 0; i < NW; ++i) mom[c][i] += __shfl_xor_sync(kFull, mom[c][i], 16);   // commutative
-    __syncwarp();
-    if (lane < 16) {
-#pragma unroll
-        for (int i = 0; i < NW; ++i) {
-            Pw[i * kNK + lane] = mom[0][i];
-            Pw[i * kNK + 16 + lane] = mom[1][i];
-        }
-    }
     __syncwarp();
 }
 
