@@ -1546,9 +1546,8 @@ __device__ __forceinline__ void far_pp_k(const PairArgs &A, const FarGeom &G, co
             const double rna = (-rx) * na[0] + (-ry) * na[1] + (-rz) * na[2];
             const double wq = wp * G.w[r];
             const double rho = sqrt(r2);
-            const double iq = 1.0 / rho;
             double xs[1] = {__dmul_rn(rho, cx)}, fs[1];
-            special::eval_ulocal<5, 1>(xs, [&](int) { return __dmul_rn(iq, ic); }, fs, tab);
+            special::eval_ulocal<5, 1>(xs, [&](int) { return __dmul_rn(1.0 / rho, ic); }, fs, tab);
             if (pp) {
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
@@ -1559,6 +1558,7 @@ __device__ __forceinline__ void far_pp_k(const PairArgs &A, const FarGeom &G, co
                 }
             }
             if (spec && (q % LPP) == g) {
+                const double iq = 1.0 / rho;
                 const double Uf = -rnb * iq, Ur = -rna * iq;
                 const double P = 1.0 / __dmul_rn(rho, rho);
                 const double c0 = A.inv2a, cc = A.inv2a - A.step * P;
@@ -1739,12 +1739,12 @@ __device__ __forceinline__ void far_pp_v(const PairArgs &A, const FarGeom &G, in
         for (int r = 0; r < nq1; ++r, ++q) {
             const double rx = x0 - G.yp[3 * r], ry = x1 - G.yp[3 * r + 1], rz = x2 - G.yp[3 * r + 2];
             const double rho = sqrt(rx * rx + ry * ry + rz * rz);
-            const double iq = 1.0 / rho;
             const double wq = wp * G.w[r];
             double xs[4], fs[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) xs[j] = __dmul_rn(rho, cx[j]);
-            special::eval_ulocal<4, 4>(xs, [&](int j) { return __dmul_rn(iq, ic[j]); }, fs, tab);
+            // (1 / rho only where a lane takes the asymptote: the division stays off the common path)
+            special::eval_ulocal<4, 4>(xs, [&](int j) { return __dmul_rn(1.0 / rho, ic[j]); }, fs, tab);
             if (pp) {
                 // compensated sum (TwoProd by fma + TwoSum): the point sum of a gap
                 // carries no rounding of its own, so the time second difference
@@ -1761,6 +1761,7 @@ __device__ __forceinline__ void far_pp_v(const PairArgs &A, const FarGeom &G, in
                 }
             }
             if (spec && (q & 1) == g) {
+                const double iq = 1.0 / rho;
                 const double Aq = rho * A.inv2a2, Bq = A.inva * iq;
                 const double cq = A.step * Bq + Aq;
                 s0 = fma(wq, Aq, s0);
