@@ -432,10 +432,17 @@ __device__ __forceinline__ void eval_ulocal(const double (&x)[NJ], const IXF &ix
 #pragma unroll
         for (int j = 0; j < NJ; ++j) q[j] = fma(q[j], u[j], w[m][j].x);
     }
+    bool any_h = false;
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
         r[j] = KIND == 4 ? fma(__dmul_rn(x[j], x[j]), q[j], kTwoInvSqrtPi) : q[j];
-        if (huge[j]) r[j] = asymptote<KIND>(x[j], ixf(j));
+        any_h |= huge[j];
+    }
+    // (the vote only skips code: the asymptote replaces a lane's own value whoever else is active)
+    if (__any_sync(__activemask(), any_h)) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            if (huge[j]) r[j] = asymptote<KIND>(x[j], ixf(j));
     }
 }
 
